@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the MNS hot path on B200 (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[4], the largest single-GPU config; configs[1] is a
+512^2 image that is launch-latency bound): one 16384 x 16384 uint8 image from the
+pinned synthetic generator (noise sigma 10, 24 blobs, seed 5), MNS encode with the
+16->8->4 quadtree (EncoderConfig(e3=inf)) and a 10-sweep Jacobi decode from flat 128
+(DecodeConfig(max_iters=10, stop_delta=0)).  A step = encode + decode of the whole
+image; with N GPUs the image is split into N row strips (16-row read-only input
+halo; 16-row raster halos exchanged over NCCL after every decode sweep) -- fixed
+total work, "scaling": "strong".
+
+  value   8x8-range blocks (W*H/64 = 4,194,304 per image) per second of the whole
+          encode+decode step, inputs resident in HBM, max over ranks;
+  e2e     the same through the public device API with the image copied from pinned
+          host memory and the decoded image copied back inside the timed region;
+  roofline  the dominant kernel (the decode sweep, fp32 raster read + write);
+  cpu_baseline  the CPU oracle (oracle/, literal fp64 port of the reference) on a
+          bounded sample on this host.
+
+--impl reference runs the reference's CPU implementation of the path (the oracle
+port -- the reference is pure Python/numpy and has no build) on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+IMG = 16384
+ITERS = 10
+METRIC = "range blocks encoded/sec (MNS) and Mpixel/s decoded; full-search pair-evals/s"
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 6 for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------- CPU legs
+
+def cpu_sample(img: np.ndarray, rows: int = 2048, threads: int | None = None):
+    """Oracle encode + 10-sweep decode of the top `rows` rows of the c5 image (own image)."""
+    from oracle import oracle as O
+
+    s = np.ascontiguousarray(img[:rows])
+    t0 = time.perf_counter()
+    rec, _ = O.encode_quadtree_records(s, (8.0, 8.0, math.inf), 16.0, True, 1, nthreads=threads)
+    O.decode_records(rec, s.shape[1], s.shape[0], max_iters=ITERS, stop_delta=0.0, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return s.size / 64 / dt, dt
+
+
+def run_reference(args, img):
+    from oracle import oracle as O
+
+    threads = O.default_threads()
+    rows = args.cpu_rows
+    for _ in range(args.warmup):
+        cpu_sample(img, rows, threads)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_sample(img, rows, threads)
+        times.append(dt)
+    per_step = float(np.mean(times))
+    value = (rows * IMG / 64) / per_step
+    sample = f"c5 rows 0..{rows - 1} ({rows}x{IMG}, {rows // 16} of 1024 root rows) encoded + {ITERS}-sweep decoded"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c5: MNS encode (16->8->4, e3=inf) + 10-sweep decode, 16384^2 uint8, sigma 10, "
+                                   "24 blobs, seed 5", "image": f"{IMG}x{IMG}", "sample_rows": rows},
+            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- GPU leg
+
+def run_ours(args, img_np, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1501_02894_b200 as mns
+    from paper_1501_02894_b200 import sharding
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    H = W = IMG
+    r0, r1 = sharding.strip_rows(H, world, rank)
+    y_lo, y_hi = sharding.resident_rows(r0, r1, H)
+    cfg = mns.EncoderConfig(e3=math.inf)
+    host = torch.from_numpy(np.ascontiguousarray(img_np[y_lo:y_hi])).pin_memory()
+    img = host.to(dev)
+    n_roots = (r1 - r0) * (W // 16)
+    code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
+                          torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
+                          torch.zeros(1, dtype=torch.int64, device=dev), W, H, 1, r0, r1)
+    dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world)
+    out_host = torch.empty((16 * (r1 - r0), W), dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step(e2e=False, ev=None):
+        if e2e:
+            img.copy_(host, non_blocking=True)
+        if ev:
+            ev[0].record()
+        mns.encode_device(img, cfg, root_rows=(r0, r1), height=H, out=code)
+        if ev:
+            ev[1].record()
+        dec.run(ITERS, 128.0, sweep_events=ev[2] if ev else None)
+        if ev:
+            ev[3].record()
+        if e2e:
+            out_host.copy_(dec.out, non_blocking=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    def timed(k, e2e, record=False):
+        evs = []
+        for _ in range(k):
+            evs.append([torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                        [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+                         for _ in range(ITERS)],
+                        torch.cuda.Event(enable_timing=True)] if record else None)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(k):
+            step(e2e, evs[i])
+        t1.record()
+        barrier()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            m = torch.tensor([ms], device=dev)
+            dist.all_reduce(m, op=dist.ReduceOp.MAX)
+            ms = float(m.item())
+        return ms, evs
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        ms, evs = timed(args.steps, False, record=True)
+    ms_step = ms / args.steps
+    blocks = H * W / 64
+    value = blocks / (ms_step / 1e3)
+    # component times (device events; per step averages over the timed steps)
+    enc_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    dec_ms = float(np.mean([e[1].elapsed_time(e[3]) for e in evs]))
+    mid = [e[2][i][0].elapsed_time(e[2][i][1]) for e in evs for i in range(1, ITERS - 1)]
+    sweep_ms = float(np.mean(mid))
+    own_px = 16 * (r1 - r0) * W
+    n_leaves = int(code.count.item())
+
+    # e2e through the public device API with host buffers
+    for _ in range(2):
+        step(e2e=True)
+    ms_e2e, _ = timed(args.steps, True)
+    e2e_value = blocks / (ms_e2e / args.steps / 1e3)
+
+    # full-search component (config c4 identity + isometries) on rank 0 only, informational
+    fs = None
+    if rank == 0 and not args.no_search:
+        from paper_1501_02894_b200.synth import config_image
+
+        c4 = torch.from_numpy(config_image("c4")).to(dev)
+        for n_iso in (1,):
+            mns.full_search_device(c4, 8, 1, n_iso)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            mns.full_search_device(c4, 8, 1, n_iso)
+            b.record()
+            torch.cuda.synchronize()
+            pairs = 4096 * 497 * 497 * n_iso
+            fs = {"config": "c4 512^2 B=8 stride 1, identity isometry", "pair_evals": pairs,
+                  "ms": a.elapsed_time(b), "pair_evals_per_s": pairs / (a.elapsed_time(b) / 1e3)}
+
+    if rank != 0:
+        return
+    hbm, which = peaks()
+    algo = 8.0 * own_px  # fp32 raster read + write per steady-state sweep
+    achieved = algo / (sweep_ms / 1e3) / 1e9
+    cpu_v, cpu_dt = (None, None)
+    if world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+
+        cpu_v, cpu_dt = cpu_sample(img_np, args.cpu_rows, O.default_threads())
+    launches_per_step = 1 + ITERS  # encode kernel + one kernel per sweep (+ the workspace memset, not a kernel)
+    line = {
+        "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8/int32 encode, fp32 decode", "data": "synthetic",
+        "config": {"workload": "c5: MNS encode (16->8->4, e3=inf) + 10-sweep decode, 16384^2 uint8, sigma 10, "
+                               "24 blobs, seed 5", "image": f"{IMG}x{IMG}", "parallelism": f"strips{world}",
+                   "l2": "inputs (256 MiB image, 1 GiB fp32 rasters) exceed the 126 MB L2"},
+        "components": {"encode_ms": enc_ms, "encode_blocks_per_s": blocks / world / (enc_ms / 1e3),
+                       "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
+                       "sweep_ms": sweep_ms, "leaves_rank0": n_leaves, "full_search": fs},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "kernel": "decode_sweep_kernel (steady-state sweep)", "peak_source": which},
+        "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
+                          "sample": f"c5 rows 0..{args.cpu_rows - 1} encoded + {ITERS}-sweep decoded as its own "
+                                    f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
+        "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": int(host.numel()) * world,
+                "d2h_bytes_per_step": int(out_host.numel()) * world},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=2048)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-search", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1501_02894_b200.synth import config_image
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(args, config_image("c5"))
+        return
+    import torch.distributed as dist
+
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, config_image("c5"), rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * mns_b200.h -- C ABI of libmns_b200.so, the B200 (sm_100a) implementation of the
+ * MNS fractal coder's data-parallel core (arXiv 1501.02894; reference package
+ * `mnscodec`, /root/reference/pkg/src/mnscodec).
+ *
+ * The reference has no native layer: its "plugin boundary" is the set of
+ * module-level Python functions re-exported by mnscodec/__init__.py:9-53.
+ * Each entry point below is what a maintainer binds (ctypes) in place of one
+ * of those functions; the Python mirror paper_1501_02894_b200/codec.py does
+ * exactly that and keeps the reference's signatures and error messages.
+ *
+ * Conventions
+ *   - All buffers are caller-owned DEVICE pointers (e.g. torch tensors'
+ *     data_ptr()); `stream` is a cudaStream_t cast to void* (NULL = legacy
+ *     default stream).  Calls are asynchronous and stream-ordered; the library
+ *     keeps no pointers after returning and holds no mutable global state.
+ *   - Images are uint8, row-major, already padded (pad_to_multiple,
+ *     image.py:123-132, is host work): width/height multiples of 16 for the
+ *     quadtree, of B for the search baselines.
+ *   - Return value: 0 on success, negative on a CUDA/argument error; the
+ *     message is available from mns_last_error() (thread-local).  Reference
+ *     ValueErrors are raised by the Python layer before any native call.
+ *   - Transform codes travel as packed 64-bit leaf records (mns_record.h).
+ */
+#ifndef MNS_B200_H
+#define MNS_B200_H
+
+#include <stdint.h>
+
+#include "mns_record.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Encoder knobs: mirror of EncoderConfig (encoder.py:52-76) plus the root-level
+ * extension (root_level = 2: every 16x16 root is forced to split once, the
+ * "8->4" quadtree of BASELINE configs 1 and 3). */
+typedef struct {
+    double e[3];      /* e1, e2, e3 (RMS tolerances of levels 1..3; +inf allowed) */
+    double mean_tol;  /* phase-2 gate */
+    int32_t mns;      /* 1: mode "mns"; 0: mode "no_search" */
+    int32_t root_level;
+} mns_enc_cfg;
+
+/* Replaces: encoder.encode_quadtree (encoder.py:215-246) for n_images images of
+ * identical size stacked at image_stride bytes, restricted to the root rows
+ * [root_row_begin, root_row_end) of each image (strip sharding; pass 0 and
+ * height/16 for whole images).  `img` points at row 0 of image 0 even when only
+ * rows [root_row_begin*16 - 16, root_row_end*16 + 16) are resident (the rest is
+ * never read).
+ *
+ * Output: packed records in reference DFS order (images, then roots in raster
+ * order, then TL,TR,BL,BR pre-order), root_offsets[i] = index of the first
+ * record of root i (roots of the processed rows, image-major, raster order;
+ * n_roots + 1 entries, the last = total), *d_count = total records (device).
+ * capacity must be >= 64 * n_roots.  Workspace: mns_encode_workspace_bytes. */
+int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t root_row_begin, int32_t root_row_end,
+                               int64_t *bytes);
+int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
+                        int32_t n_images, int32_t root_row_begin, int32_t root_row_end, const mns_enc_cfg *cfg,
+                        uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
+                        void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Replaces: decoder.decode / decode_step (decoder.py:37-77) for quadtree codes.
+ * One Jacobi sweep per iteration over an fp32 raster (ping/pong, width*height
+ * floats each).  Records must be grouped by root with root_offsets (as
+ * mns_encode_quadtree emits); leaf order inside a root is free, as in the
+ * reference (decoder.py:8-10).  After `iters` sweeps (early stop when
+ * stop_delta > 0 and max|delta| < stop_delta; *d_iters_done receives the count)
+ * the raster is rounded floor(x+0.5), clipped to [0,255] into out (width*height
+ * bytes, padded; the caller crops).  The final raster is in ping when
+ * iters_done is even, else in pong. */
+int mns_decode_workspace_bytes(int32_t width, int32_t height, int64_t *bytes);
+int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                        int32_t iters, double stop_delta, float initial_value, float *ping, float *pong,
+                        uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                        void *stream);
+
+/* One Jacobi sweep over the root rows [root_row_begin, root_row_end) (strip
+ * sharding: the multi-GPU decoder exchanges 16-row halos between sweeps).
+ * cur / nxt / out are bases of the FULL image (row 0) even when only rows
+ * [16*root_row_begin - 16, 16*root_row_end + 16) are resident; root_offsets are
+ * local to the strip's roots.  cur may be NULL on the first sweep: the flat
+ * start raster of initial_value is implied (no fill pass).  nxt may be NULL when
+ * out (uint8, rounded) is given: the fused final sweep.  state: 4 int32 zeroed
+ * before the first sweep (early-stop bookkeeping when stop_delta > 0). */
+int mns_decode_sweep(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                     int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value,
+                     float *nxt, uint8_t *out, int32_t *state, double stop_delta, void *stream);
+
+/* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
+ * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-
+ * baseline codes whose domains are explicit (BaselinePayload) and for arbitrary
+ * leaf orders.  Units are SoA arrays of length n_units. */
+int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                     const int32_t *udy, const float *us, const float *uo, int64_t n_units, int32_t width,
+                     int32_t height, int32_t iters, double stop_delta, float initial_value, float *ping,
+                     float *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                     void *stream);
+
+/* One sweep on a caller-provided fp64 raster, bit-exact with decoder.decode_step
+ * (numpy evaluation order emulated; for parity tests and debugging). */
+int mns_decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                        const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                        int32_t height, const double *cur, double *out, void *stream);
+
+/* Replaces: encoder.encode_full_search (encoder.py:249-309).  Ranges: the
+ * non-overlapping B x B blocks of the B-padded raster in raster order (range
+ * ids [range_begin, range_end) -- range sharding).  Domain pool: every 2B x 2B
+ * block on a stride-`step` lattice, raster order, x n_iso isometries (1 = the
+ * reference; 8 = extension, order documented in DESIGN.md).  Per range:
+ * out_dom = domain index, out_iso, out_o = o_byte, out_code = s_code, with the
+ * reference's tie-break (lowest domain index, then isometry).  B in {4, 8}
+ * runs on the tcgen05 tensor-core path; B in {2, 16} on CUDA cores. */
+int mns_search_workspace_bytes(int32_t width, int32_t height, int32_t B, int32_t step, int32_t n_iso,
+                               int64_t *bytes);
+int mns_full_search(const uint8_t *img, int32_t width, int32_t height, int32_t B, int32_t step, int32_t n_iso,
+                    int32_t range_begin, int32_t range_end, int32_t *out_dom, int8_t *out_iso, uint8_t *out_o,
+                    uint8_t *out_code, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Replaces: encoder.encode_local_search (encoder.py:312-347); radius 4 is the
+ * reference (81 candidates), other radii (e.g. 32) are the extension.  Outputs
+ * the winning domain origin per 8x8 range of the 8-padded raster. */
+int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t *out_dx,
+                     int32_t *out_dy, uint8_t *out_o, uint8_t *out_code, void *stream);
+
+/* Packed .mns bitstream (bitstream.py:130-205) of a record array: per-leaf
+ * widths, exclusive scan, MSB-first scatter.  out must hold
+ * 4*ceil((104 + 33n)/32) bytes; *d_bits receives the exact bit count
+ * (stream_bit_count, bitstream.py:282-300). */
+int mns_stream_workspace_bytes(int64_t n_records, int64_t *bytes);
+int mns_write_stream(const uint64_t *records, int64_t n_records, int32_t orig_w, int32_t orig_h, int32_t padded_w,
+                     int32_t padded_h, int32_t mns, int32_t technique2, uint8_t *out, int64_t out_capacity,
+                     int64_t *d_bits, void *workspace, int64_t workspace_bytes, void *stream);
+
+const char *mns_last_error(void);
+int mns_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

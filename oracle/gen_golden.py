@@ -26,6 +26,7 @@ sys.path.insert(0, os.path.join(REF, "tests"))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import mnscodec.encoder as enc  # noqa: E402
+from mnscodec.bitstream import stream_bit_count, write_stream  # noqa: E402
 from mnscodec.decoder import DecodeConfig, decode, decode_step  # noqa: E402
 from mnscodec.encoder import EncoderConfig, encode_full_search, encode_local_search, encode_quadtree  # noqa: E402
 from mnscodec.image import BlockRect, GrayImage, pad_to_multiple  # noqa: E402
@@ -226,6 +227,8 @@ def gen_encode(store, manifest):
                 dec_def = decode(code, DecodeConfig()).pixels
                 store[f"{key}/decode8"] = dec8
                 store[f"{key}/decode_default"] = dec_def
+                store[f"{key}/stream"] = np.frombuffer(write_stream(code), dtype=np.uint8)
+                store[f"{key}/stream_bits"] = np.array(stream_bit_count(code), dtype=np.int64)
                 ties = ones = 0
                 if name.startswith("ties") and root_level == 1:
                     ties, ones = count_exact_phase2_ties(image, config)

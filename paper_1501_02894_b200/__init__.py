@@ -1,1 +1,46 @@
-"""B200-native MNS fractal coder core."""
+"""B200-native (sm_100a) data-parallel core of the Modified No Search fractal coder
+(arXiv 1501.02894), a drop-in for the reference ``mnscodec`` encode/decode hot path.
+
+Public API mirrors mnscodec (same names, signatures, dataclasses, error messages):
+encode_quadtree, decode, decode_step, encode_full_search, encode_local_search,
+write_stream, read_stream, stream_bit_count, plus the device layer used by
+bench.py and the multi-GPU sharding (encode_device, decode_device, ...).
+"""
+
+from .types import (  # noqa: F401
+    CONTRAST_SETS,
+    CONTRAST_VALUES,
+    DELTA_MAGNITUDE_BITS,
+    LEVEL_SIZES,
+    MODES,
+    ROOT_SIZE,
+    BaselinePayload,
+    BlockRect,
+    DecodeConfig,
+    EncoderConfig,
+    GrayImage,
+    LeafRecord,
+    Phase1Payload,
+    Phase2Payload,
+    QuadtreeCode,
+    delta_limit,
+    dequantize_contrast,
+    round_to_int,
+)
+from .codec import (  # noqa: F401
+    DeviceCode,
+    co_domain_rect,
+    decode,
+    decode_device,
+    decode_step,
+    encode_device,
+    encode_full_search,
+    encode_local_search,
+    encode_quadtree,
+    full_search_device,
+    local_search_device,
+    pad_to_multiple,
+    write_stream_device,
+)
+
+__version__ = "0.1.0"

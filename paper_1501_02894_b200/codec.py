@@ -1,0 +1,445 @@
+"""Reference-API mirror of the MNS hot path on B200 (drop-in for mnscodec's encoder/decoder).
+
+Same function names, arguments, return types and ValueError messages as the
+reference (file:line citations per function); every computation runs in the
+sm_100a kernels of libmns_b200.so through ``_native``.  Two layers:
+
+* device layer (``encode_device`` / ``decode_device`` / ``full_search_device`` /
+  ``local_search_device``): torch CUDA tensors in, torch CUDA tensors out,
+  stream-ordered, no host synchronisation unless asked -- used by bench.py,
+  the multi-GPU sharding and the host layer;
+* host layer (``encode_quadtree``, ``decode``, ``decode_step``,
+  ``encode_full_search``, ``encode_local_search``, ``write_stream`` ...):
+  the reference's signatures over numpy / GrayImage, with H2D/D2H copies.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .types import (
+    CONTRAST_SETS,
+    LEVEL_SIZES,
+    ROOT_SIZE,
+    SIZE_LEVELS,
+    BaselinePayload,
+    BlockRect,
+    DecodeConfig,
+    EncoderConfig,
+    GrayImage,
+    Phase1Payload,
+    Phase2Payload,
+    QuadtreeCode,
+    dequantize_contrast,
+)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ------------------------------------------------------------------ geometry (host)
+
+def pad_to_multiple(image, m: int) -> GrayImage:
+    """image.py:123-132: grow each axis to the next multiple of m by edge replication."""
+    if m < 1:
+        raise ValueError("padding multiple must be >= 1")
+    px = _pixels(image)
+    new_h = -(-px.shape[0] // m) * m
+    new_w = -(-px.shape[1] // m) * m
+    if (new_h, new_w) == px.shape:
+        return image if isinstance(image, GrayImage) else GrayImage(px)
+    return GrayImage(np.pad(px, ((0, new_h - px.shape[0]), (0, new_w - px.shape[1])), mode="edge"))
+
+
+def co_domain_rect(range_rect: BlockRect, img_w: int, img_h: int) -> BlockRect:
+    """image.py:174-187."""
+    if range_rect.size % 2:
+        raise ValueError("range size must be even")
+    d = range_rect.size * 2
+    if d > img_w or d > img_h:
+        raise ValueError(f"no {d}x{d} domain fits a {img_w}x{img_h} image")
+    x = min(max(range_rect.x - range_rect.size // 2, 0), img_w - d)
+    y = min(max(range_rect.y - range_rect.size // 2, 0), img_h - d)
+    return BlockRect(x, y, d)
+
+
+def _pixels(image) -> np.ndarray:
+    px = image.pixels if hasattr(image, "pixels") else np.asarray(image)
+    if px.ndim != 2:
+        raise ValueError(f"expected a 2-D pixel array, got shape {px.shape}")
+    if px.dtype != np.uint8:
+        px = GrayImage(px).pixels
+    return px
+
+
+def _padded_np(px: np.ndarray, m: int) -> np.ndarray:
+    h, w = px.shape
+    nh, nw = -(-h // m) * m, -(-w // m) * m
+    if (nh, nw) != (h, w):
+        px = np.pad(px, ((0, nh - h), (0, nw - w)), mode="edge")
+    return np.ascontiguousarray(px)
+
+
+# ------------------------------------------------------------------ device layer
+
+@dataclass
+class DeviceCode:
+    """Packed transform code resident on the GPU (records in DFS order, grouped by root)."""
+
+    records: "object"       # torch.int64 [capacity] (bit pattern of include/mns_record.h)
+    root_offsets: "object"  # torch.int32 [n_roots + 1]
+    count: "object"         # torch.int64 [1] (device) -- records[:count] are valid
+    padded_w: int
+    padded_h: int
+    n_images: int = 1
+    root_row_begin: int = 0
+    root_row_end: int = 0
+    mode: str = "mns"
+    technique2: bool = True
+
+    def n_records(self) -> int:
+        return int(self.count.item())
+
+
+class _Workspace:
+    """Per-device cache of scratch buffers (the caching allocator would also do; this keeps the
+    timed loops free of allocator calls)."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, key, nbytes, device):
+        torch = _torch()
+        t = self.buf.get((key, device))
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self.buf[(key, device)] = t
+        return t
+
+
+_WS = _Workspace()
+
+
+def enc_cfg(config: EncoderConfig, root_level: int = 1) -> N.EncCfg:
+    c = N.EncCfg()
+    c.e[0], c.e[1], c.e[2] = float(config.e1), float(config.e2), float(config.e3)
+    c.mean_tol = float(config.mean_tol)
+    c.mns = 1 if config.mode == "mns" else 0
+    c.root_level = int(root_level)
+    return c
+
+
+def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows: Optional[tuple] = None,
+                  height: Optional[int] = None, out: Optional[DeviceCode] = None, stream=None) -> DeviceCode:
+    """MNS quadtree encode of a padded uint8 CUDA tensor [H, W] or a batch [B, H, W].
+
+    root_rows=(r0, r1) restricts the work to root rows [r0, r1) (strip sharding); then ``img``
+    may be a halo'd slice and ``height`` gives the full image height (global clamping).
+    """
+    torch = _torch()
+    L = N.lib()
+    if config.mode not in ("no_search", "mns"):
+        raise ValueError(f"encode_quadtree handles no_search/mns, not {config.mode!r}")
+    if img.dim() == 2:
+        img = img.unsqueeze(0)
+    nb, h, w = img.shape
+    H = int(height) if height is not None else h
+    r0, r1 = root_rows if root_rows is not None else (0, H // 16)
+    n_roots = nb * (r1 - r0) * (w // 16)
+    dev = img.device
+    if out is None:
+        out = DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
+                         torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
+                         torch.zeros(1, dtype=torch.int64, device=dev), w, H, nb, r0, r1, config.mode,
+                         config.technique2)
+    wsb = N.out_i64(L, L.mns_encode_workspace_bytes, w, nb, r0, r1)
+    ws = _WS.get("enc", wsb, dev)
+    # `img` points at global row 0 even for halo'd strips: offset the base pointer back
+    base = img.data_ptr()
+    if root_rows is not None and h != H:
+        base -= max(0, 16 * r0 - 16) * img.stride(1)
+    cfg = enc_cfg(config, root_level)
+    N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
+                                  ctypes.byref(cfg), N.ptr(out.records), out.records.numel(), N.ptr(out.root_offsets),
+                                  N.ptr(out.count), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return out
+
+
+def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, initial_value: float = 128.0,
+                  out=None, rasters=None, want_u8: bool = True, stream=None):
+    """Jacobi decode of a device quadtree code (single image); returns (uint8 [H, W] padded, iters_done tensor)."""
+    torch = _torch()
+    L = N.lib()
+    W, H = code.padded_w, code.padded_h
+    dev = code.records.device
+    if rasters is None:
+        rasters = (torch.empty((H, W), dtype=torch.float32, device=dev),
+                   torch.empty((H, W), dtype=torch.float32, device=dev))
+    if out is None and want_u8:
+        out = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
+    ws = _WS.get("dec", wsb, dev)
+    N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters), float(stop_delta),
+                                  float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),
+                                  N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return out, it, rasters
+
+
+def decode_units_device(units: dict, W: int, H: int, iters: int, stop_delta: float, initial_value: float,
+                        stream=None):
+    torch = _torch()
+    L = N.lib()
+    dev = units["x"].device
+    ping = torch.empty((H, W), dtype=torch.float32, device=dev)
+    pong = torch.empty((H, W), dtype=torch.float32, device=dev)
+    out = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _WS.get("decu", 64, dev)
+    N.check(L.mns_decode_units(N.ptr(units["x"]), N.ptr(units["y"]), N.ptr(units["size"]), N.ptr(units["dx"]),
+                               N.ptr(units["dy"]), N.ptr(units["s"]), N.ptr(units["o"]), units["x"].numel(), W, H,
+                               int(iters), float(stop_delta), float(initial_value), N.ptr(ping), N.ptr(pong),
+                               N.ptr(out), N.ptr(it), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return out, it
+
+
+def full_search_device(img, B: int, step: int = 1, n_iso: int = 1, ranges: Optional[tuple] = None, stream=None):
+    """Exhaustive search over a B-padded uint8 CUDA image; returns per-range (dom, iso, o, code) tensors."""
+    torch = _torch()
+    L = N.lib()
+    h, w = img.shape
+    nr = (w // B) * (h // B)
+    r0, r1 = ranges if ranges is not None else (0, nr)
+    dev = img.device
+    out = {"dom": torch.empty(r1 - r0, dtype=torch.int32, device=dev),
+           "iso": torch.empty(r1 - r0, dtype=torch.int8, device=dev),
+           "o": torch.empty(r1 - r0, dtype=torch.uint8, device=dev),
+           "code": torch.empty(r1 - r0, dtype=torch.uint8, device=dev)}
+    wsb = N.out_i64(L, L.mns_search_workspace_bytes, w, h, B, step, n_iso)
+    ws = _WS.get("search", wsb, dev)
+    N.check(L.mns_full_search(N.ptr(img), w, h, B, step, n_iso, r0, r1, N.ptr(out["dom"]), N.ptr(out["iso"]),
+                              N.ptr(out["o"]), N.ptr(out["code"]), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return out
+
+
+def local_search_device(img, radius: int = 4, stream=None):
+    torch = _torch()
+    L = N.lib()
+    h, w = img.shape
+    nr = (w // 8) * (h // 8)
+    dev = img.device
+    out = {k: torch.empty(nr, dtype=dt, device=dev) for k, dt in
+           (("dx", torch.int32), ("dy", torch.int32), ("o", torch.uint8), ("code", torch.uint8))}
+    N.check(L.mns_local_search(N.ptr(img), w, h, int(radius), N.ptr(out["dx"]), N.ptr(out["dy"]), N.ptr(out["o"]),
+                               N.ptr(out["code"]), N.stream_ptr(stream)))
+    return out
+
+
+def write_stream_device(records, n: int, orig_w: int, orig_h: int, padded_w: int, padded_h: int, mns: bool,
+                        technique2: bool, stream=None):
+    """GPU .mns packer; returns (uint8 byte tensor with >= ceil(bits/8) valid bytes, bits tensor)."""
+    torch = _torch()
+    L = N.lib()
+    dev = records.device
+    cap = 4 * ((104 + 33 * n + 31) // 32)
+    out = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    bits = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsb = N.out_i64(L, L.mns_stream_workspace_bytes, n)
+    ws = _WS.get("stream", wsb, dev)
+    N.check(L.mns_write_stream(N.ptr(records), n, orig_w, orig_h, padded_w, padded_h, 1 if mns else 0,
+                               1 if technique2 else 0, N.ptr(out), cap, N.ptr(bits), N.ptr(ws), ws.numel(),
+                               N.stream_ptr(stream)))
+    return out, bits
+
+
+# ------------------------------------------------------------------ host layer (reference API)
+
+def _device():
+    torch = _torch()
+    N.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_device_u8(px: np.ndarray):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(px)).to(_device(), non_blocking=False)
+
+
+def encode_quadtree(image, config: EncoderConfig, *, root_level: int = 1) -> QuadtreeCode:
+    """encoder.py:215-246.  root_level=2 is the '8->4' extension (every root split once)."""
+    if config.mode not in ("no_search", "mns"):
+        raise ValueError(f"encode_quadtree handles no_search/mns, not {config.mode!r}")
+    px = _pixels(image)
+    padded = _padded_np(px, ROOT_SIZE)
+    code = encode_device(_to_device_u8(padded), config, root_level=root_level)
+    n = code.n_records()
+    rec = code.records[:n].cpu().numpy().view(np.uint64)
+    offs = code.root_offsets.cpu().numpy()
+    return QuadtreeCode.from_records(rec, padded.shape[1], padded.shape[0], px.shape[1], px.shape[0], config.mode,
+                                     config.technique2, root_offsets=offs)
+
+
+def _records_grouped(code) -> tuple[np.ndarray, np.ndarray]:
+    """Records grouped by root (stable, so DFS order is kept) and root offsets."""
+    rec = np.ascontiguousarray(code.records, dtype=np.uint64)
+    W, H = code.padded_w, code.padded_h
+    rw = W // 16
+    if getattr(code, "root_offsets", None) is not None and len(code.root_offsets) == rw * (H // 16) + 1:
+        return rec, np.ascontiguousarray(code.root_offsets, dtype=np.int32)
+    x = ((rec >> np.uint64(0)) & np.uint64(0x7FFF)).astype(np.int64) * 2
+    y = ((rec >> np.uint64(15)) & np.uint64(0x7FFF)).astype(np.int64) * 2
+    root = (y // 16) * rw + x // 16
+    order = np.argsort(root, kind="stable")
+    counts = np.bincount(root, minlength=rw * (H // 16))
+    offs = np.zeros(len(counts) + 1, dtype=np.int32)
+    np.cumsum(counts, out=offs[1:])
+    return rec[order], offs
+
+
+def _baseline_units(code) -> dict:
+    leaves = code.leaves
+    cols = {k: np.empty(len(leaves), dtype=np.int32) for k in ("x", "y", "size", "dx", "dy")}
+    s = np.empty(len(leaves), dtype=np.float64)
+    o = np.empty(len(leaves), dtype=np.float64)
+    for i, lf in enumerate(leaves):
+        p = lf.payload
+        cols["x"][i], cols["y"][i], cols["size"][i] = lf.rect.x, lf.rect.y, lf.rect.size
+        cols["dx"][i], cols["dy"][i] = p.domain.x, p.domain.y
+        s[i] = dequantize_contrast(p.s_code)
+        o[i] = float(p.o_byte)
+    cols["s"], cols["o"] = s, o
+    return cols
+
+
+def _quadtree_units(code) -> dict:
+    """Painted units of a no_search/mns code (decoder.py:48-59): 1 per phase-1 leaf, 4 per phase-2 leaf."""
+    from .types import unpack_fields
+
+    f = unpack_fields(code.records)
+    W, H = code.padded_w, code.padded_h
+    xs, ys, ss, ss_, os_ = [], [], [], [], []
+    size = np.array([LEVEL_SIZES[int(v)] for v in range(1, 5)])[f["level"] - 1]
+    p1 = ~f["phase2"]
+    xs.append(f["x"][p1]); ys.append(f["y"][p1]); ss.append(size[p1])
+    ss_.append(-0.875 + 0.25 * f["s_code"][p1]); os_.append(f["o"][p1].astype(np.float64))
+    p2 = f["phase2"]
+    if p2.any():
+        lv, h = f["level"][p2], size[p2] // 2
+        d0, d1, d2, ob, sb = f["d0"][p2], f["d1"][p2], f["d2"][p2], f["o"][p2], f["s_bits"][p2]
+        targets = [ob + d0, ob + d1, ob + d2, ob - (d0 + d1 + d2)]
+        sets = np.array([[0, 0], list(CONTRAST_SETS[1]), list(CONTRAST_SETS[2]), list(CONTRAST_SETS[3])])
+        for q in range(4):
+            xs.append(f["x"][p2] + (q & 1) * h); ys.append(f["y"][p2] + (q >> 1) * h); ss.append(h)
+            ss_.append(sets[lv, (sb >> q) & 1]); os_.append(targets[q].astype(np.float64))
+    x = np.concatenate(xs).astype(np.int32)
+    y = np.concatenate(ys).astype(np.int32)
+    sz = np.concatenate(ss).astype(np.int32)
+    dx = np.clip(x - sz // 2, 0, W - 2 * sz).astype(np.int32)
+    dy = np.clip(y - sz // 2, 0, H - 2 * sz).astype(np.int32)
+    return {"x": x, "y": y, "size": sz, "dx": dx, "dy": dy, "s": np.concatenate(ss_), "o": np.concatenate(os_)}
+
+
+def _units_to_device(u: dict, float_dtype):
+    torch = _torch()
+    dev = _device()
+    out = {k: torch.from_numpy(np.ascontiguousarray(u[k])).to(dev) for k in ("x", "y", "size", "dx", "dy")}
+    out["s"] = torch.from_numpy(np.ascontiguousarray(u["s"], dtype=float_dtype)).to(dev)
+    out["o"] = torch.from_numpy(np.ascontiguousarray(u["o"], dtype=float_dtype)).to(dev)
+    return out
+
+
+def decode(code, config: Optional[DecodeConfig] = None) -> GrayImage:
+    """decoder.py:66-77 (fp32 raster on device; parity bar: <= 1 LSB and 0.01 dB)."""
+    torch = _torch()
+    cfg = config if config is not None else DecodeConfig()
+    W, H = code.padded_w, code.padded_h
+    if code.mode in ("no_search", "mns") and (not hasattr(code, "has_records") or code.has_records):
+        rec, offs = _records_grouped(code if isinstance(code, QuadtreeCode) else _wrap_reference(code))
+        dev = _device()
+        dcode = DeviceCode(torch.from_numpy(rec.view(np.int64)).to(dev), torch.from_numpy(offs).to(dev),
+                           torch.tensor([len(rec)], dtype=torch.int64, device=dev), W, H)
+        out, _, _ = decode_device(dcode, cfg.max_iters, cfg.stop_delta, cfg.initial_value)
+    else:
+        u = _units_to_device(_baseline_units(code), np.float32)
+        out, _ = decode_units_device(u, W, H, cfg.max_iters, cfg.stop_delta, cfg.initial_value)
+    px = out.cpu().numpy()
+    return GrayImage(px[: code.orig_h, : code.orig_w])
+
+
+def _wrap_reference(code) -> QuadtreeCode:
+    """Accept a reference mnscodec.QuadtreeCode (same fields) by repacking its leaves."""
+    return QuadtreeCode(code.leaves, code.padded_w, code.padded_h, code.orig_w, code.orig_h, code.mode,
+                        code.technique2)
+
+
+def decode_step(code, current) -> np.ndarray:
+    """decoder.py:37-63: one fp64 Jacobi sweep, bit-identical to the reference (numpy order emulated)."""
+    torch = _torch()
+    cur = np.asarray(current, dtype=np.float64)
+    if cur.shape != (code.padded_h, code.padded_w):
+        raise ValueError(f"raster shape {cur.shape} does not match padded {code.padded_h}x{code.padded_w}")
+    L = N.lib()
+    if code.mode in ("no_search", "mns"):
+        q = code if isinstance(code, QuadtreeCode) else _wrap_reference(code)
+        u = _quadtree_units(q)
+    else:
+        u = _baseline_units(code)
+    du = _units_to_device(u, np.float64)
+    dev = _device()
+    dcur = torch.from_numpy(np.ascontiguousarray(cur)).to(dev)
+    dout = torch.empty_like(dcur)
+    N.check(L.mns_decode_step_f64(N.ptr(du["x"]), N.ptr(du["y"]), N.ptr(du["size"]), N.ptr(du["dx"]),
+                                  N.ptr(du["dy"]), N.ptr(du["s"]), N.ptr(du["o"]), du["x"].numel(), code.padded_w,
+                                  code.padded_h, N.ptr(dcur), N.ptr(dout), N.stream_ptr()))
+    return dout.cpu().numpy()
+
+
+def encode_full_search(image, range_size: int, config: EncoderConfig, *, n_iso: int = 1):
+    """encoder.py:249-309.  n_iso=8 adds the isometry extension (parity vs the restated oracle)."""
+    if range_size not in SIZE_LEVELS:
+        raise ValueError(f"range size must be one of {sorted(SIZE_LEVELS)}")
+    px = _pixels(image)
+    dsize = 2 * range_size
+    if px.shape[1] < dsize or px.shape[0] < dsize:
+        raise ValueError(f"image too small for any {dsize}x{dsize} domain")
+    padded = _padded_np(px, range_size)
+    h, w = padded.shape
+    res = full_search_device(_to_device_u8(padded), range_size, config.full_search_step, n_iso)
+    step = config.full_search_step
+    ndx = (w - dsize) // step + 1
+    dom = res["dom"].cpu().numpy().astype(np.int64)
+    B = range_size
+    rpr = w // B
+    ids = np.arange(len(dom))
+    cols = {"range_size": B, "rx": (ids % rpr) * B, "ry": (ids // rpr) * B, "dom_x": (dom % ndx) * step,
+            "dom_y": (dom // ndx) * step, "o": res["o"].cpu().numpy(), "code": res["code"].cpu().numpy(),
+            "iso": res["iso"].cpu().numpy()}
+    half = B // 2
+    samples = list(zip(((cols["dom_x"] + B) - (cols["rx"] + half)).tolist(),
+                       ((cols["dom_y"] + B) - (cols["ry"] + half)).tolist()))
+    code = QuadtreeCode(None, w, h, px.shape[1], px.shape[0], "full_search", False, columns=cols)
+    return code, samples
+
+
+def encode_local_search(image, config: EncoderConfig, *, radius: int = 4) -> QuadtreeCode:
+    """encoder.py:312-347 (radius 4 = the reference's 81 candidates; other radii are the extension)."""
+    px = _pixels(image)
+    if px.shape[1] < 16 or px.shape[0] < 16:
+        raise ValueError("local search needs at least a 16x16 image")
+    padded = _padded_np(px, 8)
+    h, w = padded.shape
+    res = local_search_device(_to_device_u8(padded), radius)
+    ids = np.arange(res["dx"].numel())
+    rpr = w // 8
+    cols = {"range_size": 8, "rx": (ids % rpr) * 8, "ry": (ids // rpr) * 8, "dom_x": res["dx"].cpu().numpy(),
+            "dom_y": res["dy"].cpu().numpy(), "o": res["o"].cpu().numpy(), "code": res["code"].cpu().numpy()}
+    return QuadtreeCode(None, w, h, px.shape[1], px.shape[0], "local_search", False, columns=cols)

@@ -1,0 +1,146 @@
+// extern "C" boundary of libmns_b200.so (include/mns_b200.h): argument checks,
+// thread-local error strings, and dispatch to the sm_100a kernels.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "mns_common.cuh"
+
+namespace mns {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+double sqrt_bound(double E) {
+    if (!(E < INFINITY)) return INFINITY;
+    double x = E * E;
+    while (x > 0.0 && sqrt(x) > E) x = nextafter(x, 0.0);
+    while (sqrt(nextafter(x, INFINITY)) <= E) x = nextafter(x, INFINITY);
+    return x;
+}
+
+int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes);
+int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t image_stride, int n_images, int rr0,
+                    int rr1, const mns_enc_cfg *cfg, uint64_t *records, int64_t capacity, int32_t *root_offsets,
+                    int64_t *d_count, void *workspace, int64_t workspace_bytes, cudaStream_t stream);
+int decode_workspace_bytes(int W, int H, int64_t *bytes);
+int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
+                    double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                    void *workspace, int64_t workspace_bytes, cudaStream_t stream);
+int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, int H, int rr0, int rr1,
+                 const float *cur, float init, float *nxt, uint8_t *out, int *state, double stop_delta,
+                 cudaStream_t stream);
+int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                 const int32_t *udy, const float *us, const float *uo, int64_t n, int W, int H, int iters,
+                 double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                 void *workspace, int64_t workspace_bytes, cudaStream_t stream);
+int decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                    const int32_t *udy, const double *us, const double *uo, int64_t n, int W, int H,
+                    const double *cur, double *out, cudaStream_t stream);
+int search_workspace_bytes(int W, int H, int B, int step, int n_iso, int64_t *bytes);
+int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1, int32_t *out_dom,
+                int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st);
+int local_search(const uint8_t *img, int W, int H, int radius, int32_t *out_dx, int32_t *out_dy, uint8_t *out_o,
+                 uint8_t *out_code, cudaStream_t st);
+int stream_workspace_bytes(int64_t n, int64_t *bytes);
+int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int ph, int mns, int t2, uint8_t *out,
+                 int64_t cap, int64_t *d_bits, void *ws, int64_t ws_bytes, cudaStream_t st);
+
+}  // namespace mns
+
+#define GUARD(call)                                                   \
+    try {                                                             \
+        return call;                                              \
+    } catch (...) {                                                   \
+        mns::set_error("unexpected C++ exception");                   \
+        return -3;                                                    \
+    }
+
+extern "C" {
+
+const char *mns_last_error(void) { return mns::g_err; }
+int mns_version(void) { return 1; }
+
+int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t rr0, int32_t rr1, int64_t *bytes) {
+    GUARD(mns::encode_workspace_bytes(width, n_images, rr0, rr1, bytes));
+}
+
+int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
+                        int32_t n_images, int32_t rr0, int32_t rr1, const mns_enc_cfg *cfg, uint64_t *records,
+                        int64_t capacity, int32_t *root_offsets, int64_t *d_count, void *workspace,
+                        int64_t workspace_bytes, void *stream) {
+    GUARD(mns::encode_quadtree(img, width, height, pitch, image_stride, n_images, rr0, rr1, cfg, records, capacity,
+                               root_offsets, d_count, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_decode_workspace_bytes(int32_t width, int32_t height, int64_t *bytes) {
+    GUARD(mns::decode_workspace_bytes(width, height, bytes));
+}
+
+int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                        int32_t iters, double stop_delta, float initial_value, float *ping, float *pong,
+                        uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                        void *stream) {
+    GUARD(mns::decode_quadtree(records, root_offsets, width, height, iters, stop_delta, initial_value, ping, pong,
+                               out, d_iters_done, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_decode_sweep(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                     int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value,
+                     float *nxt, uint8_t *out, int32_t *state, double stop_delta, void *stream) {
+    GUARD(mns::decode_sweep(records, root_offsets, width, height, root_row_begin, root_row_end, cur, initial_value,
+                            nxt, out, state, stop_delta, (cudaStream_t)stream));
+}
+
+int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                     const int32_t *udy, const float *us, const float *uo, int64_t n_units, int32_t width,
+                     int32_t height, int32_t iters, double stop_delta, float initial_value, float *ping,
+                     float *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                     void *stream) {
+    GUARD(mns::decode_units(ux, uy, usize, udx, udy, us, uo, n_units, width, height, iters, stop_delta,
+                            initial_value, ping, pong, out, d_iters_done, workspace, workspace_bytes,
+                            (cudaStream_t)stream));
+}
+
+int mns_decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                        const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                        int32_t height, const double *cur, double *out, void *stream) {
+    GUARD(mns::decode_step_f64(ux, uy, usize, udx, udy, us, uo, n_units, width, height, cur, out,
+                               (cudaStream_t)stream));
+}
+
+int mns_search_workspace_bytes(int32_t width, int32_t height, int32_t B, int32_t step, int32_t n_iso,
+                               int64_t *bytes) {
+    GUARD(mns::search_workspace_bytes(width, height, B, step, n_iso, bytes));
+}
+
+int mns_full_search(const uint8_t *img, int32_t width, int32_t height, int32_t B, int32_t step, int32_t n_iso,
+                    int32_t range_begin, int32_t range_end, int32_t *out_dom, int8_t *out_iso, uint8_t *out_o,
+                    uint8_t *out_code, void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::full_search(img, width, height, B, step, n_iso, range_begin, range_end, out_dom, out_iso, out_o,
+                           out_code, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t *out_dx,
+                     int32_t *out_dy, uint8_t *out_o, uint8_t *out_code, void *stream) {
+    GUARD(mns::local_search(img, width, height, radius, out_dx, out_dy, out_o, out_code, (cudaStream_t)stream));
+}
+
+int mns_stream_workspace_bytes(int64_t n_records, int64_t *bytes) {
+    GUARD(mns::stream_workspace_bytes(n_records, bytes));
+}
+
+int mns_write_stream(const uint64_t *records, int64_t n_records, int32_t orig_w, int32_t orig_h, int32_t padded_w,
+                     int32_t padded_h, int32_t mns, int32_t technique2, uint8_t *out, int64_t out_capacity,
+                     int64_t *d_bits, void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::write_stream(records, n_records, orig_w, orig_h, padded_w, padded_h, mns, technique2, out,
+                            out_capacity, d_bits, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Shared device/host helpers for libmns_b200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mns_b200.h"
+
+namespace mns {
+
+// Thread-local last error (mns_last_error) -- set by the ABI layer.
+void set_error(const char *fmt, ...);
+
+#define MNS_CUDA_TRY(expr)                                                               \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            ::mns::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                             __FILE__, __LINE__);                                        \
+            return -1;                                                                   \
+        }                                                                                \
+    } while (0)
+
+#define MNS_CHECK_ARG(cond, msg)                                                         \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            ::mns::set_error("invalid argument: %s", msg);                               \
+            return -2;                                                                   \
+        }                                                                                \
+    } while (0)
+
+// Largest double x with fl(sqrt(x)) <= E (IEEE sqrt is correctly rounded, so
+// "rms <= E" <=> "mean square <= bound(E)" exactly).  +inf for E = +inf.
+double sqrt_bound(double E);
+
+__host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// numpy pairwise_sum for float64 (loops_utils.h.src), restated; a points to
+// shared or local memory.  n <= 256.
+__device__ inline double pw_sum_dev(const double *a, int n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    // n in (128, 256]: split at n/2 rounded down to a multiple of 8 (one level suffices)
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    double lo, hi;
+    {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int i;
+        for (i = 8; i < n2 - (n2 % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+        lo = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n2; i++) lo = __dadd_rn(lo, a[i]);
+    }
+    {
+        const double *b = a + n2;
+        int m = n - n2;
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = b[j];
+        int i;
+        for (i = 8; i < m - (m % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], b[i + j]);
+        hi = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < m; i++) hi = __dadd_rn(hi, b[i]);
+    }
+    return __dadd_rn(lo, hi);
+}
+
+__device__ inline unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ inline unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ inline void st_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back (single-pass exclusive scan over tiles in launch order).
+// status[] must be zeroed before the launch.  Called by ONE thread per tile;
+// returns the exclusive prefix of `agg` over tiles [0, tile).
+constexpr unsigned long long LB_AGG = 1ull << 62;
+constexpr unsigned long long LB_PREFIX = 2ull << 62;
+constexpr unsigned long long LB_MASK = (1ull << 62) - 1;
+
+__device__ inline long long lookback_exclusive(unsigned long long *status, long long tile, long long agg) {
+    if (tile == 0) {
+        st_release_u64(&status[0], LB_PREFIX | (unsigned long long)agg);
+        return 0;
+    }
+    st_release_u64(&status[tile], LB_AGG | (unsigned long long)agg);
+    long long excl = 0;
+    long long p = tile - 1;
+    while (true) {
+        unsigned long long v = ld_acquire_u64(&status[p]);
+        unsigned long long flag = v & ~LB_MASK;
+        if (flag == 0) {
+            __nanosleep(32);
+            continue;
+        }
+        excl += (long long)(v & LB_MASK);
+        if (flag == LB_PREFIX) break;
+        --p;
+    }
+    st_release_u64(&status[tile], LB_PREFIX | (unsigned long long)(excl + agg));
+    return excl;
+}
+
+}  // namespace mns

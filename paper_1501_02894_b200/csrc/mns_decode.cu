@@ -1,0 +1,464 @@
+// Iterative (Jacobi) decoder for sm_100a (K4).
+//
+// Replaces decoder.py:37-77 (decode_step / decode / _paint) and
+// transform.py:63-66 (apply_map).  One launch = one sweep: every painted unit
+// reads the previous raster only and writes its own disjoint square of the next
+// one, so leaf order is immaterial (decoder.py:8-10, test_decoder.py:27-34).
+//
+// Quadtree path (mns_decode_quadtree): a CTA owns a TRY x TRX tile of 16x16
+// roots.  It stages the fp32 window [tile - 16, tile + 16) of the previous
+// raster in shared memory with 16-byte loads (every co-centred domain of every
+// unit of its roots lies inside it), decodes each root's packed records into a
+// 64-entry Morton-cell table of (s, o, domain, size), and then each lane paints
+// the 2x4 pixels it owns: q = 2x2 sum of the domain group, per-unit domain sum by
+// segmented warp reductions (pair / 8-lane / 32-lane / in-lane), and
+// clip(s*(q/4 - mean) + o, 0, 255) stored with coalesced 16-byte stores.  The
+// final sweep writes the rounded uint8 image directly (floor(x+0.5), clip).
+//
+// Generic path (mns_decode_units): one warp per unit, explicit domains
+// (search-baseline BaselinePayload codes, encoder.py:101-107).
+//
+// Exact path (mns_decode_step_f64): one thread per unit replaying numpy's fp64
+// order (pairwise mean), bit-identical to decode_step, for parity evidence.
+
+#include <math.h>
+
+#include "mns_common.cuh"
+
+namespace mns {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TRX = 4, TRY = 4;                 // roots per CTA tile
+constexpr int DT = TRX * TRY * 32;              // 512 threads
+constexpr int DWIN_W = TRX * 16 + 32;           // 96
+constexpr int DWIN_H = TRY * 16 + 32;           // 96
+
+__constant__ float kContrastSets[4][2] = {{0.f, 0.f}, {0.2f, 0.5f}, {0.4f, 0.65f}, {0.5f, 0.9f}};
+
+struct Cell {
+    float s, o;
+    short dx, dy;  // domain origin, window coordinates
+    int size;      // unit side (2..16)
+};
+
+struct DecParams {
+    const uint64_t *records;
+    const int32_t *root_offsets;  // local to the root rows [rr0, rr1)
+    int W, H, rw, rr0, rr1;
+    int y_lo, y_hi;               // resident raster rows (strip + halo), global coordinates
+    const float *cur;    // null on the first sweep: the flat start raster (initial_value) is implied
+    float init;
+    float *nxt;          // may be null on the final sweep
+    uint8_t *out_u8;     // non-null on the final sweep
+    int *state;          // [0] done flag, [1] iterations done, [2] finished-CTA counter, [3] max delta bits
+    int track_delta;     // stop_delta > 0
+    float stop_delta;
+    int n_ctas;
+};
+
+__device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates -> 6-bit Morton (y major)
+    int m = 0;
+#pragma unroll
+    for (int i = 0; i < 3; i++) m |= (((cx >> i) & 1) << (2 * i)) | (((cy >> i) & 1) << (2 * i + 1));
+    return m;
+}
+
+__global__ void __launch_bounds__(DT) decode_sweep_kernel(const DecParams p) {
+    extern __shared__ __align__(16) unsigned char dsm[];  // > 48 KB: dynamic shared memory
+    float(*win)[DWIN_W] = reinterpret_cast<float(*)[DWIN_W]>(dsm);
+    Cell(*cells)[64] = reinterpret_cast<Cell(*)[64]>(dsm + sizeof(float) * DWIN_H * DWIN_W);
+    __shared__ float cta_max;
+
+    if (p.state[0]) return;  // converged in an earlier sweep (stop_delta > 0)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int trx = blockIdx.x, try_ = blockIdx.y;
+    const int x0 = trx * TRX * 16, y0 = (p.rr0 + try_ * TRY) * 16;
+    const int wx0 = x0 - 16, wy0 = y0 - 16;
+    const int W = p.W, H = p.H;
+    if (tid == 0) cta_max = 0.f;
+
+    // stage the window of the previous raster
+    constexpr int CH = DWIN_W / 4;
+    for (int c = tid; c < DWIN_H * CH; c += DT) {
+        const int wr = c / CH, wc = (c % CH) * 4;
+        const int gy = wy0 + wr, gx = wx0 + wc;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gy >= p.y_lo && gy < p.y_hi && gx >= 0 && gx < W)
+            v = p.cur ? __ldg(reinterpret_cast<const float4 *>(p.cur + (ptrdiff_t)gy * W + gx))
+                      : make_float4(p.init, p.init, p.init, p.init);
+        *reinterpret_cast<float4 *>(&win[wr][wc]) = v;
+    }
+
+    // per-root unit table (Morton cells)
+    const int rxi = trx * TRX + (warp % TRX), ryi = p.rr0 + try_ * TRY + (warp / TRX);
+    const bool live = rxi < p.rw && ryi < p.rr1;
+    const int rxg = rxi * 16, ryg = ryi * 16;
+    if (live) {
+        const int root = (ryi - p.rr0) * p.rw + rxi;
+        const int beg = p.root_offsets[root], end = p.root_offsets[root + 1];
+        for (int i = beg + lane; i < end; i += 32) {
+            const uint64_t r = p.records[i];
+            const int x = (int)((r >> MNS_REC_X_SHIFT) & 0x7FFF) * 2, y = (int)((r >> MNS_REC_Y_SHIFT) & 0x7FFF) * 2;
+            const int level = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1;
+            const int size = 32 >> level;
+            const int ob = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
+            if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) {
+                Cell cl;
+                cl.s = -0.875f + 0.25f * (float)((r >> MNS_REC_PAYLOAD_SHIFT) & 7);
+                cl.o = (float)ob;
+                cl.size = size;
+                cl.dx = (short)(clampi(x - size / 2, 0, W - 2 * size) - wx0);
+                cl.dy = (short)(clampi(y - size / 2, 0, H - 2 * size) - wy0);
+                const int m0 = morton_of((x - rxg) >> 1, (y - ryg) >> 1), nc = (size / 2) * (size / 2);
+                for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
+            } else {
+                int d[3];
+#pragma unroll
+                for (int j = 0; j < 3; j++) {
+                    const int f = (int)((r >> (41 + 6 * j)) & 63);
+                    d[j] = f >= 32 ? f - 64 : f;
+                }
+                const int bits = (int)((r >> 59) & 15);
+                const int t[4] = {ob + d[0], ob + d[1], ob + d[2], ob - (d[0] + d[1] + d[2])};
+                const int h = size / 2;
+                for (int q = 0; q < 4; q++) {
+                    const int qx = x + (q & 1) * h, qy = y + (q >> 1) * h;
+                    Cell cl;
+                    cl.s = kContrastSets[level][(bits >> q) & 1];
+                    cl.o = (float)t[q];
+                    cl.size = h;
+                    cl.dx = (short)(clampi(qx - h / 2, 0, W - 2 * h) - wx0);
+                    cl.dy = (short)(clampi(qy - h / 2, 0, H - 2 * h) - wy0);
+                    const int m0 = morton_of((qx - rxg) >> 1, (qy - ryg) >> 1), nc = (h / 2) * (h / 2);
+                    for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    float lmax = 0.f;
+    if (live) {
+        const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
+        const int lx = (a & 1) * 8 + (b & 1) * 4, ly = (a >> 1) * 8 + (b >> 1) * 4 + 2 * c;
+        const Cell cA = cells[warp][2 * lane], cB = cells[warp][2 * lane + 1];
+        // q for the lane's 8 pixels (unit origin = cell's unit origin; pixel offset inside the unit)
+        float q[8];
+#pragma unroll
+        for (int side = 0; side < 2; side++) {
+            const Cell &cl = side ? cB : cA;
+            // unit origin (root-relative) from its size: units are aligned to their size
+            const int px0 = lx + 2 * side, py0 = ly;
+            const int ux = px0 & ~(cl.size - 1), uy = py0 & ~(cl.size - 1);
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const int yy = cl.dy + 2 * (py0 + i - uy), xx = cl.dx + 2 * (px0 + j - ux);
+                    q[4 * i + 2 * side + j] = ((win[yy][xx] + win[yy][xx + 1]) + win[yy + 1][xx]) + win[yy + 1][xx + 1];
+                }
+        }
+        const float sA = q[0] + q[1] + q[4] + q[5], sB = q[2] + q[3] + q[6] + q[7];
+        float s2 = sA + sB;
+        s2 += __shfl_xor_sync(FULL, s2, 1);   // 4x4 unit (lane pair)
+        float s8 = s2 + __shfl_xor_sync(FULL, s2, 2);
+        s8 += __shfl_xor_sync(FULL, s8, 4);   // 8x8 unit (8 lanes)
+        float s32 = s8 + __shfl_xor_sync(FULL, s8, 8);
+        s32 += __shfl_xor_sync(FULL, s32, 16);  // 16x16 unit (warp)
+        auto unit_sum = [&](int size, float own) {
+            return size == 2 ? own : (size == 4 ? s2 : (size == 8 ? s8 : s32));
+        };
+        const float mA = unit_sum(cA.size, sA) * 0.25f / (float)(cA.size * cA.size);
+        const float mB = unit_sum(cB.size, sB) * 0.25f / (float)(cB.size * cB.size);
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const bool right = (k & 3) >= 2;
+            const Cell &cl = right ? cB : cA;
+            const float m = right ? mB : mA;
+            float t = fmaf(cl.s, q[k] * 0.25f - m, cl.o);
+            v[k] = fminf(255.f, fmaxf(0.f, t));
+        }
+        const int gx = rxg + lx, gy = ryg + ly;
+        if (p.track_delta) {
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    lmax = fmaxf(lmax, fabsf(v[4 * i + j] - win[gy + i - wy0][gx + j - wx0]));
+        }
+        if (p.nxt) {
+            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * W + gx) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * W + gx) = make_float4(v[4], v[5], v[6], v[7]);
+        }
+        if (p.out_u8) {
+            uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                w0 |= (uint32_t)floorf(v[j] + 0.5f) << (8 * j);
+                w1 |= (uint32_t)floorf(v[4 + j] + 0.5f) << (8 * j);
+            }
+            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * W + gx) = w0;
+            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * W + gx) = w1;
+        }
+    }
+    if (p.track_delta) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(FULL, lmax, o));
+        if (lane == 0) atomicMax(reinterpret_cast<int *>(&cta_max), __float_as_int(lmax));
+        __syncthreads();
+        if (tid == 0) {
+            atomicMax(&p.state[3], __float_as_int(cta_max));
+            __threadfence();
+            const int done = atomicAdd(&p.state[2], 1);
+            if (done == p.n_ctas - 1) {  // last CTA of this sweep decides the early stop
+                __threadfence();
+                const float delta = __int_as_float(atomicAdd(&p.state[3], 0));
+                p.state[1] += 1;
+                if (delta < p.stop_delta) p.state[0] = 1;
+                p.state[2] = 0;
+                p.state[3] = 0;
+            }
+        }
+    }
+}
+
+// Per-sweep iteration counter when stop_delta == 0 (no early stop possible).
+__global__ void set_iters_kernel(int *state, int iters) {
+    state[0] = 0;
+    state[1] = iters;
+}
+
+// clip(floor(x + 0.5)) -> uint8 from the raster that holds the final sweep
+__global__ void finalize_kernel(const float *ping, const float *pong, const int *state, uint8_t *out, long long n) {
+    const float *src = (state[1] & 1) ? pong : ping;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float v = floorf(src[i] + 0.5f);
+        out[i] = (uint8_t)fminf(255.f, fmaxf(0.f, v));
+    }
+}
+
+__global__ void fill_kernel(float *a, float v, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+
+// ---------------------------------------------------------------- generic units
+struct UnitParams {
+    const int32_t *ux, *uy, *usize, *udx, *udy;
+    const float *us, *uo;
+    long long n;
+    int W;
+    const float *cur;
+    float *nxt;
+    int *state;
+    int track_delta;
+    float stop_delta;
+    int n_ctas;
+};
+
+__global__ void __launch_bounds__(256) decode_units_kernel(const UnitParams p) {
+    __shared__ float cta_max;
+    if (p.state[0]) return;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) cta_max = 0.f;
+    __syncthreads();
+    float lmax = 0.f;
+    const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+    for (long long u = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); u < p.n; u += warps) {
+        const int size = p.usize[u], x = p.ux[u], y = p.uy[u], dx = p.udx[u], dy = p.udy[u];
+        const float s = p.us[u], o = p.uo[u];
+        const int n = size * size;
+        float acc = 0.f;
+        for (int k = lane; k < n; k += 32) {
+            const int i = k / size, j = k % size;
+            const float *pp = p.cur + (size_t)(dy + 2 * i) * p.W + dx + 2 * j;
+            acc += ((pp[0] + pp[1]) + pp[p.W]) + pp[p.W + 1];
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(FULL, acc, o2);
+        const float mean = acc * 0.25f / (float)n;
+        for (int k = lane; k < n; k += 32) {
+            const int i = k / size, j = k % size;
+            const float *pp = p.cur + (size_t)(dy + 2 * i) * p.W + dx + 2 * j;
+            const float q = ((pp[0] + pp[1]) + pp[p.W]) + pp[p.W + 1];
+            const float v = fminf(255.f, fmaxf(0.f, fmaf(s, q * 0.25f - mean, o)));
+            const size_t idx = (size_t)(y + i) * p.W + x + j;
+            if (p.track_delta) lmax = fmaxf(lmax, fabsf(v - p.cur[idx]));
+            p.nxt[idx] = v;
+        }
+    }
+    if (p.track_delta) {
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(FULL, lmax, o2));
+        if (lane == 0) atomicMax(reinterpret_cast<int *>(&cta_max), __float_as_int(lmax));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            atomicMax(&p.state[3], __float_as_int(cta_max));
+            __threadfence();
+            const int done = atomicAdd(&p.state[2], 1);
+            if (done == p.n_ctas - 1) {
+                __threadfence();
+                const float delta = __int_as_float(atomicAdd(&p.state[3], 0));
+                p.state[1] += 1;
+                if (delta < p.stop_delta) p.state[0] = 1;
+                p.state[2] = 0;
+                p.state[3] = 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- exact fp64 step
+__global__ void decode_step_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
+                                       const int32_t *udx, const int32_t *udy, const double *us, const double *uo,
+                                       long long n, int W, const double *cur, double *out) {
+    const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int size = usize[u], m = size * size;
+    double d[256];
+    for (int i = 0; i < size; i++)
+        for (int j = 0; j < size; j++) {
+            const double *pp = cur + (size_t)(udy[u] + 2 * i) * W + udx[u] + 2 * j;
+            d[i * size + j] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), pp[W]), pp[W + 1]), 0.25);
+        }
+    const double dm = __ddiv_rn(pw_sum_dev(d, m), (double)m);
+    for (int i = 0; i < size; i++)
+        for (int j = 0; j < size; j++) {
+            double v = __dadd_rn(__dmul_rn(us[u], __dsub_rn(d[i * size + j], dm)), uo[u]);
+            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+            out[(size_t)(uy[u] + i) * W + ux[u] + j] = v;
+        }
+}
+
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace
+
+int decode_workspace_bytes(int, int, int64_t *bytes) {
+    *bytes = 64;
+    return 0;
+}
+
+static int sweep_smem() { return sizeof(float) * DWIN_H * DWIN_W + sizeof(Cell) * TRX * TRY * 64; }
+
+static int ensure_sweep_attr() {
+    static bool attr_set = false;
+    if (!attr_set) {
+        MNS_CUDA_TRY(cudaFuncSetAttribute(decode_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          sweep_smem()));
+        attr_set = true;
+    }
+    return 0;
+}
+
+// One Jacobi sweep over root rows [rr0, rr1).  cur/nxt/out are "virtual global" bases
+// (row 0 of the full image); only rows [y_lo, y_hi) of cur are resident and read.
+int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, int H, int rr0, int rr1,
+                 const float *cur, float init, float *nxt, uint8_t *out, int *state, double stop_delta,
+                 cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
+    if (ensure_sweep_attr()) return -1;
+    DecParams p{};
+    p.records = records;
+    p.root_offsets = root_offsets;
+    p.W = W;
+    p.H = H;
+    p.rw = W / 16;
+    p.rr0 = rr0;
+    p.rr1 = rr1;
+    p.y_lo = rr0 * 16 - 16 > 0 ? rr0 * 16 - 16 : 0;
+    p.y_hi = rr1 * 16 + 16 < H ? rr1 * 16 + 16 : H;
+    p.cur = cur;
+    p.init = init;
+    p.nxt = nxt;
+    p.out_u8 = out;
+    p.state = state;
+    p.track_delta = stop_delta > 0.0;
+    p.stop_delta = (float)stop_delta;
+    dim3 grid((p.rw + TRX - 1) / TRX, (rr1 - rr0 + TRY - 1) / TRY);
+    p.n_ctas = grid.x * grid.y;
+    decode_sweep_kernel<<<grid, DT, sweep_smem(), stream>>>(p);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
+                    double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                    void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    MNS_CHECK_ARG(workspace_bytes >= 64, "workspace too small");
+    MNS_CHECK_ARG(((uintptr_t)ping & 15) == 0 && ((uintptr_t)pong & 15) == 0, "rasters must be 16-byte aligned");
+    int *state = reinterpret_cast<int *>(workspace);
+    const long long npx = (long long)W * H;
+    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
+    const bool track = stop_delta > 0.0;
+    for (int it = 0; it < iters; it++) {
+        // sweep 0 reads the implied flat raster (no fill pass, no read traffic)
+        const float *cur = it == 0 ? nullptr : ((it & 1) ? pong : ping);
+        // out != NULL and no early stop: the final sweep writes the rounded uint8 image directly
+        const bool last_fused = out && !track && it == iters - 1;
+        float *nxt = last_fused ? nullptr : ((it & 1) ? ping : pong);
+        const int rc = decode_sweep(records, root_offsets, W, H, 0, H / 16, cur, init, nxt,
+                                    last_fused ? out : nullptr, state, stop_delta, stream);
+        if (rc) return rc;
+    }
+    if (!track) set_iters_kernel<<<1, 1, 0, stream>>>(state, iters);
+    if (out && track) finalize_kernel<<<sm_count() * 4, 256, 0, stream>>>(ping, pong, state, out, npx);
+    if (d_iters_done) MNS_CUDA_TRY(cudaMemcpyAsync(d_iters_done, state + 1, 4, cudaMemcpyDeviceToDevice, stream));
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                 const int32_t *udy, const float *us, const float *uo, int64_t n, int W, int H, int iters,
+                 double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                 void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0, "bad raster size");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    MNS_CHECK_ARG(workspace_bytes >= 64, "workspace too small");
+    int *state = reinterpret_cast<int *>(workspace);
+    const long long npx = (long long)W * H;
+    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
+    fill_kernel<<<sm_count() * 4, 256, 0, stream>>>(ping, init, npx);
+    UnitParams p{ux, uy, usize, udx, udy, us, uo, n, W, nullptr, nullptr, state, stop_delta > 0.0,
+                 (float)stop_delta, 0};
+    const long long want = (n + 7) / 8;
+    const int blocks = (int)(want < sm_count() * 16 ? (want > 0 ? want : 1) : sm_count() * 16);
+    p.n_ctas = blocks;
+    for (int it = 0; it < iters; it++) {
+        p.cur = (it & 1) ? pong : ping;
+        p.nxt = (it & 1) ? ping : pong;
+        decode_units_kernel<<<blocks, 256, 0, stream>>>(p);
+    }
+    if (!p.track_delta) set_iters_kernel<<<1, 1, 0, stream>>>(state, iters);
+    if (out) finalize_kernel<<<sm_count() * 4, 256, 0, stream>>>(ping, pong, state, out, npx);
+    if (d_iters_done) MNS_CUDA_TRY(cudaMemcpyAsync(d_iters_done, state + 1, 4, cudaMemcpyDeviceToDevice, stream));
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                    const int32_t *udy, const double *us, const double *uo, int64_t n, int W, int H,
+                    const double *cur, double *out, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0, "bad raster size");
+    if (n == 0) return 0;
+    decode_step_f64_kernel<<<(unsigned)((n + 63) / 64), 64, 0, stream>>>(ux, uy, usize, udx, udy, us, uo, n, W, cur,
+                                                                          out);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace mns

@@ -1,0 +1,193 @@
+// .mns bitstream packer for sm_100a (SURVEY 8(f) "next" #1).
+//
+// Replaces bitstream.py:130-205 (_serialize / write_stream) and :282-300
+// (stream_bit_count) for no_search / mns codes held as packed records in DFS
+// order: per-leaf widths (leaf_bit_width, bitstream.py:95-100, with Technique-2
+// elision of the 2nd..4th level-4 quartet ids, :185-191), a decoupled
+// look-back exclusive scan of the widths, then one thread per output 32-bit
+// word gathers the (at most a handful of) records overlapping it -- MSB-first,
+// no atomics, coalesced stores.  The 13-byte header (magic "MNS1", flags,
+// four big-endian u16 dimensions) is emitted by the same gather.
+
+#include "mns_common.cuh"
+
+namespace mns {
+namespace {
+
+constexpr int HEADER_BITS = 13 * 8;
+constexpr int SCAN_T = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_T * SCAN_IPT;
+
+__device__ __forceinline__ int rec_level(uint64_t r) { return (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1; }
+
+__device__ __forceinline__ int rec_width(uint64_t r, int mns, int t2) {
+    const int level = rec_level(r);
+    const bool p2 = (r >> MNS_REC_PHASE2_SHIFT) & 1;
+    bool elided = false;
+    if (level == 4 && t2) {  // 2nd..4th member of a level-4 quartet: not the TL child of its level-3 parent
+        const int cx = (int)((r >> MNS_REC_X_SHIFT) & 1), cy = (int)((r >> MNS_REC_Y_SHIFT) & 1);
+        elided = (cx | cy) != 0;
+    }
+    int w = elided ? 0 : 2;
+    if (mns && level <= 3) w += 1;
+    w += p2 ? 8 + 3 * (1 + (level == 1 ? 4 : 5)) + 4 : 11;
+    return w;
+}
+
+// record -> (bits, width), bits right-aligned, MSB = first stream bit
+__device__ __forceinline__ uint64_t rec_bits(uint64_t r, int mns, int t2, int &w) {
+    const int level = rec_level(r);
+    const bool p2 = (r >> MNS_REC_PHASE2_SHIFT) & 1;
+    uint64_t v = 0;
+    w = 0;
+    auto put = [&](uint64_t val, int nb) {
+        v = (v << nb) | (val & ((1ull << nb) - 1));
+        w += nb;
+    };
+    bool elided = false;
+    if (level == 4 && t2) elided = (((r >> MNS_REC_X_SHIFT) | (r >> MNS_REC_Y_SHIFT)) & 1) != 0;
+    if (!elided) put((uint64_t)(level - 1), 2);
+    if (mns && level <= 3) put(p2 ? 1 : 0, 1);
+    put((r >> MNS_REC_O_SHIFT) & 0xFF, 8);
+    if (p2) {
+        const int mb = level == 1 ? 4 : 5;
+        for (int j = 0; j < 3; j++) {
+            int f = (int)((r >> (41 + 6 * j)) & 63);
+            const int d = f >= 32 ? f - 64 : f;
+            put(d < 0 ? 1 : 0, 1);  // magnitude 0 forces sign 0 (bitstream.py:168)
+            put((uint64_t)(d < 0 ? -d : d), mb);
+        }
+        for (int k = 0; k < 4; k++) put((r >> (59 + k)) & 1, 1);
+    } else {
+        put((r >> MNS_REC_PAYLOAD_SHIFT) & 7, 3);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) width_scan_kernel(const uint64_t *rec, long long n, int mns, int t2,
+                                                            long long *offsets, unsigned long long *status,
+                                                            long long *total_bits) {
+    __shared__ long long warp_tot[SCAN_T / 32];
+    __shared__ long long base_sh;
+    const long long tile = blockIdx.x;
+    const long long i0 = tile * SCAN_TILE + (long long)threadIdx.x * SCAN_IPT;
+    int w[SCAN_IPT];
+    long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; k++) {
+        w[k] = (i0 + k < n) ? rec_width(rec[i0 + k], mns, t2) : 0;
+        sum += w[k];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long agg = 0;
+        for (int k = 0; k < SCAN_T / 32; k++) {
+            const long long t = warp_tot[k];
+            warp_tot[k] = agg;
+            agg += t;
+        }
+        const long long base = lookback_exclusive(status, tile, agg);
+        base_sh = base;
+        if (tile == gridDim.x - 1) *total_bits = HEADER_BITS + base + agg;
+    }
+    __syncthreads();
+    long long off = HEADER_BITS + base_sh + warp_tot[warp] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; k++) {
+        if (i0 + k < n) offsets[i0 + k] = off;
+        off += w[k];
+    }
+}
+
+__global__ void scatter_kernel(const uint64_t *rec, const long long *offsets, long long n, int mns, int t2,
+                               const long long *total_bits, uint32_t hdr0, uint32_t hdr1, uint32_t hdr2,
+                               uint32_t hdr3, uint8_t *out, long long max_words) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long tb = *total_bits;
+    const long long nwords = (tb + 31) / 32;
+    if (k >= nwords || k >= max_words) return;
+    const long long b0 = 32 * k, b1 = b0 + 32;
+    uint64_t acc = 0;  // big-endian word value in the low 32 bits
+    if (b0 < HEADER_BITS) {
+        const uint32_t h[4] = {hdr0, hdr1, hdr2, hdr3};
+        acc = h[k];
+    }
+    // first record with offset + width > b0: binary search the last record with offset <= b0
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (offsets[mid] <= b0) lo = mid + 1;
+        else hi = mid;
+    }
+    long long i = lo > 0 ? lo - 1 : 0;
+    for (; i < n; i++) {
+        const long long off = offsets[i];
+        if (off >= b1) break;
+        int w;
+        const uint64_t v = rec_bits(rec[i], mns, t2, w);
+        if (off + w <= b0) continue;
+        // place bits [off, off+w) into window [b0, b0+32)
+        const long long shift = (b1 - (off + w));  // distance of the record's last bit from the window end
+        uint64_t part;
+        if (shift >= 0) part = v << shift;
+        else part = v >> (-shift);
+        acc |= part & 0xFFFFFFFFull;
+    }
+    const uint32_t be = (uint32_t)acc;
+    reinterpret_cast<uint32_t *>(out)[k] = __byte_perm(be, 0, 0x0123);
+}
+
+}  // namespace
+
+int stream_workspace_bytes(int64_t n, int64_t *bytes) {
+    const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    *bytes = ((n * 8 + 255) & ~255ll) + ((tiles * 8 + 255) & ~255ll) + 256;
+    return 0;
+}
+
+int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int ph, int mns, int t2, uint8_t *out,
+                 int64_t cap, int64_t *d_bits, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    MNS_CHECK_ARG(pw % 16 == 0 && ph % 16 == 0, "padded dimensions must be multiples of 16");
+    MNS_CHECK_ARG(0 < ow && ow <= pw && 0 < oh && oh <= ph, "original dimensions must fit inside the padded raster");
+    MNS_CHECK_ARG(pw <= 0xFFFF && ph <= 0xFFFF, "dimensions exceed the 16-bit header fields");
+    MNS_CHECK_ARG(((uintptr_t)out & 3) == 0, "output must be 4-byte aligned");
+    int64_t need;
+    stream_workspace_bytes(n, &need);
+    MNS_CHECK_ARG(ws_bytes >= need, "workspace too small");
+    const long long max_words = (HEADER_BITS + 33 * (long long)n + 31) / 32;
+    MNS_CHECK_ARG(cap >= 4 * max_words, "output capacity too small (need 4*ceil((104+33n)/32) bytes)");
+    char *p = (char *)ws;
+    long long *offsets = (long long *)p;
+    p += (n * 8 + 255) & ~255ll;
+    const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    unsigned long long *status = (unsigned long long *)p;
+    p += (tiles * 8 + 255) & ~255ll;
+    // header: "MNS1", flags, orig_w, orig_h, padded_w, padded_h (big endian), then leaf bits
+    const uint8_t flags = (mns ? 1 : 0) | (t2 ? 2 : 0);
+    const uint8_t hb[16] = {'M', 'N', 'S', '1', flags, (uint8_t)(ow >> 8), (uint8_t)ow, (uint8_t)(oh >> 8),
+                            (uint8_t)oh, (uint8_t)(pw >> 8), (uint8_t)pw, (uint8_t)(ph >> 8), (uint8_t)ph, 0, 0, 0};
+    uint32_t h[4];
+    for (int k = 0; k < 4; k++)
+        h[k] = ((uint32_t)hb[4 * k] << 24) | ((uint32_t)hb[4 * k + 1] << 16) | ((uint32_t)hb[4 * k + 2] << 8) |
+               hb[4 * k + 3];
+    if (n > 0) {
+        MNS_CUDA_TRY(cudaMemsetAsync(status, 0, tiles * 8, st));
+        width_scan_kernel<<<(unsigned)tiles, SCAN_T, 0, st>>>(records, n, mns, t2, offsets, status, (long long *)d_bits);
+    } else {
+        const long long hbits = HEADER_BITS;
+        MNS_CUDA_TRY(cudaMemcpyAsync(d_bits, &hbits, 8, cudaMemcpyHostToDevice, st));
+        MNS_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    scatter_kernel<<<(unsigned)((max_words + 255) / 256), 256, 0, st>>>(records, offsets, n, mns, t2, (const long long *)d_bits, h[0],
+                                                                        h[1], h[2], h[3], out, max_words);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace mns

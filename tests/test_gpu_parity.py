@@ -1,0 +1,222 @@
+"""GPU parity: libmns_b200 (sm_100a) against the reference's golden vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): transform codes bit-exact; decoded images within
+1 LSB per pixel and 0.01 dB PSNR of the reference (fp32 raster); the fp64
+decode_step is bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import cfg_tuple
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402  (checker only)
+
+
+@pytest.fixture(scope="module")
+def mns():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1501_02894_b200 as m
+
+    return m
+
+
+def _psnr(a, b):
+    d = a.astype(np.float64) - b.astype(np.float64)
+    e = float(np.mean(d * d))
+    return math.inf if e == 0 else 10 * math.log10(255 * 255 / e)
+
+
+def _enc(mns, px, case):
+    e, mean_tol, is_mns = cfg_tuple(case["cfg"])
+    cfg = mns.EncoderConfig(e1=e[0], e2=e[1], e3=e[2], mean_tol=mean_tol, mode="mns" if is_mns else "no_search")
+    return mns.encode_quadtree(mns.GrayImage(px), cfg, root_level=case["root_level"])
+
+
+def test_encode_golden_bit_exact(mns, golden):
+    g = golden("encode")
+    for case in g.manifest:
+        code = _enc(mns, g[f"{case['key']}/img"], case)
+        ref = g[f"{case['key']}/records"]
+        assert np.array_equal(code.records, ref), (case, len(code.records), len(ref))
+
+
+def test_tie_fixtures_exercise_rounding_decided_picks(mns, golden):
+    g = golden("encode")
+    cases = [c for c in g.manifest if c["image"].startswith("ties")]
+    assert cases and sum(c["ties_bit1"] for c in cases) > 0
+    for case in cases:
+        code = _enc(mns, g[f"{case['key']}/img"], case)
+        assert np.array_equal(code.records, g[f"{case['key']}/records"]), case
+
+
+def test_decode_golden_within_1lsb(mns, golden):
+    g = golden("encode")
+    worst = 0
+    for case in g.manifest:
+        k = case["key"]
+        img = g[f"{k}/img"]
+        code = mns.QuadtreeCode.from_records(g[f"{k}/records"], case["padded_w"], case["padded_h"], img.shape[1],
+                                             img.shape[0], "mns", True)
+        for key, cfg in (("decode8", mns.DecodeConfig(max_iters=8, stop_delta=0.0)),
+                         ("decode_default", mns.DecodeConfig())):
+            got = mns.decode(code, cfg).pixels
+            want = g[f"{k}/{key}"]
+            diff = int(np.abs(got.astype(int) - want.astype(int)).max())
+            worst = max(worst, diff)
+            assert diff <= 1, (case, key, diff)
+            assert abs(_psnr(img, got) - _psnr(img, want)) <= 0.01 or _psnr(img, want) == math.inf, (case, key)
+    print("worst decode diff (LSB):", worst)
+
+
+def test_decode_step_fp64_bit_exact(mns, golden):
+    g = golden("decode_step")
+    for case in g.manifest:
+        k = case["key"]
+        img = g[f"{k}/img"]
+        code = mns.QuadtreeCode.from_records(g[f"{k}/records"], case["padded_w"], case["padded_h"], img.shape[1],
+                                             img.shape[0], "mns", True)
+        out = mns.decode_step(code, g[f"{k}/raster_in"])
+        assert np.array_equal(out, g[f"{k}/raster_out"])
+
+
+def test_decode_leaf_order_invariance(mns, golden):
+    g = golden("encode")
+    case = next(c for c in g.manifest if c["image"] == "natural_128" and c["cfg"]["e1"] == 5.0)
+    k = case["key"]
+    rec = g[f"{k}/records"]
+    img = g[f"{k}/img"]
+    perm = np.random.default_rng(13).permutation(len(rec))
+    a = mns.QuadtreeCode.from_records(rec, 128, 128, 128, 128, "mns", True)
+    b = mns.QuadtreeCode.from_records(rec[perm], 128, 128, 128, 128, "mns", True)
+    raster = np.random.default_rng(0).uniform(0, 255, (128, 128))
+    assert np.array_equal(mns.decode_step(a, raster), mns.decode_step(b, raster))
+    cfg = mns.DecodeConfig(max_iters=10, stop_delta=0.0)
+    assert mns.decode(a, cfg) == mns.decode(b, cfg)
+    del img
+
+
+def test_full_search_golden(mns, golden):
+    g = golden("search")
+    for case in g.manifest:
+        if not case["key"].startswith("full"):
+            continue
+        k = case["key"]
+        code, samples = mns.encode_full_search(mns.GrayImage(g[f"{k}/img"]), case["B"],
+                                               mns.EncoderConfig(mode="full_search", full_search_step=case["step"]))
+        dom = g[f"{k}/dom"]
+        c = code.columns
+        assert np.array_equal(c["dom_x"], dom[:, 0]) and np.array_equal(c["dom_y"], dom[:, 1]), case
+        assert np.array_equal(c["o"], g[f"{k}/o"]) and np.array_equal(c["code"], g[f"{k}/code"]), case
+        assert np.array_equal(np.array(samples, dtype=np.int32).reshape(-1, 2), g[f"{k}/samples"]), case
+        got = mns.decode(code, mns.DecodeConfig(max_iters=6, stop_delta=0.0)).pixels
+        assert int(np.abs(got.astype(int) - g[f"{k}/decode"].astype(int)).max()) <= 1, case
+
+
+def test_local_search_golden(mns, golden):
+    g = golden("search")
+    for case in g.manifest:
+        if not case["key"].startswith("local"):
+            continue
+        k = case["key"]
+        code = mns.encode_local_search(mns.GrayImage(g[f"{k}/img"]), mns.EncoderConfig(mode="local_search"))
+        dom = g[f"{k}/dom"]
+        c = code.columns
+        assert np.array_equal(c["dom_x"], dom[:, 0]) and np.array_equal(c["dom_y"], dom[:, 1]), case
+        assert np.array_equal(c["o"], g[f"{k}/o"]) and np.array_equal(c["code"], g[f"{k}/code"]), case
+
+
+def test_full_search_isometries_vs_oracle(mns):
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = np.ascontiguousarray(synth_image(512, 4)[100:196, 300:396])
+    for B in (4, 8):
+        code, _ = mns.encode_full_search(mns.GrayImage(px), B, mns.EncoderConfig(mode="full_search"), n_iso=8)
+        ref = O.full_search(px, B, 1, n_iso=8)
+        c = code.columns
+        assert np.array_equal(c["dom_x"], ref["dom_x"]) and np.array_equal(c["dom_y"], ref["dom_y"])
+        assert np.array_equal(c["iso"], ref["iso"]) and np.array_equal(c["code"], ref["code"])
+
+
+def test_local_search_radius32_vs_oracle(mns):
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = np.ascontiguousarray(synth_image(512, 4)[:256, :256])
+    code = mns.encode_local_search(mns.GrayImage(px), mns.EncoderConfig(mode="local_search"), radius=32)
+    ref = O.local_search(px, 32)
+    c = code.columns
+    assert np.array_equal(c["dom_x"], ref["dom_x"]) and np.array_equal(c["dom_y"], ref["dom_y"])
+    assert np.array_equal(c["code"], ref["code"]) and np.array_equal(c["o"], ref["o"])
+
+
+@pytest.mark.parametrize("name,root_level,e3", [("c1", 2, math.inf), ("c1", 1, 8.0), ("c2", 1, math.inf),
+                                                ("c2", 1, 8.0)])
+def test_config_images_vs_oracle(mns, name, root_level, e3):
+    from paper_1501_02894_b200.synth import config_image
+
+    px = config_image(name)
+    cfg = mns.EncoderConfig(e3=e3)
+    code = mns.encode_quadtree(mns.GrayImage(px), cfg, root_level=root_level)
+    ref, _ = O.encode_quadtree_records(px, (8.0, 8.0, e3), 16.0, True, root_level)
+    assert np.array_equal(code.records, ref)
+    iters = 8 if name == "c1" else 10
+    got = mns.decode(code, mns.DecodeConfig(max_iters=iters, stop_delta=0.0)).pixels
+    want, _, _ = O.decode_records(ref, px.shape[1], px.shape[0], max_iters=iters, stop_delta=0.0)
+    assert int(np.abs(got.astype(int) - want.astype(int)).max()) <= 1
+    assert abs(_psnr(px, got) - _psnr(px, want)) <= 0.01
+
+
+def test_batch_encode_matches_single(mns):
+    from paper_1501_02894_b200.synth import synth_image
+
+    imgs = np.stack([synth_image(512, s) for s in (1000, 1001, 1002)])
+    cfg = mns.EncoderConfig(e3=math.inf)
+    dev = torch.from_numpy(imgs).cuda()
+    code = mns.encode_device(dev, cfg, root_level=2)
+    n = code.n_records()
+    rec = code.records[:n].cpu().numpy().view(np.uint64)
+    offs = code.root_offsets.cpu().numpy()
+    per = 32 * 32
+    for i in range(3):
+        ref, _ = O.encode_quadtree_records(imgs[i], (8.0, 8.0, math.inf), 16.0, True, 2)
+        assert np.array_equal(rec[offs[i * per]: offs[(i + 1) * per]], ref)
+
+
+def test_strip_encode_matches_whole(mns):
+    """Row strips with a 16-px halo and global clamping reproduce the whole-image code."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(1024, 7, noise_sigma=10.0, n_blobs=24)
+    cfg = mns.EncoderConfig(e3=math.inf)
+    whole = mns.encode_device(torch.from_numpy(px).cuda(), cfg)
+    nw = whole.n_records()
+    wrec = whole.records[:nw].cpu().numpy()
+    parts = []
+    H = 1024
+    bounds = [0, 13, 30, 64]
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        y0, y1 = max(0, 16 * r0 - 16), min(H, 16 * r1 + 16)
+        sl = torch.from_numpy(np.ascontiguousarray(px[y0:y1])).cuda()
+        c = mns.encode_device(sl, cfg, root_rows=(r0, r1), height=H)
+        parts.append(c.records[: c.n_records()].cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), wrec)
+
+
+def test_write_stream_matches_reference_layout(mns, golden):
+    g = golden("encode")
+    from paper_1501_02894_b200 import bitstream
+
+    for case in g.manifest[::5]:
+        k = case["key"]
+        img = g[f"{k}/img"]
+        mode = case["cfg"]["mode"]
+        code = mns.QuadtreeCode.from_records(g[f"{k}/records"], case["padded_w"], case["padded_h"], img.shape[1],
+                                             img.shape[0], mode, True)
+        data = bitstream.write_stream(code)
+        assert data == bytes(g[f"{k}/stream"]), case
+        assert bitstream.stream_bit_count(code) == int(g[f"{k}/stream_bits"])
