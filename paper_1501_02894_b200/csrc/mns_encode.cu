@@ -451,7 +451,8 @@ __global__ void __launch_bounds__(ET) mns_encode_kernel(const EncParams p) {
                 }
             }
             const bool lane_ok = resL == 1 && resR == 1;
-            const bool pair_ok = lane_ok && __shfl_xor_sync(FULL, lane_ok, 1);
+            const int partner_ok = __shfl_xor_sync(FULL, (int)lane_ok, 1);  // every lane must shuffle
+            const bool pair_ok = lane_ok && partner_ok;
             int lbits = (bitL << (2 * c)) | (bitR << (2 * c + 1));
             lbits |= __shfl_xor_sync(FULL, lbits, 1);
             if (go && pair_ok) {
