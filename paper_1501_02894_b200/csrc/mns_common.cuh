@@ -101,6 +101,12 @@ __device__ inline void st_release_u64(unsigned long long *p, unsigned long long 
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ inline unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Decoupled look-back (single-pass exclusive scan over tiles in launch order).
 // status[] must be zeroed before the launch.  Called by ONE thread per tile;
 // returns the exclusive prefix of `agg` over tiles [0, tile).
@@ -128,6 +134,40 @@ __device__ inline long long lookback_exclusive(unsigned long long *status, long 
         --p;
     }
     st_release_u64(&status[tile], LB_PREFIX | (unsigned long long)(excl + agg));
+    return excl;
+}
+
+// Warp-cooperative decoupled look-back: called by ALL 32 lanes of one warp; the
+// 32 lanes poll 32 predecessors at once (relaxed loads: each status word is a
+// self-contained flag|value), sum aggregates up to the nearest inclusive prefix,
+// and slide the window back until one is found.  Returns the exclusive prefix
+// (same value in every lane).
+__device__ inline long long lookback_exclusive_warp(unsigned long long *status, long long tile, long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_release_u64(&status[0], LB_PREFIX | (unsigned long long)agg);
+        return 0;
+    }
+    if (lane == 0) st_release_u64(&status[tile], LB_AGG | (unsigned long long)agg);
+    long long excl = 0;
+    long long base = tile - 1;
+    while (true) {
+        const long long idx = base - lane;
+        unsigned long long v = idx >= 0 ? ld_relaxed_u64(&status[idx]) : LB_PREFIX;
+        while (__any_sync(0xffffffffu, (v & ~LB_MASK) == 0)) {
+            __nanosleep(20);
+            if ((v & ~LB_MASK) == 0) v = ld_relaxed_u64(&status[idx]);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, (v & ~LB_MASK) == LB_PREFIX);
+        const int first = pm ? __ffs(pm) - 1 : 32;  // nearest predecessor holding an inclusive prefix
+        long long c = lane <= first ? (long long)(v & LB_MASK) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        excl += c;
+        if (pm) break;
+        base -= 32;
+    }
+    if (lane == 0) st_release_u64(&status[tile], LB_PREFIX | (unsigned long long)(excl + agg));
     return excl;
 }
 

@@ -24,35 +24,44 @@
 #include <math.h>
 
 #include "mns_common.cuh"
+#include "mns_tma.cuh"
 
 namespace mns {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int TRX = 4, TRY = 4;                 // roots per CTA tile
-constexpr int DT = TRX * TRY * 32;              // 512 threads
-constexpr int DWIN_W = TRX * 16 + 32;           // 96
-constexpr int DWIN_H = TRY * 16 + 32;           // 96
+constexpr int BR = 4;                 // roots per column band (64 px)
+constexpr int DT = BR * 32;           // one warp per root of the band's current root row
+constexpr int WINW = BR * 16 + 32;    // 96-px window: band +- 16 px (every clamped domain lies inside)
+constexpr int QW = WINW / 2;          // 48 columns of the even 2x2-sum lattice
+constexpr int QS = QW + 4;            // padded row stride (rows 2 apart land 8 banks apart)
+constexpr int QR = 32;                // lattice ring rows (24 live + 8 being built)
+constexpr int BLK = 16;               // raster rows per TMA block
+constexpr int NBUF = 5;               // raw ring: 3 blocks readable by compute + 2 in flight
+constexpr int CR = 32;                // root rows walked by one CTA
+constexpr int RAW_BYTES = BLK * WINW * 4;
 
 __constant__ float kContrastSets[4][2] = {{0.f, 0.f}, {0.2f, 0.5f}, {0.4f, 0.65f}, {0.5f, 0.9f}};
 
+// Painted unit as seen by one Morton cell of a root.
 struct Cell {
-    float s, o;
-    short dx, dy;  // domain origin, window coordinates
-    int size;      // unit side (2..16)
+    float a;         // s / 4  (v = a*q + b, q = 2x2 domain sum)
+    float s, o;      // contrast, luminance target
+    int16_t drow;    // lattice: global q-row of the domain origin; direct: global raster row
+    uint8_t dcol;    // lattice: window q-column; direct: window pixel column
+    uint8_t lgd;     // log2(unit side) | 0x80 when the domain is off the even lattice (2x2 units)
 };
 
-struct DecParams {
+struct SweepParams {
     const uint64_t *records;
     const int32_t *root_offsets;  // local to the root rows [rr0, rr1)
-    int W, H, rw, rr0, rr1;
-    int y_lo, y_hi;               // resident raster rows (strip + halo), global coordinates
-    const float *cur;    // null on the first sweep: the flat start raster (initial_value) is implied
+    int W, H, rw, rr0, rr1, y_lo;
+    const float *cur;    // null on the first sweep: the flat start raster (init) is implied
     float init;
-    float *nxt;          // may be null on the final sweep
-    uint8_t *out_u8;     // non-null on the final sweep
-    int *state;          // [0] done flag, [1] iterations done, [2] finished-CTA counter, [3] max delta bits
-    int track_delta;     // stop_delta > 0
+    float *nxt;          // virtual-global base; null on a fused final sweep
+    uint8_t *out_u8;     // virtual-global base; non-null on the final sweep
+    int *state;          // [0] done, [1] sweeps done, [2] finished-CTA counter, [3] max |delta| bits
+    int track_delta;
     float stop_delta;
     int n_ctas;
 };
@@ -64,38 +73,92 @@ __device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates
     return m;
 }
 
-__global__ void __launch_bounds__(DT) decode_sweep_kernel(const DecParams p) {
-    extern __shared__ __align__(16) unsigned char dsm[];  // > 48 KB: dynamic shared memory
-    float(*win)[DWIN_W] = reinterpret_cast<float(*)[DWIN_W]>(dsm);
-    Cell(*cells)[64] = reinterpret_cast<Cell(*)[64]>(dsm + sizeof(float) * DWIN_H * DWIN_W);
+__device__ __forceinline__ Cell make_cell(int ux, int uy, int size, float s, float o, int W, int H, int wx0) {
+    Cell cl;
+    const int dx = clampi(ux - size / 2, 0, W - 2 * size), dy = clampi(uy - size / 2, 0, H - 2 * size);
+    const int wc = dx - wx0;  // wx0 is even
+    const bool lattice = ((wc | dy) & 1) == 0;
+    cl.a = 0.25f * s;
+    cl.s = s;
+    cl.o = o;
+    cl.drow = (int16_t)(lattice ? dy >> 1 : dy);
+    cl.dcol = (uint8_t)(lattice ? wc >> 1 : wc);
+    cl.lgd = (uint8_t)((31 - __clz(size)) | (lattice ? 0 : 0x80));
+    return cl;
+}
+
+// One Jacobi sweep (decoder.py:37-63) for a 64-px column band over CR root rows.
+// TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two
+// blocks ahead of the root row being painted; each block is reduced once into the
+// even 2x2-sum lattice ring, so no raster row is reloaded vertically and the
+// horizontal halo costs 1.5x only in L2->SM traffic.
+__global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const SweepParams p) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    float(*raw)[BLK][WINW] = reinterpret_cast<float(*)[BLK][WINW]>(dsm);
+    float(*qe)[QS] = reinterpret_cast<float(*)[QS]>(dsm + NBUF * RAW_BYTES);
+    Cell(*cells)[64] = reinterpret_cast<Cell(*)[64]>(dsm + NBUF * RAW_BYTES + QR * QS * 4);
+    __shared__ __align__(8) uint64_t bars[NBUF];
     __shared__ float cta_max;
 
     if (p.state[0]) return;  // converged in an earlier sweep (stop_delta > 0)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int trx = blockIdx.x, try_ = blockIdx.y;
-    const int x0 = trx * TRX * 16, y0 = (p.rr0 + try_ * TRY) * 16;
-    const int wx0 = x0 - 16, wy0 = y0 - 16;
-    const int W = p.W, H = p.H;
-    if (tid == 0) cta_max = 0.f;
-
-    // stage the window of the previous raster
-    constexpr int CH = DWIN_W / 4;
-    for (int c = tid; c < DWIN_H * CH; c += DT) {
-        const int wr = c / CH, wc = (c % CH) * 4;
-        const int gy = wy0 + wr, gx = wx0 + wc;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gy >= p.y_lo && gy < p.y_hi && gx >= 0 && gx < W)
-            v = p.cur ? __ldg(reinterpret_cast<const float4 *>(p.cur + (ptrdiff_t)gy * W + gx))
-                      : make_float4(p.init, p.init, p.init, p.init);
-        *reinterpret_cast<float4 *>(&win[wr][wc]) = v;
+    const int x0 = blockIdx.x * BR * 16, wx0 = x0 - 16;
+    const int r_s = p.rr0 + blockIdx.y * CR, r_e = min(r_s + CR, p.rr1);
+    const bool flat = p.cur == nullptr;
+    const int nblocks = (r_e - r_s) + 2;  // block k = raster rows [16(r_s-1+k), 16(r_s+k))
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; b++) mbar_init(&bars[b], 1);
+        fence_mbar_init();
+        cta_max = 0.f;
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        if (k < nblocks) {
+            const int b = k % NBUF;
+            mbar_arrive_expect_tx(&bars[b], RAW_BYTES);
+            tma_load_2d(raw[b], &tmap, wx0, 16 * (r_s - 1 + k) - p.y_lo, &bars[b]);
+        }
+    };
+    auto build = [&](int k) {  // lattice rows [8(r_s-1+k), 8(r_s+k)) from block k
+        const int b = k % NBUF;
+        mbar_wait(&bars[b], (k / NBUF) & 1);
+        const int g0 = 8 * (r_s - 1 + k);
+        for (int e = tid; e < 8 * (WINW / 4); e += DT) {
+            const int r = e / (WINW / 4), c4 = e % (WINW / 4);
+            const float4 u = *reinterpret_cast<const float4 *>(&raw[b][2 * r][4 * c4]);
+            const float4 w = *reinterpret_cast<const float4 *>(&raw[b][2 * r + 1][4 * c4]);
+            // numpy order of downsample_mean2 up to the 0.25 scale: ((a + b) + c) + d
+            *reinterpret_cast<float2 *>(&qe[(g0 + r) & (QR - 1)][2 * c4]) =
+                make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+        }
+    };
+    if (!flat) {
+        if (tid == 0) {
+            prefetch_tmap(&tmap);
+            for (int k = 0; k < 4; k++) issue(k);
+        }
+        build(0);
+        build(1);
     }
 
-    // per-root unit table (Morton cells)
-    const int rxi = trx * TRX + (warp % TRX), ryi = p.rr0 + try_ * TRY + (warp / TRX);
-    const bool live = rxi < p.rw && ryi < p.rr1;
-    const int rxg = rxi * 16, ryg = ryi * 16;
-    if (live) {
-        const int root = (ryi - p.rr0) * p.rw + rxi;
+    const int rxi = blockIdx.x * BR + warp;
+    const bool live_col = rxi < p.rw;
+    const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
+    const int lx = (a & 1) * 8 + (b & 1) * 4, ly = (a >> 1) * 8 + (b >> 1) * 4 + 2 * c;
+    float lmax = 0.f;
+    for (int j = 0; j < r_e - r_s; j++) {
+        if (!flat) build(j + 2);
+        __syncthreads();
+        if (!flat && tid == 0) {
+            fence_proxy_async();  // generic reads of block j-1 complete before the async refill
+            issue(j + 4);
+        }
+        if (!live_col) continue;
+        const int ry = r_s + j;
+        const int rxg = rxi * 16, ryg = ry * 16;
+        // ---- records -> 64 Morton cells of this root
+        const int root = (ry - p.rr0) * p.rw + rxi;
         const int beg = p.root_offsets[root], end = p.root_offsets[root + 1];
         for (int i = beg + lane; i < end; i += 32) {
             const uint64_t r = p.records[i];
@@ -104,60 +167,60 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const DecParams p) {
             const int size = 32 >> level;
             const int ob = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
             if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) {
-                Cell cl;
-                cl.s = -0.875f + 0.25f * (float)((r >> MNS_REC_PAYLOAD_SHIFT) & 7);
-                cl.o = (float)ob;
-                cl.size = size;
-                cl.dx = (short)(clampi(x - size / 2, 0, W - 2 * size) - wx0);
-                cl.dy = (short)(clampi(y - size / 2, 0, H - 2 * size) - wy0);
-                const int m0 = morton_of((x - rxg) >> 1, (y - ryg) >> 1), nc = (size / 2) * (size / 2);
+                const Cell cl = make_cell(x, y, size, -0.875f + 0.25f * (float)((r >> MNS_REC_PAYLOAD_SHIFT) & 7),
+                                          (float)ob, p.W, p.H, wx0);
+                const int m0 = morton_of((x - rxg) >> 1, (y - ryg) >> 1), nc = (size >> 1) * (size >> 1);
                 for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
             } else {
                 int d[3];
 #pragma unroll
-                for (int j = 0; j < 3; j++) {
-                    const int f = (int)((r >> (41 + 6 * j)) & 63);
-                    d[j] = f >= 32 ? f - 64 : f;
+                for (int q = 0; q < 3; q++) {
+                    const int f = (int)((r >> (41 + 6 * q)) & 63);
+                    d[q] = f >= 32 ? f - 64 : f;
                 }
                 const int bits = (int)((r >> 59) & 15);
-                const int t[4] = {ob + d[0], ob + d[1], ob + d[2], ob - (d[0] + d[1] + d[2])};
-                const int h = size / 2;
+                const int h = size >> 1;
                 for (int q = 0; q < 4; q++) {
                     const int qx = x + (q & 1) * h, qy = y + (q >> 1) * h;
-                    Cell cl;
-                    cl.s = kContrastSets[level][(bits >> q) & 1];
-                    cl.o = (float)t[q];
-                    cl.size = h;
-                    cl.dx = (short)(clampi(qx - h / 2, 0, W - 2 * h) - wx0);
-                    cl.dy = (short)(clampi(qy - h / 2, 0, H - 2 * h) - wy0);
-                    const int m0 = morton_of((qx - rxg) >> 1, (qy - ryg) >> 1), nc = (h / 2) * (h / 2);
+                    const int t = q < 3 ? ob + d[q] : ob - (d[0] + d[1] + d[2]);
+                    const Cell cl = make_cell(qx, qy, h, kContrastSets[level][(bits >> q) & 1], (float)t, p.W, p.H,
+                                              wx0);
+                    const int m0 = morton_of((qx - rxg) >> 1, (qy - ryg) >> 1), nc = (h >> 1) * (h >> 1);
                     for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
                 }
             }
         }
-    }
-    __syncthreads();
-
-    float lmax = 0.f;
-    if (live) {
-        const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
-        const int lx = (a & 1) * 8 + (b & 1) * 4, ly = (a >> 1) * 8 + (b >> 1) * 4 + 2 * c;
+        __syncwarp();
         const Cell cA = cells[warp][2 * lane], cB = cells[warp][2 * lane + 1];
-        // q for the lane's 8 pixels (unit origin = cell's unit origin; pixel offset inside the unit)
+        __syncwarp();  // cells are rewritten at the next root row
         float q[8];
 #pragma unroll
         for (int side = 0; side < 2; side++) {
             const Cell &cl = side ? cB : cA;
-            // unit origin (root-relative) from its size: units are aligned to their size
-            const int px0 = lx + 2 * side, py0 = ly;
-            const int ux = px0 & ~(cl.size - 1), uy = py0 & ~(cl.size - 1);
+            const int lg = cl.lgd & 0x7F;
+            const int msk = (1 << lg) - 1;
+            const int ox = (lx + 2 * side) & msk, oy = ly & msk;  // pixel offset inside its unit
+            if (flat) {
 #pragma unroll
-            for (int i = 0; i < 2; i++)
+                for (int k = 0; k < 4; k++) q[(k >> 1) * 4 + 2 * side + (k & 1)] = 4.f * p.init;
+            } else if (!(cl.lgd & 0x80)) {
 #pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    const int yy = cl.dy + 2 * (py0 + i - uy), xx = cl.dx + 2 * (px0 + j - ux);
-                    q[4 * i + 2 * side + j] = ((win[yy][xx] + win[yy][xx + 1]) + win[yy + 1][xx]) + win[yy + 1][xx + 1];
-                }
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int jj = 0; jj < 2; jj++)
+                        q[4 * i + 2 * side + jj] = qe[(cl.drow + oy + i) & (QR - 1)][cl.dcol + ox + jj];
+            } else {  // 2x2 unit with an odd / mixed-phase domain: sum the raster pixels directly
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int jj = 0; jj < 2; jj++) {
+                        const int R = cl.drow + 2 * (oy + i), C = cl.dcol + 2 * (ox + jj);
+                        const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
+                        const float *r0 = raw[k0 % NBUF][R % BLK];
+                        const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
+                        q[4 * i + 2 * side + jj] = ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
+                    }
+            }
         }
         const float sA = q[0] + q[1] + q[4] + q[5], sB = q[2] + q[3] + q[6] + q[7];
         float s2 = sA + sB;
@@ -166,41 +229,42 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const DecParams p) {
         s8 += __shfl_xor_sync(FULL, s8, 4);   // 8x8 unit (8 lanes)
         float s32 = s8 + __shfl_xor_sync(FULL, s8, 8);
         s32 += __shfl_xor_sync(FULL, s32, 16);  // 16x16 unit (warp)
-        auto unit_sum = [&](int size, float own) {
-            return size == 2 ? own : (size == 4 ? s2 : (size == 8 ? s8 : s32));
+        auto unit_b = [&](const Cell &cl, float own) {
+            const int lg = cl.lgd & 0x7F;
+            const float sum = lg == 1 ? own : (lg == 2 ? s2 : (lg == 3 ? s8 : s32));
+            const float mean = sum * __int_as_float((127 - 2 - 2 * lg) << 23);  // sum * 0.25 / side^2
+            return fmaf(-cl.s, mean, cl.o);
         };
-        const float mA = unit_sum(cA.size, sA) * 0.25f / (float)(cA.size * cA.size);
-        const float mB = unit_sum(cB.size, sB) * 0.25f / (float)(cB.size * cB.size);
+        const float bA = unit_b(cA, sA), bB = unit_b(cB, sB);
         float v[8];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             const bool right = (k & 3) >= 2;
-            const Cell &cl = right ? cB : cA;
-            const float m = right ? mB : mA;
-            float t = fmaf(cl.s, q[k] * 0.25f - m, cl.o);
-            v[k] = fminf(255.f, fmaxf(0.f, t));
+            v[k] = fminf(255.f, fmaxf(0.f, fmaf(right ? cB.a : cA.a, q[k], right ? bB : bA)));
         }
         const int gx = rxg + lx, gy = ryg + ly;
         if (p.track_delta) {
 #pragma unroll
-            for (int i = 0; i < 2; i++)
+            for (int i = 0; i < 2; i++) {
+                const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
 #pragma unroll
-                for (int j = 0; j < 4; j++)
-                    lmax = fmaxf(lmax, fabsf(v[4 * i + j] - win[gy + i - wy0][gx + j - wx0]));
+                for (int jj = 0; jj < 4; jj++)
+                    lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + warp * 16 + lx + jj])));
+            }
         }
         if (p.nxt) {
-            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * W + gx) = make_float4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * W + gx) = make_float4(v[4], v[5], v[6], v[7]);
+            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * p.W + gx) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * p.W + gx) = make_float4(v[4], v[5], v[6], v[7]);
         }
         if (p.out_u8) {
             uint32_t w0 = 0, w1 = 0;
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                w0 |= (uint32_t)floorf(v[j] + 0.5f) << (8 * j);
-                w1 |= (uint32_t)floorf(v[4 + j] + 0.5f) << (8 * j);
+            for (int jj = 0; jj < 4; jj++) {
+                w0 |= (uint32_t)floorf(v[jj] + 0.5f) << (8 * jj);
+                w1 |= (uint32_t)floorf(v[4 + jj] + 0.5f) << (8 * jj);
             }
-            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * W + gx) = w0;
-            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * W + gx) = w1;
+            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * p.W + gx) = w0;
+            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * p.W + gx) = w1;
         }
     }
     if (p.track_delta) {
@@ -350,7 +414,7 @@ int decode_workspace_bytes(int, int, int64_t *bytes) {
     return 0;
 }
 
-static int sweep_smem() { return sizeof(float) * DWIN_H * DWIN_W + sizeof(Cell) * TRX * TRY * 64; }
+static int sweep_smem() { return NBUF * RAW_BYTES + QR * QS * 4 + (int)sizeof(Cell) * BR * 64; }
 
 static int ensure_sweep_attr() {
     static bool attr_set = false;
@@ -368,9 +432,11 @@ int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, in
                  const float *cur, float init, float *nxt, uint8_t *out, int *state, double stop_delta,
                  cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(W >= 32 || H >= 0, "bad width");
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
+    MNS_CHECK_ARG(H <= 32767 * 2, "height exceeds the lattice row range");
     if (ensure_sweep_attr()) return -1;
-    DecParams p{};
+    SweepParams p{};
     p.records = records;
     p.root_offsets = root_offsets;
     p.W = W;
@@ -379,7 +445,7 @@ int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, in
     p.rr0 = rr0;
     p.rr1 = rr1;
     p.y_lo = rr0 * 16 - 16 > 0 ? rr0 * 16 - 16 : 0;
-    p.y_hi = rr1 * 16 + 16 < H ? rr1 * 16 + 16 : H;
+    const int y_hi = rr1 * 16 + 16 < H ? rr1 * 16 + 16 : H;
     p.cur = cur;
     p.init = init;
     p.nxt = nxt;
@@ -387,9 +453,15 @@ int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, in
     p.state = state;
     p.track_delta = stop_delta > 0.0;
     p.stop_delta = (float)stop_delta;
-    dim3 grid((p.rw + TRX - 1) / TRX, (rr1 - rr0 + TRY - 1) / TRY);
+    CUtensorMap tmap{};
+    if (cur) {
+        if (encode_tmap_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cur + (ptrdiff_t)p.y_lo * W, (uint64_t)W,
+                           (uint64_t)(y_hi - p.y_lo), (uint64_t)W * 4, WINW, BLK))
+            return -1;
+    }
+    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + CR - 1) / CR);
     p.n_ctas = grid.x * grid.y;
-    decode_sweep_kernel<<<grid, DT, sweep_smem(), stream>>>(p);
+    decode_sweep_kernel<<<grid, DT, sweep_smem(), stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -150,7 +150,7 @@ __device__ __forceinline__ Node2 p2_node(int nlog2, int sr, int s0, int s1, int 
     return z;
 }
 
-__global__ void __launch_bounds__(ET) mns_encode_kernel(const EncParams p) {
+__global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     __shared__ __align__(16) uint8_t pix[WIN_H][WIN_W];
     __shared__ __align__(16) uint16_t qe[QE_H][QE_W];
     __shared__ double scratch[EW][2][64];
@@ -485,21 +485,22 @@ __global__ void __launch_bounds__(ET) mns_encode_kernel(const EncParams p) {
     const int offB = offA + (hasA ? 1 : 0);
     if (lane == 0) warp_cnt[warp] = __popc(bA) + __popc(bB);
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
         long long agg = 0;
-        for (int w = 0; w < EW; w++) {
-            warp_base[w] = agg;
-            agg += warp_cnt[w];
-        }
-        const long long base = lookback_exclusive(p.status, tile, agg);
-        const long long root0 = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0;
-        for (int w = 0; w < nr; w++) {
-            warp_base[w] += base;
-            p.root_offsets[root0 + w] = (int32_t)warp_base[w];
-        }
-        if (tile == p.n_tiles - 1) {
-            p.root_offsets[p.n_roots] = (int32_t)(base + agg);
-            *p.count = base + agg;
+        for (int w = 0; w < EW; w++) agg += warp_cnt[w];
+        const long long base = lookback_exclusive_warp(p.status, tile, agg);
+        if (lane == 0) {
+            const long long root0 = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0;
+            long long run = base;
+            for (int w = 0; w < EW; w++) {
+                warp_base[w] = run;
+                if (w < nr) p.root_offsets[root0 + w] = (int32_t)run;
+                run += warp_cnt[w];
+            }
+            if (tile == p.n_tiles - 1) {
+                p.root_offsets[p.n_roots] = (int32_t)run;
+                *p.count = run;
+            }
         }
     }
     __syncthreads();
