@@ -156,7 +156,8 @@ def run_ours(args, img_np, rank, world, local_rank):
     n_roots = (r1 - r0) * (W // 16)
     code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
                           torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
-                          torch.zeros(1, dtype=torch.int64, device=dev), W, H, 1, r0, r1)
+                          torch.zeros(1, dtype=torch.int64, device=dev), W, H, 1, r0, r1,
+                          unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device=dev))
     dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world)
     out_host = torch.empty((16 * (r1 - r0), W), dtype=torch.uint8).pin_memory()
     stream = torch.cuda.current_stream()

@@ -54,13 +54,20 @@ typedef struct {
  * order, then TL,TR,BL,BR pre-order), root_offsets[i] = index of the first
  * record of root i (roots of the processed rows, image-major, raster order;
  * n_roots + 1 entries, the last = total), *d_count = total records (device).
- * capacity must be >= 64 * n_roots.  Workspace: mns_encode_workspace_bytes. */
+ * capacity must be >= 64 * n_roots.  unit_map (optional, 32 words per root)
+ * receives the decoder's unit map.  Workspace: mns_encode_workspace_bytes. */
 int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t root_row_begin, int32_t root_row_end,
                                int64_t *bytes);
 int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
                         int32_t n_images, int32_t root_row_begin, int32_t root_row_end, const mns_enc_cfg *cfg,
                         uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
-                        void *workspace, int64_t workspace_bytes, void *stream);
+                        uint32_t *unit_map, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Decoder unit map (mns_record.h) of a record array grouped by root: 32 uint32
+ * words (64 cells) per root of the root rows [root_row_begin, root_row_end).
+ * mns_encode_quadtree emits the same map directly when unit_map != NULL. */
+int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,
+                       int32_t root_row_end, uint32_t *unit_map, void *stream);
 
 /* Replaces: decoder.decode / decode_step (decoder.py:37-77) for quadtree codes.
  * One Jacobi sweep per iteration over an fp32 raster (ping/pong, width*height
@@ -80,14 +87,14 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
 /* One Jacobi sweep over the root rows [root_row_begin, root_row_end) (strip
  * sharding: the multi-GPU decoder exchanges 16-row halos between sweeps).
  * cur / nxt / out are bases of the FULL image (row 0) even when only rows
- * [16*root_row_begin - 16, 16*root_row_end + 16) are resident; root_offsets are
+ * [16*root_row_begin - 16, 16*root_row_end + 16) are resident; the unit map is
  * local to the strip's roots.  cur may be NULL on the first sweep: the flat
  * start raster of initial_value is implied (no fill pass).  nxt may be NULL when
  * out (uint8, rounded) is given: the fused final sweep.  state: 4 int32 zeroed
  * before the first sweep (early-stop bookkeeping when stop_delta > 0). */
-int mns_decode_sweep(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
-                     int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value,
-                     float *nxt, uint8_t *out, int32_t *state, double stop_delta, void *stream);
+int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, int32_t root_row_begin,
+                     int32_t root_row_end, const float *cur, float initial_value, float *nxt, uint8_t *out,
+                     int32_t *state, double stop_delta, void *stream);
 
 /* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
  * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-

@@ -46,4 +46,37 @@ MNS_REC_INLINE uint64_t mns_rec_phase2(int x, int y, int level, int o_byte, int 
            ((uint64_t)(s_bits & 15) << 59);
 }
 
+/* Unit map (decoder input): one uint16 per 2x2 cell of every 16x16 root, 64 per
+ * root in Morton (= DFS) order, roots in raster order.  A cell names the painted
+ * unit covering it (decoder.py:48-62: a phase-1 leaf, or one quadrant of a
+ * phase-2 leaf):
+ *   bits  0..3   contrast index: 0..7 phase-1 code k (s = -0.875 + 0.25k);
+ *                8 + 2*(level-1) + bit for a phase-2 quadrant (CONTRAST_SETS)
+ *   bits  4..13  luminance target + 32 (phase-2 targets span -31..286)
+ *   bits 14..15  log2(unit side) - 1 (side 2, 4, 8, 16)
+ * The unit's origin is the cell position rounded down to the side; its domain is
+ * the co-centred one (image.py:174-187). */
+MNS_REC_INLINE uint16_t mns_unit_desc(int s_index, int target, int side_log2) {
+    return (uint16_t)((s_index & 15) | ((target + 32) << 4) | ((side_log2 - 1) << 14));
+}
+
+/* Descriptor of the unit covering root-relative pixel (px, py) (even) of leaf record r. */
+MNS_REC_INLINE uint16_t mns_unit_of_record(uint64_t r, int rx, int ry, int px, int py) {
+    const int x = (int)((r >> MNS_REC_X_SHIFT) & 0x7FFF) * 2 - rx, y = (int)((r >> MNS_REC_Y_SHIFT) & 0x7FFF) * 2 - ry;
+    const int level = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1;
+    const int lg = 5 - level; /* side = 32 >> level */
+    const int o = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
+    if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) return mns_unit_desc((int)((r >> MNS_REC_PAYLOAD_SHIFT) & 7), o, lg);
+    const int h = 1 << (lg - 1);
+    const int q = ((py - y) >= h ? 2 : 0) + ((px - x) >= h ? 1 : 0);
+    int d[3];
+    for (int j = 0; j < 3; j++) {
+        const int f = (int)((r >> (41 + 6 * j)) & 63);
+        d[j] = f >= 32 ? f - 64 : f;
+    }
+    const int t = q < 3 ? o + d[q] : o - (d[0] + d[1] + d[2]);
+    const int bit = (int)((r >> (59 + q)) & 1);
+    return mns_unit_desc(8 + 2 * (level - 1) + bit, t, lg - 1);
+}
+
 #endif

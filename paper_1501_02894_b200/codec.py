@@ -105,6 +105,7 @@ class DeviceCode:
     root_row_end: int = 0
     mode: str = "mns"
     technique2: bool = True
+    unit_map: "object" = None  # torch.int32 [n_roots * 32]: decoder unit map (mns_record.h), optional
 
     def n_records(self) -> int:
         return int(self.count.item())
@@ -139,7 +140,8 @@ def enc_cfg(config: EncoderConfig, root_level: int = 1) -> N.EncCfg:
 
 
 def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows: Optional[tuple] = None,
-                  height: Optional[int] = None, out: Optional[DeviceCode] = None, stream=None) -> DeviceCode:
+                  height: Optional[int] = None, out: Optional[DeviceCode] = None, with_unit_map: bool = True,
+                  stream=None) -> DeviceCode:
     """MNS quadtree encode of a padded uint8 CUDA tensor [H, W] or a batch [B, H, W].
 
     root_rows=(r0, r1) restricts the work to root rows [r0, r1) (strip sharding); then ``img``
@@ -160,7 +162,8 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
         out = DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
                          torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
                          torch.zeros(1, dtype=torch.int64, device=dev), w, H, nb, r0, r1, config.mode,
-                         config.technique2)
+                         config.technique2,
+                         torch.empty(32 * n_roots, dtype=torch.int32, device=dev) if with_unit_map else None)
     wsb = N.out_i64(L, L.mns_encode_workspace_bytes, w, nb, r0, r1)
     ws = _WS.get("enc", wsb, dev)
     # `img` points at global row 0 even for halo'd strips: offset the base pointer back
@@ -170,8 +173,20 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     cfg = enc_cfg(config, root_level)
     N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
                                   ctypes.byref(cfg), N.ptr(out.records), out.records.numel(), N.ptr(out.root_offsets),
-                                  N.ptr(out.count), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+                                  N.ptr(out.count), N.ptr(out.unit_map), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
     return out
+
+
+def build_unit_map(code: DeviceCode, stream=None):
+    """Decoder unit map of a device code whose encoder did not emit one."""
+    torch = _torch()
+    L = N.lib()
+    r0, r1 = code.root_row_begin, code.root_row_end or code.padded_h // 16
+    n_roots = (code.padded_w // 16) * (r1 - r0)
+    code.unit_map = torch.empty(32 * n_roots, dtype=torch.int32, device=code.records.device)
+    N.check(L.mns_build_unit_map(N.ptr(code.records), N.ptr(code.root_offsets), code.padded_w, r0, r1,
+                                 N.ptr(code.unit_map), N.stream_ptr(stream)))
+    return code.unit_map
 
 
 def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, initial_value: float = 128.0,

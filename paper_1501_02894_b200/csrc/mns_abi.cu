@@ -61,14 +61,16 @@ int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int elem_bytes, 
 int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes);
 int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t image_stride, int n_images, int rr0,
                     int rr1, const mns_enc_cfg *cfg, uint64_t *records, int64_t capacity, int32_t *root_offsets,
-                    int64_t *d_count, void *workspace, int64_t workspace_bytes, cudaStream_t stream);
+                    int64_t *d_count, uint32_t *unit_map, void *workspace, int64_t workspace_bytes,
+                    cudaStream_t stream);
+int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1, uint32_t *unit_map,
+                   cudaStream_t stream);
 int decode_workspace_bytes(int W, int H, int64_t *bytes);
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
-int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, int H, int rr0, int rr1,
-                 const float *cur, float init, float *nxt, uint8_t *out, int *state, double stop_delta,
-                 cudaStream_t stream);
+int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const float *cur, float init,
+                 float *nxt, uint8_t *out, int *state, double stop_delta, cudaStream_t stream);
 int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
                  const int32_t *udy, const float *us, const float *uo, int64_t n, int W, int H, int iters,
                  double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
@@ -106,10 +108,16 @@ int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t rr0, int
 
 int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
                         int32_t n_images, int32_t rr0, int32_t rr1, const mns_enc_cfg *cfg, uint64_t *records,
-                        int64_t capacity, int32_t *root_offsets, int64_t *d_count, void *workspace,
-                        int64_t workspace_bytes, void *stream) {
+                        int64_t capacity, int32_t *root_offsets, int64_t *d_count, uint32_t *unit_map,
+                        void *workspace, int64_t workspace_bytes, void *stream) {
     GUARD(mns::encode_quadtree(img, width, height, pitch, image_stride, n_images, rr0, rr1, cfg, records, capacity,
-                               root_offsets, d_count, workspace, workspace_bytes, (cudaStream_t)stream));
+                               root_offsets, d_count, unit_map, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,
+                       int32_t root_row_end, uint32_t *unit_map, void *stream) {
+    GUARD(mns::build_unit_map(records, root_offsets, width, root_row_begin, root_row_end, unit_map,
+                              (cudaStream_t)stream));
 }
 
 int mns_decode_workspace_bytes(int32_t width, int32_t height, int64_t *bytes) {
@@ -124,11 +132,11 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
                                out, d_iters_done, workspace, workspace_bytes, (cudaStream_t)stream));
 }
 
-int mns_decode_sweep(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
-                     int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value,
-                     float *nxt, uint8_t *out, int32_t *state, double stop_delta, void *stream) {
-    GUARD(mns::decode_sweep(records, root_offsets, width, height, root_row_begin, root_row_end, cur, initial_value,
-                            nxt, out, state, stop_delta, (cudaStream_t)stream));
+int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, int32_t root_row_begin,
+                     int32_t root_row_end, const float *cur, float initial_value, float *nxt, uint8_t *out,
+                     int32_t *state, double stop_delta, void *stream) {
+    GUARD(mns::decode_sweep(unit_map, width, height, root_row_begin, root_row_end, cur, initial_value, nxt, out,
+                            state, stop_delta, (cudaStream_t)stream));
 }
 
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

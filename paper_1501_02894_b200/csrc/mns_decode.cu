@@ -41,20 +41,12 @@ constexpr int NBUF = 5;               // raw ring: 3 blocks readable by compute 
 constexpr int CR = 32;                // root rows walked by one CTA
 constexpr int RAW_BYTES = BLK * WINW * 4;
 
-__constant__ float kContrastSets[4][2] = {{0.f, 0.f}, {0.2f, 0.5f}, {0.4f, 0.65f}, {0.5f, 0.9f}};
-
-// Painted unit as seen by one Morton cell of a root.
-struct Cell {
-    float a;         // s / 4  (v = a*q + b, q = 2x2 domain sum)
-    float s, o;      // contrast, luminance target
-    int16_t drow;    // lattice: global q-row of the domain origin; direct: global raster row
-    uint8_t dcol;    // lattice: window q-column; direct: window pixel column
-    uint8_t lgd;     // log2(unit side) | 0x80 when the domain is off the even lattice (2x2 units)
-};
+// contrast of a unit-map index (mns_record.h): 0..7 phase-1 codes, 8..13 phase-2 sets
+__constant__ float kUnitS[16] = {-0.875f, -0.625f, -0.375f, -0.125f, 0.125f, 0.375f, 0.625f, 0.875f,
+                                 0.2f,    0.5f,    0.4f,    0.65f,   0.5f,   0.9f,   0.f,    0.f};
 
 struct SweepParams {
-    const uint64_t *records;
-    const int32_t *root_offsets;  // local to the root rows [rr0, rr1)
+    const uint32_t *unit_map;  // 32 words (64 cells) per root of the rows [rr0, rr1)
     int W, H, rw, rr0, rr1, y_lo;
     const float *cur;    // null on the first sweep: the flat start raster (init) is implied
     float init;
@@ -73,33 +65,47 @@ __device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates
     return m;
 }
 
-__device__ __forceinline__ Cell make_cell(int ux, int uy, int size, float s, float o, int W, int H, int wx0) {
-    Cell cl;
-    const int dx = clampi(ux - size / 2, 0, W - 2 * size), dy = clampi(uy - size / 2, 0, H - 2 * size);
+struct Unit {
+    float a, b;      // v = a*q + b once the domain mean is known (b = o - s*mean)
+    float s, o;
+    int drow, dcol;  // lattice (global q-row, window q-col) or direct (global row, window col)
+    int lg, ox, oy;  // log2(side), pixel offset of the lane's cell inside the unit
+    bool lattice;
+};
+
+__device__ __forceinline__ Unit unit_of(uint32_t d, const float *st, int px, int py, int rxg, int ryg, int W, int H,
+                                        int wx0) {
+    Unit u;
+    u.s = st[d & 15];
+    u.o = (float)((int)((d >> 4) & 1023) - 32);
+    u.lg = (int)(d >> 14) + 1;
+    const int side = 1 << u.lg;
+    const int ux = px & ~(side - 1), uy = py & ~(side - 1);
+    u.ox = px - ux;
+    u.oy = py - uy;
+    const int dx = clampi(rxg + ux - side / 2, 0, W - 2 * side), dy = clampi(ryg + uy - side / 2, 0, H - 2 * side);
     const int wc = dx - wx0;  // wx0 is even
-    const bool lattice = ((wc | dy) & 1) == 0;
-    cl.a = 0.25f * s;
-    cl.s = s;
-    cl.o = o;
-    cl.drow = (int16_t)(lattice ? dy >> 1 : dy);
-    cl.dcol = (uint8_t)(lattice ? wc >> 1 : wc);
-    cl.lgd = (uint8_t)((31 - __clz(size)) | (lattice ? 0 : 0x80));
-    return cl;
+    u.lattice = ((wc | dy) & 1) == 0;
+    u.drow = u.lattice ? dy >> 1 : dy;
+    u.dcol = u.lattice ? wc >> 1 : wc;
+    u.a = 0.25f * u.s;
+    return u;
 }
 
 // One Jacobi sweep (decoder.py:37-63) for a 64-px column band over CR root rows.
 // TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two
 // blocks ahead of the root row being painted; each block is reduced once into the
 // even 2x2-sum lattice ring, so no raster row is reloaded vertically and the
-// horizontal halo costs 1.5x only in L2->SM traffic.
+// horizontal halo costs 1.5x only in L2->SM traffic.  The unit map words of the
+// next root row are prefetched into registers one step ahead.
 __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
     float(*raw)[BLK][WINW] = reinterpret_cast<float(*)[BLK][WINW]>(dsm);
     float(*qe)[QS] = reinterpret_cast<float(*)[QS]>(dsm + NBUF * RAW_BYTES);
-    Cell(*cells)[64] = reinterpret_cast<Cell(*)[64]>(dsm + NBUF * RAW_BYTES + QR * QS * 4);
     __shared__ __align__(8) uint64_t bars[NBUF];
     __shared__ float cta_max;
+    __shared__ float st[16];
 
     if (p.state[0]) return;  // converged in an earlier sweep (stop_delta > 0)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -107,6 +113,7 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
     const int r_s = p.rr0 + blockIdx.y * CR, r_e = min(r_s + CR, p.rr1);
     const bool flat = p.cur == nullptr;
     const int nblocks = (r_e - r_s) + 2;  // block k = raster rows [16(r_s-1+k), 16(r_s+k))
+    if (tid < 16) st[tid] = kUnitS[tid];
     if (tid == 0) {
         for (int b = 0; b < NBUF; b++) mbar_init(&bars[b], 1);
         fence_mbar_init();
@@ -146,126 +153,95 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
     const bool live_col = rxi < p.rw;
     const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
     const int lx = (a & 1) * 8 + (b & 1) * 4, ly = (a >> 1) * 8 + (b >> 1) * 4 + 2 * c;
+    const uint32_t *umap = p.unit_map + (size_t)((r_s - p.rr0) * p.rw + rxi) * 32 + lane;
+    uint32_t word = live_col ? __ldg(umap) : 0u;
     float lmax = 0.f;
     for (int j = 0; j < r_e - r_s; j++) {
+        const uint32_t wnext = (live_col && j + 1 < r_e - r_s) ? __ldg(umap + (size_t)(j + 1) * p.rw * 32) : 0u;
         if (!flat) build(j + 2);
         __syncthreads();
         if (!flat && tid == 0) {
             fence_proxy_async();  // generic reads of block j-1 complete before the async refill
             issue(j + 4);
         }
-        if (!live_col) continue;
-        const int ry = r_s + j;
-        const int rxg = rxi * 16, ryg = ry * 16;
-        // ---- records -> 64 Morton cells of this root
-        const int root = (ry - p.rr0) * p.rw + rxi;
-        const int beg = p.root_offsets[root], end = p.root_offsets[root + 1];
-        for (int i = beg + lane; i < end; i += 32) {
-            const uint64_t r = p.records[i];
-            const int x = (int)((r >> MNS_REC_X_SHIFT) & 0x7FFF) * 2, y = (int)((r >> MNS_REC_Y_SHIFT) & 0x7FFF) * 2;
-            const int level = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1;
-            const int size = 32 >> level;
-            const int ob = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
-            if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) {
-                const Cell cl = make_cell(x, y, size, -0.875f + 0.25f * (float)((r >> MNS_REC_PAYLOAD_SHIFT) & 7),
-                                          (float)ob, p.W, p.H, wx0);
-                const int m0 = morton_of((x - rxg) >> 1, (y - ryg) >> 1), nc = (size >> 1) * (size >> 1);
-                for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
-            } else {
-                int d[3];
+        if (live_col) {
+            const int ry = r_s + j;
+            const int rxg = rxi * 16, ryg = ry * 16;
+            Unit uA = unit_of(word & 0xFFFFu, st, lx, ly, rxg, ryg, p.W, p.H, wx0);
+            Unit uB = unit_of(word >> 16, st, lx + 2, ly, rxg, ryg, p.W, p.H, wx0);
+            float q[8];
 #pragma unroll
-                for (int q = 0; q < 3; q++) {
-                    const int f = (int)((r >> (41 + 6 * q)) & 63);
-                    d[q] = f >= 32 ? f - 64 : f;
-                }
-                const int bits = (int)((r >> 59) & 15);
-                const int h = size >> 1;
-                for (int q = 0; q < 4; q++) {
-                    const int qx = x + (q & 1) * h, qy = y + (q >> 1) * h;
-                    const int t = q < 3 ? ob + d[q] : ob - (d[0] + d[1] + d[2]);
-                    const Cell cl = make_cell(qx, qy, h, kContrastSets[level][(bits >> q) & 1], (float)t, p.W, p.H,
-                                              wx0);
-                    const int m0 = morton_of((qx - rxg) >> 1, (qy - ryg) >> 1), nc = (h >> 1) * (h >> 1);
-                    for (int k = 0; k < nc; k++) cells[warp][m0 + k] = cl;
+            for (int side = 0; side < 2; side++) {
+                const Unit &u = side ? uB : uA;
+                if (flat) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) q[(k >> 1) * 4 + 2 * side + (k & 1)] = 4.f * p.init;
+                } else if (u.lattice) {
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+#pragma unroll
+                        for (int jj = 0; jj < 2; jj++)
+                            q[4 * i + 2 * side + jj] = qe[(u.drow + u.oy + i) & (QR - 1)][u.dcol + u.ox + jj];
+                } else {  // 2x2 unit with an odd / mixed-phase domain: sum the raster pixels directly
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+#pragma unroll
+                        for (int jj = 0; jj < 2; jj++) {
+                            const int R = u.drow + 2 * (u.oy + i), C = u.dcol + 2 * (u.ox + jj);
+                            const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
+                            const float *r0 = raw[k0 % NBUF][R % BLK];
+                            const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
+                            q[4 * i + 2 * side + jj] = ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
+                        }
                 }
             }
-        }
-        __syncwarp();
-        const Cell cA = cells[warp][2 * lane], cB = cells[warp][2 * lane + 1];
-        __syncwarp();  // cells are rewritten at the next root row
-        float q[8];
+            const float sA = q[0] + q[1] + q[4] + q[5], sB = q[2] + q[3] + q[6] + q[7];
+            float s2 = sA + sB;
+            s2 += __shfl_xor_sync(FULL, s2, 1);   // 4x4 unit (lane pair)
+            float s8 = s2 + __shfl_xor_sync(FULL, s2, 2);
+            s8 += __shfl_xor_sync(FULL, s8, 4);   // 8x8 unit (8 lanes)
+            float s32 = s8 + __shfl_xor_sync(FULL, s8, 8);
+            s32 += __shfl_xor_sync(FULL, s32, 16);  // 16x16 unit (warp)
+            auto unit_b = [&](const Unit &u, float own) {
+                const float sum = u.lg == 1 ? own : (u.lg == 2 ? s2 : (u.lg == 3 ? s8 : s32));
+                const float mean = sum * __int_as_float((127 - 2 - 2 * u.lg) << 23);  // sum * 0.25 / side^2
+                return fmaf(-u.s, mean, u.o);
+            };
+            uA.b = unit_b(uA, sA);
+            uB.b = unit_b(uB, sB);
+            float v[8];
 #pragma unroll
-        for (int side = 0; side < 2; side++) {
-            const Cell &cl = side ? cB : cA;
-            const int lg = cl.lgd & 0x7F;
-            const int msk = (1 << lg) - 1;
-            const int ox = (lx + 2 * side) & msk, oy = ly & msk;  // pixel offset inside its unit
-            if (flat) {
+            for (int k = 0; k < 8; k++) {
+                const bool right = (k & 3) >= 2;
+                v[k] = fminf(255.f, fmaxf(0.f, fmaf(right ? uB.a : uA.a, q[k], right ? uB.b : uA.b)));
+            }
+            const int gx = rxg + lx, gy = ryg + ly;
+            if (p.track_delta) {
 #pragma unroll
-                for (int k = 0; k < 4; k++) q[(k >> 1) * 4 + 2 * side + (k & 1)] = 4.f * p.init;
-            } else if (!(cl.lgd & 0x80)) {
+                for (int i = 0; i < 2; i++) {
+                    const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
 #pragma unroll
-                for (int i = 0; i < 2; i++)
+                    for (int jj = 0; jj < 4; jj++)
+                        lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + warp * 16 + lx + jj])));
+                }
+            }
+            if (p.nxt) {
+                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * p.W + gx) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * p.W + gx) =
+                    make_float4(v[4], v[5], v[6], v[7]);
+            }
+            if (p.out_u8) {
+                uint32_t w0 = 0, w1 = 0;
 #pragma unroll
-                    for (int jj = 0; jj < 2; jj++)
-                        q[4 * i + 2 * side + jj] = qe[(cl.drow + oy + i) & (QR - 1)][cl.dcol + ox + jj];
-            } else {  // 2x2 unit with an odd / mixed-phase domain: sum the raster pixels directly
-#pragma unroll
-                for (int i = 0; i < 2; i++)
-#pragma unroll
-                    for (int jj = 0; jj < 2; jj++) {
-                        const int R = cl.drow + 2 * (oy + i), C = cl.dcol + 2 * (ox + jj);
-                        const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
-                        const float *r0 = raw[k0 % NBUF][R % BLK];
-                        const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
-                        q[4 * i + 2 * side + jj] = ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
-                    }
+                for (int jj = 0; jj < 4; jj++) {
+                    w0 |= (uint32_t)floorf(v[jj] + 0.5f) << (8 * jj);
+                    w1 |= (uint32_t)floorf(v[4 + jj] + 0.5f) << (8 * jj);
+                }
+                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * p.W + gx) = w0;
+                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * p.W + gx) = w1;
             }
         }
-        const float sA = q[0] + q[1] + q[4] + q[5], sB = q[2] + q[3] + q[6] + q[7];
-        float s2 = sA + sB;
-        s2 += __shfl_xor_sync(FULL, s2, 1);   // 4x4 unit (lane pair)
-        float s8 = s2 + __shfl_xor_sync(FULL, s2, 2);
-        s8 += __shfl_xor_sync(FULL, s8, 4);   // 8x8 unit (8 lanes)
-        float s32 = s8 + __shfl_xor_sync(FULL, s8, 8);
-        s32 += __shfl_xor_sync(FULL, s32, 16);  // 16x16 unit (warp)
-        auto unit_b = [&](const Cell &cl, float own) {
-            const int lg = cl.lgd & 0x7F;
-            const float sum = lg == 1 ? own : (lg == 2 ? s2 : (lg == 3 ? s8 : s32));
-            const float mean = sum * __int_as_float((127 - 2 - 2 * lg) << 23);  // sum * 0.25 / side^2
-            return fmaf(-cl.s, mean, cl.o);
-        };
-        const float bA = unit_b(cA, sA), bB = unit_b(cB, sB);
-        float v[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const bool right = (k & 3) >= 2;
-            v[k] = fminf(255.f, fmaxf(0.f, fmaf(right ? cB.a : cA.a, q[k], right ? bB : bA)));
-        }
-        const int gx = rxg + lx, gy = ryg + ly;
-        if (p.track_delta) {
-#pragma unroll
-            for (int i = 0; i < 2; i++) {
-                const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
-#pragma unroll
-                for (int jj = 0; jj < 4; jj++)
-                    lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + warp * 16 + lx + jj])));
-            }
-        }
-        if (p.nxt) {
-            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * p.W + gx) = make_float4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * p.W + gx) = make_float4(v[4], v[5], v[6], v[7]);
-        }
-        if (p.out_u8) {
-            uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-            for (int jj = 0; jj < 4; jj++) {
-                w0 |= (uint32_t)floorf(v[jj] + 0.5f) << (8 * jj);
-                w1 |= (uint32_t)floorf(v[4 + jj] + 0.5f) << (8 * jj);
-            }
-            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * p.W + gx) = w0;
-            *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * p.W + gx) = w1;
-        }
+        word = wnext;
     }
     if (p.track_delta) {
 #pragma unroll
@@ -286,6 +262,27 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
             }
         }
     }
+}
+
+// Unit map from records grouped by root (one warp per root): cells in smem, then one
+// coalesced 32-bit word (two cells) per lane.
+__global__ void build_unit_map_kernel(const uint64_t *records, const int32_t *root_offsets, int rw, int rr0,
+                                      long long n_roots, uint32_t *unit_map) {
+    __shared__ uint16_t cells[8][64];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long root = (long long)blockIdx.x * 8 + warp;
+    if (root >= n_roots) return;
+    const int rxg = (int)(root % rw) * 16, ryg = (int)(rr0 + root / rw) * 16;
+    for (int i = root_offsets[root] + lane; i < root_offsets[root + 1]; i += 32) {
+        const uint64_t r = records[i];
+        const int x = (int)((r >> MNS_REC_X_SHIFT) & 0x7FFF) * 2 - rxg, y = (int)((r >> MNS_REC_Y_SHIFT) & 0x7FFF) * 2 - ryg;
+        const int size = 32 >> ((int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1);
+        for (int cy = y; cy < y + size; cy += 2)
+            for (int cx = x; cx < x + size; cx += 2)
+                cells[warp][morton_of(cx >> 1, cy >> 1)] = mns_unit_of_record(r, rxg, ryg, cx, cy);
+    }
+    __syncwarp();
+    unit_map[root * 32 + lane] = (uint32_t)cells[warp][2 * lane] | ((uint32_t)cells[warp][2 * lane + 1] << 16);
 }
 
 // Per-sweep iteration counter when stop_delta == 0 (no early stop possible).
@@ -409,12 +406,12 @@ int sm_count() {
 
 }  // namespace
 
-int decode_workspace_bytes(int, int, int64_t *bytes) {
-    *bytes = 64;
+int decode_workspace_bytes(int W, int H, int64_t *bytes) {
+    *bytes = 256 + 128ll * (W / 16) * (H / 16);  // state + unit map
     return 0;
 }
 
-static int sweep_smem() { return NBUF * RAW_BYTES + QR * QS * 4 + (int)sizeof(Cell) * BR * 64; }
+static int sweep_smem() { return NBUF * RAW_BYTES + QR * QS * 4; }
 
 static int ensure_sweep_attr() {
     static bool attr_set = false;
@@ -426,19 +423,26 @@ static int ensure_sweep_attr() {
     return 0;
 }
 
+int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1, uint32_t *unit_map,
+                   cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && W % 16 == 0 && 0 <= rr0 && rr0 < rr1, "bad unit-map geometry");
+    const long long n_roots = (long long)(W / 16) * (rr1 - rr0);
+    build_unit_map_kernel<<<(unsigned)((n_roots + 7) / 8), 256, 0, stream>>>(records, root_offsets, W / 16, rr0,
+                                                                             n_roots, unit_map);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // One Jacobi sweep over root rows [rr0, rr1).  cur/nxt/out are "virtual global" bases
 // (row 0 of the full image); only rows [y_lo, y_hi) of cur are resident and read.
-int decode_sweep(const uint64_t *records, const int32_t *root_offsets, int W, int H, int rr0, int rr1,
-                 const float *cur, float init, float *nxt, uint8_t *out, int *state, double stop_delta,
-                 cudaStream_t stream) {
+int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const float *cur, float init,
+                 float *nxt, uint8_t *out, int *state, double stop_delta, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
-    MNS_CHECK_ARG(W >= 32 || H >= 0, "bad width");
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
-    MNS_CHECK_ARG(H <= 32767 * 2, "height exceeds the lattice row range");
+    MNS_CHECK_ARG(H <= 65534, "height exceeds the record coordinate range");
     if (ensure_sweep_attr()) return -1;
     SweepParams p{};
-    p.records = records;
-    p.root_offsets = root_offsets;
+    p.unit_map = unit_map;
     p.W = W;
     p.H = H;
     p.rw = W / 16;
@@ -471,11 +475,16 @@ int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
-    MNS_CHECK_ARG(workspace_bytes >= 64, "workspace too small");
+    int64_t need;
+    decode_workspace_bytes(W, H, &need);
+    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
     MNS_CHECK_ARG(((uintptr_t)ping & 15) == 0 && ((uintptr_t)pong & 15) == 0, "rasters must be 16-byte aligned");
     int *state = reinterpret_cast<int *>(workspace);
+    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
     const long long npx = (long long)W * H;
     MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
+    int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
+    if (rc) return rc;
     const bool track = stop_delta > 0.0;
     for (int it = 0; it < iters; it++) {
         // sweep 0 reads the implied flat raster (no fill pass, no read traffic)
@@ -483,8 +492,8 @@ int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W,
         // out != NULL and no early stop: the final sweep writes the rounded uint8 image directly
         const bool last_fused = out && !track && it == iters - 1;
         float *nxt = last_fused ? nullptr : ((it & 1) ? ping : pong);
-        const int rc = decode_sweep(records, root_offsets, W, H, 0, H / 16, cur, init, nxt,
-                                    last_fused ? out : nullptr, state, stop_delta, stream);
+        rc = decode_sweep(umap, W, H, 0, H / 16, cur, init, nxt, last_fused ? out : nullptr, state, stop_delta,
+                          stream);
         if (rc) return rc;
     }
     if (!track) set_iters_kernel<<<1, 1, 0, stream>>>(state, iters);

@@ -50,6 +50,7 @@ struct EncParams {
     double tol[4];  // E_level (emulation path compares rms > tol like the reference)
     double mean_tol;
     uint64_t *out;
+    uint32_t *unit_map;  // optional: decoder unit map (mns_record.h), 32 words per root
     int32_t *root_offsets;
     int64_t *count;
     unsigned long long *status;
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     // ---- per-warp root: K1c moments + K2 decisions
     uint64_t recA = 0, recB = 0;
     bool hasA = false, hasB = false;
+    uint32_t umap = 0;
     if (warp < nr) {
         const int rxg = x0 + warp * 16, ryg = y0;
         const int wrx = 16 + warp * 16, wry = 16;
@@ -478,6 +480,12 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
             recA = phase1(rxg + lx, ryg + ly, 4, 2, m4L, INFINITY, dummy);
             recB = phase1(rxg + lx + 2, ryg + ly, 4, 2, m4R, INFINITY, dummy);
         }
+        if (p.unit_map) {  // the decoder's per-cell unit map for this lane's two cells
+            const uint64_t cov = (vis1 && acc1) ? rec1 : (vis2 && acc2) ? rec2 : (vis3 && acc3) ? rec3 : recA;
+            const uint64_t covB = vis4 ? recB : cov;
+            umap = (uint32_t)mns_unit_of_record(cov, rxg, ryg, lx, ly) |
+                   ((uint32_t)mns_unit_of_record(covB, rxg, ryg, lx + 2, ly) << 16);
+        }
     }
     const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
     const unsigned lt = lanemask_lt();
@@ -508,6 +516,10 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
         const long long wb = warp_base[warp];
         if (hasA) p.out[wb + offA] = recA;
         if (hasB) p.out[wb + offB] = recB;
+        if (p.unit_map) {
+            const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + warp;
+            p.unit_map[root * 32 + lane] = umap;
+        }
     }
 }
 
@@ -522,7 +534,8 @@ int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *b
 
 int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t image_stride, int n_images, int rr0,
                     int rr1, const mns_enc_cfg *cfg, uint64_t *records, int64_t capacity, int32_t *root_offsets,
-                    int64_t *d_count, void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
+                    int64_t *d_count, uint32_t *unit_map, void *workspace, int64_t workspace_bytes,
+                    cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(W <= 65534 && H <= 65534, "dimensions exceed the record coordinate range");
     MNS_CHECK_ARG(pitch >= W && pitch % 16 == 0, "pitch must be >= width and a multiple of 16");
@@ -562,6 +575,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     p.p1b[4] = INFINITY;
     p.mean_tol = cfg->mean_tol;
     p.out = records;
+    p.unit_map = unit_map;
     p.root_offsets = root_offsets;
     p.count = d_count;
     p.status = reinterpret_cast<unsigned long long *>(workspace);

@@ -72,6 +72,10 @@ class StripDecoder:
         self.pong = torch.empty((rows, width), dtype=torch.float32, device=dev)
         self.out = torch.empty((16 * (r1 - r0), width), dtype=torch.uint8, device=dev)
         self.state = torch.zeros(4, dtype=torch.int32, device=dev)
+        if code.unit_map is None:
+            from .codec import build_unit_map
+
+            build_unit_map(code)
 
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
@@ -89,8 +93,7 @@ class StripDecoder:
             nxt = None if last else bufs[it & 1]
             if sweep_events is not None:
                 sweep_events[it][0].record()
-            N.check(L.mns_decode_sweep(N.ptr(self.code.records), N.ptr(self.code.root_offsets), self.W, self.H,
-                                       self.r0, self.r1,
+            N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1,
                                        self._vbase(cur, self.y_lo, 4) if cur is not None else ctypes.c_void_p(0),
                                        float(initial_value),
                                        self._vbase(nxt, self.y_lo, 4) if nxt is not None else ctypes.c_void_p(0),
