@@ -33,12 +33,15 @@ namespace mns {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int EW = 8;                // roots (warps) per CTA
+constexpr int EW = 8;                // warps per CTA
 constexpr int ET = EW * 32;
-constexpr int WIN_W = EW * 16 + 32;  // 160
+constexpr int RPW = 4;               // roots encoded by each warp per tile (in turn)
+constexpr int TR = EW * RPW;         // 32 consecutive roots of one root row per tile
+constexpr int WIN_W = TR * 16 + 32;  // 544
 constexpr int WIN_H = 48;
-constexpr int QE_W = WIN_W / 2;      // 80
+constexpr int QE_W = WIN_W / 2;      // 272
 constexpr int QE_H = WIN_H / 2;      // 24
+constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + EW * 2 * 64 * 8 + TR * 64 * 8;
 
 struct EncParams {
     const uint8_t *img;
@@ -66,6 +69,21 @@ __device__ __forceinline__ int xsum(int v, int G) {
     return v;
 }
 
+// 2^-k as an exact double
+__device__ __forceinline__ double pow2neg(int k) { return __longlong_as_double((long long)(1023 - k) << 52); }
+
+// Quantised contrast code = 4 + clamp(floor(16N/D), -4, 3) (4 when D == 0): the
+// reference's quantize_contrast(fl(4N/D)) (transform.py:46-53), exactly.  A fast
+// fp32 quotient is corrected by one exact int64 comparison (its error is < 1 unit).
+__device__ __forceinline__ int quant_code(long long N, long long D) {
+    if (D == 0) return 4;  // fit_affine degenerate domain: s = 0 -> bin 4
+    const long long t = 16 * N;
+    int k = (int)floorf(fminf(3.f, fmaxf(-4.f, __fdividef((float)t, (float)D))));
+    if (k > -4 && t < (long long)k * D) --k;
+    else if (k < 3 && t >= (long long)(k + 1) * D) ++k;
+    return 4 + k;
+}
+
 // Phase 1 from exact integer moments (encoder.py:145-166 + transform.py:23-80).
 __device__ __forceinline__ uint64_t phase1(int x, int y, int level, int nlog2, const Mom &m, double bnd,
                                            bool &acc) {
@@ -73,12 +91,7 @@ __device__ __forceinline__ uint64_t phase1(int x, int y, int level, int nlog2, c
     const int o = (2 * m.sr + (int)n) >> (nlog2 + 1);  // round_to_int(mean)
     const long long N = n * m.sqr - (long long)m.sq * m.sr;
     const long long D = n * m.sqq - (long long)m.sq * m.sq;
-    int code = 4;  // fit_affine degenerate domain: s = 0 -> bin 4
-    if (D != 0) {
-        double f = floor((double)(16 * N) / (double)D);
-        f = fmin(3.0, fmax(-4.0, f));
-        code = 4 + (int)f;
-    }
+    const int code = quant_code(N, D);
     const long long k2 = 2 * code - 7;
     const long long A = (long long)m.srr - 2ll * o * m.sr + n * o * o;
     const long long X = 1024ll * n * A - 64ll * k2 * N + k2 * k2 * D;
@@ -95,8 +108,8 @@ __device__ __forceinline__ int p2_quad(int nlog2, const Mom &m, int t, double sl
     const long long D = n * m.sqq - (long long)m.sq * m.sq;
     bit = 0;
     if (D == 0) return (double)A <= bnd_n ? 1 : 0;  // d - mean(d) == 0: both candidates identical
-    const double X = (double)N / (double)(4 * n);    // sum (r - t)(d - dbar), exact
-    const double Y = (double)D / (double)(16 * n);   // sum (d - dbar)^2, exact
+    const double X = (double)N * pow2neg(nlog2 + 2);  // sum (r - t)(d - dbar), exact
+    const double Y = (double)D * pow2neg(nlog2 + 4);  // sum (d - dbar)^2, exact
     const double Ad = (double)A;
     const double lo = Ad - 2.0 * slo * X + slo * slo * Y;
     const double hi = Ad - 2.0 * shi * X + shi * shi * Y;
@@ -152,11 +165,14 @@ __device__ __forceinline__ Node2 p2_node(int nlog2, int sr, int s0, int s1, int 
 }
 
 __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
-    __shared__ __align__(16) uint8_t pix[WIN_H][WIN_W];
-    __shared__ __align__(16) uint16_t qe[QE_H][QE_W];
-    __shared__ double scratch[EW][2][64];
-    __shared__ int warp_cnt[EW];
-    __shared__ long long warp_base[EW];
+    extern __shared__ __align__(16) unsigned char esm[];
+    uint64_t(*stage)[64] = reinterpret_cast<uint64_t(*)[64]>(esm);  // per-root records, DFS order
+    double(*scratch)[2][64] = reinterpret_cast<double(*)[2][64]>(esm + TR * 64 * 8);
+    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TR * 64 * 8 + EW * 2 * 64 * 8);
+    uint16_t(*qe)[QE_W] =
+        reinterpret_cast<uint16_t(*)[QE_W]>(esm + TR * 64 * 8 + EW * 2 * 64 * 8 + WIN_H * WIN_W);
+    __shared__ int root_cnt[TR];
+    __shared__ long long root_base[TR];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long tile = blockIdx.x;
@@ -164,8 +180,8 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     const int img_i = (int)(tile / per_img);
     const int rem = (int)(tile % per_img);
     const int ry = p.rr0 + rem / p.tiles_per_row;
-    const int rx0 = (rem % p.tiles_per_row) * EW;
-    const int nr = min(EW, p.rw - rx0);
+    const int rx0 = (rem % p.tiles_per_row) * TR;
+    const int nr = min(TR, p.rw - rx0);
     const uint8_t *img = p.img + (size_t)img_i * p.image_stride;
     const int x0 = rx0 * 16, y0 = ry * 16;
     const int wx0 = x0 - 16, wy0 = y0 - 16;
@@ -193,13 +209,16 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     }
     __syncthreads();
 
-    // ---- per-warp root: K1c moments + K2 decisions
+    // ---- each warp encodes roots warp, warp + 8, ... of the tile: K1c moments + K2 decisions
+    for (int rr = 0; rr < RPW; rr++) {
+    const int slot = rr * EW + warp;
+    if (slot >= nr) break;
     uint64_t recA = 0, recB = 0;
     bool hasA = false, hasB = false;
     uint32_t umap = 0;
-    if (warp < nr) {
-        const int rxg = x0 + warp * 16, ryg = y0;
-        const int wrx = 16 + warp * 16, wry = 16;
+    {
+        const int rxg = x0 + slot * 16, ryg = y0;
+        const int wrx = 16 + slot * 16, wry = 16;
         const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
         const int ax = (a & 1) * 8, ay = (a >> 1) * 8, bx = (b & 1) * 4, by = (b >> 1) * 4;
         const int lx = ax + bx, ly = ay + by + 2 * c;  // lane's 2x4 pixel block (root-relative)
@@ -490,20 +509,27 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
     const unsigned lt = lanemask_lt();
     const int offA = __popc(bA & lt) + __popc(bB & lt);
-    const int offB = offA + (hasA ? 1 : 0);
-    if (lane == 0) warp_cnt[warp] = __popc(bA) + __popc(bB);
+    if (hasA) stage[slot][offA] = recA;
+    if (hasB) stage[slot][offA + (hasA ? 1 : 0)] = recB;
+    if (lane == 0) root_cnt[slot] = __popc(bA) + __popc(bB);
+    if (p.unit_map) {
+        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
+        p.unit_map[root * 32 + lane] = umap;
+    }
+    }  // roots of this warp
     __syncthreads();
+    // ---- one decoupled look-back per 32 roots, then coalesced record copies
     if (warp == 0) {
         long long agg = 0;
-        for (int w = 0; w < EW; w++) agg += warp_cnt[w];
+        for (int k = 0; k < nr; k++) agg += root_cnt[k];
         const long long base = lookback_exclusive_warp(p.status, tile, agg);
         if (lane == 0) {
             const long long root0 = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0;
             long long run = base;
-            for (int w = 0; w < EW; w++) {
-                warp_base[w] = run;
-                if (w < nr) p.root_offsets[root0 + w] = (int32_t)run;
-                run += warp_cnt[w];
+            for (int k = 0; k < nr; k++) {
+                root_base[k] = run;
+                p.root_offsets[root0 + k] = (int32_t)run;
+                run += root_cnt[k];
             }
             if (tile == p.n_tiles - 1) {
                 p.root_offsets[p.n_roots] = (int32_t)run;
@@ -512,14 +538,9 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
         }
     }
     __syncthreads();
-    if (warp < nr) {
-        const long long wb = warp_base[warp];
-        if (hasA) p.out[wb + offA] = recA;
-        if (hasB) p.out[wb + offB] = recB;
-        if (p.unit_map) {
-            const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + warp;
-            p.unit_map[root * 32 + lane] = umap;
-        }
+    for (int k = warp; k < nr; k += EW) {
+        const long long b0 = root_base[k];
+        for (int i = lane; i < root_cnt[k]; i += 32) p.out[b0 + i] = stage[k][i];
     }
 }
 
@@ -527,7 +548,7 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
 
 int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes) {
     const int rw = width / 16;
-    const long long tiles = (long long)n_images * (rr1 - rr0) * ((rw + EW - 1) / EW);
+    const long long tiles = (long long)n_images * (rr1 - rr0) * ((rw + TR - 1) / TR);
     *bytes = tiles * 8;
     return 0;
 }
@@ -561,7 +582,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     p.rr0 = rr0;
     p.rows = rr1 - rr0;
     p.rw = rw;
-    p.tiles_per_row = (rw + EW - 1) / EW;
+    p.tiles_per_row = (rw + TR - 1) / TR;
     p.mns = cfg->mns;
     p.root_level = cfg->root_level;
     p.min_dim = W < H ? W : H;
@@ -582,7 +603,12 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     p.n_tiles = need / 8;
     p.n_roots = n_roots;
     MNS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, stream));
-    mns_encode_kernel<<<(unsigned)p.n_tiles, ET, 0, stream>>>(p);
+    static bool attr_set = false;
+    if (!attr_set) {
+        MNS_CUDA_TRY(cudaFuncSetAttribute(mns_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC_SMEM));
+        attr_set = true;
+    }
+    mns_encode_kernel<<<(unsigned)p.n_tiles, ET, ENC_SMEM, stream>>>(p);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
