@@ -30,8 +30,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int elem_bytes, const void *base, uint64_t width,
-                   uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h) {
+static int encode_tmap_impl(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
+                            uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h,
+                            CUtensorMapSwizzle swz) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         void *ptr = nullptr;
@@ -43,19 +44,28 @@ int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int elem_bytes, 
         }
         fn = (EncodeTiledFn)ptr;
     }
-    (void)elem_bytes;
     const cuuint64_t dims[2] = {width, height};
     const cuuint64_t strides[1] = {row_bytes};
     const cuuint32_t box[2] = {box_w, box_h};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(map, dtype, 2, const_cast<void *>(base), dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
         return -1;
     }
     return 0;
+}
+
+int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int, const void *base, uint64_t width,
+                   uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h) {
+    return encode_tmap_impl(map, dtype, base, width, height, row_bytes, box_w, box_h, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+int encode_tmap_2d_swizzled(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
+                            uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h) {
+    return encode_tmap_impl(map, dtype, base, width, height, row_bytes, box_w, box_h, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes);

@@ -35,6 +35,21 @@ double sqrt_bound(double E);
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Isometry t of a B x B block (full-search extension; the reference has none):
+// d_t(i, j) = d(src_t(i, j)); t = 0 is the identity.
+__host__ __device__ inline int iso_src(int t, int i, int j, int B) {
+    switch (t) {
+    case 0: return i * B + j;                      // identity
+    case 1: return i * B + (B - 1 - j);            // mirror columns
+    case 2: return (B - 1 - i) * B + j;            // mirror rows
+    case 3: return (B - 1 - i) * B + (B - 1 - j);  // rotate 180
+    case 4: return j * B + i;                      // transpose
+    case 5: return (B - 1 - j) * B + i;            // rotate 90 clockwise
+    case 6: return j * B + (B - 1 - i);            // rotate 90 counter-clockwise
+    default: return (B - 1 - j) * B + (B - 1 - i); // anti-transpose
+    }
+}
+
 // numpy pairwise_sum for float64 (loops_utils.h.src), restated; a points to
 // shared or local memory.  n <= 256.
 __device__ inline double pw_sum_dev(const double *a, int n) {

@@ -14,24 +14,11 @@
 // B in {4, 8} lives in mns_search_tc.cu.
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "mns_common.cuh"
 
 namespace mns {
-
-// isometry t of a B x B block: d_t(i, j) = d(src_t(i, j)) (t = 0 identity)
-__host__ __device__ inline int iso_src(int t, int i, int j, int B) {
-    switch (t) {
-    case 0: return i * B + j;
-    case 1: return i * B + (B - 1 - j);
-    case 2: return (B - 1 - i) * B + j;
-    case 3: return (B - 1 - i) * B + (B - 1 - j);
-    case 4: return j * B + i;
-    case 5: return (B - 1 - j) * B + i;
-    case 6: return j * B + (B - 1 - i);
-    default: return (B - 1 - j) * B + (B - 1 - i);
-    }
-}
 
 namespace {
 
@@ -292,18 +279,26 @@ struct SearchWs {
 
 static int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
+int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso);
+
 int search_workspace_bytes(int W, int H, int B, int step, int n_iso, int64_t *bytes) {
     const long long ndx = (W - 2 * B) / step + 1, ndy = (H - 2 * B) / step + 1;
     const long long ndom = ndx * ndy, n = (long long)B * B;
     const long long nranges = (long long)(W / B) * (H / B);
     *bytes = align256(ndom * n * 2) + align256(ndom * 4) + align256(ndom * 8) + align256(nranges * 8);
-    (void)n_iso;
+    if (B <= 8) *bytes += align256(search_tc_workspace_bytes(W, H, B, step, n_iso));
     return 0;
 }
 
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
                    const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
-                   unsigned long long *best, cudaStream_t st, bool *handled);
+                   unsigned long long *best, void *tc_ws, cudaStream_t st, bool *handled);
+
+// MNS_SEARCH_CUDA_CORES=1 selects the exact CUDA-core path for every B (A/B checks of the tensor-core path).
+static bool force_cuda_cores() {
+    const char *e = getenv("MNS_SEARCH_CUDA_CORES");
+    return e && e[0] == '1';
+}
 
 int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1, int32_t *out_dom,
                 int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st) {
@@ -329,11 +324,15 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     w.pD = (long long *)p;
     p += align256(ndom * 8);
     w.best = (unsigned long long *)p;
+    p += align256(nranges * 8);
+    void *tc_ws = B <= 8 ? (void *)p : nullptr;
     const int sms = sm_count_search();
     pool_kernel<<<sms * 8, 256, 0, st>>>(img, W, B, step, (int)ndx, ndom, w.pool, w.psq, w.pD);
     fill_u64_kernel<<<64, 256, 0, st>>>(w.best, ~0ull, r1 - r0);
     bool handled = false;
-    int rc = full_search_tc(img, W, H, B, step, n_iso, r0, r1, w.pool, w.psq, w.pD, ndom, w.best, st, &handled);
+    int rc = 0;
+    if (!force_cuda_cores()) rc = full_search_tc(img, W, H, B, step, n_iso, r0, r1, w.pool, w.psq, w.pD, ndom, w.best,
+                                               tc_ws, st, &handled);
     if (rc) return rc;
     if (!handled) {
         const int tiles = (r1 - r0 + 7) / 8;

@@ -1,12 +1,428 @@
-// tcgen05 tensor-core full search (B in {4, 8}) -- see DESIGN.md.  Placeholder
-// dispatcher until the UMMA kernel lands: reports "not handled" so the exact
-// CUDA-core path runs.
+// tcgen05 tensor-core full search (K3) for B in {2, 4, 8} on sm_100a.
+//
+// Replaces encoder.py:249-309 (encode_full_search): the range x domain cross
+// products C[row][d] = sum_k r_row[k] * q_d[k] run as an FP16 x FP16 -> FP32 UMMA
+// GEMM (exact: q <= 1020, r <= 255, B^2 <= 64 -> every partial sum is an integer
+// < 2^24).  rows = (range, isometry) pairs (M, 128 per CTA tile), columns = domains
+// (N = 256 per MMA tile), K = 64 (zero-padded for B < 8).
+//
+// Warp roles (12 warps): w0 TMA producer (A once, B tiles through a 4-stage
+// ring, 128B-swizzled K-major), w1 single-thread MMA issuer (4 x K=16 per tile
+// into one of two 256-column TMEM accumulators), w2 TMEM allocator, w4..w11
+// epilogue: each thread owns one TMEM lane (= one range row) and half of the
+// 256 columns.
+//
+// Epilogue (exact): the reference's per-domain SSE is
+//   1024 n SSE = 1024 n A - 64 k2 N + k2^2 D,  N = n C - Sq Sr,
+// minimised over the odd k2 in [-7, 7]; its continuous relaxation gives the lower
+// bound -1024 N^2 / D.  Against the row's running exact best V* an element can
+// only win if |N/n| >= sqrt(-V*/1024)/n * sqrt(D); that test is 2 FFMA + 1 FMNMX
+// per element (with rounding slack), and only surviving elements are evaluated
+// exactly in int64 and folded into the row's lexicographic (value, index) key.
+// Constant ranges (N == 0 for every domain) take the precomputed argmin of D.
+
+#include <cuda_fp16.h>
+#include <math.h>
+
 #include "mns_common.cuh"
+#include "mns_tma.cuh"
 
 namespace mns {
-int full_search_tc(const uint8_t *, int, int, int, int, int, int, int, const uint16_t *, const int32_t *,
-                   const long long *, long long, unsigned long long *, cudaStream_t, bool *handled) {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int BM = 128, BN = 256, BK = 64;   // MMA tile (M rows, N domains, K)
+constexpr int STAGES = 4;
+constexpr int NTHREADS = 384;
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KB
+constexpr int CONST_BYTES = BN * 16;          // (Sq, sqrt(D), D, 32n/D) per column
+constexpr int SMEM_BYTES = 1024 + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES + 256;
+
+struct TcParams {
+    int n_rows;          // (r1 - r0) * n_iso
+    int n_iso, r0, n;    // n = B*B
+    long long ndom;
+    int dtiles_per_chunk, n_dtiles;
+    const float4 *consts;        // [ndom_pad] (Sq, sqrt_rd(D), D, 32n/D)
+    const int32_t *psq;          // exact Sq
+    const long long *pD;         // exact D
+    const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range (-1 = padding row)
+    const int32_t *row_flat;     // [n_rows_pad] 1 if the range is constant (N == 0 for every domain)
+    const unsigned long long *flat_key;  // argmin-D key for constant ranges
+    unsigned long long *best;    // [r1 - r0]
+};
+
+__device__ __forceinline__ unsigned long long make_key(long long val, long long cand) {
+    return ((unsigned long long)(val + (1ll << 42)) << 21) | (unsigned long long)cand;
+}
+
+// exact min over odd k2 in [-7, 7] of k2^2 D - 64 k2 N: an fp32 estimate of the vertex
+// 32N/D picks the nearest odd k2; it and both odd neighbours are evaluated exactly.
+__device__ __forceinline__ long long best_val_exact(long long N, long long D) {
+    if (D == 0) return 0;  // N == 0 whenever D == 0
+    const float t = __fdividef(32.f * (float)N, (float)D);
+    const int k = 2 * (int)floorf(fminf(8.f, fmaxf(-8.f, t)) * 0.5f) + 1;
+    long long best = LLONG_MAX;
+#pragma unroll
+    for (int dk = -2; dk <= 2; dk += 2) {
+        const long long k2 = k + dk;
+        if (k2 < -7 || k2 > 7) continue;
+        const long long v = k2 * k2 * D - 64 * k2 * N;
+        best = v < best ? v : best;
+    }
+    return best;
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    // K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (1), version 1
+    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+          "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    full_search_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const TcParams p) {
+    extern __shared__ __align__(1024) unsigned char tsm_raw[];
+    unsigned char *tsm = reinterpret_cast<unsigned char *>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = tsm;
+    unsigned char *sB = tsm + A_BYTES;
+    float4 *sC = reinterpret_cast<float4 *>(tsm + A_BYTES + STAGES * B_BYTES);  // [2][BN]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES);
+    uint64_t *full_bar = bars, *empty_bar = bars + STAGES, *a_bar = bars + 2 * STAGES;
+    uint64_t *tfull = bars + 2 * STAGES + 1, *tempty = bars + 2 * STAGES + 3;
+    uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tile = blockIdx.y;
+    const int dt0 = blockIdx.x * p.dtiles_per_chunk;
+    const int dt1 = min(p.n_dtiles, dt0 + p.dtiles_per_chunk);
+    const int ntiles = dt1 - dt0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(a_bar, 1);
+        for (int a = 0; a < 2; a++) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_base_sh)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_base_sh;
+
+    if (warp == 0) {
+        // ===== TMA producer
+        if (lane == 0) {
+            prefetch_tmap(&tmA);
+            prefetch_tmap(&tmB);
+            mbar_arrive_expect_tx(a_bar, A_BYTES);
+            tma_load_2d(sA, &tmA, 0, m_tile * BM, a_bar);
+            for (int t = 0; t < ntiles; t++) {
+                const int s = t % STAGES;
+                if (t >= STAGES) mbar_wait(&empty_bar[s], ((t / STAGES) - 1) & 1);
+                mbar_arrive_expect_tx(&full_bar[s], B_BYTES);
+                tma_load_2d(sB + s * B_BYTES, &tmB, 0, (dt0 + t) * BN, &full_bar[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (one thread)
+        if (lane == 0) {
+            // instruction descriptor: F32 accumulate, F16 A/B, K-major both, N = 256, M = 128
+            const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            mbar_wait(a_bar, 0);
+            tc_fence_after();
+            const uint64_t adesc = umma_desc_sw128(smem_u32(sA));
+            for (int t = 0; t < ntiles; t++) {
+                const int s = t % STAGES, acc = t & 1;
+                if (t >= 2) mbar_wait(&tempty[acc], ((t / 2) - 1) & 1);
+                mbar_wait(&full_bar[s], (t / STAGES) & 1);
+                tc_fence_after();
+                const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + s * B_BYTES));
+#pragma unroll
+                for (int k = 0; k < BK / 16; k++)  // +32 B per K=16 step inside the 128B swizzle atom
+                    umma_f16(tmem + acc * BN, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
+                umma_commit(&empty_bar[s]);  // frees the B stage when these MMAs complete
+                umma_commit(&tfull[acc]);    // accumulator ready for the epilogue
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ===== epilogue: one TMEM lane (= range row) per thread, half of the columns per warp pair
+        const int ew = warp - EPI_WARP0;       // 0..7
+        const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+        const int half = ew >> 2;              // column half (0: 0..127, 1: 128..255)
+        const int row = m_tile * BM + quarter * 32 + lane;
+        const bool active = row < p.n_rows;
+        const int sr = active ? p.row_sr[row] : 0;
+        const bool flat = active ? p.row_flat[row] != 0 : true;
+        const int iso = row % p.n_iso;
+        const float sr_n = (float)sr / (float)p.n;  // exact: n is a power of two
+        unsigned long long best = ~0ull;
+        long long vstar = LLONG_MAX;   // threshold: best exact value known for this range (any row / CTA)
+        float scl = 0.f;               // sqrt(-V*/1024)/n rounded down; 0 = no skipping
+        const float slack = 16.f;
+        const int rr = row / p.n_iso;
+        const float n64 = -64.f * (float)p.n;
+        auto set_threshold = [&](long long v) {
+            if (v < vstar) {
+                vstar = v;
+                // LB = -1024 N^2 / D > V*  <=>  |N/n| < sqrt(-V*/1024)/n * sqrt(D)
+                scl = v < 0 ? __fmul_rd(__fsqrt_rd((float)(-(double)v / 1024.0) * 0.999f), 1.0f / (float)p.n)
+                            : 0.f;
+            }
+        };
+        for (int t = 0; t < ntiles; t++) {
+            const int acc = t & 1, cbuf = t & 1;
+            const long long dbase = (long long)(dt0 + t) * BN;
+            {   // stage this tile's column constants (epilogue warps only, named barrier 1)
+                const int e = threadIdx.x - EPI_WARP0 * 32;  // 0..255
+                const long long d = dbase + e;
+                sC[cbuf * BN + e] = d < p.ndom ? p.consts[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            // share the running best: other CTAs' results for this range (global keys) and the
+            // other isometry rows of the same range (adjacent lanes)
+            if (active && !flat) {
+                const unsigned long long g = *((volatile unsigned long long *)&p.best[rr]);
+                if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
+            }
+            for (int o = 1; o < p.n_iso; o <<= 1) {
+                const long long other = __shfl_xor_sync(FULL, vstar, o);
+                if (active && !flat) set_threshold(other);
+            }
+            named_sync(1, EPI_WARPS * 32);
+            mbar_wait(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            for (int ch = 0; ch < BN / 2 / 32; ch++) {
+                const int col0 = half * (BN / 2) + ch * 32;
+                float c[32];
+                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + col0, c);
+                if (flat || !active) continue;
+                // level 1: continuous lower bound (2 FFMA + FMNMX per element)
+                float m = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const float4 k = sC[cbuf * BN + col0 + j];
+                    const float n1 = fmaf(-k.x, sr_n, c[j]);          // N / n (fp32, |err| <= 2)
+                    m = fmaxf(m, fmaf(-scl, k.y, fabsf(n1)));
+                }
+                if (m < -slack) continue;
+                // level 2: quantised value in fp32 at the two odd k2 around the vertex; level 3: exact
+                const float vthr = (float)vstar;
+#pragma unroll 4
+                for (int j = 0; j < 32; j++) {
+                    const float4 k = sC[cbuf * BN + col0 + j];
+                    const float n1 = fmaf(-k.x, sr_n, c[j]);
+                    if (fmaf(-scl, k.y, fabsf(n1)) < -slack) continue;
+                    const float tv = n1 * k.w;  // 32 N / D
+                    const float mf = fminf(3.f, fmaxf(-4.f, rintf(fmaf(tv, 0.5f, -0.5f))));
+                    const float k2a = fmaf(2.f, mf, 1.f);
+                    const float k2b = fminf(7.f, fmaxf(-7.f, tv > k2a ? k2a + 2.f : k2a - 2.f));
+                    const float va = k2a * fmaf(k2a, k.z, n64 * n1), vb = k2b * fmaf(k2b, k.z, n64 * n1);
+                    const float vt = fminf(va, vb);
+                    const float margin = 131072.f + 1e-5f * (fabsf(vt) + 49.f * k.z);
+                    // the vertex estimate is off by <= 2 * 32n/D (n1 error <= 2): trust it only when tight
+                    if (vstar != LLONG_MAX && k.w < 0.1f && vt - margin > vthr) continue;
+                    const long long d = dbase + col0 + j;
+                    if (d >= p.ndom) continue;
+                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)p.psq[d] * sr;
+                    const long long v = best_val_exact(N, p.pD[d]);
+                    const unsigned long long key = make_key(v, d * p.n_iso + iso);
+                    if (key < best) {
+                        best = key;
+                        set_threshold(v);
+                        atomicMin(&p.best[rr], key);  // publish to the other CTAs of this range
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (active) atomicMin(&p.best[rr], flat ? *p.flat_key : best);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ---- operand preparation
+__global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
+                                long long ndom_pad, int n, __half *Q, float4 *consts) {
+    for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndom_pad;
+         d += (long long)gridDim.x * blockDim.x) {
+        for (int k = 0; k < BK; k++)
+            Q[d * BK + k] = __float2half_rn(d < ndom && k < n ? (float)pool[d * n + k] : 0.f);
+        const float Df = d < ndom ? (float)pD[d] : 0.f;
+        consts[d] = d < ndom ? make_float4((float)psq[d], __fsqrt_rd(__ll2float_rd(pD[d])), Df,
+                                           Df > 0.f ? 32.f * (float)n / Df : 0.f)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+__global__ void range_rows_kernel(const uint8_t *img, int W, int B, int n_iso, int r0, int n_rows, int n_rows_pad,
+                                  __half *A, int32_t *row_sr, int32_t *row_flat) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n_rows_pad) return;
+    const int n = B * B;
+    if (row >= n_rows) {
+        for (int k = 0; k < BK; k++) A[(size_t)row * BK + k] = __float2half_rn(0.f);
+        row_sr[row] = 0;
+        row_flat[row] = 1;
+        return;
+    }
+    const int ri = r0 + row / n_iso, t = row % n_iso, rpr = W / B;
+    const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
+    float v[BK];
+    for (int k = 0; k < BK; k++) v[k] = 0.f;
+    int sr = 0, srr = 0;
+    for (int e = 0; e < n; e++) {
+        const int r = img[(size_t)(ry + e / B) * W + rx + e % B];
+        v[iso_src(t, e / B, e % B, B)] = (float)r;  // row[src_t(e)] = r(e)
+        sr += r;
+        srr += r * r;
+    }
+    for (int k = 0; k < BK; k++) A[(size_t)row * BK + k] = __float2half_rn(v[k]);
+    row_sr[row] = sr;
+    row_flat[row] = ((long long)n * srr - (long long)sr * sr) == 0;
+}
+
+__global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, unsigned long long *key) {
+    unsigned long long best = ~0ull;
+    for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndom;
+         d += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = make_key(pD[d], d * n_iso);  // constant range: val = D (k2 = +-1), iso 0
+        best = k < best ? k : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(FULL, best, o);
+        best = other < best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(key, best);
+}
+
+}  // namespace
+
+int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso) {
+    const long long ndx = (W - 2 * B) / step + 1, ndy = (H - 2 * B) / step + 1, ndom = ndx * ndy;
+    const long long ndom_pad = (ndom + BN - 1) / BN * BN;
+    const long long rows_pad = ((long long)(W / B) * (H / B) * n_iso + BM - 1) / BM * BM;
+    return ndom_pad * BK * 2 + ndom_pad * 16 + rows_pad * BK * 2 + rows_pad * 8 + 1024;
+}
+
+int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
+                   const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
+                   unsigned long long *best, void *tc_ws, cudaStream_t st, bool *handled) {
     *handled = false;
+    if (!(B == 2 || B == 4 || B == 8) || !tc_ws) return 0;
+    const int n = B * B;
+    const long long ndom_pad = (ndom + BN - 1) / BN * BN;
+    const int n_rows = (r1 - r0) * n_iso;
+    const int n_rows_pad = (n_rows + BM - 1) / BM * BM;
+    char *q = (char *)tc_ws;
+    __half *Q = (__half *)q;
+    q += ndom_pad * BK * 2;
+    float4 *consts = (float4 *)q;
+    q += ndom_pad * 16;
+    __half *A = (__half *)q;
+    q += (long long)n_rows_pad * BK * 2;
+    int32_t *row_sr = (int32_t *)q;
+    q += (long long)n_rows_pad * 4;
+    int32_t *row_flat = (int32_t *)q;
+    q += (long long)n_rows_pad * 4;
+    unsigned long long *fkey = (unsigned long long *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+
+    pool_f16_kernel<<<296, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
+    range_rows_kernel<<<(n_rows_pad + 127) / 128, 128, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, A, row_sr,
+                                                                 row_flat);
+    MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
+    flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
+
+    CUtensorMap tmA, tmB;
+    if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
+    if (encode_tmap_2d_swizzled(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, ndom_pad, BK * 2, BK, BN)) return -1;
+
+    TcParams p{};
+    p.n_rows = n_rows;
+    p.n_iso = n_iso;
+    p.r0 = r0;
+    p.n = n;
+    p.ndom = ndom;
+    p.n_dtiles = (int)(ndom_pad / BN);
+    p.dtiles_per_chunk = 24;
+    p.consts = consts;
+    p.psq = psq;
+    p.pD = pD;
+    p.row_sr = row_sr;
+    p.row_flat = row_flat;
+    p.flat_key = fkey;
+    p.best = best;
+    static bool attr_set = false;
+    if (!attr_set) {
+        MNS_CUDA_TRY(cudaFuncSetAttribute(full_search_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          SMEM_BYTES));
+        attr_set = true;
+    }
+    dim3 grid((p.n_dtiles + p.dtiles_per_chunk - 1) / p.dtiles_per_chunk, n_rows_pad / BM);
+    full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
+    MNS_CUDA_TRY(cudaGetLastError());
+    *handled = true;
     return 0;
 }
+
 }  // namespace mns

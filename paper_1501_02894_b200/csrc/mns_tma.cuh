@@ -26,7 +26,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
@@ -48,5 +48,8 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 // Host: cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
 int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int elem_bytes, const void *base, uint64_t width,
                    uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h);
+// Same with 128-byte swizzle (K-major UMMA operand tiles; box_w * elem = 128 B).
+int encode_tmap_2d_swizzled(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
+                            uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h);
 
 }  // namespace mns
