@@ -51,24 +51,31 @@ __device__ __forceinline__ unsigned long long make_key(long long val, long long 
     return ((unsigned long long)(val + (1ll << 42)) << 21) | (unsigned long long)cand;
 }
 
-// ---- domain pool: q values (u16, n per domain, raster order over the stride lattice), Sq, D
+// ---- domain pool: q values (u16, n per domain, raster order over the stride lattice), Sq, D.
+//      One warp per domain: lanes own consecutive q (coalesced), Sq / Sqq by warp reduction.
 __global__ void pool_kernel(const uint8_t *img, int W, int B, int step, int ndx, long long ndom, uint16_t *pool,
                             int32_t *psq, long long *pD) {
-    const int n = B * B;
-    for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndom;
-         d += (long long)gridDim.x * blockDim.x) {
+    const int n = B * B, lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long d = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); d < ndom; d += warps) {
         const int x = (int)(d % ndx) * step, y = (int)(d / ndx) * step;
         long long sq = 0, sqq = 0;
-        for (int i = 0; i < B; i++)
-            for (int j = 0; j < B; j++) {
-                const uint8_t *p = img + (size_t)(y + 2 * i) * W + x + 2 * j;
-                const int q = p[0] + p[1] + p[W] + p[W + 1];
-                pool[d * n + i * B + j] = (uint16_t)q;
-                sq += q;
-                sqq += q * q;
-            }
-        psq[d] = (int32_t)sq;
-        pD[d] = n * sqq - sq * sq;
+        for (int k = lane; k < n; k += 32) {
+            const uint8_t *p = img + (size_t)(y + 2 * (k / B)) * W + x + 2 * (k % B);
+            const int q = p[0] + p[1] + p[W] + p[W + 1];
+            pool[d * n + k] = (uint16_t)q;
+            sq += q;
+            sqq += q * q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sq += __shfl_xor_sync(FULL, sq, o);
+            sqq += __shfl_xor_sync(FULL, sqq, o);
+        }
+        if (lane == 0) {
+            psq[d] = (int32_t)sq;
+            pD[d] = n * sqq - sq * sq;
+        }
     }
 }
 
@@ -327,7 +334,7 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     p += align256(nranges * 8);
     void *tc_ws = B <= 8 ? (void *)p : nullptr;
     const int sms = sm_count_search();
-    pool_kernel<<<sms * 8, 256, 0, st>>>(img, W, B, step, (int)ndx, ndom, w.pool, w.psq, w.pD);
+    pool_kernel<<<sms * 16, 256, 0, st>>>(img, W, B, step, (int)ndx, ndom, w.pool, w.psq, w.pD);
     fill_u64_kernel<<<64, 256, 0, st>>>(w.best, ~0ull, r1 - r0);
     bool handled = false;
     int rc = 0;

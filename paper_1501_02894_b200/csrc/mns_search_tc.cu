@@ -1,10 +1,10 @@
 // tcgen05 tensor-core full search (K3) for B in {2, 4, 8} on sm_100a.
 //
-// Replaces encoder.py:249-309 (encode_full_search): the range x domain cross
-// products C[row][d] = sum_k r_row[k] * q_d[k] run as an FP16 x FP16 -> FP32 UMMA
-// GEMM (exact: q <= 1020, r <= 255, B^2 <= 64 -> every partial sum is an integer
-// < 2^24).  rows = (range, isometry) pairs (M, 128 per CTA tile), columns = domains
-// (N = 256 per MMA tile), K = 64 (zero-padded for B < 8).
+// Replaces encoder.py:249-309 (encode_full_search).  The range x domain cross
+// products C = sum_k q_d[k] r_row[k] run as an FP16 x FP16 -> FP32 UMMA GEMM that
+// is exact (q <= 1020, r <= 255, B^2 <= 64: every partial sum is an integer < 2^24).
+// rows = (range, isometry) pairs (M, 128 per CTA tile), columns = domains
+// (N = 128 per MMA tile), K = 64 (zero-padded for B < 8).
 //
 // Warp roles (12 warps): w0 TMA producer (A once, B tiles through a 4-stage
 // ring, 128B-swizzled K-major), w1 single-thread MMA issuer (4 x K=16 per tile
@@ -16,9 +16,12 @@
 //   1024 n SSE = 1024 n A - 64 k2 N + k2^2 D,  N = n C - Sq Sr,
 // minimised over the odd k2 in [-7, 7]; its continuous relaxation gives the lower
 // bound -1024 N^2 / D.  Against the row's running exact best V* an element can
-// only win if |N/n| >= sqrt(-V*/1024)/n * sqrt(D); that test is 2 FFMA + 1 FMNMX
-// per element (with rounding slack), and only surviving elements are evaluated
-// exactly in int64 and folded into the row's lexicographic (value, index) key.
+// only win if |N/n| >= sqrt(-V*/1024)/n * sqrt(D); with N/n = C - Sq*Sr/n that test is
+// 2 FFMA + 1 FMNMX per element.  Survivors (voted per column across the warp) pass
+// a rigorous fp32 lower bound of the quantised value; the rest are evaluated exactly
+// in int64 from C and the tile's staged (Sq, D) and folded into the row's
+// lexicographic (value, index) key.  A prepass over a 1/64 domain sample seeds the
+// per-range bests (shared through global keys) so few candidates are ever exact-evaluated.
 // Constant ranges (N == 0 for every domain) take the precomputed argmin of D.
 
 #include <cuda_fp16.h>
@@ -29,27 +32,33 @@
 
 namespace mns {
 
+#ifdef MNS_TC_STATS
+__device__ unsigned long long g_tc_stats[4];  // chunks, level-1 passes, level-2 entries, exact evaluations
+#endif
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int BM = 128, BN = 256, BK = 64;   // MMA tile (M rows, N domains, K)
+constexpr int BM = 128, BN = 128, BK = 64;   // MMA tile (M rows, N domains, K)
+constexpr int MH = 2;                         // M halves per CTA: 256 rows share every B tile
 constexpr int STAGES = 4;
-constexpr int NTHREADS = 384;
-constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
-constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-constexpr int B_BYTES = BN * BK * 2;          // 32 KB
-constexpr int CONST_BYTES = BN * 16;          // (Sq, sqrt(D), D, 32n/D) per column
-constexpr int SMEM_BYTES = 1024 + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES + 256;
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
+constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;  // 640
+constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB
+constexpr int B_BYTES = BN * BK * 2;          // 16 KB
+constexpr int CONST_BYTES = BN * 16;          // (Sq, sqrt(D)) + exact D per column
+constexpr int TMEM_COLS = 2 * MH * BN;        // 2 accumulator stages x 2 M halves x 128 columns = 512
+constexpr int SMEM_BYTES = 1024 + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES + 512;
 
 struct TcParams {
     int n_rows;          // (r1 - r0) * n_iso
     int n_iso, r0, n;    // n = B*B
     long long ndom;
     int dtiles_per_chunk, n_dtiles;
-    const float4 *consts;        // [ndom_pad] (Sq, sqrt_rd(D), D, 32n/D)
-    const int32_t *psq;          // exact Sq
+    int dstride;                 // domain of column c of tile t: ((dt0 + t) * BN + c) * dstride
+    const float2 *consts;        // [ndom_pad] (Sq, sqrt_rd(D))
     const long long *pD;         // exact D
-    const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range (-1 = padding row)
+    const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range
     const int32_t *row_flat;     // [n_rows_pad] 1 if the range is constant (N == 0 for every domain)
     const unsigned long long *flat_key;  // argmin-D key for constant ranges
     unsigned long long *best;    // [r1 - r0]
@@ -96,20 +105,17 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
+constexpr int CH = 16;  // accumulator columns per TMEM load
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[CH]) {
+    uint32_t r[CH];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-          "=r"(r[30]), "=r"(r[31])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < CH; i++) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -121,6 +127,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
+// 1D bulk copy global -> shared completing on an mbarrier (size multiple of 16 B)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     full_search_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const TcParams p) {
@@ -128,11 +142,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned char *tsm = reinterpret_cast<unsigned char *>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = tsm;
     unsigned char *sB = tsm + A_BYTES;
-    float4 *sC = reinterpret_cast<float4 *>(tsm + A_BYTES + STAGES * B_BYTES);  // [2][BN]
+    float2 *sL = reinterpret_cast<float2 *>(tsm + A_BYTES + STAGES * B_BYTES);              // [2][BN] (Sq, sqrt D)
+    long long *sD = reinterpret_cast<long long *>(tsm + A_BYTES + STAGES * B_BYTES + 2 * BN * 8);  // [2][BN] D
     uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES);
     uint64_t *full_bar = bars, *empty_bar = bars + STAGES, *a_bar = bars + 2 * STAGES;
     uint64_t *tfull = bars + 2 * STAGES + 1, *tempty = bars + 2 * STAGES + 3;
-    uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 5);
+    uint64_t *cfull = bars + 2 * STAGES + 5, *cempty = bars + 2 * STAGES + 7;  // column-constant double buffer
+    uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 9);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m_tile = blockIdx.y;
@@ -149,13 +165,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int a = 0; a < 2; a++) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], EPI_WARPS);
+            mbar_init(&cfull[a], 1);
+            mbar_init(&cempty[a], EPI_WARPS);
         }
         fence_mbar_init();
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_base_sh)),
-                     "r"(512));
+                     "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -169,13 +187,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
             mbar_arrive_expect_tx(a_bar, A_BYTES);
-            tma_load_2d(sA, &tmA, 0, m_tile * BM, a_bar);
+            for (int h = 0; h < MH; h++) tma_load_2d(sA + h * BM * BK * 2, &tmA, 0, (m_tile * MH + h) * BM, a_bar);
+            int tc = 0;  // next tile whose column constants are streamed (kept <= 2 tiles ahead of the epilogue)
+            auto stream_consts = [&](int upto) {
+                for (; tc < ntiles && tc < upto; tc++) {
+                    const int cb = tc & 1;
+                    if (tc >= 2) mbar_wait(&cempty[cb], ((tc >> 1) - 1) & 1);
+                    mbar_arrive_expect_tx(&cfull[cb], BN * 16);
+                    const long long b0 = (long long)(dt0 + tc) * BN;
+                    bulk_g2s(sL + cb * BN, p.consts + b0, BN * 8, &cfull[cb]);
+                    bulk_g2s(sD + cb * BN, p.pD + b0, BN * 8, &cfull[cb]);
+                }
+            };
             for (int t = 0; t < ntiles; t++) {
                 const int s = t % STAGES;
+                stream_consts(t + 1);
                 if (t >= STAGES) mbar_wait(&empty_bar[s], ((t / STAGES) - 1) & 1);
                 mbar_arrive_expect_tx(&full_bar[s], B_BYTES);
                 tma_load_2d(sB + s * B_BYTES, &tmB, 0, (dt0 + t) * BN, &full_bar[s]);
             }
+            stream_consts(ntiles);
         }
     } else if (warp == 1) {
         // ===== MMA issuer (one thread)
@@ -185,7 +216,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                    ((uint32_t)(BM >> 4) << 24);
             mbar_wait(a_bar, 0);
             tc_fence_after();
-            const uint64_t adesc = umma_desc_sw128(smem_u32(sA));
+            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
             for (int t = 0; t < ntiles; t++) {
                 const int s = t % STAGES, acc = t & 1;
                 if (t >= 2) mbar_wait(&tempty[acc], ((t / 2) - 1) & 1);
@@ -193,92 +224,119 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_after();
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + s * B_BYTES));
 #pragma unroll
-                for (int k = 0; k < BK / 16; k++)  // +32 B per K=16 step inside the 128B swizzle atom
-                    umma_f16(tmem + acc * BN, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
+                for (int h = 0; h < MH; h++) {  // both M halves against the same B tile
+                    const uint64_t adesc = adesc0 + (uint64_t)((h * BM * BK * 2) >> 4);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; k++)  // +32 B per K=16 step inside the 128B swizzle atom
+                        umma_f16(tmem + (acc * MH + h) * BN, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
+                }
                 umma_commit(&empty_bar[s]);  // frees the B stage when these MMAs complete
                 umma_commit(&tfull[acc]);    // accumulator ready for the epilogue
             }
         }
     } else if (warp >= EPI_WARP0) {
         // ===== epilogue: one TMEM lane (= range row) per thread, half of the columns per warp pair
-        const int ew = warp - EPI_WARP0;       // 0..7
+        const int ew = warp - EPI_WARP0;       // 0..15
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
-        const int half = ew >> 2;              // column half (0: 0..127, 1: 128..255)
-        const int row = m_tile * BM + quarter * 32 + lane;
+        const int mh = (ew >> 2) & 1;          // M half
+        const int half = ew >> 3;              // column half (0: 0..63, 1: 64..127)
+        const int row = (m_tile * MH + mh) * BM + quarter * 32 + lane;
         const bool active = row < p.n_rows;
         const int sr = active ? p.row_sr[row] : 0;
         const bool flat = active ? p.row_flat[row] != 0 : true;
         const int iso = row % p.n_iso;
-        const float sr_n = (float)sr / (float)p.n;  // exact: n is a power of two
+        const float sr_n = (float)sr / (float)p.n;  // exact (n is a power of two)
+        const float err = 2.f;          // |fl(C - Sq*Sr/n) - N/n| <= 2 (one FMA rounding, |N/n| < 2^25)
+        const float slack = err + 4.f;  // plus the rounding of the test's own FFMA
         unsigned long long best = ~0ull;
         long long vstar = LLONG_MAX;   // threshold: best exact value known for this range (any row / CTA)
         float scl = 0.f;               // sqrt(-V*/1024)/n rounded down; 0 = no skipping
-        const float slack = 16.f;
         const int rr = row / p.n_iso;
         const float n64 = -64.f * (float)p.n;
+        const float inv_n = 1.0f / (float)p.n;  // exact (power of two)
         auto set_threshold = [&](long long v) {
             if (v < vstar) {
                 vstar = v;
-                // LB = -1024 N^2 / D > V*  <=>  |N/n| < sqrt(-V*/1024)/n * sqrt(D)
-                scl = v < 0 ? __fmul_rd(__fsqrt_rd((float)(-(double)v / 1024.0) * 0.999f), 1.0f / (float)p.n)
-                            : 0.f;
+                // LB = -1024 N^2 / D > V*  <=>  |N/n| < sqrt(-V*/1024)/n * sqrt(D)  (rounded down)
+                scl = v < 0 ? __fmul_rd(__fsqrt_rd(__fmul_rd(__ll2float_rd(-v), 0.999f / 1024.f)), inv_n) : 0.f;
             }
         };
+        // column constants of tile t arrive in sL/sD[t & 1] through the producer's bulk copies (cfull)
+        unsigned long long g = (active && !flat) ? *((volatile unsigned long long *)&p.best[rr]) : ~0ull;
         for (int t = 0; t < ntiles; t++) {
             const int acc = t & 1, cbuf = t & 1;
             const long long dbase = (long long)(dt0 + t) * BN;
-            {   // stage this tile's column constants (epilogue warps only, named barrier 1)
-                const int e = threadIdx.x - EPI_WARP0 * 32;  // 0..255
-                const long long d = dbase + e;
-                sC[cbuf * BN + e] = d < p.ndom ? p.consts[d] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            // share the running best: other CTAs' results for this range (global keys) and the
-            // other isometry rows of the same range (adjacent lanes)
-            if (active && !flat) {
-                const unsigned long long g = *((volatile unsigned long long *)&p.best[rr]);
-                if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
-            }
-            for (int o = 1; o < p.n_iso; o <<= 1) {
-                const long long other = __shfl_xor_sync(FULL, vstar, o);
-                if (active && !flat) set_threshold(other);
-            }
-            named_sync(1, EPI_WARPS * 32);
+            // share the running best: other CTAs' results for this range (global keys, polled one tile
+            // ahead) and the other isometry rows of the same range (adjacent lanes)
+            if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
+            g = (active && !flat && t + 1 < ntiles) ? *((volatile unsigned long long *)&p.best[rr]) : ~0ull;
+            mbar_wait(&cfull[cbuf], (t >> 1) & 1);
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
-            for (int ch = 0; ch < BN / 2 / 32; ch++) {
-                const int col0 = half * (BN / 2) + ch * 32;
-                float c[32];
-                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + col0, c);
-                if (flat || !active) continue;
-                // level 1: continuous lower bound (2 FFMA + FMNMX per element)
-                float m = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const float4 k = sC[cbuf * BN + col0 + j];
-                    const float n1 = fmaf(-k.x, sr_n, c[j]);          // N / n (fp32, |err| <= 2)
-                    m = fmaxf(m, fmaf(-scl, k.y, fabsf(n1)));
+            if ((t & 3) == 0) {
+                for (int o = 1; o < p.n_iso; o <<= 1) {
+                    const long long other = __shfl_xor_sync(FULL, vstar, o);
+                    if (active && !flat) set_threshold(other);
                 }
-                if (m < -slack) continue;
-                // level 2: quantised value in fp32 at the two odd k2 around the vertex; level 3: exact
-                const float vthr = (float)vstar;
-#pragma unroll 4
-                for (int j = 0; j < 32; j++) {
-                    const float4 k = sC[cbuf * BN + col0 + j];
+            }
+            for (int ch = 0; ch < BN / 2 / CH; ch++) {
+                const int col0 = half * (BN / 2) + ch * CH;
+                float c[CH];
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MH + mh) * BN + col0, c);
+#ifdef TC_EXP
+                if (TC_EXP == 2) continue;
+#endif
+                const bool live = active && !flat;
+                // level 1: continuous lower bound, 2 FFMA + FMNMX per element
+                float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent max chains
+                const float4 *l4 = reinterpret_cast<const float4 *>(&sL[cbuf * BN + col0]);
+#pragma unroll
+                for (int j = 0; j < CH; j += 2) {
+                    const float4 k = l4[j >> 1];  // (Sq, sqrt D) of columns j, j+1
+                    const float n1a = fmaf(-k.x, sr_n, c[j]), n1b = fmaf(-k.z, sr_n, c[j + 1]);
+                    mm[(j >> 1) & 3] = fmaxf(mm[(j >> 1) & 3], fmaxf(fmaf(-scl, k.y, fabsf(n1a)), fmaf(-scl, k.w, fabsf(n1b))));
+                }
+                const bool chunk_pass = live && fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])) >= -slack;
+#ifdef MNS_TC_STATS
+                if (lane == 0) atomicAdd(&g_tc_stats[0], 1ull);
+#endif
+                if (!__any_sync(FULL, chunk_pass)) continue;  // the common case: nobody can win here
+#ifdef MNS_TC_STATS
+                if (lane == 0) atomicAdd(&g_tc_stats[1], 1ull);
+#endif
+#ifdef TC_EXP
+                if (TC_EXP == 1) { if (mm[0] == 12345.f) best = 0; continue; }
+#endif
+                // level 2 per column, only for the (lane, column) pairs that pass level 1: a rigorous
+                // lower bound of the quantised value over every odd k2 with |n1 - N/n| <= err; level 3: exact
+#pragma unroll
+                for (int j = 0; j < CH; j++) {
+                    const float2 k = sL[cbuf * BN + col0 + j];
                     const float n1 = fmaf(-k.x, sr_n, c[j]);
-                    if (fmaf(-scl, k.y, fabsf(n1)) < -slack) continue;
-                    const float tv = n1 * k.w;  // 32 N / D
-                    const float mf = fminf(3.f, fmaxf(-4.f, rintf(fmaf(tv, 0.5f, -0.5f))));
-                    const float k2a = fmaf(2.f, mf, 1.f);
-                    const float k2b = fminf(7.f, fmaxf(-7.f, tv > k2a ? k2a + 2.f : k2a - 2.f));
-                    const float va = k2a * fmaf(k2a, k.z, n64 * n1), vb = k2b * fmaf(k2b, k.z, n64 * n1);
-                    const float vt = fminf(va, vb);
-                    const float margin = 131072.f + 1e-5f * (fabsf(vt) + 49.f * k.z);
-                    // the vertex estimate is off by <= 2 * 32n/D (n1 error <= 2): trust it only when tight
-                    if (vstar != LLONG_MAX && k.w < 0.1f && vt - margin > vthr) continue;
-                    const long long d = dbase + col0 + j;
+                    const bool pj = chunk_pass && fmaf(-scl, k.y, fabsf(n1)) >= -slack;
+                    if (!__any_sync(FULL, pj)) continue;
+                    if (!pj) continue;
+#ifdef MNS_TC_STATS
+                    atomicAdd(&g_tc_stats[2], 1ull);
+#endif
+                    const long long Dx = sD[cbuf * BN + col0 + j];
+                    const float Df = (float)Dx;
+                    const float a = n64 * n1, eb = -n64 * err;
+                    float vlb = INFINITY;
+#pragma unroll
+                    for (int k2i = -7; k2i <= 7; k2i += 2) {
+                        const float k2 = (float)k2i;
+                        vlb = fminf(vlb, fmaf(k2, fmaf(k2, Df, a), -fabsf(k2) * eb));
+                    }
+                    const float margin = 1024.f + 1e-5f * (fabsf(vlb) + 49.f * Df + fabsf(a) * 7.f);
+                    if (vstar != LLONG_MAX && vlb - margin > (float)vstar) continue;
+#ifdef MNS_TC_STATS
+                    atomicAdd(&g_tc_stats[3], 1ull);
+#endif
+                    const long long d = (dbase + col0 + j) * p.dstride;
                     if (d >= p.ndom) continue;
-                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)p.psq[d] * sr;
-                    const long long v = best_val_exact(N, p.pD[d]);
+                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)(int)k.x * sr;  // exact
+                    const long long v = best_val_exact(N, Dx);
                     const unsigned long long key = make_key(v, d * p.n_iso + iso);
                     if (key < best) {
                         best = key;
@@ -289,7 +347,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                mbar_arrive(&tempty[acc]);
+                mbar_arrive(&cempty[cbuf]);
+            }
         }
         if (active) atomicMin(&p.best[rr], flat ? *p.flat_key : best);
     }
@@ -297,21 +358,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
 }
 
 // ---- operand preparation
 __global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
-                                long long ndom_pad, int n, __half *Q, float4 *consts) {
-    for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndom_pad;
-         d += (long long)gridDim.x * blockDim.x) {
-        for (int k = 0; k < BK; k++)
+                                long long ndom_pad, int n, __half *Q, float2 *consts) {
+    const int lane = threadIdx.x & 31;  // one warp per domain: coalesced 128-byte fp16 rows
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long d = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); d < ndom_pad; d += warps) {
+        for (int k = lane; k < BK; k += 32)
             Q[d * BK + k] = __float2half_rn(d < ndom && k < n ? (float)pool[d * n + k] : 0.f);
-        const float Df = d < ndom ? (float)pD[d] : 0.f;
-        consts[d] = d < ndom ? make_float4((float)psq[d], __fsqrt_rd(__ll2float_rd(pD[d])), Df,
-                                           Df > 0.f ? 32.f * (float)n / Df : 0.f)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane == 0)
+            consts[d] = d < ndom ? make_float2((float)psq[d], __fsqrt_rd(__ll2float_rd(pD[d]))) : make_float2(0.f, 0.f);
     }
 }
 
@@ -320,26 +380,33 @@ __global__ void range_rows_kernel(const uint8_t *img, int W, int B, int n_iso, i
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n_rows_pad) return;
     const int n = B * B;
-    if (row >= n_rows) {
-        for (int k = 0; k < BK; k++) A[(size_t)row * BK + k] = __float2half_rn(0.f);
-        row_sr[row] = 0;
-        row_flat[row] = 1;
-        return;
-    }
-    const int ri = r0 + row / n_iso, t = row % n_iso, rpr = W / B;
-    const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
     float v[BK];
     for (int k = 0; k < BK; k++) v[k] = 0.f;
     int sr = 0, srr = 0;
-    for (int e = 0; e < n; e++) {
-        const int r = img[(size_t)(ry + e / B) * W + rx + e % B];
-        v[iso_src(t, e / B, e % B, B)] = (float)r;  // row[src_t(e)] = r(e)
-        sr += r;
-        srr += r * r;
+    if (row < n_rows) {
+        const int ri = r0 + row / n_iso, t = row % n_iso, rpr = W / B;
+        const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
+        for (int e = 0; e < n; e++) {
+            const int r = img[(size_t)(ry + e / B) * W + rx + e % B];
+            v[iso_src(t, e / B, e % B, B)] = (float)r;  // row[src_t(e)] = r(e)
+            sr += r;
+            srr += r * r;
+        }
     }
     for (int k = 0; k < BK; k++) A[(size_t)row * BK + k] = __float2half_rn(v[k]);
     row_sr[row] = sr;
-    row_flat[row] = ((long long)n * srr - (long long)sr * sr) == 0;
+    row_flat[row] = row >= n_rows || ((long long)n * srr - (long long)sr * sr) == 0;
+}
+
+// prepass column constants: every `stride`-th domain, contiguous, zero-padded
+__global__ void gather_sample_kernel(const float2 *consts, const long long *pD, long long ndom, int stride,
+                                     long long nsample_pad, float2 *cs, long long *ds) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsample_pad;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long d = i * stride;
+        cs[i] = d < ndom ? consts[d] : make_float2(0.f, 0.f);
+        ds[i] = d < ndom ? pD[d] : 0;
+    }
 }
 
 __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, unsigned long long *key) {
@@ -358,11 +425,20 @@ __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, 
 
 }  // namespace
 
+#ifdef MNS_TC_STATS
+extern "C" void mns_tc_stats(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_tc_stats, sizeof(g_tc_stats));
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_tc_stats, z, sizeof(z));
+}
+#endif
+
 int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso) {
     const long long ndx = (W - 2 * B) / step + 1, ndy = (H - 2 * B) / step + 1, ndom = ndx * ndy;
     const long long ndom_pad = (ndom + BN - 1) / BN * BN;
-    const long long rows_pad = ((long long)(W / B) * (H / B) * n_iso + BM - 1) / BM * BM;
-    return ndom_pad * BK * 2 + ndom_pad * 16 + rows_pad * BK * 2 + rows_pad * 8 + 1024;
+    const long long rows_pad = ((long long)(W / B) * (H / B) * n_iso + MH * BM - 1) / (MH * BM) * (MH * BM);
+    const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
+    return ndom_pad * BK * 2 + ndom_pad * 8 + rows_pad * BK * 2 + rows_pad * 8 + nsample_pad * 16 + 2048;
 }
 
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
@@ -373,29 +449,40 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     const int n = B * B;
     const long long ndom_pad = (ndom + BN - 1) / BN * BN;
     const int n_rows = (r1 - r0) * n_iso;
-    const int n_rows_pad = (n_rows + BM - 1) / BM * BM;
+    const int n_rows_pad = (n_rows + MH * BM - 1) / (MH * BM) * (MH * BM);
     char *q = (char *)tc_ws;
     __half *Q = (__half *)q;
     q += ndom_pad * BK * 2;
-    float4 *consts = (float4 *)q;
-    q += ndom_pad * 16;
+    float2 *consts = (float2 *)q;
+    q += ndom_pad * 8;
     __half *A = (__half *)q;
     q += (long long)n_rows_pad * BK * 2;
     int32_t *row_sr = (int32_t *)q;
     q += (long long)n_rows_pad * 4;
     int32_t *row_flat = (int32_t *)q;
     q += (long long)n_rows_pad * 4;
+    q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+    const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
+    float2 *cons_s = (float2 *)q;
+    q += nsample_pad * 8;
+    long long *pD_s = (long long *)q;
+    q += nsample_pad * 8;
     unsigned long long *fkey = (unsigned long long *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
 
-    pool_f16_kernel<<<296, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
+    pool_f16_kernel<<<148 * 16, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
     range_rows_kernel<<<(n_rows_pad + 127) / 128, 128, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, A, row_sr,
                                                                  row_flat);
     MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
     flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
 
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmS;
+    constexpr int SAMPLE = 128;  // prepass: every 128th domain seeds each row's best (strided TMA view)
+    const long long nsample = (ndom + SAMPLE - 1) / SAMPLE;
     if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
     if (encode_tmap_2d_swizzled(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, ndom_pad, BK * 2, BK, BN)) return -1;
+    if (encode_tmap_2d_swizzled(&tmS, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, nsample, (uint64_t)BK * 2 * SAMPLE, BK,
+                                BN))
+        return -1;
 
     TcParams p{};
     p.n_rows = n_rows;
@@ -403,10 +490,7 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     p.r0 = r0;
     p.n = n;
     p.ndom = ndom;
-    p.n_dtiles = (int)(ndom_pad / BN);
-    p.dtiles_per_chunk = 24;
     p.consts = consts;
-    p.psq = psq;
     p.pD = pD;
     p.row_sr = row_sr;
     p.row_flat = row_flat;
@@ -418,7 +502,20 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
                                           SMEM_BYTES));
         attr_set = true;
     }
-    dim3 grid((p.n_dtiles + p.dtiles_per_chunk - 1) / p.dtiles_per_chunk, n_rows_pad / BM);
+    if (ndom >= 16 * SAMPLE) {  // prepass over the sample
+        gather_sample_kernel<<<64, 256, 0, st>>>(consts, pD, ndom, SAMPLE, nsample_pad, cons_s, pD_s);
+        TcParams q = p;
+        q.consts = cons_s;
+        q.pD = pD_s;
+        q.dstride = SAMPLE;
+        q.n_dtiles = (int)((nsample + BN - 1) / BN);
+        q.dtiles_per_chunk = q.n_dtiles;  // one CTA per M tile: a single cold start per row
+        full_search_tc_kernel<<<dim3(1, n_rows_pad / (MH * BM)), NTHREADS, SMEM_BYTES, st>>>(tmA, tmS, q);
+    }
+    p.dstride = 1;
+    p.n_dtiles = (int)(ndom_pad / BN);
+    p.dtiles_per_chunk = 48;
+    dim3 grid((p.n_dtiles + p.dtiles_per_chunk - 1) / p.dtiles_per_chunk, n_rows_pad / (MH * BM));
     full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
     MNS_CUDA_TRY(cudaGetLastError());
     *handled = true;

@@ -220,3 +220,34 @@ def test_write_stream_matches_reference_layout(mns, golden):
         data = bitstream.write_stream(code)
         assert data == bytes(g[f"{k}/stream"]), case
         assert bitstream.stream_bit_count(code) == int(g[f"{k}/stream_bits"])
+
+
+def test_full_search_tensor_core_matches_exact_cuda_core_path(mns, monkeypatch):
+    """tcgen05 path vs the exact CUDA-core path, incl. the fp16/fp32 worst case (saturated image)."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    cases = [(np.ascontiguousarray(synth_image(512, 4)[64:192, 128:256]), 8, 8),
+             (np.ascontiguousarray(synth_image(512, 9)[:96, :96]), 4, 8),
+             (np.full((64, 64), 255, np.uint8), 8, 1),
+             (np.random.default_rng(2).integers(250, 256, (64, 64), dtype=np.uint8), 8, 8)]
+    for px, B, n_iso in cases:
+        img = torch.from_numpy(px).cuda()
+        monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "0")
+        a = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, 1, n_iso).items()}
+        monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "1")
+        b = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, 1, n_iso).items()}
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (px.shape, B, n_iso, k)
+
+
+def test_full_search_c4_sample_vs_oracle(mns):
+    """c4 (512^2, B=8, stride 1, 247,009 domains): GPU vs the oracle on a strided sample of ranges."""
+    from paper_1501_02894_b200.synth import config_image
+
+    px = config_image("c4")
+    res = mns.full_search_device(torch.from_numpy(px).cuda(), 8, 1, 1)
+    dom = res["dom"].cpu().numpy()
+    ids = np.arange(0, 4096, 97)
+    ref = O.full_search(px, 8, 1, n_iso=1, range_ids=ids)
+    assert np.array_equal(dom[ids], ref["dom"])
+    assert np.array_equal(res["code"].cpu().numpy()[ids], ref["code"])
