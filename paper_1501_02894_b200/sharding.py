@@ -80,8 +80,9 @@ class StripDecoder:
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
 
-    def run(self, iters: int = 10, initial_value: float = 128.0, stream=None, sweep_events=None):
-        """iters sweeps (stop_delta = 0); the last writes the rounded uint8 strip into self.out."""
+    def run(self, iters: int = 10, initial_value: float = 128.0, stream=None, sweep_events=None, out=None):
+        """iters sweeps (stop_delta = 0); the last writes the rounded uint8 strip into `out` (default self.out)."""
+        out = self.out if out is None else out
         from . import _native as N
 
         L = N.lib()
@@ -97,10 +98,10 @@ class StripDecoder:
                                        self._vbase(cur, self.y_lo, 4) if cur is not None else ctypes.c_void_p(0),
                                        float(initial_value),
                                        self._vbase(nxt, self.y_lo, 4) if nxt is not None else ctypes.c_void_p(0),
-                                       self._vbase(self.out, 16 * self.r0, 1) if last else ctypes.c_void_p(0),
+                                       self._vbase(out, 16 * self.r0, 1) if last else ctypes.c_void_p(0),
                                        N.ptr(self.state), 0.0, s))
             if sweep_events is not None:
                 sweep_events[it][1].record()
             if not last and self.world > 1:
                 exchange_halos(nxt, self.r0, self.r1, self.H, self.rank, self.world)
-        return self.out
+        return out
