@@ -45,6 +45,15 @@ ITERS = 10
 METRIC = "range blocks encoded/sec (MNS) and Mpixel/s decoded; full-search pair-evals/s"
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return int(json.load(f)[kernel]["per_launch_bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -312,7 +321,9 @@ def run_ours(args, img_np, rank, world, local_rank):
                        "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
                        "sweep_ms": sweep_ms, "leaves_rank0": n_leaves, "full_search": fs},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None, "kernel": "decode_sweep_kernel (steady-state sweep)", "peak_source": which},
+                     "traffic": measured_traffic("decode_sweep_kernel") if world == 1 else None,
+                     "algorithmic_bytes": algo, "kernel": "decode_sweep_kernel (steady-state sweep)",
+                     "peak_source": which},
         "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
                           "sample": f"c5 rows 0..{args.cpu_rows - 1} encoded + {ITERS}-sweep decoded as its own "
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
