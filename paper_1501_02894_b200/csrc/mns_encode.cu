@@ -35,13 +35,12 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int EW = 8;                // warps per CTA
 constexpr int ET = EW * 32;
-constexpr int RPW = 4;               // roots encoded by each warp per tile (in turn)
+constexpr int RPW = 2;               // roots encoded by each warp per tile (in turn)
 constexpr int TR = EW * RPW;         // 32 consecutive roots of one root row per tile
 constexpr int WIN_W = TR * 16 + 32;  // 544
 constexpr int WIN_H = 48;
 constexpr int QE_W = WIN_W / 2;      // 272
 constexpr int QE_H = WIN_H / 2;      // 24
-constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + EW * 2 * 64 * 8 + TR * 64 * 8;
 
 struct EncParams {
     const uint8_t *img;
@@ -164,15 +163,101 @@ __device__ __forceinline__ Node2 p2_node(int nlog2, int sr, int s0, int s1, int 
     return z;
 }
 
-__global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
+// ---- node geometry inside a 16x16 root (Morton order = reference DFS order)
+__device__ __forceinline__ int node2_x(int k) { return 8 * (k & 1); }
+__device__ __forceinline__ int node2_y(int k) { return 8 * (k >> 1); }
+__device__ __forceinline__ int node3_x(int m) { return node2_x(m >> 2) + 4 * (m & 1); }
+__device__ __forceinline__ int node3_y(int m) { return node2_y(m >> 2) + 4 * ((m >> 1) & 1); }
+__device__ __forceinline__ int node4_x(int c) { return node3_x(c >> 2) + 2 * (c & 1); }
+__device__ __forceinline__ int node4_y(int c) { return node3_y(c >> 2) + 2 * ((c >> 1) & 1); }
+
+// Shared-memory layout of one tile (32 roots); moments and decisions are per node.
+struct TileSmem {
+    Mom m1[TR];
+    Mom m2[TR][4];
+    Mom m3[TR][16];
+    int sr4[TR][64], srr4[TR][64];  // level-4 range sums (q moments are computed lazily)
+    uint64_t rec1[TR], rec2[TR][4], rec3[TR][16], rec4[TR][64];
+    uint8_t acc1[TR], acc2[TR][4], acc3[TR][16];
+    int root_cnt[TR];
+    long long root_base[TR];
+};
+constexpr int TILE_SMEM = (int)sizeof(TileSmem);
+constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + TR * 64 * 8 + TILE_SMEM + 64;
+
+struct Win {  // the staged window and the tile/image geometry a decision thread needs
+    const uint8_t (*pix)[WIN_W];
+    const uint16_t (*qe)[QE_W];
+    int x0, y0, wx0, wy0, W, H;
+};
+
+// q of pixel (py, px) (root-relative) against the co-centred domain of node (nx, ny, s) of root slot
+__device__ __forceinline__ int dom_q(const Win &w, int slot, int nx, int ny, int s, int px, int py) {
+    const int rxg = w.x0 + 16 * slot, ryg = w.y0;
+    const int gdx = clampi(rxg + nx - s / 2, 0, w.W - 2 * s), gdy = clampi(ryg + ny - s / 2, 0, w.H - 2 * s);
+    const int wx = gdx - w.wx0 + 2 * (px - nx), wy = gdy - w.wy0 + 2 * (py - ny);
+    if (((wx | wy) & 1) == 0) return w.qe[wy >> 1][wx >> 1];
+    const uint8_t *pp = &w.pix[wy][wx];
+    return (int)pp[0] + pp[1] + pp[WIN_W] + pp[WIN_W + 1];
+}
+
+__device__ __forceinline__ int pixel(const Win &w, int slot, int px, int py) {
+    return w.pix[16 + py][16 + 16 * slot + px];
+}
+
+// Reference-order emulation of one phase-2 quadrant (transform.py:69-80 rms_error) -- the
+// quadrant is the child (cx, cy, cs) of a node at `level`; the domain is the child's own.
+// Returns 1 accept / 0 reject and the chosen bit.
+__device__ int emulate_quadrant(const Win &w, int slot, int cx, int cy, int cs, const Mom &m, int t, double slo,
+                                double shi, double tol, int &bit) {
+    double lo[64], hi[64];
+    const int n = cs * cs;
+    const double dm = ((double)m.sq * 0.25) / (double)n;
+    const double td = (double)t;
+    for (int i = 0; i < cs; i++)
+        for (int j = 0; j < cs; j++) {
+            const int q = dom_q(w, slot, cx, cy, cs, cx + j, cy + i);
+            const int r = pixel(w, slot, cx + j, cy + i);
+            lo[i * cs + j] = emu_sq(r, q, dm, slo, td);
+            hi[i * cs + j] = emu_sq(r, q, dm, shi, td);
+        }
+    const double rlo = __dsqrt_rn(pw_sum_dev(lo, n) / (double)n), rhi = __dsqrt_rn(pw_sum_dev(hi, n) / (double)n);
+    bit = rlo <= rhi ? 0 : 1;
+    return ((bit ? rhi : rlo) > tol) ? 0 : 1;
+}
+
+// Phase 2 of node (nx, ny, size) at `level` from its own Sr and its 4 children's moments
+// (encoder.py:169-212).  Returns true with *rec on acceptance.
+__device__ bool phase2_node(const Win &w, const EncParams &p, int slot, int level, int nx, int ny, int size, int sr,
+                            const Mom *kids, uint64_t *rec) {
+    const int nlog2 = 2 * (5 - level);  // node pixels: 256, 64, 16
+    const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
+                            p.mean_tol);
+    if (!z.pass) return false;
+    const double slo = level == 1 ? 0.2 : (level == 2 ? 0.4 : 0.5);
+    const double shi = level == 1 ? 0.5 : (level == 2 ? 0.65 : 0.9);
+    const int h = size / 2;
+    const double bnd_n = p.p2b[level] * (double)(h * h);
+    int bits = 0;
+    for (int k = 0; k < 4; k++) {
+        int bit;
+        int res = p2_quad(nlog2 - 2, kids[k], z.t[k], slo, shi, bnd_n, bit);
+        if (res == 2)
+            res = emulate_quadrant(w, slot, nx + (k & 1) * h, ny + (k >> 1) * h, h, kids[k], z.t[k], slo, shi,
+                                   p.tol[level], bit);
+        if (res != 1) return false;
+        bits |= bit << k;
+    }
+    *rec = mns_rec_phase2(w.x0 + 16 * slot + nx, w.y0 + ny, level, z.o, z.d0, z.d1, z.d2, bits);
+    return true;
+}
+
+__global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const EncParams p) {
     extern __shared__ __align__(16) unsigned char esm[];
     uint64_t(*stage)[64] = reinterpret_cast<uint64_t(*)[64]>(esm);  // per-root records, DFS order
-    double(*scratch)[2][64] = reinterpret_cast<double(*)[2][64]>(esm + TR * 64 * 8);
-    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TR * 64 * 8 + EW * 2 * 64 * 8);
-    uint16_t(*qe)[QE_W] =
-        reinterpret_cast<uint16_t(*)[QE_W]>(esm + TR * 64 * 8 + EW * 2 * 64 * 8 + WIN_H * WIN_W);
-    __shared__ int root_cnt[TR];
-    __shared__ long long root_base[TR];
+    TileSmem &ts = *reinterpret_cast<TileSmem *>(esm + TR * 64 * 8);
+    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TR * 64 * 8 + TILE_SMEM);
+    uint16_t(*qe)[QE_W] = reinterpret_cast<uint16_t(*)[QE_W]>(esm + TR * 64 * 8 + TILE_SMEM + WIN_H * WIN_W);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long tile = blockIdx.x;
@@ -185,11 +270,12 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     const uint8_t *img = p.img + (size_t)img_i * p.image_stride;
     const int x0 = rx0 * 16, y0 = ry * 16;
     const int wx0 = x0 - 16, wy0 = y0 - 16;
+    const Win w{pix, qe, x0, y0, wx0, wy0, p.W, p.H};
 
     // ---- K1a: stage the pixel window (16-byte coalesced loads, zero outside the image)
-    constexpr int CH = WIN_W / 16;
-    for (int c = tid; c < WIN_H * CH; c += ET) {
-        const int wr = c / CH, wc = (c % CH) * 16;
+    constexpr int CHK = WIN_W / 16;
+    for (int c = tid; c < WIN_H * CHK; c += ET) {
+        const int wr = c / CHK, wc = (c % CHK) * 16;
         const int gy = wy0 + wr, gx = wx0 + wc;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (gy >= 0 && gy < p.H && gx >= 0 && gx < p.W)
@@ -209,327 +295,196 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     }
     __syncthreads();
 
-    // ---- each warp encodes roots warp, warp + 8, ... of the tile: K1c moments + K2 decisions
-    for (int rr = 0; rr < RPW; rr++) {
-    const int slot = rr * EW + warp;
-    if (slot >= nr) break;
-    uint64_t recA = 0, recB = 0;
-    bool hasA = false, hasB = false;
-    uint32_t umap = 0;
+    const bool try1 = p.root_level == 1 && p.min_dim >= 32;  // encoder.py:231 guard 2*size <= min_dim
+    // ---- K1c: pixel-parallel block moments of every level-1..3 node (lane = 2x4 pixel block)
     {
-        const int rxg = x0 + slot * 16, ryg = y0;
-        const int wrx = 16 + slot * 16, wry = 16;
         const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
-        const int ax = (a & 1) * 8, ay = (a >> 1) * 8, bx = (b & 1) * 4, by = (b >> 1) * 4;
-        const int lx = ax + bx, ly = ay + by + 2 * c;  // lane's 2x4 pixel block (root-relative)
-        const int W = p.W, H = p.H;
-
-        int r[8];
-        {
-            const uint32_t w0 = *reinterpret_cast<const uint32_t *>(&pix[wry + ly][wrx + lx]);
-            const uint32_t w1 = *reinterpret_cast<const uint32_t *>(&pix[wry + ly + 1][wrx + lx]);
+        const int lx = node3_x(4 * a + b), ly = node3_y(4 * a + b) + 2 * c;
+        for (int slot = warp; slot < nr; slot += EW) {
+            const int wrx = 16 + 16 * slot;
+            int r[8];
+            const uint32_t w0 = *reinterpret_cast<const uint32_t *>(&pix[16 + ly][wrx + lx]);
+            const uint32_t w1 = *reinterpret_cast<const uint32_t *>(&pix[16 + ly + 1][wrx + lx]);
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 r[j] = (w0 >> (8 * j)) & 0xFF;
                 r[4 + j] = (w1 >> (8 * j)) & 0xFF;
             }
+            const int srL = r[0] + r[1] + r[4] + r[5], srR = r[2] + r[3] + r[6] + r[7];
+            const int srrL = r[0] * r[0] + r[1] * r[1] + r[4] * r[4] + r[5] * r[5];
+            const int srrR = r[2] * r[2] + r[3] * r[3] + r[6] * r[6] + r[7] * r[7];
+            ts.sr4[slot][2 * lane] = srL;
+            ts.sr4[slot][2 * lane + 1] = srR;
+            ts.srr4[slot][2 * lane] = srrL;
+            ts.srr4[slot][2 * lane + 1] = srrR;
+            // partial q-moments of this lane's 8 pixels against the domain of node (nx, ny, s)
+            auto part = [&](int nx, int ny, int s, int &sq, int &sqq, int &sqr) {
+                const int gdx = clampi(x0 + 16 * slot + nx - s / 2, 0, p.W - 2 * s);
+                const int gdy = clampi(y0 + ny - s / 2, 0, p.H - 2 * s);
+                const int qr = (gdy - wy0) / 2 + (ly - ny), qc = (gdx - wx0) / 2 + (lx - nx);
+                sq = sqq = sqr = 0;
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const int q = qe[qr + i][qc + j];
+                        sq += q;
+                        sqq += q * q;
+                        sqr += q * r[4 * i + j];
+                    }
+            };
+            int v[5];  // sr, srr, sq, sqq, sqr
+            // level 3 (lane pairs)
+            v[0] = srL + srR;
+            v[1] = srrL + srrR;
+            part(lx, ly - 2 * c, 4, v[2], v[3], v[4]);
+#pragma unroll
+            for (int k = 0; k < 5; k++) v[k] += __shfl_xor_sync(FULL, v[k], 1);
+            if (c == 0) ts.m3[slot][4 * a + b] = Mom{v[0], v[1], v[2], v[3], v[4]};
+            // level 2 (8-lane groups)
+            v[0] = srL + srR;
+            v[1] = srrL + srrR;
+            part(node2_x(a), node2_y(a), 8, v[2], v[3], v[4]);
+#pragma unroll
+            for (int k = 0; k < 5; k++) {
+                v[k] += __shfl_xor_sync(FULL, v[k], 1);
+                v[k] += __shfl_xor_sync(FULL, v[k], 2);
+                v[k] += __shfl_xor_sync(FULL, v[k], 4);
+            }
+            if ((lane & 7) == 0) ts.m2[slot][a] = Mom{v[0], v[1], v[2], v[3], v[4]};
+            // level 1 (whole warp)
+            v[0] = srL + srR;
+            v[1] = srrL + srrR;
+            if (try1) {
+                part(0, 0, 16, v[2], v[3], v[4]);
+            } else {
+                v[2] = v[3] = v[4] = 0;
+            }
+#pragma unroll
+            for (int k = 0; k < 5; k++) v[k] = __reduce_add_sync(FULL, v[k]);
+            if (lane == 0) ts.m1[slot] = Mom{v[0], v[1], v[2], v[3], v[4]};
         }
-        Mom m4L, m4R;
-        m4L.sr = r[0] + r[1] + r[4] + r[5];
-        m4R.sr = r[2] + r[3] + r[6] + r[7];
-        m4L.srr = r[0] * r[0] + r[1] * r[1] + r[4] * r[4] + r[5] * r[5];
-        m4R.srr = r[2] * r[2] + r[3] * r[3] + r[6] * r[6] + r[7] * r[7];
-        Mom m3, m2, m1;  // range sums of the lane's level-3 / level-2 / level-1 node
-        m3.sr = m4L.sr + m4R.sr;
-        m3.srr = m4L.srr + m4R.srr;
-        m3.sr += __shfl_xor_sync(FULL, m3.sr, 1);
-        m3.srr += __shfl_xor_sync(FULL, m3.srr, 1);
-        m2.sr = m3.sr + __shfl_xor_sync(FULL, m3.sr, 2);
-        m2.srr = m3.srr + __shfl_xor_sync(FULL, m3.srr, 2);
-        m2.sr += __shfl_xor_sync(FULL, m2.sr, 4);
-        m2.srr += __shfl_xor_sync(FULL, m2.srr, 4);
-        m1.sr = m2.sr + __shfl_xor_sync(FULL, m2.sr, 8);
-        m1.srr = m2.srr + __shfl_xor_sync(FULL, m2.srr, 8);
-        m1.sr += __shfl_xor_sync(FULL, m1.sr, 16);
-        m1.srr += __shfl_xor_sync(FULL, m1.srr, 16);
+    }
+    __syncthreads();
 
-        // even-phase moments of this lane's 8 pixels against the domain of node (nx, ny, s)
-        auto even_moments = [&](int nx, int ny, int s, Mom &m) {
-            const int gdx = clampi(rxg + nx - s / 2, 0, W - 2 * s);
-            const int gdy = clampi(ryg + ny - s / 2, 0, H - 2 * s);
-            const int qr = (gdy - wy0) / 2 + (ly - ny), qc = (gdx - wx0) / 2 + (lx - nx);
-            int sq = 0, sqq = 0, sqr = 0;
-#pragma unroll
-            for (int i = 0; i < 2; i++)
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const int q = qe[qr + i][qc + j];
-                    sq += q;
-                    sqq += q * q;
-                    sqr += q * r[4 * i + j];
-                }
-            m.sq = sq;
-            m.sqq = sqq;
-            m.sqr = sqr;
-        };
-        auto even_q = [&](int nx, int ny, int s, int i, int j) -> int {
-            const int gdx = clampi(rxg + nx - s / 2, 0, W - 2 * s);
-            const int gdy = clampi(ryg + ny - s / 2, 0, H - 2 * s);
-            return qe[(gdy - wy0) / 2 + (ly - ny) + i][(gdx - wx0) / 2 + (lx - nx) + j];
-        };
-        // level-4 node at (nx, ly): 2x2 range, 4x4 domain (odd phase in the interior)
-        auto l4_q = [&](int nx, int i, int j) -> int {
-            const int gdx = clampi(rxg + nx - 1, 0, W - 4), gdy = clampi(ryg + ly - 1, 0, H - 4);
-            const uint8_t *pp = &pix[gdy - wy0 + 2 * i][gdx - wx0 + 2 * j];
-            return (int)pp[0] + pp[1] + pp[WIN_W] + pp[WIN_W + 1];
-        };
-        auto l4_moments = [&](int nx, int ro, Mom &m) {
-            int sq = 0, sqq = 0, sqr = 0;
-#pragma unroll
-            for (int i = 0; i < 2; i++)
-#pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    const int q = l4_q(nx, i, j);
-                    sq += q;
-                    sqq += q * q;
-                    sqr += q * r[4 * i + ro + j];
-                }
-            m.sq = sq;
-            m.sqq = sqq;
-            m.sqr = sqr;
-        };
-
-        const bool mns = p.mns != 0;
-        const bool vis1 = p.root_level == 1;
-        const bool try1 = vis1 && p.min_dim >= 32;  // encoder.py:231 guard 2*size <= min_dim
-        bool acc1 = false;
-        uint64_t rec1 = 0;
+    // ---- K2: node-parallel decisions, level by level (one thread per node)
+    const bool mns = p.mns != 0;
+    if (tid < nr) {  // level 1: one thread per root
+        const int s = tid;
+        bool acc = false;
+        uint64_t rec = 0;
         if (try1) {
-            even_moments(0, 0, 16, m1);
-            m1.sq = xsum(m1.sq, 32);
-            m1.sqq = xsum(m1.sqq, 32);
-            m1.sqr = xsum(m1.sqr, 32);
-            rec1 = phase1(rxg, ryg, 1, 8, m1, p.p1b[1], acc1);
+            rec = phase1(x0 + 16 * s, y0, 1, 8, ts.m1[s], p.p1b[1], acc);
+            if (!acc && mns) acc = phase2_node(w, p, s, 1, 0, 0, 16, ts.m1[s].sr, ts.m2[s], &rec);
         }
-        // level-2 moments: needed unless the root was accepted by phase 1
-        if (!acc1) {
-            even_moments(ax, ay, 8, m2);
-            m2.sq = xsum(m2.sq, 8);
-            m2.sqq = xsum(m2.sqq, 8);
-            m2.sqr = xsum(m2.sqr, 8);
+        ts.acc1[s] = acc;
+        ts.rec1[s] = rec;
+    }
+    __syncthreads();
+    if (tid < 4 * nr) {  // level 2: one thread per node
+        const int s = tid >> 2, k = tid & 3;
+        const bool vis = p.root_level == 2 || !ts.acc1[s];
+        bool acc = false;
+        uint64_t rec = 0;
+        if (vis) {
+            const int nx = node2_x(k), ny = node2_y(k);
+            rec = phase1(x0 + 16 * s + nx, y0 + ny, 2, 6, ts.m2[s][k], p.p1b[2], acc);
+            if (!acc && mns) acc = phase2_node(w, p, s, 2, nx, ny, 8, ts.m2[s][k].sr, &ts.m3[s][4 * k], &rec);
         }
-        // ---- phase 2 at level 1 (node = root, quadrants = level-2 nodes)
-        if (try1 && !acc1 && mns) {
-            const Node2 z = p2_node(8, m1.sr, __shfl_sync(FULL, m2.sr, 0), __shfl_sync(FULL, m2.sr, 8),
-                                    __shfl_sync(FULL, m2.sr, 16), __shfl_sync(FULL, m2.sr, 24), 15, p.mean_tol);
-            if (z.pass) {  // warp-uniform
-                int bit;
-                int res = p2_quad(6, m2, z.t[a], 0.2, 0.5, p.p2b[1] * 64.0, bit);
-                unsigned amb = __ballot_sync(FULL, res == 2 && (lane & 7) == 0);
-                while (amb) {
-                    const int g = __ffs(amb) - 1;
-                    amb &= amb - 1;
-                    if ((lane >> 3) == (g >> 3)) {
-                        const double dm = ((double)m2.sq * 0.25) / 64.0;
-                        const double t = (double)z.t[a];
-#pragma unroll
-                        for (int i = 0; i < 2; i++)
-#pragma unroll
-                            for (int j = 0; j < 4; j++) {
-                                const int q = even_q(ax, ay, 8, i, j);
-                                const int idx = (by + 2 * c + i) * 8 + bx + j;
-                                scratch[warp][0][idx] = emu_sq(r[4 * i + j], q, dm, 0.2, t);
-                                scratch[warp][1][idx] = emu_sq(r[4 * i + j], q, dm, 0.5, t);
-                            }
-                    }
-                    __syncwarp();
-                    int rr = 0, bb = 0;
-                    if (lane == g) {
-                        const double rlo = __dsqrt_rn(pw_sum_dev(scratch[warp][0], 64) / 64.0);
-                        const double rhi = __dsqrt_rn(pw_sum_dev(scratch[warp][1], 64) / 64.0);
-                        bb = rlo <= rhi ? 0 : 1;
-                        rr = ((bb ? rhi : rlo) > p.tol[1]) ? 0 : 1;
-                    }
-                    rr = __shfl_sync(FULL, rr, g);
-                    bb = __shfl_sync(FULL, bb, g);
-                    if ((lane >> 3) == (g >> 3)) {
-                        res = rr;
-                        bit = bb;
-                    }
-                    __syncwarp();
-                }
-                if (__all_sync(FULL, res == 1)) {
-                    const int bits = __shfl_sync(FULL, bit, 0) | (__shfl_sync(FULL, bit, 8) << 1) |
-                                     (__shfl_sync(FULL, bit, 16) << 2) | (__shfl_sync(FULL, bit, 24) << 3);
-                    acc1 = true;
-                    rec1 = mns_rec_phase2(rxg, ryg, 1, z.o, z.d0, z.d1, z.d2, bits);
-                }
-            }
-        }
-
-        // ---- level 2
-        const bool vis2 = vis1 ? !acc1 : true;
-        bool acc2 = false;
-        uint64_t rec2 = 0;
-        if (vis2) rec2 = phase1(rxg + ax, ryg + ay, 2, 6, m2, p.p1b[2], acc2);
-        if (__any_sync(FULL, vis2 && !acc2)) {
-            even_moments(ax + bx, ay + by, 4, m3);
-            m3.sq = xsum(m3.sq, 2);
-            m3.sqq = xsum(m3.sqq, 2);
-            m3.sqr = xsum(m3.sqr, 2);
-        }
-        const bool try2p2 = mns && vis2 && !acc2;
-        if (__any_sync(FULL, try2p2)) {
-            const int gb = lane & ~7;
-            const Node2 z = p2_node(6, m2.sr, __shfl_sync(FULL, m3.sr, gb), __shfl_sync(FULL, m3.sr, gb + 2),
-                                    __shfl_sync(FULL, m3.sr, gb + 4), __shfl_sync(FULL, m3.sr, gb + 6), 31,
-                                    p.mean_tol);
-            const bool go = try2p2 && z.pass;
-            int bit = 0;
-            int res = go ? p2_quad(4, m3, z.t[b], 0.4, 0.65, p.p2b[2] * 16.0, bit) : 0;
-            unsigned amb = __ballot_sync(FULL, go && res == 2 && c == 0);
-            while (amb) {
-                const int g = __ffs(amb) - 1;
-                amb &= amb - 1;
-                if ((lane >> 1) == (g >> 1)) {
-                    const double dm = ((double)m3.sq * 0.25) / 16.0;
-                    const double t = (double)z.t[b];
-#pragma unroll
-                    for (int i = 0; i < 2; i++)
-#pragma unroll
-                        for (int j = 0; j < 4; j++) {
-                            const int q = even_q(ax + bx, ay + by, 4, i, j);
-                            const int idx = (2 * c + i) * 4 + j;
-                            scratch[warp][0][idx] = emu_sq(r[4 * i + j], q, dm, 0.4, t);
-                            scratch[warp][1][idx] = emu_sq(r[4 * i + j], q, dm, 0.65, t);
-                        }
-                }
-                __syncwarp();
-                int rr = 0, bb = 0;
-                if (lane == g) {
-                    const double rlo = __dsqrt_rn(pw_sum_dev(scratch[warp][0], 16) / 16.0);
-                    const double rhi = __dsqrt_rn(pw_sum_dev(scratch[warp][1], 16) / 16.0);
-                    bb = rlo <= rhi ? 0 : 1;
-                    rr = ((bb ? rhi : rlo) > p.tol[2]) ? 0 : 1;
-                }
-                rr = __shfl_sync(FULL, rr, g);
-                bb = __shfl_sync(FULL, bb, g);
-                if ((lane >> 1) == (g >> 1)) {
-                    res = rr;
-                    bit = bb;
-                }
-                __syncwarp();
-            }
-            const unsigned okm = __ballot_sync(FULL, res == 1);
-            const int bits = __shfl_sync(FULL, bit, gb) | (__shfl_sync(FULL, bit, gb + 2) << 1) |
-                             (__shfl_sync(FULL, bit, gb + 4) << 2) | (__shfl_sync(FULL, bit, gb + 6) << 3);
-            if (go && ((okm >> gb) & 0xFFu) == 0xFFu) {
-                acc2 = true;
-                rec2 = mns_rec_phase2(rxg + ax, ryg + ay, 2, z.o, z.d0, z.d1, z.d2, bits);
-            }
-        }
-
-        // ---- level 3
-        const bool vis3 = vis2 && !acc2;
-        bool acc3 = false;
-        uint64_t rec3 = 0;
-        if (vis3) rec3 = phase1(rxg + ax + bx, ryg + ay + by, 3, 4, m3, p.p1b[3], acc3);
-        if (__any_sync(FULL, vis3 && !acc3)) {
-            l4_moments(lx, 0, m4L);
-            l4_moments(lx + 2, 2, m4R);
-        }
-        const bool try3p2 = mns && vis3 && !acc3;
-        if (__any_sync(FULL, try3p2)) {
-            const int pb = lane & ~1;
-            const Node2 z = p2_node(4, m3.sr, __shfl_sync(FULL, m4L.sr, pb), __shfl_sync(FULL, m4R.sr, pb),
-                                    __shfl_sync(FULL, m4L.sr, pb + 1), __shfl_sync(FULL, m4R.sr, pb + 1), 31,
-                                    p.mean_tol);
-            const bool go = try3p2 && z.pass;
-            int bitL = 0, bitR = 0, resL = 0, resR = 0;
-            if (go) {
-                resL = p2_quad(2, m4L, z.t[2 * c], 0.5, 0.9, p.p2b[3] * 4.0, bitL);
-                resR = p2_quad(2, m4R, z.t[2 * c + 1], 0.5, 0.9, p.p2b[3] * 4.0, bitR);
-                // in-register emulation for ambiguous 2x2 quadrants (n = 4: sequential sum)
-                for (int side = 0; side < 2; side++) {
-                    int &res = side ? resR : resL;
-                    int &bit = side ? bitR : bitL;
-                    if (res != 2) continue;
-                    const Mom &m = side ? m4R : m4L;
-                    const int nx = lx + 2 * side;
-                    const double dm = ((double)m.sq * 0.25) / 4.0;
-                    const double t = (double)z.t[2 * c + side];
-                    double slo = 0.0, shi = 0.0;
+        ts.acc2[s][k] = acc;
+        ts.rec2[s][k] = rec;
+    }
+    __syncthreads();
+    for (int t = tid; t < 16 * nr; t += ET) {  // level 3 (and the level-4 quartets below it)
+        const int s = t >> 4, m = t & 15;
+        const bool vis = (p.root_level == 2 || !ts.acc1[s]) && !ts.acc2[s][m >> 2];
+        bool acc = false;
+        uint64_t rec = 0;
+        if (vis) {
+            const int nx = node3_x(m), ny = node3_y(m);
+            rec = phase1(x0 + 16 * s + nx, y0 + ny, 3, 4, ts.m3[s][m], p.p1b[3], acc);
+            if (!acc) {  // level-4 moments (odd-phase domains) of the 4 children, then phase 2 / split
+                Mom k4[4];
+                for (int c = 0; c < 4; c++) {
+                    const int cx = nx + 2 * (c & 1), cy = ny + 2 * (c >> 1);
+                    Mom mm{ts.sr4[s][4 * m + c], ts.srr4[s][4 * m + c], 0, 0, 0};
                     for (int i = 0; i < 2; i++)
                         for (int j = 0; j < 2; j++) {
-                            const int q = l4_q(nx, i, j);
-                            const int rv = r[4 * i + 2 * side + j];
-                            slo = __dadd_rn(slo, emu_sq(rv, q, dm, 0.5, t));
-                            shi = __dadd_rn(shi, emu_sq(rv, q, dm, 0.9, t));
+                            const int q = dom_q(w, s, cx, cy, 2, cx + j, cy + i);
+                            mm.sq += q;
+                            mm.sqq += q * q;
+                            mm.sqr += q * pixel(w, s, cx + j, cy + i);
                         }
-                    const double rlo = __dsqrt_rn(slo / 4.0), rhi = __dsqrt_rn(shi / 4.0);
-                    bit = rlo <= rhi ? 0 : 1;
-                    res = ((bit ? rhi : rlo) > p.tol[3]) ? 0 : 1;
+                    k4[c] = mm;
                 }
-            }
-            const bool lane_ok = resL == 1 && resR == 1;
-            const int partner_ok = __shfl_xor_sync(FULL, (int)lane_ok, 1);  // every lane must shuffle
-            const bool pair_ok = lane_ok && partner_ok;
-            int lbits = (bitL << (2 * c)) | (bitR << (2 * c + 1));
-            lbits |= __shfl_xor_sync(FULL, lbits, 1);
-            if (go && pair_ok) {
-                acc3 = true;
-                rec3 = mns_rec_phase2(rxg + ax + bx, ryg + ay + by, 3, z.o, z.d0, z.d1, z.d2, lbits);
+                if (mns) acc = phase2_node(w, p, s, 3, nx, ny, 4, ts.m3[s][m].sr, k4, &rec);
+                if (!acc)
+                    for (int c = 0; c < 4; c++) {
+                        bool dummy;
+                        ts.rec4[s][4 * m + c] =
+                            phase1(x0 + 16 * s + nx + 2 * (c & 1), y0 + ny + 2 * (c >> 1), 4, 2, k4[c], INFINITY, dummy);
+                    }
             }
         }
+        ts.acc3[s][m] = acc;
+        ts.rec3[s][m] = rec;
+    }
+    __syncthreads();
 
-        // ---- level 4 (always accepts) and emission in Morton (= DFS) order
+    // ---- K2b: DFS (Morton) emission per root: lane owns cells 2l, 2l+1; unit map words
+    for (int slot = warp; slot < nr; slot += EW) {
+        const int a = lane >> 3, m3 = lane >> 1, c = lane & 1;
+        const bool vis1 = p.root_level == 1;
+        const bool acc1 = ts.acc1[slot];
+        const bool vis2 = !vis1 || !acc1;
+        const bool acc2 = ts.acc2[slot][a];
+        const bool vis3 = vis2 && !acc2;
+        const bool acc3 = ts.acc3[slot][m3];
         const bool vis4 = vis3 && !acc3;
+        uint64_t recA = 0, recB = 0, cov = 0;
+        bool hasA = false, hasB = false;
         if (vis1 && acc1) {
             hasA = lane == 0;
-            recA = rec1;
+            cov = recA = ts.rec1[slot];
         } else if (vis2 && acc2) {
             hasA = (lane & 7) == 0;
-            recA = rec2;
+            cov = recA = ts.rec2[slot][a];
         } else if (vis3 && acc3) {
             hasA = c == 0;
-            recA = rec3;
+            cov = recA = ts.rec3[slot][m3];
         } else if (vis4) {
-            bool dummy;
             hasA = hasB = true;
-            recA = phase1(rxg + lx, ryg + ly, 4, 2, m4L, INFINITY, dummy);
-            recB = phase1(rxg + lx + 2, ryg + ly, 4, 2, m4R, INFINITY, dummy);
+            recA = ts.rec4[slot][2 * lane];
+            recB = ts.rec4[slot][2 * lane + 1];
+            cov = recA;
         }
-        if (p.unit_map) {  // the decoder's per-cell unit map for this lane's two cells
-            const uint64_t cov = (vis1 && acc1) ? rec1 : (vis2 && acc2) ? rec2 : (vis3 && acc3) ? rec3 : recA;
-            const uint64_t covB = vis4 ? recB : cov;
-            umap = (uint32_t)mns_unit_of_record(cov, rxg, ryg, lx, ly) |
-                   ((uint32_t)mns_unit_of_record(covB, rxg, ryg, lx + 2, ly) << 16);
+        const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
+        const unsigned lt = lanemask_lt();
+        const int offA = __popc(bA & lt) + __popc(bB & lt);
+        if (hasA) stage[slot][offA] = recA;
+        if (hasB) stage[slot][offA + (hasA ? 1 : 0)] = recB;
+        if (lane == 0) ts.root_cnt[slot] = __popc(bA) + __popc(bB);
+        if (p.unit_map) {
+            const int rxg = x0 + 16 * slot, lx = node4_x(2 * lane), ly = node4_y(2 * lane);
+            const uint32_t umap = (uint32_t)mns_unit_of_record(cov, rxg, y0, lx, ly) |
+                                  ((uint32_t)mns_unit_of_record(vis4 ? recB : cov, rxg, y0, lx + 2, ly) << 16);
+            const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
+            p.unit_map[root * 32 + lane] = umap;
         }
     }
-    const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
-    const unsigned lt = lanemask_lt();
-    const int offA = __popc(bA & lt) + __popc(bB & lt);
-    if (hasA) stage[slot][offA] = recA;
-    if (hasB) stage[slot][offA + (hasA ? 1 : 0)] = recB;
-    if (lane == 0) root_cnt[slot] = __popc(bA) + __popc(bB);
-    if (p.unit_map) {
-        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
-        p.unit_map[root * 32 + lane] = umap;
-    }
-    }  // roots of this warp
     __syncthreads();
     // ---- one decoupled look-back per 32 roots, then coalesced record copies
     if (warp == 0) {
         long long agg = 0;
-        for (int k = 0; k < nr; k++) agg += root_cnt[k];
+        for (int k = 0; k < nr; k++) agg += ts.root_cnt[k];
         const long long base = lookback_exclusive_warp(p.status, tile, agg);
         if (lane == 0) {
             const long long root0 = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0;
             long long run = base;
             for (int k = 0; k < nr; k++) {
-                root_base[k] = run;
+                ts.root_base[k] = run;
                 p.root_offsets[root0 + k] = (int32_t)run;
-                run += root_cnt[k];
+                run += ts.root_cnt[k];
             }
             if (tile == p.n_tiles - 1) {
                 p.root_offsets[p.n_roots] = (int32_t)run;
@@ -539,8 +494,8 @@ __global__ void __launch_bounds__(ET, 3) mns_encode_kernel(const EncParams p) {
     }
     __syncthreads();
     for (int k = warp; k < nr; k += EW) {
-        const long long b0 = root_base[k];
-        for (int i = lane; i < root_cnt[k]; i += 32) p.out[b0 + i] = stage[k][i];
+        const long long b0 = ts.root_base[k];
+        for (int i = lane; i < ts.root_cnt[k]; i += 32) p.out[b0 + i] = stage[k][i];
     }
 }
 
