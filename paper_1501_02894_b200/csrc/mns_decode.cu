@@ -30,10 +30,11 @@ namespace mns {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int BR = 4;                 // roots per column band (64 px)
-constexpr int DT = BR * 32;           // one warp per root of the band's current root row
-constexpr int WINW = BR * 16 + 32;    // 96-px window: band +- 16 px (every clamped domain lies inside)
-constexpr int QW = WINW / 2;          // 48 columns of the even 2x2-sum lattice
+constexpr int BR = 8;                 // roots per column band (128 px)
+constexpr int NW = BR / 2;            // warps; each paints two side-by-side roots per root row
+constexpr int DT = NW * 32;
+constexpr int WINW = BR * 16 + 32;    // 160-px window: band +- 16 px (every clamped domain lies inside)
+constexpr int QW = WINW / 2;          // 80 columns of the even 2x2-sum lattice
 constexpr int QS = QW + 4;            // padded row stride (rows 2 apart land 8 banks apart)
 constexpr int QR = 32;                // lattice ring rows (24 live + 8 being built)
 constexpr int BLK = 16;               // raster rows per TMA block
@@ -65,39 +66,38 @@ __device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates
     return m;
 }
 
-struct Unit {
-    float a, b;      // v = a*q + b once the domain mean is known (b = o - s*mean)
-    float s, o;
-    int drow, dcol;  // lattice (global q-row, window q-col) or direct (global row, window col)
-    int lg, ox, oy;  // log2(side), pixel offset of the lane's cell inside the unit
-    bool lattice;
-};
-
-__device__ __forceinline__ Unit unit_of(uint32_t d, const float *st, int px, int py, int rxg, int ryg, int W, int H,
-                                        int wx0) {
-    Unit u;
-    u.s = st[d & 15];
-    u.o = (float)((int)((d >> 4) & 1023) - 32);
-    u.lg = (int)(d >> 14) + 1;
-    const int side = 1 << u.lg;
-    const int ux = px & ~(side - 1), uy = py & ~(side - 1);
-    u.ox = px - ux;
-    u.oy = py - uy;
-    const int dx = clampi(rxg + ux - side / 2, 0, W - 2 * side), dy = clampi(ryg + uy - side / 2, 0, H - 2 * side);
-    const int wc = dx - wx0;  // wx0 is even
-    u.lattice = ((wc | dy) & 1) == 0;
-    u.drow = u.lattice ? dy >> 1 : dy;
-    u.dcol = u.lattice ? wc >> 1 : wc;
-    u.a = 0.25f * u.s;
-    return u;
+// Domain offset of a lane's 4x4 block inside a unit of side 2^(k+1) (k = 1..3): the block's
+// first domain pixel is (rxg + X - 16, ryg + Y - 16) with X = 2px - ux - side/2 + 16 (ux = px
+// rounded down to the unit), i.e. the co-centred domain (encoder.py:139-157) plus twice the
+// block's offset inside the unit.  Interior roots never clamp, so the three sizes fit one
+// register per coordinate (3 x 6 bits), built once per lane.
+__device__ __forceinline__ uint32_t offset_table(int pc) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 1; k <= 3; k++) {
+        const int side = 2 << k;
+        t |= (uint32_t)(2 * pc - (pc & ~(side - 1)) - side / 2 + 16) << (6 * k);
+    }
+    return t;
 }
 
-// One Jacobi sweep (decoder.py:37-63) for a 64-px column band over CR root rows.
-// TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two
-// blocks ahead of the root row being painted; each block is reduced once into the
-// even 2x2-sum lattice ring, so no raster row is reloaded vertically and the
-// horizontal halo costs 1.5x only in L2->SM traffic.  The unit map words of the
-// next root row are prefetched into registers one step ahead.
+// Same offset for roots on the image border: the domain is clamped into the image.
+__device__ __forceinline__ int clamped_offset(int pc, int side, int rg, int extent) {
+    const int uc = pc & ~(side - 1);
+    return clampi(rg + uc - side / 2, 0, extent - 2 * side) - rg + 2 * (pc - uc) + 16;
+}
+
+__device__ __forceinline__ float unit_o(uint32_t d) { return (float)((int)((d >> 4) & 1023) - 32); }
+
+// One Jacobi sweep (decoder.py:37-63) for a 128-px column band over CR root rows.
+// TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two blocks
+// ahead of the root row being painted; each block is reduced once into the even 2x2-sum
+// lattice ring (numpy's downsample_mean2 order, image.py), so no raster row is reloaded
+// vertically.  Lane l of a warp owns the Morton-aligned 4x4 pixel block l & 15 of root
+// l >> 4: any unit of side >= 4 covers the whole block (units are aligned to their side),
+// so one 64-bit unit-map load, one unit decode and 16 lattice loads serve 16 pixels; only
+// 2x2 units (odd domains) sum raster pixels directly.  The unit-map words of the next root
+// row are prefetched into registers one step ahead.
 __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -127,17 +127,31 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
             tma_load_2d(raw[b], &tmap, wx0, 16 * (r_s - 1 + k) - p.y_lo, &bars[b]);
         }
     };
+    // this thread's lattice-build elements (the same for every block): e = tid + i * DT
+    constexpr int NE = 8 * (WINW / 4), NPT = (NE + DT - 1) / DT;
+    int b_raw[NPT], b_row[NPT], b_col[NPT];
+#pragma unroll
+    for (int i = 0; i < NPT; i++) {
+        const int e = tid + i * DT, r = e / (WINW / 4), c4 = e % (WINW / 4);
+        b_raw[i] = 2 * r * WINW + 4 * c4;
+        b_row[i] = r;
+        b_col[i] = 2 * c4;
+    }
+    const uint32_t bar0 = smem_u32(&bars[0]);
     auto build = [&](int k) {  // lattice rows [8(r_s-1+k), 8(r_s+k)) from block k
         const int b = k % NBUF;
-        mbar_wait(&bars[b], (k / NBUF) & 1);
+        mbar_wait_addr(bar0 + 8 * b, (k / NBUF) & 1);
         const int g0 = 8 * (r_s - 1 + k);
-        for (int e = tid; e < 8 * (WINW / 4); e += DT) {
-            const int r = e / (WINW / 4), c4 = e % (WINW / 4);
-            const float4 u = *reinterpret_cast<const float4 *>(&raw[b][2 * r][4 * c4]);
-            const float4 w = *reinterpret_cast<const float4 *>(&raw[b][2 * r + 1][4 * c4]);
-            // numpy order of downsample_mean2 up to the 0.25 scale: ((a + b) + c) + d
-            *reinterpret_cast<float2 *>(&qe[(g0 + r) & (QR - 1)][2 * c4]) =
-                make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+        const float *rb = &raw[b][0][0];
+#pragma unroll
+        for (int i = 0; i < NPT; i++) {
+            if (i + 1 < NPT || tid + i * DT < NE) {
+                const float4 u = *reinterpret_cast<const float4 *>(rb + b_raw[i]);
+                const float4 w = *reinterpret_cast<const float4 *>(rb + b_raw[i] + WINW);
+                // numpy order of downsample_mean2 up to the 0.25 scale: ((a + b) + c) + d
+                *reinterpret_cast<float2 *>(&qe[(g0 + b_row[i]) & (QR - 1)][b_col[i]]) =
+                    make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+            }
         }
     };
     if (!flat) {
@@ -149,96 +163,133 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
         build(1);
     }
 
-    const int rxi = blockIdx.x * BR + warp;
+    const int l = lane & 15, rc = 2 * warp + (lane >> 4);  // block in root, root column in band
+    const int lx = 4 * (l & 1) + 8 * ((l >> 2) & 1), ly = 4 * ((l >> 1) & 1) + 8 * ((l >> 3) & 1);
+    const int rxi = blockIdx.x * BR + rc;
     const bool live_col = rxi < p.rw;
-    const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
-    const int lx = (a & 1) * 8 + (b & 1) * 4, ly = (a >> 1) * 8 + (b >> 1) * 4 + 2 * c;
-    const uint32_t *umap = p.unit_map + (size_t)((r_s - p.rr0) * p.rw + rxi) * 32 + lane;
-    uint32_t word = live_col ? __ldg(umap) : 0u;
+    // cells 4l .. 4l+3 of the root (Morton order) = unit-map words 2l, 2l+1
+    const uint2 *umap = reinterpret_cast<const uint2 *>(p.unit_map + (size_t)((r_s - p.rr0) * p.rw + rxi) * 32) + l;
+    const size_t ustride = (size_t)p.rw * 16;
+    uint2 word = live_col ? __ldg(umap) : make_uint2(0u, 0u);
+    const uint32_t tx = offset_table(lx), ty = offset_table(ly);
+    const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
+    const int rh = p.H / 16, wcol0 = 16 * rc;
     float lmax = 0.f;
     for (int j = 0; j < r_e - r_s; j++) {
-        const uint32_t wnext = (live_col && j + 1 < r_e - r_s) ? __ldg(umap + (size_t)(j + 1) * p.rw * 32) : 0u;
+        umap += ustride;
+        const uint2 wnext = (live_col && j + 1 < r_e - r_s) ? __ldg(umap) : make_uint2(0u, 0u);
         if (!flat) build(j + 2);
         __syncthreads();
         if (!flat && tid == 0) {
             fence_proxy_async();  // generic reads of block j-1 complete before the async refill
             issue(j + 4);
         }
-        if (live_col) {
-            const int ry = r_s + j;
-            const int rxg = rxi * 16, ryg = ry * 16;
-            Unit uA = unit_of(word & 0xFFFFu, st, lx, ly, rxg, ryg, p.W, p.H, wx0);
-            Unit uB = unit_of(word >> 16, st, lx + 2, ly, rxg, ryg, p.W, p.H, wx0);
-            float q[8];
+        const int ry = r_s + j;
+        const int rxg = rxi * 16, ryg = ry * 16;
+        const uint32_t d0 = word.x & 0xFFFFu;
+        const int k = (int)(d0 >> 14);  // log2(side) - 1 of the unit holding cell 0
+        float v[16];
+        float own = 0.f, sa = 0.f, sb = 0.f;
+        if (live_col && k > 0) {  // one unit of side >= 4 covers the 4x4 block
+            sa = st[d0 & 15];
+            sb = unit_o(d0);
+            if (flat) {
 #pragma unroll
-            for (int side = 0; side < 2; side++) {
-                const Unit &u = side ? uB : uA;
+                for (int e = 0; e < 16; e++) v[e] = 4.f * p.init;
+            } else {
+                int X, Y;
+                if (interior_col && ry >= 1 && ry + 1 < rh) {
+                    X = (int)((tx >> (6 * k)) & 63);
+                    Y = (int)((ty >> (6 * k)) & 63);
+                } else {
+                    X = clamped_offset(lx, 2 << k, rxg, p.W);
+                    Y = clamped_offset(ly, 2 << k, ryg, p.H);
+                }
+                const int qr = (ryg - 16 + Y) >> 1, qc = (wcol0 + X) >> 1;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const float *row = &qe[(qr + i) & (QR - 1)][qc];
+#pragma unroll
+                    for (int jj = 0; jj < 4; jj++) v[4 * i + jj] = row[jj];
+                }
+            }
+            own = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) +
+                  (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+        } else if (live_col) {  // four 2x2 units with odd (or clamped) 4x4 domains
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t d = c == 0 ? d0 : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
+                const int px = lx + 2 * (c & 1), py = ly + 2 * (c >> 1);
+                float q[4];
                 if (flat) {
 #pragma unroll
-                    for (int k = 0; k < 4; k++) q[(k >> 1) * 4 + 2 * side + (k & 1)] = 4.f * p.init;
-                } else if (u.lattice) {
+                    for (int e = 0; e < 4; e++) q[e] = 4.f * p.init;
+                } else {
+                    const int dx = clampi(rxg + px - 1, 0, p.W - 4), dy = clampi(ryg + py - 1, 0, p.H - 4);
+                    const int C = dx - wx0;
 #pragma unroll
-                    for (int i = 0; i < 2; i++)
-#pragma unroll
-                        for (int jj = 0; jj < 2; jj++)
-                            q[4 * i + 2 * side + jj] = qe[(u.drow + u.oy + i) & (QR - 1)][u.dcol + u.ox + jj];
-                } else {  // 2x2 unit with an odd / mixed-phase domain: sum the raster pixels directly
-#pragma unroll
-                    for (int i = 0; i < 2; i++)
+                    for (int i = 0; i < 2; i++) {
+                        const int R = dy + 2 * i;
+                        const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
+                        const float *r0 = raw[k0 % NBUF][R % BLK];
+                        const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
 #pragma unroll
                         for (int jj = 0; jj < 2; jj++) {
-                            const int R = u.drow + 2 * (u.oy + i), C = u.dcol + 2 * (u.ox + jj);
-                            const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
-                            const float *r0 = raw[k0 % NBUF][R % BLK];
-                            const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
-                            q[4 * i + 2 * side + jj] = ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
+                            const int cc = C + 2 * jj;
+                            q[2 * i + jj] = ((r0[cc] + r0[cc + 1]) + r1[cc]) + r1[cc + 1];
                         }
+                    }
                 }
-            }
-            const float sA = q[0] + q[1] + q[4] + q[5], sB = q[2] + q[3] + q[6] + q[7];
-            float s2 = sA + sB;
-            s2 += __shfl_xor_sync(FULL, s2, 1);   // 4x4 unit (lane pair)
-            float s8 = s2 + __shfl_xor_sync(FULL, s2, 2);
-            s8 += __shfl_xor_sync(FULL, s8, 4);   // 8x8 unit (8 lanes)
-            float s32 = s8 + __shfl_xor_sync(FULL, s8, 8);
-            s32 += __shfl_xor_sync(FULL, s32, 16);  // 16x16 unit (warp)
-            auto unit_b = [&](const Unit &u, float own) {
-                const float sum = u.lg == 1 ? own : (u.lg == 2 ? s2 : (u.lg == 3 ? s8 : s32));
-                const float mean = sum * __int_as_float((127 - 2 - 2 * u.lg) << 23);  // sum * 0.25 / side^2
-                return fmaf(-u.s, mean, u.o);
-            };
-            uA.b = unit_b(uA, sA);
-            uB.b = unit_b(uB, sB);
-            float v[8];
+                const float s = st[d & 15];
+                const float b = fmaf(-s, ((q[0] + q[1]) + (q[2] + q[3])) * 0.0625f, unit_o(d));
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const bool right = (k & 3) >= 2;
-                v[k] = fminf(255.f, fmaxf(0.f, fmaf(right ? uB.a : uA.a, q[k], right ? uB.b : uA.b)));
-            }
-            const int gx = rxg + lx, gy = ryg + ly;
-            if (p.track_delta) {
+                for (int i = 0; i < 2; i++)
 #pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
-#pragma unroll
-                    for (int jj = 0; jj < 4; jj++)
-                        lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + warp * 16 + lx + jj])));
-                }
+                    for (int jj = 0; jj < 2; jj++) {
+                        const int e = 4 * (2 * (c >> 1) + i) + 2 * (c & 1) + jj;
+                        v[e] = fminf(255.f, fmaxf(0.f, fmaf(0.25f * s, q[2 * i + jj], b)));
+                    }
             }
-            if (p.nxt) {
-                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)gy * p.W + gx) = make_float4(v[0], v[1], v[2], v[3]);
-                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + 1) * p.W + gx) =
-                    make_float4(v[4], v[5], v[6], v[7]);
-            }
-            if (p.out_u8) {
-                uint32_t w0 = 0, w1 = 0;
+        }
+        // unit sums: 4x4 = own block, 8x8 = 4 lanes (l bits 0,1), 16x16 = the root's 16 lanes
+        float s8 = own + __shfl_xor_sync(FULL, own, 1);
+        s8 += __shfl_xor_sync(FULL, s8, 2);
+        float s16 = s8 + __shfl_xor_sync(FULL, s8, 4);
+        s16 += __shfl_xor_sync(FULL, s16, 8);
+        if (!live_col) {
+            word = wnext;
+            continue;
+        }
+        if (k > 0) {
+            const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
+            const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
+            const float b = fmaf(-sa, mean, sb), a = 0.25f * sa;
 #pragma unroll
-                for (int jj = 0; jj < 4; jj++) {
-                    w0 |= (uint32_t)floorf(v[jj] + 0.5f) << (8 * jj);
-                    w1 |= (uint32_t)floorf(v[4 + jj] + 0.5f) << (8 * jj);
-                }
-                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)gy * p.W + gx) = w0;
-                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + 1) * p.W + gx) = w1;
+            for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, fmaf(a, v[e], b)));
+        }
+        const int gx = rxg + lx, gy = ryg + ly;
+        if (p.track_delta) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++)
+                    lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + wcol0 + lx + jj])));
+            }
+        }
+        if (p.nxt) {
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + i) * p.W + gx) =
+                    make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        if (p.out_u8) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) w |= (uint32_t)floorf(v[4 * i + jj] + 0.5f) << (8 * jj);
+                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + i) * p.W + gx) = w;
             }
         }
         word = wnext;
