@@ -77,7 +77,8 @@ int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int
  * stop_delta > 0 and max|delta| < stop_delta; *d_iters_done receives the count)
  * the raster is rounded floor(x+0.5), clipped to [0,255] into out (width*height
  * bytes, padded; the caller crops).  The final raster is in ping when
- * iters_done is even, else in pong. */
+ * iters_done is even, else in pong -- except when out != NULL and stop_delta == 0:
+ * then sweeps run two per pass (mns_decode_sweep2) and only out is defined. */
 int mns_decode_workspace_bytes(int32_t width, int32_t height, int64_t *bytes);
 int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
                         int32_t iters, double stop_delta, float initial_value, float *ping, float *pong,
@@ -95,6 +96,18 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
 int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, int32_t root_row_begin,
                      int32_t root_row_end, const float *cur, float initial_value, float *nxt, uint8_t *out,
                      int32_t *state, double stop_delta, void *stream);
+
+/* Two sweeps t -> t+2 in one pass (stop_delta == 0 only): raster t is read once,
+ * t+2 written once, t+1 stays on chip.  Rows [16*root_row_begin - 32,
+ * 16*root_row_end + 32) of cur must be resident (32-row halo; exchanged once per
+ * pass on the multi-GPU decoder).  unit_map holds the root rows starting at
+ * unit_map_row_begin, which must cover [root_row_begin - 1, root_row_end + 1)
+ * clipped to the image.  cur NULL = flat start raster; exactly one of nxt (fp32)
+ * and out (rounded uint8, final pass) is non-NULL.  Same result as two
+ * mns_decode_sweep calls. */
+int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                      int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value, float *nxt,
+                      uint8_t *out, void *stream);
 
 /* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
  * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-

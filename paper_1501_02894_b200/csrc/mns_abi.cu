@@ -81,6 +81,8 @@ int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
 int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const float *cur, float init,
                  float *nxt, uint8_t *out, int *state, double stop_delta, cudaStream_t stream);
+int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur, float init,
+                  float *nxt, uint8_t *out, cudaStream_t stream);
 int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
                  const int32_t *udy, const float *us, const float *uo, int64_t n, int W, int H, int iters,
                  double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
@@ -147,6 +149,13 @@ int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, in
                      int32_t *state, double stop_delta, void *stream) {
     GUARD(mns::decode_sweep(unit_map, width, height, root_row_begin, root_row_end, cur, initial_value, nxt, out,
                             state, stop_delta, (cudaStream_t)stream));
+}
+
+int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                      int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value, float *nxt,
+                      uint8_t *out, void *stream) {
+    GUARD(mns::decode_sweep2(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end, cur,
+                             initial_value, nxt, out, (cudaStream_t)stream));
 }
 
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

@@ -57,6 +57,7 @@ struct SweepParams {
     int track_delta;
     float stop_delta;
     int n_ctas;
+    int umap_r0;         // first root row held by unit_map (pair kernel: may be rr0 - 1)
 };
 
 __device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates -> 6-bit Morton (y major)
@@ -89,15 +90,127 @@ __device__ __forceinline__ int clamped_offset(int pc, int side, int rg, int exte
 
 __device__ __forceinline__ float unit_o(uint32_t d) { return (float)((int)((d >> 4) & 1023) - 32); }
 
+// Where a lane paints: the Morton-aligned 4x4 block l = lane & 15 of a root; any unit of side
+// >= 4 covers the whole block (units are aligned to their side), so one 64-bit unit-map load
+// (cells 4l..4l+3), one unit decode and 16 lattice loads serve 16 pixels; only 2x2 units
+// (odd domains) sum raster pixels directly.
+struct Lane {
+    int lx, ly;        // block offset in the root
+    uint32_t tx, ty;   // offset_table(lx), offset_table(ly)
+};
+
+__device__ __forceinline__ Lane lane_of(int lane) {
+    Lane L;
+    const int l = lane & 15;
+    L.lx = 4 * (l & 1) + 8 * ((l >> 2) & 1);
+    L.ly = 4 * ((l >> 1) & 1) + 8 * ((l >> 3) & 1);
+    L.tx = offset_table(L.lx);
+    L.ty = offset_table(L.ly);
+    return L;
+}
+
+// v[16] = clip(s * (q - mean) + o) of the lane's 4x4 block of root (rxg, ryg) (decoder.py:32-34,
+// transform.py:63-66).  Domain sums q come from the even 2x2-sum lattice ring `lat` (row =
+// absolute raster row / 2 mod QR, column = window column / 2, window origin wx0) or, for 2x2
+// units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
+// lane of the warp must call it (segmented shuffles); `live` lanes get v.
+template <int QSTR, class RawSum>
+__device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
+                                            const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
+                                            bool interior, int W, int H, float (&v)[16]) {
+    const uint32_t d0 = word.x & 0xFFFFu;
+    const int k = (int)(d0 >> 14);  // log2(side) - 1 of the unit holding cell 0
+    float own = 0.f, sa = 0.f, sb = 0.f;
+    if (live && k > 0) {  // one unit of side >= 4 covers the 4x4 block
+        sa = st[d0 & 15];
+        sb = unit_o(d0);
+        if (flat) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) v[e] = 4.f * init;
+        } else {
+            int X, Y;
+            if (interior) {
+                X = (int)((L.tx >> (6 * k)) & 63);
+                Y = (int)((L.ty >> (6 * k)) & 63);
+            } else {
+                X = clamped_offset(L.lx, 2 << k, rxg, W);
+                Y = clamped_offset(L.ly, 2 << k, ryg, H);
+            }
+            const int qr = (ryg - 16 + Y) >> 1, qc = (rxg - 16 + X - wx0) >> 1;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float *row = lat + ((qr + i) & (QR - 1)) * QSTR + qc;
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) v[4 * i + jj] = row[jj];
+            }
+        }
+        own = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) +
+              (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+    } else if (live) {  // four 2x2 units with odd (or clamped) 4x4 domains
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const uint32_t d = c == 0 ? d0 : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
+            const int px = L.lx + 2 * (c & 1), py = L.ly + 2 * (c >> 1);
+            float q[4];
+            if (flat) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) q[e] = 4.f * init;
+            } else {
+                const int dx = clampi(rxg + px - 1, 0, W - 4), dy = clampi(ryg + py - 1, 0, H - 4);
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int jj = 0; jj < 2; jj++) q[2 * i + jj] = raw_sum(dy + 2 * i, dx - wx0 + 2 * jj);
+            }
+            const float s = st[d & 15];
+            const float b = fmaf(-s, ((q[0] + q[1]) + (q[2] + q[3])) * 0.0625f, unit_o(d));
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+#pragma unroll
+                for (int jj = 0; jj < 2; jj++)
+                    v[4 * (2 * (c >> 1) + i) + 2 * (c & 1) + jj] =
+                        fminf(255.f, fmaxf(0.f, fmaf(0.25f * s, q[2 * i + jj], b)));
+        }
+    }
+    // unit sums: 4x4 = own block, 8x8 = 4 lanes (lane bits 0,1), 16x16 = the root's 16 lanes
+    float s8 = own + __shfl_xor_sync(FULL, own, 1);
+    s8 += __shfl_xor_sync(FULL, s8, 2);
+    float s16 = s8 + __shfl_xor_sync(FULL, s8, 4);
+    s16 += __shfl_xor_sync(FULL, s16, 8);
+    if (live && k > 0) {
+        const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
+        const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
+        const float b = fmaf(-sa, mean, sb), a = 0.25f * sa;
+#pragma unroll
+        for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, fmaf(a, v[e], b)));
+    }
+}
+
+// fp32 -> rounded uint8 rows of a 4x4 block (floor(x + 0.5); x is already clipped to [0, 255])
+__device__ __forceinline__ void store_block(const float (&v)[16], float *nxt, uint8_t *out, int W, int gx, int gy) {
+    if (nxt) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            *reinterpret_cast<float4 *>(nxt + (ptrdiff_t)(gy + i) * W + gx) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    if (out) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) w |= (uint32_t)floorf(v[4 * i + jj] + 0.5f) << (8 * jj);
+            *reinterpret_cast<uint32_t *>(out + (ptrdiff_t)(gy + i) * W + gx) = w;
+        }
+    }
+}
+
 // One Jacobi sweep (decoder.py:37-63) for a 128-px column band over CR root rows.
 // TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two blocks
 // ahead of the root row being painted; each block is reduced once into the even 2x2-sum
 // lattice ring (numpy's downsample_mean2 order, image.py), so no raster row is reloaded
-// vertically.  Lane l of a warp owns the Morton-aligned 4x4 pixel block l & 15 of root
-// l >> 4: any unit of side >= 4 covers the whole block (units are aligned to their side),
-// so one 64-bit unit-map load, one unit decode and 16 lattice loads serve 16 pixels; only
-// 2x2 units (odd domains) sum raster pixels directly.  The unit-map words of the next root
-// row are prefetched into registers one step ahead.
+// vertically.  Warp w paints roots 2w, 2w+1 of the band (paint_block).  The unit-map
+// words of the next root row are prefetched into registers one step ahead.
 __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -162,18 +275,23 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
         build(0);
         build(1);
     }
+    auto raw_sum = [&](int R, int C) {  // 2x2 raster sum at absolute row R, window column C
+        const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
+        const float *r0 = raw[k0 % NBUF][R % BLK];
+        const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
+        return ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
+    };
 
-    const int l = lane & 15, rc = 2 * warp + (lane >> 4);  // block in root, root column in band
-    const int lx = 4 * (l & 1) + 8 * ((l >> 2) & 1), ly = 4 * ((l >> 1) & 1) + 8 * ((l >> 3) & 1);
+    const Lane L = lane_of(lane);
+    const int rc = 2 * warp + (lane >> 4);  // root column in the band
     const int rxi = blockIdx.x * BR + rc;
     const bool live_col = rxi < p.rw;
-    // cells 4l .. 4l+3 of the root (Morton order) = unit-map words 2l, 2l+1
-    const uint2 *umap = reinterpret_cast<const uint2 *>(p.unit_map + (size_t)((r_s - p.rr0) * p.rw + rxi) * 32) + l;
+    const uint2 *umap = reinterpret_cast<const uint2 *>(p.unit_map + (size_t)((r_s - p.rr0) * p.rw + rxi) * 32) +
+                        (lane & 15);
     const size_t ustride = (size_t)p.rw * 16;
     uint2 word = live_col ? __ldg(umap) : make_uint2(0u, 0u);
-    const uint32_t tx = offset_table(lx), ty = offset_table(ly);
     const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
-    const int rh = p.H / 16, wcol0 = 16 * rc;
+    const int rh = p.H / 16;
     float lmax = 0.f;
     for (int j = 0; j < r_e - r_s; j++) {
         umap += ustride;
@@ -186,113 +304,21 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
         }
         const int ry = r_s + j;
         const int rxg = rxi * 16, ryg = ry * 16;
-        const uint32_t d0 = word.x & 0xFFFFu;
-        const int k = (int)(d0 >> 14);  // log2(side) - 1 of the unit holding cell 0
         float v[16];
-        float own = 0.f, sa = 0.f, sb = 0.f;
-        if (live_col && k > 0) {  // one unit of side >= 4 covers the 4x4 block
-            sa = st[d0 & 15];
-            sb = unit_o(d0);
-            if (flat) {
-#pragma unroll
-                for (int e = 0; e < 16; e++) v[e] = 4.f * p.init;
-            } else {
-                int X, Y;
-                if (interior_col && ry >= 1 && ry + 1 < rh) {
-                    X = (int)((tx >> (6 * k)) & 63);
-                    Y = (int)((ty >> (6 * k)) & 63);
-                } else {
-                    X = clamped_offset(lx, 2 << k, rxg, p.W);
-                    Y = clamped_offset(ly, 2 << k, ryg, p.H);
-                }
-                const int qr = (ryg - 16 + Y) >> 1, qc = (wcol0 + X) >> 1;
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const float *row = &qe[(qr + i) & (QR - 1)][qc];
-#pragma unroll
-                    for (int jj = 0; jj < 4; jj++) v[4 * i + jj] = row[jj];
-                }
-            }
-            own = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) +
-                  (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-        } else if (live_col) {  // four 2x2 units with odd (or clamped) 4x4 domains
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const uint32_t d = c == 0 ? d0 : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
-                const int px = lx + 2 * (c & 1), py = ly + 2 * (c >> 1);
-                float q[4];
-                if (flat) {
-#pragma unroll
-                    for (int e = 0; e < 4; e++) q[e] = 4.f * p.init;
-                } else {
-                    const int dx = clampi(rxg + px - 1, 0, p.W - 4), dy = clampi(ryg + py - 1, 0, p.H - 4);
-                    const int C = dx - wx0;
-#pragma unroll
-                    for (int i = 0; i < 2; i++) {
-                        const int R = dy + 2 * i;
-                        const int k0 = R / BLK - (r_s - 1), k1 = (R + 1) / BLK - (r_s - 1);
-                        const float *r0 = raw[k0 % NBUF][R % BLK];
-                        const float *r1 = raw[k1 % NBUF][(R + 1) % BLK];
-#pragma unroll
-                        for (int jj = 0; jj < 2; jj++) {
-                            const int cc = C + 2 * jj;
-                            q[2 * i + jj] = ((r0[cc] + r0[cc + 1]) + r1[cc]) + r1[cc + 1];
-                        }
-                    }
-                }
-                const float s = st[d & 15];
-                const float b = fmaf(-s, ((q[0] + q[1]) + (q[2] + q[3])) * 0.0625f, unit_o(d));
-#pragma unroll
-                for (int i = 0; i < 2; i++)
-#pragma unroll
-                    for (int jj = 0; jj < 2; jj++) {
-                        const int e = 4 * (2 * (c >> 1) + i) + 2 * (c & 1) + jj;
-                        v[e] = fminf(255.f, fmaxf(0.f, fmaf(0.25f * s, q[2 * i + jj], b)));
-                    }
-            }
-        }
-        // unit sums: 4x4 = own block, 8x8 = 4 lanes (l bits 0,1), 16x16 = the root's 16 lanes
-        float s8 = own + __shfl_xor_sync(FULL, own, 1);
-        s8 += __shfl_xor_sync(FULL, s8, 2);
-        float s16 = s8 + __shfl_xor_sync(FULL, s8, 4);
-        s16 += __shfl_xor_sync(FULL, s16, 8);
-        if (!live_col) {
-            word = wnext;
-            continue;
-        }
-        if (k > 0) {
-            const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
-            const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
-            const float b = fmaf(-sa, mean, sb), a = 0.25f * sa;
-#pragma unroll
-            for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, fmaf(a, v[e], b)));
-        }
-        const int gx = rxg + lx, gy = ryg + ly;
+        paint_block<QS>(word, live_col, L, st, &qe[0][0], raw_sum, flat, p.init, rxg, ryg, wx0,
+                        interior_col && ry >= 1 && ry + 1 < rh, p.W, p.H, v);
+        word = wnext;
+        if (!live_col) continue;
         if (p.track_delta) {
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const float *old = flat ? nullptr : raw[(j + 1) % NBUF][ly + i];
+                const float *old = flat ? nullptr : raw[(j + 1) % NBUF][L.ly + i];
 #pragma unroll
                 for (int jj = 0; jj < 4; jj++)
-                    lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + wcol0 + lx + jj])));
+                    lmax = fmaxf(lmax, fabsf(v[4 * i + jj] - (flat ? p.init : old[16 + 16 * rc + L.lx + jj])));
             }
         }
-        if (p.nxt) {
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-                *reinterpret_cast<float4 *>(p.nxt + (ptrdiff_t)(gy + i) * p.W + gx) =
-                    make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-        if (p.out_u8) {
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int jj = 0; jj < 4; jj++) w |= (uint32_t)floorf(v[4 * i + jj] + 0.5f) << (8 * jj);
-                *reinterpret_cast<uint32_t *>(p.out_u8 + (ptrdiff_t)(gy + i) * p.W + gx) = w;
-            }
-        }
-        word = wnext;
+        store_block(v, p.nxt, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
     }
     if (p.track_delta) {
 #pragma unroll
@@ -312,6 +338,161 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
                 p.state[3] = 0;
             }
         }
+    }
+}
+
+// ------------------------------------------------------------- two sweeps per pass
+// Sweeps t -> t+1 -> t+2 in one pass over HBM (no early stop): raster t is read once and
+// t+2 written once; t+1 never leaves shared memory.  Stage A (NWA warps) paints t+1 for the
+// band plus one root on each side (its domains reach 16 px out) into a 4-deep raw ring and
+// straight into the t+1 lattice ring (the 2x2 sums of a lane's own 4x4 block, numpy order);
+// stage B (NW warps) paints t+2 of the band two root rows behind, from those rings.  Raster t
+// streams through a 3-deep TMA ring (one block being reduced into the t lattice, two in
+// flight); stage A's rare 2x2 units read raster t through L2.  Rows: A recomputes one root
+// row above and below the CTA's CR2 rows; resident halo 32 rows (mns_decode_sweep2).
+constexpr int WA = BR * 16 + 64;      // 192-px window of raster t: band +- 32 px
+constexpr int QSA = WA / 2 + 4;       // t-lattice row stride (100: rows 2 apart 8 banks apart)
+constexpr int NT = 3;                 // raster-t ring
+constexpr int NM = 4;                 // t+1 raw ring (B reads rows i-3..i-1 while A writes i)
+constexpr int CR2 = 64;               // root rows per CTA
+constexpr int NWA = (BR + 2) / 2;     // stage-A warps (two roots each)
+constexpr int DT2 = (NWA + NW) * 32;
+constexpr int TRAW_BYTES = BLK * WA * 4;
+constexpr int PAIR_SMEM = NT * TRAW_BYTES + NM * RAW_BYTES + QR * QSA * 4 + QR * QS * 4;
+
+__global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                             const SweepParams p) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    float(*traw)[BLK][WA] = reinterpret_cast<float(*)[BLK][WA]>(dsm);
+    float(*mraw)[BLK][WINW] = reinterpret_cast<float(*)[BLK][WINW]>(dsm + NT * TRAW_BYTES);
+    float(*qa)[QSA] = reinterpret_cast<float(*)[QSA]>(dsm + NT * TRAW_BYTES + NM * RAW_BYTES);
+    float(*qb)[QS] = reinterpret_cast<float(*)[QS]>(dsm + NT * TRAW_BYTES + NM * RAW_BYTES + QR * QSA * 4);
+    __shared__ __align__(8) uint64_t bars[NT];
+    __shared__ float st[16];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int x0 = blockIdx.x * BR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
+    const int r_s = p.rr0 + blockIdx.y * CR2, r_e = min(r_s + CR2, p.rr1);
+    const int rh = p.H / 16;
+    const bool flat = p.cur == nullptr;
+    const int nblocks = (r_e - r_s) + 4;  // block k = raster-t root row r_s - 2 + k
+    if (tid < 16) st[tid] = kUnitS[tid];
+    if (tid == 0) {
+        for (int b = 0; b < NT; b++) mbar_init(&bars[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        if (k < nblocks) {
+            const int b = k % NT;
+            mbar_arrive_expect_tx(&bars[b], TRAW_BYTES);
+            tma_load_2d(traw[b], &tmap, xa0, 16 * (r_s - 2 + k) - p.y_lo, &bars[b]);
+        }
+    };
+    constexpr int NE = 8 * (WA / 4), NPT = (NE + DT2 - 1) / DT2;
+    int b_raw[NPT], b_row[NPT], b_col[NPT];
+#pragma unroll
+    for (int i = 0; i < NPT; i++) {
+        const int e = tid + i * DT2, r = e / (WA / 4), c4 = e % (WA / 4);
+        b_raw[i] = 2 * r * WA + 4 * c4;
+        b_row[i] = r;
+        b_col[i] = 2 * c4;
+    }
+    const uint32_t bar0 = smem_u32(&bars[0]);
+    auto build = [&](int k) {  // t-lattice rows of root row r_s - 2 + k
+        const int b = k % NT;
+        mbar_wait_addr(bar0 + 8 * b, (k / NT) & 1);
+        const int g0 = 8 * (r_s - 2 + k);
+        const float *rb = &traw[b][0][0];
+#pragma unroll
+        for (int i = 0; i < NPT; i++) {
+            if (i + 1 < NPT || tid + i * DT2 < NE) {
+                const float4 u = *reinterpret_cast<const float4 *>(rb + b_raw[i]);
+                const float4 w = *reinterpret_cast<const float4 *>(rb + b_raw[i] + WA);
+                *reinterpret_cast<float2 *>(&qa[(g0 + b_row[i]) & (QR - 1)][b_col[i]]) =
+                    make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+            }
+        }
+    };
+    if (!flat) {
+        if (tid == 0) {
+            prefetch_tmap(&tmap);
+            for (int k = 0; k < NT; k++) issue(k);
+        }
+        build(0);
+        build(1);
+        __syncthreads();
+        if (tid == 0) {
+            fence_proxy_async();
+            issue(NT);
+            issue(NT + 1);
+        }
+    }
+
+    const Lane L = lane_of(lane);
+    const bool stage_a = warp < NWA;
+    // stage A: root columns -1 .. BR of the band; stage B: 0 .. BR-1
+    const int rc = stage_a ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - NWA) + (lane >> 4);
+    const int rxi = blockIdx.x * BR + rc;
+    const bool col_ok = rxi >= 0 && rxi < p.rw;
+    const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
+    const int lag = stage_a ? 0 : 2;  // iteration i: A paints root row i, B paints i - 2
+    auto word_of = [&](int row) {
+        const bool ok = col_ok && row >= r_s - (stage_a ? 1 : 0) && row < r_e + (stage_a ? 1 : 0) && row >= 0 &&
+                        row < rh;
+        return ok ? __ldg(reinterpret_cast<const uint2 *>(p.unit_map + (size_t)((row - p.umap_r0) * p.rw + rxi) * 32) +
+                          (lane & 15))
+                  : make_uint2(0u, 0u);
+    };
+    auto raw_t = [&](int R, int C) {  // raster t through L2 (window origin xa0)
+        const float *r0 = p.cur + (ptrdiff_t)R * p.W + xa0 + C;
+        const float *r1 = r0 + p.W;
+        return ((__ldg(r0) + __ldg(r0 + 1)) + __ldg(r1)) + __ldg(r1 + 1);
+    };
+    auto raw_m = [&](int R, int C) {  // raster t+1 from the smem ring (window origin xb0)
+        const float *r0 = mraw[(R >> 4) & (NM - 1)][R & 15];
+        const float *r1 = mraw[((R + 1) >> 4) & (NM - 1)][(R + 1) & 15];
+        return ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
+    };
+    uint2 word = word_of(r_s - 1 - lag);
+    for (int i = r_s - 1; i <= r_e + 1; i++) {
+        const int row = i - lag;
+        const uint2 wnext = word_of(row + 1);
+        const int k = i - r_s + 3;
+        if (!flat && k < nblocks) build(k);
+        __syncthreads();
+        if (!flat && tid == 0) {
+            fence_proxy_async();  // generic reads of the block just reduced complete before its refill
+            issue(k + NT);
+        }
+        const int rxg = rxi * 16, ryg = row * 16;
+        const bool interior = interior_col && row >= 1 && row + 1 < rh;
+        float v[16];
+        if (stage_a) {
+            const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
+            paint_block<QSA>(word, live, L, st, &qa[0][0], raw_t, flat, p.init, rxg, ryg, xa0, interior, p.W, p.H,
+                             v);
+            if (live) {
+                const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
+                float *m = &mraw[row & (NM - 1)][L.ly][wc];
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    *reinterpret_cast<float4 *>(m + r * WINW) =
+                        make_float4(v[4 * r], v[4 * r + 1], v[4 * r + 2], v[4 * r + 3]);
+                const int g = (ryg + L.ly) >> 1;
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+                    *reinterpret_cast<float2 *>(&qb[(g + r) & (QR - 1)][wc >> 1]) =
+                        make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
+                                    ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]);
+            }
+        } else {
+            const bool live = col_ok && row >= r_s;
+            paint_block<QS>(word, live, L, st, &qb[0][0], raw_m, false, p.init, rxg, ryg, xb0, interior, p.W, p.H,
+                            v);
+            if (live) store_block(v, p.nxt, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
+        }
+        word = wnext;
     }
 }
 
@@ -521,6 +702,53 @@ int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const
     return 0;
 }
 
+static int ensure_pair_attr() {
+    static bool attr_set = false;
+    if (!attr_set) {
+        MNS_CUDA_TRY(cudaFuncSetAttribute(decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM));
+        attr_set = true;
+    }
+    return 0;
+}
+
+// Two sweeps over root rows [rr0, rr1) in one pass.  cur/nxt/out are virtual-global bases;
+// rows [16 rr0 - 32, 16 rr1 + 32) of cur are resident (32-row halo), and unit_map holds the
+// root rows [umap_r0, ...) covering [rr0 - 1, rr1 + 1) clipped to the image.
+int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur, float init,
+                  float *nxt, uint8_t *out, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
+    MNS_CHECK_ARG(umap_r0 <= (rr0 > 0 ? rr0 - 1 : 0) && umap_r0 >= 0, "unit map must start at root row rr0 - 1");
+    MNS_CHECK_ARG(H <= 65534, "height exceeds the record coordinate range");
+    MNS_CHECK_ARG((nxt != nullptr) != (out != nullptr), "exactly one of nxt / out");
+    if (ensure_pair_attr()) return -1;
+    SweepParams p{};
+    p.unit_map = unit_map;
+    p.umap_r0 = umap_r0;
+    p.W = W;
+    p.H = H;
+    p.rw = W / 16;
+    p.rr0 = rr0;
+    p.rr1 = rr1;
+    p.y_lo = rr0 * 16 - 32 > 0 ? rr0 * 16 - 32 : 0;
+    const int y_hi = rr1 * 16 + 32 < H ? rr1 * 16 + 32 : H;
+    p.cur = cur;
+    p.init = init;
+    p.nxt = nxt;
+    p.out_u8 = out;
+    CUtensorMap tmap{};
+    if (cur) {
+        if (encode_tmap_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cur + (ptrdiff_t)p.y_lo * W, (uint64_t)W,
+                           (uint64_t)(y_hi - p.y_lo), (uint64_t)W * 4, WA, BLK))
+            return -1;
+    }
+    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + CR2 - 1) / CR2);
+    p.n_ctas = grid.x * grid.y;
+    decode_pair_kernel<<<grid, DT2, PAIR_SMEM, stream>>>(tmap, p);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
@@ -537,6 +765,30 @@ int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W,
     int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
     if (rc) return rc;
     const bool track = stop_delta > 0.0;
+    if (out && !track && iters >= 2) {
+        // no early stop and only the uint8 image wanted: an odd first sweep alone, then two
+        // sweeps per pass (the fp32 raster is not materialised after the last sweep)
+        const float *cur = nullptr;
+        int it = 0;
+        if (iters & 1) {
+            rc = decode_sweep(umap, W, H, 0, H / 16, nullptr, init, pong, nullptr, state, 0.0, stream);
+            if (rc) return rc;
+            cur = pong;
+            it = 1;
+        }
+        for (; it < iters; it += 2) {
+            const bool last = it + 2 == iters;
+            float *nxt = last ? nullptr : (cur == ping ? pong : ping);
+            rc = decode_sweep2(umap, 0, W, H, 0, H / 16, cur, init, nxt, last ? out : nullptr, stream);
+            if (rc) return rc;
+            cur = nxt;
+        }
+        set_iters_kernel<<<1, 1, 0, stream>>>(state, iters);
+        MNS_CUDA_TRY(cudaGetLastError());
+        if (d_iters_done)
+            MNS_CUDA_TRY(cudaMemcpyAsync(d_iters_done, state + 1, 4, cudaMemcpyDeviceToDevice, stream));
+        return 0;
+    }
     for (int it = 0; it < iters; it++) {
         // sweep 0 reads the implied flat raster (no fill pass, no read traffic)
         const float *cur = it == 0 ? nullptr : ((it & 1) ? pong : ping);

@@ -5,8 +5,10 @@ SURVEY 8(e):
 * one huge image (config c5)     -- row strips of whole root rows; every strip reads a
   16-row read-only halo of the input (all clamped domains of a root lie within 16 rows
   of it) and uses GLOBAL coordinates for clamping, so encode needs no exchange;
-  the Jacobi decode exchanges the 16 boundary rows of the raster with the up/down
-  neighbours after every sweep (NCCL send/recv over NVLink; gloo in the CPU tests);
+  the Jacobi decode runs two sweeps per pass, so it keeps a 32-row raster halo and
+  exchanges the 32 boundary rows with the up/down neighbours after every pass (NCCL
+  send/recv over NVLink; gloo in the CPU tests), plus one unit-map root row per side
+  once per code;
 * full / local search (config c4) -- ranges split across ranks, pool replicated.
 Codes stay on the rank that produced them (root_offsets are strip-local); a
 gather to rank 0 is a plain all_gather of sizes + records when the caller needs it.
@@ -16,7 +18,8 @@ from __future__ import annotations
 
 import ctypes
 
-HALO = 16  # rows: every co-centred domain of a 16x16 root lies within 16 rows of it
+HALO = 16      # rows: every co-centred domain of a 16x16 root lies within 16 rows of it
+DEC_HALO = 32  # decode rasters: two sweeps per pass need the halo of the halo
 
 
 def split(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -29,43 +32,79 @@ def strip_rows(height: int, world: int, rank: int) -> tuple[int, int]:
     return split(height // 16, world, rank)
 
 
-def resident_rows(r0: int, r1: int, height: int) -> tuple[int, int]:
+def resident_rows(r0: int, r1: int, height: int, halo: int = HALO) -> tuple[int, int]:
     """Pixel rows [y_lo, y_hi) a strip needs resident (its rows plus the halo, clipped)."""
-    return max(0, 16 * r0 - HALO), min(height, 16 * r1 + HALO)
+    return max(0, 16 * r0 - halo), min(height, 16 * r1 + halo)
 
 
-def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> None:
-    """After a sweep: send my first/last HALO own rows to the neighbours, receive theirs into my halos.
+def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None,
+                   halo: int = HALO) -> None:
+    """After a sweep: send my first/last `halo` own rows to the neighbours, receive theirs into my halos.
 
-    ``raster`` holds rows [y_lo, y_hi) (resident_rows) of the full image.  Works for any
-    torch.distributed backend (NCCL on GPUs, gloo on CPU).
+    ``raster`` holds rows [y_lo, y_hi) (resident_rows with the same halo) of the full image.  Works
+    for any torch.distributed backend (NCCL on GPUs, gloo on CPU).
     """
     import torch.distributed as dist
 
     if world == 1:
         return
-    y_lo, y_hi = resident_rows(r0, r1, height)
+    if 16 * (r1 - r0) < halo:
+        raise ValueError(f"strip of {16 * (r1 - r0)} rows is thinner than the {halo}-row halo")
+    y_lo, y_hi = resident_rows(r0, r1, height, halo)
     own0, own1 = 16 * r0 - y_lo, 16 * r1 - y_lo
     ops = []
     if rank > 0:
-        ops.append(dist.P2POp(dist.isend, raster[own0: own0 + HALO], rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, raster[own0 - HALO: own0], rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, raster[own0: own0 + halo], rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, raster[own0 - halo: own0], rank - 1, group))
     if rank < world - 1:
-        ops.append(dist.P2POp(dist.isend, raster[own1 - HALO: own1], rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, raster[own1: own1 + HALO], rank + 1, group))
+        ops.append(dist.P2POp(dist.isend, raster[own1 - halo: own1], rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, raster[own1: own1 + halo], rank + 1, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+def unit_map_rows(r0: int, r1: int, height: int) -> tuple[int, int]:
+    """Root rows [u0, u1) of a strip's decoder unit map: its own rows plus one on each side."""
+    return max(0, r0 - 1), min(height // 16, r1 + 1)
+
+
+def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> None:
+    """Swap the boundary root rows of the decoder unit map with the neighbours (once per code).
+
+    ``umap`` is [u1 - u0, W/16 * 32] int32 (unit_map_rows); own rows are [r0 - u0, r1 - u0).
+    """
+    import torch.distributed as dist
+
+    if world == 1:
+        return
+    u0, _ = unit_map_rows(r0, r1, height)
+    own0, own1 = r0 - u0, r1 - u0
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, umap[own0], rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, umap[own0 - 1], rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, umap[own1 - 1], rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, umap[own1], rank + 1, group))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
 
 
 class StripDecoder:
-    """Jacobi decode of one rank's strip: strip-local code + fp32 halo'd ping/pong rasters."""
+    """Jacobi decode of one rank's strip: strip-local code + fp32 halo'd ping/pong rasters.
+
+    Sweeps run two per pass (mns_decode_sweep2) on rasters with DEC_HALO resident rows; the
+    32 boundary rows are exchanged once per pass, and the unit map carries one neighbour root
+    row on each side.  ``code.unit_map`` is rebound to a view of that halo'd map, so an encoder
+    writing into ``code`` fills it in place.
+    """
 
     def __init__(self, code, height: int, width: int, r0: int, r1: int, rank: int = 0, world: int = 1):
         import torch
 
         self.code, self.H, self.W, self.r0, self.r1 = code, height, width, r0, r1
         self.rank, self.world = rank, world
-        self.y_lo, self.y_hi = resident_rows(r0, r1, height)
+        self.y_lo, self.y_hi = resident_rows(r0, r1, height, DEC_HALO)
         dev = code.records.device
         rows = self.y_hi - self.y_lo
         self.ping = torch.empty((rows, width), dtype=torch.float32, device=dev)
@@ -76,32 +115,65 @@ class StripDecoder:
             from .codec import build_unit_map
 
             build_unit_map(code)
+        self.u0, self.u1 = unit_map_rows(r0, r1, height)
+        rw32 = (width // 16) * 32
+        self.umap = torch.zeros((self.u1 - self.u0, rw32), dtype=torch.int32, device=dev)
+        own = self.umap[r0 - self.u0: r1 - self.u0]
+        own.copy_(code.unit_map.view(r1 - r0, rw32))
+        code.unit_map = own.view(-1)
 
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
 
+    def launches(self, iters: int) -> int:
+        """Kernel launches of run(iters): an odd first sweep alone, then two sweeps per pass."""
+        return iters // 2 + (iters & 1)
+
     def run(self, iters: int = 10, initial_value: float = 128.0, stream=None, sweep_events=None, out=None):
-        """iters sweeps (stop_delta = 0); the last writes the rounded uint8 strip into `out` (default self.out)."""
+        """iters sweeps (stop_delta = 0); the last pass writes the rounded uint8 strip into `out` (default self.out).
+
+        sweep_events[i] = (start, end) CUDA events recorded around launch i (see launches()).
+        """
         out = self.out if out is None else out
         from . import _native as N
 
+        if iters < 1:
+            raise ValueError("max_iters must be >= 1")
         L = N.lib()
         s = N.stream_ptr(stream)
-        bufs = (self.ping, self.pong)
-        for it in range(iters):
-            cur = None if it == 0 else bufs[(it - 1) & 1]
-            last = it == iters - 1
-            nxt = None if last else bufs[it & 1]
+        exchange_unit_map_rows(self.umap, self.r0, self.r1, self.H, self.rank, self.world)
+        ob = self._vbase(out, 16 * self.r0, 1)
+        cur, it, n = None, 0, 0
+        if iters & 1:  # odd count: the flat first sweep alone
+            last = iters == 1
             if sweep_events is not None:
-                sweep_events[it][0].record()
-            N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1,
-                                       self._vbase(cur, self.y_lo, 4) if cur is not None else ctypes.c_void_p(0),
+                sweep_events[n][0].record()
+            N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1, ctypes.c_void_p(0),
                                        float(initial_value),
-                                       self._vbase(nxt, self.y_lo, 4) if nxt is not None else ctypes.c_void_p(0),
-                                       self._vbase(out, 16 * self.r0, 1) if last else ctypes.c_void_p(0),
-                                       N.ptr(self.state), 0.0, s))
+                                       ctypes.c_void_p(0) if last else self._vbase(self.pong, self.y_lo, 4),
+                                       ob if last else ctypes.c_void_p(0), N.ptr(self.state), 0.0, s))
             if sweep_events is not None:
-                sweep_events[it][1].record()
-            if not last and self.world > 1:
-                exchange_halos(nxt, self.r0, self.r1, self.H, self.rank, self.world)
+                sweep_events[n][1].record()
+            n += 1
+            it = 1
+            if not last:
+                cur = self.pong
+                exchange_halos(cur, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO)
+        while it < iters:
+            last = it + 2 == iters
+            nxt = None if last else (self.ping if cur is not self.ping else self.pong)
+            if sweep_events is not None:
+                sweep_events[n][0].record()
+            N.check(L.mns_decode_sweep2(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
+                                        self._vbase(cur, self.y_lo, 4) if cur is not None else ctypes.c_void_p(0),
+                                        float(initial_value),
+                                        self._vbase(nxt, self.y_lo, 4) if nxt is not None else ctypes.c_void_p(0),
+                                        ob if last else ctypes.c_void_p(0), s))
+            if sweep_events is not None:
+                sweep_events[n][1].record()
+            n += 1
+            it += 2
+            if not last:
+                exchange_halos(nxt, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO)
+                cur = nxt
         return out

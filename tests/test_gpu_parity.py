@@ -251,3 +251,112 @@ def test_full_search_c4_sample_vs_oracle(mns):
     ref = O.full_search(px, 8, 1, n_iso=1, range_ids=ids)
     assert np.array_equal(dom[ids], ref["dom"])
     assert np.array_equal(res["code"].cpu().numpy()[ids], ref["code"])
+
+
+def _sweeps_single(N, L, umap, W, H, rr, cur, init, n):
+    """n single sweeps (mns_decode_sweep) from cur (None = flat); returns the last fp32 raster."""
+    import ctypes
+
+    state = torch.zeros(4, dtype=torch.int32, device="cuda")
+    for _ in range(n):
+        nxt = torch.full((H, W), float("nan"), device="cuda")
+        N.check(L.mns_decode_sweep(N.ptr(umap), W, H, rr[0], rr[1], N.ptr(cur) if cur is not None else ctypes.c_void_p(0),
+                                   init, N.ptr(nxt), ctypes.c_void_p(0), N.ptr(state), 0.0, None))
+        cur = nxt
+    return cur
+
+
+@pytest.mark.parametrize("W,H,e3,rr", [(512, 512, 8.0, None), (400, 48, 8.0, None), (16, 16, math.inf, None),
+                                       (1024, 1040, math.inf, None), (640, 640, 8.0, (5, 17)),
+                                       (640, 640, math.inf, (0, 3)), (640, 640, 8.0, (37, 40))])
+def test_pair_pass_equals_two_sweeps(mns, W, H, e3, rr):
+    """mns_decode_sweep2 (t -> t+2 in one pass, t+1 on chip) is bit-identical to two single sweeps,
+    on whole images (partial bands, one root row, 2x2-unit-heavy codes) and strip row ranges
+    with a unit map that starts one root row above the strip."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+    from paper_1501_02894_b200.synth import synth_image
+
+    L = N.lib()
+    side = max(W, H)
+    px = np.ascontiguousarray(synth_image(side, 11, noise_sigma=12.0, n_blobs=8)[:H, :W])
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=e3))
+    umap = code.unit_map
+    rh = H // 16
+    r0, r1 = rr if rr is not None else (0, rh)
+    u0 = max(0, r0 - 1)
+    sub = umap[u0 * (W // 16) * 32:]
+    g = torch.Generator(device="cuda").manual_seed(W + H)
+    t0 = torch.rand((H, W), device="cuda", generator=g) * 255.0
+    for cur in (None, t0):
+        want = _sweeps_single(N, L, umap, W, H, (0, rh), cur, 128.0, 2)
+        got = torch.full((H, W), float("nan"), device="cuda")
+        N.check(L.mns_decode_sweep2(N.ptr(sub), u0, W, H, r0, r1, N.ptr(cur) if cur is not None else ctypes.c_void_p(0),
+                                    128.0, N.ptr(got), ctypes.c_void_p(0), None))
+        out = torch.zeros((H, W), dtype=torch.uint8, device="cuda")
+        N.check(L.mns_decode_sweep2(N.ptr(sub), u0, W, H, r0, r1, N.ptr(cur) if cur is not None else ctypes.c_void_p(0),
+                                    128.0, ctypes.c_void_p(0), N.ptr(out), None))
+        torch.cuda.synchronize()
+        y0, y1 = 16 * r0, 16 * r1
+        assert torch.equal(got[y0:y1], want[y0:y1])
+        assert torch.equal(out[y0:y1], torch.floor(want[y0:y1] + 0.5).to(torch.uint8))
+
+
+def test_strip_decoder_matches_whole_decode(mns):
+    """StripDecoder (pair passes, 32-row halos, halo'd unit map) on one GPU, strip by strip with the
+    halos copied between strips by hand, equals the whole-image decode_device."""
+    from paper_1501_02894_b200 import sharding
+    from paper_1501_02894_b200.synth import synth_image
+
+    H = W = 512
+    px = synth_image(H, 9, noise_sigma=10.0, n_blobs=12)
+    cfg = mns.EncoderConfig(e3=8.0)
+    whole = mns.encode_device(torch.from_numpy(px).cuda(), cfg)
+    want, _, _ = mns.decode_device(whole, iters=9)
+    bounds = [0, 7, 19, 32]
+    codes, decs = [], []
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        y0, y1 = max(0, 16 * r0 - 16), min(H, 16 * r1 + 16)
+        c = mns.encode_device(torch.from_numpy(np.ascontiguousarray(px[y0:y1])).cuda(), cfg, root_rows=(r0, r1),
+                              height=H)
+        d = sharding.StripDecoder(c, H, W, r0, r1)
+        codes.append(c)
+        decs.append(d)
+    # unit-map halo rows (what exchange_unit_map_rows does over NCCL)
+    for a, b in zip(decs[:-1], decs[1:]):
+        a.umap[-1].copy_(b.umap[b.r0 - b.u0])
+        b.umap[0].copy_(a.umap[a.r1 - 1 - a.u0])
+    # 9 sweeps = 1 single + 4 pairs, raster halos exchanged by hand after every launch
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+
+    L = N.lib()
+    curs = [None] * 3
+    for n in range(5):
+        nxts = []
+        for i, d in enumerate(decs):
+            last = n == 4
+            nxt = None if last else (d.ping if curs[i] is not d.ping else d.pong)
+            vb = (lambda t: d._vbase(t, d.y_lo, 4))
+            ob = d._vbase(d.out, 16 * d.r0, 1)
+            if n == 0:
+                N.check(L.mns_decode_sweep(N.ptr(d.code.unit_map), W, H, d.r0, d.r1, ctypes.c_void_p(0), 128.0,
+                                           vb(nxt), ctypes.c_void_p(0), N.ptr(d.state), 0.0, None))
+            else:
+                N.check(L.mns_decode_sweep2(N.ptr(d.umap), d.u0, W, H, d.r0, d.r1, vb(curs[i]), 128.0,
+                                            vb(nxt) if nxt is not None else ctypes.c_void_p(0),
+                                            ob if last else ctypes.c_void_p(0), None))
+            nxts.append(nxt)
+        if n < 4:
+            for a, b, ra, rb in zip(decs[:-1], decs[1:], nxts[:-1], nxts[1:]):
+                h = sharding.DEC_HALO
+                a_own1 = 16 * a.r1 - a.y_lo
+                b_own0 = 16 * b.r0 - b.y_lo
+                ra[a_own1: a_own1 + h].copy_(rb[b_own0: b_own0 + h])
+                rb[b_own0 - h: b_own0].copy_(ra[a_own1 - h: a_own1])
+        curs = nxts
+    got = torch.cat([d.out for d in decs])
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)

@@ -54,21 +54,37 @@ def test_split_covers_rows():
                 assert y_lo == max(0, 16 * r0 - 16) and y_hi == min(H, 16 * r1 + 16)
 
 
-def _halo_worker(rank, world, H, W):
+def _halo_worker(rank, world, H, W, halo):
     r0, r1 = sharding.strip_rows(H, world, rank)
-    y_lo, y_hi = sharding.resident_rows(r0, r1, H)
+    y_lo, y_hi = sharding.resident_rows(r0, r1, H, halo)
     rows = torch.arange(y_lo, y_hi, dtype=torch.float32)[:, None].repeat(1, W)
     raster = rows.clone()
     own0, own1 = 16 * r0 - y_lo, 16 * r1 - y_lo
     raster[:own0] = -1.0
     raster[own1:] = -1.0
-    sharding.exchange_halos(raster, r0, r1, H, rank, world)
+    sharding.exchange_halos(raster, r0, r1, H, rank, world, halo=halo)
     assert torch.equal(raster, rows), f"rank {rank}: halo rows not exchanged"
 
 
+@pytest.mark.parametrize("world,halo", [(2, 16), (3, 16), (2, 32), (3, 32)])
+def test_exchange_halos_gloo(world, halo):
+    _run(world, _halo_worker, 128, 48, halo)
+
+
+def _umap_worker(rank, world, H, rw32):
+    r0, r1 = sharding.strip_rows(H, world, rank)
+    u0, u1 = sharding.unit_map_rows(r0, r1, H)
+    want = torch.arange(u0, u1, dtype=torch.int32)[:, None].repeat(1, rw32)
+    umap = want.clone()
+    umap[: r0 - u0] = -1
+    umap[r1 - u0:] = -1
+    sharding.exchange_unit_map_rows(umap, r0, r1, H, rank, world)
+    assert torch.equal(umap, want), f"rank {rank}: unit-map halo rows not exchanged"
+
+
 @pytest.mark.parametrize("world", [2, 3])
-def test_exchange_halos_gloo(world):
-    _run(world, _halo_worker, 128, 48)
+def test_exchange_unit_map_rows_gloo(world):
+    _run(world, _umap_worker, 160, 64)
 
 
 def _strip_decode_worker(rank, world, px, records, iters, out_dir):
@@ -100,6 +116,48 @@ def test_strip_decode_matches_whole_image(world, tmp_path):
     records, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
     iters = 6
     _run(world, _strip_decode_worker, px, records, iters, str(tmp_path))
+    _, whole, _ = O.decode_records(records, 128, 128, max_iters=iters, stop_delta=0.0)
+    strips = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
+    assert np.array_equal(strips, whole)
+
+
+def _pair_decode_worker(rank, world, px, records, iters, out_dir):
+    """Two sweeps per pass like mns_decode_sweep2: sweep A over the strip +- one root row (units
+    of the neighbour rows come from the unit-map halo), sweep B over the strip, then the 32-row
+    raster halo exchange.  Everything outside the resident rows is NaN poison."""
+    from oracle import oracle as O
+
+    H, W = px.shape
+    r0, r1 = sharding.strip_rows(H, world, rank)
+    y_lo, y_hi = sharding.resident_rows(r0, r1, H, sharding.DEC_HALO)
+    u0, u1 = sharding.unit_map_rows(r0, r1, H)
+    units = O.records_to_units(records, W, H)
+    wide = units[(units["y"] >= 16 * u0) & (units["y"] < 16 * u1)]
+    mine = units[(units["y"] >= 16 * r0) & (units["y"] < 16 * r1)]
+    local = torch.full((y_hi - y_lo, W), 128.0, dtype=torch.float64)
+    for _ in range(iters // 2):
+        full = np.full((H, W), np.nan)
+        full[y_lo:y_hi] = local.numpy()
+        mid = O.decode_step_units(wide, full, nthreads=1)
+        keep = np.full((H, W), np.nan)
+        keep[16 * u0: 16 * u1] = mid[16 * u0: 16 * u1]
+        nxt = O.decode_step_units(mine, keep, nthreads=1)
+        local[16 * r0 - y_lo: 16 * r1 - y_lo] = torch.from_numpy(nxt[16 * r0: 16 * r1])
+        sharding.exchange_halos(local, r0, r1, H, rank, world, halo=sharding.DEC_HALO)
+    own = local[16 * r0 - y_lo: 16 * r1 - y_lo].numpy()
+    assert np.isfinite(own).all()
+    np.save(os.path.join(out_dir, f"strip{rank}.npy"), own)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pair_pass_strip_decode_matches_whole_image(world, tmp_path):
+    from oracle import oracle as O
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(128, 23, noise_sigma=10.0, n_blobs=6)
+    records, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
+    iters = 6
+    _run(world, _pair_decode_worker, px, records, iters, str(tmp_path))
     _, whole, _ = O.decode_records(records, 128, 128, max_iters=iters, stop_delta=0.0)
     strips = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
     assert np.array_equal(strips, whole)
