@@ -89,7 +89,8 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
  * sharding: the multi-GPU decoder exchanges 16-row halos between sweeps).
  * cur / nxt / out are bases of the FULL image (row 0) even when only rows
  * [16*root_row_begin - 16, 16*root_row_end + 16) are resident; the unit map is
- * local to the strip's roots.  cur may be NULL on the first sweep: the flat
+ * local to the strip's roots.  cur holds values in [0, 255] (every sweep's
+ * output does; the clip is elided when it provably cannot bind).  cur may be NULL on the first sweep: the flat
  * start raster of initial_value is implied (no fill pass).  nxt may be NULL when
  * out (uint8, rounded) is given: the fused final sweep.  state: 4 int32 zeroed
  * before the first sweep (early-stop bookkeeping when stop_delta > 0). */
@@ -102,7 +103,8 @@ int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, in
  * 16*root_row_end + 32) of cur must be resident (32-row halo; exchanged once per
  * pass on the multi-GPU decoder).  unit_map holds the root rows starting at
  * unit_map_row_begin, which must cover [root_row_begin - 1, root_row_end + 1)
- * clipped to the image.  cur NULL = flat start raster; exactly one of nxt (fp32)
+ * clipped to the image.  cur NULL = flat start raster, else values in [0, 255];
+ * exactly one of nxt (fp32)
  * and out (rounded uint8, final pass) is non-NULL.  Same result as two
  * mns_decode_sweep calls. */
 int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,

@@ -109,11 +109,35 @@ __device__ __forceinline__ Lane lane_of(int lane) {
     return L;
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): same per-lane IEEE rounding as fmaf / fadd.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
 // v[16] = clip(s * (q - mean) + o) of the lane's 4x4 block of root (rxg, ryg) (decoder.py:32-34,
 // transform.py:63-66).  Domain sums q come from the even 2x2-sum lattice ring `lat` (row =
 // absolute raster row / 2 mod QR, column = window column / 2, window origin wx0) or, for 2x2
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
+// The clip is skipped when a warp vote shows no lane can leave [0, 255]: v = fl(a q + b) is
+// monotone in q, so its values at the bounds of q (0 .. 1020 for a raster in [0, 255]; 4 init on
+// the flat start) bound every pixel exactly.
 template <int QSTR, class RawSum>
 __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
                                             const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
@@ -144,8 +168,12 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                 for (int jj = 0; jj < 4; jj++) v[4 * i + jj] = row[jj];
             }
         }
-        own = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) +
-              (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+        const float2 p0 = fadd2(make_float2(v[0], v[1]), make_float2(v[2], v[3]));
+        const float2 p1 = fadd2(make_float2(v[4], v[5]), make_float2(v[6], v[7]));
+        const float2 p2 = fadd2(make_float2(v[8], v[9]), make_float2(v[10], v[11]));
+        const float2 p3 = fadd2(make_float2(v[12], v[13]), make_float2(v[14], v[15]));
+        const float2 pp = fadd2(fadd2(p0, p1), fadd2(p2, p3));
+        own = pp.x + pp.y;
     } else if (live) {  // four 2x2 units with odd (or clamped) 4x4 domains
 #pragma unroll
         for (int c = 0; c < 4; c++) {
@@ -172,17 +200,34 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                         fminf(255.f, fmaxf(0.f, fmaf(0.25f * s, q[2 * i + jj], b)));
         }
     }
-    // unit sums: 4x4 = own block, 8x8 = 4 lanes (lane bits 0,1), 16x16 = the root's 16 lanes
-    float s8 = own + __shfl_xor_sync(FULL, own, 1);
-    s8 += __shfl_xor_sync(FULL, s8, 2);
-    float s16 = s8 + __shfl_xor_sync(FULL, s8, 4);
-    s16 += __shfl_xor_sync(FULL, s16, 8);
+    // unit sums: 4x4 = own block, 8x8 = 4 lanes (lane bits 0,1), 16x16 = the root's 16 lanes; two
+    // shuffle rounds of three independent butterflies (every lane of a group adds the same pair
+    // sums, so the group's sum is bit-identical on all its lanes)
+    const float t1 = __shfl_xor_sync(FULL, own, 1), t2 = __shfl_xor_sync(FULL, own, 2),
+                t3 = __shfl_xor_sync(FULL, own, 3);
+    const float s8 = (own + t1) + (t2 + t3);
+    const float u1 = __shfl_xor_sync(FULL, s8, 4), u2 = __shfl_xor_sync(FULL, s8, 8),
+                u3 = __shfl_xor_sync(FULL, s8, 12);
+    const float s16 = (s8 + u1) + (u2 + u3);
+    bool inside = true;
     if (live && k > 0) {
         const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
         const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
         const float b = fmaf(-sa, mean, sb), a = 0.25f * sa;
+        const float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
 #pragma unroll
-        for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, fmaf(a, v[e], b)));
+        for (int m = 0; m < 8; m++) {
+            const float2 r = ffma2(make_float2(v[2 * m], v[2 * m + 1]), a2, b2);
+            v[2 * m] = r.x;
+            v[2 * m + 1] = r.y;
+        }
+        const float qlo = flat ? 4.f * init : 0.f, qhi = flat ? 4.f * init : 1020.f;
+        const float lo = fmaf(a, a >= 0.f ? qlo : qhi, b), hi = fmaf(a, a >= 0.f ? qhi : qlo, b);
+        inside = lo >= 0.f && hi <= 255.f;
+    }
+    if (!__all_sync(FULL, inside)) {  // (re-clipping the already clipped 2x2-unit pixels is a no-op)
+#pragma unroll
+        for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
     }
 }
 
@@ -352,9 +397,15 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
 // row above and below the CTA's CR2 rows; resident halo 32 rows (mns_decode_sweep2).
 constexpr int WA = BR * 16 + 64;      // 192-px window of raster t: band +- 32 px
 constexpr int QSA = WA / 2 + 4;       // t-lattice row stride (100: rows 2 apart 8 banks apart)
-constexpr int NT = 3;                 // raster-t ring
+#ifndef PAIR_NT
+#define PAIR_NT 3
+#endif
+#ifndef PAIR_CR2
+#define PAIR_CR2 64
+#endif
+constexpr int NT = PAIR_NT;           // raster-t ring
 constexpr int NM = 4;                 // t+1 raw ring (B reads rows i-3..i-1 while A writes i)
-constexpr int CR2 = 64;               // root rows per CTA
+constexpr int CR2 = PAIR_CR2;         // root rows per CTA
 constexpr int NWA = (BR + 2) / 2;     // stage-A warps (two roots each)
 constexpr int DT2 = (NWA + NW) * 32;
 constexpr int TRAW_BYTES = BLK * WA * 4;
@@ -437,12 +488,12 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
     const bool col_ok = rxi >= 0 && rxi < p.rw;
     const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
     const int lag = stage_a ? 0 : 2;  // iteration i: A paints root row i, B paints i - 2
+    const int row_lo = stage_a ? max(r_s - 1, 0) : r_s, row_hi = stage_a ? min(r_e + 1, rh) : r_e;
+    const uint2 *ubase = reinterpret_cast<const uint2 *>(p.unit_map) + ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 +
+                         (lane & 15);
     auto word_of = [&](int row) {
-        const bool ok = col_ok && row >= r_s - (stage_a ? 1 : 0) && row < r_e + (stage_a ? 1 : 0) && row >= 0 &&
-                        row < rh;
-        return ok ? __ldg(reinterpret_cast<const uint2 *>(p.unit_map + (size_t)((row - p.umap_r0) * p.rw + rxi) * 32) +
-                          (lane & 15))
-                  : make_uint2(0u, 0u);
+        return col_ok && row >= row_lo && row < row_hi ? __ldg(ubase + (ptrdiff_t)row * p.rw * 16)
+                                                       : make_uint2(0u, 0u);
     };
     auto raw_t = [&](int R, int C) {  // raster t through L2 (window origin xa0)
         const float *r0 = p.cur + (ptrdiff_t)R * p.W + xa0 + C;
