@@ -55,7 +55,9 @@ typedef struct {
  * record of root i (roots of the processed rows, image-major, raster order;
  * n_roots + 1 entries, the last = total), *d_count = total records (device).
  * capacity must be >= 64 * n_roots.  unit_map (optional, 32 words per root)
- * receives the decoder's unit map.  Workspace: mns_encode_workspace_bytes. */
+ * receives the decoder's unit map.  Workspace: mns_encode_workspace_bytes (64
+ * staged record slots per root + the compaction scan state; two kernels: the
+ * encoder, whose CTAs never wait on one another, then the scan + compaction). */
 int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t root_row_begin, int32_t root_row_end,
                                int64_t *bytes);
 int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,

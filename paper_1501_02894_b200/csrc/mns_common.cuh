@@ -154,8 +154,9 @@ __device__ inline long long lookback_exclusive(unsigned long long *status, long 
 
 // Warp-cooperative decoupled look-back: called by ALL 32 lanes of one warp; the
 // 32 lanes poll 32 predecessors at once (relaxed loads: each status word is a
-// self-contained flag|value), sum aggregates up to the nearest inclusive prefix,
-// and slide the window back until one is found.  Returns the exclusive prefix
+// self-contained flag|value), wait only until every predecessor up to the nearest
+// inclusive prefix has published (not the whole window), sum those aggregates, and
+// slide the window back while none is inclusive.  Returns the exclusive prefix
 // (same value in every lane).
 __device__ inline long long lookback_exclusive_warp(unsigned long long *status, long long tile, long long agg) {
     const int lane = threadIdx.x & 31;
@@ -169,11 +170,14 @@ __device__ inline long long lookback_exclusive_warp(unsigned long long *status, 
     while (true) {
         const long long idx = base - lane;
         unsigned long long v = idx >= 0 ? ld_relaxed_u64(&status[idx]) : LB_PREFIX;
-        while (__any_sync(0xffffffffu, (v & ~LB_MASK) == 0)) {
+        unsigned pm;
+        while (true) {  // wait only for the predecessors up to the nearest inclusive prefix
+            const unsigned inv = __ballot_sync(0xffffffffu, (v & ~LB_MASK) == 0);
+            pm = __ballot_sync(0xffffffffu, (v & ~LB_MASK) == LB_PREFIX);
+            if (inv == 0 || (pm && __ffs(pm) < __ffs(inv))) break;
             __nanosleep(20);
             if ((v & ~LB_MASK) == 0) v = ld_relaxed_u64(&status[idx]);
         }
-        const unsigned pm = __ballot_sync(0xffffffffu, (v & ~LB_MASK) == LB_PREFIX);
         const int first = pm ? __ffs(pm) - 1 : 32;  // nearest predecessor holding an inclusive prefix
         long long c = lane <= first ? (long long)(v & LB_MASK) : 0;
 #pragma unroll

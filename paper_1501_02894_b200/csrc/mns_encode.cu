@@ -1,13 +1,13 @@
 // MNS quadtree encoder for sm_100a: block moments (K1) + phase-1/phase-2 matcher
-// with DFS compaction (K2) in ONE single-pass kernel.
+// + per-root DFS emission (K2) in one kernel, then a scan + compaction kernel.
 //
 // Replaces the reference's per-node Python recursion
 //   encoder.py:215-246 encode_quadtree / visit, :145-166 try_phase1,
 //   :169-212 try_phase2, image.py:146-187 block helpers, transform.py:23-80.
 //
-// Work decomposition: one CTA = up to 8 consecutive 16x16 roots of one root row
-// (one warp per root).  The CTA stages the uint8 window [x0-16, x0+144) x
-// [y0-16, y0+32) (every clamped domain of every node of its roots lies inside,
+// Work decomposition: one CTA = up to TR = 16 consecutive 16x16 roots of one root
+// row (warp w owns roots w and w + 8).  The CTA stages the uint8 window
+// [x0-16, x0+16*TR+16) x [y0-16, y0+32) (every clamped domain of every node of its roots lies inside,
 // SURVEY 7 "geometry") with 16-byte coalesced loads, and builds the table of
 // even-phase 2x2 pixel sums q (0..1020, u16) with packed SIMD-in-register adds.
 // Levels 1-3 read q from that table (their domain origins are always even);
@@ -23,7 +23,9 @@
 //               fp64 evaluation emulated bit-exactly (no FMA, numpy pairwise sum).
 // Emission: leaves are keyed by the Morton index of their top-left 2x2 cell
 //   (= reference DFS order TL,TR,BL,BR); lane l owns cells 2l, 2l+1, so a warp
-//   compacts its root with two ballots; CTAs chain with a decoupled look-back.
+//   compacts its root with two ballots into the root's 64 staged slots;
+//   compact_records_kernel scans the per-root counts (decoupled look-back over
+//   uniform tiles) and copies the records to their final offsets.
 
 #include <math.h>
 
@@ -36,7 +38,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int EW = 8;                // warps per CTA
 constexpr int ET = EW * 32;
 constexpr int RPW = 2;               // roots encoded by each warp per tile (in turn)
-constexpr int TR = EW * RPW;         // 32 consecutive roots of one root row per tile
+constexpr int TR = EW * RPW;         // 16 consecutive roots of one root row per tile
+static_assert(RPW == 2, "the warp-local decision rounds map two roots onto one warp");
 constexpr int WIN_W = TR * 16 + 32;  // 544
 constexpr int WIN_H = 48;
 constexpr int QE_W = WIN_W / 2;      // 272
@@ -51,22 +54,15 @@ struct EncParams {
     double p2b[4];  // bound(E_level): phase-2 quadrant accepts iff SSE <= n_k * p2b
     double tol[4];  // E_level (emulation path compares rms > tol like the reference)
     double mean_tol;
-    uint64_t *out;
+    uint64_t *stage;     // 64 record slots per root (workspace); compacted by compact_records_kernel
     uint32_t *unit_map;  // optional: decoder unit map (mns_record.h), 32 words per root
-    int32_t *root_offsets;
-    int64_t *count;
-    unsigned long long *status;
-    long long n_tiles, n_roots;
+    int32_t *root_cnt;   // per-root record counts (root_offsets, scanned in place by the compaction)
+    long long n_roots;
 };
 
 struct Mom {
     int sr, srr, sq, sqq, sqr;
 };
-
-__device__ __forceinline__ int xsum(int v, int G) {
-    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
 
 // 2^-k as an exact double
 __device__ __forceinline__ double pow2neg(int k) { return __longlong_as_double((long long)(1023 - k) << 52); }
@@ -179,11 +175,9 @@ struct TileSmem {
     int sr4[TR][64], srr4[TR][64];  // level-4 range sums (q moments are computed lazily)
     uint64_t rec1[TR], rec2[TR][4], rec3[TR][16], rec4[TR][64];
     uint8_t acc1[TR], acc2[TR][4], acc3[TR][16];
-    int root_cnt[TR];
-    long long root_base[TR];
 };
 constexpr int TILE_SMEM = (int)sizeof(TileSmem);
-constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + TR * 64 * 8 + TILE_SMEM + 64;
+constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + TILE_SMEM + 64;
 
 struct Win {  // the staged window and the tile/image geometry a decision thread needs
     const uint8_t (*pix)[WIN_W];
@@ -252,12 +246,50 @@ __device__ bool phase2_node(const Win &w, const EncParams &p, int slot, int leve
     return true;
 }
 
+// Phase 1 + phase 2 of one level-1/2 node with its 4 quadrants on 4 consecutive lanes (lane & 3 =
+// quadrant): same decisions as phase1 / phase2_node, the fp64 quadrant tests in parallel.  Every
+// lane of the warp must call it (ballots); lanes with !live take no part.  Returns the record on
+// the group's quadrant-0 lane via acc / rec.
+__device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p, bool live, int slot, int level,
+                                                int nx, int ny, const Mom &m, const Mom *kids, bool try_node,
+                                                bool &acc, uint64_t &rec) {
+    const int lane = threadIdx.x & 31, quad = lane & 3;
+    const int size = 32 >> level, nlog2 = 2 * (5 - level);
+    acc = false;
+    rec = 0;
+    bool want2 = false, ok = false;
+    int bit = 0;
+    Node2 z{};
+    if (live && try_node) {
+        rec = phase1(w.x0 + 16 * slot + nx, w.y0 + ny, level, nlog2, m, p.p1b[level], acc);
+        if (!acc && p.mns) {
+            z = p2_node(nlog2, m.sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
+                        p.mean_tol);
+            want2 = z.pass;
+            if (want2) {
+                const double slo = level == 1 ? 0.2 : 0.4, shi = level == 1 ? 0.5 : 0.65;
+                const int h = size / 2;
+                int res = p2_quad(nlog2 - 2, kids[quad], z.t[quad], slo, shi, p.p2b[level] * (double)(h * h), bit);
+                if (res == 2)
+                    res = emulate_quadrant(w, slot, nx + (quad & 1) * h, ny + (quad >> 1) * h, h, kids[quad],
+                                           z.t[quad], slo, shi, p.tol[level], bit);
+                ok = res == 1;
+            }
+        }
+    }
+    const unsigned okm = __ballot_sync(FULL, ok), bitm = __ballot_sync(FULL, bit != 0);
+    const int g = lane & ~3;
+    if (want2 && ((okm >> g) & 15u) == 15u) {
+        acc = true;
+        rec = mns_rec_phase2(w.x0 + 16 * slot + nx, w.y0 + ny, level, z.o, z.d0, z.d1, z.d2, (int)((bitm >> g) & 15u));
+    }
+}
+
 __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const EncParams p) {
     extern __shared__ __align__(16) unsigned char esm[];
-    uint64_t(*stage)[64] = reinterpret_cast<uint64_t(*)[64]>(esm);  // per-root records, DFS order
-    TileSmem &ts = *reinterpret_cast<TileSmem *>(esm + TR * 64 * 8);
-    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TR * 64 * 8 + TILE_SMEM);
-    uint16_t(*qe)[QE_W] = reinterpret_cast<uint16_t(*)[QE_W]>(esm + TR * 64 * 8 + TILE_SMEM + WIN_H * WIN_W);
+    TileSmem &ts = *reinterpret_cast<TileSmem *>(esm);
+    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TILE_SMEM);
+    uint16_t(*qe)[QE_W] = reinterpret_cast<uint16_t(*)[QE_W]>(esm + TILE_SMEM + WIN_H * WIN_W);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long tile = blockIdx.x;
@@ -365,71 +397,76 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const EncParams p) {
             if (lane == 0) ts.m1[slot] = Mom{v[0], v[1], v[2], v[3], v[4]};
         }
     }
-    __syncthreads();
+    __syncwarp();
 
-    // ---- K2: node-parallel decisions, level by level (one thread per node)
+    // ---- K2: decisions, warp-local (warp w owns root slots w, w + EW: everything from here to
+    // the emission reads only this warp's moments, so no CTA barrier).  Round 1: level-1 nodes
+    // on lanes 8-9 and level-2 nodes on lanes 0-7 (a level-2 node is decided whether or not its
+    // root is accepted -- the emission's visibility flags discard covered decisions); round 2:
+    // the visible level-3 nodes (and the level-4 quartets below them), one per lane.
     const bool mns = p.mns != 0;
-    if (tid < nr) {  // level 1: one thread per root
-        const int s = tid;
-        bool acc = false;
-        uint64_t rec = 0;
-        if (try1) {
-            rec = phase1(x0 + 16 * s, y0, 1, 8, ts.m1[s], p.p1b[1], acc);
-            if (!acc && mns) acc = phase2_node(w, p, s, 1, 0, 0, 16, ts.m1[s].sr, ts.m2[s], &rec);
+    {  // round 1: the 8 level-2 nodes of this warp's two roots x 4 quadrant lanes
+        const int node = lane >> 2, s = warp + EW * (node >> 2), k = node & 3;
+        const bool live = s < nr;
+        const int sc = live ? s : 0;
+        bool acc;
+        uint64_t rec;
+        node_quad_lanes(w, p, live, sc, 2, node2_x(k), node2_y(k), ts.m2[sc][k], &ts.m3[sc][4 * k], true, acc, rec);
+        if (live && (lane & 3) == 0) {
+            ts.acc2[s][k] = acc;
+            ts.rec2[s][k] = rec;
         }
-        ts.acc1[s] = acc;
-        ts.rec1[s] = rec;
     }
-    __syncthreads();
-    if (tid < 4 * nr) {  // level 2: one thread per node
-        const int s = tid >> 2, k = tid & 3;
-        const bool vis = p.root_level == 2 || !ts.acc1[s];
-        bool acc = false;
-        uint64_t rec = 0;
-        if (vis) {
-            const int nx = node2_x(k), ny = node2_y(k);
-            rec = phase1(x0 + 16 * s + nx, y0 + ny, 2, 6, ts.m2[s][k], p.p1b[2], acc);
-            if (!acc && mns) acc = phase2_node(w, p, s, 2, nx, ny, 8, ts.m2[s][k].sr, &ts.m3[s][4 * k], &rec);
+    {  // round 2: the 2 level-1 roots x 4 quadrant lanes (lanes 0-7)
+        const int s = warp + EW * (lane >> 2);
+        const bool live = lane < 8 && s < nr;
+        const int sc = live ? s : 0;
+        bool acc;
+        uint64_t rec;
+        node_quad_lanes(w, p, live, sc, 1, 0, 0, ts.m1[sc], ts.m2[sc], try1, acc, rec);
+        if (live && (lane & 3) == 0) {
+            ts.acc1[s] = acc;
+            ts.rec1[s] = rec;
         }
-        ts.acc2[s][k] = acc;
-        ts.rec2[s][k] = rec;
     }
-    __syncthreads();
-    for (int t = tid; t < 16 * nr; t += ET) {  // level 3 (and the level-4 quartets below it)
-        const int s = t >> 4, m = t & 15;
-        const bool vis = (p.root_level == 2 || !ts.acc1[s]) && !ts.acc2[s][m >> 2];
-        bool acc = false;
-        uint64_t rec = 0;
-        if (vis) {
-            const int nx = node3_x(m), ny = node3_y(m);
-            rec = phase1(x0 + 16 * s + nx, y0 + ny, 3, 4, ts.m3[s][m], p.p1b[3], acc);
-            if (!acc) {  // level-4 moments (odd-phase domains) of the 4 children, then phase 2 / split
-                Mom k4[4];
-                for (int c = 0; c < 4; c++) {
-                    const int cx = nx + 2 * (c & 1), cy = ny + 2 * (c >> 1);
-                    Mom mm{ts.sr4[s][4 * m + c], ts.srr4[s][4 * m + c], 0, 0, 0};
-                    for (int i = 0; i < 2; i++)
-                        for (int j = 0; j < 2; j++) {
-                            const int q = dom_q(w, s, cx, cy, 2, cx + j, cy + i);
-                            mm.sq += q;
-                            mm.sqq += q * q;
-                            mm.sqr += q * pixel(w, s, cx + j, cy + i);
-                        }
-                    k4[c] = mm;
-                }
-                if (mns) acc = phase2_node(w, p, s, 3, nx, ny, 4, ts.m3[s][m].sr, k4, &rec);
-                if (!acc)
+    __syncwarp();
+    {
+        const int s = warp + EW * (lane >> 4), m = lane & 15;
+        if (s < nr) {
+            const bool vis = (p.root_level == 2 || !ts.acc1[s]) && !ts.acc2[s][m >> 2];
+            bool acc = false;
+            uint64_t rec = 0;
+            if (vis) {
+                const int nx = node3_x(m), ny = node3_y(m);
+                rec = phase1(x0 + 16 * s + nx, y0 + ny, 3, 4, ts.m3[s][m], p.p1b[3], acc);
+                if (!acc) {  // level-4 moments (odd-phase domains) of the 4 children, then phase 2 / split
+                    Mom k4[4];
                     for (int c = 0; c < 4; c++) {
-                        bool dummy;
-                        ts.rec4[s][4 * m + c] =
-                            phase1(x0 + 16 * s + nx + 2 * (c & 1), y0 + ny + 2 * (c >> 1), 4, 2, k4[c], INFINITY, dummy);
+                        const int cx = nx + 2 * (c & 1), cy = ny + 2 * (c >> 1);
+                        Mom mm{ts.sr4[s][4 * m + c], ts.srr4[s][4 * m + c], 0, 0, 0};
+                        for (int i = 0; i < 2; i++)
+                            for (int j = 0; j < 2; j++) {
+                                const int q = dom_q(w, s, cx, cy, 2, cx + j, cy + i);
+                                mm.sq += q;
+                                mm.sqq += q * q;
+                                mm.sqr += q * pixel(w, s, cx + j, cy + i);
+                            }
+                        k4[c] = mm;
                     }
+                    if (mns) acc = phase2_node(w, p, s, 3, nx, ny, 4, ts.m3[s][m].sr, k4, &rec);
+                    if (!acc)
+                        for (int c = 0; c < 4; c++) {
+                            bool dummy;
+                            ts.rec4[s][4 * m + c] = phase1(x0 + 16 * s + nx + 2 * (c & 1), y0 + ny + 2 * (c >> 1), 4,
+                                                           2, k4[c], INFINITY, dummy);
+                        }
+                }
             }
+            ts.acc3[s][m] = acc;
+            ts.rec3[s][m] = rec;
         }
-        ts.acc3[s][m] = acc;
-        ts.rec3[s][m] = rec;
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- K2b: DFS (Morton) emission per root: lane owns cells 2l, 2l+1; unit map words
     for (int slot = warp; slot < nr; slot += EW) {
@@ -461,50 +498,93 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const EncParams p) {
         const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
         const unsigned lt = lanemask_lt();
         const int offA = __popc(bA & lt) + __popc(bB & lt);
-        if (hasA) stage[slot][offA] = recA;
-        if (hasB) stage[slot][offA + (hasA ? 1 : 0)] = recB;
-        if (lane == 0) ts.root_cnt[slot] = __popc(bA) + __popc(bB);
+        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
+        uint64_t *st = p.stage + root * 64;
+        if (hasA) st[offA] = recA;
+        if (hasB) st[offA + (hasA ? 1 : 0)] = recB;
+        if (lane == 0) p.root_cnt[root] = __popc(bA) + __popc(bB);
         if (p.unit_map) {
             const int rxg = x0 + 16 * slot, lx = node4_x(2 * lane), ly = node4_y(2 * lane);
             const uint32_t umap = (uint32_t)mns_unit_of_record(cov, rxg, y0, lx, ly) |
                                   ((uint32_t)mns_unit_of_record(vis4 ? recB : cov, rxg, y0, lx + 2, ly) << 16);
-            const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
             p.unit_map[root * 32 + lane] = umap;
         }
     }
+}
+
+// Compaction (second half of the encode): exclusive scan of the per-root counts into
+// root_offsets (in place) with a decoupled look-back over uniform 2048-root tiles, then a
+// coalesced copy of every root's staged records to its offset.  Keeping the scan out of the
+// encoder means no encoder CTA ever waits on another.
+constexpr int CT_THREADS = 256, CT_PER = 8, CT_ROOTS = CT_THREADS * CT_PER;
+
+__global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint64_t *stage, int32_t *root_offsets,
+                                                                     long long n_roots, uint64_t *out,
+                                                                     int64_t *count, unsigned long long *status) {
+    __shared__ int offs[CT_ROOTS], cnts[CT_ROOTS];
+    __shared__ int warp_tot[CT_THREADS / 32];
+    __shared__ long long tile_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long tile = blockIdx.x, r0 = tile * CT_ROOTS;
+    int c[CT_PER], run = 0;
+#pragma unroll
+    for (int i = 0; i < CT_PER; i++) {
+        const long long r = r0 + tid * CT_PER + i;
+        c[i] = r < n_roots ? root_offsets[r] : 0;
+        run += c[i];
+    }
+    int incl = run;  // block-wide inclusive scan of the thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
-    // ---- one decoupled look-back per 32 roots, then coalesced record copies
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < CT_THREADS / 32; k++) {
+        wbase += k < warp ? warp_tot[k] : 0;
+        total += warp_tot[k];
+    }
     if (warp == 0) {
-        long long agg = 0;
-        for (int k = 0; k < nr; k++) agg += ts.root_cnt[k];
-        const long long base = lookback_exclusive_warp(p.status, tile, agg);
-        if (lane == 0) {
-            const long long root0 = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0;
-            long long run = base;
-            for (int k = 0; k < nr; k++) {
-                ts.root_base[k] = run;
-                p.root_offsets[root0 + k] = (int32_t)run;
-                run += ts.root_cnt[k];
-            }
-            if (tile == p.n_tiles - 1) {
-                p.root_offsets[p.n_roots] = (int32_t)run;
-                *p.count = run;
-            }
-        }
+        const long long b = lookback_exclusive_warp(status, tile, total);
+        if (lane == 0) tile_base = b;
+    }
+    int e = wbase + incl - run;
+#pragma unroll
+    for (int i = 0; i < CT_PER; i++) {
+        offs[tid * CT_PER + i] = e;
+        cnts[tid * CT_PER + i] = c[i];
+        e += c[i];
     }
     __syncthreads();
-    for (int k = warp; k < nr; k += EW) {
-        const long long b0 = ts.root_base[k];
-        for (int i = lane; i < ts.root_cnt[k]; i += 32) p.out[b0 + i] = stage[k][i];
+    const long long base = tile_base;
+#pragma unroll
+    for (int i = 0; i < CT_PER; i++) {
+        const long long r = r0 + tid * CT_PER + i;
+        if (r < n_roots) root_offsets[r] = (int32_t)(base + offs[tid * CT_PER + i]);
+    }
+    if (r0 + CT_ROOTS >= n_roots && tid == 0) {  // last tile
+        root_offsets[n_roots] = (int32_t)(base + total);
+        *count = base + total;
+    }
+    for (int k = warp; k < CT_ROOTS && r0 + k < n_roots; k += CT_THREADS / 32) {
+        const int n = cnts[k];
+        const uint64_t *src = stage + (r0 + k) * 64;
+        uint64_t *dst = out + base + offs[k];
+        for (int i = lane; i < n; i += 32) dst[i] = src[i];
     }
 }
 
 }  // namespace
 
+static long long compact_tiles(long long n_roots) { return (n_roots + CT_ROOTS - 1) / CT_ROOTS; }
+
 int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes) {
-    const int rw = width / 16;
-    const long long tiles = (long long)n_images * (rr1 - rr0) * ((rw + TR - 1) / TR);
-    *bytes = tiles * 8;
+    const long long n_roots = (long long)n_images * (rr1 - rr0) * (width / 16);
+    // [compaction look-back status, 256-B aligned][64 staged record slots per root]
+    *bytes = ((compact_tiles(n_roots) * 8 + 255) / 256) * 256 + n_roots * 64 * 8;
     return 0;
 }
 
@@ -526,6 +606,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     int64_t need;
     encode_workspace_bytes(W, n_images, rr0, rr1, &need);
     MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
+    MNS_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "workspace must be 16-byte aligned");
 
     EncParams p{};
     p.img = img;
@@ -550,20 +631,24 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     }
     p.p1b[4] = INFINITY;
     p.mean_tol = cfg->mean_tol;
-    p.out = records;
+    const long long ctiles = compact_tiles(n_roots);
+    const size_t status_bytes = ((ctiles * 8 + 255) / 256) * 256;
+    unsigned long long *status = reinterpret_cast<unsigned long long *>(workspace);
+    p.stage = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(workspace) + status_bytes);
     p.unit_map = unit_map;
-    p.root_offsets = root_offsets;
-    p.count = d_count;
-    p.status = reinterpret_cast<unsigned long long *>(workspace);
-    p.n_tiles = need / 8;
+    p.root_cnt = root_offsets;
     p.n_roots = n_roots;
-    MNS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, stream));
+    MNS_CUDA_TRY(cudaMemsetAsync(status, 0, ctiles * 8, stream));
     static bool attr_set = false;
     if (!attr_set) {
         MNS_CUDA_TRY(cudaFuncSetAttribute(mns_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC_SMEM));
         attr_set = true;
     }
-    mns_encode_kernel<<<(unsigned)p.n_tiles, ET, ENC_SMEM, stream>>>(p);
+    const long long n_tiles = (long long)n_images * p.rows * p.tiles_per_row;
+    mns_encode_kernel<<<(unsigned)n_tiles, ET, ENC_SMEM, stream>>>(p);
+    MNS_CUDA_TRY(cudaGetLastError());
+    compact_records_kernel<<<(unsigned)ctiles, CT_THREADS, 0, stream>>>(p.stage, root_offsets, n_roots, records,
+                                                                        d_count, status);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
