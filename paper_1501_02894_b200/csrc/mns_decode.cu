@@ -136,22 +136,39 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
 // The clip is skipped when a warp vote shows no lane can leave [0, 255]: v = fl(a q + b) is
-// monotone in q, so its values at the bounds of q (0 .. 1020 for a raster in [0, 255]; 4 init on
-// the flat start) bound every pixel exactly.
+// monotone in q, so its values at the bounds of q (0 .. 1020 for a raster in [0, 255]) bound
+// every pixel exactly.
 template <int QSTR, class RawSum>
 __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
                                             const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
                                             bool interior, int W, int H, float (&v)[16]) {
+    if (flat) {
+        // Flat start raster (kernel-uniform): every domain mean is init exactly (sums of equal
+        // power-of-two multiples of init are exact), so each unit paints the constant
+        // clip(fl(s/4 * 4 init + fl(o - s init))) -- the generic path's value, without its loads,
+        // sums and shuffles.
+        if (live) {
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t d = c == 0 ? word.x & 0xFFFFu
+                                          : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
+                const float sc = st[d & 15];
+                const float x = fminf(255.f, fmaxf(0.f, fmaf(0.25f * sc, 4.f * init, fmaf(-sc, init, unit_o(d)))));
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int jj = 0; jj < 2; jj++) v[4 * (2 * (c >> 1) + i) + 2 * (c & 1) + jj] = x;
+            }
+        }
+        return;
+    }
     const uint32_t d0 = word.x & 0xFFFFu;
     const int k = (int)(d0 >> 14);  // log2(side) - 1 of the unit holding cell 0
     float own = 0.f, sa = 0.f, sb = 0.f;
     if (live && k > 0) {  // one unit of side >= 4 covers the 4x4 block
         sa = st[d0 & 15];
         sb = unit_o(d0);
-        if (flat) {
-#pragma unroll
-            for (int e = 0; e < 16; e++) v[e] = 4.f * init;
-        } else {
+        {
             int X, Y;
             if (interior) {
                 X = (int)((L.tx >> (6 * k)) & 63);
@@ -180,10 +197,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             const uint32_t d = c == 0 ? d0 : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
             const int px = L.lx + 2 * (c & 1), py = L.ly + 2 * (c >> 1);
             float q[4];
-            if (flat) {
-#pragma unroll
-                for (int e = 0; e < 4; e++) q[e] = 4.f * init;
-            } else {
+            {
                 const int dx = clampi(rxg + px - 1, 0, W - 4), dy = clampi(ryg + py - 1, 0, H - 4);
 #pragma unroll
                 for (int i = 0; i < 2; i++)
@@ -221,8 +235,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             v[2 * m] = r.x;
             v[2 * m + 1] = r.y;
         }
-        const float qlo = flat ? 4.f * init : 0.f, qhi = flat ? 4.f * init : 1020.f;
-        const float lo = fmaf(a, a >= 0.f ? qlo : qhi, b), hi = fmaf(a, a >= 0.f ? qhi : qlo, b);
+        const float lo = fmaf(a, a >= 0.f ? 0.f : 1020.f, b), hi = fmaf(a, a >= 0.f ? 1020.f : 0.f, b);
         inside = lo >= 0.f && hi <= 255.f;
     }
     if (!__all_sync(FULL, inside)) {  // (re-clipping the already clipped 2x2-unit pixels is a no-op)

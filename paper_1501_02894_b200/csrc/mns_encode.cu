@@ -521,7 +521,7 @@ constexpr int CT_THREADS = 256, CT_PER = 8, CT_ROOTS = CT_THREADS * CT_PER;
 __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint64_t *stage, int32_t *root_offsets,
                                                                      long long n_roots, uint64_t *out,
                                                                      int64_t *count, unsigned long long *status) {
-    __shared__ int offs[CT_ROOTS], cnts[CT_ROOTS];
+    __shared__ int offs[CT_ROOTS];
     __shared__ int warp_tot[CT_THREADS / 32];
     __shared__ long long tile_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -555,7 +555,6 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
 #pragma unroll
     for (int i = 0; i < CT_PER; i++) {
         offs[tid * CT_PER + i] = e;
-        cnts[tid * CT_PER + i] = c[i];
         e += c[i];
     }
     __syncthreads();
@@ -569,11 +568,33 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
         root_offsets[n_roots] = (int32_t)(base + total);
         *count = base + total;
     }
-    for (int k = warp; k < CT_ROOTS && r0 + k < n_roots; k += CT_THREADS / 32) {
-        const int n = cnts[k];
-        const uint64_t *src = stage + (r0 + k) * 64;
-        uint64_t *dst = out + base + offs[k];
-        for (int i = lane; i < n; i += 32) dst[i] = src[i];
+    // flattened copy: output record j of the tile comes from the root whose range holds j
+    // (binary search over the tile's offsets); 4 independent read-only loads per thread in flight
+    const int nr_tile = (int)min((long long)CT_ROOTS, n_roots - r0);
+    auto root_of = [&](int j) {
+        int lo = 0, hi = nr_tile - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (offs[mid] <= j) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    };
+    uint64_t *dst = out + base;
+    for (int j0 = 0; j0 < total; j0 += 4 * CT_THREADS) {
+        uint64_t v[4];
+        int jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            jj[u] = j0 + u * CT_THREADS + tid;
+            if (jj[u] < total) {
+                const int k = root_of(jj[u]);
+                v[u] = __ldg(stage + (r0 + k) * 64 + (jj[u] - offs[k]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (jj[u] < total) dst[jj[u]] = v[u];
     }
 }
 
