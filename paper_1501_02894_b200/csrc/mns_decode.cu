@@ -36,7 +36,10 @@ constexpr int DT = NW * 32;
 constexpr int WINW = BR * 16 + 32;    // 160-px window: band +- 16 px (every clamped domain lies inside)
 constexpr int QW = WINW / 2;          // 80 columns of the even 2x2-sum lattice
 constexpr int QS = QW + 4;            // padded row stride (rows 2 apart land 8 banks apart)
+constexpr int QH = QW / 2;            // lattice rows are stored de-interleaved: even columns, then odd
+constexpr int WINWP = WINW + 4;       // t+1 raw-ring row stride (rows 4 apart land 16 banks apart)
 constexpr int QR = 32;                // lattice ring rows (24 live + 8 being built)
+constexpr int QRP = QR + 3;           // + copies of ring rows 0..2, so a 4-row read never wraps
 constexpr int BLK = 16;               // raster rows per TMA block
 constexpr int NBUF = 5;               // raw ring: 3 blocks readable by compute + 2 in flight
 constexpr int CR = 32;                // root rows walked by one CTA
@@ -109,6 +112,22 @@ __device__ __forceinline__ Lane lane_of(int lane) {
     return L;
 }
 
+// Lattice rows are de-interleaved (column c at (c & 1) * HALF + c / 2): the 4 columns a lane
+// reads come from two base pointers with immediate offsets, and the lanes of a warp, whose
+// columns all share one parity, spread over all 32 banks.  Store the pair of columns (c, c+1),
+// c even, at ring row r (mod QR) and, for ring rows 0..2, at their padded copies.
+template <int QSTR, int HALF>
+__device__ __forceinline__ void lat_store(float *lat, int r, int c, float2 val) {
+    const int rr = r & (QR - 1);
+    float *row = lat + rr * QSTR + (c >> 1);
+    row[0] = val.x;
+    row[HALF] = val.y;
+    if (rr < QRP - QR) {
+        row[QR * QSTR] = val.x;
+        row[QR * QSTR + HALF] = val.y;
+    }
+}
+
 // Packed fp32 pairs (sm_100 FFMA2 / FADD2): same per-lane IEEE rounding as fmaf / fadd.
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     float2 d;
@@ -135,10 +154,7 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // absolute raster row / 2 mod QR, column = window column / 2, window origin wx0) or, for 2x2
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
-// The clip is skipped when a warp vote shows no lane can leave [0, 255]: v = fl(a q + b) is
-// monotone in q, so its values at the bounds of q (0 .. 1020 for a raster in [0, 255]) bound
-// every pixel exactly.
-template <int QSTR, class RawSum>
+template <int QSTR, int HALF, class RawSum>
 __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
                                             const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
                                             bool interior, int W, int H, float (&v)[16]) {
@@ -178,11 +194,15 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                 Y = clamped_offset(L.ly, 2 << k, ryg, H);
             }
             const int qr = (ryg - 16 + Y) >> 1, qc = (rxg - 16 + X - wx0) >> 1;
+            const float *row = lat + (qr & (QR - 1)) * QSTR;  // rows +0..+3 stay inside QRP
+            const float *p0 = row + (qc & 1) * HALF + (qc >> 1);              // columns qc, qc + 2
+            const float *p1 = row + ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);  // columns qc + 1, qc + 3
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const float *row = lat + ((qr + i) & (QR - 1)) * QSTR + qc;
-#pragma unroll
-                for (int jj = 0; jj < 4; jj++) v[4 * i + jj] = row[jj];
+                v[4 * i + 0] = p0[i * QSTR];
+                v[4 * i + 1] = p1[i * QSTR];
+                v[4 * i + 2] = p0[i * QSTR + 1];
+                v[4 * i + 3] = p1[i * QSTR + 1];
             }
         }
         const float2 p0 = fadd2(make_float2(v[0], v[1]), make_float2(v[2], v[3]));
@@ -223,7 +243,6 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
     const float u1 = __shfl_xor_sync(FULL, s8, 4), u2 = __shfl_xor_sync(FULL, s8, 8),
                 u3 = __shfl_xor_sync(FULL, s8, 12);
     const float s16 = (s8 + u1) + (u2 + u3);
-    bool inside = true;
     if (live && k > 0) {
         const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
         const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
@@ -235,10 +254,6 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             v[2 * m] = r.x;
             v[2 * m + 1] = r.y;
         }
-        const float lo = fmaf(a, a >= 0.f ? 0.f : 1020.f, b), hi = fmaf(a, a >= 0.f ? 1020.f : 0.f, b);
-        inside = lo >= 0.f && hi <= 255.f;
-    }
-    if (!__all_sync(FULL, inside)) {  // (re-clipping the already clipped 2x2-unit pixels is a no-op)
 #pragma unroll
         for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
     }
@@ -247,18 +262,19 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
 // fp32 -> rounded uint8 rows of a 4x4 block (floor(x + 0.5); x is already clipped to [0, 255])
 __device__ __forceinline__ void store_block(const float (&v)[16], float *nxt, uint8_t *out, int W, int gx, int gy) {
     if (nxt) {
+        float *d = nxt + (ptrdiff_t)gy * W + gx;
 #pragma unroll
-        for (int i = 0; i < 4; i++)
-            *reinterpret_cast<float4 *>(nxt + (ptrdiff_t)(gy + i) * W + gx) =
-                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        for (int i = 0; i < 4; i++, d += W)
+            *reinterpret_cast<float4 *>(d) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
     if (out) {
+        uint8_t *d = out + (ptrdiff_t)gy * W + gx;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
+        for (int i = 0; i < 4; i++, d += W) {
             uint32_t w = 0;
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) w |= (uint32_t)floorf(v[4 * i + jj] + 0.5f) << (8 * jj);
-            *reinterpret_cast<uint32_t *>(out + (ptrdiff_t)(gy + i) * W + gx) = w;
+            *reinterpret_cast<uint32_t *>(d) = w;
         }
     }
 }
@@ -320,8 +336,8 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
                 const float4 u = *reinterpret_cast<const float4 *>(rb + b_raw[i]);
                 const float4 w = *reinterpret_cast<const float4 *>(rb + b_raw[i] + WINW);
                 // numpy order of downsample_mean2 up to the 0.25 scale: ((a + b) + c) + d
-                *reinterpret_cast<float2 *>(&qe[(g0 + b_row[i]) & (QR - 1)][b_col[i]]) =
-                    make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+                lat_store<QS, QH>(&qe[0][0], g0 + b_row[i], b_col[i],
+                              make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w));
             }
         }
     };
@@ -363,7 +379,7 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
         const int ry = r_s + j;
         const int rxg = rxi * 16, ryg = ry * 16;
         float v[16];
-        paint_block<QS>(word, live_col, L, st, &qe[0][0], raw_sum, flat, p.init, rxg, ryg, wx0,
+        paint_block<QS, QH>(word, live_col, L, st, &qe[0][0], raw_sum, flat, p.init, rxg, ryg, wx0,
                         interior_col && ry >= 1 && ry + 1 < rh, p.W, p.H, v);
         word = wnext;
         if (!live_col) continue;
@@ -422,15 +438,16 @@ constexpr int CR2 = PAIR_CR2;         // root rows per CTA
 constexpr int NWA = (BR + 2) / 2;     // stage-A warps (two roots each)
 constexpr int DT2 = (NWA + NW) * 32;
 constexpr int TRAW_BYTES = BLK * WA * 4;
-constexpr int PAIR_SMEM = NT * TRAW_BYTES + NM * RAW_BYTES + QR * QSA * 4 + QR * QS * 4;
+constexpr int MRAW_BYTES = BLK * WINWP * 4;
+constexpr int PAIR_SMEM = NT * TRAW_BYTES + NM * MRAW_BYTES + QRP * QSA * 4 + QRP * QS * 4;
 
 __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_constant__ CUtensorMap tmap,
                                                              const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
     float(*traw)[BLK][WA] = reinterpret_cast<float(*)[BLK][WA]>(dsm);
-    float(*mraw)[BLK][WINW] = reinterpret_cast<float(*)[BLK][WINW]>(dsm + NT * TRAW_BYTES);
-    float(*qa)[QSA] = reinterpret_cast<float(*)[QSA]>(dsm + NT * TRAW_BYTES + NM * RAW_BYTES);
-    float(*qb)[QS] = reinterpret_cast<float(*)[QS]>(dsm + NT * TRAW_BYTES + NM * RAW_BYTES + QR * QSA * 4);
+    float(*mraw)[BLK][WINWP] = reinterpret_cast<float(*)[BLK][WINWP]>(dsm + NT * TRAW_BYTES);
+    float(*qa)[QSA] = reinterpret_cast<float(*)[QSA]>(dsm + NT * TRAW_BYTES + NM * MRAW_BYTES);
+    float(*qb)[QS] = reinterpret_cast<float(*)[QS]>(dsm + NT * TRAW_BYTES + NM * MRAW_BYTES + QRP * QSA * 4);
     __shared__ __align__(8) uint64_t bars[NT];
     __shared__ float st[16];
 
@@ -473,8 +490,8 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
             if (i + 1 < NPT || tid + i * DT2 < NE) {
                 const float4 u = *reinterpret_cast<const float4 *>(rb + b_raw[i]);
                 const float4 w = *reinterpret_cast<const float4 *>(rb + b_raw[i] + WA);
-                *reinterpret_cast<float2 *>(&qa[(g0 + b_row[i]) & (QR - 1)][b_col[i]]) =
-                    make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w);
+                lat_store<QSA, WA / 4>(&qa[0][0], g0 + b_row[i], b_col[i],
+                               make_float2(((u.x + u.y) + w.x) + w.y, ((u.z + u.w) + w.z) + w.w));
             }
         }
     };
@@ -504,9 +521,9 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
     const int row_lo = stage_a ? max(r_s - 1, 0) : r_s, row_hi = stage_a ? min(r_e + 1, rh) : r_e;
     const uint2 *ubase = reinterpret_cast<const uint2 *>(p.unit_map) + ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 +
                          (lane & 15);
-    auto word_of = [&](int row) {
-        return col_ok && row >= row_lo && row < row_hi ? __ldg(ubase + (ptrdiff_t)row * p.rw * 16)
-                                                       : make_uint2(0u, 0u);
+    const ptrdiff_t ustride = (ptrdiff_t)p.rw * 16;
+    auto word_of = [&](int row, const uint2 *ptr) {
+        return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
     };
     auto raw_t = [&](int R, int C) {  // raster t through L2 (window origin xa0)
         const float *r0 = p.cur + (ptrdiff_t)R * p.W + xa0 + C;
@@ -518,10 +535,12 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
         const float *r1 = mraw[((R + 1) >> 4) & (NM - 1)][(R + 1) & 15];
         return ((r0[C] + r0[C + 1]) + r1[C]) + r1[C + 1];
     };
-    uint2 word = word_of(r_s - 1 - lag);
+    const uint2 *uptr = ubase + (ptrdiff_t)(r_s - 1 - lag) * ustride;
+    uint2 word = word_of(r_s - 1 - lag, uptr);
     for (int i = r_s - 1; i <= r_e + 1; i++) {
         const int row = i - lag;
-        const uint2 wnext = word_of(row + 1);
+        uptr += ustride;
+        const uint2 wnext = word_of(row + 1, uptr);
         const int k = i - r_s + 3;
         if (!flat && k < nblocks) build(k);
         __syncthreads();
@@ -534,25 +553,25 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
         float v[16];
         if (stage_a) {
             const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
-            paint_block<QSA>(word, live, L, st, &qa[0][0], raw_t, flat, p.init, rxg, ryg, xa0, interior, p.W, p.H,
+            paint_block<QSA, WA / 4>(word, live, L, st, &qa[0][0], raw_t, flat, p.init, rxg, ryg, xa0, interior, p.W, p.H,
                              v);
             if (live) {
                 const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
                 float *m = &mraw[row & (NM - 1)][L.ly][wc];
 #pragma unroll
                 for (int r = 0; r < 4; r++)
-                    *reinterpret_cast<float4 *>(m + r * WINW) =
+                    *reinterpret_cast<float4 *>(m + r * WINWP) =
                         make_float4(v[4 * r], v[4 * r + 1], v[4 * r + 2], v[4 * r + 3]);
                 const int g = (ryg + L.ly) >> 1;
 #pragma unroll
                 for (int r = 0; r < 2; r++)
-                    *reinterpret_cast<float2 *>(&qb[(g + r) & (QR - 1)][wc >> 1]) =
-                        make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
-                                    ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]);
+                    lat_store<QS, QH>(&qb[0][0], g + r, wc >> 1,
+                                  make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
+                                              ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]));
             }
         } else {
             const bool live = col_ok && row >= r_s;
-            paint_block<QS>(word, live, L, st, &qb[0][0], raw_m, false, p.init, rxg, ryg, xb0, interior, p.W, p.H,
+            paint_block<QS, QH>(word, live, L, st, &qb[0][0], raw_m, false, p.init, rxg, ryg, xb0, interior, p.W, p.H,
                             v);
             if (live) store_block(v, p.nxt, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
         }
@@ -707,7 +726,7 @@ int decode_workspace_bytes(int W, int H, int64_t *bytes) {
     return 0;
 }
 
-static int sweep_smem() { return NBUF * RAW_BYTES + QR * QS * 4; }
+static int sweep_smem() { return NBUF * RAW_BYTES + QRP * QS * 4; }
 
 static int ensure_sweep_attr() {
     static bool attr_set = false;
