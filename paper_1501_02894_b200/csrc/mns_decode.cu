@@ -237,12 +237,16 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
     // unit sums: 4x4 = own block, 8x8 = 4 lanes (lane bits 0,1), 16x16 = the root's 16 lanes; two
     // shuffle rounds of three independent butterflies (every lane of a group adds the same pair
     // sums, so the group's sum is bit-identical on all its lanes)
-    const float t1 = __shfl_xor_sync(FULL, own, 1), t2 = __shfl_xor_sync(FULL, own, 2),
-                t3 = __shfl_xor_sync(FULL, own, 3);
-    const float s8 = (own + t1) + (t2 + t3);
-    const float u1 = __shfl_xor_sync(FULL, s8, 4), u2 = __shfl_xor_sync(FULL, s8, 8),
-                u3 = __shfl_xor_sync(FULL, s8, 12);
-    const float s16 = (s8 + u1) + (u2 + u3);
+    // (skipped when no lane of the warp holds a unit larger than its own 4x4 block)
+    float s8 = own, s16 = own;
+    if (__any_sync(FULL, live && k > 1)) {
+        const float t1 = __shfl_xor_sync(FULL, own, 1), t2 = __shfl_xor_sync(FULL, own, 2),
+                    t3 = __shfl_xor_sync(FULL, own, 3);
+        s8 = (own + t1) + (t2 + t3);
+        const float u1 = __shfl_xor_sync(FULL, s8, 4), u2 = __shfl_xor_sync(FULL, s8, 8),
+                    u3 = __shfl_xor_sync(FULL, s8, 12);
+        s16 = (s8 + u1) + (u2 + u3);
+    }
     if (live && k > 0) {
         const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
         const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
