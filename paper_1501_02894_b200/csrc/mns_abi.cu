@@ -30,9 +30,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static int encode_tmap_impl(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
-                            uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h,
-                            CUtensorMapSwizzle swz) {
+static EncodeTiledFn encode_tiled_fn() {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         void *ptr = nullptr;
@@ -40,10 +38,18 @@ static int encode_tmap_impl(CUtensorMap *map, CUtensorMapDataType dtype, const v
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess || !ptr) {
             set_error("cuTensorMapEncodeTiled unavailable");
-            return -1;
+            return nullptr;
         }
         fn = (EncodeTiledFn)ptr;
     }
+    return fn;
+}
+
+static int encode_tmap_impl(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
+                            uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h,
+                            CUtensorMapSwizzle swz) {
+    const EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return -1;
     const cuuint64_t dims[2] = {width, height};
     const cuuint64_t strides[1] = {row_bytes};
     const cuuint32_t box[2] = {box_w, box_h};
@@ -53,6 +59,25 @@ static int encode_tmap_impl(CUtensorMap *map, CUtensorMapDataType dtype, const v
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return -1;
+    }
+    return 0;
+}
+
+int encode_tmap_3d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t d0, uint64_t d1,
+                   uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1,
+                   uint32_t box2) {
+    const EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) return -1;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+    const cuuint32_t box[3] = {box0, box1, box2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(map, dtype, 3, const_cast<void *>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (3d) failed (%d)", (int)r);
         return -1;
     }
     return 0;

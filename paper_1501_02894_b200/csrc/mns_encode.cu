@@ -30,6 +30,7 @@
 #include <math.h>
 
 #include "mns_common.cuh"
+#include "mns_tma.cuh"
 
 namespace mns {
 namespace {
@@ -46,8 +47,7 @@ constexpr int QE_W = WIN_W / 2;      // 272
 constexpr int QE_H = WIN_H / 2;      // 24
 
 struct EncParams {
-    const uint8_t *img;
-    int64_t pitch, image_stride;
+    int y_res0;  // first resident image row (the tensor map's row 0)
     int W, H, n_images, rr0, rows, rw, tiles_per_row;
     int mns, root_level, min_dim;
     double p1b[5];  // phase-1 accept bound on 1024*n*SSE per level (inf for level 4)
@@ -167,7 +167,7 @@ __device__ __forceinline__ int node3_y(int m) { return node2_y(m >> 2) + 4 * ((m
 __device__ __forceinline__ int node4_x(int c) { return node3_x(c >> 2) + 2 * (c & 1); }
 __device__ __forceinline__ int node4_y(int c) { return node3_y(c >> 2) + 2 * ((c >> 1) & 1); }
 
-// Shared-memory layout of one tile (32 roots); moments and decisions are per node.
+// Shared-memory layout of one tile (TR roots); moments and decisions are per node.
 struct TileSmem {
     Mom m1[TR];
     Mom m2[TR][4];
@@ -176,7 +176,7 @@ struct TileSmem {
     uint64_t rec1[TR], rec2[TR][4], rec3[TR][16], rec4[TR][64];
     uint8_t acc1[TR], acc2[TR][4], acc3[TR][16];
 };
-constexpr int TILE_SMEM = (int)sizeof(TileSmem);
+constexpr int TILE_SMEM = ((int)sizeof(TileSmem) + 127) / 128 * 128;  // the TMA window follows, 128-B aligned
 constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + TILE_SMEM + 64;
 
 struct Win {  // the staged window and the tile/image geometry a decision thread needs
@@ -285,36 +285,33 @@ __device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p
     }
 }
 
-__global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const EncParams p) {
-    extern __shared__ __align__(16) unsigned char esm[];
+__global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                           const EncParams p) {
+    extern __shared__ __align__(128) unsigned char esm[];
     TileSmem &ts = *reinterpret_cast<TileSmem *>(esm);
     uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TILE_SMEM);
     uint16_t(*qe)[QE_W] = reinterpret_cast<uint16_t(*)[QE_W]>(esm + TILE_SMEM + WIN_H * WIN_W);
+    __shared__ __align__(8) uint64_t wbar;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long tile = blockIdx.x;
-    const int per_img = p.rows * p.tiles_per_row;
-    const int img_i = (int)(tile / per_img);
-    const int rem = (int)(tile % per_img);
-    const int ry = p.rr0 + rem / p.tiles_per_row;
-    const int rx0 = (rem % p.tiles_per_row) * TR;
+    const int img_i = blockIdx.z;
+    const int ry = p.rr0 + blockIdx.y;
+    const int rx0 = blockIdx.x * TR;
     const int nr = min(TR, p.rw - rx0);
-    const uint8_t *img = p.img + (size_t)img_i * p.image_stride;
     const int x0 = rx0 * 16, y0 = ry * 16;
     const int wx0 = x0 - 16, wy0 = y0 - 16;
     const Win w{pix, qe, x0, y0, wx0, wy0, p.W, p.H};
 
-    // ---- K1a: stage the pixel window (16-byte coalesced loads, zero outside the image)
-    constexpr int CHK = WIN_W / 16;
-    for (int c = tid; c < WIN_H * CHK; c += ET) {
-        const int wr = c / CHK, wc = (c % CHK) * 16;
-        const int gy = wy0 + wr, gx = wx0 + wc;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (gy >= 0 && gy < p.H && gx >= 0 && gx < p.W)
-            v = __ldg(reinterpret_cast<const uint4 *>(img + (size_t)gy * p.pitch + gx));
-        *reinterpret_cast<uint4 *>(&pix[wr][wc]) = v;
+    // ---- K1a: stage the pixel window with one TMA box (the image viewed as u16 pairs, so a
+    // 288-byte window row is one 144-element box row; out-of-image bytes are zero-filled)
+    if (tid == 0) {
+        mbar_init(&wbar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&wbar, WIN_H * WIN_W);
+        tma_load_3d(&pix[0][0], &tmap, wx0 / 2, wy0 - p.y_res0, img_i, &wbar);
     }
     __syncthreads();
+    mbar_wait(&wbar, 0);
     // ---- K1b: even-phase 2x2 sums, 4 per thread-step via packed u16x2 adds
     for (int c = tid; c < QE_H * (QE_W / 4); c += ET) {
         const int qi = c / (QE_W / 4), qj = (c % (QE_W / 4)) * 4;
@@ -630,9 +627,6 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     MNS_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "workspace must be 16-byte aligned");
 
     EncParams p{};
-    p.img = img;
-    p.pitch = pitch;
-    p.image_stride = image_stride;
     p.W = W;
     p.H = H;
     p.n_images = n_images;
@@ -665,8 +659,18 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
         MNS_CUDA_TRY(cudaFuncSetAttribute(mns_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC_SMEM));
         attr_set = true;
     }
-    const long long n_tiles = (long long)n_images * p.rows * p.tiles_per_row;
-    mns_encode_kernel<<<(unsigned)n_tiles, ET, ENC_SMEM, stream>>>(p);
+    // rows [16 rr0 - 16, 16 rr1 + 16) of each image are resident: the tensor map starts there
+    p.y_res0 = 16 * rr0 - 16 > 0 ? 16 * rr0 - 16 : 0;
+    const int y_res1 = 16 * rr1 + 16 < H ? 16 * rr1 + 16 : H;
+    MNS_CHECK_ARG(n_images <= 65535 && p.rows <= 65535, "grid too large");
+    CUtensorMap tmap{};
+    if (encode_tmap_3d(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, img + (ptrdiff_t)p.y_res0 * pitch, (uint64_t)W / 2,
+                       (uint64_t)(y_res1 - p.y_res0), (uint64_t)n_images, (uint64_t)pitch,
+                       (uint64_t)(n_images > 1 ? image_stride : pitch * (int64_t)(y_res1 - p.y_res0)), WIN_W / 2,
+                       WIN_H, 1))
+        return -1;
+    const dim3 grid((unsigned)p.tiles_per_row, (unsigned)p.rows, (unsigned)n_images);
+    mns_encode_kernel<<<grid, ET, ENC_SMEM, stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
     compact_records_kernel<<<(unsigned)ctiles, CT_THREADS, 0, stream>>>(p.stage, root_offsets, n_roots, records,
                                                                         d_count, status);

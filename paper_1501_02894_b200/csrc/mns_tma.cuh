@@ -51,6 +51,15 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
+// 3D tile load: box at (x, y, z) (elements)
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -58,6 +67,10 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 // Host: cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
 int encode_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, int elem_bytes, const void *base, uint64_t width,
                    uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h);
+// 3D (batched images): dims (d0, d1, d2), byte strides of dims 1 and 2, box (box0, box1, box2).
+int encode_tmap_3d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t d0, uint64_t d1,
+                   uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1,
+                   uint32_t box2);
 // Same with 128-byte swizzle (K-major UMMA operand tiles; box_w * elem = 128 B).
 int encode_tmap_2d_swizzled(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t width,
                             uint64_t height, uint64_t row_bytes, uint32_t box_w, uint32_t box_h);
