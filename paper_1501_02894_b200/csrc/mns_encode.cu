@@ -29,6 +29,8 @@
 
 #include <math.h>
 
+#include <climits>
+
 #include "mns_common.cuh"
 #include "mns_tma.cuh"
 
@@ -565,33 +567,35 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
         root_offsets[n_roots] = (int32_t)(base + total);
         *count = base + total;
     }
-    // flattened copy: output record j of the tile comes from the root whose range holds j
-    // (binary search over the tile's offsets); 4 independent read-only loads per thread in flight
+    // copy, one 32-root chunk per warp at a time: lane l holds the chunk's root l offset; output
+    // record j of the chunk belongs to the last root whose offset is <= j (5-step shuffle search);
+    // 4 independent read-only loads per lane in flight
     const int nr_tile = (int)min((long long)CT_ROOTS, n_roots - r0);
-    auto root_of = [&](int j) {
-        int lo = 0, hi = nr_tile - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (offs[mid] <= j) lo = mid;
-            else hi = mid - 1;
-        }
-        return lo;
-    };
     uint64_t *dst = out + base;
-    for (int j0 = 0; j0 < total; j0 += 4 * CT_THREADS) {
-        uint64_t v[4];
-        int jj[4];
+    for (int c0 = 32 * warp; c0 < nr_tile; c0 += CT_THREADS) {
+        const int nk = min(32, nr_tile - c0);
+        const int my_off = lane < nk ? offs[c0 + lane] : INT_MAX;
+        const int j_lo = __shfl_sync(FULL, my_off, 0);
+        const int j_hi = c0 + nk < nr_tile ? offs[c0 + nk] : total;
+        for (int j0 = j_lo; j0 < j_hi; j0 += 4 * 32) {
+            uint64_t v[4];
+            int jj[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            jj[u] = j0 + u * CT_THREADS + tid;
-            if (jj[u] < total) {
-                const int k = root_of(jj[u]);
-                v[u] = __ldg(stage + (r0 + k) * 64 + (jj[u] - offs[k]));
+            for (int u = 0; u < 4; u++) {
+                jj[u] = j0 + 32 * u + lane;
+                int k = 0;  // largest chunk root with offset <= j (roots with no records never win ties)
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int o = __shfl_sync(FULL, my_off, k + step < 32 ? k + step : 31);
+                    if (k + step < nk && o <= jj[u]) k += step;
+                }
+                const int ok = __shfl_sync(FULL, my_off, k);
+                if (jj[u] < j_hi) v[u] = __ldg(stage + (r0 + c0 + k) * 64 + (jj[u] - ok));
             }
-        }
 #pragma unroll
-        for (int u = 0; u < 4; u++)
-            if (jj[u] < total) dst[jj[u]] = v[u];
+            for (int u = 0; u < 4; u++)
+                if (jj[u] < j_hi) dst[jj[u]] = v[u];
+        }
     }
 }
 
