@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     full_search_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const TcParams p) {
     extern __shared__ __align__(1024) unsigned char tsm_raw[];
-    unsigned char *tsm = reinterpret_cast<unsigned char *>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-B aligned base as an offset from the shared array (keeps shared-space addressing: LDS, not LD.E)
+    unsigned char *tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
     unsigned char *sA = tsm;
     unsigned char *sB = tsm + A_BYTES;
     float2 *sL = reinterpret_cast<float2 *>(tsm + A_BYTES + STAGES * B_BYTES);              // [2][BN] (Sq, sqrt D)
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (active && !flat) set_threshold(other);
                 }
             }
+#pragma unroll 1
             for (int ch = 0; ch < BN / 2 / CH; ch++) {
                 const int col0 = half * (BN / 2) + ch * CH;
                 float c[CH];
