@@ -158,6 +158,21 @@ int mns_write_stream(const uint64_t *records, int64_t n_records, int32_t orig_w,
                      int32_t padded_h, int32_t mns, int32_t technique2, uint8_t *out, int64_t out_capacity,
                      int64_t *d_bits, void *workspace, int64_t workspace_bytes, void *stream);
 
+/* Rate-distortion metrics on device (bench.py:39-79 rd_sweep):
+ * exact sum of squared differences of two W x H uint8 images (metrics.py:16-31
+ * mse = sse / (W*H)), and the leaf tallies of a record array (encoder.py:135-142):
+ * out5 = {level-1, level-2, level-3, level-4 leaves, phase-2 leaves}. */
+int mns_image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int32_t width, int32_t height,
+                  uint64_t *d_sse, void *stream);
+int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out5, void *stream);
+
+/* Domain-offset histogram of a full-search result (bench.py:119-127 offset_histogram
+ * over the samples of encoder.py:249-309): offset = domain centre - range centre
+ * of each of the (W/B)*(H/B) ranges; dense int32 counts hist_x[dx + W] (2W+1),
+ * hist_y[dy + H] (2H+1) and joint[(dy + H)*(2W+1) + dx + W]. */
+int mns_offset_histogram(const int32_t *dom, int64_t n_ranges, int32_t width, int32_t height, int32_t range_size,
+                         int32_t step, int32_t *hist_x, int32_t *hist_y, int32_t *joint, void *stream);
+
 const char *mns_last_error(void);
 int mns_version(void);
 

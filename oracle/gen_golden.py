@@ -26,6 +26,7 @@ sys.path.insert(0, os.path.join(REF, "tests"))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import mnscodec.encoder as enc  # noqa: E402
+from mnscodec.bench import histogram_csv, offset_histogram, rd_sweep  # noqa: E402
 from mnscodec.bitstream import stream_bit_count, write_stream  # noqa: E402
 from mnscodec.decoder import DecodeConfig, decode, decode_step  # noqa: E402
 from mnscodec.encoder import EncoderConfig, encode_full_search, encode_local_search, encode_quadtree  # noqa: E402
@@ -340,10 +341,51 @@ def gen_nodes(store, manifest):
     print(f"node cases: {len(cases)}")
 
 
-def main():
+def gen_rd(store, manifest):
+    """Reference rd_sweep rows (bench.py:39-79) and offset-histogram CSVs (bench.py:119-142)."""
+    imgs = {
+        "constant_64": np.full((64, 64), 42, dtype=np.uint8),
+        "natural_128": natural_image(128, 128, seed=3).pixels,
+        "synth_c2_crop_96x80": np.ascontiguousarray(synth_image(512, 2)[100:180, 300:396]),
+        "scene_72x56": np.ascontiguousarray(scene_image(256, 256, seed=7).pixels[40:96, 20:92]),
+    }
+    grid = [4.0, 8.0, (6.0, 8.0, 10.0)]
+    k = 0
+    for name, px in imgs.items():
+        for dec in (None, DecodeConfig(max_iters=6, stop_delta=0.0)):
+            pts = rd_sweep(GrayImage(px), ["no_search", "mns"], grid, (True, False), decode_config=dec)
+            key = f"rd{k}"
+            store[f"{key}/img"] = px
+            store[f"{key}/bits"] = np.array([p.bits for p in pts], dtype=np.int64)
+            store[f"{key}/psnr"] = np.array([p.psnr for p in pts], dtype=np.float64)
+            store[f"{key}/leaves"] = np.array([p.leaf_counts for p in pts], dtype=np.int64)
+            store[f"{key}/phase2"] = np.array([p.phase2_count for p in pts], dtype=np.int64)
+            manifest.append(dict(key=key, image=name, grid=[list(g) if isinstance(g, tuple) else g for g in grid],
+                                 decode=None if dec is None else [dec.max_iters, dec.stop_delta, dec.initial_value],
+                                 rows=[[p.mode, list(p.thresholds), p.technique2] for p in pts]))
+            k += 1
+    j = 0
+    for name in ("natural_128", "scene_72x56"):
+        px = imgs[name]
+        for B in (4, 8):
+            _, samples = encode_full_search(GrayImage(px), B, EncoderConfig(mode="full_search"))
+            key = f"hist{j}"
+            store[f"{key}/img"] = px
+            store[f"{key}/csv"] = np.array(histogram_csv(offset_histogram(samples)))
+            manifest.append(dict(key=key, image=name, B=B))
+            j += 1
+    print(f"rd cases: {k} sweeps, {j} histograms")
+
+
+def main(argv=None):
+    """Regenerate every golden set, or only the named ones (e.g. ``gen_golden.py rd``)."""
     os.makedirs(OUT, exist_ok=True)
-    for name, fn in (("encode", gen_encode), ("decode_step", gen_decode_step), ("search", gen_search),
-                     ("nodes", gen_nodes)):
+    table = (("encode", gen_encode), ("decode_step", gen_decode_step), ("search", gen_search),
+             ("nodes", gen_nodes), ("rd", gen_rd))
+    want = set(argv or []) or {n for n, _ in table}
+    for name, fn in table:
+        if name not in want:
+            continue
         store, manifest = {}, []
         fn(store, manifest)
         store["manifest"] = np.array(json.dumps(manifest))
@@ -352,4 +394,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

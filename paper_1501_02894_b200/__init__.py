@@ -43,4 +43,15 @@ from .codec import (  # noqa: F401
     write_stream_device,
 )
 
+from .rd import (  # noqa: F401  (reference mnscodec.bench)
+    RD_CSV_COLUMNS,
+    OffsetHistogram,
+    RdPoint,
+    histogram_csv,
+    offset_histogram,
+    offset_histogram_device,
+    rd_csv,
+    rd_sweep,
+)
+
 __version__ = "0.1.0"

@@ -124,6 +124,12 @@ int stream_workspace_bytes(int64_t n, int64_t *bytes);
 int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int ph, int mns, int t2, uint8_t *out,
                  int64_t cap, int64_t *d_bits, void *ws, int64_t ws_bytes, cudaStream_t st);
 
+int image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int W, int H, uint64_t *out,
+              cudaStream_t stream);
+int code_stats(const uint64_t *records, int64_t n, int64_t *out5, cudaStream_t stream);
+int offset_histogram(const int32_t *dom, int64_t n_ranges, int W, int H, int B, int step, int32_t *hist_x,
+                     int32_t *hist_y, int32_t *joint, cudaStream_t stream);
+
 }  // namespace mns
 
 #define GUARD(call)                                                   \
@@ -138,6 +144,21 @@ extern "C" {
 
 const char *mns_last_error(void) { return mns::g_err; }
 int mns_version(void) { return 1; }
+
+int mns_image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int32_t width, int32_t height,
+                  uint64_t *d_sse, void *stream) {
+    GUARD(mns::image_sse(a, pitch_a, b, pitch_b, width, height, d_sse, (cudaStream_t)stream));
+}
+
+int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out5, void *stream) {
+    GUARD(mns::code_stats(records, n_records, d_out5, (cudaStream_t)stream));
+}
+
+int mns_offset_histogram(const int32_t *dom, int64_t n_ranges, int32_t width, int32_t height, int32_t range_size,
+                         int32_t step, int32_t *hist_x, int32_t *hist_y, int32_t *joint, void *stream) {
+    GUARD(mns::offset_histogram(dom, n_ranges, width, height, range_size, step, hist_x, hist_y, joint,
+                                (cudaStream_t)stream));
+}
 
 int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t rr0, int32_t rr1, int64_t *bytes) {
     GUARD(mns::encode_workspace_bytes(width, n_images, rr0, rr1, bytes));
