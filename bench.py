@@ -148,6 +148,95 @@ def run_reference(args, img):
 
 # ------------------------------------------------------------------------- GPU leg
 
+def small_configs(dev, rank, world):
+    """BASELINE configs 1-3: c1/c2 are latency-bound single images -- one encode +
+    decode step captured in a CUDA graph and replayed 1000 times back to back (rank 0); c3 is the
+    batched 8->4 encode of 256 512^2 images (seeds 1000..1255), split across ranks, no collective."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1501_02894_b200 as mns
+    from paper_1501_02894_b200 import sharding
+    from paper_1501_02894_b200.synth import batch_seeds, config_image, synth_image
+
+    def dev_code(nb, H, W):
+        n_roots = nb * (H // 16) * (W // 16)
+        return mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
+                              torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
+                              torch.zeros(1, dtype=torch.int64, device=dev), W, H, nb,
+                              unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device=dev))
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    out = {}
+    cfg = mns.EncoderConfig(e3=math.inf)
+    if rank == 0:
+        for name, root_level, iters, desc in (("c1", 2, 8, "256^2, 8->4 quadtree, 8 decode sweeps"),
+                                              ("c2", 1, 10, "512^2, 16->8->4 quadtree, 10 decode sweeps")):
+            px = config_image(name)
+            H, W = px.shape
+            img = torch.from_numpy(px).to(dev)
+            code = dev_code(1, H, W)
+            u8 = torch.empty((H, W), dtype=torch.uint8, device=dev)
+            rasters = (torch.empty((H, W), dtype=torch.float32, device=dev),
+                       torch.empty((H, W), dtype=torch.float32, device=dev))
+
+            def step():
+                mns.encode_device(img, cfg, root_level=root_level, out=code)
+                mns.decode_device(code, iters=iters, stop_delta=0.0, initial_value=128.0, out=u8, rasters=rasters)
+
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(3):
+                    step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            for _ in range(10):
+                g.replay()
+            torch.cuda.synchronize()
+            reps = 1000
+            a, b = ev(), ev()
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            us = a.elapsed_time(b) * 1e3 / reps
+            out[name] = {"config": desc, "latency_us": us, "blocks_per_s": W * H / 64 / (us * 1e-6),
+                         "graph_replays": reps}
+    # c3: batched encode, images split across ranks
+    i0, i1 = sharding.split(256, world, rank)
+    seeds = batch_seeds()[i0:i1]
+    batch = torch.from_numpy(np.stack([synth_image(512, s, noise_sigma=6.0, n_blobs=6) for s in seeds])).to(dev)
+    code = dev_code(len(seeds), 512, 512)
+    for _ in range(3):
+        mns.encode_device(batch, cfg, root_level=2, out=code)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    reps = 20
+    a, b = ev(), ev()
+    a.record()
+    for _ in range(reps):
+        mns.encode_device(batch, cfg, root_level=2, out=code)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    if world > 1:
+        m = torch.tensor([ms], device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        ms = float(m.item())
+    out["c3"] = {"config": "256 x 512^2 (seeds 1000..1255), 8->4 quadtree, encode only, images split across "
+                           f"{world} rank(s)", "ms_per_batch": ms, "images_per_s": 256 / (ms / 1e3),
+                 "blocks_per_s": 256 * 4096 / (ms / 1e3)}
+    return out
+
+
 def run_ours(args, img_np, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -306,6 +395,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                                  "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3),
                                  "effective_tflops": 2 * 64 * pairs / (ms / 1e3) / 1e12}
 
+    small = None if args.no_small else small_configs(dev, rank, world)
+
     if rank != 0:
         return
     hbm, which = peaks()
@@ -327,7 +418,7 @@ def run_ours(args, img_np, rank, world, local_rank):
         "components": {"encode_ms": enc_ms, "encode_blocks_per_s": blocks / world / (enc_ms / 1e3),
                        "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
                        "pass_ms": pass_ms, "sweeps_per_pass": 2, "sweep_ms_effective": pass_ms / 2,
-                       "leaves_rank0": n_leaves, "full_search": fs},
+                       "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic("decode_pair_kernel") if world == 1 else None,
                      "algorithmic_bytes": algo, "kernel": "decode_pair_kernel (steady-state pass = 2 sweeps)",
@@ -354,6 +445,7 @@ def main():
                     help="rows of the c5 image the cpu_baseline leg encodes + decodes (default: all of it)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-search", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the c1/c2 graph-replay latency and c3 batch legs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -61,7 +61,17 @@ struct SweepParams {
     float stop_delta;
     int n_ctas;
     int umap_r0;         // first root row held by unit_map (pair kernel: may be rr0 - 1)
+    int cr;              // root rows walked by one CTA (rows_per_cta)
 };
+
+// Root rows per CTA: the kernel's nominal chunk, shortened on small images so the grid still
+// covers the SMs (c1/c2 are latency-bound: fewer serial rows per CTA beat the extra halo rows).
+static int rows_per_cta(int rows, int bands, int nominal) {
+    const int target = 2 * 148;  // two CTAs per SM
+    int cr = nominal;
+    while (cr > 4 && (long long)bands * ((rows + cr - 1) / cr) < target) cr /= 2;
+    return cr;
+}
 
 __device__ __forceinline__ int morton_of(int cx, int cy) {  // 3-bit coordinates -> 6-bit Morton (y major)
     int m = 0;
@@ -283,7 +293,7 @@ __device__ __forceinline__ void store_block(const float (&v)[16], float *nxt, ui
     }
 }
 
-// One Jacobi sweep (decoder.py:37-63) for a 128-px column band over CR root rows.
+// One Jacobi sweep (decoder.py:37-63) for a 128-px column band over p.cr root rows.
 // TMA streams 16-row raster blocks (OOB zero fill) into a 5-deep smem ring, two blocks
 // ahead of the root row being painted; each block is reduced once into the even 2x2-sum
 // lattice ring (numpy's downsample_mean2 order, image.py), so no raster row is reloaded
@@ -301,7 +311,7 @@ __global__ void __launch_bounds__(DT) decode_sweep_kernel(const __grid_constant_
     if (p.state[0]) return;  // converged in an earlier sweep (stop_delta > 0)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int x0 = blockIdx.x * BR * 16, wx0 = x0 - 16;
-    const int r_s = p.rr0 + blockIdx.y * CR, r_e = min(r_s + CR, p.rr1);
+    const int r_s = p.rr0 + blockIdx.y * p.cr, r_e = min(r_s + p.cr, p.rr1);
     const bool flat = p.cur == nullptr;
     const int nblocks = (r_e - r_s) + 2;  // block k = raster rows [16(r_s-1+k), 16(r_s+k))
     if (tid < 16) st[tid] = kUnitS[tid];
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int x0 = blockIdx.x * BR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
-    const int r_s = p.rr0 + blockIdx.y * CR2, r_e = min(r_s + CR2, p.rr1);
+    const int r_s = p.rr0 + blockIdx.y * p.cr, r_e = min(r_s + p.cr, p.rr1);
     const int rh = p.H / 16;
     const bool flat = p.cur == nullptr;
     const int nblocks = (r_e - r_s) + 4;  // block k = raster-t root row r_s - 2 + k
@@ -782,7 +792,8 @@ int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const
                            (uint64_t)(y_hi - p.y_lo), (uint64_t)W * 4, WINW, BLK))
             return -1;
     }
-    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + CR - 1) / CR);
+    p.cr = rows_per_cta(rr1 - rr0, (p.rw + BR - 1) / BR, CR);
+    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + p.cr - 1) / p.cr);
     p.n_ctas = grid.x * grid.y;
     decode_sweep_kernel<<<grid, DT, sweep_smem(), stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
@@ -829,7 +840,8 @@ int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, 
                            (uint64_t)(y_hi - p.y_lo), (uint64_t)W * 4, WA, BLK))
             return -1;
     }
-    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + CR2 - 1) / CR2);
+    p.cr = rows_per_cta(rr1 - rr0, (p.rw + BR - 1) / BR, CR2);
+    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + p.cr - 1) / p.cr);
     p.n_ctas = grid.x * grid.y;
     decode_pair_kernel<<<grid, DT2, PAIR_SMEM, stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
