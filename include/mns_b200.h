@@ -158,6 +158,19 @@ int mns_write_stream(const uint64_t *records, int64_t n_records, int32_t orig_w,
                      int32_t padded_h, int32_t mns, int32_t technique2, uint8_t *out, int64_t out_capacity,
                      int64_t *d_bits, void *workspace, int64_t workspace_bytes, void *stream);
 
+/* .mns reader (bitstream.py:208-279 read_stream) for the leaf body of a
+ * container whose 13-byte header the caller has validated (mns / technique2 flags, padded
+ * dimensions).  Speculative parallel token parse; writes records in DFS order (capacity >=
+ * 64 * n_roots), root_offsets[n_roots + 1] and *d_count.  d_status[0] = first format error
+ * as a key (bit position << 16 | code << 8 | a << 4 | b; -1 = none; codes: 1 level-a leaf
+ * inside a level-b node, 2 quartet interrupted by a level-a id, 3 negative-zero delta,
+ * 4 truncated), d_status[1] = bit position after the final leaf (-1 if the stream ended
+ * before every root was tiled).  Trailing / padding checks are the caller's. */
+int mns_read_stream_workspace_bytes(int64_t n_bytes, int64_t *bytes);
+int mns_read_stream(const uint8_t *data, int64_t n_bytes, int32_t mns, int32_t technique2, int32_t padded_w,
+                    int32_t padded_h, uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
+                    int64_t *d_status, void *workspace, int64_t workspace_bytes, void *stream);
+
 /* Rate-distortion metrics on device (bench.py:39-79 rd_sweep):
  * exact sum of squared differences of two W x H uint8 images (metrics.py:16-31
  * mse = sse / (W*H)), and the leaf tallies of a record array (encoder.py:135-142):

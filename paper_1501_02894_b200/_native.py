@@ -64,6 +64,8 @@ def _declare(L):
         "mns_local_search": [P, I32, I32, I32, P, P, P, P, P],
         "mns_stream_workspace_bytes": [I64, P],
         "mns_write_stream": [P, I64, I32, I32, I32, I32, I32, I32, P, I64, P, P, I64, P],
+        "mns_read_stream_workspace_bytes": [I64, P],
+        "mns_read_stream": [P, I64, I32, I32, I32, I32, P, I64, P, P, P, P, I64, P],
         "mns_image_sse": [P, I64, P, I64, I32, I32, P, P],
         "mns_code_stats": [P, I64, P, P],
         "mns_offset_histogram": [P, I64, I32, I32, I32, I32, P, P, P, P],
@@ -80,7 +82,8 @@ def _declare(L):
 
 EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_build_unit_map", "mns_decode_workspace_bytes", "mns_decode_quadtree",
            "mns_decode_sweep", "mns_decode_sweep2", "mns_decode_units", "mns_decode_step_f64", "mns_search_workspace_bytes", "mns_full_search",
-           "mns_local_search", "mns_stream_workspace_bytes", "mns_write_stream", "mns_image_sse", "mns_code_stats", "mns_offset_histogram",
+           "mns_local_search", "mns_stream_workspace_bytes", "mns_write_stream", "mns_read_stream_workspace_bytes", "mns_read_stream",
+           "mns_image_sse", "mns_code_stats", "mns_offset_histogram",
            "mns_last_error",
            "mns_version")
 

@@ -1,9 +1,10 @@
 """.mns container (reference: bitstream.py) over packed records.
 
 write_stream packs on the GPU (csrc/mns_stream.cu: widths -> look-back scan ->
-MSB-first word gather); stream_bit_count / level_id_bit_count are vectorised
-numpy accounting over the packed records; read_stream is the host-side parser
-(the reference's format, byte for byte).  Error messages follow the reference
+MSB-first word gather) and read_stream parses on the GPU (csrc/mns_stream_read.cu:
+speculative token walks + scans); stream_bit_count / level_id_bit_count are
+vectorised numpy accounting over the packed records; read_stream_host is the
+sequential host parser used as the checker (the reference's format, byte for byte).  Error messages follow the reference
 (bitstream.py:107-200, :208-279).
 """
 
@@ -175,8 +176,8 @@ class _Bits:
         return v
 
 
-def read_stream(data: bytes) -> QuadtreeCode:
-    """bitstream.py:208-279: exact inverse of write_stream (host parser)."""
+def _header(data: bytes):
+    """bitstream.py:210-222: magic, flags and dimensions, with the reference's errors."""
     if len(data) < HEADER_BYTES:
         raise StreamFormatError("truncated header")
     if data[:4] != MAGIC:
@@ -191,6 +192,46 @@ def read_stream(data: bytes) -> QuadtreeCode:
         raise StreamFormatError("zero image dimension in header")
     if pw % ROOT_SIZE or ph % ROOT_SIZE or pw < ow or ph < oh:
         raise StreamFormatError("padded dimensions inconsistent with original dimensions")
+    return mode, t2, ow, oh, pw, ph
+
+
+def read_stream(data: bytes) -> QuadtreeCode:
+    """bitstream.py:208-279: exact inverse of write_stream, parsed on the GPU
+    (csrc/mns_stream_read.cu: speculative token walks + scans); the first format error raises
+    the same StreamFormatError as the reference's sequential parser."""
+    from . import codec
+
+    data = bytes(data)
+    mode, t2, ow, oh, pw, ph = _header(data)
+    import torch
+
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(codec._device())
+    code, status = codec.read_stream_device(buf, mode == "mns", t2, pw, ph)
+    key, end = (int(v) for v in status.cpu().tolist())
+    if key != -1:
+        err, a, b = (key >> 8) & 0xFF, (key >> 4) & 0xF, key & 0xF
+        if err == 1:
+            raise StreamFormatError(f"level-{a} leaf cannot appear inside a level-{b} node")
+        if err == 2:
+            raise StreamFormatError(f"level-4 quartet interrupted by level-{a} id")
+        if err == 3:
+            raise StreamFormatError("non-canonical negative-zero delta")
+        raise StreamFormatError("truncated stream")
+    if end < 0:
+        raise StreamFormatError("truncated stream")
+    left = len(data) * 8 - end
+    if left >= 8:
+        raise StreamFormatError(f"{left} trailing bits after the final leaf")
+    if left and data[-1] & ((1 << left) - 1):
+        raise StreamFormatError("nonzero padding bits")
+    n = code.n_records()
+    rec = code.records[:n].cpu().numpy().view(np.uint64)
+    return QuadtreeCode.from_records(rec, pw, ph, ow, oh, mode, t2, root_offsets=code.root_offsets.cpu().numpy())
+
+
+def read_stream_host(data: bytes) -> QuadtreeCode:
+    """bitstream.py:208-279 as a sequential host parser (the checker for read_stream's errors)."""
+    mode, t2, ow, oh, pw, ph = _header(data)
     rd = _Bits(data, HEADER_BYTES)
     leaves = []
 

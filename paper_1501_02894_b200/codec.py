@@ -276,6 +276,27 @@ def write_stream_device(records, n: int, orig_w: int, orig_h: int, padded_w: int
     return out, bits
 
 
+def read_stream_device(data, mns: bool, technique2: bool, padded_w: int, padded_h: int, stream=None):
+    """GPU .mns body parser (csrc/mns_stream_read.cu).  ``data`` is the whole container as a uint8
+    CUDA tensor (header validated by the caller).  Returns (DeviceCode, status int64[2]): status[0]
+    the first format-error key (-1 none), status[1] the bit position after the final leaf."""
+    torch = _torch()
+    L = N.lib()
+    dev = data.device
+    n_roots = (padded_w // 16) * (padded_h // 16)
+    code = DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
+                      torch.zeros(n_roots + 1, dtype=torch.int32, device=dev),
+                      torch.zeros(1, dtype=torch.int64, device=dev), padded_w, padded_h, 1, 0, padded_h // 16,
+                      "mns" if mns else "no_search", bool(technique2))
+    status = torch.empty(2, dtype=torch.int64, device=dev)
+    wsb = N.out_i64(L, L.mns_read_stream_workspace_bytes, data.numel())
+    ws = _WS.get("read", wsb, dev)
+    N.check(L.mns_read_stream(N.ptr(data), data.numel(), 1 if mns else 0, 1 if technique2 else 0, padded_w, padded_h,
+                              N.ptr(code.records), code.records.numel(), N.ptr(code.root_offsets), N.ptr(code.count),
+                              N.ptr(status), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return code, status
+
+
 # ------------------------------------------------------------------ host layer (reference API)
 
 def _device():
@@ -286,7 +307,10 @@ def _device():
 
 def _to_device_u8(px: np.ndarray):
     torch = _torch()
-    return torch.from_numpy(np.ascontiguousarray(px)).to(_device(), non_blocking=False)
+    px = np.ascontiguousarray(px)
+    if not px.flags.writeable:  # torch.from_numpy wants a writable buffer
+        px = px.copy()
+    return torch.from_numpy(px).to(_device(), non_blocking=False)
 
 
 def encode_quadtree(image, config: EncoderConfig, *, root_level: int = 1) -> QuadtreeCode:

@@ -126,6 +126,10 @@ int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int
 
 int image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int W, int H, uint64_t *out,
               cudaStream_t stream);
+int read_stream_workspace_bytes(int64_t nbytes, int64_t *bytes);
+int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, int ph, uint64_t *records,
+                int64_t capacity, int32_t *root_offsets, int64_t *d_count, int64_t *d_status, void *workspace,
+                int64_t workspace_bytes, cudaStream_t s);
 int code_stats(const uint64_t *records, int64_t n, int64_t *out5, cudaStream_t stream);
 int offset_histogram(const int32_t *dom, int64_t n_ranges, int W, int H, int B, int step, int32_t *hist_x,
                      int32_t *hist_y, int32_t *joint, cudaStream_t stream);
@@ -144,6 +148,17 @@ extern "C" {
 
 const char *mns_last_error(void) { return mns::g_err; }
 int mns_version(void) { return 1; }
+
+int mns_read_stream_workspace_bytes(int64_t n_bytes, int64_t *bytes) {
+    GUARD(mns::read_stream_workspace_bytes(n_bytes, bytes));
+}
+
+int mns_read_stream(const uint8_t *data, int64_t n_bytes, int32_t mns, int32_t technique2, int32_t padded_w,
+                    int32_t padded_h, uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
+                    int64_t *d_status, void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::read_stream(data, n_bytes, mns, technique2, padded_w, padded_h, records, capacity, root_offsets,
+                           d_count, d_status, workspace, workspace_bytes, (cudaStream_t)stream));
+}
 
 int mns_image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int32_t width, int32_t height,
                   uint64_t *d_sse, void *stream) {

@@ -85,7 +85,7 @@ def test_stream_accounting_and_parser_match_reference(golden):
         code = mns.QuadtreeCode.from_records(g[f"{k}/records"], case["padded_w"], case["padded_h"], img.shape[1],
                                              img.shape[0], case["cfg"]["mode"], True)
         assert bitstream.stream_bit_count(code) == int(g[f"{k}/stream_bits"])
-        back = bitstream.read_stream(bytes(g[f"{k}/stream"]))
+        back = bitstream.read_stream_host(bytes(g[f"{k}/stream"]))
         assert np.array_equal(back.records, g[f"{k}/records"])
         assert (back.orig_w, back.orig_h, back.padded_w, back.padded_h) == (img.shape[1], img.shape[0],
                                                                             case["padded_w"], case["padded_h"])
