@@ -43,6 +43,8 @@ from .codec import (  # noqa: F401
     write_stream_device,
 )
 
+from . import bitstream  # noqa: F401  (reference mnscodec.bitstream)
+from .bitstream import read_stream, stream_bit_count, write_stream  # noqa: F401
 from .rd import (  # noqa: F401  (reference mnscodec.bench)
     RD_CSV_COLUMNS,
     OffsetHistogram,
