@@ -46,7 +46,7 @@ constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
 constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;  // 640
 constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB
 constexpr int B_BYTES = BN * BK * 2;          // 16 KB
-constexpr int CONST_BYTES = BN * 16;          // (Sq, sqrt(D)) + exact D per column
+constexpr int CONST_BYTES = BN * 16;          // -Sq, sqrt(D) (planar floats) + exact D per column
 constexpr int TMEM_COLS = 2 * MH * BN;        // 2 accumulator stages x 2 M halves x 128 columns = 512
 constexpr int SMEM_BYTES = 1024 + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES + 512;
 
@@ -56,7 +56,7 @@ struct TcParams {
     long long ndom;
     int dtiles_per_chunk, n_dtiles;
     int dstride;                 // domain of column c of tile t: ((dt0 + t) * BN + c) * dstride
-    const float2 *consts;        // [ndom_pad] (Sq, sqrt_rd(D))
+    const float2 *consts;        // per 128-domain tile: 128 floats -Sq, then 128 floats sqrt_rd(D)
     const long long *pD;         // exact D
     const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range
     const int32_t *row_flat;     // [n_rows_pad] 1 if the range is constant (N == 0 for every domain)
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned char *tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
     unsigned char *sA = tsm;
     unsigned char *sB = tsm + A_BYTES;
-    float2 *sL = reinterpret_cast<float2 *>(tsm + A_BYTES + STAGES * B_BYTES);              // [2][BN] (Sq, sqrt D)
+    float2 *sL = reinterpret_cast<float2 *>(tsm + A_BYTES + STAGES * B_BYTES);              // [2][BN] -Sq | sqrt D
     long long *sD = reinterpret_cast<long long *>(tsm + A_BYTES + STAGES * B_BYTES + 2 * BN * 8);  // [2][BN] D
     uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + A_BYTES + STAGES * B_BYTES + 2 * CONST_BYTES);
     uint64_t *full_bar = bars, *empty_bar = bars + STAGES, *a_bar = bars + 2 * STAGES;
@@ -291,12 +291,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const bool live = active && !flat;
                 // level 1: continuous lower bound, 2 FFMA + FMNMX per element
                 float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent max chains
-                const float4 *l4 = reinterpret_cast<const float4 *>(&sL[cbuf * BN + col0]);
+                const float *lq = reinterpret_cast<const float *>(&sL[cbuf * BN]) + col0;  // -Sq
+                const float *ld = lq + BN;                                                   // sqrt D
+                const float2 srn2 = make_float2(sr_n, sr_n);
 #pragma unroll
-                for (int j = 0; j < CH; j += 2) {
-                    const float4 k = l4[j >> 1];  // (Sq, sqrt D) of columns j, j+1
-                    const float n1a = fmaf(-k.x, sr_n, c[j]), n1b = fmaf(-k.z, sr_n, c[j + 1]);
-                    mm[(j >> 1) & 3] = fmaxf(mm[(j >> 1) & 3], fmaxf(fmaf(-scl, k.y, fabsf(n1a)), fmaf(-scl, k.w, fabsf(n1b))));
+                for (int j = 0; j < CH; j += 4) {
+                    const float4 nq = *reinterpret_cast<const float4 *>(lq + j);
+                    const float4 sd = *reinterpret_cast<const float4 *>(ld + j);
+                    // n1 = C - Sq*Sr/n for two columns per FFMA2 (same rounding as fmaf)
+                    const float2 n01 = ffma2_rn(make_float2(nq.x, nq.y), srn2, make_float2(c[j], c[j + 1]));
+                    const float2 n23 = ffma2_rn(make_float2(nq.z, nq.w), srn2, make_float2(c[j + 2], c[j + 3]));
+                    mm[(j >> 2) & 1] = fmaxf(mm[(j >> 2) & 1], fmaxf(fmaf(-scl, sd.x, fabsf(n01.x)),
+                                                                     fmaf(-scl, sd.y, fabsf(n01.y))));
+                    mm[2 + ((j >> 2) & 1)] = fmaxf(mm[2 + ((j >> 2) & 1)], fmaxf(fmaf(-scl, sd.z, fabsf(n23.x)),
+                                                                                 fmaf(-scl, sd.w, fabsf(n23.y))));
                 }
                 const bool chunk_pass = live && fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])) >= -slack;
 #ifdef MNS_TC_STATS
@@ -313,9 +321,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // lower bound of the quantised value over every odd k2 with |n1 - N/n| <= err; level 3: exact
 #pragma unroll
                 for (int j = 0; j < CH; j++) {
-                    const float2 k = sL[cbuf * BN + col0 + j];
-                    const float n1 = fmaf(-k.x, sr_n, c[j]);
-                    const bool pj = chunk_pass && fmaf(-scl, k.y, fabsf(n1)) >= -slack;
+                    const float nsq = lq[j], sqd = ld[j];  // -Sq, sqrt D
+                    const float n1 = fmaf(nsq, sr_n, c[j]);
+                    const bool pj = chunk_pass && fmaf(-scl, sqd, fabsf(n1)) >= -slack;
                     if (!__any_sync(FULL, pj)) continue;
                     if (!pj) continue;
 #ifdef MNS_TC_STATS
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
                     const long long d = (dbase + col0 + j) * p.dstride;
                     if (d >= p.ndom) continue;
-                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)(int)k.x * sr;  // exact
+                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)(int)(-nsq) * sr;  // exact
                     const long long v = best_val_exact(N, Dx);
                     const unsigned long long key = make_key(v, d * p.n_iso + iso);
                     if (key < best) {
@@ -372,8 +380,11 @@ __global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const 
     for (long long d = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); d < ndom_pad; d += warps) {
         for (int k = lane; k < BK; k += 32)
             Q[d * BK + k] = __float2half_rn(d < ndom && k < n ? (float)pool[d * n + k] : 0.f);
-        if (lane == 0)
-            consts[d] = d < ndom ? make_float2((float)psq[d], __fsqrt_rd(__ll2float_rd(pD[d]))) : make_float2(0.f, 0.f);
+        if (lane == 0) {  // planar per 128-domain tile: -Sq then sqrt_rd(D)
+            float *cf = reinterpret_cast<float *>(consts) + (d / BN) * 2 * BN + d % BN;
+            cf[0] = d < ndom ? -(float)psq[d] : 0.f;
+            cf[BN] = d < ndom ? __fsqrt_rd(__ll2float_rd(pD[d])) : 0.f;
+        }
     }
 }
 
@@ -406,7 +417,10 @@ __global__ void gather_sample_kernel(const float2 *consts, const long long *pD, 
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsample_pad;
          i += (long long)gridDim.x * blockDim.x) {
         const long long d = i * stride;
-        cs[i] = d < ndom ? consts[d] : make_float2(0.f, 0.f);
+        const float *src = reinterpret_cast<const float *>(consts) + (d / BN) * 2 * BN + d % BN;
+        float *dst = reinterpret_cast<float *>(cs) + (i / BN) * 2 * BN + i % BN;
+        dst[0] = d < ndom ? src[0] : 0.f;
+        dst[BN] = d < ndom ? src[BN] : 0.f;
         ds[i] = d < ndom ? pD[d] : 0;
     }
 }
