@@ -361,6 +361,7 @@ def run_ours(args, img_np, rank, world, local_rank):
     # steady-state passes: not the first (flat start, reads nothing) nor the last (uint8 output)
     mid = [e[2][i][0].elapsed_time(e[2][i][1]) for e in evs for i in range(1, n_launch - 1)]
     pass_ms = float(np.mean(mid))
+    pass_ms_each = [float(np.mean([e[2][i][0].elapsed_time(e[2][i][1]) for e in evs])) for i in range(n_launch)]
     own_px = 16 * (r1 - r0) * W
     n_leaves = int(code.count.item())
 
@@ -417,7 +418,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                    "l2": "inputs (256 MiB image, 1 GiB fp32 rasters) exceed the 126 MB L2"},
         "components": {"encode_ms": enc_ms, "encode_blocks_per_s": blocks / world / (enc_ms / 1e3),
                        "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
-                       "pass_ms": pass_ms, "sweeps_per_pass": 2, "sweep_ms_effective": pass_ms / 2,
+                       "pass_ms": pass_ms, "pass_ms_each": pass_ms_each, "sweeps_per_pass": 2,
+                       "sweep_ms_effective": pass_ms / 2,
                        "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic("decode_pair_kernel") if world == 1 else None,

@@ -360,3 +360,23 @@ def test_strip_decoder_matches_whole_decode(mns):
     got = torch.cat([d.out for d in decs])
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("h,w", [(1, 1), (3, 5), (17, 9), (31, 33), (16, 200)])
+def test_tiny_and_odd_images_vs_oracle(mns, h, w):
+    """Images smaller than one root or not a multiple of 16: edge-replicated padding
+    (image.py:123-132), the level-1 room guard on the padded size (encoder.py:226-231),
+    and the decode crop (decoder.py:76-77)."""
+    rng = np.random.default_rng(h * 1000 + w)
+    px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    padded = np.pad(px, ((0, -h % 16), (0, -w % 16)), mode="edge")
+    for mode in ("mns", "no_search"):
+        cfg = mns.EncoderConfig(e1=6.0, e2=6.0, e3=6.0, mode=mode)
+        code = mns.encode_quadtree(mns.GrayImage(px), cfg)
+        ref, _ = O.encode_quadtree_records(padded, (6.0, 6.0, 6.0), 16.0, mode == "mns")
+        assert np.array_equal(code.records, ref), (h, w, mode)
+        assert (code.orig_w, code.orig_h, code.padded_w, code.padded_h) == (w, h) + padded.shape[::-1]
+        got = mns.decode(code, mns.DecodeConfig(max_iters=5, stop_delta=0.0)).pixels
+        want, _, _ = O.decode_records(ref, padded.shape[1], padded.shape[0], max_iters=5, stop_delta=0.0)
+        assert got.shape == (h, w)
+        assert int(np.abs(got.astype(int) - want[:h, :w].astype(int)).max()) <= 1
