@@ -365,6 +365,30 @@ def run_ours(args, img_np, rank, world, local_rank):
     own_px = 16 * (r1 - r0) * W
     n_leaves = int(code.count.item())
 
+    # multi-GPU: the same step with the final code gather to rank 0
+    gather = None
+    if world > 1:
+        def step_gather():
+            step()
+            sharding.gather_codes(code.records, int(code.count.item()), code.root_offsets, rank, world)
+
+        for _ in range(2):
+            step_gather()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            step_gather()
+        g1.record()
+        barrier()
+        gms = g0.elapsed_time(g1) / args.steps
+        m = torch.tensor([gms], device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        gms = float(m.item())
+        gather = {"ms_per_step": gms, "blocks_per_s": H * W / 64 / (gms / 1e3),
+                  "note": "step + gather of every strip's records and root offsets to rank 0 (size all_gather, "
+                          "then point-to-point sends over NCCL)"}
+
     # e2e through the public device API with host buffers: every step copies its image from pinned host
     # memory and its decoded image back; copies of steps k+1 / k-1 overlap step k's kernels on two copy
     # streams (double-buffered device image and output), all inside the timed region
@@ -420,7 +444,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                        "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
                        "pass_ms": pass_ms, "pass_ms_each": pass_ms_each, "sweeps_per_pass": 2,
                        "sweep_ms_effective": pass_ms / 2,
-                       "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small},
+                       "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small,
+                       "with_code_gather": gather},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic("decode_pair_kernel") if world == 1 else None,
                      "algorithmic_bytes": algo, "kernel": "decode_pair_kernel (steady-state pass = 2 sweeps)",

@@ -10,8 +10,10 @@ SURVEY 8(e):
   send/recv over NVLink; gloo in the CPU tests), plus one unit-map root row per side
   once per code;
 * full / local search (config c4) -- ranges split across ranks, pool replicated.
-Codes stay on the rank that produced them (root_offsets are strip-local); a
-gather to rank 0 is a plain all_gather of sizes + records when the caller needs it.
+Codes stay on the rank that produced them (root_offsets are strip-local);
+gather_codes concatenates them on rank 0 in strip (= root raster) order: one
+all_gather of the sizes, then point-to-point sends of each rank's records and
+root offsets straight into their slices of rank 0's buffers.
 """
 
 from __future__ import annotations
@@ -88,6 +90,54 @@ def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world
         ops.append(dist.P2POp(dist.irecv, umap[own1], rank + 1, group))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+
+
+def gather_codes(records, count: int, root_offsets, rank: int, world: int, dst: int = 0, group=None):
+    """Concatenate per-rank codes on rank ``dst`` (the final code gather).
+
+    ``records[:count]`` (int64, mns_record.h) and ``root_offsets`` (int32, n_local_roots + 1,
+    strip-local) of each rank's contiguous share of roots (strip rows of one image, or images of a
+    batch).  Returns (records, root_offsets) of the whole job on ``dst`` -- records in rank order,
+    root offsets rebased -- and None on the other ranks.  Any torch.distributed backend.
+    """
+    import torch
+    import torch.distributed as dist
+
+    n_roots = root_offsets.numel() - 1
+    if world == 1:
+        return records[:count], root_offsets
+    sizes = torch.tensor([count, n_roots], dtype=torch.int64, device=records.device)
+    all_sizes = [torch.empty_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    counts = [int(t[0]) for t in all_sizes]
+    roots = [int(t[1]) for t in all_sizes]
+    if rank != dst:
+        ops = [dist.P2POp(dist.isend, records[:count].contiguous(), dst, group),
+               dist.P2POp(dist.isend, root_offsets[:n_roots].contiguous(), dst, group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return None
+    total, total_roots = sum(counts), sum(roots)
+    out = torch.empty(total, dtype=records.dtype, device=records.device)
+    offs = torch.empty(total_roots + 1, dtype=root_offsets.dtype, device=root_offsets.device)
+    rb = [sum(counts[:r]) for r in range(world)]
+    ob = [sum(roots[:r]) for r in range(world)]
+    ops = []
+    for r in range(world):
+        if r == dst:
+            out[rb[r]: rb[r] + counts[r]].copy_(records[:count])
+            offs[ob[r]: ob[r] + roots[r]].copy_(root_offsets[:n_roots])
+        else:
+            ops.append(dist.P2POp(dist.irecv, out[rb[r]: rb[r] + counts[r]], r, group))
+            ops.append(dist.P2POp(dist.irecv, offs[ob[r]: ob[r] + roots[r]], r, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for r in range(world):  # strip-local offsets -> global
+        if rb[r]:
+            offs[ob[r]: ob[r] + roots[r]] += rb[r]
+    offs[total_roots] = total
+    return out, offs
 
 
 class StripDecoder:

@@ -163,6 +163,34 @@ def test_pair_pass_strip_decode_matches_whole_image(world, tmp_path):
     assert np.array_equal(strips, whole)
 
 
+def _gather_worker(rank, world, out_dir):  # noqa: ARG001
+    counts = [5, 0, 9, 3][:world]
+    n_roots = [2, 1, 3, 2][:world]
+    base = 1000 * rank
+    rec = torch.arange(base, base + counts[rank] + 4, dtype=torch.int64)  # 4 junk slots past count
+    offs = torch.tensor(sorted(np.random.default_rng(rank).integers(0, counts[rank] + 1, n_roots[rank]).tolist())
+                        + [counts[rank]], dtype=torch.int32)
+    offs[0] = 0
+    got = sharding.gather_codes(rec, counts[rank], offs, rank, world)
+    if rank != 0:
+        assert got is None
+        return
+    out, o = got
+    want = np.concatenate([np.arange(1000 * r, 1000 * r + counts[r]) for r in range(world)])
+    assert np.array_equal(out.numpy(), want)
+    want_o = []
+    for r in range(world):  # each rank's strip-local offsets, rebased by the records before it
+        lo = sorted(np.random.default_rng(r).integers(0, counts[r] + 1, n_roots[r]).tolist())
+        lo[0] = 0
+        want_o += [v + sum(counts[:r]) for v in lo]
+    assert o.numpy().tolist() == want_o + [sum(counts)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_codes_gloo(world, tmp_path):
+    _run(world, _gather_worker, str(tmp_path))
+
+
 def test_batch_and_range_splits():
     for n, world in ((256, 1), (256, 8), (4096, 3), (7, 4)):
         parts = [sharding.split(n, world, r) for r in range(world)]
