@@ -1,6 +1,8 @@
 // Shared device/host helpers for libmns_b200 (sm_100a).
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,6 +22,20 @@ void set_error(const char *fmt, ...);
             return -1;                                                                   \
         }                                                                                \
     } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting: set it once per
+// (kernel, device) -- `done` is the call site's bitmask of devices already configured.
+template <class Kernel>
+inline cudaError_t ensure_dynamic_smem(Kernel kernel, int bytes, std::atomic<unsigned long long> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 #define MNS_CHECK_ARG(cond, msg)                                                         \
     do {                                                                                 \

@@ -743,12 +743,8 @@ int decode_workspace_bytes(int W, int H, int64_t *bytes) {
 static int sweep_smem() { return NBUF * RAW_BYTES + QRP * QS * 4; }
 
 static int ensure_sweep_attr() {
-    static bool attr_set = false;
-    if (!attr_set) {
-        MNS_CUDA_TRY(cudaFuncSetAttribute(decode_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          sweep_smem()));
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> done{0};
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_sweep_kernel, sweep_smem(), done));
     return 0;
 }
 
@@ -801,10 +797,9 @@ int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const
 }
 
 static int ensure_pair_attr() {
-    static bool attr_set = false;
-    if (!attr_set) {
-        MNS_CUDA_TRY(cudaFuncSetAttribute(decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM));
-        attr_set = true;
+    {
+        static std::atomic<unsigned long long> done{0};
+        MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_kernel, PAIR_SMEM, done));
     }
     return 0;
 }

@@ -658,10 +658,9 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     p.root_cnt = root_offsets;
     p.n_roots = n_roots;
     MNS_CUDA_TRY(cudaMemsetAsync(status, 0, ctiles * 8, stream));
-    static bool attr_set = false;
-    if (!attr_set) {
-        MNS_CUDA_TRY(cudaFuncSetAttribute(mns_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC_SMEM));
-        attr_set = true;
+    {
+        static std::atomic<unsigned long long> done{0};
+        MNS_CUDA_TRY(ensure_dynamic_smem(mns_encode_kernel, ENC_SMEM, done));
     }
     // rows [16 rr0 - 16, 16 rr1 + 16) of each image are resident: the tensor map starts there
     p.y_res0 = 16 * rr0 - 16 > 0 ? 16 * rr0 - 16 : 0;

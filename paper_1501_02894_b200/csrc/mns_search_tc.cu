@@ -549,11 +549,9 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     p.row_flat = row_flat;
     p.flat_key = fkey;
     p.best = best;
-    static bool attr_set = false;
-    if (!attr_set) {
-        MNS_CUDA_TRY(cudaFuncSetAttribute(full_search_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SMEM_BYTES));
-        attr_set = true;
+    {
+        static std::atomic<unsigned long long> done{0};
+        MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel, SMEM_BYTES, done));
     }
     if (ndom >= 16 * SAMPLE) {  // prepass over the sample
         gather_sample_kernel<<<64, 256, 0, st>>>(consts, pD, ndom, SAMPLE, nsample_pad, cons_s, pD_s);
