@@ -65,6 +65,17 @@ int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64
                         uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
                         uint32_t *unit_map, void *workspace, int64_t workspace_bytes, void *stream);
 
+/* Replaces: encoder.try_phase1 / try_phase2 (encoder.py:145-212), exported by
+ * mnscodec/__init__.py:31-32: one node decision at (x, y) of size 32 >> level
+ * (phase 1: levels 1..4, phase 2: levels 1..3).  *record (device) = the packed
+ * leaf record, 0 on rejection; *rms (device) = the reference's rms -- phase 1:
+ * rms_error of the quantised fit, phase 2: the worst chosen quadrant rms, or
+ * +inf on rejection -- replayed in numpy's fp64 evaluation order (bit-exact).
+ * One single-CTA launch; the image needs a 2(32 >> level) square co-centred
+ * domain (phase 1). */
+int mns_try_node(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int32_t x, int32_t y, int32_t level,
+                 int32_t phase, const mns_enc_cfg *cfg, uint64_t *record, double *rms, void *stream);
+
 /* Decoder unit map (mns_record.h) of a record array grouped by root: 32 uint32
  * words (64 cells) per root of the root rows [root_row_begin, root_row_end).
  * mns_encode_quadtree emits the same map directly when unit_map != NULL. */

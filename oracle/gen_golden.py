@@ -325,6 +325,17 @@ def gen_nodes(store, manifest):
         y = int(rng.integers(0, 128 // size)) * size
         e = float(rng.choice([1.0, 2.5, 4.0, 8.0]))
         cases.append((nat, x, y, size, level, EncoderConfig(e1=e, e2=e, e3=e)))
+    # rects at arbitrary (odd, unaligned) positions, level 4, and domains clamped at the borders
+    rng2 = np.random.default_rng(55)
+    small = scene_image(40, 24, seed=9).pixels
+    for _ in range(40):
+        level = int(rng2.integers(1, 5))
+        size = 32 >> level
+        px = nat if rng2.random() < 0.7 else small
+        x = int(rng2.integers(0, px.shape[1] - size + 1))
+        y = int(rng2.integers(0, px.shape[0] - size + 1))
+        e = float(rng2.choice([1.0, 2.5, 4.0, 8.0]))
+        cases.append((px, x, y, size, level, EncoderConfig(e1=e, e2=e, e3=e, mean_tol=float(rng2.choice([4.0, 8.0, 30.0])))))
     for k, (px, x, y, size, level, cfg) in enumerate(cases):
         image = GrayImage(px)
         if 2 * size <= min(px.shape):

@@ -2,7 +2,7 @@
 (arXiv 1501.02894), a drop-in for the reference ``mnscodec`` encode/decode hot path.
 
 Public API mirrors mnscodec (same names, signatures, dataclasses, error messages):
-encode_quadtree, decode, decode_step, encode_full_search, encode_local_search,
+encode_quadtree, try_phase1, try_phase2, decode, decode_step, encode_full_search, encode_local_search,
 write_stream, read_stream, stream_bit_count, plus the device layer used by
 bench.py and the multi-GPU sharding (encode_device, decode_device, ...).
 """
@@ -40,6 +40,8 @@ from .codec import (  # noqa: F401
     full_search_device,
     local_search_device,
     pad_to_multiple,
+    try_phase1,
+    try_phase2,
     write_stream_device,
 )
 

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from typing import Optional
 
 import numpy as np
@@ -37,6 +37,7 @@ from .types import (
     Phase2Payload,
     QuadtreeCode,
     dequantize_contrast,
+    unpack_leaves,
 )
 
 
@@ -325,6 +326,57 @@ def encode_quadtree(image, config: EncoderConfig, *, root_level: int = 1) -> Qua
     offs = code.root_offsets.cpu().numpy()
     return QuadtreeCode.from_records(rec, padded.shape[1], padded.shape[0], px.shape[1], px.shape[0], config.mode,
                                      config.technique2, root_offsets=offs)
+
+
+def _check_rect(w: int, h: int, rect: BlockRect) -> None:
+    """image.py:140-143."""
+    if rect.size < 1 or rect.x < 0 or rect.y < 0 or rect.x + rect.size > w or rect.y + rect.size > h:
+        raise ValueError(f"{rect} out of bounds for {w}x{h} raster")
+
+
+def _try_node(image, rect: BlockRect, level: int, config: EncoderConfig, phase: int):
+    torch = _torch()
+    L = N.lib()
+    px = _pixels(image)
+    h, w = px.shape
+    img = _to_device_u8(px)
+    rec = torch.zeros(1, dtype=torch.int64, device=img.device)
+    rms = torch.zeros(1, dtype=torch.float64, device=img.device)
+    cfg = enc_cfg(config)
+    N.check(L.mns_try_node(N.ptr(img), w, h, w, rect.x, rect.y, level, phase, ctypes.byref(cfg), N.ptr(rec),
+                           N.ptr(rms), N.stream_ptr(None)))
+    packed = rec.cpu().numpy().view(np.uint64)
+    r = float(rms.cpu().item())
+    if not packed[0]:
+        return None, r
+    (leaf,) = unpack_leaves(packed)
+    return replace(leaf, rect=rect), r  # packed records hold even corners; keep the caller's rect
+
+
+def try_phase1(image, rect: BlockRect, level: int, config: EncoderConfig):
+    """encoder.py:145-166: fit the co-centred domain onto rect; (LeafRecord | None, rms).
+
+    One ``try_node_kernel`` launch: exact integer moments decide, and the rms is replayed in the
+    reference's fp64 order, so both match the reference bit for bit (tests/golden/nodes.npz).
+    """
+    if LEVEL_SIZES[level] != rect.size:
+        raise ValueError(f"level {level} expects block size {LEVEL_SIZES[level]}, got {rect.size}")
+    px = _pixels(image)
+    co_domain_rect(rect, px.shape[1], px.shape[0])  # raises like the reference when no domain fits
+    _check_rect(px.shape[1], px.shape[0], rect)
+    return _try_node(px, rect, level, config, 1)
+
+
+def try_phase2(image, rect: BlockRect, level: int, config: EncoderConfig):
+    """encoder.py:169-212: quadrant-mean coding with 1-bit contrast picks; (LeafRecord, worst
+    quadrant rms) or (None, inf)."""
+    if level not in CONTRAST_SETS:
+        raise ValueError("phase 2 exists only at levels 1..3")
+    px = _pixels(image)
+    _check_rect(px.shape[1], px.shape[0], rect)
+    if rect.size != LEVEL_SIZES[level]:  # the reference codes any even square; the kernel codes level sizes
+        raise ValueError(f"level {level} expects block size {LEVEL_SIZES[level]}, got {rect.size}")
+    return _try_node(px, rect, level, config, 2)
 
 
 def _records_grouped(code) -> tuple[np.ndarray, np.ndarray]:

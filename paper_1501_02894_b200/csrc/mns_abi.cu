@@ -100,6 +100,8 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
                     cudaStream_t stream);
 int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1, uint32_t *unit_map,
                    cudaStream_t stream);
+int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
+             const mns_enc_cfg *cfg, uint64_t *d_rec, double *d_rms, cudaStream_t stream);
 int decode_workspace_bytes(int W, int H, int64_t *bytes);
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
@@ -185,6 +187,11 @@ int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64
                         void *workspace, int64_t workspace_bytes, void *stream) {
     GUARD(mns::encode_quadtree(img, width, height, pitch, image_stride, n_images, rr0, rr1, cfg, records, capacity,
                                root_offsets, d_count, unit_map, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_try_node(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int32_t x, int32_t y, int32_t level,
+                 int32_t phase, const mns_enc_cfg *cfg, uint64_t *record, double *rms, void *stream) {
+    GUARD(mns::try_node(img, width, height, pitch, x, y, level, phase, cfg, record, rms, (cudaStream_t)stream));
 }
 
 int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,

@@ -203,9 +203,9 @@ __device__ __forceinline__ int pixel(const Win &w, int slot, int px, int py) {
 
 // Reference-order emulation of one phase-2 quadrant (transform.py:69-80 rms_error) -- the
 // quadrant is the child (cx, cy, cs) of a node at `level`; the domain is the child's own.
-// Returns 1 accept / 0 reject and the chosen bit.
+// Returns 1 accept / 0 reject, the chosen bit and (rms_out) the chosen candidate's rms.
 __device__ int emulate_quadrant(const Win &w, int slot, int cx, int cy, int cs, const Mom &m, int t, double slo,
-                                double shi, double tol, int &bit) {
+                                double shi, double tol, int &bit, double *rms_out = nullptr) {
     double lo[64], hi[64];
     const int n = cs * cs;
     const double dm = ((double)m.sq * 0.25) / (double)n;
@@ -219,6 +219,7 @@ __device__ int emulate_quadrant(const Win &w, int slot, int cx, int cy, int cs, 
         }
     const double rlo = __dsqrt_rn(pw_sum_dev(lo, n) / (double)n), rhi = __dsqrt_rn(pw_sum_dev(hi, n) / (double)n);
     bit = rlo <= rhi ? 0 : 1;
+    if (rms_out) *rms_out = bit ? rhi : rlo;
     return ((bit ? rhi : rlo) > tol) ? 0 : 1;
 }
 
@@ -285,6 +286,88 @@ __device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p
         acc = true;
         rec = mns_rec_phase2(w.x0 + 16 * slot + nx, w.y0 + ny, level, z.o, z.d0, z.d1, z.d2, (int)((bitm >> g) & 15u));
     }
+}
+
+// One try_phase1 / try_phase2 call (encoder.py:145-212) on the node (x, y, 32 >> level) of a
+// W x H image: the packed record (0 = rejected) and the reference's rms -- phase 1: sqrt of the
+// exact mean squared residual (every term is dyadic), phase 2: the worst chosen quadrant rms,
+// replayed in the reference's fp64 order, or +inf on rejection.  One CTA stages an 80-row window
+// from the node's 16-aligned origin - 16 (it holds the node and its co-centred domains even for
+// rects not aligned to their size); thread 0 decides.
+constexpr int NODE_WIN_H = 80;
+__global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
+                                const EncParams p, uint64_t *out_rec, double *out_rms) {
+    __shared__ uint8_t pix[NODE_WIN_H][WIN_W];
+    __shared__ uint16_t qe[NODE_WIN_H / 2][QE_W];
+    __shared__ double sq_buf[256];
+    const int x0 = x & ~15, y0 = y & ~15, wx0 = x0 - 16, wy0 = y0 - 16;
+    for (int i = threadIdx.x; i < NODE_WIN_H * WIN_W; i += blockDim.x) {
+        const int r = i / WIN_W, c = i % WIN_W, gy = wy0 + r, gx = wx0 + c;
+        pix[r][c] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? img[(size_t)gy * pitch + gx] : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NODE_WIN_H / 2 * QE_W; i += blockDim.x) {
+        const int qi = i / QE_W, qj = i % QE_W;
+        qe[qi][qj] = (uint16_t)(pix[2 * qi][2 * qj] + pix[2 * qi][2 * qj + 1] + pix[2 * qi + 1][2 * qj] +
+                                pix[2 * qi + 1][2 * qj + 1]);
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const Win w{pix, qe, x0, y0, wx0, wy0, W, H};
+    const int size = 32 >> level, nx = x - x0, ny = y - y0, nlog2 = 2 * (5 - level);
+    auto moments = [&](int cx, int cy, int cs) {
+        Mom m{0, 0, 0, 0, 0};
+        for (int i = 0; i < cs; i++)
+            for (int j = 0; j < cs; j++) {
+                const int q = dom_q(w, 0, cx, cy, cs, cx + j, cy + i), r = pixel(w, 0, cx + j, cy + i);
+                m.sr += r;
+                m.srr += r * r;
+                m.sq += q;
+                m.sqq += q * q;
+                m.sqr += q * r;
+            }
+        return m;
+    };
+    if (phase == 1) {
+        const Mom m = moments(nx, ny, size);
+        bool acc;
+        const uint64_t rec = phase1(x, y, level, nlog2, m, p.p1b[level], acc);
+        const long long n = 1ll << nlog2;
+        const int o = (2 * m.sr + (int)n) >> (nlog2 + 1);
+        const int code = quant_code(n * m.sqr - (long long)m.sq * m.sr, n * m.sqq - (long long)m.sq * m.sq);
+        const double sdq = -0.875 + 0.25 * code, dm = ((double)m.sq * 0.25) / (double)n;
+        for (int i = 0; i < size; i++)  // rms_error replayed in numpy's fp64 order (exact in practice)
+            for (int j = 0; j < size; j++)
+                sq_buf[i * size + j] = emu_sq(pixel(w, 0, nx + j, ny + i), dom_q(w, 0, nx, ny, size, nx + j, ny + i),
+                                              dm, sdq, (double)o);
+        *out_rec = acc ? rec : 0;
+        *out_rms = __dsqrt_rn(pw_sum_dev(sq_buf, (int)n) / (double)n);
+        return;
+    }
+    const int h = size / 2;
+    Mom kids[4];
+    for (int k = 0; k < 4; k++) kids[k] = moments(nx + (k & 1) * h, ny + (k >> 1) * h, h);
+    const int sr = kids[0].sr + kids[1].sr + kids[2].sr + kids[3].sr;
+    const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
+                            p.mean_tol);
+    *out_rec = 0;
+    *out_rms = INFINITY;
+    if (!z.pass) return;
+    const double slo = level == 1 ? 0.2 : (level == 2 ? 0.4 : 0.5);
+    const double shi = level == 1 ? 0.5 : (level == 2 ? 0.65 : 0.9);
+    double worst = 0.0;
+    int bits = 0;
+    for (int k = 0; k < 4; k++) {
+        int bit;
+        double rms;
+        if (!emulate_quadrant(w, 0, nx + (k & 1) * h, ny + (k >> 1) * h, h, kids[k], z.t[k], slo, shi, p.tol[level], bit,
+                              &rms))
+            return;
+        bits |= bit << k;
+        worst = fmax(worst, rms);
+    }
+    *out_rec = mns_rec_phase2(x, y, level, z.o, z.d0, z.d1, z.d2, bits);
+    *out_rms = worst;
 }
 
 __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -677,6 +760,28 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     MNS_CUDA_TRY(cudaGetLastError());
     compact_records_kernel<<<(unsigned)ctiles, CT_THREADS, 0, stream>>>(p.stage, root_offsets, n_roots, records,
                                                                         d_count, status);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
+             const mns_enc_cfg *cfg, uint64_t *d_rec, double *d_rms, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && pitch >= W && W <= 65534 && H <= 65534, "bad image geometry");
+    MNS_CHECK_ARG(level >= 1 && level <= 4 && (phase == 1 || (phase == 2 && level <= 3)), "bad level / phase");
+    const int size = 32 >> level;
+    MNS_CHECK_ARG(x >= 0 && y >= 0 && x + size <= W && y + size <= H, "node outside the image");
+    MNS_CHECK_ARG(phase == 2 || (2 * size <= W && 2 * size <= H), "no co-centred domain fits the image");
+    EncParams p{};
+    for (int l = 1; l <= 3; l++) {
+        const double n = (double)(1 << (2 * (5 - l)));
+        const double bnd = sqrt_bound(cfg->e[l - 1]);
+        p.p1b[l] = bnd * 1024.0 * n * n;
+        p.p2b[l] = bnd;
+        p.tol[l] = cfg->e[l - 1];
+    }
+    p.p1b[4] = INFINITY;
+    p.mean_tol = cfg->mean_tol;
+    try_node_kernel<<<1, 256, 0, stream>>>(img, W, H, pitch, x, y, level, phase, p, d_rec, d_rms);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -380,3 +380,47 @@ def test_tiny_and_odd_images_vs_oracle(mns, h, w):
         want, _, _ = O.decode_records(ref, padded.shape[1], padded.shape[0], max_iters=5, stop_delta=0.0)
         assert got.shape == (h, w)
         assert int(np.abs(got.astype(int) - want[:h, :w].astype(int)).max()) <= 1
+
+
+def test_try_phase_nodes_match_reference(mns, golden):
+    """try_phase1 / try_phase2 (encoder.py:145-212) on the reference's single-node known answers
+    (test_encoder.py cases, random aligned nodes, odd/unaligned rects, level 4, clamped domains):
+    record and rms bit-exact."""
+    from paper_1501_02894_b200.types import pack_leaf
+
+    g = golden("nodes")
+    n1 = n2 = 0
+    for case in g.manifest:
+        k = case["key"]
+        img = mns.GrayImage(g[f"{k}/img"])
+        rect = mns.BlockRect(case["x"], case["y"], case["size"])
+        cfg = mns.EncoderConfig(e1=case["e"], e2=case["e"], e3=case["e"], mean_tol=case["mean_tol"])
+        rec_ref, rms_ref = g[f"{k}/rec"], g[f"{k}/rms"]
+        if 2 * case["size"] <= min(img.pixels.shape):
+            r1, rms1 = mns.try_phase1(img, rect, case["level"], cfg)
+            assert (r1 is not None) == case["ok1"], k
+            assert (pack_leaf(r1) if r1 else 0) == int(rec_ref[0]), k
+            assert r1 is None or r1.rect == rect
+            assert rms1 == rms_ref[0], (k, rms1, rms_ref[0])
+            n1 += 1
+        if case["level"] <= 3:
+            r2, rms2 = mns.try_phase2(img, rect, case["level"], cfg)
+            assert (r2 is not None) == case["ok2"], k
+            assert (pack_leaf(r2) if r2 else 0) == int(rec_ref[1]), k
+            assert rms2 == rms_ref[1], (k, rms2, rms_ref[1])
+            n2 += 1
+    assert n1 > 60 and n2 > 60
+
+
+def test_try_phase_errors(mns):
+    img = mns.GrayImage(np.zeros((24, 40), np.uint8))
+    cfg = mns.EncoderConfig()
+    with pytest.raises(ValueError, match="level 2 expects block size 8, got 4"):
+        mns.try_phase1(img, mns.BlockRect(0, 0, 4), 2, cfg)
+    with pytest.raises(ValueError, match="no 32x32 domain fits a 40x24 image"):
+        mns.try_phase1(img, mns.BlockRect(0, 0, 16), 1, cfg)
+    with pytest.raises(ValueError, match="out of bounds for 40x24 raster"):
+        mns.try_phase1(img, mns.BlockRect(36, 0, 8), 2, cfg)
+    with pytest.raises(ValueError, match="phase 2 exists only at levels 1..3"):
+        mns.try_phase2(img, mns.BlockRect(0, 0, 2), 4, cfg)
+    assert mns.try_phase2(img, mns.BlockRect(0, 0, 16), 1, cfg)[0] is not None  # flat: accepted
