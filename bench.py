@@ -257,7 +257,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                           torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
                           torch.zeros(1, dtype=torch.int64, device=dev), W, H, 1, r0, r1,
                           unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device=dev))
-    dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world)
+    # e3 = inf: the code has no 2x2 leaves, so the decoder carries the 2x2-sum lattice between passes
+    dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world, lattice=True)
     out_host = torch.empty((16 * (r1 - r0), W), dtype=torch.uint8).pin_memory()
     stream = torch.cuda.current_stream()
 
@@ -425,7 +426,10 @@ def run_ours(args, img_np, rank, world, local_rank):
     if rank != 0:
         return
     hbm, which = peaks()
-    algo = 8.0 * own_px  # fp32 raster t read + t+2 written per steady-state pass
+    # state read + written per steady-state pass: the fp32 lattice (W/2 x H/2) of t and of t+2 in lattice
+    # mode, else the fp32 raster of t and of t+2
+    algo = (2.0 if dec.lattice else 8.0) * own_px
+    kname = "decode_pair_lat_kernel" if dec.lattice else "decode_pair_kernel"
     achieved = algo / (pass_ms / 1e3) / 1e9
     cpu_v, cpu_dt = (None, None)
     if world == 1 and not args.no_cpu:
@@ -447,8 +451,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                        "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small,
                        "with_code_gather": gather},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": measured_traffic("decode_pair_kernel") if world == 1 else None,
-                     "algorithmic_bytes": algo, "kernel": "decode_pair_kernel (steady-state pass = 2 sweeps)",
+                     "traffic": measured_traffic(kname) if world == 1 else None,
+                     "algorithmic_bytes": algo, "kernel": f"{kname} (steady-state pass = 2 sweeps)",
                      "peak_source": which},
         "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
                           "sample": f"c5 rows 0..{args.cpu_baseline_rows - 1} encoded + {ITERS}-sweep decoded as its own "

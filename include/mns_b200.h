@@ -124,6 +124,33 @@ int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int3
                       int32_t root_row_begin, int32_t root_row_end, const float *cur, float initial_value, float *nxt,
                       uint8_t *out, void *stream);
 
+/* Lattice-state decoding for codes WITHOUT 2x2 units (every leaf side >= 4, e.g.
+ * the 16->8->4 quadtree, e3 = inf).  Such a code reads the previous raster only
+ * through its even 2x2-sum lattice (image.py:160-171 downsample_mean2 order), so
+ * the state between passes is that lattice: (height/2) rows of width/2 floats,
+ * each row de-interleaved (the width/4 even lattice columns, then the odd ones),
+ * a quarter of the raster's bytes with bit-identical values -- the decoded image
+ * equals the raster path's bit for bit.  *d_error (device int32, zeroed by the
+ * caller) is set to 1 if a 2x2 unit is met (the output is then undefined; use
+ * the raster path).
+ *
+ * mns_decode_pass_lattice: two sweeps t -> t+2 (as mns_decode_sweep2; lattice
+ * rows [8*root_row_begin - 16, 8*root_row_end + 16) of cur_lattice resident,
+ * 16-byte aligned; cur_lattice NULL = flat start; exactly one of nxt_lattice
+ * and out).  mns_decode_flat_lattice: the single first sweep from the flat
+ * raster, written as lattice (odd sweep counts).  mns_decode_quadtree_lattice:
+ * the whole decode (stop_delta = 0) into the uint8 image, as mns_decode_quadtree
+ * with out != NULL; lat_ping / lat_pong hold (height/2)*(width/2) floats each. */
+int mns_decode_pass_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                            int32_t root_row_begin, int32_t root_row_end, const float *cur_lattice, float initial_value,
+                            float *nxt_lattice, uint8_t *out, int32_t *d_error, void *stream);
+int mns_decode_flat_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                            int32_t root_row_begin, int32_t root_row_end, float initial_value, float *nxt_lattice,
+                            void *stream);
+int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                                int32_t iters, float initial_value, float *lat_ping, float *lat_pong, uint8_t *out,
+                                int32_t *d_error, void *workspace, int64_t workspace_bytes, void *stream);
+
 /* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
  * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-
  * baseline codes whose domains are explicit (BaselinePayload) and for arbitrary
@@ -185,10 +212,12 @@ int mns_read_stream(const uint8_t *data, int64_t n_bytes, int32_t mns, int32_t t
 /* Rate-distortion metrics on device (bench.py:39-79 rd_sweep):
  * exact sum of squared differences of two W x H uint8 images (metrics.py:16-31
  * mse = sse / (W*H)), and the leaf tallies of a record array (encoder.py:135-142):
- * out5 = {level-1, level-2, level-3, level-4 leaves, phase-2 leaves}. */
+ * out6 = {level-1, level-2, level-3, level-4 leaves, phase-2 leaves, leaves painted
+ * as 2x2 units (level 4 and level-3 phase 2: a code with none can be decoded on
+ * lattice state, mns_decode_pass_lattice)}. */
 int mns_image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch_b, int32_t width, int32_t height,
                   uint64_t *d_sse, void *stream);
-int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out5, void *stream);
+int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out6, void *stream);
 
 /* Domain-offset histogram of a full-search result (bench.py:119-127 offset_histogram
  * over the samples of encoder.py:249-309): offset = domain centre - range centre

@@ -46,12 +46,22 @@ from .codec import (  # noqa: F401
 )
 
 from . import bitstream  # noqa: F401  (reference mnscodec.bitstream)
-from .bitstream import read_stream, stream_bit_count, write_stream  # noqa: F401
+from .bitstream import (  # noqa: F401
+    StreamFormatError,
+    leaf_bit_width,
+    level_id_bit_count,
+    payload_bit_width,
+    read_stream,
+    stream_bit_count,
+    write_stream,
+)
 from .rd import (  # noqa: F401  (reference mnscodec.bench)
     RD_CSV_COLUMNS,
     OffsetHistogram,
     RdPoint,
     histogram_csv,
+    mse,
+    psnr,
     offset_histogram,
     offset_histogram_device,
     rd_csv,

@@ -107,6 +107,7 @@ class DeviceCode:
     mode: str = "mns"
     technique2: bool = True
     unit_map: "object" = None  # torch.int32 [n_roots * 32]: decoder unit map (mns_record.h), optional
+    min_leaf: int = 0          # smallest painted unit side if known (4: no 2x2 units -> lattice-state decode), 0 unknown
 
     def n_records(self) -> int:
         return int(self.count.item())
@@ -171,6 +172,9 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     base = img.data_ptr()
     if root_rows is not None and h != H:
         base -= max(0, 16 * r0 - 16) * img.stride(1)
+    # e3 = inf: every visited level-3 node passes phase 1 (encoder.py:160-165, before phase 2), so no
+    # leaf is 2x2 and no level-3 phase-2 leaf has 2x2 quadrants
+    out.min_leaf = 4 if math.isinf(config.e3) else 0
     cfg = enc_cfg(config, root_level)
     N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
                                   ctypes.byref(cfg), N.ptr(out.records), out.records.numel(), N.ptr(out.root_offsets),
@@ -190,9 +194,24 @@ def build_unit_map(code: DeviceCode, stream=None):
     return code.unit_map
 
 
+def min_leaf_side(code: DeviceCode) -> int:
+    """Smallest unit side the decoder paints for a device code: 2 if any leaf is 2x2 or is a level-3
+    phase-2 leaf (2x2 quadrants), else 4 (from the encoder's guarantee, else counted on the GPU)."""
+    if not code.min_leaf:
+        from .rd import unit2_leaves
+
+        code.min_leaf = 2 if unit2_leaves(code.records, code.n_records()) else 4
+    return code.min_leaf
+
+
 def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, initial_value: float = 128.0,
                   out=None, rasters=None, want_u8: bool = True, stream=None):
-    """Jacobi decode of a device quadtree code (single image); returns (uint8 [H, W] padded, iters_done tensor)."""
+    """Jacobi decode of a device quadtree code (single image); returns (uint8 [H, W] padded, iters_done tensor).
+
+    Codes without 2x2 units decoded to uint8 with stop_delta == 0 run on lattice state
+    (mns_decode_quadtree_lattice: a quarter of the raster traffic, identical output); the rest on
+    fp32 rasters (mns_decode_quadtree).
+    """
     torch = _torch()
     L = N.lib()
     W, H = code.padded_w, code.padded_h
@@ -205,6 +224,15 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
     it = torch.zeros(1, dtype=torch.int32, device=dev)
     wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
     ws = _WS.get("dec", wsb, dev)
+    if want_u8 and stop_delta == 0.0 and min_leaf_side(code) >= 4:
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        n_lat = (H // 2) * (W // 2)
+        lat = (rasters[0].view(-1)[:n_lat], rasters[1].view(-1)[:n_lat])
+        N.check(L.mns_decode_quadtree_lattice(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters),
+                                              float(initial_value), N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out),
+                                              N.ptr(err), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+        it.fill_(int(iters))
+        return out, it, rasters
     N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters), float(stop_delta),
                                   float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),
                                   N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
@@ -456,8 +484,12 @@ def decode(code, config: Optional[DecodeConfig] = None) -> GrayImage:
     if code.mode in ("no_search", "mns") and (not hasattr(code, "has_records") or code.has_records):
         rec, offs = _records_grouped(code if isinstance(code, QuadtreeCode) else _wrap_reference(code))
         dev = _device()
+        lv = (rec >> np.uint64(30)) & np.uint64(3)  # level - 1 (include/mns_record.h)
+        p2 = (rec >> np.uint64(32)) & np.uint64(1)
+        unit2 = bool(((lv == 3) | ((lv == 2) & (p2 == 1))).any())  # 2x2 leaves or level-3 phase-2 quadrants
         dcode = DeviceCode(torch.from_numpy(rec.view(np.int64)).to(dev), torch.from_numpy(offs).to(dev),
-                           torch.tensor([len(rec)], dtype=torch.int64, device=dev), W, H)
+                           torch.tensor([len(rec)], dtype=torch.int64, device=dev), W, H,
+                           min_leaf=2 if unit2 else 4)
         out, _, _ = decode_device(dcode, cfg.max_iters, cfg.stop_delta, cfg.initial_value)
     else:
         u = _units_to_device(_baseline_units(code), np.float32)

@@ -103,6 +103,13 @@ int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, 
 int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
              const mns_enc_cfg *cfg, uint64_t *d_rec, double *d_rms, cudaStream_t stream);
 int decode_workspace_bytes(int W, int H, int64_t *bytes);
+int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
+                        float init, float *nxt, uint8_t *out, int *err, cudaStream_t stream);
+int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
+                        cudaStream_t stream);
+int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
+                            float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
+                            int64_t workspace_bytes, cudaStream_t stream);
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
@@ -132,7 +139,7 @@ int read_stream_workspace_bytes(int64_t nbytes, int64_t *bytes);
 int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, int ph, uint64_t *records,
                 int64_t capacity, int32_t *root_offsets, int64_t *d_count, int64_t *d_status, void *workspace,
                 int64_t workspace_bytes, cudaStream_t s);
-int code_stats(const uint64_t *records, int64_t n, int64_t *out5, cudaStream_t stream);
+int code_stats(const uint64_t *records, int64_t n, int64_t *out6, cudaStream_t stream);
 int offset_histogram(const int32_t *dom, int64_t n_ranges, int W, int H, int B, int step, int32_t *hist_x,
                      int32_t *hist_y, int32_t *joint, cudaStream_t stream);
 
@@ -167,8 +174,8 @@ int mns_image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t p
     GUARD(mns::image_sse(a, pitch_a, b, pitch_b, width, height, d_sse, (cudaStream_t)stream));
 }
 
-int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out5, void *stream) {
-    GUARD(mns::code_stats(records, n_records, d_out5, (cudaStream_t)stream));
+int mns_code_stats(const uint64_t *records, int64_t n_records, int64_t *d_out6, void *stream) {
+    GUARD(mns::code_stats(records, n_records, d_out6, (cudaStream_t)stream));
 }
 
 int mns_offset_histogram(const int32_t *dom, int64_t n_ranges, int32_t width, int32_t height, int32_t range_size,
@@ -224,6 +231,27 @@ int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int3
                       uint8_t *out, void *stream) {
     GUARD(mns::decode_sweep2(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end, cur,
                              initial_value, nxt, out, (cudaStream_t)stream));
+}
+
+int mns_decode_pass_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                            int32_t root_row_begin, int32_t root_row_end, const float *cur_lattice, float initial_value,
+                            float *nxt_lattice, uint8_t *out, int32_t *d_error, void *stream) {
+    GUARD(mns::decode_pass_lattice(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end,
+                                   cur_lattice, initial_value, nxt_lattice, out, d_error, (cudaStream_t)stream));
+}
+
+int mns_decode_flat_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+                            int32_t root_row_begin, int32_t root_row_end, float initial_value, float *nxt_lattice,
+                            void *stream) {
+    GUARD(mns::decode_flat_lattice(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end,
+                                   initial_value, nxt_lattice, (cudaStream_t)stream));
+}
+
+int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
+                                int32_t iters, float initial_value, float *lat_ping, float *lat_pong, uint8_t *out,
+                                int32_t *d_error, void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::decode_quadtree_lattice(records, root_offsets, width, height, iters, initial_value, lat_ping, lat_pong,
+                                       out, d_error, workspace, workspace_bytes, (cudaStream_t)stream));
 }
 
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

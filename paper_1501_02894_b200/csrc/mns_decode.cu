@@ -164,7 +164,7 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // absolute raster row / 2 mod QR, column = window column / 2, window origin wx0) or, for 2x2
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
-template <int QSTR, int HALF, class RawSum>
+template <int QSTR, int HALF, int RING = QR, bool RAW = true, class RawSum>
 __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
                                             const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
                                             bool interior, int W, int H, float (&v)[16]) {
@@ -204,7 +204,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                 Y = clamped_offset(L.ly, 2 << k, ryg, H);
             }
             const int qr = (ryg - 16 + Y) >> 1, qc = (rxg - 16 + X - wx0) >> 1;
-            const float *row = lat + (qr & (QR - 1)) * QSTR;  // rows +0..+3 stay inside QRP
+            const float *row = lat + (qr & (RING - 1)) * QSTR;  // rows +0..+3 stay inside the padded ring
             const float *p0 = row + (qc & 1) * HALF + (qc >> 1);              // columns qc, qc + 2
             const float *p1 = row + ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);  // columns qc + 1, qc + 3
 #pragma unroll
@@ -221,7 +221,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
         const float2 p3 = fadd2(make_float2(v[12], v[13]), make_float2(v[14], v[15]));
         const float2 pp = fadd2(fadd2(p0, p1), fadd2(p2, p3));
         own = pp.x + pp.y;
-    } else if (live) {  // four 2x2 units with odd (or clamped) 4x4 domains
+    } else if (RAW && live) {  // four 2x2 units with odd (or clamped) 4x4 domains
 #pragma unroll
         for (int c = 0; c < 4; c++) {
             const uint32_t d = c == 0 ? d0 : (c == 1 ? word.x >> 16 : (c == 2 ? word.y & 0xFFFFu : word.y >> 16));
@@ -593,6 +593,172 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------- lattice-state passes
+// A code without 2x2 units (every unit side >= 4, e.g. the 16->8->4 quadtree with e3 = inf) reads
+// the previous raster only through its even 2x2-sum lattice (downsample_mean2's order), so the
+// state carried between passes can be that lattice: a quarter of the raster's bytes, bit-identical
+// values.  Global layout: (H/2) rows of W/2 floats, each row de-interleaved (the W/4 even lattice
+// columns, then the W/4 odd ones) -- the layout paint_block reads, so TMA lands 8-row blocks of it
+// straight in the stage-A ring (a 3D box: 52 columns x {even, odd} x 8 rows; the 4 extra columns
+// keep the box row a 16-byte multiple and pad the ring row to 104 floats).  Stage A paints t+1
+// into the on-chip lattice qb, stage B paints t+2 and stores its lattice (or, on the last pass, the
+// uint8 image).  No raster reduction, no t+1 raw ring: ~35 KB of shared memory instead of 105 KB.
+constexpr int LHB = WA / 4 + 4;    // 52 staged lattice columns per parity
+constexpr int LQS = 2 * LHB;       // 104-float ring row: even half | odd half
+constexpr int LQR = 64;            // t-lattice ring rows: 8 root-row slots (up to 5 in flight)
+constexpr int LNS = LQR / 8;
+constexpr int LQRP = LQR + 8;      // + a second copy of slot 0, so a 4-row read never wraps
+constexpr int LBOX = 8 * LQS * 4;  // bytes of one slot
+constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * QS * 4;
+#ifndef LAT_MINB
+#define LAT_MINB 3
+#endif
+
+__global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                        const SweepParams p) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    float(*qa)[LQS] = reinterpret_cast<float(*)[LQS]>(dsm);
+    float(*qb)[QS] = reinterpret_cast<float(*)[QS]>(dsm + LQRP * LQS * 4);
+    __shared__ __align__(8) uint64_t bars[LNS];
+    __shared__ float st[16];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int x0 = blockIdx.x * BR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
+    const int r_s = p.rr0 + blockIdx.y * p.cr, r_e = min(r_s + p.cr, p.rr1);
+    const int rh = p.H / 16, lw = p.W / 2;
+    const bool flat = p.cur == nullptr;
+    const int nblocks = (r_e - r_s) + 4;  // block k = the 8 lattice rows of root row r_s - 2 + k
+    if (tid < 16) st[tid] = kUnitS[tid];
+    if (tid == 0) {
+        for (int b = 0; b < LNS; b++) mbar_init(&bars[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        if (k < nblocks) {
+            const int row = r_s - 2 + k, slot = row & (LNS - 1), z = 8 * row - p.y_lo / 2;
+            mbar_arrive_expect_tx(&bars[slot], slot == 0 ? 2 * LBOX : LBOX);
+            tma_load_3d(&qa[8 * slot][0], &tmap, x0 / 4 - 8, 0, z, &bars[slot]);
+            if (slot == 0) tma_load_3d(&qa[LQR][0], &tmap, x0 / 4 - 8, 0, z, &bars[0]);
+        }
+    };
+    const uint32_t bar0 = smem_u32(&bars[0]);
+    uint32_t phase = 0;  // per-slot parity of the next wait (stage-A threads wait on every block in order)
+    auto wait_block = [&](int k) {
+        if (k < nblocks) {
+            const int slot = (r_s - 2 + k) & (LNS - 1);
+            mbar_wait_addr(bar0 + 8 * slot, (phase >> slot) & 1);
+            phase ^= 1u << slot;
+        }
+    };
+    const Lane L = lane_of(lane);
+    const bool stage_a = warp < NWA;
+    if (!flat) {
+        if (tid == 0) {
+            prefetch_tmap(&tmap);
+            for (int k = 0; k < LNS; k++) issue(k);
+        }
+        if (stage_a) {
+            wait_block(0);
+            wait_block(1);
+        }
+    }
+    // stage A: root columns -1 .. BR of the band; stage B: 0 .. BR-1
+    const int rc = stage_a ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - NWA) + (lane >> 4);
+    const int rxi = blockIdx.x * BR + rc;
+    const bool col_ok = rxi >= 0 && rxi < p.rw;
+    const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
+    const int lag = stage_a ? 0 : 2;  // iteration i: A paints root row i, B paints i - 2
+    const int row_lo = stage_a ? max(r_s - 1, 0) : r_s, row_hi = stage_a ? min(r_e + 1, rh) : r_e;
+    const uint2 *ubase = reinterpret_cast<const uint2 *>(p.unit_map) + ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 +
+                         (lane & 15);
+    const ptrdiff_t ustride = (ptrdiff_t)p.rw * 16;
+    auto word_of = [&](int row, const uint2 *ptr) {
+        return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
+    };
+    auto no_raw = [](int, int) { return 0.f; };
+    const uint2 *uptr = ubase + (ptrdiff_t)(r_s - 1 - lag) * ustride;
+    uint2 word = word_of(r_s - 1 - lag, uptr);
+    for (int i = r_s - 1; i <= r_e + 1; i++) {
+        const int row = i - lag;
+        uptr += ustride;
+        const uint2 wnext = word_of(row + 1, uptr);
+        __syncthreads();
+        if (!flat && tid == 0 && i >= r_s) {
+            fence_proxy_async();  // generic reads of the slot just released complete before its refill
+            issue(i - r_s + LNS);
+        }
+        const int rxg = rxi * 16, ryg = row * 16;
+        const bool interior = interior_col && row >= 1 && row + 1 < rh;
+        float v[16];
+        if (stage_a) {
+            if (!flat) wait_block(i - r_s + 3);
+            const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
+            paint_block<LQS, LHB, LQR, false>(word, live, L, st, &qa[0][0], no_raw, flat, p.init, rxg, ryg, xa0,
+                                              interior, p.W, p.H, v);
+            if (live) {
+                if (!flat && (word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
+                const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
+                const int g = (ryg + L.ly) >> 1;
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+                    lat_store<QS, QH>(&qb[0][0], g + r, wc >> 1,
+                                      make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
+                                                  ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]));
+            }
+        } else {
+            const bool live = col_ok && row >= r_s;
+            paint_block<QS, QH, QR, false>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg, xb0,
+                                           interior, p.W, p.H, v);
+            if (live) {
+                if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);
+                if (p.nxt) {  // the lattice of t+2, de-interleaved rows
+                    const int gy = (ryg + L.ly) >> 1, gc = (rxg + L.lx) >> 2;
+                    float *d = p.nxt + (ptrdiff_t)gy * lw + gc;
+#pragma unroll
+                    for (int r = 0; r < 2; r++, d += lw) {
+                        d[0] = ((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5];
+                        d[lw / 2] = ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7];
+                    }
+                } else {
+                    store_block(v, nullptr, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
+                }
+            }
+        }
+        word = wnext;
+    }
+}
+
+// The first sweep from the flat raster straight into lattice form (an odd sweep count): every
+// unit paints the constant x = clip(s/4 * 4 init + (o - s init)) (paint_block's flat path), and
+// each 2x2 cell lies inside one unit, so its lattice entry is ((x + x) + x) + x.  One thread per
+// unit-map word (two cells).
+__global__ void flat_lattice_kernel(const uint32_t *unit_map, int umap_r0, int rw, int rr0, int rr1, float init,
+                                    float *nxt) {
+    const long long n = (long long)(rr1 - rr0) * rw * 32;
+    const int lw = rw * 8;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long root = i >> 5;
+        const int word = (int)(i & 31), ry = rr0 + (int)(root / rw), rx = (int)(root % rw);
+        const uint32_t w = unit_map[((long long)(ry - umap_r0) * rw + rx) * 32 + word];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const uint32_t d = h ? w >> 16 : w & 0xFFFFu;
+            const int m = 2 * word + h;
+            int cx = 0, cy = 0;
+#pragma unroll
+            for (int b = 0; b < 3; b++) {
+                cx |= ((m >> (2 * b)) & 1) << b;
+                cy |= ((m >> (2 * b + 1)) & 1) << b;
+            }
+            const float sc = kUnitS[d & 15];
+            const float x = fminf(255.f, fmaxf(0.f, fmaf(0.25f * sc, 4.f * init, fmaf(-sc, init, unit_o(d)))));
+            const int gy = 8 * ry + cy, gx = 8 * rx + cx;
+            nxt[(ptrdiff_t)gy * lw + (gx & 1) * (lw / 2) + (gx >> 1)] = ((x + x) + x) + x;
+        }
+    }
+}
+
 // Unit map from records grouped by root (one warp per root): cells in smem, then one
 // coalesced 32-bit word (two cells) per lane.
 __global__ void build_unit_map_kernel(const uint64_t *records, const int32_t *root_offsets, int rw, int rr0,
@@ -840,6 +1006,102 @@ int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, 
     p.n_ctas = grid.x * grid.y;
     decode_pair_kernel<<<grid, DT2, PAIR_SMEM, stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+static int ensure_lat_attr() {
+    static std::atomic<unsigned long long> done{0};
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel, LAT_SMEM, done));
+    return 0;
+}
+
+// Two sweeps over root rows [rr0, rr1) on lattice state (see decode_pair_lat_kernel).  cur/nxt are
+// virtual-global lattice bases (lattice row 0); lattice rows [8 rr0 - 16, 8 rr1 + 16) of cur are
+// resident.  err (device int) is set to 1 if a 2x2 unit is met.
+int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
+                        float init, float *nxt, uint8_t *out, int *err, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
+    MNS_CHECK_ARG(umap_r0 <= (rr0 > 0 ? rr0 - 1 : 0) && umap_r0 >= 0, "unit map must start at root row rr0 - 1");
+    MNS_CHECK_ARG(H <= 65534, "height exceeds the record coordinate range");
+    MNS_CHECK_ARG((nxt != nullptr) != (out != nullptr), "exactly one of nxt / out");
+    MNS_CHECK_ARG(err != nullptr, "error flag required");
+    if (ensure_lat_attr()) return -1;
+    SweepParams p{};
+    p.unit_map = unit_map;
+    p.umap_r0 = umap_r0;
+    p.W = W;
+    p.H = H;
+    p.rw = W / 16;
+    p.rr0 = rr0;
+    p.rr1 = rr1;
+    p.y_lo = rr0 * 16 - 32 > 0 ? rr0 * 16 - 32 : 0;
+    const int y_hi = rr1 * 16 + 32 < H ? rr1 * 16 + 32 : H;
+    p.cur = cur;
+    p.init = init;
+    p.nxt = nxt;
+    p.out_u8 = out;
+    p.state = err;
+    CUtensorMap tmap{};
+    if (cur) {
+        MNS_CHECK_ARG(((uintptr_t)cur & 15) == 0, "lattice must be 16-byte aligned");
+        if (encode_tmap_3d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cur + (ptrdiff_t)(p.y_lo / 2) * (W / 2),
+                           (uint64_t)(W / 4), 2, (uint64_t)((y_hi - p.y_lo) / 2), (uint64_t)W, (uint64_t)W * 2, LHB,
+                           2, 8))
+            return -1;
+    }
+    p.cr = rows_per_cta(rr1 - rr0, (p.rw + BR - 1) / BR, CR2);
+    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + p.cr - 1) / p.cr);
+    p.n_ctas = grid.x * grid.y;
+    decode_pair_lat_kernel<<<grid, DT2, LAT_SMEM, stream>>>(tmap, p);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
+                        cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16 && 0 <= umap_r0 && umap_r0 <= rr0, "bad root row range");
+    const long long n = (long long)(rr1 - rr0) * (W / 16) * 32;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 8);
+    flat_lattice_kernel<<<blocks, 256, 0, stream>>>(unit_map, umap_r0, W / 16, rr0, rr1, init, nxt);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// decode_quadtree for codes without 2x2 units, on lattice state (lat_ping / lat_pong: (H/2) x (W/2)
+// floats each); stop_delta = 0, uint8 output.  *err (device) = 1 if the code had a 2x2 unit.
+int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
+                            float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
+                            int64_t workspace_bytes, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    MNS_CHECK_ARG(out != nullptr && err != nullptr, "out and err required");
+    int64_t need;
+    decode_workspace_bytes(W, H, &need);
+    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
+    int *state = reinterpret_cast<int *>(workspace);
+    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
+    MNS_CUDA_TRY(cudaMemsetAsync(err, 0, 4, stream));
+    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
+    int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
+    if (rc) return rc;
+    if (iters == 1) return decode_sweep(umap, W, H, 0, H / 16, nullptr, init, nullptr, out, state, 0.0, stream);
+    const float *cur = nullptr;
+    int it = 0;
+    if (iters & 1) {
+        rc = decode_flat_lattice(umap, 0, W, H, 0, H / 16, init, lat_pong, stream);
+        if (rc) return rc;
+        cur = lat_pong;
+        it = 1;
+    }
+    for (; it < iters; it += 2) {
+        const bool last = it + 2 == iters;
+        float *nxt = last ? nullptr : (cur == lat_ping ? lat_pong : lat_ping);
+        rc = decode_pass_lattice(umap, 0, W, H, 0, H / 16, cur, init, nxt, last ? out : nullptr, err, stream);
+        if (rc) return rc;
+        cur = nxt;
+    }
     return 0;
 }
 

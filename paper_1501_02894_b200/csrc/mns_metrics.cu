@@ -28,16 +28,18 @@ __global__ void sse_kernel(const uint8_t *a, int64_t pa, const uint8_t *b, int64
 
 // out[0..3] = leaves per level 1..4, out[4] = phase-2 leaves (warp-aggregated atomics)
 __global__ void code_stats_kernel(const uint64_t *rec, long long n, unsigned long long *out) {
-    unsigned long long c[5] = {0, 0, 0, 0, 0};
+    unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const uint64_t r = rec[i];
         const int lv = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3);
 #pragma unroll
         for (int k = 0; k < 4; k++) c[k] += lv == k;
-        c[4] += (r >> MNS_REC_PHASE2_SHIFT) & 1;
+        const int p2 = (int)((r >> MNS_REC_PHASE2_SHIFT) & 1);
+        c[4] += p2;
+        c[5] += lv == 3 || (lv == 2 && p2);  // leaves painted as 2x2 units (level 4, level-3 quadrants)
     }
 #pragma unroll
-    for (int k = 0; k < 5; k++) {
+    for (int k = 0; k < 6; k++) {
         unsigned long long v = c[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -87,12 +89,12 @@ int image_sse(const uint8_t *a, int64_t pitch_a, const uint8_t *b, int64_t pitch
     return 0;
 }
 
-int code_stats(const uint64_t *records, int64_t n, int64_t *out5, cudaStream_t stream) {
+int code_stats(const uint64_t *records, int64_t n, int64_t *out6, cudaStream_t stream) {
     MNS_CHECK_ARG(n >= 0, "negative record count");
-    MNS_CUDA_TRY(cudaMemsetAsync(out5, 0, 5 * 8, stream));
+    MNS_CUDA_TRY(cudaMemsetAsync(out6, 0, 6 * 8, stream));
     if (n == 0) return 0;
     const long long blocks = (n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184;
-    code_stats_kernel<<<(unsigned)blocks, 256, 0, stream>>>(records, n, reinterpret_cast<unsigned long long *>(out5));
+    code_stats_kernel<<<(unsigned)blocks, 256, 0, stream>>>(records, n, reinterpret_cast<unsigned long long *>(out6));
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -40,11 +40,13 @@ def resident_rows(r0: int, r1: int, height: int, halo: int = HALO) -> tuple[int,
 
 
 def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None,
-                   halo: int = HALO) -> None:
+                   halo: int = HALO, row_div: int = 1) -> None:
     """After a sweep: send my first/last `halo` own rows to the neighbours, receive theirs into my halos.
 
-    ``raster`` holds rows [y_lo, y_hi) (resident_rows with the same halo) of the full image.  Works
-    for any torch.distributed backend (NCCL on GPUs, gloo on CPU).
+    ``raster`` holds rows [y_lo, y_hi) (resident_rows with the same halo) of the full image, or with
+    row_div = 2 the lattice rows [y_lo/2, y_hi/2) of lattice-state decoding (one lattice row per two
+    raster rows; halo/2 rows exchanged).  Works for any torch.distributed backend (NCCL on GPUs,
+    gloo on CPU).
     """
     import torch.distributed as dist
 
@@ -53,14 +55,14 @@ def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int,
     if 16 * (r1 - r0) < halo:
         raise ValueError(f"strip of {16 * (r1 - r0)} rows is thinner than the {halo}-row halo")
     y_lo, y_hi = resident_rows(r0, r1, height, halo)
-    own0, own1 = 16 * r0 - y_lo, 16 * r1 - y_lo
+    own0, own1, hl = (16 * r0 - y_lo) // row_div, (16 * r1 - y_lo) // row_div, halo // row_div
     ops = []
     if rank > 0:
-        ops.append(dist.P2POp(dist.isend, raster[own0: own0 + halo], rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, raster[own0 - halo: own0], rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, raster[own0: own0 + hl], rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, raster[own0 - hl: own0], rank - 1, group))
     if rank < world - 1:
-        ops.append(dist.P2POp(dist.isend, raster[own1 - halo: own1], rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, raster[own1: own1 + halo], rank + 1, group))
+        ops.append(dist.P2POp(dist.isend, raster[own1 - hl: own1], rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, raster[own1: own1 + hl], rank + 1, group))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
 
@@ -141,26 +143,32 @@ def gather_codes(records, count: int, root_offsets, rank: int, world: int, dst: 
 
 
 class StripDecoder:
-    """Jacobi decode of one rank's strip: strip-local code + fp32 halo'd ping/pong rasters.
+    """Jacobi decode of one rank's strip: strip-local code + fp32 halo'd ping/pong state.
 
-    Sweeps run two per pass (mns_decode_sweep2) on rasters with DEC_HALO resident rows; the
-    32 boundary rows are exchanged once per pass, and the unit map carries one neighbour root
-    row on each side.  ``code.unit_map`` is rebound to a view of that halo'd map, so an encoder
-    writing into ``code`` fills it in place.
+    Sweeps run two per pass on state with DEC_HALO resident raster rows; the boundary rows are
+    exchanged once per pass, and the unit map carries one neighbour root row on each side.
+    ``code.unit_map`` is rebound to a view of that halo'd map, so an encoder writing into ``code``
+    fills it in place.  Codes without 2x2 units (``code.min_leaf == 4``, e.g. e3 = inf) run on
+    lattice state (mns_decode_pass_lattice: the even 2x2-sum lattice, a quarter of the raster's
+    bytes, identical output); ``lattice`` forces the choice.
     """
 
-    def __init__(self, code, height: int, width: int, r0: int, r1: int, rank: int = 0, world: int = 1):
+    def __init__(self, code, height: int, width: int, r0: int, r1: int, rank: int = 0, world: int = 1,
+                 lattice=None):
         import torch
 
         self.code, self.H, self.W, self.r0, self.r1 = code, height, width, r0, r1
         self.rank, self.world = rank, world
+        self.lattice = (getattr(code, "min_leaf", 0) == 4) if lattice is None else bool(lattice)
         self.y_lo, self.y_hi = resident_rows(r0, r1, height, DEC_HALO)
         dev = code.records.device
         rows = self.y_hi - self.y_lo
-        self.ping = torch.empty((rows, width), dtype=torch.float32, device=dev)
-        self.pong = torch.empty((rows, width), dtype=torch.float32, device=dev)
+        shape = (rows // 2, width // 2) if self.lattice else (rows, width)
+        self.ping = torch.empty(shape, dtype=torch.float32, device=dev)
+        self.pong = torch.empty(shape, dtype=torch.float32, device=dev)
         self.out = torch.empty((16 * (r1 - r0), width), dtype=torch.uint8, device=dev)
         self.state = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.error = torch.zeros(1, dtype=torch.int32, device=dev)  # lattice mode: 1 if a 2x2 unit was met
         if code.unit_map is None:
             from .codec import build_unit_map
 
@@ -175,9 +183,21 @@ class StripDecoder:
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
 
+    def _state_base(self, t):
+        """Virtual-global base (row 0) of a resident state tensor."""
+        if t is None:
+            return ctypes.c_void_p(0)
+        if self.lattice:
+            return ctypes.c_void_p(t.data_ptr() - (self.y_lo // 2) * (self.W // 2) * 4)
+        return self._vbase(t, self.y_lo, 4)
+
     def launches(self, iters: int) -> int:
         """Kernel launches of run(iters): an odd first sweep alone, then two sweeps per pass."""
         return iters // 2 + (iters & 1)
+
+    def _exchange(self, t):
+        exchange_halos(t, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO,
+                       row_div=2 if self.lattice else 1)
 
     def run(self, iters: int = 10, initial_value: float = 128.0, stream=None, sweep_events=None, out=None):
         """iters sweeps (stop_delta = 0); the last pass writes the rounded uint8 strip into `out` (default self.out).
@@ -198,32 +218,39 @@ class StripDecoder:
             last = iters == 1
             if sweep_events is not None:
                 sweep_events[n][0].record()
-            N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1, ctypes.c_void_p(0),
-                                       float(initial_value),
-                                       ctypes.c_void_p(0) if last else self._vbase(self.pong, self.y_lo, 4),
-                                       ob if last else ctypes.c_void_p(0), N.ptr(self.state), 0.0, s))
+            if self.lattice and not last:
+                N.check(L.mns_decode_flat_lattice(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
+                                                  float(initial_value), self._state_base(self.pong), s))
+            else:
+                N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1,
+                                           ctypes.c_void_p(0), float(initial_value),
+                                           ctypes.c_void_p(0) if last else self._state_base(self.pong),
+                                           ob if last else ctypes.c_void_p(0), N.ptr(self.state), 0.0, s))
             if sweep_events is not None:
                 sweep_events[n][1].record()
             n += 1
             it = 1
             if not last:
                 cur = self.pong
-                exchange_halos(cur, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO)
+                self._exchange(cur)
         while it < iters:
             last = it + 2 == iters
             nxt = None if last else (self.ping if cur is not self.ping else self.pong)
             if sweep_events is not None:
                 sweep_events[n][0].record()
-            N.check(L.mns_decode_sweep2(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
-                                        self._vbase(cur, self.y_lo, 4) if cur is not None else ctypes.c_void_p(0),
-                                        float(initial_value),
-                                        self._vbase(nxt, self.y_lo, 4) if nxt is not None else ctypes.c_void_p(0),
-                                        ob if last else ctypes.c_void_p(0), s))
+            if self.lattice:
+                N.check(L.mns_decode_pass_lattice(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
+                                                  self._state_base(cur), float(initial_value), self._state_base(nxt),
+                                                  ob if last else ctypes.c_void_p(0), N.ptr(self.error), s))
+            else:
+                N.check(L.mns_decode_sweep2(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
+                                            self._state_base(cur), float(initial_value), self._state_base(nxt),
+                                            ob if last else ctypes.c_void_p(0), s))
             if sweep_events is not None:
                 sweep_events[n][1].record()
             n += 1
             it += 2
             if not last:
-                exchange_halos(nxt, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO)
+                self._exchange(nxt)
                 cur = nxt
         return out

@@ -424,3 +424,196 @@ def test_try_phase_errors(mns):
     with pytest.raises(ValueError, match="phase 2 exists only at levels 1..3"):
         mns.try_phase2(img, mns.BlockRect(0, 0, 2), 4, cfg)
     assert mns.try_phase2(img, mns.BlockRect(0, 0, 16), 1, cfg)[0] is not None  # flat: accepted
+
+
+def _lattice_of(t):
+    """Even 2x2-sum lattice of an fp32 raster in downsample_mean2's order, rows de-interleaved
+    (even lattice columns, then odd): the state of lattice-mode decoding."""
+    q = ((t[0::2, 0::2] + t[0::2, 1::2]) + t[1::2, 0::2]) + t[1::2, 1::2]
+    return torch.cat([q[:, 0::2], q[:, 1::2]], dim=1).contiguous()
+
+
+@pytest.mark.parametrize("W,H,rr", [(512, 512, None), (400, 48, None), (16, 16, None), (1024, 1040, None),
+                                    (640, 640, (5, 17)), (640, 640, (0, 3)), (640, 640, (37, 40)),
+                                    (2064, 272, None)])
+def test_lattice_pass_equals_two_sweeps(mns, W, H, rr):
+    """mns_decode_pass_lattice on a code without 2x2 units (e3 = inf): from the flat start and from
+    a random raster's lattice, its t+2 lattice equals the lattice of two single raster sweeps and
+    its uint8 output their rounding, bit for bit; mns_decode_flat_lattice equals one flat sweep."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+    from paper_1501_02894_b200.synth import synth_image
+
+    L = N.lib()
+    side = max(W, H)
+    px = np.ascontiguousarray(synth_image(side, 13, noise_sigma=12.0, n_blobs=8)[:H, :W])
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+    assert code.min_leaf == 4
+    umap = code.unit_map
+    rh = H // 16
+    r0, r1 = rr if rr is not None else (0, rh)
+    u0 = max(0, r0 - 1)
+    sub = umap[u0 * (W // 16) * 32:]
+    g = torch.Generator(device="cuda").manual_seed(W + H + 1)
+    t0 = torch.rand((H, W), device="cuda", generator=g) * 255.0
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ly0, ly1 = 8 * r0, 8 * r1
+    for cur in (None, t0):
+        want = _sweeps_single(N, L, umap, W, H, (0, rh), cur, 128.0, 2)
+        lat_cur = _lattice_of(cur) if cur is not None else None
+        got = torch.full((H // 2, W // 2), float("nan"), device="cuda")
+        N.check(L.mns_decode_pass_lattice(N.ptr(sub), u0, W, H, r0, r1,
+                                          N.ptr(lat_cur) if lat_cur is not None else ctypes.c_void_p(0), 128.0,
+                                          N.ptr(got), ctypes.c_void_p(0), N.ptr(err), None))
+        out = torch.zeros((H, W), dtype=torch.uint8, device="cuda")
+        N.check(L.mns_decode_pass_lattice(N.ptr(sub), u0, W, H, r0, r1,
+                                          N.ptr(lat_cur) if lat_cur is not None else ctypes.c_void_p(0), 128.0,
+                                          ctypes.c_void_p(0), N.ptr(out), N.ptr(err), None))
+        torch.cuda.synchronize()
+        assert torch.equal(got[ly0:ly1], _lattice_of(want)[ly0:ly1])
+        assert torch.equal(out[16 * r0:16 * r1], torch.floor(want[16 * r0:16 * r1] + 0.5).to(torch.uint8))
+    one = _sweeps_single(N, L, umap, W, H, (0, rh), None, 128.0, 1)
+    flat = torch.full((H // 2, W // 2), float("nan"), device="cuda")
+    N.check(L.mns_decode_flat_lattice(N.ptr(sub), u0, W, H, r0, r1, 128.0, N.ptr(flat), None))
+    torch.cuda.synchronize()
+    assert torch.equal(flat[ly0:ly1], _lattice_of(one)[ly0:ly1])
+    assert int(err.item()) == 0
+
+
+@pytest.mark.parametrize("side,iters", [(512, 10), (512, 9), (256, 1), (256, 2), (48, 3), (1024, 8)])
+def test_lattice_decode_equals_raster_decode(mns, side, iters):
+    """Whole-image decode of an e3 = inf code: the lattice-state path (mns_decode_quadtree_lattice,
+    chosen by decode_device) and the raster path (mns_decode_quadtree) give the identical image."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+    from paper_1501_02894_b200.synth import synth_image
+
+    L = N.lib()
+    px = synth_image(side, 21, noise_sigma=9.0, n_blobs=10)
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+    got, it, _ = mns.decode_device(code, iters=iters)
+    W = H = side
+    ras = [torch.empty((H, W), device="cuda") for _ in range(2)]
+    want = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, iters, 0.0, 128.0,
+                                  N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert int(it.item()) == iters
+
+
+def test_lattice_decode_flags_2x2_units(mns):
+    """A code with 2x2 leaves forced down the lattice path raises the error flag (the caller must
+    use the raster path); decode_device picks the raster path for it by itself."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+    from paper_1501_02894_b200.synth import synth_image
+
+    L = N.lib()
+    px = synth_image(256, 5, noise_sigma=20.0, n_blobs=8)
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e1=2.0, e2=2.0, e3=2.0))
+    assert mns.codec.min_leaf_side(code) == 2
+    lat = [torch.empty((128, 128), device="cuda") for _ in range(2)]
+    out = torch.empty((256, 256), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    wsb = N.out_i64(L, L.mns_decode_workspace_bytes, 256, 256)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_quadtree_lattice(N.ptr(code.records), N.ptr(code.root_offsets), 256, 256, 4, 128.0,
+                                          N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out), N.ptr(err), N.ptr(ws), wsb, None))
+    assert int(err.item()) == 1
+    ras = [torch.empty((256, 256), device="cuda") for _ in range(2)]
+    got, _, _ = mns.decode_device(code, iters=4)
+    want = torch.empty((256, 256), dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), 256, 256, 4, 0.0, 128.0,
+                                  N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("iters", [10, 7])
+def test_strip_decoder_lattice_matches_whole_decode(mns, iters):
+    """StripDecoder in lattice mode (e3 = inf code), strip by strip with the 16 lattice halo rows
+    copied between strips by hand after every launch, equals the whole-image raster decode."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+    from paper_1501_02894_b200 import sharding
+    from paper_1501_02894_b200.synth import synth_image
+
+    L = N.lib()
+    H = W = 512
+    px = synth_image(H, 19, noise_sigma=10.0, n_blobs=12)
+    cfg = mns.EncoderConfig(e3=math.inf)
+    whole = mns.encode_device(torch.from_numpy(px).cuda(), cfg)
+    ras = [torch.empty((H, W), device="cuda") for _ in range(2)]
+    want = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_quadtree(N.ptr(whole.records), N.ptr(whole.root_offsets), W, H, iters, 0.0, 128.0,
+                                  N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
+    bounds = [0, 5, 19, 32]
+    decs = []
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        y0, y1 = max(0, 16 * r0 - 16), min(H, 16 * r1 + 16)
+        c = mns.encode_device(torch.from_numpy(np.ascontiguousarray(px[y0:y1])).cuda(), cfg, root_rows=(r0, r1),
+                              height=H)
+        d = sharding.StripDecoder(c, H, W, r0, r1)
+        assert d.lattice and d.ping.shape == ((d.y_hi - d.y_lo) // 2, W // 2)
+        decs.append(d)
+    for a, b in zip(decs[:-1], decs[1:]):
+        a.umap[-1].copy_(b.umap[b.r0 - b.u0])
+        b.umap[0].copy_(a.umap[a.r1 - 1 - a.u0])
+    n_launch = iters // 2 + (iters & 1)
+    curs = [None] * 3
+    for n in range(n_launch):
+        nxts = []
+        last = n == n_launch - 1
+        for i, d in enumerate(decs):
+            nxt = None if last else (d.ping if curs[i] is not d.ping else d.pong)
+            ob = d._vbase(d.out, 16 * d.r0, 1)
+            if n == 0 and iters & 1:
+                N.check(L.mns_decode_flat_lattice(N.ptr(d.umap), d.u0, W, H, d.r0, d.r1, 128.0, d._state_base(nxt),
+                                                  None))
+            else:
+                N.check(L.mns_decode_pass_lattice(N.ptr(d.umap), d.u0, W, H, d.r0, d.r1, d._state_base(curs[i]),
+                                                  128.0, d._state_base(nxt), ob if last else ctypes.c_void_p(0),
+                                                  N.ptr(d.error), None))
+            nxts.append(nxt)
+        if not last:
+            h = sharding.DEC_HALO // 2
+            for a, b, ra, rb in zip(decs[:-1], decs[1:], nxts[:-1], nxts[1:]):
+                a_own1 = (16 * a.r1 - a.y_lo) // 2
+                b_own0 = (16 * b.r0 - b.y_lo) // 2
+                ra[a_own1: a_own1 + h].copy_(rb[b_own0: b_own0 + h])
+                rb[b_own0 - h: b_own0].copy_(ra[a_own1 - h: a_own1])
+        curs = nxts
+    got = torch.cat([d.out for d in decs])
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert all(int(d.error.item()) == 0 for d in decs)
+    # and the run() driver itself (world = 1) on one whole-image strip
+    d = sharding.StripDecoder(mns.encode_device(torch.from_numpy(px).cuda(), cfg), H, W, 0, H // 16)
+    assert torch.equal(d.run(iters), want)
+
+
+def test_unit2_leaf_count_matches_host(mns, golden):
+    """The GPU tally of leaves painted as 2x2 units (level 4 and level-3 phase 2) that routes a code
+    to the raster or lattice decoder, against the host count on every golden code."""
+    from paper_1501_02894_b200 import rd
+    from paper_1501_02894_b200.types import unpack_fields
+
+    g = golden("encode")
+    seen = set()
+    for case in g.manifest:
+        rec = g[f"{case['key']}/records"]
+        f = unpack_fields(rec)
+        want = int(((f["level"] == 4) | ((f["level"] == 3) & (f["phase2"] == 1))).sum())
+        dev = torch.from_numpy(rec.view(np.int64)).cuda()
+        assert rd.unit2_leaves(dev, len(rec)) == want, case["key"]
+        seen.add(want > 0)
+    assert seen == {True, False}

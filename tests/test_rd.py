@@ -96,3 +96,21 @@ def test_offset_histogram_device_matches_reference_csv(cuda, golden):
         assert rd.histogram_csv(h) == str(G[f"{k}/csv"]), k
         B, (ih, iw) = case["B"], G[f"{k}/img"].shape
         assert h.total == (-(-ih // B)) * (-(-iw // B))  # one sample per range of the B-padded image
+
+
+@pytest.mark.gpu
+def test_mse_psnr_match_float64_mean(cuda):
+    """metrics.py:16-31: the GPU's exact SSE / n equals numpy's float64 mean of the squares."""
+    import paper_1501_02894_b200 as mns
+
+    rng = np.random.default_rng(3)
+    for h, w in [(1, 1), (7, 13), (64, 64), (333, 517), (1024, 2048)]:
+        a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-9, 10, (h, w)), 0, 255).astype(np.uint8)
+        d = a.astype(np.float64) - b.astype(np.float64)
+        want = float(np.mean(d * d))
+        assert mns.mse(mns.GrayImage(a), mns.GrayImage(b)) == want
+        assert mns.psnr(a, b) == (math.inf if want == 0 else 10.0 * math.log10(255.0 * 255.0 / want))
+    assert mns.psnr(a, a) == math.inf
+    with pytest.raises(ValueError, match="image dimensions differ"):
+        mns.mse(np.zeros((4, 4), np.uint8), np.zeros((4, 5), np.uint8))

@@ -71,6 +71,24 @@ def test_exchange_halos_gloo(world, halo):
     _run(world, _halo_worker, 128, 48, halo)
 
 
+def _lattice_halo_worker(rank, world, H, W):
+    # lattice-state decoding: one lattice row per two raster rows, DEC_HALO / 2 rows exchanged
+    r0, r1 = sharding.strip_rows(H, world, rank)
+    y_lo, y_hi = sharding.resident_rows(r0, r1, H, sharding.DEC_HALO)
+    rows = torch.arange(y_lo // 2, y_hi // 2, dtype=torch.float32)[:, None].repeat(1, W // 2)
+    lat = rows.clone()
+    own0, own1 = (16 * r0 - y_lo) // 2, (16 * r1 - y_lo) // 2
+    lat[:own0] = -1.0
+    lat[own1:] = -1.0
+    sharding.exchange_halos(lat, r0, r1, H, rank, world, halo=sharding.DEC_HALO, row_div=2)
+    assert torch.equal(lat, rows), f"rank {rank}: lattice halo rows not exchanged"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_lattice_halos_gloo(world):
+    _run(world, _lattice_halo_worker, 160, 48)
+
+
 def _umap_worker(rank, world, H, rw32):
     r0, r1 = sharding.strip_rows(H, world, rank)
     u0, u1 = sharding.unit_map_rows(r0, r1, H)
@@ -158,6 +176,52 @@ def test_pair_pass_strip_decode_matches_whole_image(world, tmp_path):
     records, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
     iters = 6
     _run(world, _pair_decode_worker, px, records, iters, str(tmp_path))
+    _, whole, _ = O.decode_records(records, 128, 128, max_iters=iters, stop_delta=0.0)
+    strips = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
+    assert np.array_equal(strips, whole)
+
+
+def _lattice_decode_worker(rank, world, px, records, iters, out_dir):
+    """Lattice-state strip decode (StripDecoder with min_leaf 4): the carried state is the 2x2-sum
+    lattice of the resident rows; each pass expands it to a raster whose lattice it is (in fp64,
+    l/4 in each of the four pixels sums back to l exactly), runs the two oracle sweeps, keeps the
+    lattice of the own rows and exchanges 16 lattice halo rows.  NaN poison outside the halo."""
+    from oracle import oracle as O
+
+    H, W = px.shape
+    r0, r1 = sharding.strip_rows(H, world, rank)
+    y_lo, y_hi = sharding.resident_rows(r0, r1, H, sharding.DEC_HALO)
+    u0, u1 = sharding.unit_map_rows(r0, r1, H)
+    units = O.records_to_units(records, W, H)
+    wide = units[(units["y"] >= 16 * u0) & (units["y"] < 16 * u1)]
+    mine = units[(units["y"] >= 16 * r0) & (units["y"] < 16 * r1)]
+    lat = torch.full(((y_hi - y_lo) // 2, W // 2), 4 * 128.0, dtype=torch.float64)
+    own = None
+    for p in range(iters // 2):
+        full = np.full((H, W), np.nan)
+        full[y_lo:y_hi] = np.repeat(np.repeat(lat.numpy() / 4, 2, axis=0), 2, axis=1)
+        mid = O.decode_step_units(wide, full, nthreads=1)
+        keep = np.full((H, W), np.nan)
+        keep[16 * u0: 16 * u1] = mid[16 * u0: 16 * u1]
+        nxt = O.decode_step_units(mine, keep, nthreads=1)
+        own = nxt[16 * r0: 16 * r1]
+        q = ((own[0::2, 0::2] + own[0::2, 1::2]) + own[1::2, 0::2]) + own[1::2, 1::2]
+        lat[(16 * r0 - y_lo) // 2: (16 * r1 - y_lo) // 2] = torch.from_numpy(q)
+        if p + 1 < iters // 2:
+            sharding.exchange_halos(lat, r0, r1, H, rank, world, halo=sharding.DEC_HALO, row_div=2)
+    assert np.isfinite(own).all()
+    np.save(os.path.join(out_dir, f"strip{rank}.npy"), own)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_lattice_strip_decode_matches_whole_image(world, tmp_path):
+    from oracle import oracle as O
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(128, 29, noise_sigma=10.0, n_blobs=6)
+    records, _ = O.encode_quadtree_records(px, (8.0, 8.0, float("inf")), 16.0, True)
+    iters = 6
+    _run(world, _lattice_decode_worker, px, records, iters, str(tmp_path))
     _, whole, _ = O.decode_records(records, 128, 128, max_iters=iters, stop_delta=0.0)
     strips = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
     assert np.array_equal(strips, whole)
