@@ -149,6 +149,19 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return d;
 }
 
+// three-input min / max (sm_100 FMNMX3)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
@@ -268,8 +281,20 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             v[2 * m] = r.x;
             v[2 * m + 1] = r.y;
         }
+        // clip only lanes whose block leaves [0, 255] (FMNMX3 range of the 16 values, then the
+        // per-value clip on the rare lanes that need it)
+        float lo = fmin3(v[0], v[1], v[2]), hi = fmax3(v[0], v[1], v[2]);
 #pragma unroll
-        for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
+        for (int e = 3; e < 15; e += 2) {
+            lo = fmin3(lo, v[e], v[e + 1]);
+            hi = fmax3(hi, v[e], v[e + 1]);
+        }
+        lo = fminf(lo, v[15]);
+        hi = fmaxf(hi, v[15]);
+        if (lo < 0.f || hi > 255.f) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
+        }
     }
 }
 
@@ -611,7 +636,7 @@ constexpr int LQRP = LQR + 8;      // + a second copy of slot 0, so a 4-row read
 constexpr int LBOX = 8 * LQS * 4;  // bytes of one slot
 constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * QS * 4;
 #ifndef LAT_MINB
-#define LAT_MINB 3
+#define LAT_MINB 4
 #endif
 
 __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -697,7 +722,6 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
             paint_block<LQS, LHB, LQR, false>(word, live, L, st, &qa[0][0], no_raw, flat, p.init, rxg, ryg, xa0,
                                               interior, p.W, p.H, v);
             if (live) {
-                if (!flat && (word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
                 const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
                 const int g = (ryg + L.ly) >> 1;
 #pragma unroll
@@ -711,7 +735,7 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
             paint_block<QS, QH, QR, false>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg, xb0,
                                            interior, p.W, p.H, v);
             if (live) {
-                if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);
+                if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
                 if (p.nxt) {  // the lattice of t+2, de-interleaved rows
                     const int gy = (ryg + L.ly) >> 1, gc = (rxg + L.lx) >> 2;
                     float *d = p.nxt + (ptrdiff_t)gy * lw + gc;
