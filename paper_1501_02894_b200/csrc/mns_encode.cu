@@ -45,7 +45,8 @@ constexpr int TR = EW * RPW;         // 16 consecutive roots of one root row per
 static_assert(RPW == 2, "the warp-local decision rounds map two roots onto one warp");
 constexpr int WIN_W = TR * 16 + 32;  // 544
 constexpr int WIN_H = 48;
-constexpr int QE_W = WIN_W / 2;      // 272
+constexpr int QE_WL = WIN_W / 2;     // 272 q columns
+constexpr int QE_W = QE_WL + 4;      // row stride 276: K1c's lanes read rows 2 apart, 4 banks apart
 constexpr int QE_H = WIN_H / 2;      // 24
 
 struct EncParams {
@@ -306,8 +307,8 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
         pix[r][c] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? img[(size_t)gy * pitch + gx] : 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < NODE_WIN_H / 2 * QE_W; i += blockDim.x) {
-        const int qi = i / QE_W, qj = i % QE_W;
+    for (int i = threadIdx.x; i < NODE_WIN_H / 2 * QE_WL; i += blockDim.x) {
+        const int qi = i / QE_WL, qj = i % QE_WL;
         qe[qi][qj] = (uint16_t)(pix[2 * qi][2 * qj] + pix[2 * qi][2 * qj + 1] + pix[2 * qi + 1][2 * qj] +
                                 pix[2 * qi + 1][2 * qj + 1]);
     }
@@ -398,8 +399,8 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
     __syncthreads();
     mbar_wait(&wbar, 0);
     // ---- K1b: even-phase 2x2 sums, 4 per thread-step via packed u16x2 adds
-    for (int c = tid; c < QE_H * (QE_W / 4); c += ET) {
-        const int qi = c / (QE_W / 4), qj = (c % (QE_W / 4)) * 4;
+    for (int c = tid; c < QE_H * (QE_WL / 4); c += ET) {
+        const int qi = c / (QE_WL / 4), qj = (c % (QE_WL / 4)) * 4;
         const uint2 a = *reinterpret_cast<const uint2 *>(&pix[2 * qi][2 * qj]);
         const uint2 b = *reinterpret_cast<const uint2 *>(&pix[2 * qi + 1][2 * qj]);
         uint2 s;
@@ -598,7 +599,14 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
 // root_offsets (in place) with a decoupled look-back over uniform 2048-root tiles, then a
 // coalesced copy of every root's staged records to its offset.  Keeping the scan out of the
 // encoder means no encoder CTA ever waits on another.
-constexpr int CT_THREADS = 256, CT_PER = 8, CT_ROOTS = CT_THREADS * CT_PER;
+#ifndef CT_PER_DEF
+#define CT_PER_DEF 8
+#endif
+#ifndef CT_U_DEF
+#define CT_U_DEF 4
+#endif
+constexpr int CT_THREADS = 256, CT_PER = CT_PER_DEF, CT_ROOTS = CT_THREADS * CT_PER;
+constexpr int CT_U = CT_U_DEF;  // staged-record loads in flight per lane
 
 __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint64_t *stage, int32_t *root_offsets,
                                                                      long long n_roots, uint64_t *out,
@@ -660,11 +668,11 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
         const int my_off = lane < nk ? offs[c0 + lane] : INT_MAX;
         const int j_lo = __shfl_sync(FULL, my_off, 0);
         const int j_hi = c0 + nk < nr_tile ? offs[c0 + nk] : total;
-        for (int j0 = j_lo; j0 < j_hi; j0 += 4 * 32) {
-            uint64_t v[4];
-            int jj[4];
+        for (int j0 = j_lo; j0 < j_hi; j0 += CT_U * 32) {
+            uint64_t v[CT_U];
+            int jj[CT_U];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < CT_U; u++) {
                 jj[u] = j0 + 32 * u + lane;
                 int k = 0;  // largest chunk root with offset <= j (roots with no records never win ties)
 #pragma unroll
@@ -676,7 +684,7 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
                 if (jj[u] < j_hi) v[u] = __ldg(stage + (r0 + c0 + k) * 64 + (jj[u] - ok));
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < CT_U; u++)
                 if (jj[u] < j_hi) dst[jj[u]] = v[u];
         }
     }
