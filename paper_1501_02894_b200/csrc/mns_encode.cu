@@ -71,43 +71,52 @@ struct Mom {
 __device__ __forceinline__ double pow2neg(int k) { return __longlong_as_double((long long)(1023 - k) << 52); }
 
 // Quantised contrast code = 4 + clamp(floor(16N/D), -4, 3) (4 when D == 0): the
-// reference's quantize_contrast(fl(4N/D)) (transform.py:46-53), exactly.  A fast
-// fp32 quotient is corrected by one exact int64 comparison (its error is < 1 unit).
-__device__ __forceinline__ int quant_code(long long N, long long D) {
-    if (D == 0) return 4;  // fit_affine degenerate domain: s = 0 -> bin 4
-    const long long t = 16 * N;
+// reference's quantize_contrast(fl(4N/D)) (transform.py:46-53), exactly.  t = 16N and D are
+// exact doubles (|16N|, 4|D| < 2^53); a fast fp32 quotient is corrected by one exact fp64
+// comparison (its error is < 1 unit).
+__device__ __forceinline__ int quant_code(double t, double D) {
+    if (D == 0.0) return 4;  // fit_affine degenerate domain: s = 0 -> bin 4
     int k = (int)floorf(fminf(3.f, fmaxf(-4.f, __fdividef((float)t, (float)D))));
-    if (k > -4 && t < (long long)k * D) --k;
-    else if (k < 3 && t >= (long long)(k + 1) * D) ++k;
+    if (k > -4 && t < (double)k * D) --k;
+    else if (k < 3 && t >= (double)(k + 1) * D) ++k;
     return 4 + k;
 }
 
-// Phase 1 from exact integer moments (encoder.py:145-166 + transform.py:23-80).
+// N = n Sqr - Sq Sr and D = n Sqq - Sq^2 (one wide multiply-add each), as exact doubles
+__device__ __forceinline__ double mom_N(int nlog2, const Mom &m) {
+    return (double)(((long long)m.sqr << nlog2) - (long long)m.sq * m.sr);
+}
+__device__ __forceinline__ double mom_D(int nlog2, const Mom &m) {
+    return (double)(((long long)m.sqq << nlog2) - (long long)m.sq * m.sq);
+}
+
+// Phase 1 from exact integer moments (encoder.py:145-166 + transform.py:23-80).  Every term of
+// 1024 n SSE = 1024 n A - 64 k2 N + k2^2 D is an integer below 2^53, so two fp64 FMAs give it
+// exactly; an infinite bound (E = inf) accepts without it.
 __device__ __forceinline__ uint64_t phase1(int x, int y, int level, int nlog2, const Mom &m, double bnd,
                                            bool &acc) {
-    const long long n = 1ll << nlog2;
-    const int o = (2 * m.sr + (int)n) >> (nlog2 + 1);  // round_to_int(mean)
-    const long long N = n * m.sqr - (long long)m.sq * m.sr;
-    const long long D = n * m.sqq - (long long)m.sq * m.sq;
-    const int code = quant_code(N, D);
-    const long long k2 = 2 * code - 7;
-    const long long A = (long long)m.srr - 2ll * o * m.sr + n * o * o;
-    const long long X = 1024ll * n * A - 64ll * k2 * N + k2 * k2 * D;
-    acc = (double)X <= bnd;
+    const int o = (2 * m.sr + (1 << nlog2)) >> (nlog2 + 1);  // round_to_int(mean)
+    const double N = mom_N(nlog2, m), D = mom_D(nlog2, m);
+    const int code = quant_code(16.0 * N, D);
+    if (bnd == INFINITY) {
+        acc = true;
+    } else {
+        const int k2 = 2 * code - 7;
+        const int A = m.srr - 2 * o * m.sr + ((o * o) << nlog2);  // sum (r - o)^2 < 2^25
+        acc = fma((double)(k2 * k2), D, fma((double)(-64 * k2), N, (double)A * (double)(1024 << nlog2))) <= bnd;
+    }
     return mns_rec_phase1(x, y, level, o, code);
 }
 
 // Phase-2 quadrant decision from moments: 0 reject, 1 accept, 2 ambiguous (emulate).
 __device__ __forceinline__ int p2_quad(int nlog2, const Mom &m, int t, double slo, double shi, double bnd_n,
                                        int &bit) {
-    const long long n = 1ll << nlog2;
-    const long long A = (long long)m.srr - 2ll * t * m.sr + n * t * t;
-    const long long N = n * m.sqr - (long long)m.sq * m.sr;
-    const long long D = n * m.sqq - (long long)m.sq * m.sq;
+    const int A = m.srr - 2 * t * m.sr + ((t * t) << nlog2);  // sum (r - t)^2 < 2^25
+    const double N = mom_N(nlog2, m), D = mom_D(nlog2, m);
     bit = 0;
-    if (D == 0) return (double)A <= bnd_n ? 1 : 0;  // d - mean(d) == 0: both candidates identical
-    const double X = (double)N * pow2neg(nlog2 + 2);  // sum (r - t)(d - dbar), exact
-    const double Y = (double)D * pow2neg(nlog2 + 4);  // sum (d - dbar)^2, exact
+    if (D == 0.0) return (double)A <= bnd_n ? 1 : 0;  // d - mean(d) == 0: both candidates identical
+    const double X = N * pow2neg(nlog2 + 2);  // sum (r - t)(d - dbar), exact
+    const double Y = D * pow2neg(nlog2 + 4);  // sum (d - dbar)^2, exact
     const double Ad = (double)A;
     const double lo = Ad - 2.0 * slo * X + slo * slo * Y;
     const double hi = Ad - 2.0 * shi * X + shi * shi * Y;
@@ -335,7 +344,7 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
         const uint64_t rec = phase1(x, y, level, nlog2, m, p.p1b[level], acc);
         const long long n = 1ll << nlog2;
         const int o = (2 * m.sr + (int)n) >> (nlog2 + 1);
-        const int code = quant_code(n * m.sqr - (long long)m.sq * m.sr, n * m.sqq - (long long)m.sq * m.sq);
+        const int code = (int)((rec >> MNS_REC_PAYLOAD_SHIFT) & 7);  // the record's contrast code
         const double sdq = -0.875 + 0.25 * code, dm = ((double)m.sq * 0.25) / (double)n;
         for (int i = 0; i < size; i++)  // rms_error replayed in numpy's fp64 order (exact in practice)
             for (int j = 0; j < size; j++)
