@@ -281,19 +281,23 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             v[2 * m] = r.x;
             v[2 * m + 1] = r.y;
         }
-        // clip only lanes whose block leaves [0, 255] (FMNMX3 range of the 16 values, then the
-        // per-value clip on the rare lanes that need it)
-        float lo = fmin3(v[0], v[1], v[2]), hi = fmax3(v[0], v[1], v[2]);
+        // The clip binds only if the unit's map leaves [0, 255] over q in [0, 1020] (the input
+        // raster is in [0, 255]; fl(a q + b) is monotone in q): test the two ends, then the
+        // block's actual FMNMX3 range, and clip only the lanes that need it.
+        const float e0 = b, e1 = fmaf(a, 1020.f, b);
+        if (fminf(e0, e1) < 0.f || fmaxf(e0, e1) > 255.f) {
+            float lo = fmin3(v[0], v[1], v[2]), hi = fmax3(v[0], v[1], v[2]);
 #pragma unroll
-        for (int e = 3; e < 15; e += 2) {
-            lo = fmin3(lo, v[e], v[e + 1]);
-            hi = fmax3(hi, v[e], v[e + 1]);
-        }
-        lo = fminf(lo, v[15]);
-        hi = fmaxf(hi, v[15]);
-        if (lo < 0.f || hi > 255.f) {
+            for (int e = 3; e < 15; e += 2) {
+                lo = fmin3(lo, v[e], v[e + 1]);
+                hi = fmax3(hi, v[e], v[e + 1]);
+            }
+            lo = fminf(lo, v[15]);
+            hi = fmaxf(hi, v[15]);
+            if (lo < 0.f || hi > 255.f) {
 #pragma unroll
-            for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
+                for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
+            }
         }
     }
 }
