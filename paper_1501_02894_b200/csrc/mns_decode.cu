@@ -23,6 +23,8 @@
 
 #include <math.h>
 
+#include <type_traits>
+
 #include "mns_common.cuh"
 #include "mns_tma.cuh"
 
@@ -643,6 +645,7 @@ constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * QS * 4;
 #define LAT_MINB 4
 #endif
 
+template <bool FLAT, bool OUT>
 __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                         const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -655,7 +658,6 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
     const int x0 = blockIdx.x * BR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
     const int r_s = p.rr0 + blockIdx.y * p.cr, r_e = min(r_s + p.cr, p.rr1);
     const int rh = p.H / 16, lw = p.W / 2;
-    const bool flat = p.cur == nullptr;
     const int nblocks = (r_e - r_s) + 4;  // block k = the 8 lattice rows of root row r_s - 2 + k
     if (tid < 16) st[tid] = kUnitS[tid];
     if (tid == 0) {
@@ -682,7 +684,7 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
     };
     const Lane L = lane_of(lane);
     const bool stage_a = warp < NWA;
-    if (!flat) {
+    if (!FLAT) {
         if (tid == 0) {
             prefetch_tmap(&tmap);
             for (int k = 0; k < LNS; k++) issue(k);
@@ -692,69 +694,81 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
             wait_block(1);
         }
     }
-    // stage A: root columns -1 .. BR of the band; stage B: 0 .. BR-1
-    const int rc = stage_a ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - NWA) + (lane >> 4);
-    const int rxi = blockIdx.x * BR + rc;
-    const bool col_ok = rxi >= 0 && rxi < p.rw;
-    const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
-    const int lag = stage_a ? 0 : 2;  // iteration i: A paints root row i, B paints i - 2
-    const int row_lo = stage_a ? max(r_s - 1, 0) : r_s, row_hi = stage_a ? min(r_e + 1, rh) : r_e;
-    const uint2 *ubase = reinterpret_cast<const uint2 *>(p.unit_map) + ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 +
-                         (lane & 15);
-    const ptrdiff_t ustride = (ptrdiff_t)p.rw * 16;
-    auto word_of = [&](int row, const uint2 *ptr) {
-        return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
-    };
     auto no_raw = [](int, int) { return 0.f; };
-    const uint2 *uptr = ubase + (ptrdiff_t)(r_s - 1 - lag) * ustride;
-    uint2 word = word_of(r_s - 1 - lag, uptr);
-    for (int i = r_s - 1; i <= r_e + 1; i++) {
-        const int row = i - lag;
-        uptr += ustride;
-        const uint2 wnext = word_of(row + 1, uptr);
-        __syncthreads();
-        if (!flat && tid == 0 && i >= r_s) {
-            fence_proxy_async();  // generic reads of the slot just released complete before its refill
-            issue(i - r_s + LNS);
-        }
-        const int rxg = rxi * 16, ryg = row * 16;
-        const bool interior = interior_col && row >= 1 && row + 1 < rh;
-        float v[16];
-        if (stage_a) {
-            if (!flat) wait_block(i - r_s + 3);
-            const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
-            paint_block<LQS, LHB, LQR, false>(word, live, L, st, &qa[0][0], no_raw, flat, p.init, rxg, ryg, xa0,
-                                              interior, p.W, p.H, v);
-            if (live) {
-                const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
-                const int g = (ryg + L.ly) >> 1;
-#pragma unroll
-                for (int r = 0; r < 2; r++)
-                    lat_store<QS, QH>(&qb[0][0], g + r, wc >> 1,
-                                      make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
-                                                  ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]));
-            }
-        } else {
-            const bool live = col_ok && row >= r_s;
-            paint_block<QS, QH, QR, false>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg, xb0,
-                                           interior, p.W, p.H, v);
-            if (live) {
-                if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
-                if (p.nxt) {  // the lattice of t+2, de-interleaved rows
-                    const int gy = (ryg + L.ly) >> 1, gc = (rxg + L.lx) >> 2;
-                    float *d = p.nxt + (ptrdiff_t)gy * lw + gc;
-#pragma unroll
-                    for (int r = 0; r < 2; r++, d += lw) {
-                        d[0] = ((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5];
-                        d[lw / 2] = ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7];
+    // One loop per stage (warp-uniform roles; the same iteration count, one barrier per iteration).
+    // Iteration i: A paints root row i of t+1 (root columns -1 .. BR of the band), B paints root
+    // row i - 2 of t+2 (columns 0 .. BR-1).
+    auto run = [&](auto role) {
+        constexpr bool A = decltype(role)::value;
+        const int rc = A ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - NWA) + (lane >> 4);
+        const int rxi = blockIdx.x * BR + rc;
+        const bool col_ok = rxi >= 0 && rxi < p.rw;
+        const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
+        constexpr int lag = A ? 0 : 2;
+        const int row_lo = A ? max(r_s - 1, 0) : r_s, row_hi = A ? min(r_e + 1, rh) : r_e;
+        const uint2 *uptr = reinterpret_cast<const uint2 *>(p.unit_map) +
+                            ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 + (lane & 15) +
+                            (ptrdiff_t)(r_s - 1 - lag) * p.rw * 16;
+        const ptrdiff_t ustride = (ptrdiff_t)p.rw * 16;
+        auto word_of = [&](int row, const uint2 *ptr) {
+            return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
+        };
+        const int rxg = rxi * 16;
+        uint2 word = word_of(r_s - 1 - lag, uptr);
+        for (int i = r_s - 1; i <= r_e + 1; i++) {
+            const int row = i - lag;
+            uptr += ustride;
+            const uint2 wnext = word_of(row + 1, uptr);
+            __syncthreads();
+            const int ryg = row * 16;
+            const bool interior = interior_col && row >= 1 && row + 1 < rh;
+            float v[16];
+            if (A) {
+                if (!FLAT) {
+                    if (tid == 0 && i >= r_s) {
+                        fence_proxy_async();  // generic reads of the slot just released complete before its refill
+                        issue(i - r_s + LNS);
                     }
-                } else {
-                    store_block(v, nullptr, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
+                    wait_block(i - r_s + 3);
+                }
+                const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
+                paint_block<LQS, LHB, LQR, false>(word, live, L, st, &qa[0][0], no_raw, FLAT, p.init, rxg, ryg, xa0,
+                                                  interior, p.W, p.H, v);
+                if (live) {
+                    const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
+                    const int g = (ryg + L.ly) >> 1;
+#pragma unroll
+                    for (int r = 0; r < 2; r++)
+                        lat_store<QS, QH>(&qb[0][0], g + r, wc >> 1,
+                                          make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
+                                                      ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]));
+                }
+            } else {
+                const bool live = col_ok && row >= r_s;
+                paint_block<QS, QH, QR, false>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg, xb0,
+                                               interior, p.W, p.H, v);
+                if (live) {
+                    if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
+                    if (!OUT) {  // the lattice of t+2, de-interleaved rows
+                        const int gy = (ryg + L.ly) >> 1, gc = (rxg + L.lx) >> 2;
+                        float *d = p.nxt + (ptrdiff_t)gy * lw + gc;
+#pragma unroll
+                        for (int r = 0; r < 2; r++, d += lw) {
+                            d[0] = ((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5];
+                            d[lw / 2] = ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7];
+                        }
+                    } else {
+                        store_block(v, nullptr, p.out_u8, p.W, rxg + L.lx, ryg + L.ly);
+                    }
                 }
             }
+            word = wnext;
         }
-        word = wnext;
-    }
+    };
+    if (stage_a)
+        run(std::true_type{});
+    else
+        run(std::false_type{});
 }
 
 // The first sweep from the flat raster straight into lattice form (an odd sweep count): every
@@ -1038,8 +1052,11 @@ int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, 
 }
 
 static int ensure_lat_attr() {
-    static std::atomic<unsigned long long> done{0};
-    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel, LAT_SMEM, done));
+    static std::atomic<unsigned long long> d0{0}, d1{0}, d2{0}, d3{0};
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel<false, false>, LAT_SMEM, d0));
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel<false, true>, LAT_SMEM, d1));
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel<true, false>, LAT_SMEM, d2));
+    MNS_CUDA_TRY(ensure_dynamic_smem(decode_pair_lat_kernel<true, true>, LAT_SMEM, d3));
     return 0;
 }
 
@@ -1081,7 +1098,12 @@ int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int
     p.cr = rows_per_cta(rr1 - rr0, (p.rw + BR - 1) / BR, CR2);
     dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + p.cr - 1) / p.cr);
     p.n_ctas = grid.x * grid.y;
-    decode_pair_lat_kernel<<<grid, DT2, LAT_SMEM, stream>>>(tmap, p);
+    if (cur)
+        (out ? decode_pair_lat_kernel<false, true> : decode_pair_lat_kernel<false, false>)<<<grid, DT2, LAT_SMEM,
+                                                                                               stream>>>(tmap, p);
+    else
+        (out ? decode_pair_lat_kernel<true, true> : decode_pair_lat_kernel<true, false>)<<<grid, DT2, LAT_SMEM,
+                                                                                             stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
