@@ -179,10 +179,31 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // absolute raster row / 2 mod QR, column = window column / 2, window origin wx0) or, for 2x2
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
-template <int QSTR, int HALF, int RING = QR, bool RAW = true, class RawSum>
+// Lattice addressing of an interior lane, per unit size k = 1..3, fixed for a kernel: the column
+// offsets of its two de-interleaved base pointers (7 bits each) and the lattice-row offset of its
+// domain from 8 * (root row) + 8 (5 bits) -- so a paint needs no per-block coordinate arithmetic.
+struct LaneTab {
+    uint32_t t[3];
+};
+
+template <int QSTR, int HALF>
+__device__ __forceinline__ LaneTab lane_tab(const Lane &L, int rc, int col_base) {
+    LaneTab T;
+#pragma unroll
+    for (int k = 1; k <= 3; k++) {
+        const int dx = (int)((L.tx >> (6 * k)) & 63) / 2 - 8, dy = (int)((L.ty >> (6 * k)) & 63) / 2 - 8;
+        const int qc = 8 * rc + col_base + dx;  // window lattice column of the domain's first column
+        const uint32_t c0 = (qc & 1) * HALF + (qc >> 1), c1 = ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);
+        T.t[k - 1] = c0 | (c1 << 7) | ((uint32_t)(dy + 8) << 14);
+    }
+    return T;
+}
+
+template <int QSTR, int HALF, int RING = QR, bool RAW = true, bool FAST = false, class RawSum>
 __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L, const float *st, const float *lat,
                                             const RawSum &raw_sum, bool flat, float init, int rxg, int ryg, int wx0,
-                                            bool interior, int W, int H, float (&v)[16]) {
+                                            bool interior, int W, int H, float (&v)[16],
+                                            const LaneTab *tab = nullptr) {
     if (flat) {
         // Flat start raster (kernel-uniform): every domain mean is init exactly (sums of equal
         // power-of-two multiples of init are exact), so each unit paints the constant
@@ -210,18 +231,26 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
         sa = st[d0 & 15];
         sb = unit_o(d0);
         {
-            int X, Y;
-            if (interior) {
-                X = (int)((L.tx >> (6 * k)) & 63);
-                Y = (int)((L.ty >> (6 * k)) & 63);
+            const float *p0, *p1;  // columns qc, qc + 2 and qc + 1, qc + 3 of the domain's first lattice row
+            if (FAST && interior) {
+                const uint32_t t = k == 1 ? tab->t[0] : (k == 2 ? tab->t[1] : tab->t[2]);
+                const float *row = lat + ((ryg >> 1) + (int)(t >> 14) - 8 & (RING - 1)) * QSTR;
+                p0 = row + (t & 127);
+                p1 = row + ((t >> 7) & 127);
             } else {
-                X = clamped_offset(L.lx, 2 << k, rxg, W);
-                Y = clamped_offset(L.ly, 2 << k, ryg, H);
+                int X, Y;
+                if (interior) {
+                    X = (int)((L.tx >> (6 * k)) & 63);
+                    Y = (int)((L.ty >> (6 * k)) & 63);
+                } else {
+                    X = clamped_offset(L.lx, 2 << k, rxg, W);
+                    Y = clamped_offset(L.ly, 2 << k, ryg, H);
+                }
+                const int qr = (ryg - 16 + Y) >> 1, qc = (rxg - 16 + X - wx0) >> 1;
+                const float *row = lat + (qr & (RING - 1)) * QSTR;  // rows +0..+3 stay inside the padded ring
+                p0 = row + (qc & 1) * HALF + (qc >> 1);
+                p1 = row + ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);
             }
-            const int qr = (ryg - 16 + Y) >> 1, qc = (rxg - 16 + X - wx0) >> 1;
-            const float *row = lat + (qr & (RING - 1)) * QSTR;  // rows +0..+3 stay inside the padded ring
-            const float *p0 = row + (qc & 1) * HALF + (qc >> 1);              // columns qc, qc + 2
-            const float *p1 = row + ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);  // columns qc + 1, qc + 3
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 v[4 * i + 0] = p0[i * QSTR];
@@ -714,6 +743,7 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
             return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
         };
         const int rxg = rxi * 16;
+        const LaneTab tab = A ? lane_tab<LQS, LHB>(L, rc, 16) : lane_tab<QS, QH>(L, rc, 8);
         uint2 word = word_of(r_s - 1 - lag, uptr);
         for (int i = r_s - 1; i <= r_e + 1; i++) {
             const int row = i - lag;
@@ -732,8 +762,8 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
                     wait_block(i - r_s + 3);
                 }
                 const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
-                paint_block<LQS, LHB, LQR, false>(word, live, L, st, &qa[0][0], no_raw, FLAT, p.init, rxg, ryg, xa0,
-                                                  interior, p.W, p.H, v);
+                paint_block<LQS, LHB, LQR, false, true>(word, live, L, st, &qa[0][0], no_raw, FLAT, p.init, rxg, ryg,
+                                                        xa0, interior, p.W, p.H, v, &tab);
                 if (live) {
                     const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
                     const int g = (ryg + L.ly) >> 1;
@@ -745,8 +775,8 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
                 }
             } else {
                 const bool live = col_ok && row >= r_s;
-                paint_block<QS, QH, QR, false>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg, xb0,
-                                               interior, p.W, p.H, v);
+                paint_block<QS, QH, QR, false, true>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg,
+                                                     xb0, interior, p.W, p.H, v, &tab);
                 if (live) {
                     if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
                     if (!OUT) {  // the lattice of t+2, de-interleaved rows
