@@ -57,6 +57,7 @@ struct EncParams {
     double p2b[4];  // bound(E_level): phase-2 quadrant accepts iff SSE <= n_k * p2b
     double tol[4];  // E_level (emulation path compares rms > tol like the reference)
     double mean_tol;
+    int gate[4];    // phase-2 mean gate per level: |n * (O_k - O_i)| > gate  <=>  |O_k - O_i| > mean_tol
     uint64_t *stage;     // 64 record slots per root (workspace); compacted by compact_records_kernel
     uint32_t *unit_map;  // optional: decoder unit map (mns_record.h), 32 words per root
     int32_t *root_cnt;   // per-root record counts (root_offsets, scanned in place by the compaction)
@@ -76,18 +77,23 @@ __device__ __forceinline__ double pow2neg(int k) { return __longlong_as_double((
 // comparison (its error is < 1 unit).
 __device__ __forceinline__ int quant_code(double t, double D) {
     if (D == 0.0) return 4;  // fit_affine degenerate domain: s = 0 -> bin 4
-    int k = (int)floorf(fminf(3.f, fmaxf(-4.f, __fdividef((float)t, (float)D))));
-    if (k > -4 && t < (double)k * D) --k;
-    else if (k < 3 && t >= (double)(k + 1) * D) ++k;
-    return 4 + k;
+    const float q = fminf(3.5f, fmaxf(-4.5f, __fdividef((float)t, (float)D)));
+    const float f = floorf(q);
+    int k = (int)f;
+    // the fp32 quotient is within 1e-5 of t/D: away from an integer it already is the floor
+    if (q - f < 1e-4f || q - f > 1.f - 1e-4f) {
+        if (t < (double)k * D) --k;
+        else if (t >= (double)(k + 1) * D) ++k;
+    }
+    return 4 + min(3, max(-4, k));
 }
 
 // N = n Sqr - Sq Sr and D = n Sqq - Sq^2 (one wide multiply-add each), as exact doubles
-__device__ __forceinline__ double mom_N(int nlog2, const Mom &m) {
-    return (double)(((long long)m.sqr << nlog2) - (long long)m.sq * m.sr);
+__device__ __forceinline__ double mom_N(int nlog2, const Mom &m) {  // Sq * Sr < 2^53: one exact FMA
+    return fma((double)m.sqr, (double)(1 << nlog2), -((double)m.sq * (double)m.sr));
 }
 __device__ __forceinline__ double mom_D(int nlog2, const Mom &m) {
-    return (double)(((long long)m.sqq << nlog2) - (long long)m.sq * m.sq);
+    return fma((double)m.sqq, (double)(1 << nlog2), -((double)m.sq * (double)m.sq));
 }
 
 // Phase 1 from exact integer moments (encoder.py:145-166 + transform.py:23-80).  Every term of
@@ -149,14 +155,13 @@ struct Node2 {  // phase-2 node-level quantities (gate, o_byte, deltas, targets)
     int o, d0, d1, d2, t[4];
 };
 
-__device__ __forceinline__ Node2 p2_node(int nlog2, int sr, int s0, int s1, int s2, int s3, int limit,
-                                         double mean_tol) {
+// The gate compares exact dyadic means (encoder.py:187): |O_k - O_i| > mean_tol  <=>
+// |n (O_k - O_i)| > mean_tol * n  <=>  |df| > floor(mean_tol * n) for the integer df (host: gate).
+__device__ __forceinline__ Node2 p2_node(int nlog2, int sr, int s0, int s1, int s2, int s3, int limit, int gate) {
     Node2 z;
     const int n = 1 << nlog2;
     const int df[4] = {4 * s0 - sr, 4 * s1 - sr, 4 * s2 - sr, 4 * s3 - sr};  // n * (O_k - O_i)
-    z.pass = true;
-    for (int k = 0; k < 4; k++)
-        if ((double)abs(df[k]) > mean_tol * (double)n) z.pass = false;  // encoder.py:187
+    z.pass = max(max(abs(df[0]), abs(df[1])), max(abs(df[2]), abs(df[3]))) <= gate;
     z.o = (2 * sr + n) >> (nlog2 + 1);
     z.d0 = (2 * df[0] + n) >> (nlog2 + 1);  // floor((O_k - O_i) + 0.5), arithmetic shift = floor
     z.d1 = (2 * df[1] + n) >> (nlog2 + 1);
@@ -239,7 +244,7 @@ __device__ bool phase2_node(const Win &w, const EncParams &p, int slot, int leve
                             const Mom *kids, uint64_t *rec) {
     const int nlog2 = 2 * (5 - level);  // node pixels: 256, 64, 16
     const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
-                            p.mean_tol);
+                            p.gate[level]);
     if (!z.pass) return false;
     const double slo = level == 1 ? 0.2 : (level == 2 ? 0.4 : 0.5);
     const double shi = level == 1 ? 0.5 : (level == 2 ? 0.65 : 0.9);
@@ -277,7 +282,7 @@ __device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p
         rec = phase1(w.x0 + 16 * slot + nx, w.y0 + ny, level, nlog2, m, p.p1b[level], acc);
         if (!acc && p.mns) {
             z = p2_node(nlog2, m.sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
-                        p.mean_tol);
+                        p.gate[level]);
             want2 = z.pass;
             if (want2) {
                 const double slo = level == 1 ? 0.2 : 0.4, shi = level == 1 ? 0.5 : 0.65;
@@ -359,7 +364,7 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
     for (int k = 0; k < 4; k++) kids[k] = moments(nx + (k & 1) * h, ny + (k >> 1) * h, h);
     const int sr = kids[0].sr + kids[1].sr + kids[2].sr + kids[3].sr;
     const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
-                            p.mean_tol);
+                            p.gate[level]);
     *out_rec = 0;
     *out_rms = INFINITY;
     if (!z.pass) return;
@@ -703,6 +708,15 @@ __global__ void __launch_bounds__(CT_THREADS) compact_records_kernel(const uint6
 
 static long long compact_tiles(long long n_roots) { return (n_roots + CT_ROOTS - 1) / CT_ROOTS; }
 
+// Integer form of the phase-2 mean gate at node size n: floor(mean_tol * n) (exact: n is a power of
+// two), saturated -- |df| <= 4 * 255 * 256 never exceeds INT_MAX; NaN never fails, like the float test.
+static int mean_gate(double mean_tol, int n) {
+    const double x = mean_tol * (double)n;
+    if (!(x == x) || x >= 2147483647.0) return INT_MAX;
+    if (x < -2147483647.0) return -1;
+    return (int)floor(x);
+}
+
 int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *bytes) {
     const long long n_roots = (long long)n_images * (rr1 - rr0) * (width / 16);
     // [compaction look-back status, 256-B aligned][64 staged record slots per root]
@@ -750,6 +764,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     }
     p.p1b[4] = INFINITY;
     p.mean_tol = cfg->mean_tol;
+    for (int l = 1; l <= 3; l++) p.gate[l] = mean_gate(cfg->mean_tol, 1 << (2 * (5 - l)));
     const long long ctiles = compact_tiles(n_roots);
     const size_t status_bytes = ((ctiles * 8 + 255) / 256) * 256;
     unsigned long long *status = reinterpret_cast<unsigned long long *>(workspace);
@@ -798,6 +813,7 @@ int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int 
     }
     p.p1b[4] = INFINITY;
     p.mean_tol = cfg->mean_tol;
+    for (int l = 1; l <= 3; l++) p.gate[l] = mean_gate(cfg->mean_tol, 1 << (2 * (5 - l)));
     try_node_kernel<<<1, 256, 0, stream>>>(img, W, H, pitch, x, y, level, phase, p, d_rec, d_rms);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
