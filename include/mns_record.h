@@ -79,4 +79,33 @@ MNS_REC_INLINE uint16_t mns_unit_of_record(uint64_t r, int rx, int ry, int px, i
     return mns_unit_desc(8 + 2 * (level - 1) + bit, t, lg - 1);
 }
 
+/* Both descriptors of the horizontally adjacent cells (px, py) and (px + 2, py) (px a multiple of
+ * 4) of one leaf record r of side >= 4, packed low | high << 16: the record's fields are decoded
+ * once (the encoder's emission, a lane's two cells). */
+MNS_REC_INLINE uint32_t mns_unit_pair_of_record(uint64_t r, int rx, int ry, int px, int py) {
+    const int level = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1;
+    const int lg = 5 - level;
+    const int o = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
+    if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) {
+        const uint32_t d = mns_unit_desc((int)((r >> MNS_REC_PAYLOAD_SHIFT) & 7), o, lg);
+        return d | (d << 16);
+    }
+    const int x = (int)((r >> MNS_REC_X_SHIFT) & 0x7FFF) * 2 - rx, y = (int)((r >> MNS_REC_Y_SHIFT) & 0x7FFF) * 2 - ry;
+    const int h = 1 << (lg - 1);
+    const int qy = (py - y) >= h ? 2 : 0;
+    int d[3];
+    for (int j = 0; j < 3; j++) {
+        const int f = (int)((r >> (41 + 6 * j)) & 63);
+        d[j] = f >= 32 ? f - 64 : f;
+    }
+    uint32_t out = 0;
+    for (int c = 0; c < 2; c++) {
+        const int q = qy + ((px + 2 * c - x) >= h ? 1 : 0);
+        const int t = q < 3 ? o + d[q] : o - (d[0] + d[1] + d[2]);
+        const int bit = (int)((r >> (59 + q)) & 1);
+        out |= (uint32_t)mns_unit_desc(8 + 2 * (level - 1) + bit, t, lg - 1) << (16 * c);
+    }
+    return out;
+}
+
 #endif

@@ -417,9 +417,12 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
         const int qi = c / (QE_WL / 4), qj = (c % (QE_WL / 4)) * 4;
         const uint2 a = *reinterpret_cast<const uint2 *>(&pix[2 * qi][2 * qj]);
         const uint2 b = *reinterpret_cast<const uint2 *>(&pix[2 * qi + 1][2 * qj]);
+        // bytes 0, 2 and 1, 3 of each word zero-extended into u16 lanes (PRMT), summed lane-wise
         uint2 s;
-        s.x = (a.x & 0x00FF00FFu) + ((a.x >> 8) & 0x00FF00FFu) + (b.x & 0x00FF00FFu) + ((b.x >> 8) & 0x00FF00FFu);
-        s.y = (a.y & 0x00FF00FFu) + ((a.y >> 8) & 0x00FF00FFu) + (b.y & 0x00FF00FFu) + ((b.y >> 8) & 0x00FF00FFu);
+        s.x = (__byte_perm(a.x, 0u, 0x4240) + __byte_perm(a.x, 0u, 0x4341)) +
+              (__byte_perm(b.x, 0u, 0x4240) + __byte_perm(b.x, 0u, 0x4341));
+        s.y = (__byte_perm(a.y, 0u, 0x4240) + __byte_perm(a.y, 0u, 0x4341)) +
+              (__byte_perm(b.y, 0u, 0x4240) + __byte_perm(b.y, 0u, 0x4341));
         *reinterpret_cast<uint2 *>(&qe[qi][qj]) = s;
     }
     __syncthreads();
@@ -602,8 +605,9 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
         if (lane == 0) p.root_cnt[root] = __popc(bA) + __popc(bB);
         if (p.unit_map) {
             const int rxg = x0 + 16 * slot, lx = node4_x(2 * lane), ly = node4_y(2 * lane);
-            const uint32_t umap = (uint32_t)mns_unit_of_record(cov, rxg, y0, lx, ly) |
-                                  ((uint32_t)mns_unit_of_record(vis4 ? recB : cov, rxg, y0, lx + 2, ly) << 16);
+            const uint32_t umap = vis4 ? (uint32_t)mns_unit_of_record(recA, rxg, y0, lx, ly) |
+                                             ((uint32_t)mns_unit_of_record(recB, rxg, y0, lx + 2, ly) << 16)
+                                       : mns_unit_pair_of_record(cov, rxg, y0, lx, ly);
             p.unit_map[root * 32 + lane] = umap;
         }
     }
