@@ -663,28 +663,42 @@ __global__ void __launch_bounds__(DT2, 2) decode_pair_kernel(const __grid_consta
 // keep the box row a 16-byte multiple and pad the ring row to 104 floats).  Stage A paints t+1
 // into the on-chip lattice qb, stage B paints t+2 and stores its lattice (or, on the last pass, the
 // uint8 image).  No raster reduction, no t+1 raw ring: ~35 KB of shared memory instead of 105 KB.
-constexpr int LHB = WA / 4 + 4;    // 52 staged lattice columns per parity
-constexpr int LQS = 2 * LHB;       // 104-float ring row: even half | odd half
-constexpr int LQR = 64;            // t-lattice ring rows: 8 root-row slots (up to 5 in flight)
-constexpr int LNS = LQR / 8;
-constexpr int LQRP = LQR + 8;      // + a second copy of slot 0, so a 4-row read never wraps
-constexpr int LBOX = 8 * LQS * 4;  // bytes of one slot
-constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * QS * 4;
-#ifndef LAT_MINB
-#define LAT_MINB 4
+#ifndef LAT_BR
+#define LAT_BR 8
 #endif
+constexpr int LBR = LAT_BR;               // roots per column band
+constexpr int LNWA = (LBR + 2) / 2;       // stage-A warps (the band +- 1 root, two roots each)
+constexpr int LNWB = LBR / 2;             // stage-B warps
+constexpr int LDT = (LNWA + LNWB) * 32;
+constexpr int LWA = LBR * 16 + 64;        // raster-t window: band +- 32 px
+constexpr int LHB = LWA / 4 + 4;          // staged lattice columns per parity (+4: 16-byte box rows)
+constexpr int LQS = 2 * LHB;              // ring row: even half | odd half
+constexpr int LQR = 64;                   // t-lattice ring rows: 8 root-row slots (up to 5 in flight)
+constexpr int LNS = LQR / 8;
+constexpr int LQRP = LQR + 8;             // + a second copy of slot 0, so a 4-row read never wraps
+constexpr int LBOX = 8 * LQS * 4;         // bytes of one slot
+constexpr int LQBW = (LBR * 16 + 32) / 2; // t+1 lattice columns (band +- 16 px)
+constexpr int LQBS = LQBW + 4;            // padded row stride
+constexpr int LQBH = LQBW / 2;            // de-interleave half
+constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * LQBS * 4;
+#ifndef LAT_MINB
+#define LAT_MINB (LBR == 8 ? 4 : 2)
+#endif
+// lane_tab packs column offsets into 7 bits (A: rc <= LBR, B: rc <= LBR - 1, |dx| <= 8)
+static_assert(LHB + (8 * LBR + 16 + 8 + 1) / 2 < 128 && LQBH + (8 * LBR + 8 + 1) / 2 < 128,
+              "lane_tab column offsets exceed 7 bits");
 
 template <bool FLAT, bool OUT>
-__global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                         const SweepParams p) {
     extern __shared__ __align__(128) unsigned char dsm[];
     float(*qa)[LQS] = reinterpret_cast<float(*)[LQS]>(dsm);
-    float(*qb)[QS] = reinterpret_cast<float(*)[QS]>(dsm + LQRP * LQS * 4);
+    float(*qb)[LQBS] = reinterpret_cast<float(*)[LQBS]>(dsm + LQRP * LQS * 4);
     __shared__ __align__(8) uint64_t bars[LNS];
     __shared__ float st[16];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int x0 = blockIdx.x * BR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
+    const int x0 = blockIdx.x * LBR * 16, xa0 = x0 - 32, xb0 = x0 - 16;
     const int r_s = p.rr0 + blockIdx.y * p.cr, r_e = min(r_s + p.cr, p.rr1);
     const int rh = p.H / 16, lw = p.W / 2;
     const int nblocks = (r_e - r_s) + 4;  // block k = the 8 lattice rows of root row r_s - 2 + k
@@ -712,7 +726,7 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
         }
     };
     const Lane L = lane_of(lane);
-    const bool stage_a = warp < NWA;
+    const bool stage_a = warp < LNWA;
     if (!FLAT) {
         if (tid == 0) {
             prefetch_tmap(&tmap);
@@ -725,12 +739,12 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
     }
     auto no_raw = [](int, int) { return 0.f; };
     // One loop per stage (warp-uniform roles; the same iteration count, one barrier per iteration).
-    // Iteration i: A paints root row i of t+1 (root columns -1 .. BR of the band), B paints root
-    // row i - 2 of t+2 (columns 0 .. BR-1).
+    // Iteration i: A paints root row i of t+1 (root columns -1 .. LBR of the band), B paints root
+    // row i - 2 of t+2 (columns 0 .. LBR-1).
     auto run = [&](auto role) {
         constexpr bool A = decltype(role)::value;
-        const int rc = A ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - NWA) + (lane >> 4);
-        const int rxi = blockIdx.x * BR + rc;
+        const int rc = A ? 2 * warp + (lane >> 4) - 1 : 2 * (warp - LNWA) + (lane >> 4);
+        const int rxi = blockIdx.x * LBR + rc;
         const bool col_ok = rxi >= 0 && rxi < p.rw;
         const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
         constexpr int lag = A ? 0 : 2;
@@ -743,7 +757,7 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
             return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
         };
         const int rxg = rxi * 16;
-        const LaneTab tab = A ? lane_tab<LQS, LHB>(L, rc, 16) : lane_tab<QS, QH>(L, rc, 8);
+        const LaneTab tab = A ? lane_tab<LQS, LHB>(L, rc, 16) : lane_tab<LQBS, LQBH>(L, rc, 8);
         uint2 word = word_of(r_s - 1 - lag, uptr);
         for (int i = r_s - 1; i <= r_e + 1; i++) {
             const int row = i - lag;
@@ -769,13 +783,13 @@ __global__ void __launch_bounds__(DT2, LAT_MINB) decode_pair_lat_kernel(const __
                     const int g = (ryg + L.ly) >> 1;
 #pragma unroll
                     for (int r = 0; r < 2; r++)
-                        lat_store<QS, QH>(&qb[0][0], g + r, wc >> 1,
+                        lat_store<LQBS, LQBH>(&qb[0][0], g + r, wc >> 1,
                                           make_float2(((v[8 * r] + v[8 * r + 1]) + v[8 * r + 4]) + v[8 * r + 5],
                                                       ((v[8 * r + 2] + v[8 * r + 3]) + v[8 * r + 6]) + v[8 * r + 7]));
                 }
             } else {
                 const bool live = col_ok && row >= r_s;
-                paint_block<QS, QH, QR, false, true>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg,
+                paint_block<LQBS, LQBH, QR, false, true>(word, live, L, st, &qb[0][0], no_raw, false, p.init, rxg, ryg,
                                                      xb0, interior, p.W, p.H, v, &tab);
                 if (live) {
                     if ((word.x & 0xFFFFu) >> 14 == 0) atomicOr(p.state, 1);  // a 2x2 unit: needs the raster path
@@ -1125,14 +1139,14 @@ int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int
                            2, 8))
             return -1;
     }
-    p.cr = rows_per_cta(rr1 - rr0, (p.rw + BR - 1) / BR, CR2);
-    dim3 grid((p.rw + BR - 1) / BR, (rr1 - rr0 + p.cr - 1) / p.cr);
+    p.cr = rows_per_cta(rr1 - rr0, (p.rw + LBR - 1) / LBR, CR2);
+    dim3 grid((p.rw + LBR - 1) / LBR, (rr1 - rr0 + p.cr - 1) / p.cr);
     p.n_ctas = grid.x * grid.y;
     if (cur)
-        (out ? decode_pair_lat_kernel<false, true> : decode_pair_lat_kernel<false, false>)<<<grid, DT2, LAT_SMEM,
+        (out ? decode_pair_lat_kernel<false, true> : decode_pair_lat_kernel<false, false>)<<<grid, LDT, LAT_SMEM,
                                                                                                stream>>>(tmap, p);
     else
-        (out ? decode_pair_lat_kernel<true, true> : decode_pair_lat_kernel<true, false>)<<<grid, DT2, LAT_SMEM,
+        (out ? decode_pair_lat_kernel<true, true> : decode_pair_lat_kernel<true, false>)<<<grid, LDT, LAT_SMEM,
                                                                                              stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
