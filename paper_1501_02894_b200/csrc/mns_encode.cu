@@ -499,11 +499,11 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
     }
     __syncwarp();
 
-    // ---- K2: decisions, warp-local (warp w owns root slots w, w + EW: everything from here to
-    // the emission reads only this warp's moments, so no CTA barrier).  Round 1: level-1 nodes
-    // on lanes 8-9 and level-2 nodes on lanes 0-7 (a level-2 node is decided whether or not its
-    // root is accepted -- the emission's visibility flags discard covered decisions); round 2:
-    // the visible level-3 nodes (and the level-4 quartets below them), one per lane.
+    // ---- K2: decisions.  Round 1 (warp-local: warp w owns root slots w, w + EW): the 8 level-2
+    // nodes of its roots x 4 quadrant lanes (a node is decided whether or not a parent accepts --
+    // the emission's visibility flags discard covered decisions); round 2 (warp-local): the level-3
+    // nodes not covered by a level-2 leaf (and the level-4 quartets below them), one per lane;
+    // round 3 (CTA-wide, warps 0-1): the level-1 roots.
     const bool mns = p.mns != 0;
     {  // round 1: the 8 level-2 nodes of this warp's two roots x 4 quadrant lanes
         const int node = lane >> 2, s = warp + EW * (node >> 2), k = node & 3;
@@ -517,23 +517,11 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
             ts.rec2[s][k] = rec;
         }
     }
-    {  // round 2: the 2 level-1 roots x 4 quadrant lanes (lanes 0-7)
-        const int s = warp + EW * (lane >> 2);
-        const bool live = lane < 8 && s < nr;
-        const int sc = live ? s : 0;
-        bool acc;
-        uint64_t rec;
-        node_quad_lanes(w, p, live, sc, 1, 0, 0, ts.m1[sc], ts.m2[sc], try1, acc, rec);
-        if (live && (lane & 3) == 0) {
-            ts.acc1[s] = acc;
-            ts.rec1[s] = rec;
-        }
-    }
     __syncwarp();
     {
         const int s = warp + EW * (lane >> 4), m = lane & 15;
         if (s < nr) {
-            const bool vis = (p.root_level == 2 || !ts.acc1[s]) && !ts.acc2[s][m >> 2];
+            const bool vis = !ts.acc2[s][m >> 2];  // a level-1 acceptance is applied at the emission
             bool acc = false;
             uint64_t rec = 0;
             if (vis) {
@@ -566,7 +554,22 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
             ts.rec3[s][m] = rec;
         }
     }
-    __syncwarp();
+    // round 3: the level-1 roots of the whole tile, 16 roots x 4 quadrant lanes on warps 0-1 (every
+    // lane busy, instead of 8 lanes of every warp); the other warps wait at the emission barrier
+    __syncthreads();
+    if (warp < 2) {
+        const int s = 8 * warp + (lane >> 2);
+        const bool live = s < nr;
+        const int sc = live ? s : 0;
+        bool acc;
+        uint64_t rec;
+        node_quad_lanes(w, p, live, sc, 1, 0, 0, ts.m1[sc], ts.m2[sc], try1, acc, rec);
+        if (live && (lane & 3) == 0) {
+            ts.acc1[s] = acc;
+            ts.rec1[s] = rec;
+        }
+    }
+    __syncthreads();
 
     // ---- K2b: DFS (Morton) emission per root: lane owns cells 2l, 2l+1; unit map words
     for (int slot = warp; slot < nr; slot += EW) {
