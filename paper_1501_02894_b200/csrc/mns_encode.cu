@@ -428,74 +428,81 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
     __syncthreads();
 
     const bool try1 = p.root_level == 1 && p.min_dim >= 32;  // encoder.py:231 guard 2*size <= min_dim
-    // ---- K1c: pixel-parallel block moments of every level-1..3 node (lane = 2x4 pixel block)
+    // ---- K1c: block moments of every level-1..3 node.  Lane = one 4x4 level-3 node (16 pixels);
+    // half-warps take the warp's two roots (slots warp, warp + EW) in one pass.  Level-2 sums over 4
+    // lanes, level-1 sums over the half-warp (its Sr, Srr from the level-2 partials).
     {
-        const int a = lane >> 3, b = (lane >> 1) & 3, c = lane & 1;
-        const int lx = node3_x(4 * a + b), ly = node3_y(4 * a + b) + 2 * c;
-        for (int slot = warp; slot < nr; slot += EW) {
-            const int wrx = 16 + 16 * slot;
-            int r[8];
-            const uint32_t w0 = *reinterpret_cast<const uint32_t *>(&pix[16 + ly][wrx + lx]);
-            const uint32_t w1 = *reinterpret_cast<const uint32_t *>(&pix[16 + ly + 1][wrx + lx]);
+        const int hw = lane >> 4, m = lane & 15;
+        const int slot = warp + EW * hw;
+        const bool live = slot < nr;
+        const int sl = live ? slot : 0;
+        const int lx = node3_x(m), ly = node3_y(m);
+        int r[16];
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                r[j] = (w0 >> (8 * j)) & 0xFF;
-                r[4 + j] = (w1 >> (8 * j)) & 0xFF;
-            }
-            const int srL = r[0] + r[1] + r[4] + r[5], srR = r[2] + r[3] + r[6] + r[7];
-            const int srrL = r[0] * r[0] + r[1] * r[1] + r[4] * r[4] + r[5] * r[5];
-            const int srrR = r[2] * r[2] + r[3] * r[3] + r[6] * r[6] + r[7] * r[7];
-            ts.sr4[slot][2 * lane] = srL;
-            ts.sr4[slot][2 * lane + 1] = srR;
-            ts.srr4[slot][2 * lane] = srrL;
-            ts.srr4[slot][2 * lane + 1] = srrR;
-            // partial q-moments of this lane's 8 pixels against the domain of node (nx, ny, s)
-            auto part = [&](int nx, int ny, int s, int &sq, int &sqq, int &sqr) {
-                const int gdx = clampi(x0 + 16 * slot + nx - s / 2, 0, p.W - 2 * s);
-                const int gdy = clampi(y0 + ny - s / 2, 0, p.H - 2 * s);
-                const int qr = (gdy - wy0) / 2 + (ly - ny), qc = (gdx - wx0) / 2 + (lx - nx);
-                sq = sqq = sqr = 0;
+        for (int i = 0; i < 4; i++) {
+            const uint32_t wd = *reinterpret_cast<const uint32_t *>(&pix[16 + ly + i][16 + 16 * sl + lx]);
 #pragma unroll
-                for (int i = 0; i < 2; i++)
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const int q = qe[qr + i][qc + j];
-                        sq += q;
-                        sqq += q * q;
-                        sqr += q * r[4 * i + j];
-                    }
-            };
-            int v[5];  // sr, srr, sq, sqq, sqr
-            // level 3 (lane pairs)
-            v[0] = srL + srR;
-            v[1] = srrL + srrR;
-            part(lx, ly - 2 * c, 4, v[2], v[3], v[4]);
-#pragma unroll
-            for (int k = 0; k < 5; k++) v[k] += __shfl_xor_sync(FULL, v[k], 1);
-            if (c == 0) ts.m3[slot][4 * a + b] = Mom{v[0], v[1], v[2], v[3], v[4]};
-            // level 2 (8-lane groups)
-            v[0] = srL + srR;
-            v[1] = srrL + srrR;
-            part(node2_x(a), node2_y(a), 8, v[2], v[3], v[4]);
-#pragma unroll
-            for (int k = 0; k < 5; k++) {
-                v[k] += __shfl_xor_sync(FULL, v[k], 1);
-                v[k] += __shfl_xor_sync(FULL, v[k], 2);
-                v[k] += __shfl_xor_sync(FULL, v[k], 4);
-            }
-            if ((lane & 7) == 0) ts.m2[slot][a] = Mom{v[0], v[1], v[2], v[3], v[4]};
-            // level 1 (whole warp)
-            v[0] = srL + srR;
-            v[1] = srrL + srrR;
-            if (try1) {
-                part(0, 0, 16, v[2], v[3], v[4]);
-            } else {
-                v[2] = v[3] = v[4] = 0;
-            }
-#pragma unroll
-            for (int k = 0; k < 5; k++) v[k] = __reduce_add_sync(FULL, v[k]);
-            if (lane == 0) ts.m1[slot] = Mom{v[0], v[1], v[2], v[3], v[4]};
+            for (int j = 0; j < 4; j++) r[4 * i + j] = (wd >> (8 * j)) & 0xFF;
         }
+        // 2x2 cell sums (level-4 ranges, Morton order inside the node) and the node's Sr, Srr
+        int sr3 = 0, srr3 = 0;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int i0 = 2 * (c >> 1), j0 = 2 * (c & 1);
+            const int a0 = r[4 * i0 + j0], a1 = r[4 * i0 + j0 + 1], a2 = r[4 * i0 + 4 + j0], a3 = r[4 * i0 + 5 + j0];
+            const int cs = a0 + a1 + a2 + a3, css = a0 * a0 + a1 * a1 + a2 * a2 + a3 * a3;
+            if (live) {
+                ts.sr4[slot][4 * m + c] = cs;
+                ts.srr4[slot][4 * m + c] = css;
+            }
+            sr3 += cs;
+            srr3 += css;
+        }
+        // q-moments of the lane's 16 pixels against the domain of node (nx, ny, s)
+        auto part = [&](int nx, int ny, int s, int &sq, int &sqq, int &sqr) {
+            const int gdx = clampi(x0 + 16 * sl + nx - s / 2, 0, p.W - 2 * s);
+            const int gdy = clampi(y0 + ny - s / 2, 0, p.H - 2 * s);
+            const uint16_t *qp = &qe[(gdy - wy0) / 2 + (ly - ny)][(gdx - wx0) / 2 + (lx - nx)];
+            sq = sqq = sqr = 0;
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int q = qp[i * QE_W + j];
+                    sq += q;
+                    sqq += q * q;
+                    sqr += q * r[4 * i + j];
+                }
+        };
+        int sq, sqq, sqr;
+        part(lx, ly, 4, sq, sqq, sqr);  // level 3: the lane is the node
+        if (live) ts.m3[slot][m] = Mom{sr3, srr3, sq, sqq, sqr};
+        // level 2 (4-lane groups)
+        const int k2 = m >> 2;
+        int v[5] = {sr3, srr3, 0, 0, 0};
+        part(node2_x(k2), node2_y(k2), 8, v[2], v[3], v[4]);
+#pragma unroll
+        for (int k = 0; k < 5; k++) {
+            v[k] += __shfl_xor_sync(FULL, v[k], 1);
+            v[k] += __shfl_xor_sync(FULL, v[k], 2);
+        }
+        if (live && (m & 3) == 0) ts.m2[slot][k2] = Mom{v[0], v[1], v[2], v[3], v[4]};
+        // level 1 (half-warp): Sr, Srr from the level-2 sums, the q-moments from the lanes
+        int u[5] = {v[0], v[1], 0, 0, 0};
+        if (try1) part(0, 0, 16, u[2], u[3], u[4]);
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            u[k] += __shfl_xor_sync(FULL, u[k], 4);
+            u[k] += __shfl_xor_sync(FULL, u[k], 8);
+        }
+#pragma unroll
+        for (int k = 2; k < 5; k++) {
+            u[k] += __shfl_xor_sync(FULL, u[k], 1);
+            u[k] += __shfl_xor_sync(FULL, u[k], 2);
+            u[k] += __shfl_xor_sync(FULL, u[k], 4);
+            u[k] += __shfl_xor_sync(FULL, u[k], 8);
+        }
+        if (live && m == 0) ts.m1[slot] = Mom{u[0], u[1], u[2], u[3], u[4]};
     }
     __syncwarp();
 
