@@ -481,10 +481,12 @@ def test_lattice_pass_equals_two_sweeps(mns, W, H, rr):
     assert int(err.item()) == 0
 
 
-@pytest.mark.parametrize("side,iters", [(512, 10), (512, 9), (256, 1), (256, 2), (48, 3), (1024, 8)])
-def test_lattice_decode_equals_raster_decode(mns, side, iters):
-    """Whole-image decode of an e3 = inf code: the lattice-state path (mns_decode_quadtree_lattice,
-    chosen by decode_device) and the raster path (mns_decode_quadtree) give the identical image."""
+@pytest.mark.parametrize("side,iters,root_level", [(512, 10, 1), (512, 9, 1), (256, 1, 1), (256, 2, 1), (48, 3, 1),
+                                                   (1024, 8, 1), (256, 8, 2), (512, 7, 2)])
+def test_lattice_decode_equals_raster_decode(mns, side, iters, root_level):
+    """Whole-image decode of an e3 = inf code (16->8->4, and the 8->4 root_level=2 form of configs
+    c1/c3): the lattice-state path (mns_decode_quadtree_lattice, chosen by decode_device) and the
+    raster path (mns_decode_quadtree) give the identical image."""
     import ctypes
 
     from paper_1501_02894_b200 import _native as N
@@ -492,7 +494,8 @@ def test_lattice_decode_equals_raster_decode(mns, side, iters):
 
     L = N.lib()
     px = synth_image(side, 21, noise_sigma=9.0, n_blobs=10)
-    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf), root_level=root_level)
+    assert code.min_leaf == 4
     got, it, _ = mns.decode_device(code, iters=iters)
     W = H = side
     ras = [torch.empty((H, W), device="cuda") for _ in range(2)]
