@@ -180,7 +180,7 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // units, from raw_sum(R, C) = the 2x2 raster sum at absolute row R, window column C.  Every
 // lane of the warp must call it (segmented shuffles); `live` lanes get v.
 // Lattice addressing of an interior lane, per unit size k = 1..3, fixed for a kernel: the column
-// offsets of its two de-interleaved base pointers (7 bits each) and the lattice-row offset of its
+// offsets of its two de-interleaved base pointers (8 bits each) and the lattice-row offset of its
 // domain from 8 * (root row) + 8 (5 bits) -- so a paint needs no per-block coordinate arithmetic.
 struct LaneTab {
     uint32_t t[3];
@@ -194,7 +194,7 @@ __device__ __forceinline__ LaneTab lane_tab(const Lane &L, int rc, int col_base)
         const int dx = (int)((L.tx >> (6 * k)) & 63) / 2 - 8, dy = (int)((L.ty >> (6 * k)) & 63) / 2 - 8;
         const int qc = 8 * rc + col_base + dx;  // window lattice column of the domain's first column
         const uint32_t c0 = (qc & 1) * HALF + (qc >> 1), c1 = ((qc + 1) & 1) * HALF + ((qc + 1) >> 1);
-        T.t[k - 1] = c0 | (c1 << 7) | ((uint32_t)(dy + 8) << 14);
+        T.t[k - 1] = c0 | (c1 << 8) | ((uint32_t)(dy + 8) << 16);
     }
     return T;
 }
@@ -234,9 +234,9 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             const float *p0, *p1;  // columns qc, qc + 2 and qc + 1, qc + 3 of the domain's first lattice row
             if (FAST && interior) {
                 const uint32_t t = k == 1 ? tab->t[0] : (k == 2 ? tab->t[1] : tab->t[2]);
-                const float *row = lat + ((ryg >> 1) + (int)(t >> 14) - 8 & (RING - 1)) * QSTR;
-                p0 = row + (t & 127);
-                p1 = row + ((t >> 7) & 127);
+                const float *row = lat + ((ryg >> 1) + (int)(t >> 16) - 8 & (RING - 1)) * QSTR;
+                p0 = row + (t & 255);
+                p1 = row + ((t >> 8) & 255);
             } else {
                 int X, Y;
                 if (interior) {
@@ -684,9 +684,9 @@ constexpr int LAT_SMEM = LQRP * LQS * 4 + QRP * LQBS * 4;
 #ifndef LAT_MINB
 #define LAT_MINB (LBR == 8 ? 4 : 2)
 #endif
-// lane_tab packs column offsets into 7 bits (A: rc <= LBR, B: rc <= LBR - 1, |dx| <= 8)
-static_assert(LHB + (8 * LBR + 16 + 8 + 1) / 2 < 128 && LQBH + (8 * LBR + 8 + 1) / 2 < 128,
-              "lane_tab column offsets exceed 7 bits");
+// lane_tab packs column offsets into 8 bits (A: rc <= LBR, B: rc <= LBR - 1, |dx| <= 8)
+static_assert(LHB + (8 * LBR + 16 + 8 + 1) / 2 < 256 && LQBH + (8 * LBR + 8 + 1) / 2 < 256,
+              "lane_tab column offsets exceed 8 bits");
 
 template <bool FLAT, bool OUT>
 __global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __grid_constant__ CUtensorMap tmap,
