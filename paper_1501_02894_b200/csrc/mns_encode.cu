@@ -578,47 +578,64 @@ __global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant
     }
     __syncthreads();
 
-    // ---- K2b: DFS (Morton) emission per root: lane owns cells 2l, 2l+1; unit map words
-    for (int slot = warp; slot < nr; slot += EW) {
-        const int a = lane >> 3, m3 = lane >> 1, c = lane & 1;
+    // ---- K2b: DFS (Morton) emission.  Half-warps take the warp's two roots in one pass; lane m
+    // owns level-3 node m (cells 4m..4m+3): the covering leaf's record on the first lane it covers,
+    // or the node's four level-4 records; offsets by two ballots (records per lane: 0, 1 or 4).
+    {
+        const int hw = lane >> 4, m = lane & 15, a = m >> 2;
+        const int slot = warp + EW * hw;
+        const bool live = slot < nr;
+        const int sl = live ? slot : 0;
         const bool vis1 = p.root_level == 1;
-        const bool acc1 = ts.acc1[slot];
+        const bool acc1 = ts.acc1[sl];
         const bool vis2 = !vis1 || !acc1;
-        const bool acc2 = ts.acc2[slot][a];
+        const bool acc2 = ts.acc2[sl][a];
         const bool vis3 = vis2 && !acc2;
-        const bool acc3 = ts.acc3[slot][m3];
+        const bool acc3 = ts.acc3[sl][m];
         const bool vis4 = vis3 && !acc3;
-        uint64_t recA = 0, recB = 0, cov = 0;
-        bool hasA = false, hasB = false;
+        uint64_t cov;
+        int nrec;
         if (vis1 && acc1) {
-            hasA = lane == 0;
-            cov = recA = ts.rec1[slot];
+            nrec = m == 0;
+            cov = ts.rec1[sl];
         } else if (vis2 && acc2) {
-            hasA = (lane & 7) == 0;
-            cov = recA = ts.rec2[slot][a];
+            nrec = (m & 3) == 0;
+            cov = ts.rec2[sl][a];
         } else if (vis3 && acc3) {
-            hasA = c == 0;
-            cov = recA = ts.rec3[slot][m3];
-        } else if (vis4) {
-            hasA = hasB = true;
-            recA = ts.rec4[slot][2 * lane];
-            recB = ts.rec4[slot][2 * lane + 1];
-            cov = recA;
+            nrec = 1;
+            cov = ts.rec3[sl][m];
+        } else {
+            nrec = 4;
+            cov = ts.rec4[sl][4 * m];
         }
-        const unsigned bA = __ballot_sync(FULL, hasA), bB = __ballot_sync(FULL, hasB);
-        const unsigned lt = lanemask_lt();
-        const int offA = __popc(bA & lt) + __popc(bB & lt);
-        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + slot;
-        uint64_t *st = p.stage + root * 64;
-        if (hasA) st[offA] = recA;
-        if (hasB) st[offA + (hasA ? 1 : 0)] = recB;
-        if (lane == 0) p.root_cnt[root] = __popc(bA) + __popc(bB);
-        if (p.unit_map) {
-            const int rxg = x0 + 16 * slot, lx = node4_x(2 * lane), ly = node4_y(2 * lane);
-            const uint32_t umap = vis4 ? (uint32_t)mns_unit_of_record(recA, rxg, y0, lx, ly) |
-                                             ((uint32_t)mns_unit_of_record(recB, rxg, y0, lx + 2, ly) << 16)
-                                       : mns_unit_pair_of_record(cov, rxg, y0, lx, ly);
-            p.unit_map[root * 32 + lane] = umap;
+        if (!live) nrec = 0;
+        const unsigned half = hw ? 0xFFFF0000u : 0x0000FFFFu, lt = lanemask_lt() & half;
+        const unsigned b1 = __ballot_sync(FULL, nrec != 0) & half, b4 = __ballot_sync(FULL, nrec == 4) & half;
+        const int off = __popc(b1 & lt) + 3 * __popc(b4 & lt);
+        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + sl;
+        if (live) {
+            uint64_t *st = p.stage + root * 64 + off;
+            if (nrec == 4) {
+#pragma unroll
+                for (int c = 0; c < 4; c++) st[c] = ts.rec4[sl][4 * m + c];
+            } else if (nrec) {
+                st[0] = cov;
+            }
+            if (m == 0) p.root_cnt[root] = __popc(b1) + 3 * __popc(b4);
+            if (p.unit_map) {
+                const int rxg = x0 + 16 * sl, lx = node3_x(m), ly = node3_y(m);
+                uint2 u;
+                if (vis4) {
+                    u.x = (uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m], rxg, y0, lx, ly) |
+                          ((uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 1], rxg, y0, lx + 2, ly) << 16);
+                    u.y = (uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 2], rxg, y0, lx, ly + 2) |
+                          ((uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 3], rxg, y0, lx + 2, ly + 2) << 16);
+                } else {
+                    u.x = mns_unit_pair_of_record(cov, rxg, y0, lx, ly);
+                    u.y = mns_unit_pair_of_record(cov, rxg, y0, lx, ly + 2);
+                }
+                *reinterpret_cast<uint2 *>(&p.unit_map[root * 32 + 2 * m]) = u;
+            }
         }
     }
 }
