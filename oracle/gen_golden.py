@@ -388,11 +388,55 @@ def gen_rd(store, manifest):
     print(f"rd cases: {k} sweeps, {j} histograms")
 
 
+def stress_images():
+    """Adversarial structures for the exact decisions: saturated blocks, hard edges, checkerboards at
+    several node sizes, gradients (contrast-bin edges), flat patches (D = 0), small-amplitude noise."""
+    rng = np.random.default_rng(99)
+    n = 192
+    y, x = np.mgrid[0:n, 0:n]
+    imgs = {
+        "checker2": np.where(((x // 2) + (y // 2)) % 2 == 0, 255, 0),
+        "checker4x8": np.where(((x // 4) + (y // 8)) % 2 == 0, 250, 3),
+        "ramp": np.clip(x * 1.33 + y * 0.01, 0, 255),
+        "sincos": np.clip(128 + 127 * np.sin(x / 3.0) * np.cos(y / 5.0), 0, 255),
+        "edge": np.where(x < n // 2, 0, 255) + 0 * y,
+        "binary_noise": rng.integers(0, 2, (n, n)) * 255,
+        "low_noise": rng.integers(120, 137, (n, n)),
+        "gauss_noise": np.clip(rng.normal(128, 40, (n, n)), 0, 255),
+        "flat": np.full((n, n), 77),
+        "tiles": np.clip((x % 16) * 16 + (y % 16), 0, 255),
+    }
+    return {k: np.ascontiguousarray(np.rint(v).astype(np.uint8)) for k, v in imgs.items()}
+
+
+STRESS_CONFIGS = [dict(e1=8.0, e2=8.0, e3=8.0, mean_tol=16.0, mode="mns"),
+                  dict(e1=2.0, e2=3.0, e3=math.inf, mean_tol=16.0, mode="mns"),
+                  dict(e1=0.5, e2=1.0, e3=1.5, mean_tol=4.0, mode="mns"),
+                  dict(e1=20.0, e2=12.0, e3=6.0, mean_tol=40.0, mode="mns"),
+                  dict(e1=5.0, e2=5.0, e3=5.0, mean_tol=16.0, mode="no_search")]
+
+
+def gen_stress(store, manifest):
+    """Reference encode_quadtree records (and an 8-sweep decode) of adversarial images."""
+    k = 0
+    for name, px in stress_images().items():
+        store[f"img/{name}"] = px
+        for ci, cfg in enumerate(STRESS_CONFIGS):
+            code = encode_quadtree(GrayImage(px), EncoderConfig(**cfg))
+            key = f"s{k}"
+            store[f"{key}/records"] = records_of(code)
+            store[f"{key}/decode8"] = decode(code, DecodeConfig(max_iters=8, stop_delta=0.0)).pixels
+            manifest.append(dict(key=key, image=name, cfg={k2: (None if v == math.inf else v) for k2, v in
+                                                          cfg.items()}))
+            k += 1
+    print(f"stress cases: {k}")
+
+
 def main(argv=None):
     """Regenerate every golden set, or only the named ones (e.g. ``gen_golden.py rd``)."""
     os.makedirs(OUT, exist_ok=True)
     table = (("encode", gen_encode), ("decode_step", gen_decode_step), ("search", gen_search),
-             ("nodes", gen_nodes), ("rd", gen_rd))
+             ("nodes", gen_nodes), ("rd", gen_rd), ("stress", gen_stress))
     want = set(argv or []) or {n for n, _ in table}
     for name, fn in table:
         if name not in want:

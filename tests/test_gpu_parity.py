@@ -620,3 +620,18 @@ def test_unit2_leaf_count_matches_host(mns, golden):
         assert rd.unit2_leaves(dev, len(rec)) == want, case["key"]
         seen.add(want > 0)
     assert seen == {True, False}
+
+
+def test_encode_stress_golden(mns, golden):
+    """Reference-generated adversarial cases (oracle/gen_golden.py gen_stress: saturated blocks, hard
+    edges, checkerboards, ramps across contrast-bin edges, flat and noisy patches; 5 configs incl.
+    no_search and e3 = inf): GPU codes bit-exact, 8-sweep decodes within 1 LSB."""
+    g = golden("stress")
+    for case in g.manifest:
+        k, c = case["key"], case["cfg"]
+        px = g[f"img/{case['image']}"]
+        cfg = mns.EncoderConfig(**{n: (math.inf if v is None else v) for n, v in c.items()})
+        code = mns.encode_quadtree(mns.GrayImage(px), cfg)
+        assert np.array_equal(code.records, g[f"{k}/records"]), case
+        got = mns.decode(code, mns.DecodeConfig(max_iters=8, stop_delta=0.0)).pixels
+        assert int(np.abs(got.astype(int) - g[f"{k}/decode8"].astype(int)).max()) <= 1, case

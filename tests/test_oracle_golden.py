@@ -90,3 +90,15 @@ def test_tie_fixtures_contain_rounding_decided_picks(golden):
     ties = [c for c in g.manifest if c["image"].startswith("ties")]
     assert sum(c["exact_ties"] for c in ties) > 100
     assert sum(c["ties_bit1"] for c in ties) > 0
+
+
+def test_oracle_stress_golden(golden):
+    """The oracle restatement against the reference on adversarial images (gen_stress)."""
+    import math
+
+    g = golden("stress")
+    for case in g.manifest:
+        c = case["cfg"]
+        e = tuple(math.inf if c[n] is None else c[n] for n in ("e1", "e2", "e3"))
+        rec, _ = O.encode_quadtree_records(g[f"img/{case['image']}"], e, c["mean_tol"], c["mode"] == "mns")
+        assert np.array_equal(rec, g[f"{case['key']}/records"]), case
