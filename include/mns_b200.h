@@ -76,6 +76,17 @@ int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64
 int mns_try_node(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int32_t x, int32_t y, int32_t level,
                  int32_t phase, const mns_enc_cfg *cfg, uint64_t *record, double *rms, void *stream);
 
+/* The same with the record compaction (the second kernel) on compact_stream,
+ * ordered after the encoder by an event: the unit map is complete when `stream`
+ * reaches this point, the records / root_offsets / d_count only when
+ * compact_stream does (so a decoder on `stream` overlaps the compaction).  The
+ * workspace stays in use until compact_stream passes the compaction. */
+int mns_encode_quadtree_split(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
+                              int32_t n_images, int32_t root_row_begin, int32_t root_row_end, const mns_enc_cfg *cfg,
+                              uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,
+                              uint32_t *unit_map, void *workspace, int64_t workspace_bytes, void *stream,
+                              void *compact_stream);
+
 /* Decoder unit map (mns_record.h) of a record array grouped by root: 32 uint32
  * words (64 cells) per root of the root rows [root_row_begin, root_row_end).
  * mns_encode_quadtree emits the same map directly when unit_map != NULL. */

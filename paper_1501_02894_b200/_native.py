@@ -52,6 +52,8 @@ def _declare(L):
         "mns_encode_workspace_bytes": [I32, I32, I32, I32, P],
         "mns_encode_quadtree": [P, I32, I32, I64, I64, I32, I32, I32, ctypes.POINTER(EncCfg), P, I64, P, P, P, P,
                                 I64, P],
+        "mns_encode_quadtree_split": [P, I32, I32, I64, I64, I32, I32, I32, ctypes.POINTER(EncCfg), P, I64, P, P,
+                                      P, P, I64, P, P],
         "mns_build_unit_map": [P, P, I32, I32, I32, P, P],
         "mns_try_node": [P, I32, I32, I64, I32, I32, I32, I32, ctypes.POINTER(EncCfg), P, P, P],
         "mns_decode_workspace_bytes": [I32, I32, P],
@@ -84,7 +86,7 @@ def _declare(L):
     return L
 
 
-EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_try_node", "mns_build_unit_map", "mns_decode_workspace_bytes", "mns_decode_quadtree",
+EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_encode_quadtree_split", "mns_try_node", "mns_build_unit_map", "mns_decode_workspace_bytes", "mns_decode_quadtree",
            "mns_decode_sweep", "mns_decode_sweep2", "mns_decode_pass_lattice",
            "mns_decode_flat_lattice", "mns_decode_quadtree_lattice", "mns_decode_units", "mns_decode_step_f64", "mns_search_workspace_bytes", "mns_full_search",
            "mns_local_search", "mns_stream_workspace_bytes", "mns_write_stream", "mns_read_stream_workspace_bytes", "mns_read_stream",

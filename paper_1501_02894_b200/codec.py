@@ -143,7 +143,7 @@ def enc_cfg(config: EncoderConfig, root_level: int = 1) -> N.EncCfg:
 
 def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows: Optional[tuple] = None,
                   height: Optional[int] = None, out: Optional[DeviceCode] = None, with_unit_map: bool = True,
-                  stream=None) -> DeviceCode:
+                  stream=None, compact_stream=None) -> DeviceCode:
     """MNS quadtree encode of a padded uint8 CUDA tensor [H, W] or a batch [B, H, W].
 
     root_rows=(r0, r1) restricts the work to root rows [r0, r1) (strip sharding); then ``img``
@@ -176,9 +176,17 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     # leaf is 2x2 and no level-3 phase-2 leaf has 2x2 quadrants
     out.min_leaf = 4 if math.isinf(config.e3) else 0
     cfg = enc_cfg(config, root_level)
-    N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
-                                  ctypes.byref(cfg), N.ptr(out.records), out.records.numel(), N.ptr(out.root_offsets),
-                                  N.ptr(out.count), N.ptr(out.unit_map), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    if compact_stream is None:
+        N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
+                                      ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
+                                      N.ptr(out.root_offsets), N.ptr(out.count), N.ptr(out.unit_map), N.ptr(ws),
+                                      ws.numel(), N.stream_ptr(stream)))
+    else:  # records / root_offsets / count become valid on compact_stream (the unit map on stream)
+        N.check(L.mns_encode_quadtree_split(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
+                                            ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
+                                            N.ptr(out.root_offsets), N.ptr(out.count), N.ptr(out.unit_map),
+                                            N.ptr(ws), ws.numel(), N.stream_ptr(stream),
+                                            N.stream_ptr(compact_stream)))
     return out
 
 

@@ -97,7 +97,7 @@ int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *b
 int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t image_stride, int n_images, int rr0,
                     int rr1, const mns_enc_cfg *cfg, uint64_t *records, int64_t capacity, int32_t *root_offsets,
                     int64_t *d_count, uint32_t *unit_map, void *workspace, int64_t workspace_bytes,
-                    cudaStream_t stream);
+                    cudaStream_t stream, cudaStream_t cstream);
 int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1, uint32_t *unit_map,
                    cudaStream_t stream);
 int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
@@ -193,7 +193,17 @@ int mns_encode_quadtree(const uint8_t *img, int32_t width, int32_t height, int64
                         int64_t capacity, int32_t *root_offsets, int64_t *d_count, uint32_t *unit_map,
                         void *workspace, int64_t workspace_bytes, void *stream) {
     GUARD(mns::encode_quadtree(img, width, height, pitch, image_stride, n_images, rr0, rr1, cfg, records, capacity,
-                               root_offsets, d_count, unit_map, workspace, workspace_bytes, (cudaStream_t)stream));
+                               root_offsets, d_count, unit_map, workspace, workspace_bytes, (cudaStream_t)stream,
+                               (cudaStream_t)stream));
+}
+
+int mns_encode_quadtree_split(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int64_t image_stride,
+                              int32_t n_images, int32_t rr0, int32_t rr1, const mns_enc_cfg *cfg, uint64_t *records,
+                              int64_t capacity, int32_t *root_offsets, int64_t *d_count, uint32_t *unit_map,
+                              void *workspace, int64_t workspace_bytes, void *stream, void *compact_stream) {
+    GUARD(mns::encode_quadtree(img, width, height, pitch, image_stride, n_images, rr0, rr1, cfg, records, capacity,
+                               root_offsets, d_count, unit_map, workspace, workspace_bytes, (cudaStream_t)stream,
+                               (cudaStream_t)compact_stream));
 }
 
 int mns_try_node(const uint8_t *img, int32_t width, int32_t height, int64_t pitch, int32_t x, int32_t y, int32_t level,

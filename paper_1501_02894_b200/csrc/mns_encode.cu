@@ -758,7 +758,7 @@ int encode_workspace_bytes(int width, int n_images, int rr0, int rr1, int64_t *b
 int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t image_stride, int n_images, int rr0,
                     int rr1, const mns_enc_cfg *cfg, uint64_t *records, int64_t capacity, int32_t *root_offsets,
                     int64_t *d_count, uint32_t *unit_map, void *workspace, int64_t workspace_bytes,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, cudaStream_t cstream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(W <= 65534 && H <= 65534, "dimensions exceed the record coordinate range");
     MNS_CHECK_ARG(pitch >= W && pitch % 16 == 0, "pitch must be >= width and a multiple of 16");
@@ -821,8 +821,15 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     const dim3 grid((unsigned)p.tiles_per_row, (unsigned)p.rows, (unsigned)n_images);
     mns_encode_kernel<<<grid, ET, ENC_SMEM, stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
-    compact_records_kernel<<<(unsigned)ctiles, CT_THREADS, 0, stream>>>(p.stage, root_offsets, n_roots, records,
-                                                                        d_count, status);
+    if (cstream != stream) {  // the compaction on its own stream, after the encoder
+        cudaEvent_t ev;
+        MNS_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        MNS_CUDA_TRY(cudaEventRecord(ev, stream));
+        MNS_CUDA_TRY(cudaStreamWaitEvent(cstream, ev, 0));
+        MNS_CUDA_TRY(cudaEventDestroy(ev));
+    }
+    compact_records_kernel<<<(unsigned)ctiles, CT_THREADS, 0, cstream>>>(p.stage, root_offsets, n_roots, records,
+                                                                         d_count, status);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -635,3 +635,21 @@ def test_encode_stress_golden(mns, golden):
         assert np.array_equal(code.records, g[f"{k}/records"]), case
         got = mns.decode(code, mns.DecodeConfig(max_iters=8, stop_delta=0.0)).pixels
         assert int(np.abs(got.astype(int) - g[f"{k}/decode8"].astype(int)).max()) <= 1, case
+
+
+def test_encode_split_stream_compaction(mns):
+    """mns_encode_quadtree_split (compaction on a second stream, joined by the caller) yields the same
+    records, root offsets and unit map as the single-stream encode."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = torch.from_numpy(synth_image(512, 31, noise_sigma=10.0, n_blobs=8)).cuda()
+    cfg = mns.EncoderConfig(e3=math.inf)
+    a = mns.encode_device(px, cfg)
+    side = torch.cuda.Stream()
+    b = mns.encode_device(px, cfg, compact_stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    n = a.n_records()
+    assert n == b.n_records()
+    assert torch.equal(a.records[:n], b.records[:n])
+    assert torch.equal(a.root_offsets, b.root_offsets)
+    assert torch.equal(a.unit_map, b.unit_map)
