@@ -425,6 +425,22 @@ def run_ours(args, img_np, rank, world, local_rank):
             fs[f"iso{n_iso}"] = {"config": f"c4 512^2 B=8 stride 1, {n_iso} isometr{'y' if n_iso == 1 else 'ies'}",
                                  "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3),
                                  "effective_tflops": 2 * 64 * pairs / (ms / 1e3) / 1e12}
+        for radius in (4, 32):  # encoder.py:312-347 local search (+-4; +-32 is the config-c4 extension)
+            for _ in range(2):
+                mns.local_search_device(c4, radius)
+            torch.cuda.synchronize()
+            runs = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                mns.local_search_device(c4, radius)
+                b.record()
+                torch.cuda.synchronize()
+                runs.append(a.elapsed_time(b))
+            ms = float(np.median(runs))
+            cands = 4096 * (2 * radius + 1) ** 2
+            fs[f"local{radius}"] = {"config": f"c4 512^2 B=8 local search +-{radius} (identity)",
+                                    "candidate_fits": cands, "ms": ms, "candidate_fits_per_s": cands / (ms / 1e3)}
 
     small = None if args.no_small else small_configs(dev, rank, world)
 
