@@ -476,7 +476,9 @@ def run_ours(args, img_np, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic(kname) if world == 1 else None,
                      "algorithmic_bytes": algo, "kernel": f"{kname} (steady-state pass = 2 sweeps)",
-                     "peak_source": which},
+                     "peak_source": which,
+                     "limiter": ("instruction issue (ncu: ~79% issue-active at 2 B/px of DRAM traffic; "
+                                 "profiles/r1/ncu_step_lattice.txt)") if dec.lattice else "latency"},
         "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
                           "sample": f"c5 rows 0..{args.cpu_baseline_rows - 1} encoded + {ITERS}-sweep decoded as its own "
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
