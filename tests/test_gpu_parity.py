@@ -653,3 +653,28 @@ def test_encode_split_stream_compaction(mns):
     assert torch.equal(a.records[:n], b.records[:n])
     assert torch.equal(a.root_offsets, b.root_offsets)
     assert torch.equal(a.unit_map, b.unit_map)
+
+
+@pytest.mark.parametrize("H,W", [(96, 32768), (20000, 48), (272, 2064)])
+def test_lattice_decode_extreme_shapes(mns, H, W):
+    """Very wide and very tall images (hundreds of column bands / one partial band, many row
+    chunks): lattice-state decode equals the raster decode bit for bit."""
+    import ctypes
+
+    from paper_1501_02894_b200 import _native as N
+
+    L = N.lib()
+    rng = np.random.default_rng(H + W)
+    base = rng.integers(60, 200, (H // 8 + 1, W // 8 + 1))
+    px = np.kron(base, np.ones((8, 8)))[:H, :W] + rng.integers(-12, 13, (H, W))
+    px = np.ascontiguousarray(np.clip(px, 0, 255).astype(np.uint8))
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+    got, _, _ = mns.decode_device(code, iters=6)
+    ras = [torch.empty((H, W), device="cuda") for _ in range(2)]
+    want = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, 6, 0.0, 128.0,
+                                  N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
