@@ -39,19 +39,14 @@ def resident_rows(r0: int, r1: int, height: int, halo: int = HALO) -> tuple[int,
     return max(0, 16 * r0 - halo), min(height, 16 * r1 + halo)
 
 
-def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None,
-                   halo: int = HALO, row_div: int = 1) -> None:
-    """After a sweep: send my first/last `halo` own rows to the neighbours, receive theirs into my halos.
-
-    ``raster`` holds rows [y_lo, y_hi) (resident_rows with the same halo) of the full image, or with
-    row_div = 2 the lattice rows [y_lo/2, y_hi/2) of lattice-state decoding (one lattice row per two
-    raster rows; halo/2 rows exchanged).  Works for any torch.distributed backend (NCCL on GPUs,
-    gloo on CPU).
-    """
+def halo_ops(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None, halo: int = HALO,
+             row_div: int = 1) -> list:
+    """The point-to-point operations of one halo exchange (see exchange_halos); reusable as long as
+    ``raster`` is the same tensor."""
     import torch.distributed as dist
 
     if world == 1:
-        return
+        return []
     if 16 * (r1 - r0) < halo:
         raise ValueError(f"strip of {16 * (r1 - r0)} rows is thinner than the {halo}-row halo")
     y_lo, y_hi = resident_rows(r0, r1, height, halo)
@@ -63,8 +58,28 @@ def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int,
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, raster[own1 - hl: own1], rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, raster[own1: own1 + hl], rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+    return ops
+
+
+def run_ops(ops) -> None:
+    """Issue a batch of point-to-point operations and wait for them (stream-ordered on NCCL)."""
+    import torch.distributed as dist
+
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def exchange_halos(raster, r0: int, r1: int, height: int, rank: int, world: int, group=None,
+                   halo: int = HALO, row_div: int = 1) -> None:
+    """After a sweep: send my first/last `halo` own rows to the neighbours, receive theirs into my halos.
+
+    ``raster`` holds rows [y_lo, y_hi) (resident_rows with the same halo) of the full image, or with
+    row_div = 2 the lattice rows [y_lo/2, y_hi/2) of lattice-state decoding (one lattice row per two
+    raster rows; halo/2 rows exchanged).  Works for any torch.distributed backend (NCCL on GPUs,
+    gloo on CPU).
+    """
+    run_ops(halo_ops(raster, r0, r1, height, rank, world, group, halo, row_div))
 
 
 def unit_map_rows(r0: int, r1: int, height: int) -> tuple[int, int]:
@@ -72,15 +87,12 @@ def unit_map_rows(r0: int, r1: int, height: int) -> tuple[int, int]:
     return max(0, r0 - 1), min(height // 16, r1 + 1)
 
 
-def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> None:
-    """Swap the boundary root rows of the decoder unit map with the neighbours (once per code).
-
-    ``umap`` is [u1 - u0, W/16 * 32] int32 (unit_map_rows); own rows are [r0 - u0, r1 - u0).
-    """
+def unit_map_ops(umap, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> list:
+    """The point-to-point operations of exchange_unit_map_rows (reusable for the same tensor)."""
     import torch.distributed as dist
 
     if world == 1:
-        return
+        return []
     u0, _ = unit_map_rows(r0, r1, height)
     own0, own1 = r0 - u0, r1 - u0
     ops = []
@@ -90,8 +102,15 @@ def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, umap[own1 - 1], rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, umap[own1], rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+    return ops
+
+
+def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> None:
+    """Swap the boundary root rows of the decoder unit map with the neighbours (once per code).
+
+    ``umap`` is [u1 - u0, W/16 * 32] int32 (unit_map_rows); own rows are [r0 - u0, r1 - u0).
+    """
+    run_ops(unit_map_ops(umap, r0, r1, height, rank, world, group))
 
 
 def gather_codes(records, count: int, root_offsets, rank: int, world: int, dst: int = 0, group=None):
@@ -179,6 +198,7 @@ class StripDecoder:
         own = self.umap[r0 - self.u0: r1 - self.u0]
         own.copy_(code.unit_map.view(r1 - r0, rw32))
         code.unit_map = own.view(-1)
+        self._ops = {}
 
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
@@ -196,8 +216,11 @@ class StripDecoder:
         return iters // 2 + (iters & 1)
 
     def _exchange(self, t):
-        exchange_halos(t, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO,
-                       row_div=2 if self.lattice else 1)
+        key = id(t)
+        if key not in self._ops:  # the P2P descriptors of each resident state tensor are built once
+            self._ops[key] = halo_ops(t, self.r0, self.r1, self.H, self.rank, self.world, halo=DEC_HALO,
+                                      row_div=2 if self.lattice else 1)
+        run_ops(self._ops[key])
 
     def run(self, iters: int = 10, initial_value: float = 128.0, stream=None, sweep_events=None, out=None):
         """iters sweeps (stop_delta = 0); the last pass writes the rounded uint8 strip into `out` (default self.out).
@@ -211,7 +234,9 @@ class StripDecoder:
             raise ValueError("max_iters must be >= 1")
         L = N.lib()
         s = N.stream_ptr(stream)
-        exchange_unit_map_rows(self.umap, self.r0, self.r1, self.H, self.rank, self.world)
+        if "umap" not in self._ops:
+            self._ops["umap"] = unit_map_ops(self.umap, self.r0, self.r1, self.H, self.rank, self.world)
+        run_ops(self._ops["umap"])
         ob = self._vbase(out, 16 * self.r0, 1)
         cur, it, n = None, 0, 0
         if iters & 1:  # odd count: the flat first sweep alone
