@@ -1,28 +1,34 @@
 // tcgen05 tensor-core full search (K3) for B in {2, 4, 8} on sm_100a.
 //
-// Replaces encoder.py:249-309 (encode_full_search).  The range x domain cross
-// products C = sum_k q_d[k] r_row[k] run as an FP16 x FP16 -> FP32 UMMA GEMM that
-// is exact (q <= 1020, r <= 255, B^2 <= 64: every partial sum is an integer < 2^24).
-// rows = (range, isometry) pairs (M, 128 per CTA tile), columns = domains
-// (N = 128 per MMA tile), K = 64 (zero-padded for B < 8).
+// Replaces encoder.py:249-309 (encode_full_search).  rows = (range, isometry) pairs (M, 128 per
+// MMA, two M halves per CTA), columns = domains (N = 128 per tile), K = 64 (zero-padded for B < 8).
 //
-// Warp roles (20 warps): w0 TMA producer (A once, B tiles through a 4-stage
-// ring, 128B-swizzled K-major), w1 single-thread MMA issuer (4 x K=16 per tile
-// into one of two 256-column TMEM accumulators), w2 TMEM allocator, w3 column-
-// constant producer (4-deep ring), w4..w19 epilogue: each thread owns one TMEM
-// lane (= one range row) and half of the 128 columns.
+// The GEMM produces, per (row, domain), the quantity the argmin filter needs:
+//   x = sum_k (r_k - Sr/n) * (q_k - Sq/n) / sqrt(D) = N / (n sqrt D),   N = n C - Sq Sr,
+// with both operands centred and the domain operand scaled by 1/sqrt(D), each rounded once to
+// fp16 (FP16 x FP16 -> FP32 UMMA).  The reference's per-domain value is
+//   1024 n SSE - 1024 n A = min over odd k2 in [-7, 7] of  k2^2 D - 64 k2 N,
+// whose continuous relaxation is -1024 N^2 / D = -1024 n^2 x^2: against the row's running exact
+// best V*, an element can only win if |x| >= scl = sqrt(-V*/1024) / n.  The computed x differs
+// from the true one by at most e_row = 2^-9 * max_k |r_k - Sr/n| (fp16 rounding of both operands:
+// sum_k |q_k - Sq/n| / sqrt(D) <= 1 by Cauchy-Schwarz, so each costs <= 2^-11 max|r_c|; the fp32
+// accumulation < 2^-16 of it; a ~2x safety factor on top), a per-ROW constant.  So level 1 is one
+// |max| per element against one per-row threshold (FMNMX3 over two elements).  Survivors (voted
+// per 16-column group) pass a rigorous fp32 lower bound of the quantised value (level 2); the
+// rest are evaluated exactly in int64 from the pooled integer q and the raw range row (level 3)
+// and folded into the row's lexicographic (value, index) key, shared across CTAs by atomicMin.
+// A prepass over a 1/128 domain sample, seeded with 5 nearby domains per range, sets the
+// thresholds; constant ranges (N == 0 for every domain) take the precomputed argmin of D.
 //
-// Epilogue (exact): the reference's per-domain SSE is
-//   1024 n SSE = 1024 n A - 64 k2 N + k2^2 D,  N = n C - Sq Sr,
-// minimised over the odd k2 in [-7, 7]; its continuous relaxation gives the lower
-// bound -1024 N^2 / D.  Against the row's running exact best V* an element can
-// only win if |N/n| >= sqrt(-V*/1024)/n * sqrt(D); with N/n = C - Sq*Sr/n that test is
-// 2 FFMA + 1 FMNMX per element.  Survivors (voted per column across the warp) pass
-// a rigorous fp32 lower bound of the quantised value; the rest are evaluated exactly
-// in int64 from C and the tile's staged (Sq, D) and folded into the row's
-// lexicographic (value, index) key.  A prepass over a 1/64 domain sample seeds the
-// per-range bests (shared through global keys) so few candidates are ever exact-evaluated.
-// Constant ranges (N == 0 for every domain) take the precomputed argmin of D.
+// Persistent CTAs (one per SM): CTA b owns a contiguous, equal share of the (M tile, domain tile)
+// units in M-major order, so every SM streams the same number of tiles and pays the prologue
+// once.  The range operand of consecutive M tiles is double-buffered in shared memory.
+//
+// Warp roles (20 warps): w0 TMA producer (A per M tile, B tiles through a 4-stage 128B-swizzled
+// ring), w1 single-thread MMA issuer (2 M halves x 4 K=16 steps per tile into one of two
+// 256-column TMEM accumulators), w2 TMEM allocator, w3 column-constant producer (4-deep ring),
+// w4..w19 epilogue: each thread owns one TMEM lane (= one row) and half of the 128 columns; it
+// loads its 64 accumulator columns, releases the accumulator, then filters from registers.
 
 #include <cuda_fp16.h>
 #include <math.h>
@@ -33,7 +39,7 @@
 namespace mns {
 
 #ifdef MNS_TC_STATS
-__device__ unsigned long long g_tc_stats[4];  // chunks, level-1 passes, level-2 entries, exact evaluations
+__device__ unsigned long long g_tc_stats[4];  // 16-col groups, level-1 group passes, level-2 entries, exact evaluations
 #endif
 
 namespace {
@@ -44,23 +50,33 @@ constexpr int MH = 2;                         // M halves per CTA: 256 rows shar
 constexpr int STAGES = 4;
 constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
 constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;  // 640
-constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB
+constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB per A buffer (two buffers)
 constexpr int B_BYTES = BN * BK * 2;          // 16 KB
-constexpr int CONST_BYTES = BN * 16;          // -Sq, sqrt(D) (planar floats) + exact D per column
 constexpr int TMEM_COLS = 2 * MH * BN;        // 2 accumulator stages x 2 M halves x 128 columns = 512
-constexpr int NCB = 4;                        // column-constant buffers (streamed by their own warp)
-constexpr int SMEM_BYTES = 1024 + A_BYTES + STAGES * B_BYTES + NCB * CONST_BYTES + 512;
+constexpr int EPI_COLS = BN / 2;              // columns per epilogue thread per tile
+constexpr int GRP = 16;                       // level-1 vote group (columns)
+constexpr int NCB = 4;                        // column-constant ring slots
+constexpr int CONST_BYTES = BN * 16;          // per tile: 128 x -Sq, 128 x sqrt_rd(D) (floats), 128 x D (int64)
+constexpr int QSIZE = 1024;                   // exact-evaluation queue entries (16 B each)
+constexpr int CONST_OFF = 2 * A_BYTES + STAGES * B_BYTES + 512;
+constexpr int QUEUE_OFF = CONST_OFF + NCB * CONST_BYTES;
+constexpr int STASH_OFF = QUEUE_OFF + QSIZE * 16;  // per epilogue warp: [GRP][32] floats
+constexpr int SMEM_BYTES = 1024 + STASH_OFF + EPI_WARPS * GRP * 32 * 4;
 
 struct TcParams {
     int n_rows;          // (r1 - r0) * n_iso
     int n_iso, r0, n;    // n = B*B
     long long ndom;
-    int dtiles_per_chunk, n_dtiles;
-    int dstride;                 // domain of column c of tile t: ((dt0 + t) * BN + c) * dstride
+    int n_dt;            // domain tiles in this launch
+    long long n_units;   // M tiles x n_dt
+    int dstride;                 // domain of column c of tile t: (t * BN + c) * dstride
     const float2 *consts;        // per 128-domain tile: 128 floats -Sq, then 128 floats sqrt_rd(D)
     const long long *pD;         // exact D
+    const uint16_t *pool;        // [ndom][n] pooled q (exact recompute of C)
+    const __half *araw;          // [n_rows_pad][BK] raw range rows (r per isometry, exact)
     const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range
     const int32_t *row_flat;     // [n_rows_pad] 1 if the range is constant (N == 0 for every domain)
+    const float *row_err;        // [n_rows_pad] e_row
     const unsigned long long *flat_key;  // argmin-D key for constant ranges
     unsigned long long *best;    // [r1 - r0]
 };
@@ -86,6 +102,37 @@ __device__ __forceinline__ long long best_val_exact(long long N, long long D) {
     return best;
 }
 
+// exact C = sum_k q_k r_k of domain d and range row `row`: the pooled q row (u16) and the raw
+// fp16 range row read as 16-byte vectors, all loads issued before the integer dot product
+__device__ __noinline__ long long exact_cross(const uint16_t *pool, const __half *araw, int n, long long d, int row) {
+    const uint16_t *qd = pool + d * n;
+    const __half *ar = araw + (size_t)row * BK;
+    long long C = 0;
+    if (n == 64) {
+        uint4 qv[8], av[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            qv[i] = __ldg(reinterpret_cast<const uint4 *>(qd) + i);
+            av[i] = __ldg(reinterpret_cast<const uint4 *>(ar) + i);
+        }
+        int acc = 0;  // < 64 * 1020 * 255 < 2^24
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t qw[4] = {qv[i].x, qv[i].y, qv[i].z, qv[i].w};
+            const uint32_t aw[4] = {av[i].x, av[i].y, av[i].z, av[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const __half2 h = *reinterpret_cast<const __half2 *>(&aw[j]);
+                acc += (int)(qw[j] & 0xFFFF) * __half2int_rn(__low2half(h)) +
+                       (int)(qw[j] >> 16) * __half2int_rn(__high2half(h));
+            }
+        }
+        return acc;
+    }
+    for (int k = 0; k < n; k++) C += (long long)qd[k] * (long long)__half2int_rn(ar[k]);
+    return C;
+}
+
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     // K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (1), version 1
     return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -106,18 +153,18 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                  : "memory");
 }
 
-constexpr int CH = 16;  // accumulator columns per TMEM load
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[CH]) {
-    uint32_t r[CH];
+// 16 accumulator columns of this warp's 32 TMEM lanes (no wait)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+    uint32_t r[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < CH; i++) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -125,8 +172,6 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // 1D bulk copy global -> shared completing on an mbarrier (size multiple of 16 B)
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -136,35 +181,66 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// mbarrier wait without a suspend-time hint: the try_wait loop never drops into a long
+// NANOSLEEP, so a waiter resumes as soon as the phase completes (the MMA <-> epilogue handshake
+// sits on the critical path of every tile)
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// mbarrier wait with a short (~0.2 us) suspend-time hint, for producers that are not on the
+// critical path
+__device__ __forceinline__ void mbar_wait_ns(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 200;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// max(|a|, |b|, m): one FMNMX3 with |.| operand modifiers
+__device__ __forceinline__ float absmax3(float m, float a, float b) { return fmaxf(m, fmaxf(fabsf(a), fabsf(b))); }
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     full_search_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const TcParams p) {
     extern __shared__ __align__(1024) unsigned char tsm_raw[];
     // 1024-B aligned base as an offset from the shared array (keeps shared-space addressing: LDS, not LD.E)
     unsigned char *tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
-    unsigned char *sA = tsm;
-    unsigned char *sB = tsm + A_BYTES;
-    float2 *sL = reinterpret_cast<float2 *>(tsm + A_BYTES + STAGES * B_BYTES);              // [NCB][BN] -Sq | sqrt D
-    long long *sD = reinterpret_cast<long long *>(tsm + A_BYTES + STAGES * B_BYTES + NCB * BN * 8);  // [NCB][BN] D
-    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + A_BYTES + STAGES * B_BYTES + NCB * CONST_BYTES);
-    uint64_t *full_bar = bars, *empty_bar = bars + STAGES, *a_bar = bars + 2 * STAGES;
-    uint64_t *tfull = bars + 2 * STAGES + 1, *tempty = bars + 2 * STAGES + 3;
-    uint64_t *cfull = bars + 2 * STAGES + 5, *cempty = bars + 2 * STAGES + 5 + NCB;  // column-constant ring
-    uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 5 + 2 * NCB);
+    unsigned char *sA = tsm;                    // [2][A_BYTES]
+    unsigned char *sB = tsm + 2 * A_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + 2 * A_BYTES + STAGES * B_BYTES);
+    uint64_t *full_bar = bars, *empty_bar = bars + STAGES;
+    uint64_t *a_full = bars + 2 * STAGES, *a_empty = bars + 2 * STAGES + 2;
+    uint64_t *tfull = bars + 2 * STAGES + 4, *tempty = bars + 2 * STAGES + 6;
+    uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 8);
+    uint32_t *q_head = tmem_base_sh + 1, *q_tail = tmem_base_sh + 2, *q_done = tmem_base_sh + 3;
+    uint64_t *cfull = bars + 2 * STAGES + 10, *cempty = bars + 2 * STAGES + 10 + NCB;  // column-constant ring
+    unsigned char *queue = tsm + QUEUE_OFF;
+    unsigned char *sC = tsm + CONST_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m_tile = blockIdx.y;
-    const int dt0 = blockIdx.x * p.dtiles_per_chunk;
-    const int dt1 = min(p.n_dtiles, dt0 + p.dtiles_per_chunk);
-    const int ntiles = dt1 - dt0;
+    // this CTA's contiguous share of the (M tile, domain tile) units, M-major
+    const long long u0 = p.n_units * blockIdx.x / gridDim.x, u1 = p.n_units * (blockIdx.x + 1) / gridDim.x;
+    const int ntiles = (int)(u1 - u0);
+    const int m_first = (int)(u0 / p.n_dt), dt_first = (int)(u0 % p.n_dt);  // then walked incrementally
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
-        mbar_init(a_bar, 1);
         for (int a = 0; a < 2; a++) {
+            mbar_init(&a_full[a], 1);
+            mbar_init(&a_empty[a], 1);
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], EPI_WARPS);
         }
@@ -172,6 +248,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&cfull[a], 1);
             mbar_init(&cempty[a], EPI_WARPS);
         }
+        *q_head = 0;
+        *q_tail = 0;
+        *q_done = 0;
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -180,51 +259,55 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    for (int i = threadIdx.x; i < QSIZE; i += NTHREADS) reinterpret_cast<uint4 *>(queue)[i].w = 0;  // no slot ready
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_base_sh;
 
     if (warp == 0) {
-        // ===== TMA producer
+        // ===== TMA producer: the A operand of every new M tile into the other A buffer, B tiles.
+        // Its waits sleep briefly (a 4-deep ring): spinning would steal issue slots from the
+        // epilogue warps on the same scheduler.
         if (lane == 0) {
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
-            mbar_arrive_expect_tx(a_bar, A_BYTES);
-            for (int h = 0; h < MH; h++) tma_load_2d(sA + h * BM * BK * 2, &tmA, 0, (m_tile * MH + h) * BM, a_bar);
-            for (int t = 0; t < ntiles; t++) {
+            int seg = -1, cur_m = -1;
+            for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+                if (m != cur_m) {
+                    cur_m = m;
+                    seg++;
+                    const int ab = seg & 1;
+                    if (seg >= 2) mbar_wait_ns(&a_empty[ab], ((seg >> 1) - 1) & 1);
+                    mbar_arrive_expect_tx(&a_full[ab], A_BYTES);
+                    for (int h = 0; h < MH; h++)
+                        tma_load_2d(sA + ab * A_BYTES + h * BM * BK * 2, &tmA, 0, (m * MH + h) * BM, &a_full[ab]);
+                }
                 const int s = t % STAGES;
-                if (t >= STAGES) mbar_wait(&empty_bar[s], ((t / STAGES) - 1) & 1);
+                if (t >= STAGES) mbar_wait_ns(&empty_bar[s], ((t / STAGES) - 1) & 1);
                 mbar_arrive_expect_tx(&full_bar[s], B_BYTES);
-                tma_load_2d(sB + s * B_BYTES, &tmB, 0, (dt0 + t) * BN, &full_bar[s]);
-            }
-        }
-    } else if (warp == 3) {
-        // ===== column constants of tile t into ring slot t % NCB, decoupled from the B tiles (with
-        // one producer for both, B(t) waited on the epilogue releasing the constants of tile t - 2)
-        if (lane == 0) {
-            for (int t = 0; t < ntiles; t++) {
-                const int cb = t % NCB;
-                if (t >= NCB) mbar_wait(&cempty[cb], ((t / NCB) - 1) & 1);
-                mbar_arrive_expect_tx(&cfull[cb], BN * 16);
-                const long long b0 = (long long)(dt0 + t) * BN;
-                bulk_g2s(sL + cb * BN, p.consts + b0, BN * 8, &cfull[cb]);
-                bulk_g2s(sD + cb * BN, p.pD + b0, BN * 8, &cfull[cb]);
+                tma_load_2d(sB + s * B_BYTES, &tmB, 0, dt * BN, &full_bar[s]);
             }
         }
     } else if (warp == 1) {
         // ===== MMA issuer (one thread)
         if (lane == 0) {
-            // instruction descriptor: F32 accumulate, F16 A/B, K-major both, N = 256, M = 128
+            // instruction descriptor: F32 accumulate, F16 A/B, K-major both, N = BN, M = 128
             const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                    ((uint32_t)(BM >> 4) << 24);
-            mbar_wait(a_bar, 0);
-            tc_fence_after();
-            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
-            for (int t = 0; t < ntiles; t++) {
+            int seg = -1, cur_m = -1;
+            uint64_t adesc0 = 0;
+            for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+                if (m != cur_m) {
+                    cur_m = m;
+                    seg++;
+                    mbar_spin(&a_full[seg & 1], (seg >> 1) & 1);
+                    tc_fence_after();
+                    adesc0 = umma_desc_sw128(smem_u32(sA + (seg & 1) * A_BYTES));
+                }
                 const int s = t % STAGES, acc = t & 1;
-                if (t >= 2) mbar_wait(&tempty[acc], ((t / 2) - 1) & 1);
-                mbar_wait(&full_bar[s], (t / STAGES) & 1);
+                if (t >= 2) mbar_spin(&tempty[acc], ((t / 2) - 1) & 1);
+                mbar_spin(&full_bar[s], (t / STAGES) & 1);
                 tc_fence_after();
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + s * B_BYTES));
 #pragma unroll
@@ -236,136 +319,224 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 umma_commit(&empty_bar[s]);  // frees the B stage when these MMAs complete
                 umma_commit(&tfull[acc]);    // accumulator ready for the epilogue
+                const bool seg_end = t + 1 == ntiles || dt + 1 == p.n_dt;
+                if (seg_end) umma_commit(&a_empty[seg & 1]);  // A buffer reusable once these complete
+            }
+        }
+    } else if (warp == 2) {
+        // ===== column constants of tile t into ring slot t % NCB (read only on the rare level-2 path)
+        if (lane == 0) {
+            for (int t = 0, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1) {
+                const int cb = t % NCB;
+                if (t >= NCB) {  // the slot's previous copy has landed and every epilogue warp is done with it
+                    mbar_wait_ns(&cfull[cb], ((t / NCB) - 1) & 1);
+                    mbar_wait_ns(&cempty[cb], ((t / NCB) - 1) & 1);
+                }
+                mbar_arrive_expect_tx(&cfull[cb], CONST_BYTES);
+                const long long b0 = (long long)dt * BN;
+                bulk_g2s(sC + cb * CONST_BYTES, p.consts + b0, BN * 8, &cfull[cb]);
+                bulk_g2s(sC + cb * CONST_BYTES + BN * 8, p.pD + b0, BN * 8, &cfull[cb]);
+            }
+        }
+    } else if (warp == 3) {
+        // ===== exact warp: pops the candidates that passed levels 1 and 2 (one per lane) and
+        // evaluates them exactly in int64 from the pooled q and the raw range row; improvements go
+        // to the global keys (atomicMin), which every epilogue lane polls.  The epilogue never waits
+        // on these global round trips.
+        uint32_t tail = 0;
+        for (;;) {
+            const uint32_t head = *(volatile uint32_t *)q_head;
+            if (head == tail) {
+                if (*(volatile uint32_t *)q_done == EPI_WARPS && *(volatile uint32_t *)q_head == tail) break;
+                __nanosleep(100);
+                continue;
+            }
+            const uint32_t cnt = min(head - tail, 32u);
+            uint32_t code = 0, m = 0, dt = 0;
+            if (lane < cnt) {
+                const uint32_t slot = tail + lane;
+                volatile uint4 *e = reinterpret_cast<volatile uint4 *>(queue) + (slot % QSIZE);
+                while (e->w != slot + 1) {
+                }
+                code = e->x;
+                m = e->y;
+                dt = e->z;
+            }
+            __syncwarp();
+            tail += cnt;
+            if (lane == 0) *(volatile uint32_t *)q_tail = tail;  // slots free once read
+            if (lane < cnt) {
+                const int col = (int)(code & 0xFF), rl = (int)(code >> 8);
+                const int row = (int)m * (MH * BM) + rl;
+                const int rr = row / p.n_iso, iso = row % p.n_iso;
+                const long long dcol = (long long)dt * BN + col;
+                const long long d = dcol * p.dstride;
+                const float *lq = reinterpret_cast<const float *>(p.consts + (long long)dt * BN);  // -Sq | sqrt_rd(D)
+                const long long C = exact_cross(p.pool, p.araw, p.n, d, row);
+                const long long N = (long long)p.n * C - (long long)(int)(-__ldg(lq + col)) * p.row_sr[row];
+                const unsigned long long key = make_key(best_val_exact(N, __ldg(p.pD + dcol)), d * p.n_iso + iso);
+#ifdef MNS_TC_STATS
+                atomicAdd(&g_tc_stats[3], 1ull);
+#endif
+                atomicMin(&p.best[rr], key);
             }
         }
     } else if (warp >= EPI_WARP0) {
-        // ===== epilogue: one TMEM lane (= range row) per thread, half of the columns per warp pair
+        // ===== epilogue: one TMEM lane (= row) per thread, half of the columns per warp
         const int ew = warp - EPI_WARP0;       // 0..15
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
         const int mh = (ew >> 2) & 1;          // M half
         const int half = ew >> 3;              // column half (0: 0..63, 1: 64..127)
-        const int row = (m_tile * MH + mh) * BM + quarter * 32 + lane;
-        const bool active = row < p.n_rows;
-        const int sr = active ? p.row_sr[row] : 0;
-        const bool flat = active ? p.row_flat[row] != 0 : true;
-        const int iso = row % p.n_iso;
-        const float sr_n = (float)sr / (float)p.n;  // exact (n is a power of two)
-        const float err = 2.f;          // |fl(C - Sq*Sr/n) - N/n| <= 2 (one FMA rounding, |N/n| < 2^25)
-        const float slack = err + 4.f;  // plus the rounding of the test's own FFMA
-        unsigned long long best = ~0ull;
-        long long vstar = LLONG_MAX;   // threshold: best exact value known for this range (any row / CTA)
-        float scl = 0.f;               // sqrt(-V*/1024)/n rounded down; 0 = no skipping
-        const int rr = row / p.n_iso;
+        const int rl = mh * BM + quarter * 32 + lane;  // row within the M tile
+        float *stash = reinterpret_cast<float *>(tsm + STASH_OFF) + ew * (GRP * 32);  // [GRP][32] per warp
         const float n64 = -64.f * (float)p.n;
         const float inv_n = 1.0f / (float)p.n;  // exact (power of two)
+        int cur_m = -1, rr = 0;
+        bool live = false;
+        float erow = 0.f, thr = -1.f;
+        long long vstar = LLONG_MAX;  // an upper bound of this range's best value (a real candidate's)
         auto set_threshold = [&](long long v) {
             if (v < vstar) {
                 vstar = v;
-                // LB = -1024 N^2 / D > V*  <=>  |N/n| < sqrt(-V*/1024)/n * sqrt(D)  (rounded down)
-                scl = v < 0 ? __fmul_rd(__fsqrt_rd(__fmul_rd(__ll2float_rd(-v), 0.999f / 1024.f)), inv_n) : 0.f;
+                // -1024 n^2 x^2 > V*  <=>  |x| < sqrt(-V*/1024)/n  (scl rounded down, thr = scl - e_row)
+                thr = v < 0 ? __fsub_rd(__fmul_rd(__fsqrt_rd(__fmul_rd(__ll2float_rd(-v), 0.999f / 1024.f)), inv_n),
+                                        erow)
+                            : -1.f;
             }
         };
-        // column constants of tile t arrive in sL/sD[t % NCB] through warp 3's bulk copies (cfull)
-        unsigned long long g = (active && !flat) ? *((volatile unsigned long long *)&p.best[rr]) : ~0ull;
-        for (int t = 0; t < ntiles; t++) {
+        unsigned long long g = ~0ull;
+        for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+            if (m != cur_m) {  // new M tile: load the row
+                cur_m = m;
+                const int row = m * (MH * BM) + rl;
+                const bool active = row < p.n_rows;
+                const bool flat = active ? p.row_flat[row] != 0 : true;
+                live = active && !flat;
+                rr = row / p.n_iso;
+                if (active && flat && row % p.n_iso == 0 && half == 0) atomicMin(&p.best[rr], *p.flat_key);
+                erow = live ? p.row_err[row] : 0.f;
+                vstar = LLONG_MAX;
+                thr = -1.f;
+                g = live ? ld_relaxed_u64(&p.best[rr]) : ~0ull;
+            }
             const int acc = t & 1, cbuf = t % NCB;
-            const long long dbase = (long long)(dt0 + t) * BN;
-            // share the running best: other CTAs' results for this range (global keys, polled one tile
-            // ahead) and the other isometry rows of the same range (adjacent lanes)
+            // the range's running best from every CTA's exact warp (global key, loaded a tile ahead)
             if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
-            g = (active && !flat && t + 1 < ntiles) ? *((volatile unsigned long long *)&p.best[rr]) : ~0ull;
-            mbar_wait(&cfull[cbuf], (t / NCB) & 1);
-            mbar_wait(&tfull[acc], (t >> 1) & 1);
-            tc_fence_after();
-            if ((t & 3) == 0) {
+            if ((t & 3) == 0) {  // and the other isometry rows of the range (adjacent lanes)
                 for (int o = 1; o < p.n_iso; o <<= 1) {
                     const long long other = __shfl_xor_sync(FULL, vstar, o);
-                    if (active && !flat) set_threshold(other);
+                    if (live) set_threshold(other);
                 }
             }
-#pragma unroll 1
-            for (int ch = 0; ch < BN / 2 / CH; ch++) {
-                const int col0 = half * (BN / 2) + ch * CH;
-                float c[CH];
-                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MH + mh) * BN + col0, c);
-#ifdef TC_EXP
-                if (TC_EXP == 2) continue;
-#endif
-                const bool live = active && !flat;
-                // level 1: continuous lower bound, 2 FFMA + FMNMX per element
-                float mm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent max chains
-                const float *lq = reinterpret_cast<const float *>(&sL[cbuf * BN]) + col0;  // -Sq
-                const float *ld = lq + BN;                                                   // sqrt D
-                const float2 srn2 = make_float2(sr_n, sr_n);
+            mbar_spin(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            g = live ? ld_relaxed_u64(&p.best[rr]) : ~0ull;
+            float c[EPI_COLS];
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MH + mh) * BN + half * EPI_COLS;
 #pragma unroll
-                for (int j = 0; j < CH; j += 4) {
-                    const float4 nq = *reinterpret_cast<const float4 *>(lq + j);
-                    const float4 sd = *reinterpret_cast<const float4 *>(ld + j);
-                    // n1 = C - Sq*Sr/n for two columns per FFMA2 (same rounding as fmaf)
-                    const float2 n01 = ffma2_rn(make_float2(nq.x, nq.y), srn2, make_float2(c[j], c[j + 1]));
-                    const float2 n23 = ffma2_rn(make_float2(nq.z, nq.w), srn2, make_float2(c[j + 2], c[j + 3]));
-                    mm[(j >> 2) & 1] = fmaxf(mm[(j >> 2) & 1], fmaxf(fmaf(-scl, sd.x, fabsf(n01.x)),
-                                                                     fmaf(-scl, sd.y, fabsf(n01.y))));
-                    mm[2 + ((j >> 2) & 1)] = fmaxf(mm[2 + ((j >> 2) & 1)], fmaxf(fmaf(-scl, sd.z, fabsf(n23.x)),
-                                                                                 fmaf(-scl, sd.w, fabsf(n23.y))));
-                }
-                const bool chunk_pass = live && fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])) >= -slack;
-#ifdef MNS_TC_STATS
-                if (lane == 0) atomicAdd(&g_tc_stats[0], 1ull);
-#endif
-                if (!__any_sync(FULL, chunk_pass)) continue;  // the common case: nobody can win here
-#ifdef MNS_TC_STATS
-                if (lane == 0) atomicAdd(&g_tc_stats[1], 1ull);
-#endif
-#ifdef TC_EXP
-                if (TC_EXP == 1) { if (mm[0] == 12345.f) best = 0; continue; }
-#endif
-                // level 2 per column, only for the (lane, column) pairs that pass level 1: a rigorous
-                // lower bound of the quantised value over every odd k2 with |n1 - N/n| <= err; level 3: exact
-#pragma unroll
-                for (int j = 0; j < CH; j++) {
-                    const float nsq = lq[j], sqd = ld[j];  // -Sq, sqrt D
-                    const float n1 = fmaf(nsq, sr_n, c[j]);
-                    const bool pj = chunk_pass && fmaf(-scl, sqd, fabsf(n1)) >= -slack;
-                    if (!__any_sync(FULL, pj)) continue;
-                    if (!pj) continue;
-#ifdef MNS_TC_STATS
-                    atomicAdd(&g_tc_stats[2], 1ull);
-#endif
-                    const long long Dx = sD[cbuf * BN + col0 + j];
-                    const float Df = (float)Dx;
-                    const float a = n64 * n1, eb = -n64 * err;
-                    float vlb = INFINITY;
-#pragma unroll
-                    for (int k2i = -7; k2i <= 7; k2i += 2) {
-                        const float k2 = (float)k2i;
-                        vlb = fminf(vlb, fmaf(k2, fmaf(k2, Df, a), -fabsf(k2) * eb));
-                    }
-                    const float margin = 1024.f + 1e-5f * (fabsf(vlb) + 49.f * Df + fabsf(a) * 7.f);
-                    if (vstar != LLONG_MAX && vlb - margin > (float)vstar) continue;
-#ifdef MNS_TC_STATS
-                    atomicAdd(&g_tc_stats[3], 1ull);
-#endif
-                    const long long d = (dbase + col0 + j) * p.dstride;
-                    if (d >= p.ndom) continue;
-                    const long long N = (long long)p.n * (long long)(int)c[j] - (long long)(int)(-nsq) * sr;  // exact
-                    const long long v = best_val_exact(N, Dx);
-                    const unsigned long long key = make_key(v, d * p.n_iso + iso);
-                    if (key < best) {
-                        best = key;
-                        set_threshold(v);
-                        atomicMin(&p.best[rr], key);  // publish to the other CTAs of this range
-                    }
-                }
-            }
+            for (int i = 0; i < EPI_COLS; i += 16) tmem_ld16(tbase + i, c + i);
+            tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&tempty[acc]);
-                mbar_arrive(&cempty[cbuf]);
+            if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained: the MMA may reuse it
+#ifdef TC_EXP
+            if (TC_EXP == 2) {
+                if (lane == 0) mbar_arrive(&cempty[cbuf]);
+                continue;  // timing experiment: MMA + accumulator drain only
             }
+#endif
+            // level 1: one |max| per 16-column group against the row threshold (FMNMX3 per 2 columns)
+            unsigned gpass = 0;
+#pragma unroll
+            for (int gi = 0; gi < EPI_COLS / GRP; gi++) {
+                float ma = 0.f, mb = 0.f;
+#pragma unroll
+                for (int j = 0; j < GRP; j += 4) {
+                    ma = absmax3(ma, c[gi * GRP + j], c[gi * GRP + j + 1]);
+                    mb = absmax3(mb, c[gi * GRP + j + 2], c[gi * GRP + j + 3]);
+                }
+                gpass |= (live && fmaxf(ma, mb) >= thr) ? 1u << gi : 0u;
+            }
+            gpass = __reduce_or_sync(FULL, gpass);
+#ifdef MNS_TC_STATS
+            if (lane == 0) atomicAdd(&g_tc_stats[0], (unsigned long long)(EPI_COLS / GRP));
+#endif
+            if (gpass) {
+                mbar_spin(&cfull[cbuf], (t / NCB) & 1);
+                const float *lq = reinterpret_cast<const float *>(sC + cbuf * CONST_BYTES);  // -Sq
+                const float *ls = lq + BN;                                                  // sqrt_rd(D)
+                const long long *ld = reinterpret_cast<const long long *>(sC + cbuf * CONST_BYTES + BN * 8);
+#pragma unroll
+                for (int gi = 0; gi < EPI_COLS / GRP; gi++) {
+                    if (!(gpass & (1u << gi))) continue;
+#ifdef MNS_TC_STATS
+                    if (lane == 0) atomicAdd(&g_tc_stats[1], 1ull);
+#endif
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < GRP; j++) stash[j * 32 + lane] = c[gi * GRP + j];
+                    __syncwarp();
+                    // level 2 per column for the (lane, column) pairs passing level 1: rigorous lower and
+                    // upper bounds of the quantised value over the odd k2 from x ~ N/(n sqrt D).  The lower
+                    // bound discards; a survivor is queued for the exact warp and its upper bound (a real
+                    // candidate's value is at most that) tightens this lane's threshold at once.
+#pragma unroll 1
+                    for (int jj = 0; jj < GRP; jj++) {
+                        const int col = half * EPI_COLS + gi * GRP + jj;
+                        const float x = stash[jj * 32 + lane];
+                        bool pj = live && fabsf(x) >= thr;
+                        if (!__any_sync(FULL, pj)) continue;
+                        if (pj) {
+#ifdef MNS_TC_STATS
+                            atomicAdd(&g_tc_stats[2], 1ull);
+#endif
+                            const float sg = ls[col];
+                            const float n1 = x * sg;  // ~ N/n
+                            // |n1 - N/n| <= sqrt(D) e_row + |x| |sqrt(D) - sg| + rounding of the product
+                            const float err = fmaf(fabsf(x), 0x1p-20f, erow) * sg * 1.0001f + 1e-6f;
+                            const long long Dx = ld[col];
+                            const float Df = (float)Dx;
+                            const float a = n64 * n1, eb = -n64 * err;
+                            float vlb = INFINITY, vub = INFINITY;
+#pragma unroll
+                            for (int k2i = -7; k2i <= 7; k2i += 2) {
+                                const float k2 = (float)k2i;
+                                const float mid = k2 * fmaf(k2, Df, a);
+                                vlb = fminf(vlb, fmaf(-fabsf(k2), eb, mid));
+                                vub = fminf(vub, fmaf(fabsf(k2), eb, mid));
+                            }
+                            const float margin = 1024.f + 1e-5f * (fabsf(vlb) + fabsf(vub) + 49.f * Df + fabsf(a) * 7.f);
+                            pj = !(vstar != LLONG_MAX && vlb - margin > (float)vstar) && (dt * BN + col) * (long long)p.dstride < p.ndom;
+                            if (pj) set_threshold((long long)ceilf(vub + margin));
+                        }
+                        // queue the survivors (16-B entries, sequence number written last)
+                        const unsigned qm = __ballot_sync(FULL, pj);
+                        if (!qm) continue;
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(q_head, (uint32_t)__popc(qm));
+                        base = __shfl_sync(FULL, base, 0);
+                        if (pj) {
+                            const uint32_t slot = base + __popc(qm & lanemask_lt());
+                            while (slot - *(volatile uint32_t *)q_tail >= (uint32_t)QSIZE) {
+                            }
+                            uint4 *e = reinterpret_cast<uint4 *>(queue) + (slot % QSIZE);
+                            *reinterpret_cast<uint2 *>(e) = make_uint2((uint32_t)col | ((uint32_t)rl << 8), (uint32_t)m);
+                            reinterpret_cast<uint32_t *>(e)[2] = (uint32_t)dt;
+                            __threadfence_block();
+                            reinterpret_cast<volatile uint32_t *>(e)[3] = slot + 1;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cempty[cbuf]);  // (waited on cfull above only if needed: the
+                                                          // producer's next copy into this slot waits for us)
         }
-        if (active) atomicMin(&p.best[rr], flat ? *p.flat_key : best);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(q_done, 1u);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -376,13 +547,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ---- operand preparation
+// Domain operand: (q_k - Sq/n) / sqrt(D) in fp16 (0 for a flat domain), planar column constants.
 __global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
                                 long long ndom_pad, int n, __half *Q, float2 *consts) {
     const int lane = threadIdx.x & 31;  // one warp per domain: coalesced 128-byte fp16 rows
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long d = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); d < ndom_pad; d += warps) {
+        const bool ok = d < ndom && pD[d] > 0;
+        const float mean = ok ? (float)psq[d] / (float)n : 0.f;   // exact: Sq < 2^17, n a power of two
+        const float inv = ok ? 1.0f / sqrtf((float)pD[d]) : 0.f;
         for (int k = lane; k < BK; k += 32)
-            Q[d * BK + k] = __float2half_rn(d < ndom && k < n ? (float)pool[d * n + k] : 0.f);
+            Q[d * BK + k] = __float2half_rn(ok && k < n ? ((float)pool[d * n + k] - mean) * inv : 0.f);
         if (lane == 0) {  // planar per 128-domain tile: -Sq then sqrt_rd(D)
             float *cf = reinterpret_cast<float *>(consts) + (d / BN) * 2 * BN + d % BN;
             cf[0] = d < ndom ? -(float)psq[d] : 0.f;
@@ -391,8 +566,10 @@ __global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const 
     }
 }
 
+// Range operand rows (range, isometry): raw r (exact recompute) and centred r - Sr/n (the GEMM),
+// both fp16, plus Sr, the constant-range flag and e_row = 2^-9 max |r - Sr/n|.
 __global__ void range_rows_kernel(const uint8_t *img, int W, int B, int n_iso, int r0, int n_rows, int n_rows_pad,
-                                  __half *A, int32_t *row_sr, int32_t *row_flat) {
+                                  __half *Araw, __half *Ac, int32_t *row_sr, int32_t *row_flat, float *row_err) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n_rows_pad) return;
     const int n = B * B;
@@ -409,9 +586,17 @@ __global__ void range_rows_kernel(const uint8_t *img, int W, int B, int n_iso, i
             srr += r * r;
         }
     }
-    for (int k = 0; k < BK; k++) A[(size_t)row * BK + k] = __float2half_rn(v[k]);
+    const float mean = (float)sr / (float)n;  // exact
+    float emax = 0.f;
+    for (int k = 0; k < BK; k++) {
+        Araw[(size_t)row * BK + k] = __float2half_rn(v[k]);
+        const float rc = k < n ? v[k] - mean : 0.f;  // exact (multiple of 1/64, |rc| < 256)
+        Ac[(size_t)row * BK + k] = __float2half_rn(rc);
+        emax = fmaxf(emax, fabsf(rc));
+    }
     row_sr[row] = sr;
     row_flat[row] = row >= n_rows || ((long long)n * srr - (long long)sr * sr) == 0;
+    row_err[row] = emax * 0x1p-9f + 1e-6f;
 }
 
 // prepass column constants: every `stride`-th domain, contiguous, zero-padded
@@ -471,6 +656,17 @@ __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, 
     if ((threadIdx.x & 31) == 0) atomicMin(key, best);
 }
 
+int sm_count_tc() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
 }  // namespace
 
 #ifdef MNS_TC_STATS
@@ -486,7 +682,7 @@ int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso) {
     const long long ndom_pad = (ndom + BN - 1) / BN * BN;
     const long long rows_pad = ((long long)(W / B) * (H / B) * n_iso + MH * BM - 1) / (MH * BM) * (MH * BM);
     const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
-    return ndom_pad * BK * 2 + ndom_pad * 8 + rows_pad * BK * 2 + rows_pad * 8 + nsample_pad * 16 + 2048;
+    return ndom_pad * BK * 2 + ndom_pad * 8 + 2 * rows_pad * BK * 2 + rows_pad * 12 + nsample_pad * 16 + 4096;
 }
 
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
@@ -503,11 +699,15 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     q += ndom_pad * BK * 2;
     float2 *consts = (float2 *)q;
     q += ndom_pad * 8;
-    __half *A = (__half *)q;
+    __half *Araw = (__half *)q;
+    q += (long long)n_rows_pad * BK * 2;
+    __half *Ac = (__half *)q;
     q += (long long)n_rows_pad * BK * 2;
     int32_t *row_sr = (int32_t *)q;
     q += (long long)n_rows_pad * 4;
     int32_t *row_flat = (int32_t *)q;
+    q += (long long)n_rows_pad * 4;
+    float *row_err = (float *)q;
     q += (long long)n_rows_pad * 4;
     q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
     const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
@@ -517,21 +717,22 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     q += nsample_pad * 8;
     unsigned long long *fkey = (unsigned long long *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
 
-    pool_f16_kernel<<<148 * 16, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
-    range_rows_kernel<<<(n_rows_pad + 127) / 128, 128, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, A, row_sr,
-                                                                 row_flat);
+    const int sms = sm_count_tc();
+    pool_f16_kernel<<<sms * 16, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
+    range_rows_kernel<<<(n_rows_pad + 127) / 128, 128, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, Araw, Ac,
+                                                                 row_sr, row_flat, row_err);
     MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
     flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
     {
         const int ndx = (W - 2 * B) / step + 1, ndy = (int)(ndom / ndx);
-        seed_best_kernel<<<(n_rows + 7) / 8, 256, 0, st>>>(A, row_sr, pool, psq, pD, W, B, step, ndx, ndy, n_iso, r0,
-                                                          n_rows, best);
+        seed_best_kernel<<<(n_rows + 7) / 8, 256, 0, st>>>(Araw, row_sr, pool, psq, pD, W, B, step, ndx, ndy, n_iso,
+                                                          r0, n_rows, best);
     }
 
     CUtensorMap tmA, tmB, tmS;
     constexpr int SAMPLE = 128;  // prepass: every 128th domain seeds each row's best (strided TMA view)
     const long long nsample = (ndom + SAMPLE - 1) / SAMPLE;
-    if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
+    if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Ac, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
     if (encode_tmap_2d_swizzled(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, ndom_pad, BK * 2, BK, BN)) return -1;
     if (encode_tmap_2d_swizzled(&tmS, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, nsample, (uint64_t)BK * 2 * SAMPLE, BK,
                                 BN))
@@ -545,28 +746,33 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     p.ndom = ndom;
     p.consts = consts;
     p.pD = pD;
+    p.pool = pool;
+    p.araw = Araw;
     p.row_sr = row_sr;
     p.row_flat = row_flat;
+    p.row_err = row_err;
     p.flat_key = fkey;
     p.best = best;
     {
         static std::atomic<unsigned long long> done{0};
         MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel, SMEM_BYTES, done));
     }
+    const long long n_mt = n_rows_pad / (MH * BM);
     if (ndom >= 16 * SAMPLE) {  // prepass over the sample
         gather_sample_kernel<<<64, 256, 0, st>>>(consts, pD, ndom, SAMPLE, nsample_pad, cons_s, pD_s);
-        TcParams q = p;
-        q.consts = cons_s;
-        q.pD = pD_s;
-        q.dstride = SAMPLE;
-        q.n_dtiles = (int)((nsample + BN - 1) / BN);
-        q.dtiles_per_chunk = q.n_dtiles;  // one CTA per M tile: a single cold start per row
-        full_search_tc_kernel<<<dim3(1, n_rows_pad / (MH * BM)), NTHREADS, SMEM_BYTES, st>>>(tmA, tmS, q);
+        TcParams q2 = p;
+        q2.consts = cons_s;
+        q2.pD = pD_s;
+        q2.dstride = SAMPLE;
+        q2.n_dt = (int)((nsample + BN - 1) / BN);
+        q2.n_units = n_mt * q2.n_dt;
+        const int grid = (int)(q2.n_units < sms ? q2.n_units : sms);
+        full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmS, q2);
     }
     p.dstride = 1;
-    p.n_dtiles = (int)(ndom_pad / BN);
-    p.dtiles_per_chunk = 48;
-    dim3 grid((p.n_dtiles + p.dtiles_per_chunk - 1) / p.dtiles_per_chunk, n_rows_pad / (MH * BM));
+    p.n_dt = (int)(ndom_pad / BN);
+    p.n_units = n_mt * p.n_dt;
+    const int grid = (int)(p.n_units < sms ? p.n_units : sms);
     full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
     MNS_CUDA_TRY(cudaGetLastError());
     *handled = true;

@@ -678,3 +678,18 @@ def test_lattice_decode_extreme_shapes(mns, H, W):
                                   N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("n_iso", [1, 8])
+def test_full_search_c4_tensor_core_equals_cuda_core_all_ranges(mns, monkeypatch, n_iso):
+    """c4 in full (4096 ranges x 247,009 domains x n_iso): the normalised-operand tcgen05 filter
+    keeps every winner -- the argmin equals the exact CUDA-core path for every range."""
+    from paper_1501_02894_b200.synth import config_image
+
+    img = torch.from_numpy(config_image("c4")).cuda()
+    monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "0")
+    a = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, 8, 1, n_iso).items()}
+    monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "1")
+    b = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, 8, 1, n_iso).items()}
+    for k in a:
+        assert np.array_equal(a[k], b[k]), (n_iso, k, int((a[k] != b[k]).sum()))
