@@ -147,11 +147,13 @@ __global__ void __launch_bounds__(256) full_search_cc_kernel(const uint8_t *img,
 }
 
 // merge isometry rows already folded via the key's candidate index; finalise code/o per range
-__global__ void search_finalize_kernel(const uint8_t *img, int W, int B, int step, int ndx, int n_iso, int r0,
-                                       int r1, const unsigned long long *best, const uint16_t *pool,
+// one warp per range: re-derive o_byte and the contrast code of the winning (domain, isometry)
+__global__ void search_finalize_kernel(const uint8_t *img, int W, int B, int n_iso, int r0, int r1,
+                                       const unsigned long long *best, const uint16_t *pool,
                                        const int32_t *psq, const long long *pD, int32_t *out_dom, int8_t *out_iso,
                                        uint8_t *out_o, uint8_t *out_code) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= r1 - r0) return;
     const int ri = r0 + i, n = B * B, rpr = W / B;
     const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
@@ -161,18 +163,21 @@ __global__ void search_finalize_kernel(const uint8_t *img, int W, int B, int ste
     const int t = (int)(cand % n_iso);
     int sr = 0;
     long long sqr = 0;
-    for (int e = 0; e < n; e++) {
+    for (int e = lane; e < n; e += 32) {
         const int r = img[(size_t)(ry + e / B) * W + rx + e % B];
         sr += r;
         sqr += (long long)r * pool[d * n + iso_src(t, e / B, e % B, B)];
     }
-    const long long N = (long long)n * sqr - (long long)psq[d] * sr;
-    out_dom[i] = (int32_t)d;
-    out_iso[i] = (int8_t)t;
-    out_o[i] = (uint8_t)((2 * sr + n) / (2 * n));
-    out_code[i] = (uint8_t)quant_code(N, pD[d]);
-    (void)step;
-    (void)ndx;
+    sr = __reduce_add_sync(FULL, sr);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sqr += __shfl_xor_sync(FULL, sqr, o);
+    if (lane == 0) {
+        const long long N = (long long)n * sqr - (long long)psq[d] * sr;
+        out_dom[i] = (int32_t)d;
+        out_iso[i] = (int8_t)t;
+        out_o[i] = (uint8_t)((2 * sr + n) / (2 * n));
+        out_code[i] = (uint8_t)quant_code(N, pD[d]);
+    }
 }
 
 __global__ void fill_u64_kernel(unsigned long long *a, unsigned long long v, long long n) {
@@ -298,7 +303,7 @@ int search_workspace_bytes(int W, int H, int B, int step, int n_iso, int64_t *by
 }
 
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
-                   const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
+                   uint16_t *pool, int32_t *psq, long long *pD, long long ndom,
                    unsigned long long *best, void *tc_ws, cudaStream_t st, bool *handled);
 
 // MNS_SEARCH_CUDA_CORES=1 selects the exact CUDA-core path for every B (A/B checks of the tensor-core path).
@@ -334,7 +339,6 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     p += align256(nranges * 8);
     void *tc_ws = B <= 8 ? (void *)p : nullptr;
     const int sms = sm_count_search();
-    pool_kernel<<<sms * 16, 256, 0, st>>>(img, W, B, step, (int)ndx, ndom, w.pool, w.psq, w.pD);
     fill_u64_kernel<<<64, 256, 0, st>>>(w.best, ~0ull, r1 - r0);
     bool handled = false;
     int rc = 0;
@@ -342,6 +346,7 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
                                                tc_ws, st, &handled);
     if (rc) return rc;
     if (!handled) {
+        pool_kernel<<<sms * 16, 256, 0, st>>>(img, W, B, step, (int)ndx, ndom, w.pool, w.psq, w.pD);
         const int tiles = (r1 - r0 + 7) / 8;
         const long long gx = (ndom + 255) / 256;
         dim3 grid((unsigned)(gx < 64 ? gx : 64), (unsigned)tiles);
@@ -352,9 +357,8 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
         default: full_search_cc_kernel<16><<<grid, 256, 0, st>>>(img, W, n_iso, r0, r1, w.pool, w.psq, w.pD, ndom, w.best); break;
         }
     }
-    search_finalize_kernel<<<(r1 - r0 + 127) / 128, 128, 0, st>>>(img, W, B, step, (int)ndx, n_iso, r0, r1, w.best,
-                                                                  w.pool, w.psq, w.pD, out_dom, out_iso, out_o,
-                                                                  out_code);
+    search_finalize_kernel<<<(r1 - r0 + 7) / 8, 256, 0, st>>>(img, W, B, n_iso, r0, r1, w.best, w.pool, w.psq, w.pD,
+                                                             out_dom, out_iso, out_o, out_code);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -47,7 +47,10 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BM = 128, BN = 128, BK = 64;   // MMA tile (M rows, N domains, K)
 constexpr int MH = 2;                         // M halves per CTA: 256 rows share every B tile
-constexpr int STAGES = 4;
+#ifndef TC_STAGES
+#define TC_STAGES 4
+#endif
+constexpr int STAGES = TC_STAGES;
 constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
 constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;  // 640
 constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB per A buffer (two buffers)
@@ -223,7 +226,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t *tfull = bars + 2 * STAGES + 4, *tempty = bars + 2 * STAGES + 6;
     uint32_t *tmem_base_sh = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 8);
     uint32_t *q_head = tmem_base_sh + 1, *q_tail = tmem_base_sh + 2, *q_done = tmem_base_sh + 3;
-    uint64_t *cfull = bars + 2 * STAGES + 10, *cempty = bars + 2 * STAGES + 10 + NCB;  // column-constant ring
+    uint64_t *cfull = bars + 2 * STAGES + 12, *cempty = bars + 2 * STAGES + 12 + NCB;  // column-constant ring
+    uint32_t *c_issued = tmem_base_sh + 4;  // constant copies issued so far
     unsigned char *queue = tsm + QUEUE_OFF;
     unsigned char *sC = tsm + CONST_OFF;
 
@@ -248,6 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&cfull[a], 1);
             mbar_init(&cempty[a], EPI_WARPS);
         }
+        *c_issued = 0;
         *q_head = 0;
         *q_tail = 0;
         *q_done = 0;
@@ -306,7 +311,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     adesc0 = umma_desc_sw128(smem_u32(sA + (seg & 1) * A_BYTES));
                 }
                 const int s = t % STAGES, acc = t & 1;
+#if !(defined(TC_EXP) && TC_EXP >= 4)
                 if (t >= 2) mbar_spin(&tempty[acc], ((t / 2) - 1) & 1);
+#endif
                 mbar_spin(&full_bar[s], (t / STAGES) & 1);
                 tc_fence_after();
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + s * B_BYTES));
@@ -326,9 +333,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 2) {
         // ===== column constants of tile t into ring slot t % NCB (read only on the rare level-2 path)
         if (lane == 0) {
+#if defined(TC_EXP) && TC_EXP >= 4
+            for (int t = 0, dt = dt_first; t < 0; t++) {
+#else
             for (int t = 0, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1) {
+#endif
                 const int cb = t % NCB;
-                if (t >= NCB) {  // the slot's previous copy has landed and every epilogue warp is done with it
+                if (t >= NCB) {  // the slot's previous copy has landed and every epilogue warp is past it
                     mbar_wait_ns(&cfull[cb], ((t / NCB) - 1) & 1);
                     mbar_wait_ns(&cempty[cb], ((t / NCB) - 1) & 1);
                 }
@@ -336,6 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const long long b0 = (long long)dt * BN;
                 bulk_g2s(sC + cb * CONST_BYTES, p.consts + b0, BN * 8, &cfull[cb]);
                 bulk_g2s(sC + cb * CONST_BYTES + BN * 8, p.pD + b0, BN * 8, &cfull[cb]);
+                *(volatile uint32_t *)c_issued = (uint32_t)(t + 1);  // copy t issued: cfull[cb]'s phase is t / NCB
             }
         }
     } else if (warp == 3) {
@@ -405,7 +417,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         };
         unsigned long long g = ~0ull;
+#if defined(TC_EXP) && TC_EXP >= 4
+        for (int t = 0, m = m_first, dt = dt_first; t < 0; t++) {
+#else
         for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+#endif
             if (m != cur_m) {  // new M tile: load the row
                 cur_m = m;
                 const int row = m * (MH * BM) + rl;
@@ -462,6 +478,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (lane == 0) atomicAdd(&g_tc_stats[0], (unsigned long long)(EPI_COLS / GRP));
 #endif
             if (gpass) {
+                // the parity wait is exact once copy t is issued (the producer issues it only after the
+                // slot's previous copy landed, so at most the phase of tile t is pending)
+                while (*(volatile uint32_t *)c_issued < (uint32_t)(t + 1)) {
+                }
                 mbar_spin(&cfull[cbuf], (t / NCB) & 1);
                 const float *lq = reinterpret_cast<const float *>(sC + cbuf * CONST_BYTES);  // -Sq
                 const float *ls = lq + BN;                                                  // sqrt_rd(D)
@@ -529,8 +549,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&cempty[cbuf]);  // (waited on cfull above only if needed: the
-                                                          // producer's next copy into this slot waits for us)
+            if (lane == 0) mbar_arrive(&cempty[cbuf]);  // done with this tile's constants
         }
         __syncwarp();
         if (lane == 0) {
@@ -547,56 +566,112 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ---- operand preparation
-// Domain operand: (q_k - Sq/n) / sqrt(D) in fp16 (0 for a flat domain), planar column constants.
-__global__ void pool_f16_kernel(const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
-                                long long ndom_pad, int n, __half *Q, float2 *consts) {
-    const int lane = threadIdx.x & 31;  // one warp per domain: coalesced 128-byte fp16 rows
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long d = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); d < ndom_pad; d += warps) {
-        const bool ok = d < ndom && pD[d] > 0;
-        const float mean = ok ? (float)psq[d] / (float)n : 0.f;   // exact: Sq < 2^17, n a power of two
-        const float inv = ok ? 1.0f / sqrtf((float)pD[d]) : 0.f;
-        for (int k = lane; k < BK; k += 32)
-            Q[d * BK + k] = __float2half_rn(ok && k < n ? ((float)pool[d * n + k] - mean) * inv : 0.f);
-        if (lane == 0) {  // planar per 128-domain tile: -Sq then sqrt_rd(D)
-            float *cf = reinterpret_cast<float *>(consts) + (d / BN) * 2 * BN + d % BN;
-            cf[0] = d < ndom ? -(float)psq[d] : 0.f;
-            cf[BN] = d < ndom ? __fsqrt_rd(__ll2float_rd(pD[d])) : 0.f;
+// Thread per domain (consecutive threads = consecutive domains of a row: the byte loads of a warp
+// coalesce): the exact pooled q (2x2 sums, u16), Sq, D = n Sqq - Sq^2, and the GEMM operand
+// (q_k - Sq/n) / sqrt(D) in fp16 (0 for a flat domain) with the planar column constants.
+template <int B>
+__global__ void __launch_bounds__(128) pool_tc_kernel(const uint8_t *img, int W, int step, int ndx, long long ndom,
+                                                      long long ndom_pad, uint16_t *pool, int32_t *psq,
+                                                      long long *pD, __half *Q, float2 *consts) {
+    constexpr int n = B * B;
+    const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (d >= ndom_pad) return;
+    float *cf = reinterpret_cast<float *>(consts) + (d / BN) * 2 * BN + d % BN;
+    uint4 *qrow = reinterpret_cast<uint4 *>(Q + d * BK);
+    if (d >= ndom) {
+        for (int i = 0; i < BK / 8; i++) qrow[i] = make_uint4(0, 0, 0, 0);
+        cf[0] = 0.f;
+        cf[BN] = 0.f;
+        return;
+    }
+    const int x = (int)(d % ndx) * step, y = (int)(d / ndx) * step;
+    int q[n];
+    int sq = 0;
+    long long sqq = 0;
+#pragma unroll
+    for (int i = 0; i < B; i++) {
+        const uint8_t *p0 = img + (size_t)(y + 2 * i) * W + x, *p1 = p0 + W;
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const int v = (int)__ldg(p0 + 2 * j) + __ldg(p0 + 2 * j + 1) + __ldg(p1 + 2 * j) + __ldg(p1 + 2 * j + 1);
+            q[i * B + j] = v;
+            sq += v;
+            sqq += v * v;
         }
     }
+    const long long D = n * sqq - (long long)sq * sq;
+    psq[d] = sq;
+    pD[d] = D;
+    if (n >= 8) {
+#pragma unroll
+        for (int k = 0; k < n; k += 8)
+            reinterpret_cast<uint4 *>(pool + d * n)[k / 8] =
+                make_uint4((uint32_t)q[k] | ((uint32_t)q[k + 1] << 16), (uint32_t)q[k + 2] | ((uint32_t)q[k + 3] << 16),
+                           (uint32_t)q[k + 4] | ((uint32_t)q[k + 5] << 16), (uint32_t)q[k + 6] | ((uint32_t)q[k + 7] << 16));
+    } else {
+#pragma unroll
+        for (int k = 0; k < n; k++) pool[d * n + k] = (uint16_t)q[k];
+    }
+    const bool ok = D > 0;
+    const float mean = (float)sq / (float)n;  // exact: Sq < 2^18, n a power of two
+    const float inv = ok ? 1.0f / sqrtf((float)D) : 0.f;
+    uint32_t h[BK / 2];
+#pragma unroll
+    for (int k = 0; k < BK; k += 2) {
+        const float a = k < n && ok ? ((float)q[k < n ? k : 0] - mean) * inv : 0.f;
+        const float b = k + 1 < n && ok ? ((float)q[k + 1 < n ? k + 1 : 0] - mean) * inv : 0.f;
+        const __half2 hv = __floats2half2_rn(a, b);
+        h[k / 2] = *reinterpret_cast<const uint32_t *>(&hv);
+    }
+#pragma unroll
+    for (int i = 0; i < BK / 8; i++) qrow[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+    cf[0] = -(float)sq;
+    cf[BN] = __fsqrt_rd(__ll2float_rd(D));
 }
 
-// Range operand rows (range, isometry): raw r (exact recompute) and centred r - Sr/n (the GEMM),
-// both fp16, plus Sr, the constant-range flag and e_row = 2^-9 max |r - Sr/n|.
+// Range operand rows (range, isometry), one warp per row: raw r (exact recompute) and centred
+// r - Sr/n (the GEMM), both fp16, plus Sr, the constant-range flag and e_row = 2^-9 max |r - Sr/n|.
+// row[k] = r(e) with k = src_t(e), i.e. e = src_{t^-1}(k) (rotations 5 and 6 are each other's inverse).
 __global__ void range_rows_kernel(const uint8_t *img, int W, int B, int n_iso, int r0, int n_rows, int n_rows_pad,
                                   __half *Araw, __half *Ac, int32_t *row_sr, int32_t *row_flat, float *row_err) {
-    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (row >= n_rows_pad) return;
     const int n = B * B;
-    float v[BK];
-    for (int k = 0; k < BK; k++) v[k] = 0.f;
-    int sr = 0, srr = 0;
-    if (row < n_rows) {
+    int v[2] = {0, 0};
+    const bool real = row < n_rows;
+    if (real) {
         const int ri = r0 + row / n_iso, t = row % n_iso, rpr = W / B;
+        const int ti = t == 5 ? 6 : (t == 6 ? 5 : t);
         const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
-        for (int e = 0; e < n; e++) {
-            const int r = img[(size_t)(ry + e / B) * W + rx + e % B];
-            v[iso_src(t, e / B, e % B, B)] = (float)r;  // row[src_t(e)] = r(e)
-            sr += r;
-            srr += r * r;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = lane + 32 * h;
+            if (k < n) {
+                const int e = iso_src(ti, k / B, k % B, B);
+                v[h] = img[(size_t)(ry + e / B) * W + rx + e % B];
+            }
         }
     }
+    const int sr = __reduce_add_sync(FULL, v[0] + v[1]);
+    const int srr = __reduce_add_sync(FULL, v[0] * v[0] + v[1] * v[1]);
     const float mean = (float)sr / (float)n;  // exact
     float emax = 0.f;
-    for (int k = 0; k < BK; k++) {
-        Araw[(size_t)row * BK + k] = __float2half_rn(v[k]);
-        const float rc = k < n ? v[k] - mean : 0.f;  // exact (multiple of 1/64, |rc| < 256)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int k = lane + 32 * h;
+        const float rc = real && k < n ? (float)v[h] - mean : 0.f;  // exact (multiple of 1/64, |rc| < 256)
+        Araw[(size_t)row * BK + k] = __float2half_rn((float)v[h]);
         Ac[(size_t)row * BK + k] = __float2half_rn(rc);
         emax = fmaxf(emax, fabsf(rc));
     }
-    row_sr[row] = sr;
-    row_flat[row] = row >= n_rows || ((long long)n * srr - (long long)sr * sr) == 0;
-    row_err[row] = emax * 0x1p-9f + 1e-6f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(FULL, emax, o));
+    if (lane == 0) {
+        row_sr[row] = sr;
+        row_flat[row] = !real || ((long long)n * srr - (long long)sr * sr) == 0;
+        row_err[row] = emax * 0x1p-9f + 1e-6f;
+    }
 }
 
 // prepass column constants: every `stride`-th domain, contiguous, zero-padded
@@ -685,8 +760,10 @@ int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso) {
     return ndom_pad * BK * 2 + ndom_pad * 8 + 2 * rows_pad * BK * 2 + rows_pad * 12 + nsample_pad * 16 + 4096;
 }
 
+// The tensor-core path; it also builds the pooled domains (pool, psq, pD) the finalize step reads.
+// *handled = false (nothing launched) when B or the workspace rule it out.
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
-                   const uint16_t *pool, const int32_t *psq, const long long *pD, long long ndom,
+                   uint16_t *pool, int32_t *psq, long long *pD, long long ndom,
                    unsigned long long *best, void *tc_ws, cudaStream_t st, bool *handled) {
     *handled = false;
     if (!(B == 2 || B == 4 || B == 8) || !tc_ws) return 0;
@@ -718,9 +795,17 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     unsigned long long *fkey = (unsigned long long *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
 
     const int sms = sm_count_tc();
-    pool_f16_kernel<<<sms * 16, 256, 0, st>>>(pool, psq, pD, ndom, ndom_pad, n, Q, consts);
-    range_rows_kernel<<<(n_rows_pad + 127) / 128, 128, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, Araw, Ac,
-                                                                 row_sr, row_flat, row_err);
+    {
+        const int ndx = (W - 2 * B) / step + 1;
+        const unsigned blocks = (unsigned)((ndom_pad + 127) / 128);
+        switch (B) {
+        case 2: pool_tc_kernel<2><<<blocks, 128, 0, st>>>(img, W, step, ndx, ndom, ndom_pad, pool, psq, pD, Q, consts); break;
+        case 4: pool_tc_kernel<4><<<blocks, 128, 0, st>>>(img, W, step, ndx, ndom, ndom_pad, pool, psq, pD, Q, consts); break;
+        default: pool_tc_kernel<8><<<blocks, 128, 0, st>>>(img, W, step, ndx, ndom, ndom_pad, pool, psq, pD, Q, consts); break;
+        }
+    }
+    range_rows_kernel<<<(n_rows_pad + 7) / 8, 256, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, Araw, Ac, row_sr,
+                                                          row_flat, row_err);
     MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
     flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
     {
