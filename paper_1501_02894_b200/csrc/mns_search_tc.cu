@@ -51,12 +51,15 @@ constexpr int MH = 2;                         // M halves per CTA: 256 rows shar
 #define TC_STAGES 4
 #endif
 constexpr int STAGES = TC_STAGES;
-constexpr int EPI_WARP0 = 4, EPI_WARPS = 16;
-constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;  // 640
+#ifndef TC_EPI_WARPS
+#define TC_EPI_WARPS 16
+#endif
+constexpr int EPI_WARP0 = 4, EPI_WARPS = TC_EPI_WARPS;  // 16: each warp 64 columns; 8: all 128
+constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB per A buffer (two buffers)
 constexpr int B_BYTES = BN * BK * 2;          // 16 KB
 constexpr int TMEM_COLS = 2 * MH * BN;        // 2 accumulator stages x 2 M halves x 128 columns = 512
-constexpr int EPI_COLS = BN / 2;              // columns per epilogue thread per tile
+constexpr int EPI_COLS = BN * 8 / EPI_WARPS;   // columns per epilogue thread per tile
 constexpr int GRP = 16;                       // level-1 vote group (columns)
 constexpr int NCB = 4;                        // column-constant ring slots
 constexpr int CONST_BYTES = BN * 16;          // per tile: 128 x -Sq, 128 x sqrt_rd(D) (floats), 128 x D (int64)
@@ -166,6 +169,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
         : "r"(taddr));
 #pragma unroll
     for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+// 32 accumulator columns (no wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -398,7 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int ew = warp - EPI_WARP0;       // 0..15
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
         const int mh = (ew >> 2) & 1;          // M half
-        const int half = ew >> 3;              // column half (0: 0..63, 1: 64..127)
+        const int half = ew >> 3;              // column block (16 warps: 0..63 | 64..127)
         const int rl = mh * BM + quarter * 32 + lane;  // row within the M tile
         float *stash = reinterpret_cast<float *>(tsm + STASH_OFF) + ew * (GRP * 32);  // [GRP][32] per warp
         const float n64 = -64.f * (float)p.n;
@@ -450,7 +467,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             float c[EPI_COLS];
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MH + mh) * BN + half * EPI_COLS;
 #pragma unroll
-            for (int i = 0; i < EPI_COLS; i += 16) tmem_ld16(tbase + i, c + i);
+            for (int i = 0; i < EPI_COLS; i += 32) tmem_ld32(tbase + i, c + i);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -473,78 +490,70 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 gpass |= (live && fmaxf(ma, mb) >= thr) ? 1u << gi : 0u;
             }
-            gpass = __reduce_or_sync(FULL, gpass);
 #ifdef MNS_TC_STATS
             if (lane == 0) atomicAdd(&g_tc_stats[0], (unsigned long long)(EPI_COLS / GRP));
 #endif
-            if (gpass) {
-                // the parity wait is exact once copy t is issued (the producer issues it only after the
-                // slot's previous copy landed, so at most the phase of tile t is pending)
+            if (__any_sync(FULL, gpass != 0)) {
+                // rare path, per lane (no warp votes): the lane's passing columns one by one.  Level 2:
+                // rigorous lower and upper bounds of the quantised value over the odd k2 from
+                // x ~ N/(n sqrt D).  The lower bound discards; a survivor is queued for the exact warp
+                // and its upper bound (a real candidate's value is at most that) tightens the lane's
+                // threshold at once.
                 while (*(volatile uint32_t *)c_issued < (uint32_t)(t + 1)) {
                 }
-                mbar_spin(&cfull[cbuf], (t / NCB) & 1);
+                mbar_spin(&cfull[cbuf], (t / NCB) & 1);  // exact: copy t is issued (see the producer)
                 const float *lq = reinterpret_cast<const float *>(sC + cbuf * CONST_BYTES);  // -Sq
                 const float *ls = lq + BN;                                                  // sqrt_rd(D)
                 const long long *ld = reinterpret_cast<const long long *>(sC + cbuf * CONST_BYTES + BN * 8);
 #pragma unroll
                 for (int gi = 0; gi < EPI_COLS / GRP; gi++) {
                     if (!(gpass & (1u << gi))) continue;
-#ifdef MNS_TC_STATS
-                    if (lane == 0) atomicAdd(&g_tc_stats[1], 1ull);
-#endif
-                    __syncwarp();
+                    uint32_t mask = 0;
 #pragma unroll
-                    for (int j = 0; j < GRP; j++) stash[j * 32 + lane] = c[gi * GRP + j];
-                    __syncwarp();
-                    // level 2 per column for the (lane, column) pairs passing level 1: rigorous lower and
-                    // upper bounds of the quantised value over the odd k2 from x ~ N/(n sqrt D).  The lower
-                    // bound discards; a survivor is queued for the exact warp and its upper bound (a real
-                    // candidate's value is at most that) tightens this lane's threshold at once.
-#pragma unroll 1
-                    for (int jj = 0; jj < GRP; jj++) {
-                        const int col = half * EPI_COLS + gi * GRP + jj;
+                    for (int j = 0; j < GRP; j++) {
+                        mask |= (fabsf(c[gi * GRP + j]) >= thr ? 1u : 0u) << j;
+                        stash[j * 32 + lane] = c[gi * GRP + j];  // lane-private column, for dynamic access
+                    }
+#ifdef MNS_TC_STATS
+                    atomicAdd(&g_tc_stats[1], 1ull);
+#endif
+                    while (mask) {
+                        const int jj = __ffs(mask) - 1;
+                        mask &= mask - 1;
                         const float x = stash[jj * 32 + lane];
-                        bool pj = live && fabsf(x) >= thr;
-                        if (!__any_sync(FULL, pj)) continue;
-                        if (pj) {
+                        if (!(fabsf(x) >= thr)) continue;  // the threshold may have tightened meanwhile
 #ifdef MNS_TC_STATS
-                            atomicAdd(&g_tc_stats[2], 1ull);
+                        atomicAdd(&g_tc_stats[2], 1ull);
 #endif
-                            const float sg = ls[col];
-                            const float n1 = x * sg;  // ~ N/n
-                            // |n1 - N/n| <= sqrt(D) e_row + |x| |sqrt(D) - sg| + rounding of the product
-                            const float err = fmaf(fabsf(x), 0x1p-20f, erow) * sg * 1.0001f + 1e-6f;
-                            const long long Dx = ld[col];
-                            const float Df = (float)Dx;
-                            const float a = n64 * n1, eb = -n64 * err;
-                            float vlb = INFINITY, vub = INFINITY;
+                        const int col = half * EPI_COLS + gi * GRP + jj;
+                        if ((dt * BN + col) * (long long)p.dstride >= p.ndom) continue;
+                        const float sg = ls[col];
+                        const float n1 = x * sg;  // ~ N/n
+                        // |n1 - N/n| <= sqrt(D) e_row + |x| |sqrt(D) - sg| + rounding of the product
+                        const float err = fmaf(fabsf(x), 0x1p-20f, erow) * sg * 1.0001f + 1e-6f;
+                        const long long Dx = ld[col];
+                        const float Df = (float)Dx;
+                        const float a = n64 * n1, eb = -n64 * err;
+                        float vlb = INFINITY, vub = INFINITY;
 #pragma unroll
-                            for (int k2i = -7; k2i <= 7; k2i += 2) {
-                                const float k2 = (float)k2i;
-                                const float mid = k2 * fmaf(k2, Df, a);
-                                vlb = fminf(vlb, fmaf(-fabsf(k2), eb, mid));
-                                vub = fminf(vub, fmaf(fabsf(k2), eb, mid));
-                            }
-                            const float margin = 1024.f + 1e-5f * (fabsf(vlb) + fabsf(vub) + 49.f * Df + fabsf(a) * 7.f);
-                            pj = !(vstar != LLONG_MAX && vlb - margin > (float)vstar) && (dt * BN + col) * (long long)p.dstride < p.ndom;
-                            if (pj) set_threshold((long long)ceilf(vub + margin));
+                        for (int k2i = -7; k2i <= 7; k2i += 2) {
+                            const float k2 = (float)k2i;
+                            const float mid = k2 * fmaf(k2, Df, a);
+                            vlb = fminf(vlb, fmaf(-fabsf(k2), eb, mid));
+                            vub = fminf(vub, fmaf(fabsf(k2), eb, mid));
                         }
-                        // queue the survivors (16-B entries, sequence number written last)
-                        const unsigned qm = __ballot_sync(FULL, pj);
-                        if (!qm) continue;
-                        uint32_t base = 0;
-                        if (lane == 0) base = atomicAdd(q_head, (uint32_t)__popc(qm));
-                        base = __shfl_sync(FULL, base, 0);
-                        if (pj) {
-                            const uint32_t slot = base + __popc(qm & lanemask_lt());
-                            while (slot - *(volatile uint32_t *)q_tail >= (uint32_t)QSIZE) {
-                            }
-                            uint4 *e = reinterpret_cast<uint4 *>(queue) + (slot % QSIZE);
-                            *reinterpret_cast<uint2 *>(e) = make_uint2((uint32_t)col | ((uint32_t)rl << 8), (uint32_t)m);
-                            reinterpret_cast<uint32_t *>(e)[2] = (uint32_t)dt;
-                            __threadfence_block();
-                            reinterpret_cast<volatile uint32_t *>(e)[3] = slot + 1;
+                        const float margin = 1024.f + 1e-5f * (fabsf(vlb) + fabsf(vub) + 49.f * Df + fabsf(a) * 7.f);
+                        if (vstar != LLONG_MAX && vlb - margin > (float)vstar) continue;
+                        set_threshold((long long)ceilf(vub + margin));
+                        // queue it (16-B entry, sequence number written last)
+                        const uint32_t slot = atomicAdd(q_head, 1u);
+                        while (slot - *(volatile uint32_t *)q_tail >= (uint32_t)QSIZE) {
                         }
+                        uint4 *e = reinterpret_cast<uint4 *>(queue) + (slot % QSIZE);
+                        *reinterpret_cast<uint2 *>(e) = make_uint2((uint32_t)col | ((uint32_t)rl << 8), (uint32_t)m);
+                        reinterpret_cast<uint32_t *>(e)[2] = (uint32_t)dt;
+                        __threadfence_block();
+                        reinterpret_cast<volatile uint32_t *>(e)[3] = slot + 1;
                     }
                 }
             }
