@@ -45,8 +45,11 @@ __device__ unsigned long long g_tc_stats[4];  // 16-col groups, level-1 group pa
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int BM = 128, BN = 128, BK = 64;   // MMA tile (M rows, N domains, K)
-constexpr int MH = 2;                         // M halves per CTA: 256 rows share every B tile
+#ifndef TC_BN
+#define TC_BN 256
+#endif
+constexpr int BM = 128, BN = TC_BN, BK = 64;  // MMA tile (M rows, N domains, K)
+constexpr int MH = 256 / BN;                  // M halves per CTA (MH * BN = 256 TMEM columns per stage)
 #ifndef TC_STAGES
 #define TC_STAGES 4
 #endif
@@ -59,7 +62,7 @@ constexpr int NTHREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int A_BYTES = MH * BM * BK * 2;     // 32 KB per A buffer (two buffers)
 constexpr int B_BYTES = BN * BK * 2;          // 16 KB
 constexpr int TMEM_COLS = 2 * MH * BN;        // 2 accumulator stages x 2 M halves x 128 columns = 512
-constexpr int EPI_COLS = BN * 8 / EPI_WARPS;   // columns per epilogue thread per tile
+constexpr int EPI_COLS = BN * 4 * MH / EPI_WARPS;  // columns per epilogue thread per tile
 constexpr int GRP = 16;                       // level-1 vote group (columns)
 constexpr int NCB = 4;                        // column-constant ring slots
 constexpr int CONST_BYTES = BN * 16;          // per tile: 128 x -Sq, 128 x sqrt_rd(D) (floats), 128 x D (int64)
@@ -414,8 +417,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ===== epilogue: one TMEM lane (= row) per thread, half of the columns per warp
         const int ew = warp - EPI_WARP0;       // 0..15
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
-        const int mh = (ew >> 2) & 1;          // M half
-        const int half = ew >> 3;              // column block (16 warps: 0..63 | 64..127)
+        const int mh = (ew >> 2) % MH;         // M half
+        const int half = ew / (4 * MH);        // column block of EPI_COLS columns
         const int rl = mh * BM + quarter * 32 + lane;  // row within the M tile
         float *stash = reinterpret_cast<float *>(tsm + STASH_OFF) + ew * (GRP * 32);  // [GRP][32] per warp
         const float n64 = -64.f * (float)p.n;
@@ -713,12 +716,19 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
     const int r_a = lane < n ? __half2int_rn(ar[lane]) : 0, r_b = lane + 32 < n ? __half2int_rn(ar[lane + 32]) : 0;
     unsigned long long kbest = ~0ull;
     const int ox[5] = {0, -B, B, 0, 0}, oy[5] = {0, 0, 0, -B, B};
-    for (int c = 0; c < 5; c++) {
+    long long dd[5];
+    int part[5];
+#pragma unroll
+    for (int c = 0; c < 5; c++) {  // all five domains' loads in flight together
         const int dx = clampi((rx - B / 2 + ox[c]) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy[c]) / step, 0, ndy - 1);
-        const long long d = (long long)dy * ndx + dx;
-        const uint16_t *qd = pool + d * n;
-        const int part = (lane < n ? (int)qd[lane] * r_a : 0) + (lane + 32 < n ? (int)qd[lane + 32] * r_b : 0);
-        const int C = __reduce_add_sync(0xffffffffu, part);  // < 2^24
+        dd[c] = (long long)dy * ndx + dx;
+        const uint16_t *qd = pool + dd[c] * n;
+        part[c] = (lane < n ? (int)qd[lane] * r_a : 0) + (lane + 32 < n ? (int)qd[lane + 32] * r_b : 0);
+    }
+#pragma unroll
+    for (int c = 0; c < 5; c++) {
+        const long long d = dd[c];
+        const int C = __reduce_add_sync(0xffffffffu, part[c]);  // < 2^24
         const long long N = (long long)n * C - (long long)psq[d] * sr;
         const unsigned long long key = make_key(best_val_exact(N, pD[d]), d * n_iso + iso);
         kbest = key < kbest ? key : kbest;
@@ -852,7 +862,11 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
         MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel, SMEM_BYTES, done));
     }
     const long long n_mt = n_rows_pad / (MH * BM);
+#ifdef TC_NO_PREPASS
+    if (false) {
+#else
     if (ndom >= 16 * SAMPLE) {  // prepass over the sample
+#endif
         gather_sample_kernel<<<64, 256, 0, st>>>(consts, pD, ndom, SAMPLE, nsample_pad, cons_s, pD_s);
         TcParams q2 = p;
         q2.consts = cons_s;
