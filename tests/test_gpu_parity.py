@@ -228,16 +228,25 @@ def test_full_search_tensor_core_matches_exact_cuda_core_path(mns, monkeypatch):
 
     cases = [(np.ascontiguousarray(synth_image(512, 4)[64:192, 128:256]), 8, 8),
              (np.ascontiguousarray(synth_image(512, 9)[:96, :96]), 4, 8),
+             (np.ascontiguousarray(synth_image(512, 7)[200:264, 40:104]), 2, 8),
+             (np.ascontiguousarray(synth_image(512, 3)[:200, :136]), 8, 1),
              (np.full((64, 64), 255, np.uint8), 8, 1),
              (np.random.default_rng(2).integers(250, 256, (64, 64), dtype=np.uint8), 8, 8)]
-    for px, B, n_iso in cases:
-        img = torch.from_numpy(px).cuda()
-        monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "0")
-        a = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, 1, n_iso).items()}
-        monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "1")
-        b = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, 1, n_iso).items()}
-        for k in a:
-            assert np.array_equal(a[k], b[k]), (px.shape, B, n_iso, k)
+    for step in (1, 3):
+        for px, B, n_iso in cases:
+            img = torch.from_numpy(px).cuda()
+            monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "0")
+            a = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, step, n_iso).items()}
+            monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "1")
+            b = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, step, n_iso).items()}
+            for k in a:
+                assert np.array_equal(a[k], b[k]), (px.shape, B, n_iso, step, k)
+            # a range interval (the per-rank shard of the multi-GPU split) equals the same slice
+            r0, r1 = 37, min(150, len(a["dom"]))
+            monkeypatch.setenv("MNS_SEARCH_CUDA_CORES", "0")
+            c = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, B, step, n_iso, ranges=(r0, r1)).items()}
+            for k in a:
+                assert np.array_equal(c[k], a[k][r0:r1]), (px.shape, B, n_iso, step, "ranges", k)
 
 
 def test_full_search_c4_sample_vs_oracle(mns):
