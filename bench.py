@@ -76,17 +76,45 @@ def tensor_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML every 2 ms from a thread
+    (a timed region is often well under 100 ms), nvidia-smi -lms 50 when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown, HwThermalSlowdown, SwThermalSlowdown, SwPowerCap}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, reason names)
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), float(mx), [n for n, b in zip(self.NAMES, self.BITS) if bits & b]))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -99,9 +127,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+            r = [v.strip() for v in line.split(",")]
+            if len(r) >= 6 and r[0].replace(".", "").isdigit() and r[1].replace(".", "").isdigit():
+                self.rows.append((float(r[0]), float(r[1]), [self.NAMES[k] for k in range(4) if r[2 + k] == "Active"]))
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -110,12 +143,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 6 for k in range(4) if r[2 + k] == "Active"})
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[2]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------------- CPU legs
@@ -492,7 +524,11 @@ def run_ours(args, img_np, rank, world, local_rank):
                      "algorithmic_bytes": algo, "kernel": f"{kname} (steady-state pass = 2 sweeps)",
                      "peak_source": which,
                      "limiter": ("instruction issue (ncu: ~79% issue-active at 2 B/px of DRAM traffic; "
-                                 "profiles/r1/ncu_step_lattice.txt)") if dec.lattice else "latency"},
+                                 "profiles/r1/ncu_step_lattice.txt)") if dec.lattice else "latency",
+                     # the same pass against SURVEY 8(d)'s raster-state formula (8 B/px per sweep: fp32 raster
+                     # read + written), i.e. what a raster-state decoder at this speed would have to move
+                     "raster_equivalent": {"bytes": 2 * 8 * own_px, "achieved": 2 * 8 * own_px / (pass_ms / 1e3) / 1e9,
+                                           "frac": 2 * 8 * own_px / (pass_ms / 1e3) / 1e9 / hbm}},
         "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
                           "sample": f"c5 rows 0..{args.cpu_baseline_rows - 1} encoded + {ITERS}-sweep decoded as its own "
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
