@@ -50,6 +50,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int BM = 128, BN = TC_BN, BK = 64;  // MMA tile (M rows, N domains, K)
 constexpr int MH = 256 / BN;                  // M halves per CTA (MH * BN = 256 TMEM columns per stage)
+#ifndef TC_POLL
+#define TC_POLL 0  // poll the global keys when (t & TC_POLL) == TC_POLL
+#endif
 #ifndef TC_STAGES
 #define TC_STAGES 4
 #endif
@@ -445,17 +448,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 g = live ? ld_relaxed_u64(&p.best[rr]) : ~0ull;
             }
             const int acc = t & 1, cbuf = t % NCB;
-            // the range's running best from every CTA's exact warp (global key, loaded a tile ahead)
+            // the range's running best from every CTA's exact warp and every isometry row of the range
+            // (global key, loaded a tile ahead)
             if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
-            if ((t & 3) == 0) {  // and the other isometry rows of the range (adjacent lanes)
-                for (int o = 1; o < p.n_iso; o <<= 1) {
-                    const long long other = __shfl_xor_sync(FULL, vstar, o);
-                    if (live) set_threshold(other);
-                }
-            }
+            g = ~0ull;
             mbar_spin(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
-            g = live ? ld_relaxed_u64(&p.best[rr]) : ~0ull;
+            if ((t & TC_POLL) == TC_POLL) g = live ? ld_relaxed_u64(&p.best[rr]) : ~0ull;
             float c[EPI_COLS];
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MH + mh) * BN + half * EPI_COLS;
 #pragma unroll
