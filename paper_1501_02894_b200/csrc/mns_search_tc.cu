@@ -17,7 +17,7 @@
 // per 16-column group) pass a rigorous fp32 lower bound of the quantised value (level 2); the
 // rest are evaluated exactly in int64 from the pooled integer q and the raw range row (level 3)
 // and folded into the row's lexicographic (value, index) key, shared across CTAs by atomicMin.
-// A prepass over a 1/128 domain sample, seeded with 5 nearby domains per range, sets the
+// A prepass over a 1/1024 domain sample, seeded with 5 nearby domains per range, sets the
 // thresholds; constant ranges (N == 0 for every domain) take the precomputed argmin of D.
 //
 // Persistent CTAs (one per SM): CTA b owns a contiguous, equal share of the (M tile, domain tile)
@@ -50,6 +50,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int BM = 128, BN = TC_BN, BK = 64;  // MMA tile (M rows, N domains, K)
 constexpr int MH = 256 / BN;                  // M halves per CTA (MH * BN = 256 TMEM columns per stage)
+#ifndef TC_SAMPLE
+#define TC_SAMPLE 1024
+#endif
 #ifndef TC_POLL
 #define TC_POLL 0  // poll the global keys when (t & TC_POLL) == TC_POLL
 #endif
@@ -763,7 +766,7 @@ int64_t search_tc_workspace_bytes(int W, int H, int B, int step, int n_iso) {
     const long long ndx = (W - 2 * B) / step + 1, ndy = (H - 2 * B) / step + 1, ndom = ndx * ndy;
     const long long ndom_pad = (ndom + BN - 1) / BN * BN;
     const long long rows_pad = ((long long)(W / B) * (H / B) * n_iso + MH * BM - 1) / (MH * BM) * (MH * BM);
-    const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
+    const long long nsample_pad = (ndom / TC_SAMPLE + 1 + BN - 1) / BN * BN;
     return ndom_pad * BK * 2 + ndom_pad * 8 + 2 * rows_pad * BK * 2 + rows_pad * 12 + nsample_pad * 16 + 4096;
 }
 
@@ -794,7 +797,7 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     float *row_err = (float *)q;
     q += (long long)n_rows_pad * 4;
     q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
-    const long long nsample_pad = (ndom / 128 + 1 + BN - 1) / BN * BN;
+    const long long nsample_pad = (ndom / TC_SAMPLE + 1 + BN - 1) / BN * BN;
     float2 *cons_s = (float2 *)q;
     q += nsample_pad * 8;
     long long *pD_s = (long long *)q;
@@ -822,7 +825,7 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     }
 
     CUtensorMap tmA, tmB, tmS;
-    constexpr int SAMPLE = 128;  // prepass: every 128th domain seeds each row's best (strided TMA view)
+    constexpr int SAMPLE = TC_SAMPLE;  // prepass: every TC_SAMPLE-th domain seeds each row's best (strided TMA view)
     const long long nsample = (ndom + SAMPLE - 1) / SAMPLE;
     if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Ac, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
     if (encode_tmap_2d_swizzled(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, ndom_pad, BK * 2, BK, BN)) return -1;
