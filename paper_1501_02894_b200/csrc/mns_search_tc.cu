@@ -691,40 +691,66 @@ __global__ void gather_sample_kernel(const float2 *consts, const long long *pD, 
     }
 }
 
-// Seeds every range's best key before the prepass (which otherwise starts without a threshold
-// and evaluates its first tiles exactly): one warp per (range, isometry) row, exact values of the
-// co-centred domain and its four B-px neighbours (clamped, snapped to the stride), atomicMin.
-// Seeds are real candidates, so the final argmin is unchanged.
+// Seeds every range's best key before the prepass (which otherwise starts without a threshold):
+// one warp per range, exact values of the domains around the co-centred one (offsets in
+// {-B, -B/2, 0, B/2, B}^2, clamped and snapped to the stride) against every isometry row of the
+// range, atomicMin.  Seeds are real candidates, so the final argmin is unchanged.
 __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const uint16_t *pool, const int32_t *psq,
                                  const long long *pD, int W, int B, int step, int ndx, int ndy, int n_iso, int r0,
-                                 int n_rows, unsigned long long *best) {
+                                 int n_ranges, unsigned long long *best) {
     const int lane = threadIdx.x & 31;
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= n_rows) return;
-    const int n = B * B, ri = r0 + row / n_iso, iso = row % n_iso, rpr = W / B;
-    const int rx = (ri % rpr) * B, ry = (ri / rpr) * B, sr = row_sr[row];
-    const __half *ar = A + (size_t)row * BK;
-    const int r_a = lane < n ? __half2int_rn(ar[lane]) : 0, r_b = lane + 32 < n ? __half2int_rn(ar[lane + 32]) : 0;
-    unsigned long long kbest = ~0ull;
-    const int ox[5] = {0, -B, B, 0, 0}, oy[5] = {0, 0, 0, -B, B};
-    long long dd[5];
-    int part[5];
+    const int rr = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (rr >= n_ranges) return;
+    const int n = B * B, ri = r0 + rr, rpr = W / B;
+    const int rx = (ri % rpr) * B, ry = (ri / rpr) * B, sr = row_sr[rr * n_iso];
+    int ra[8], rb[8];
 #pragma unroll
-    for (int c = 0; c < 5; c++) {  // all five domains' loads in flight together
-        const int dx = clampi((rx - B / 2 + ox[c]) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy[c]) / step, 0, ndy - 1);
-        dd[c] = (long long)dy * ndx + dx;
-        const uint16_t *qd = pool + dd[c] * n;
-        part[c] = (lane < n ? (int)qd[lane] * r_a : 0) + (lane + 32 < n ? (int)qd[lane + 32] * r_b : 0);
+    for (int t = 0; t < 8; t++) {
+        const __half *ar = A + (size_t)(rr * n_iso + (t < n_iso ? t : 0)) * BK;
+        ra[t] = lane < n ? __half2int_rn(ar[lane]) : 0;
+        rb[t] = lane + 32 < n ? __half2int_rn(ar[lane + 32]) : 0;
     }
+    // pick the candidate with the best continuous estimate -N^2/D (any real candidate is a valid seed),
+    // then evaluate that one exactly
+    float best_est = -1.f;
+    long long bd = -1;
+    int bt = 0, bc = 0;
+    for (int c0 = 0; c0 < 25; c0 += 5) {  // a row of five candidates: all loads in flight together
+        long long dd[5];
+        float sqf[5], idf[5];
+        int qa[5], qb[5];
 #pragma unroll
-    for (int c = 0; c < 5; c++) {
-        const long long d = dd[c];
-        const int C = __reduce_add_sync(0xffffffffu, part[c]);  // < 2^24
-        const long long N = (long long)n * C - (long long)psq[d] * sr;
-        const unsigned long long key = make_key(best_val_exact(N, pD[d]), d * n_iso + iso);
-        kbest = key < kbest ? key : kbest;
+        for (int c = 0; c < 5; c++) {
+            const int ox = (c - 2) * B / 2, oy = (c0 / 5 - 2) * B / 2;
+            const int dx = clampi((rx - B / 2 + ox) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy) / step, 0, ndy - 1);
+            dd[c] = (long long)dy * ndx + dx;
+            const uint16_t *qd = pool + dd[c] * n;
+            qa[c] = lane < n ? (int)qd[lane] : 0;
+            qb[c] = lane + 32 < n ? (int)qd[lane + 32] : 0;
+            sqf[c] = (float)psq[dd[c]] * (float)sr;
+            const long long D = pD[dd[c]];
+            idf[c] = D > 0 ? 1.f / (float)D : 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < 5; c++) {
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                if (t >= n_iso) break;
+                const int C = __reduce_add_sync(0xffffffffu, qa[c] * ra[t] + qb[c] * rb[t]);  // < 2^24
+                const float N = fmaf((float)n, (float)C, -sqf[c]);
+                const float est = N * N * idf[c];
+                if (est > best_est) {
+                    best_est = est;
+                    bd = dd[c];
+                    bt = t;
+                    bc = C;
+                }
+            }
+        }
     }
-    if (lane == 0) atomicMin(&best[row / n_iso], kbest);
+    const long long N = (long long)n * bc - (long long)psq[bd] * sr;  // exact
+    const unsigned long long kbest = make_key(best_val_exact(N, pD[bd]), bd * n_iso + bt);
+    if (lane == 0) atomicMin(&best[rr], kbest);
 }
 
 __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, unsigned long long *key) {
@@ -818,11 +844,13 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
                                                           row_flat, row_err);
     MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
     flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
+#ifndef TC_NO_SEED
     {
         const int ndx = (W - 2 * B) / step + 1, ndy = (int)(ndom / ndx);
-        seed_best_kernel<<<(n_rows + 7) / 8, 256, 0, st>>>(Araw, row_sr, pool, psq, pD, W, B, step, ndx, ndy, n_iso,
-                                                          r0, n_rows, best);
+        seed_best_kernel<<<(r1 - r0 + 7) / 8, 256, 0, st>>>(Araw, row_sr, pool, psq, pD, W, B, step, ndx, ndy, n_iso,
+                                                            r0, r1 - r0, best);
     }
+#endif
 
     CUtensorMap tmA, tmB, tmS;
     constexpr int SAMPLE = TC_SAMPLE;  // prepass: every TC_SAMPLE-th domain seeds each row's best (strided TMA view)
