@@ -161,6 +161,11 @@ int mns_decode_flat_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin
 int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
                                 int32_t iters, float initial_value, float *lat_ping, float *lat_pong, uint8_t *out,
                                 int32_t *d_error, void *workspace, int64_t workspace_bytes, void *stream);
+/* mns_decode_unit_map_lattice: mns_decode_quadtree_lattice from the unit map of every root row (as
+ * mns_encode_quadtree emits it: 32 words per root), skipping the map build; workspace >= 64 bytes. */
+int mns_decode_unit_map_lattice(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters,
+                                float initial_value, float *lat_ping, float *lat_pong, uint8_t *out, int32_t *d_error,
+                                void *workspace, int64_t workspace_bytes, void *stream);
 
 /* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
  * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-

@@ -108,6 +108,7 @@ class DeviceCode:
     technique2: bool = True
     unit_map: "object" = None  # torch.int32 [n_roots * 32]: decoder unit map (mns_record.h), optional
     min_leaf: int = 0          # smallest painted unit side if known (4: no 2x2 units -> lattice-state decode), 0 unknown
+    unit_map_valid: bool = False  # unit_map holds this code's map (emitted by the encoder / build_unit_map)
 
     def n_records(self) -> int:
         return int(self.count.item())
@@ -175,6 +176,7 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     # e3 = inf: every visited level-3 node passes phase 1 (encoder.py:160-165, before phase 2), so no
     # leaf is 2x2 and no level-3 phase-2 leaf has 2x2 quadrants
     out.min_leaf = 4 if math.isinf(config.e3) else 0
+    out.unit_map_valid = out.unit_map is not None
     cfg = enc_cfg(config, root_level)
     if compact_stream is None:
         N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
@@ -199,6 +201,7 @@ def build_unit_map(code: DeviceCode, stream=None):
     code.unit_map = torch.empty(32 * n_roots, dtype=torch.int32, device=code.records.device)
     N.check(L.mns_build_unit_map(N.ptr(code.records), N.ptr(code.root_offsets), code.padded_w, r0, r1,
                                  N.ptr(code.unit_map), N.stream_ptr(stream)))
+    code.unit_map_valid = True
     return code.unit_map
 
 
@@ -229,18 +232,25 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
                    torch.empty((H, W), dtype=torch.float32, device=dev))
     if out is None and want_u8:
         out = torch.empty((H, W), dtype=torch.uint8, device=dev)
-    it = torch.zeros(1, dtype=torch.int32, device=dev)
     wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
     ws = _WS.get("dec", wsb, dev)
     if want_u8 and stop_delta == 0.0 and min_leaf_side(code) >= 4:
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        it = torch.full((1,), int(iters), dtype=torch.int32, device=dev)
+        err = torch.empty(1, dtype=torch.int32, device=dev)  # zeroed by the library
         n_lat = (H // 2) * (W // 2)
         lat = (rasters[0].view(-1)[:n_lat], rasters[1].view(-1)[:n_lat])
-        N.check(L.mns_decode_quadtree_lattice(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters),
-                                              float(initial_value), N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out),
-                                              N.ptr(err), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
-        it.fill_(int(iters))
+        whole = code.n_images == 1 and code.root_row_begin == 0 and code.root_row_end in (0, H // 16)
+        if code.unit_map is not None and code.unit_map_valid and whole:
+            # the encoder's own unit map: no rebuild from the records
+            N.check(L.mns_decode_unit_map_lattice(N.ptr(code.unit_map), W, H, int(iters), float(initial_value),
+                                                  N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out), N.ptr(err), N.ptr(ws),
+                                                  ws.numel(), N.stream_ptr(stream)))
+        else:
+            N.check(L.mns_decode_quadtree_lattice(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters),
+                                                  float(initial_value), N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out),
+                                                  N.ptr(err), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
         return out, it, rasters
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
     N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters), float(stop_delta),
                                   float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),
                                   N.ptr(ws), ws.numel(), N.stream_ptr(stream)))

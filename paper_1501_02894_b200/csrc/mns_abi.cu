@@ -110,6 +110,8 @@ int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int
 int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
                             float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
                             int64_t workspace_bytes, cudaStream_t stream);
+int decode_umap_lattice(const uint32_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
+                        uint8_t *out, int32_t *err, int *state, cudaStream_t stream);
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
@@ -262,6 +264,17 @@ int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_off
                                 int32_t *d_error, void *workspace, int64_t workspace_bytes, void *stream) {
     GUARD(mns::decode_quadtree_lattice(records, root_offsets, width, height, iters, initial_value, lat_ping, lat_pong,
                                        out, d_error, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_decode_unit_map_lattice(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters,
+                                float initial_value, float *lat_ping, float *lat_pong, uint8_t *out, int32_t *d_error,
+                                void *workspace, int64_t workspace_bytes, void *stream) {
+    if (workspace_bytes < 64) {
+        mns::set_error("invalid argument: %s", "workspace too small");
+        return -2;
+    }
+    GUARD(mns::decode_umap_lattice(unit_map, width, height, iters, initial_value, lat_ping, lat_pong, out, d_error,
+                                   reinterpret_cast<int *>(workspace), (cudaStream_t)stream));
 }
 
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

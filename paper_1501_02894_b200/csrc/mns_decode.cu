@@ -1163,26 +1163,22 @@ int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int
     return 0;
 }
 
-// decode_quadtree for codes without 2x2 units, on lattice state (lat_ping / lat_pong: (H/2) x (W/2)
-// floats each); stop_delta = 0, uint8 output.  *err (device) = 1 if the code had a 2x2 unit.
-int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
-                            float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
-                            int64_t workspace_bytes, cudaStream_t stream) {
+// The whole lattice-state decode (codes without 2x2 units; stop_delta = 0, uint8 output) from a unit
+// map of all root rows (lat_ping / lat_pong: (H/2) x (W/2) floats each).  *err (device) = 1 if the code
+// had a 2x2 unit.  `state` (64 bytes of workspace) is used by a single-sweep decode only.
+int decode_umap_lattice(const uint32_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
+                        uint8_t *out, int32_t *err, int *state, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
     MNS_CHECK_ARG(out != nullptr && err != nullptr, "out and err required");
-    int64_t need;
-    decode_workspace_bytes(W, H, &need);
-    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
-    int *state = reinterpret_cast<int *>(workspace);
-    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
     MNS_CUDA_TRY(cudaMemsetAsync(err, 0, 4, stream));
-    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
-    int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
-    if (rc) return rc;
-    if (iters == 1) return decode_sweep(umap, W, H, 0, H / 16, nullptr, init, nullptr, out, state, 0.0, stream);
+    if (iters == 1) {
+        MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
+        return decode_sweep(umap, W, H, 0, H / 16, nullptr, init, nullptr, out, state, 0.0, stream);
+    }
     const float *cur = nullptr;
     int it = 0;
+    int rc = 0;
     if (iters & 1) {
         rc = decode_flat_lattice(umap, 0, W, H, 0, H / 16, init, lat_pong, stream);
         if (rc) return rc;
@@ -1197,6 +1193,22 @@ int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets
         cur = nxt;
     }
     return 0;
+}
+
+// decode_quadtree for codes without 2x2 units, on lattice state: the unit map is built from the
+// records into the workspace, then decode_umap_lattice.
+int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
+                            float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
+                            int64_t workspace_bytes, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    int64_t need;
+    decode_workspace_bytes(W, H, &need);
+    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
+    int *state = reinterpret_cast<int *>(workspace);
+    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
+    const int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
+    if (rc) return rc;
+    return decode_umap_lattice(umap, W, H, iters, init, lat_ping, lat_pong, out, err, state, stream);
 }
 
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,

@@ -702,3 +702,19 @@ def test_full_search_c4_tensor_core_equals_cuda_core_all_ranges(mns, monkeypatch
     b = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, 8, 1, n_iso).items()}
     for k in a:
         assert np.array_equal(a[k], b[k]), (n_iso, k, int((a[k] != b[k]).sum()))
+
+
+@pytest.mark.parametrize("root_level,iters", [(1, 10), (2, 8), (1, 7), (1, 1)])
+def test_decode_from_encoder_unit_map_equals_records_path(mns, root_level, iters):
+    """decode_device on the encoder's own unit map (mns_decode_unit_map_lattice) equals the decode that
+    rebuilds the map from the records (mns_decode_quadtree_lattice), bit for bit."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    img = torch.from_numpy(synth_image(256, 11)).cuda()
+    code = mns.encode_device(img, mns.EncoderConfig(e3=math.inf), root_level=root_level)
+    assert code.unit_map_valid
+    a, _, _ = mns.decode_device(code, iters=iters, stop_delta=0.0)
+    code.unit_map_valid = False
+    b, _, _ = mns.decode_device(code, iters=iters, stop_delta=0.0)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
