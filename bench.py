@@ -225,9 +225,16 @@ def small_configs(dev, rank, world):
             rasters = (torch.empty((H, W), dtype=torch.float32, device=dev),
                        torch.empty((H, W), dtype=torch.float32, device=dev))
 
+            s_cmp = torch.cuda.Stream()
+
             def step():
-                mns.encode_device(img, cfg, root_level=root_level, out=code)
+                # as in the c5 step: the record compaction runs on its own stream beside the decode
+                # (which reads the encoder's unit map) and is joined before the step ends
+                cur = torch.cuda.current_stream()
+                s_cmp.wait_stream(cur)
+                mns.encode_device(img, cfg, root_level=root_level, out=code, compact_stream=s_cmp)
                 mns.decode_device(code, iters=iters, stop_delta=0.0, initial_value=128.0, out=u8, rasters=rasters)
+                cur.wait_stream(s_cmp)
 
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
