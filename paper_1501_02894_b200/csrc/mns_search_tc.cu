@@ -577,45 +577,47 @@ __global__ void __launch_bounds__(128) pool_tc_kernel(const uint8_t *img, int W,
                                                       long long ndom_pad, uint16_t *pool, int32_t *psq,
                                                       long long *pD, __half *Q, float2 *consts) {
     constexpr int n = B * B;
-    const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (d >= ndom_pad) return;
+    constexpr int RS = BK / 8 + 1;  // staged row stride in 16-B chunks (one pad chunk: conflict-free)
+    __shared__ uint4 sq_rows[128 * RS], sp_rows[n == 64 ? 128 * RS : 1];
+    const int tid = threadIdx.x;
+    const long long d0 = blockIdx.x * 128ll, d = d0 + tid;  // ndom_pad is a multiple of 128
     float *cf = reinterpret_cast<float *>(consts) + (d / BN) * 2 * BN + d % BN;
-    uint4 *qrow = reinterpret_cast<uint4 *>(Q + d * BK);
-    if (d >= ndom) {
-        for (int i = 0; i < BK / 8; i++) qrow[i] = make_uint4(0, 0, 0, 0);
-        cf[0] = 0.f;
-        cf[BN] = 0.f;
-        return;
-    }
-    const int x = (int)(d % ndx) * step, y = (int)(d / ndx) * step;
     int q[n];
     int sq = 0;
     long long sqq = 0;
+    if (d < ndom) {
+        const int x = (int)(d % ndx) * step, y = (int)(d / ndx) * step;
 #pragma unroll
-    for (int i = 0; i < B; i++) {
-        const uint8_t *p0 = img + (size_t)(y + 2 * i) * W + x, *p1 = p0 + W;
+        for (int i = 0; i < B; i++) {
+            const uint8_t *p0 = img + (size_t)(y + 2 * i) * W + x, *p1 = p0 + W;
 #pragma unroll
-        for (int j = 0; j < B; j++) {
-            const int v = (int)__ldg(p0 + 2 * j) + __ldg(p0 + 2 * j + 1) + __ldg(p1 + 2 * j) + __ldg(p1 + 2 * j + 1);
-            q[i * B + j] = v;
-            sq += v;
-            sqq += v * v;
+            for (int j = 0; j < B; j++) {
+                const int v = (int)__ldg(p0 + 2 * j) + __ldg(p0 + 2 * j + 1) + __ldg(p1 + 2 * j) + __ldg(p1 + 2 * j + 1);
+                q[i * B + j] = v;
+                sq += v;
+                sqq += v * v;
+            }
         }
-    }
-    const long long D = n * sqq - (long long)sq * sq;
-    psq[d] = sq;
-    pD[d] = D;
-    if (n >= 8) {
-#pragma unroll
-        for (int k = 0; k < n; k += 8)
-            reinterpret_cast<uint4 *>(pool + d * n)[k / 8] =
-                make_uint4((uint32_t)q[k] | ((uint32_t)q[k + 1] << 16), (uint32_t)q[k + 2] | ((uint32_t)q[k + 3] << 16),
-                           (uint32_t)q[k + 4] | ((uint32_t)q[k + 5] << 16), (uint32_t)q[k + 6] | ((uint32_t)q[k + 7] << 16));
     } else {
 #pragma unroll
-        for (int k = 0; k < n; k++) pool[d * n + k] = (uint16_t)q[k];
+        for (int k = 0; k < n; k++) q[k] = 0;
     }
-    const bool ok = D > 0;
+    const long long D = n * sqq - (long long)sq * sq;
+    if (d < ndom) {
+        psq[d] = sq;
+        pD[d] = D;
+        if (n == 64) {
+#pragma unroll
+            for (int k = 0; k < n; k += 8)
+                sp_rows[tid * RS + k / 8] =
+                    make_uint4((uint32_t)q[k] | ((uint32_t)q[k + 1] << 16), (uint32_t)q[k + 2] | ((uint32_t)q[k + 3] << 16),
+                               (uint32_t)q[k + 4] | ((uint32_t)q[k + 5] << 16), (uint32_t)q[k + 6] | ((uint32_t)q[k + 7] << 16));
+        } else {
+#pragma unroll
+            for (int k = 0; k < n; k++) pool[d * n + k] = (uint16_t)q[k];
+        }
+    }
+    const bool ok = d < ndom && D > 0;
     const float mean = (float)sq / (float)n;  // exact: Sq < 2^18, n a power of two
     const float inv = ok ? 1.0f / sqrtf((float)D) : 0.f;
     uint32_t h[BK / 2];
@@ -627,9 +629,18 @@ __global__ void __launch_bounds__(128) pool_tc_kernel(const uint8_t *img, int W,
         h[k / 2] = *reinterpret_cast<const uint32_t *>(&hv);
     }
 #pragma unroll
-    for (int i = 0; i < BK / 8; i++) qrow[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-    cf[0] = -(float)sq;
-    cf[BN] = __fsqrt_rd(__ll2float_rd(D));
+    for (int i = 0; i < BK / 8; i++) sq_rows[tid * RS + i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+    cf[0] = d < ndom ? -(float)sq : 0.f;
+    cf[BN] = d < ndom ? __fsqrt_rd(__ll2float_rd(D)) : 0.f;
+    __syncthreads();
+    // the CTA's 128 rows are contiguous in global memory: coalesced 16-B stores
+    uint4 *Qo = reinterpret_cast<uint4 *>(Q + d0 * BK);
+    for (int c = tid; c < 128 * (BK / 8); c += 128) Qo[c] = sq_rows[(c / (BK / 8)) * RS + c % (BK / 8)];
+    if (n == 64) {
+        const int rows = (int)min(128ll, ndom - d0);
+        uint4 *Po = reinterpret_cast<uint4 *>(pool + d0 * n);
+        for (int c = tid; c < rows * 8; c += 128) Po[c] = sp_rows[(c / 8) * RS + c % 8];
+    }
 }
 
 // Range operand rows (range, isometry), one warp per row: raw r (exact recompute) and centred
