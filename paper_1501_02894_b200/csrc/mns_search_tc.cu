@@ -703,9 +703,11 @@ __global__ void gather_sample_kernel(const float2 *consts, const long long *pD, 
 }
 
 // Seeds every range's best key before the prepass (which otherwise starts without a threshold):
-// one warp per range, exact values of the domains around the co-centred one (offsets in
-// {-B, -B/2, 0, B/2, B}^2, clamped and snapped to the stride) against every isometry row of the
-// range, atomicMin.  Seeds are real candidates, so the final argmin is unchanged.
+// one warp per range.  The domains around the co-centred one (offsets in {-B, -B/2, 0, B/2, B}^2,
+// clamped and snapped to the stride) are scored against every isometry row of the range by the
+// continuous bound N^2/D -- lane = (isometry, quarter of the 64 pixels), 16 integer MACs and two
+// shuffles per candidate -- and the best one is evaluated exactly (any real candidate is a valid
+// seed; the final argmin is unchanged).
 __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const uint16_t *pool, const int32_t *psq,
                                  const long long *pD, int W, int B, int step, int ndx, int ndy, int n_iso, int r0,
                                  int n_ranges, unsigned long long *best) {
@@ -714,54 +716,61 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
     if (rr >= n_ranges) return;
     const int n = B * B, ri = r0 + rr, rpr = W / B;
     const int rx = (ri % rpr) * B, ry = (ri / rpr) * B, sr = row_sr[rr * n_iso];
-    int ra[8], rb[8];
+    const int t = lane >> 2, k0 = (lane & 3) * 16;  // this lane: isometry t, pixels k0 .. k0 + 15
+    const bool tl = t < n_iso;
+    int rk[16];
+    {
+        const __half *ar = A + (size_t)(rr * n_iso + (tl ? t : 0)) * BK + k0;
 #pragma unroll
-    for (int t = 0; t < 8; t++) {
-        const __half *ar = A + (size_t)(rr * n_iso + (t < n_iso ? t : 0)) * BK;
-        ra[t] = lane < n ? __half2int_rn(ar[lane]) : 0;
-        rb[t] = lane + 32 < n ? __half2int_rn(ar[lane + 32]) : 0;
+        for (int k = 0; k < 16; k++) rk[k] = tl && k0 + k < n ? __half2int_rn(ar[k]) : 0;
     }
-    // pick the candidate with the best continuous estimate -N^2/D (any real candidate is a valid seed),
-    // then evaluate that one exactly
     float best_est = -1.f;
-    long long bd = -1;
-    int bt = 0, bc = 0;
-    for (int c0 = 0; c0 < 25; c0 += 5) {  // a row of five candidates: all loads in flight together
-        long long dd[5];
-        float sqf[5], idf[5];
-        int qa[5], qb[5];
+    int bd = -1, bc = 0;
+    for (int c = 0; c < 25; c++) {
+        const int ox = (c % 5 - 2) * B / 2, oy = (c / 5 - 2) * B / 2;
+        const int dx = clampi((rx - B / 2 + ox) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy) / step, 0, ndy - 1);
+        const int d = dy * ndx + dx;
+        const uint16_t *qd = pool + (long long)d * n + k0;
+        int part = 0;
 #pragma unroll
-        for (int c = 0; c < 5; c++) {
-            const int ox = (c - 2) * B / 2, oy = (c0 / 5 - 2) * B / 2;
-            const int dx = clampi((rx - B / 2 + ox) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy) / step, 0, ndy - 1);
-            dd[c] = (long long)dy * ndx + dx;
-            const uint16_t *qd = pool + dd[c] * n;
-            qa[c] = lane < n ? (int)qd[lane] : 0;
-            qb[c] = lane + 32 < n ? (int)qd[lane + 32] : 0;
-            sqf[c] = (float)psq[dd[c]] * (float)sr;
-            const long long D = pD[dd[c]];
-            idf[c] = D > 0 ? 1.f / (float)D : 0.f;
-        }
-#pragma unroll
-        for (int c = 0; c < 5; c++) {
-#pragma unroll
-            for (int t = 0; t < 8; t++) {
-                if (t >= n_iso) break;
-                const int C = __reduce_add_sync(0xffffffffu, qa[c] * ra[t] + qb[c] * rb[t]);  // < 2^24
-                const float N = fmaf((float)n, (float)C, -sqf[c]);
-                const float est = N * N * idf[c];
-                if (est > best_est) {
-                    best_est = est;
-                    bd = dd[c];
-                    bt = t;
-                    bc = C;
-                }
-            }
+        for (int k = 0; k < 16; k++) part += (k0 + k < n ? (int)__ldg(qd + k) : 0) * rk[k];
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);  // C of (candidate c, isometry t), exact (< 2^24)
+        const long long D = __ldg(pD + d);
+        const float N = fmaf((float)n, (float)part, -(float)__ldg(psq + d) * (float)sr);
+        const float est = D > 0 && tl ? N * N / (float)D : -1.f;
+        if (est > best_est) {
+            best_est = est;
+            bd = d;
+            bc = part;
         }
     }
-    const long long N = (long long)n * bc - (long long)psq[bd] * sr;  // exact
-    const unsigned long long kbest = make_key(best_val_exact(N, pD[bd]), bd * n_iso + bt);
-    if (lane == 0) atomicMin(&best[rr], kbest);
+    // warp argmax of the estimate (ties: any -- every candidate is valid)
+    int bt = t;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        const float e2 = __shfl_xor_sync(0xffffffffu, best_est, o);
+        const int d2 = __shfl_xor_sync(0xffffffffu, bd, o), c2 = __shfl_xor_sync(0xffffffffu, bc, o),
+                  t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (e2 > best_est) {
+            best_est = e2;
+            bd = d2;
+            bc = c2;
+            bt = t2;
+        }
+    }
+    if (lane == 0) {
+        if (bd < 0) {  // flat range or flat domains only: the co-centred domain, isometry 0
+            bd = clampi((ry - B / 2) / step, 0, ndy - 1) * ndx + clampi((rx - B / 2) / step, 0, ndx - 1);
+            bt = 0;
+            const uint16_t *qd = pool + (long long)bd * n;
+            const __half *ar = A + (size_t)(rr * n_iso) * BK;
+            bc = 0;
+            for (int k = 0; k < n; k++) bc += (int)qd[k] * __half2int_rn(ar[k]);
+        }
+        const long long N = (long long)n * bc - (long long)psq[bd] * sr;  // exact
+        atomicMin(&best[rr], make_key(best_val_exact(N, pD[bd]), (long long)bd * n_iso + bt));
+    }
 }
 
 __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, unsigned long long *key) {
