@@ -716,17 +716,21 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
     if (rr >= n_ranges) return;
     const int n = B * B, ri = r0 + rr, rpr = W / B;
     const int rx = (ri % rpr) * B, ry = (ri / rpr) * B, sr = row_sr[rr * n_iso];
-    const int t = lane >> 2, k0 = (lane & 3) * 16;  // this lane: isometry t, pixels k0 .. k0 + 15
-    const bool tl = t < n_iso;
+    // lane = (slot, quarter): slot s = lane / 4 scores the (candidate, isometry) pairs s, s + 8, ... of
+    // the 25 * n_iso pairs (n_iso in {1, 8}, so a lane's isometry t = s % n_iso is fixed)
+    const int sl = lane >> 2, k0 = (lane & 3) * 16, t = sl % n_iso;
     int rk[16];
     {
-        const __half *ar = A + (size_t)(rr * n_iso + (tl ? t : 0)) * BK + k0;
+        const __half *ar = A + (size_t)(rr * n_iso + t) * BK + k0;
 #pragma unroll
-        for (int k = 0; k < 16; k++) rk[k] = tl && k0 + k < n ? __half2int_rn(ar[k]) : 0;
+        for (int k = 0; k < 16; k++) rk[k] = k0 + k < n ? __half2int_rn(ar[k]) : 0;
     }
     float best_est = -1.f;
     int bd = -1, bc = 0;
-    for (int c = 0; c < 25; c++) {
+    for (int p0 = 0; p0 < 25 * n_iso; p0 += 8) {
+        const int pi = p0 + sl;
+        const bool valid = pi < 25 * n_iso;
+        const int c = valid ? pi / n_iso : 0;
         const int ox = (c % 5 - 2) * B / 2, oy = (c / 5 - 2) * B / 2;
         const int dx = clampi((rx - B / 2 + ox) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy) / step, 0, ndy - 1);
         const int d = dy * ndx + dx;
@@ -738,7 +742,7 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
         part += __shfl_xor_sync(0xffffffffu, part, 2);  // C of (candidate c, isometry t), exact (< 2^24)
         const long long D = __ldg(pD + d);
         const float N = fmaf((float)n, (float)part, -(float)__ldg(psq + d) * (float)sr);
-        const float est = D > 0 && tl ? N * N / (float)D : -1.f;
+        const float est = valid && D > 0 ? N * N / (float)D : -1.f;
         if (est > best_est) {
             best_est = est;
             bd = d;
