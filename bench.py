@@ -152,16 +152,55 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------- CPU legs
 
-def cpu_sample(img: np.ndarray, rows: int = 2048, threads: int | None = None):
-    """Oracle encode + 10-sweep decode of the top `rows` rows of the c5 image (own image)."""
+def cpu_sample(img: np.ndarray, rows: int = 2048, threads: int | None = None, keep: bool = False):
+    """Oracle encode + 10-sweep decode of the top `rows` rows of the c5 image (own image).
+    keep=True also returns the oracle's records, per-root counts and decoded image (the parity check)."""
     from oracle import oracle as O
 
     s = np.ascontiguousarray(img[:rows])
     t0 = time.perf_counter()
-    rec, _ = O.encode_quadtree_records(s, (8.0, 8.0, math.inf), 16.0, True, 1, nthreads=threads)
-    O.decode_records(rec, s.shape[1], s.shape[0], max_iters=ITERS, stop_delta=0.0, nthreads=threads)
+    rec, counts = O.encode_quadtree_records(s, (8.0, 8.0, math.inf), 16.0, True, 1, nthreads=threads)
+    out, _, _ = O.decode_records(rec, s.shape[1], s.shape[0], max_iters=ITERS, stop_delta=0.0, nthreads=threads)
     dt = time.perf_counter() - t0
+    if keep:
+        return s.size / 64 / dt, dt, (rec, counts, out)
     return s.size / 64 / dt, dt
+
+
+def parity_check(img_np, got_rec, got_offs, got_out, r0, r1, oracle_result=None):
+    """The benchmarked output against the CPU oracle (north_star's bar): this rank's strip of the c5
+    code bit-exact (records and root offsets) and its decoded rows within 1 LSB and 0.01 dB."""
+    from oracle import oracle as O
+
+    if oracle_result is None:
+        rec, counts = O.encode_quadtree_records(img_np, (8.0, 8.0, math.inf), 16.0, True, 1)
+        out, _, _ = O.decode_records(rec, img_np.shape[1], img_np.shape[0], max_iters=ITERS, stop_delta=0.0)
+    else:
+        rec, counts, out = oracle_result
+    rw = img_np.shape[1] // 16
+    offs = np.zeros(len(counts) + 1, np.int64)
+    np.cumsum(counts, out=offs[1:])
+    a, b = offs[r0 * rw], offs[r1 * rw]
+    want_rec = rec[a:b]
+    want_offs = offs[r0 * rw: r1 * rw + 1] - a
+    rec_ok = len(got_rec) == len(want_rec) and bool(np.array_equal(got_rec, want_rec))
+    offs_ok = bool(np.array_equal(got_offs.astype(np.int64), want_offs))
+    rows = slice(16 * r0, 16 * r1)
+    src = img_np[rows].astype(np.float64)
+    want = out[rows]
+    d = np.abs(got_out.astype(np.int16) - want.astype(np.int16))
+
+    def psnr(x):
+        e = float(np.mean((src - x.astype(np.float64)) ** 2))
+        return math.inf if e == 0 else 10 * math.log10(255 * 255 / e)
+
+    dpsnr = abs(psnr(got_out) - psnr(want))
+    return {"codes": "bit-exact" if rec_ok and offs_ok else "MISMATCH", "records": int(len(got_rec)),
+            "oracle_records": int(len(want_rec)), "decode_max_lsb": int(d.max()),
+            "pixels_off_by_1": int((d == 1).sum()), "psnr_delta_db": dpsnr,
+            "pass": bool(rec_ok and offs_ok and int(d.max()) <= 1 and dpsnr <= 0.01),
+            "scope": f"root rows {r0}..{r1 - 1} of 1024 (rank 0's strip) vs the fp64 CPU oracle "
+                     "(oracle/mns_oracle.c, pinned to reference goldens)"}
 
 
 def run_reference(args, img):
@@ -497,6 +536,17 @@ def run_ours(args, img_np, rank, world, local_rank):
 
     small = None if args.no_small else small_configs(dev, rank, world)
 
+    # the benchmarked output, read back after timing for the parity check (one more untimed step)
+    final = None
+    if not args.no_parity:  # every rank steps (the decode exchanges halos); rank 0 checks its strip
+        step()
+        stream.wait_stream(s_cmp)
+        torch.cuda.synchronize()
+    if rank == 0 and not args.no_parity:
+        n_rec = int(code.count.item())
+        final = {"rec": code.records[:n_rec].cpu().numpy().view(np.uint64),
+                 "offs": code.root_offsets.cpu().numpy(), "out": dec.out.cpu().numpy()}
+
     if rank != 0:
         return
     hbm, which = peaks()
@@ -505,11 +555,16 @@ def run_ours(args, img_np, rank, world, local_rank):
     algo = (2.0 if dec.lattice else 8.0) * own_px
     kname = "decode_pair_lat_kernel" if dec.lattice else "decode_pair_kernel"
     achieved = algo / (pass_ms / 1e3) / 1e9
-    cpu_v, cpu_dt = (None, None)
+    cpu_v, cpu_dt, oracle_result = (None, None, None)
     if world == 1 and not args.no_cpu:
         from oracle import oracle as O
 
-        cpu_v, cpu_dt = cpu_sample(img_np, args.cpu_baseline_rows, O.default_threads())
+        cpu_v, cpu_dt, oracle_result = cpu_sample(img_np, args.cpu_baseline_rows, O.default_threads(), keep=True)
+        if args.cpu_baseline_rows != IMG:
+            oracle_result = None
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(img_np, final["rec"], final["offs"], final["out"], r0, r1, oracle_result)
     launches_per_step = 2 + n_launch  # encode + compaction kernels + decode passes (+ memsets, not kernels)
     line = {
         "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
@@ -541,6 +596,7 @@ def run_ours(args, img_np, rank, world, local_rank):
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
         "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": int(host.numel()) * world,
                 "d2h_bytes_per_step": int(out_host.numel()) * world},
+        "parity": parity,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
@@ -557,6 +613,7 @@ def main():
     ap.add_argument("--cpu-baseline-rows", type=int, default=IMG,
                     help="rows of the c5 image the cpu_baseline leg encodes + decodes (default: all of it)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle check of the output")
     ap.add_argument("--no-search", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the c1/c2 graph-replay latency and c3 batch legs")
     args = ap.parse_args()

@@ -183,6 +183,34 @@ int mns_decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usi
                         const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
                         int32_t height, const double *cur, double *out, void *stream);
 
+/* Replaces: decoder.decode (decoder.py:66-77) EXACTLY, including the early stop: every sweep is
+ * the bit-exact fp64 step above, the sweep's max|nxt - current| is an exact fp64 max, and the
+ * stop test `delta < stop_delta` runs on the device (later sweeps are no-ops), so the sweep count
+ * and the uint8 image (clip(floor(x + 0.5))) equal the reference's bit for bit.  Used for
+ * stop_delta > 0 (the default DecodeConfig); the fp32 decoders serve stop_delta = 0.  ping/pong:
+ * fp64 [height][width]; *d_iters_done = sweeps run; workspace >= 32 bytes. */
+int mns_decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                   const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                   int32_t height, int32_t max_iters, double stop_delta, double initial_value, double *ping,
+                   double *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                   void *stream);
+
+/* The building blocks of mns_decode_f64 for strip sharding (decoder.py:70-75 per rank, the delta
+ * all-reduced between mns_decode_f64_sweep and mns_decode_f64_decide).  state: int64[4] zeroed by
+ * the caller ([0] converged, [1] sweeps done, [2] the sweep's max|delta| as fp64 bits).  cur/nxt
+ * may be "virtual global" base pointers (row 0 of the image) of resident strips.
+ * mns_records_to_units expands n packed records into 4n unit slots (decoder.py:48-59; unused
+ * slots get size 0 and are skipped). */
+int mns_records_to_units(const uint64_t *records, int64_t n_records, int32_t width, int32_t height, int32_t *ux,
+                         int32_t *uy, int32_t *usize, int32_t *udx, int32_t *udy, double *us, double *uo,
+                         void *stream);
+int mns_decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                         const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                         const double *cur, double *nxt, int64_t *state, void *stream);
+int mns_decode_f64_decide(int64_t *state, double stop_delta, void *stream);
+int mns_decode_f64_finalize(const double *ping, const double *pong, const int64_t *state, int32_t width,
+                            int32_t row_begin, int32_t row_end, uint8_t *out, int32_t *d_iters_done, void *stream);
+
 /* Replaces: encoder.encode_full_search (encoder.py:249-309).  Ranges: the
  * non-overlapping B x B blocks of the B-padded raster in raster order (range
  * ids [range_begin, range_end) -- range sharding).  Domain pool: every 2B x 2B

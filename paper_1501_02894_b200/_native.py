@@ -66,6 +66,11 @@ def _declare(L):
         "mns_decode_unit_map_lattice": [P, I32, I32, I32, F, P, P, P, P, P, I64, P],
         "mns_decode_units": [P, P, P, P, P, P, P, I64, I32, I32, I32, D, F, P, P, P, P, P, I64, P],
         "mns_decode_step_f64": [P, P, P, P, P, P, P, I64, I32, I32, P, P, P],
+        "mns_decode_f64": [P, P, P, P, P, P, P, I64, I32, I32, I32, D, D, P, P, P, P, P, I64, P],
+        "mns_records_to_units": [P, I64, I32, I32, P, P, P, P, P, P, P, P],
+        "mns_decode_f64_sweep": [P, P, P, P, P, P, P, I64, I32, P, P, P, P],
+        "mns_decode_f64_decide": [P, D, P],
+        "mns_decode_f64_finalize": [P, P, P, I32, I32, I32, P, P, P],
         "mns_search_workspace_bytes": [I32, I32, I32, I32, I32, P],
         "mns_full_search": [P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, I64, P],
         "mns_local_search": [P, I32, I32, I32, P, P, P, P, P],
@@ -89,7 +94,9 @@ def _declare(L):
 
 EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_encode_quadtree_split", "mns_try_node", "mns_build_unit_map", "mns_decode_workspace_bytes", "mns_decode_quadtree",
            "mns_decode_sweep", "mns_decode_sweep2", "mns_decode_pass_lattice",
-           "mns_decode_flat_lattice", "mns_decode_quadtree_lattice", "mns_decode_unit_map_lattice", "mns_decode_units", "mns_decode_step_f64", "mns_search_workspace_bytes", "mns_full_search",
+           "mns_decode_flat_lattice", "mns_decode_quadtree_lattice", "mns_decode_unit_map_lattice", "mns_decode_units", "mns_decode_step_f64",
+           "mns_decode_f64", "mns_records_to_units", "mns_decode_f64_sweep", "mns_decode_f64_decide",
+           "mns_decode_f64_finalize", "mns_search_workspace_bytes", "mns_full_search",
            "mns_local_search", "mns_stream_workspace_bytes", "mns_write_stream", "mns_read_stream_workspace_bytes", "mns_read_stream",
            "mns_image_sse", "mns_code_stats", "mns_offset_histogram",
            "mns_last_error",

@@ -109,8 +109,18 @@ class DeviceCode:
     unit_map: "object" = None  # torch.int32 [n_roots * 32]: decoder unit map (mns_record.h), optional
     min_leaf: int = 0          # smallest painted unit side if known (4: no 2x2 units -> lattice-state decode), 0 unknown
     unit_map_valid: bool = False  # unit_map holds this code's map (emitted by the encoder / build_unit_map)
+    compact_event: "object" = None  # set by encode_device(compact_stream=...): records/count valid after it
+    decode_error: "object" = None   # set by decode_device on the lattice path (device int32 flag)
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: current) wait until records / root_offsets / count are complete
+        (they are produced on the compaction stream when encode_device got one)."""
+        if self.compact_event is not None:
+            torch = _torch()
+            (stream if stream is not None else torch.cuda.current_stream()).wait_event(self.compact_event)
 
     def n_records(self) -> int:
+        self.join()
         return int(self.count.item())
 
 
@@ -183,12 +193,16 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
                                       ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
                                       N.ptr(out.root_offsets), N.ptr(out.count), N.ptr(out.unit_map), N.ptr(ws),
                                       ws.numel(), N.stream_ptr(stream)))
+        out.compact_event = None
     else:  # records / root_offsets / count become valid on compact_stream (the unit map on stream)
         N.check(L.mns_encode_quadtree_split(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
                                             ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
                                             N.ptr(out.root_offsets), N.ptr(out.count), N.ptr(out.unit_map),
                                             N.ptr(ws), ws.numel(), N.stream_ptr(stream),
                                             N.stream_ptr(compact_stream)))
+        if out.compact_event is None:
+            out.compact_event = torch.cuda.Event()
+        out.compact_event.record(compact_stream)
     return out
 
 
@@ -199,6 +213,7 @@ def build_unit_map(code: DeviceCode, stream=None):
     r0, r1 = code.root_row_begin, code.root_row_end or code.padded_h // 16
     n_roots = (code.padded_w // 16) * (r1 - r0)
     code.unit_map = torch.empty(32 * n_roots, dtype=torch.int32, device=code.records.device)
+    code.join(stream)
     N.check(L.mns_build_unit_map(N.ptr(code.records), N.ptr(code.root_offsets), code.padded_w, r0, r1,
                                  N.ptr(code.unit_map), N.stream_ptr(stream)))
     code.unit_map_valid = True
@@ -216,12 +231,14 @@ def min_leaf_side(code: DeviceCode) -> int:
 
 
 def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, initial_value: float = 128.0,
-                  out=None, rasters=None, want_u8: bool = True, stream=None):
+                  out=None, rasters=None, want_u8: bool = True, stream=None, lattice=None):
     """Jacobi decode of a device quadtree code (single image); returns (uint8 [H, W] padded, iters_done tensor).
 
     Codes without 2x2 units decoded to uint8 with stop_delta == 0 run on lattice state
     (mns_decode_quadtree_lattice: a quarter of the raster traffic, identical output); the rest on
-    fp32 rasters (mns_decode_quadtree).
+    fp32 rasters (mns_decode_quadtree).  ``code.decode_error`` (device int32) is set to 1 by a lattice
+    decode that met a 2x2 unit (a wrong ``min_leaf``); callers that sync check it and rerun with
+    ``lattice=False`` (``decode`` does).
     """
     torch = _torch()
     L = N.lib()
@@ -234,23 +251,27 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
         out = torch.empty((H, W), dtype=torch.uint8, device=dev)
     wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
     ws = _WS.get("dec", wsb, dev)
-    if want_u8 and stop_delta == 0.0 and min_leaf_side(code) >= 4:
+    if want_u8 and stop_delta == 0.0 and lattice is not False and min_leaf_side(code) >= 4:
         it = torch.full((1,), int(iters), dtype=torch.int32, device=dev)
         err = torch.empty(1, dtype=torch.int32, device=dev)  # zeroed by the library
         n_lat = (H // 2) * (W // 2)
         lat = (rasters[0].view(-1)[:n_lat], rasters[1].view(-1)[:n_lat])
         whole = code.n_images == 1 and code.root_row_begin == 0 and code.root_row_end in (0, H // 16)
+        code.decode_error = err  # 1 if a 2x2 unit was met (min_leaf wrong): rerun with lattice=False
         if code.unit_map is not None and code.unit_map_valid and whole:
             # the encoder's own unit map: no rebuild from the records
             N.check(L.mns_decode_unit_map_lattice(N.ptr(code.unit_map), W, H, int(iters), float(initial_value),
                                                   N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out), N.ptr(err), N.ptr(ws),
                                                   ws.numel(), N.stream_ptr(stream)))
         else:
+            code.join(stream)
             N.check(L.mns_decode_quadtree_lattice(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters),
                                                   float(initial_value), N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out),
                                                   N.ptr(err), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
         return out, it, rasters
     it = torch.zeros(1, dtype=torch.int32, device=dev)
+    code.decode_error = None
+    code.join(stream)
     N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters), float(stop_delta),
                                   float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),
                                   N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
@@ -509,6 +530,8 @@ def decode(code, config: Optional[DecodeConfig] = None) -> GrayImage:
                            torch.tensor([len(rec)], dtype=torch.int64, device=dev), W, H,
                            min_leaf=2 if unit2 else 4)
         out, _, _ = decode_device(dcode, cfg.max_iters, cfg.stop_delta, cfg.initial_value)
+        if dcode.decode_error is not None and int(dcode.decode_error.item()):
+            out, _, _ = decode_device(dcode, cfg.max_iters, cfg.stop_delta, cfg.initial_value, lattice=False)
     else:
         u = _units_to_device(_baseline_units(code), np.float32)
         out, _ = decode_units_device(u, W, H, cfg.max_iters, cfg.stop_delta, cfg.initial_value)

@@ -126,6 +126,18 @@ int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, con
 int decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
                     const int32_t *udy, const double *us, const double *uo, int64_t n, int W, int H,
                     const double *cur, double *out, cudaStream_t stream);
+int decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx, const int32_t *udy,
+               const double *us, const double *uo, int64_t n, int W, int H, int iters, double stop_delta,
+               double init, double *ping, double *pong, uint8_t *out, int32_t *d_iters_done, void *workspace,
+               int64_t workspace_bytes, cudaStream_t st);
+int records_to_units(const uint64_t *records, int64_t n, int W, int H, int32_t *ux, int32_t *uy, int32_t *usize,
+                     int32_t *udx, int32_t *udy, double *us, double *uo, cudaStream_t st);
+int decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                     const int32_t *udy, const double *us, const double *uo, int64_t n, int W, const double *cur,
+                     double *nxt, int64_t *state, cudaStream_t st);
+int decode_f64_decide(int64_t *state, double stop_delta, cudaStream_t st);
+int decode_f64_finalize(const double *ping, const double *pong, const int64_t *state, int W, int y0, int y1,
+                        uint8_t *out, int32_t *iters_done, cudaStream_t st);
 int search_workspace_bytes(int W, int H, int B, int step, int n_iso, int64_t *bytes);
 int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1, int32_t *out_dom,
                 int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st);
@@ -292,6 +304,40 @@ int mns_decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usi
                         int32_t height, const double *cur, double *out, void *stream) {
     GUARD(mns::decode_step_f64(ux, uy, usize, udx, udy, us, uo, n_units, width, height, cur, out,
                                (cudaStream_t)stream));
+}
+
+int mns_decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                   const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                   int32_t height, int32_t max_iters, double stop_delta, double initial_value, double *ping,
+                   double *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                   void *stream) {
+    GUARD(mns::decode_f64(ux, uy, usize, udx, udy, us, uo, n_units, width, height, max_iters, stop_delta,
+                          initial_value, ping, pong, out, d_iters_done, workspace, workspace_bytes,
+                          (cudaStream_t)stream));
+}
+
+int mns_records_to_units(const uint64_t *records, int64_t n_records, int32_t width, int32_t height, int32_t *ux,
+                         int32_t *uy, int32_t *usize, int32_t *udx, int32_t *udy, double *us, double *uo,
+                         void *stream) {
+    GUARD(mns::records_to_units(records, n_records, width, height, ux, uy, usize, udx, udy, us, uo,
+                                (cudaStream_t)stream));
+}
+
+int mns_decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                         const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
+                         const double *cur, double *nxt, int64_t *state, void *stream) {
+    GUARD(mns::decode_f64_sweep(ux, uy, usize, udx, udy, us, uo, n_units, width, cur, nxt, state,
+                                (cudaStream_t)stream));
+}
+
+int mns_decode_f64_decide(int64_t *state, double stop_delta, void *stream) {
+    GUARD(mns::decode_f64_decide(state, stop_delta, (cudaStream_t)stream));
+}
+
+int mns_decode_f64_finalize(const double *ping, const double *pong, const int64_t *state, int32_t width,
+                            int32_t row_begin, int32_t row_end, uint8_t *out, int32_t *d_iters_done, void *stream) {
+    GUARD(mns::decode_f64_finalize(ping, pong, state, width, row_begin, row_end, out, d_iters_done,
+                                   (cudaStream_t)stream));
 }
 
 int mns_search_workspace_bytes(int32_t width, int32_t height, int32_t B, int32_t step, int32_t n_iso,

@@ -53,6 +53,21 @@ __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? l
 
 // Isometry t of a B x B block (full-search extension; the reference has none):
 // d_t(i, j) = d(src_t(i, j)); t = 0 is the identity.
+// Search argmin keys: (val + 2^(63-cb)) << cb | candidate, lexicographic = (value, first index).
+// |val| = |min_k2 (k2^2 D - 64 k2 N)| < n^2 * 4.18e7 (|N| <= n^2 * 65025 by Cauchy-Schwarz,
+// D <= n^2 * 260100), so the value needs 31/35/39/43 bits at n = 4/16/64/256 and the candidate
+// index gets the rest: 33/29/25/21 bits (B = 8: 2^25 (domain, isometry) pairs).
+__host__ __device__ inline int key_cand_bits(int n) { return n <= 4 ? 33 : n <= 16 ? 29 : n <= 64 ? 25 : 21; }
+__host__ __device__ inline unsigned long long make_key_cb(long long val, long long cand, int cb) {
+    return ((unsigned long long)(val + (1ll << (63 - cb))) << cb) | (unsigned long long)cand;
+}
+__host__ __device__ inline long long key_val(unsigned long long key, int cb) {
+    return (long long)(key >> cb) - (1ll << (63 - cb));
+}
+__host__ __device__ inline long long key_cand(unsigned long long key, int cb) {
+    return (long long)(key & ((1ull << cb) - 1));
+}
+
 __host__ __device__ inline int iso_src(int t, int i, int j, int B) {
     switch (t) {
     case 0: return i * B + j;                      // identity

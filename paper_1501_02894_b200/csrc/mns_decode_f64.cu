@@ -1,0 +1,219 @@
+// Exact fp64 Jacobi decode with the reference's early stop (decoder.py:66-77).
+//
+// The reference iterates decode_step in float64 and stops after the first sweep whose
+// max|nxt - current| is below stop_delta (decoder.py:70-75).  An fp32 raster cannot make that
+// decision exactly (a sweep whose true delta lies within fp32 error of stop_delta could stop one
+// sweep early or late), so codes decoded with stop_delta > 0 run here: every sweep is the
+// bit-exact fp64 step of decode_step_f64 (numpy's downsample order, pairwise mean, unfused
+// mul/add, clip), the sweep's max|delta| is an exact fp64 max (order-independent) folded into a
+// state word, and a one-thread kernel applies the reference's test.  Sweeps after convergence are
+// no-ops (every kernel reads the converged flag first), so the host enqueues max_iters sweeps
+// with no synchronisation; the final uint8 image is clip(floor(x + 0.5)) of the raster that holds
+// the last sweep -- bit-identical to the reference's decode.
+//
+// Strips (multi-GPU): the same kernels on a rank's strip with a 16-row halo ("virtual global"
+// base pointers); between the sweep and the decision the caller all-reduces (max) the state's
+// delta word over the ranks (sharding.StripDecoderF64), so every rank stops at the same sweep.
+//
+// State (int64[4]): [0] converged flag, [1] sweeps done, [2] this sweep's max|delta| (fp64 bits,
+// non-negative, so the integer max is the fp64 max), [3] spare.
+
+#include <math.h>
+
+#include "mns_common.cuh"
+#include "mns_record.h"
+
+namespace mns {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// One unit of decode_step (decoder.py:32-63, transform.py:63-66) in the reference's fp64 order.
+// Returns this unit's max |v - cur| over its pixels.
+__device__ double paint_unit_f64(int x, int y, int size, int dx, int dy, double s, double o, int W,
+                                 const double *cur, double *out) {
+    const int m = size * size;
+    double d[256];
+    for (int i = 0; i < size; i++)
+        for (int j = 0; j < size; j++) {
+            const double *pp = cur + (size_t)(dy + 2 * i) * W + dx + 2 * j;
+            d[i * size + j] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), pp[W]), pp[W + 1]), 0.25);
+        }
+    const double dm = __ddiv_rn(pw_sum_dev(d, m), (double)m);
+    double dmax = 0.0;
+    for (int i = 0; i < size; i++)
+        for (int j = 0; j < size; j++) {
+            double v = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * size + j], dm)), o);
+            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+            const size_t idx = (size_t)(y + i) * W + x + j;
+            dmax = fmax(dmax, fabs(__dsub_rn(v, cur[idx])));
+            out[idx] = v;
+        }
+    return dmax;
+}
+
+__global__ void __launch_bounds__(256) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
+                                                        const int32_t *udx, const int32_t *udy, const double *us,
+                                                        const double *uo, long long n, int W, const double *cur,
+                                                        double *nxt, long long *state) {
+    if (state[0]) return;  // converged in an earlier sweep
+    const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    double dmax = 0.0;
+    if (u < n && usize[u] > 0)
+        dmax = paint_unit_f64(ux[u], uy[u], usize[u], udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+    long long bits = __double_as_longlong(dmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
+    if ((threadIdx.x & 31) == 0 && bits > 0)
+        atomicMax(reinterpret_cast<unsigned long long *>(&state[2]), (unsigned long long)bits);
+}
+
+// decoder.py:71-75: current = nxt; stop if delta < stop_delta
+__global__ void decide_kernel(long long *state, double stop_delta) {
+    if (state[0]) return;
+    state[1] += 1;
+    if (__longlong_as_double(state[2]) < stop_delta) state[0] = 1;
+    state[2] = 0;
+}
+
+// decoder.py:76: clip(floor(x + 0.5)) of the raster holding the last sweep (sweep i writes
+// buffer (i + 1) % 2), rows [y0, y1) into out (pitch W)
+__global__ void finalize_f64_kernel(const double *ping, const double *pong, const long long *state, int W, int y0,
+                                    int y1, uint8_t *out, int32_t *iters_done) {
+    const double *src = (state[1] & 1) ? pong : ping;
+    const long long n = (long long)(y1 - y0) * W, base = (long long)y0 * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double v = floor(src[base + i] + 0.5);
+        out[i] = (uint8_t)(v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v));
+    }
+    if (iters_done && blockIdx.x == 0 && threadIdx.x == 0) *iters_done = (int32_t)state[1];
+}
+
+__global__ void fill_f64_kernel(double *a, double v, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+
+// Records (include/mns_record.h) -> painted units (decoder.py:48-59): slot 4i + k holds quadrant k
+// of a phase-2 record (k = 0..3) or, for a phase-1 record, the leaf itself in slot 4i (size 0 in
+// the other three: skipped by the sweep).
+__global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W, int H, int32_t *ux, int32_t *uy,
+                                        int32_t *usize, int32_t *udx, int32_t *udy, double *us, double *uo) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= 4 * n) return;
+    const long long i = t >> 2;
+    const int k = (int)(t & 3);
+    const uint64_t r = rec[i];
+    const int x = 2 * (int)(r & 0x7FFF), y = 2 * (int)((r >> 15) & 0x7FFF);
+    const int level = (int)((r >> MNS_REC_LEVEL_SHIFT) & 3) + 1;
+    const int size = 32 >> level;
+    const bool p2 = (r >> 32) & 1;
+    const int ob = (int)((r >> 33) & 0xFF);
+    int sz, px, py;
+    double s, o;
+    if (!p2) {
+        if (k) {
+            usize[t] = 0;
+            return;
+        }
+        sz = size;
+        px = x;
+        py = y;
+        s = -0.875 + 0.25 * (double)((r >> 41) & 7);
+        o = (double)ob;
+    } else {
+        const int h = size / 2;
+        int d[3];
+        for (int j = 0; j < 3; j++) {
+            const int v = (int)((r >> (41 + 6 * j)) & 63);
+            d[j] = v >= 32 ? v - 64 : v;
+        }
+        const int target = k < 3 ? ob + d[k] : ob - (d[0] + d[1] + d[2]);
+        const int bit = (int)((r >> (59 + k)) & 1);
+        // CONTRAST_SETS (encoder.py:36)
+        const double lo[3] = {0.2, 0.4, 0.5}, hi[3] = {0.5, 0.65, 0.9};
+        sz = h;
+        px = x + (k & 1) * h;
+        py = y + (k >> 1) * h;
+        s = bit ? hi[level - 1] : lo[level - 1];
+        o = (double)target;
+    }
+    ux[t] = px;
+    uy[t] = py;
+    usize[t] = sz;
+    udx[t] = clampi(px - sz / 2, 0, W - 2 * sz);  // co_domain_rect (image.py:174-187)
+    udy[t] = clampi(py - sz / 2, 0, H - 2 * sz);
+    us[t] = s;
+    uo[t] = o;
+}
+
+int sm_count_f64() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace
+
+int records_to_units(const uint64_t *records, int64_t n, int W, int H, int32_t *ux, int32_t *uy, int32_t *usize,
+                     int32_t *udx, int32_t *udy, double *us, double *uo, cudaStream_t st) {
+    MNS_CHECK_ARG(n >= 0 && W >= 2 && H >= 2, "bad record count or raster size");
+    if (n == 0) return 0;
+    records_to_units_kernel<<<(unsigned)((4 * n + 255) / 256), 256, 0, st>>>(records, n, W, H, ux, uy, usize, udx,
+                                                                             udy, us, uo);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                     const int32_t *udy, const double *us, const double *uo, int64_t n, int W, const double *cur,
+                     double *nxt, int64_t *state, cudaStream_t st) {
+    MNS_CHECK_ARG(n >= 0 && W > 0, "bad unit count or width");
+    if (n == 0) return 0;
+    sweep_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt,
+                                                                 reinterpret_cast<long long *>(state));
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_f64_decide(int64_t *state, double stop_delta, cudaStream_t st) {
+    decide_kernel<<<1, 1, 0, st>>>(reinterpret_cast<long long *>(state), stop_delta);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_f64_finalize(const double *ping, const double *pong, const int64_t *state, int W, int y0, int y1,
+                        uint8_t *out, int32_t *iters_done, cudaStream_t st) {
+    MNS_CHECK_ARG(W > 0 && 0 <= y0 && y0 <= y1, "bad raster rows");
+    finalize_f64_kernel<<<sm_count_f64() * 4, 256, 0, st>>>(ping, pong, reinterpret_cast<const long long *>(state), W,
+                                                            y0, y1, out, iters_done);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx, const int32_t *udy,
+               const double *us, const double *uo, int64_t n, int W, int H, int iters, double stop_delta,
+               double init, double *ping, double *pong, uint8_t *out, int32_t *d_iters_done, void *workspace,
+               int64_t workspace_bytes, cudaStream_t st) {
+    MNS_CHECK_ARG(W > 0 && H > 0, "bad raster size");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    MNS_CHECK_ARG(workspace_bytes >= 32, "workspace too small");
+    int64_t *state = reinterpret_cast<int64_t *>(workspace);
+    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 32, st));
+    fill_f64_kernel<<<sm_count_f64() * 4, 256, 0, st>>>(ping, init, (long long)W * H);
+    for (int it = 0; it < iters; it++) {
+        const double *cur = (it & 1) ? pong : ping;
+        double *nxt = (it & 1) ? ping : pong;
+        if (int rc = decode_f64_sweep(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, state, st)) return rc;
+        if (int rc = decode_f64_decide(state, stop_delta, st)) return rc;
+    }
+    return decode_f64_finalize(ping, pong, state, W, 0, H, out, d_iters_done, st);
+}
+
+}  // namespace mns

@@ -7,7 +7,8 @@
 // with k2 = 2*code - 7 the quantised contrast; the quantiser picks the odd k2
 // nearest 32N/D, which is the k2 minimising k2^2 D - 64 k2 N.  So the per-range
 // argmin over (domain, isometry) with the reference's first-index tie-break is
-// the lexicographic minimum of the 64-bit key (val + 2^42) << 21 | candidate.
+// the lexicographic minimum of the 64-bit key (val + 2^(63-cb)) << cb | candidate
+// (cb = key_cand_bits(n), mns_common.cuh).
 //
 // This file holds the CUDA-core paths (any B; the local search) and the shared
 // domain-pool preparation / finalisation; the tcgen05 tensor-core GEMM for
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) full_search_cc_kernel(const uint8_t *img,
             }
             const long long N = (long long)n * sqr - Sq * rsum[row];
             const long long v = best_val(N, D);
-            const unsigned long long key = make_key(v, d * n_iso + row % n_iso);
+            const unsigned long long key = make_key_cb(v, d * n_iso + row % n_iso, key_cand_bits(n));
             local[row] = key < local[row] ? key : local[row];
         }
     }
@@ -158,7 +159,7 @@ __global__ void search_finalize_kernel(const uint8_t *img, int W, int B, int n_i
     const int ri = r0 + i, n = B * B, rpr = W / B;
     const int rx = (ri % rpr) * B, ry = (ri / rpr) * B;
     const unsigned long long key = best[i];
-    const long long cand = (long long)(key & ((1ull << 21) - 1));
+    const long long cand = key_cand(key, key_cand_bits(n));
     const long long d = cand / n_iso;
     const int t = (int)(cand % n_iso);
     int sr = 0;
@@ -324,7 +325,7 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     search_workspace_bytes(W, H, B, step, n_iso, &need);
     MNS_CHECK_ARG(ws_bytes >= need, "workspace too small");
     const long long ndx = (W - 2 * B) / step + 1, ndy = (H - 2 * B) / step + 1, ndom = ndx * ndy;
-    MNS_CHECK_ARG(ndom * n_iso < (1ll << 21), "domain pool too large for the 21-bit candidate key");
+    MNS_CHECK_ARG(ndom * n_iso < (1ll << key_cand_bits(B * B)), "domain pool too large for the argmin key");
     if (r1 == r0) return 0;
     char *p = (char *)ws;
     SearchWs w;

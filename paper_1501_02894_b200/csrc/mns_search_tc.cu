@@ -96,9 +96,6 @@ struct TcParams {
     unsigned long long *best;    // [r1 - r0]
 };
 
-__device__ __forceinline__ unsigned long long make_key(long long val, long long cand) {
-    return ((unsigned long long)(val + (1ll << 42)) << 21) | (unsigned long long)cand;
-}
 
 // exact min over odd k2 in [-7, 7] of k2^2 D - 64 k2 N: an fp32 estimate of the vertex
 // 32N/D picks the nearest odd k2; it and both odd neighbours are evaluated exactly.
@@ -401,7 +398,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float *lq = reinterpret_cast<const float *>(p.consts + (long long)dt * BN);  // -Sq | sqrt_rd(D)
                 const long long C = exact_cross(p.pool, p.araw, p.n, d, row);
                 const long long N = (long long)p.n * C - (long long)(int)(-__ldg(lq + col)) * p.row_sr[row];
-                const unsigned long long key = make_key(best_val_exact(N, __ldg(p.pD + dcol)), d * p.n_iso + iso);
+                const unsigned long long key = make_key_cb(best_val_exact(N, __ldg(p.pD + dcol)), d * p.n_iso + iso,
+                                                              key_cand_bits(p.n));
 #ifdef MNS_TC_STATS
                 atomicAdd(&g_tc_stats[3], 1ull);
 #endif
@@ -453,7 +451,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int acc = t & 1, cbuf = t % NCB;
             // the range's running best from every CTA's exact warp and every isometry row of the range
             // (global key, loaded a tile ahead)
-            if (g != ~0ull) set_threshold((long long)(g >> 21) - (1ll << 42));
+            if (g != ~0ull) set_threshold(key_val(g, key_cand_bits(p.n)));
             g = ~0ull;
             mbar_spin(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
@@ -773,15 +771,15 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
             for (int k = 0; k < n; k++) bc += (int)qd[k] * __half2int_rn(ar[k]);
         }
         const long long N = (long long)n * bc - (long long)psq[bd] * sr;  // exact
-        atomicMin(&best[rr], make_key(best_val_exact(N, pD[bd]), (long long)bd * n_iso + bt));
+        atomicMin(&best[rr], make_key_cb(best_val_exact(N, pD[bd]), (long long)bd * n_iso + bt, key_cand_bits(n)));
     }
 }
 
-__global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, unsigned long long *key) {
+__global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, int n, unsigned long long *key) {
     unsigned long long best = ~0ull;
     for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndom;
          d += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long k = make_key(pD[d], d * n_iso);  // constant range: val = D (k2 = +-1), iso 0
+        const unsigned long long k = make_key_cb(pD[d], d * n_iso, key_cand_bits(n));  // constant range: val = D (k2 = +-1), iso 0
         best = k < best ? k : best;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -867,7 +865,7 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     range_rows_kernel<<<(n_rows_pad + 7) / 8, 256, 0, st>>>(img, W, B, n_iso, r0, n_rows, n_rows_pad, Araw, Ac, row_sr,
                                                           row_flat, row_err);
     MNS_CUDA_TRY(cudaMemsetAsync(fkey, 0xFF, 8, st));
-    flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, fkey);
+    flat_key_kernel<<<148, 256, 0, st>>>(pD, ndom, n_iso, B * B, fkey);
 #ifndef TC_NO_SEED
     {
         const int ndx = (W - 2 * B) / step + 1, ndy = (int)(ndom / ndx);

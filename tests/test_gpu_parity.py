@@ -545,6 +545,12 @@ def test_lattice_decode_flags_2x2_units(mns):
                                   N.ptr(ras[0]), N.ptr(ras[1]), N.ptr(want), ctypes.c_void_p(0), N.ptr(ws), wsb, None))
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+    # a wrong min_leaf (user-built code) is caught by the flag, and lattice=False gives the right image
+    code.min_leaf = 4
+    bad, _, _ = mns.decode_device(code, iters=4)
+    assert int(code.decode_error.item()) == 1
+    fixed, _, _ = mns.decode_device(code, iters=4, lattice=False)
+    assert torch.equal(fixed, want)
 
 
 @pytest.mark.parametrize("iters", [10, 7])
@@ -718,3 +724,17 @@ def test_decode_from_encoder_unit_map_equals_records_path(mns, root_level, iters
     b, _, _ = mns.decode_device(code, iters=iters, stop_delta=0.0)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def test_full_search_wide_key_large_pool(mns):
+    """B = 8 identity search over a 1600^2 image: 1585^2 = 2.5M domains, above the old 2^21
+    candidate cap (the key now gives B = 8 candidates 25 bits).  A range slice vs the oracle."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(1600, 12)
+    img = torch.from_numpy(px).cuda()
+    r0, r1 = 19_000, 19_024
+    got = {k: v.cpu().numpy() for k, v in mns.full_search_device(img, 8, 1, 1, ranges=(r0, r1)).items()}
+    ref = O.full_search(px, 8, 1, n_iso=1, range_ids=np.arange(r0, r1))
+    for k in ("dom", "iso", "o", "code"):
+        assert np.array_equal(got[k].astype(np.int64), ref[k].astype(np.int64)), k
