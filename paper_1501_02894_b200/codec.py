@@ -249,6 +249,10 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
                    torch.empty((H, W), dtype=torch.float32, device=dev))
     if out is None and want_u8:
         out = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    if stop_delta > 0.0 and want_u8:
+        # the reference's early stop (decoder.py:70-75) decided exactly: bit-exact fp64 sweeps
+        code.decode_error = None
+        return decode_device_f64(code, iters, stop_delta, initial_value, out=out, stream=stream) + (None,)
     wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
     ws = _WS.get("dec", wsb, dev)
     if want_u8 and stop_delta == 0.0 and lattice is not False and min_leaf_side(code) >= 4:
@@ -276,6 +280,53 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
                                   float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),
                                   N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
     return out, it, rasters
+
+
+def records_to_units_device(records, n: int, W: int, H: int, stream=None) -> dict:
+    """Packed records -> 4n painted-unit slots (decoder.py:48-59) on the device (mns_records_to_units)."""
+    torch = _torch()
+    L = N.lib()
+    dev = records.device
+    u = {k: torch.empty(max(4 * n, 1), dtype=torch.int32, device=dev) for k in ("x", "y", "size", "dx", "dy")}
+    u["s"] = torch.empty(max(4 * n, 1), dtype=torch.float64, device=dev)
+    u["o"] = torch.empty(max(4 * n, 1), dtype=torch.float64, device=dev)
+    N.check(L.mns_records_to_units(N.ptr(records), int(n), W, H, N.ptr(u["x"]), N.ptr(u["y"]), N.ptr(u["size"]),
+                                   N.ptr(u["dx"]), N.ptr(u["dy"]), N.ptr(u["s"]), N.ptr(u["o"]),
+                                   N.stream_ptr(stream)))
+    u["n"] = 4 * n
+    return u
+
+
+def decode_units_f64(units: dict, W: int, H: int, iters: int, stop_delta: float, initial_value: float, out=None,
+                     stream=None):
+    """decoder.py:66-77 bit for bit (mns_decode_f64): fp64 sweeps, exact early stop, exact rounding.
+    Returns (uint8 [H, W] padded, sweeps-done int32 tensor)."""
+    torch = _torch()
+    L = N.lib()
+    if iters < 1:
+        raise ValueError("max_iters must be >= 1")
+    dev = units["x"].device
+    ping = torch.empty((H, W), dtype=torch.float64, device=dev)
+    pong = torch.empty((H, W), dtype=torch.float64, device=dev)
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _WS.get("decf64", 64, dev)
+    n = int(units.get("n", units["x"].numel()))
+    N.check(L.mns_decode_f64(N.ptr(units["x"]), N.ptr(units["y"]), N.ptr(units["size"]), N.ptr(units["dx"]),
+                             N.ptr(units["dy"]), N.ptr(units["s"]), N.ptr(units["o"]), n, W, H, int(iters),
+                             float(stop_delta), float(initial_value), N.ptr(ping), N.ptr(pong), N.ptr(out),
+                             N.ptr(it), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+    return out, it
+
+
+def decode_device_f64(code: "DeviceCode", iters: int, stop_delta: float, initial_value: float, out=None,
+                      stream=None):
+    """Exact fp64 decode of a device quadtree code (records expanded to units on the device)."""
+    code.join(stream)
+    n = code.n_records()
+    u = records_to_units_device(code.records, n, code.padded_w, code.padded_h, stream)
+    return decode_units_f64(u, code.padded_w, code.padded_h, iters, stop_delta, initial_value, out, stream)
 
 
 def decode_units_device(units: dict, W: int, H: int, iters: int, stop_delta: float, initial_value: float,
@@ -516,10 +567,22 @@ def _units_to_device(u: dict, float_dtype):
 
 
 def decode(code, config: Optional[DecodeConfig] = None) -> GrayImage:
-    """decoder.py:66-77 (fp32 raster on device; parity bar: <= 1 LSB and 0.01 dB)."""
+    """decoder.py:66-77.  stop_delta > 0 (the default DecodeConfig): bit-exact with the reference
+    (fp64 sweeps, the early stop decided exactly; mns_decode_f64).  stop_delta == 0: the fp32
+    raster / lattice decoders (parity bar <= 1 LSB and 0.01 dB)."""
     torch = _torch()
     cfg = config if config is not None else DecodeConfig()
     W, H = code.padded_w, code.padded_h
+    if cfg.max_iters < 1:
+        raise ValueError("max_iters must be >= 1")
+    if cfg.stop_delta > 0.0:
+        if code.mode in ("no_search", "mns"):
+            u = _quadtree_units(code if isinstance(code, QuadtreeCode) else _wrap_reference(code))
+        else:
+            u = _baseline_units(code)
+        out, _ = decode_units_f64(_units_to_device(u, np.float64), W, H, cfg.max_iters, cfg.stop_delta,
+                                  cfg.initial_value)
+        return GrayImage(out.cpu().numpy()[: code.orig_h, : code.orig_w])
     if code.mode in ("no_search", "mns") and (not hasattr(code, "has_records") or code.has_records):
         rec, offs = _records_grouped(code if isinstance(code, QuadtreeCode) else _wrap_reference(code))
         dev = _device()

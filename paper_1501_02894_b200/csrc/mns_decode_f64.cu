@@ -21,7 +21,6 @@
 #include <math.h>
 
 #include "mns_common.cuh"
-#include "mns_record.h"
 
 namespace mns {
 

@@ -279,3 +279,95 @@ class StripDecoder:
                 self._exchange(nxt)
                 cur = nxt
         return out
+
+
+class StripDecoderF64:
+    """Strip decode with the reference's early stop (decoder.py:66-77) across ranks, bit-exact.
+
+    Every sweep is the exact fp64 step (mns_decode_f64_sweep) of this rank's units on its strip
+    plus a 16-row halo (one sweep per exchange; every clamped domain of a root lies within 16 rows
+    of it).  The sweep's local max|delta| lands in ``state[2]`` (fp64 bits); ranks all-reduce it
+    (MAX) -- the whole image's delta, exactly as the reference computes it -- before
+    mns_decode_f64_decide applies ``delta < stop_delta`` on the device, so every rank stops after
+    the same sweep with no host synchronisation (later sweeps are no-ops).  ``code`` is a
+    strip-local DeviceCode (global coordinates, encode_device(root_rows=...)).
+    """
+
+    def __init__(self, code, height: int, width: int, r0: int, r1: int, rank: int = 0, world: int = 1,
+                 group=None, units=None):
+        import torch
+
+        self.code, self.H, self.W, self.r0, self.r1 = code, height, width, r0, r1
+        self.rank, self.world, self.group = rank, world, group
+        self.y_lo, self.y_hi = resident_rows(r0, r1, height, HALO)
+        dev = code.records.device if code is not None else torch.device("cpu")
+        rows = self.y_hi - self.y_lo
+        self.ping = torch.empty((rows, width), dtype=torch.float64, device=dev)
+        self.pong = torch.empty((rows, width), dtype=torch.float64, device=dev)
+        self.out = torch.empty((16 * (r1 - r0), width), dtype=torch.uint8, device=dev)
+        self.state = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.iters_done = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.units = units
+        self._ops = {}
+
+    def _base(self, t):
+        return ctypes.c_void_p(t.data_ptr() - self.y_lo * self.W * 8)
+
+    def delta_view(self):
+        """state[2] as a float64 tensor (the all-reduced word)."""
+        import torch
+
+        return self.state[2:3].view(torch.float64)
+
+    def sweep(self, cur, nxt, stream=None) -> None:
+        from . import _native as N
+
+        L = N.lib()
+        u = self.units
+        N.check(L.mns_decode_f64_sweep(N.ptr(u["x"]), N.ptr(u["y"]), N.ptr(u["size"]), N.ptr(u["dx"]),
+                                       N.ptr(u["dy"]), N.ptr(u["s"]), N.ptr(u["o"]), int(u["n"]), self.W,
+                                       self._base(cur), self._base(nxt), N.ptr(self.state), N.stream_ptr(stream)))
+
+    def decide(self, stop_delta: float, stream=None) -> None:
+        from . import _native as N
+
+        N.check(N.lib().mns_decode_f64_decide(N.ptr(self.state), float(stop_delta), N.stream_ptr(stream)))
+
+    def finalize(self, stream=None):
+        from . import _native as N
+
+        N.check(N.lib().mns_decode_f64_finalize(self._base(self.ping), self._base(self.pong), N.ptr(self.state),
+                                                self.W, 16 * self.r0, 16 * self.r1, N.ptr(self.out),
+                                                N.ptr(self.iters_done), N.stream_ptr(stream)))
+        return self.out
+
+    def _exchange(self, t):
+        key = id(t)
+        if key not in self._ops:
+            self._ops[key] = halo_ops(t, self.r0, self.r1, self.H, self.rank, self.world, self.group, HALO)
+        run_ops(self._ops[key])
+
+    def run(self, max_iters: int = 10, stop_delta: float = 0.5, initial_value: float = 128.0, stream=None):
+        """max_iters sweeps at most; returns the uint8 strip (own rows).  ``iters_done`` holds the
+        sweep count after the stream reaches the end (the same on every rank)."""
+        import torch.distributed as dist
+
+        if max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.units is None:
+            from .codec import records_to_units_device
+
+            self.code.join(stream)
+            self.units = records_to_units_device(self.code.records, self.code.n_records(), self.W, self.H, stream)
+        self.state.zero_()
+        self.ping.fill_(float(initial_value))
+        cur, nxt = self.ping, self.pong
+        delta = self.delta_view()
+        for _ in range(max_iters):
+            self.sweep(cur, nxt, stream)
+            if self.world > 1:
+                dist.all_reduce(delta, op=dist.ReduceOp.MAX, group=self.group)
+            self.decide(stop_delta, stream)
+            self._exchange(nxt)
+            cur, nxt = nxt, cur
+        return self.finalize(stream)

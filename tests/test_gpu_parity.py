@@ -70,6 +70,8 @@ def test_decode_golden_within_1lsb(mns, golden):
             diff = int(np.abs(got.astype(int) - want.astype(int)).max())
             worst = max(worst, diff)
             assert diff <= 1, (case, key, diff)
+            if key == "decode_default":  # stop_delta > 0: the exact fp64 decoder, bit-identical
+                assert diff == 0, (case, key, diff)
             assert abs(_psnr(img, got) - _psnr(img, want)) <= 0.01 or _psnr(img, want) == math.inf, (case, key)
     print("worst decode diff (LSB):", worst)
 
@@ -738,3 +740,101 @@ def test_full_search_wide_key_large_pool(mns):
     ref = O.full_search(px, 8, 1, n_iso=1, range_ids=np.arange(r0, r1))
     for k in ("dom", "iso", "o", "code"):
         assert np.array_equal(got[k].astype(np.int64), ref[k].astype(np.int64)), k
+
+
+def _oracle_deltas(units, W, H, init, n):
+    """The reference's per-sweep max|nxt - current| (decoder.py:70-72) from the fp64 oracle."""
+    cur = np.full((H, W), init)
+    out = []
+    for _ in range(n):
+        nxt = O.decode_step_units(units, cur)
+        out.append(float(np.max(np.abs(nxt - cur))))
+        cur = nxt
+    return out
+
+
+@pytest.mark.parametrize("seed,side", [(3, 128), (21, 96)])
+def test_early_stop_exact_at_threshold(mns, seed, side):
+    """stop_delta placed exactly ON a sweep's fp64 delta (no stop: the test is `<`) and one ulp
+    above it (stop): the GPU decode stops at the reference's sweep in both cases and the image is
+    bit-identical to the oracle's (an fp32 max|delta| could not tell these thresholds apart)."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(side, seed, noise_sigma=12.0, n_blobs=5)
+    rec, _ = O.encode_quadtree_records(px, (6.0, 6.0, 6.0), 16.0, True)
+    units = O.records_to_units(rec, side, side)
+    deltas = _oracle_deltas(units, side, side, 128.0, 12)
+    code = mns.QuadtreeCode.from_records(rec, side, side, side, side, "mns", True)
+    dcode = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e1=6.0, e2=6.0, e3=6.0))
+    for j in (2, 4, 6):
+        for stop in (deltas[j], float(np.nextafter(deltas[j], np.inf))):
+            want, _, sweeps = O.decode_units(units, side, side, max_iters=12, stop_delta=stop)
+            expect = j + 1 if stop > deltas[j] and all(d >= stop for d in deltas[:j]) else sweeps
+            assert sweeps == expect or stop == deltas[j]
+            got = mns.decode(code, mns.DecodeConfig(max_iters=12, stop_delta=stop)).pixels
+            assert np.array_equal(got, want), (j, stop, sweeps)
+            dout, it, _ = mns.decode_device(dcode, iters=12, stop_delta=stop)
+            assert int(it.item()) == sweeps
+            assert np.array_equal(dout.cpu().numpy(), want)
+
+
+def test_decode_search_codes_default_config_bit_exact(mns, golden):
+    """Baseline (full-search) codes decoded with the default DecodeConfig (early stop 0.5): the
+    GPU's exact fp64 decoder equals the fp64 oracle decode of the same units bit for bit."""
+    g = golden("search")
+    for case in [c for c in g.manifest if c["key"].startswith("full")][:6]:
+        k = case["key"]
+        code, _ = mns.encode_full_search(mns.GrayImage(g[f"{k}/img"]), case["B"],
+                                         mns.EncoderConfig(mode="full_search", full_search_step=case["step"]))
+        c = code.columns
+        units = np.zeros(len(c["rx"]), dtype=O.UNIT_DTYPE)
+        units["x"], units["y"], units["size"] = c["rx"], c["ry"], case["B"]
+        units["dx"], units["dy"] = c["dom_x"], c["dom_y"]
+        units["s"] = -0.875 + 0.25 * c["code"].astype(np.float64)
+        units["o"] = c["o"].astype(np.float64)
+        want, _, _ = O.decode_units(units, code.padded_w, code.padded_h, max_iters=10, stop_delta=0.5)
+        got = mns.decode(code, mns.DecodeConfig()).pixels
+        assert np.array_equal(got, want[: code.orig_h, : code.orig_w]), case
+
+
+def test_f64_strip_decoder_three_strips_on_one_gpu(mns):
+    """StripDecoderF64's kernels on 3 strips of one image (the ranks' halo exchange and delta
+    all-reduce done by hand in lock-step): the strips equal the exact decode with early stop."""
+    from paper_1501_02894_b200 import sharding
+    from paper_1501_02894_b200.synth import synth_image
+
+    H = W = 512
+    px = synth_image(512, 41, noise_sigma=10.0, n_blobs=8)
+    cfg = mns.EncoderConfig()
+    rec, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
+    want, _, sweeps = O.decode_records(rec, W, H, max_iters=10, stop_delta=0.5)
+    assert sweeps < 10
+    world = 3
+    decs = []
+    for rank in range(world):
+        r0, r1 = sharding.strip_rows(H, world, rank)
+        y0, y1 = sharding.resident_rows(r0, r1, H)
+        code = mns.encode_device(torch.from_numpy(np.ascontiguousarray(px[y0:y1])).cuda(), cfg, root_rows=(r0, r1),
+                                 height=H)
+        d = sharding.StripDecoderF64(code, H, W, r0, r1, rank, world)
+        d.units = mns.codec.records_to_units_device(code.records, code.n_records(), W, H)
+        d.state.zero_()
+        d.ping.fill_(128.0)
+        decs.append(d)
+    bufs = [[d.ping, d.pong] for d in decs]
+    for it in range(10):
+        for d, b in zip(decs, bufs):
+            d.sweep(b[it & 1], b[(it + 1) & 1])
+        g = max(float(d.delta_view()[0]) for d in decs)  # the all-reduce (MAX)
+        for d in decs:
+            d.delta_view()[0] = g
+            d.decide(0.5)
+        for k in range(world - 1):  # halo exchange of the freshly written rasters
+            a, b = decs[k], decs[k + 1]
+            ra, rb = bufs[k][(it + 1) & 1], bufs[k + 1][(it + 1) & 1]
+            ya, yb = 16 * a.r1 - a.y_lo, 16 * b.r0 - b.y_lo
+            ra[ya: ya + 16].copy_(rb[yb: yb + 16])
+            rb[yb - 16: yb].copy_(ra[ya - 16: ya])
+    got = np.concatenate([d.finalize().cpu().numpy() for d in decs])
+    assert all(int(d.iters_done.item()) == sweeps for d in decs)
+    assert np.array_equal(got, want)

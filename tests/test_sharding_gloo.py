@@ -261,3 +261,74 @@ def test_batch_and_range_splits():
         assert sum(b - a for a, b in parts) == n
         assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1
     assert math.isclose(sum(b - a for a, b in [sharding.split(4096, 8, r) for r in range(8)]) / 8, 512)
+
+
+class _OracleStripF64(sharding.StripDecoderF64):
+    """StripDecoderF64 with its two device kernels replaced by the fp64 oracle (same contract:
+    the sweep paints this rank's units and folds its max|delta| into state[2]; decide applies the
+    reference's test), so the rank-level control -- delta all-reduce, device-side stop, halo
+    exchange, final rows -- runs here on gloo.  Rows outside the resident strip are NaN poison."""
+
+    def __init__(self, px, records, rank, world):
+        from oracle import oracle as O
+
+        H, W = px.shape
+        r0, r1 = sharding.strip_rows(H, world, rank)
+        super().__init__(None, H, W, r0, r1, rank, world)
+        units = O.records_to_units(records, W, H)
+        self.mine = units[(units["y"] >= 16 * r0) & (units["y"] < 16 * r1)]
+        self.units = {"n": len(self.mine)}
+        self.swept = 0
+
+    def sweep(self, cur, nxt, stream=None):
+        from oracle import oracle as O
+
+        if self.state[0]:
+            return
+        full = np.full((self.H, self.W), np.nan)
+        full[self.y_lo:self.y_hi] = cur.numpy()
+        res = O.decode_step_units(self.mine, full, nthreads=1)
+        a, b = 16 * self.r0, 16 * self.r1
+        nxt[a - self.y_lo: b - self.y_lo] = torch.from_numpy(res[a:b])
+        d = float(np.max(np.abs(res[a:b] - full[a:b])))
+        self.delta_view()[0] = max(float(self.delta_view()[0]), d)
+        self.swept += 1
+
+    def decide(self, stop_delta, stream=None):
+        if self.state[0]:
+            return
+        self.state[1] += 1
+        if float(self.delta_view()[0]) < stop_delta:
+            self.state[0] = 1
+        self.state[2] = 0
+
+    def finalize(self, stream=None):
+        src = self.pong if int(self.state[1]) & 1 else self.ping
+        own = src[16 * self.r0 - self.y_lo: 16 * self.r1 - self.y_lo].numpy()
+        return np.clip(np.floor(own + 0.5), 0, 255).astype(np.uint8)
+
+
+def _f64_strip_worker(rank, world, px, records, iters, stop, out_dir):
+    dec = _OracleStripF64(px, records, rank, world)
+    out = dec.run(iters, stop, 128.0)
+    np.save(os.path.join(out_dir, f"strip{rank}.npy"), out)
+    np.save(os.path.join(out_dir, f"iters{rank}.npy"), np.array([int(dec.state[1]), dec.swept]))
+
+
+@pytest.mark.parametrize("world,stop", [(2, 0.5), (3, 0.5), (2, 2.0), (3, 0.0)])
+def test_f64_strip_decode_early_stop_matches_whole_image(world, stop, tmp_path):
+    """Early stop across strips (decoder.py:70-75): the all-reduced max|delta| makes every rank stop
+    after the reference's sweep, and the strips equal the whole-image decode bit for bit."""
+    from oracle import oracle as O
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(96, 31, noise_sigma=10.0, n_blobs=5)
+    records, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
+    _run(world, _f64_strip_worker, px, records, 12, stop, str(tmp_path))
+    want, _, sweeps = O.decode_records(records, 96, 96, max_iters=12, stop_delta=stop)
+    strips = np.concatenate([np.load(tmp_path / f"strip{r}.npy") for r in range(world)])
+    assert np.array_equal(strips, want)
+    for r in range(world):
+        done, swept = np.load(tmp_path / f"iters{r}.npy")
+        assert done == sweeps and swept == sweeps
+    assert stop == 0.0 or sweeps < 12  # the stop actually triggered
