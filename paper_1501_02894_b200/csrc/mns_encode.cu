@@ -38,20 +38,17 @@ namespace mns {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef ENC_MINB
+#define ENC_MINB 4
+#endif
 constexpr int EW = 8;                // warps per CTA
 constexpr int ET = EW * 32;
-constexpr int RPW = 2;               // roots encoded by each warp per tile (in turn)
-constexpr int TR = EW * RPW;         // 16 consecutive roots of one root row per tile
-static_assert(RPW == 2, "the warp-local decision rounds map two roots onto one warp");
-constexpr int WIN_W = TR * 16 + 32;  // 544
-constexpr int WIN_H = 48;
-constexpr int QE_WL = WIN_W / 2;     // 272 q columns
-constexpr int QE_W = QE_WL + 4;      // row stride 276: K1c's lanes read rows 2 apart, 4 banks apart
-constexpr int QE_H = WIN_H / 2;      // 24
+constexpr int TR = 2 * EW;           // 16 consecutive roots of one root row per step (2 per warp)
+constexpr int WIN_W = TR * 16 + 32;  // 288 pixel columns: [x0 - 16, x0 + 272)
 
 struct EncParams {
     int y_res0;  // first resident image row (the tensor map's row 0)
-    int W, H, n_images, rr0, rows, rw, tiles_per_row;
+    int W, H, n_images, rr0, rows, rw, tiles_per_row, chunk_rows;
     int mns, root_level, min_dim;
     double p1b[5];  // phase-1 accept bound on 1024*n*SSE per level (inf for level 4)
     double p2b[4];  // bound(E_level): phase-2 quadrant accepts iff SSE <= n_k * p2b
@@ -181,54 +178,42 @@ __device__ __forceinline__ int node2_x(int k) { return 8 * (k & 1); }
 __device__ __forceinline__ int node2_y(int k) { return 8 * (k >> 1); }
 __device__ __forceinline__ int node3_x(int m) { return node2_x(m >> 2) + 4 * (m & 1); }
 __device__ __forceinline__ int node3_y(int m) { return node2_y(m >> 2) + 4 * ((m >> 1) & 1); }
-__device__ __forceinline__ int node4_x(int c) { return node3_x(c >> 2) + 2 * (c & 1); }
-__device__ __forceinline__ int node4_y(int c) { return node3_y(c >> 2) + 2 * ((c >> 1) & 1); }
 
-// Shared-memory layout of one tile (TR roots); moments and decisions are per node.
-struct TileSmem {
-    Mom m1[TR];
-    Mom m2[TR][4];
-    Mom m3[TR][16];
-    int sr4[TR][64], srr4[TR][64];  // level-4 range sums (q moments are computed lazily)
-    uint64_t rec1[TR], rec2[TR][4], rec3[TR][16], rec4[TR][64];
-    uint8_t acc1[TR], acc2[TR][4], acc3[TR][16];
-};
-constexpr int TILE_SMEM = ((int)sizeof(TileSmem) + 127) / 128 * 128;  // the TMA window follows, 128-B aligned
-constexpr int ENC_SMEM = WIN_H * WIN_W + QE_H * QE_W * 2 + TILE_SMEM + 64;
-
-struct Win {  // the staged window and the tile/image geometry a decision thread needs
-    const uint8_t (*pix)[WIN_W];
-    const uint16_t (*qe)[QE_W];
-    int x0, y0, wx0, wy0, W, H;
+// A staged window in shared memory addressed by GLOBAL image coordinates: pixel row gy lives at
+// window row (gy - py0) & pmask, q row gqy (q = even-phase 2x2 pixel sum) at (gqy - qy0) & qmask,
+// pixel column gx at gx - wx0 and q column gqx at gqx - wx0 / 2.  The encoder's rings use masks
+// (rows wrap); try_node_kernel's flat window uses mask -1.
+struct Win {
+    const uint8_t *pix;
+    const uint16_t *qe;
+    int ppitch, qpitch, pmask, qmask, py0, qy0, wx0, W, H;
+    __device__ __forceinline__ int px(int gx, int gy) const { return pix[((gy - py0) & pmask) * ppitch + gx - wx0]; }
+    __device__ __forceinline__ int q(int gqx, int gqy) const {
+        return qe[((gqy - qy0) & qmask) * qpitch + gqx - (wx0 >> 1)];
+    }
 };
 
-// q of pixel (py, px) (root-relative) against the co-centred domain of node (nx, ny, s) of root slot
-__device__ __forceinline__ int dom_q(const Win &w, int slot, int nx, int ny, int s, int px, int py) {
-    const int rxg = w.x0 + 16 * slot, ryg = w.y0;
-    const int gdx = clampi(rxg + nx - s / 2, 0, w.W - 2 * s), gdy = clampi(ryg + ny - s / 2, 0, w.H - 2 * s);
-    const int wx = gdx - w.wx0 + 2 * (px - nx), wy = gdy - w.wy0 + 2 * (py - ny);
-    if (((wx | wy) & 1) == 0) return w.qe[wy >> 1][wx >> 1];
-    const uint8_t *pp = &w.pix[wy][wx];
-    return (int)pp[0] + pp[1] + pp[WIN_W] + pp[WIN_W + 1];
+// q of pixel (px, py) against the co-centred domain of node (x, y, s) (image.py:174-187; global)
+__device__ __forceinline__ int dom_q(const Win &w, int x, int y, int s, int px, int py) {
+    const int gdx = clampi(x - s / 2, 0, w.W - 2 * s), gdy = clampi(y - s / 2, 0, w.H - 2 * s);
+    const int gx = gdx + 2 * (px - x), gy = gdy + 2 * (py - y);
+    if (((gx | gy) & 1) == 0) return w.q(gx >> 1, gy >> 1);
+    return w.px(gx, gy) + w.px(gx + 1, gy) + w.px(gx, gy + 1) + w.px(gx + 1, gy + 1);
 }
 
-__device__ __forceinline__ int pixel(const Win &w, int slot, int px, int py) {
-    return w.pix[16 + py][16 + 16 * slot + px];
-}
-
-// Reference-order emulation of one phase-2 quadrant (transform.py:69-80 rms_error) -- the
-// quadrant is the child (cx, cy, cs) of a node at `level`; the domain is the child's own.
-// Returns 1 accept / 0 reject, the chosen bit and (rms_out) the chosen candidate's rms.
-__device__ int emulate_quadrant(const Win &w, int slot, int cx, int cy, int cs, const Mom &m, int t, double slo,
-                                double shi, double tol, int &bit, double *rms_out = nullptr) {
+// Reference-order emulation of one phase-2 quadrant (transform.py:69-80 rms_error): the quadrant
+// is the square (cx, cy, cs) (global) and its domain the co-centred one.  Returns 1 accept /
+// 0 reject, the chosen bit and (rms_out) the chosen candidate's rms.
+__device__ __forceinline__ int emulate_quadrant(const Win &w, int cx, int cy, int cs, int sq, int t, double slo,
+                                             double shi, double tol, int &bit, double *rms_out = nullptr) {
     double lo[64], hi[64];
     const int n = cs * cs;
-    const double dm = ((double)m.sq * 0.25) / (double)n;
+    const double dm = ((double)sq * 0.25) / (double)n;
     const double td = (double)t;
     for (int i = 0; i < cs; i++)
         for (int j = 0; j < cs; j++) {
-            const int q = dom_q(w, slot, cx, cy, cs, cx + j, cy + i);
-            const int r = pixel(w, slot, cx + j, cy + i);
+            const int q = dom_q(w, cx, cy, cs, cx + j, cy + i);
+            const int r = w.px(cx + j, cy + i);
             lo[i * cs + j] = emu_sq(r, q, dm, slo, td);
             hi[i * cs + j] = emu_sq(r, q, dm, shi, td);
         }
@@ -238,9 +223,9 @@ __device__ int emulate_quadrant(const Win &w, int slot, int cx, int cy, int cs, 
     return ((bit ? rhi : rlo) > tol) ? 0 : 1;
 }
 
-// Phase 2 of node (nx, ny, size) at `level` from its own Sr and its 4 children's moments
-// (encoder.py:169-212).  Returns true with *rec on acceptance.
-__device__ bool phase2_node(const Win &w, const EncParams &p, int slot, int level, int nx, int ny, int size, int sr,
+// Phase 2 of node (nx, ny, size) at `level` (global) from its own Sr and its 4 children's
+// moments (encoder.py:169-212), serially.  Returns true with *rec on acceptance.
+__device__ bool phase2_node(const Win &w, const EncParams &p, int level, int nx, int ny, int size, int sr,
                             const Mom *kids, uint64_t *rec) {
     const int nlog2 = 2 * (5 - level);  // node pixels: 256, 64, 16
     const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
@@ -255,52 +240,114 @@ __device__ bool phase2_node(const Win &w, const EncParams &p, int slot, int leve
         int bit;
         int res = p2_quad(nlog2 - 2, kids[k], z.t[k], slo, shi, bnd_n, bit);
         if (res == 2)
-            res = emulate_quadrant(w, slot, nx + (k & 1) * h, ny + (k >> 1) * h, h, kids[k], z.t[k], slo, shi,
+            res = emulate_quadrant(w, nx + (k & 1) * h, ny + (k >> 1) * h, h, kids[k].sq, z.t[k], slo, shi,
                                    p.tol[level], bit);
         if (res != 1) return false;
         bits |= bit << k;
     }
-    *rec = mns_rec_phase2(w.x0 + 16 * slot + nx, w.y0 + ny, level, z.o, z.d0, z.d1, z.d2, bits);
+    *rec = mns_rec_phase2(nx, ny, level, z.o, z.d0, z.d1, z.d2, bits);
     return true;
 }
 
-// Phase 1 + phase 2 of one level-1/2 node with its 4 quadrants on 4 consecutive lanes (lane & 3 =
-// quadrant): same decisions as phase1 / phase2_node, the fp64 quadrant tests in parallel.  Every
-// lane of the warp must call it (ballots); lanes with !live take no part.  Returns the record on
-// the group's quadrant-0 lane via acc / rec.
-__device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p, bool live, int slot, int level,
-                                                int nx, int ny, const Mom &m, const Mom *kids, bool try_node,
-                                                bool &acc, uint64_t &rec) {
-    const int lane = threadIdx.x & 31, quad = lane & 3;
+// A sure rejection: the node's best fit with FREE contrast and offset (least squares), whose
+// SSE_min = (Dr D - N^2) / (n D) (Dr = n Srr - Sr^2, D = n Sqq - Sq^2, N = n Sqr - Sq Sr; D = 0:
+// SSE_min = Dr / n), already exceeds bound * n.  The quantised phase-1 fit and every phase-2
+// candidate (fixed luminance, a contrast from the set) are special cases of that fit, so their SSE
+// is >= SSE_min.  bn2 = bound * n^2 (inf never rejects).  Levels 2-4 (n <= 64): Dr and D are exact
+// 32-bit integers and N one correctly rounded FMA, so each input carries one fp32 rounding; level 1
+// also rounds n Sqq and n Sqr, whose absolute errors enter the margin (`extra`).  The margin is
+// 16x the worst rounding error, so "true" is never wrong.
+template <int NL>
+__device__ __forceinline__ bool surely_above(const Mom &m, float bn2) {
+    float dr, d, nn, extra = 0.f;
+    if (NL <= 6) {
+        dr = (float)((m.srr << NL) - m.sr * m.sr);
+        const unsigned du = ((unsigned)m.sqq << NL) - (unsigned)m.sq * (unsigned)m.sq;
+        d = (float)du;
+        nn = fmaf(-(float)m.sq, (float)m.sr, (float)(m.sqr << NL));
+        if (du == 0u) return dr > bn2 * (1.f + 1.f / 1048576.f);
+    } else {
+        dr = (float)(((unsigned)m.srr << NL) - (unsigned)m.sr * (unsigned)m.sr);
+        const float S = (float)m.sqq * (float)(1 << NL), T = (float)m.sqr * (float)(1 << NL);
+        d = fmaf(-(float)m.sq, (float)m.sq, S);
+        nn = fmaf(-(float)m.sq, (float)m.sr, T);
+        extra = (dr + bn2) * S + fabsf(nn) * T;
+    }
+    const float a = dr * d, b = nn * nn, c = bn2 * d;
+    return a - b - c > (a + b + c + extra) * (1.f / 1048576.f);
+}
+
+// The phase-2 mean gate (encoder.py:186-188) fails: some quadrant mean is farther than mean_tol from
+// the block mean (integer form of p2_node's test).
+__device__ __forceinline__ bool gate_fails(int nlog2, int sr, const int *ks, int gate) {
+    (void)nlog2;
+    const int d = max(max(abs(4 * ks[0] - sr), abs(4 * ks[1] - sr)), max(abs(4 * ks[2] - sr), abs(4 * ks[3] - sr)));
+    return d > gate;
+}
+
+// Phase 1 + phase 2 of one level-1/2 node (global (nx, ny)) with its 4 quadrant tests on 4 lanes of
+// the warp: this lane tests quadrant `quad` (moments `kid`) when is_quad; ks = the 4 children's
+// Sr; gather(ballot) extracts the node's 4 quadrant bits.  Same decisions as phase1 / phase2_node.
+// Every lane of the warp must call it (ballots); the result lands on every lane of the node.
+template <class Gather>
+__device__ __forceinline__ void node_decide(const Win &w, const EncParams &p, bool active, bool is_quad, int quad,
+                                            int level, int nx, int ny, const Mom &m, const int *ks, const Mom &kid,
+                                            Gather gather, bool &acc, uint64_t &rec) {
     const int size = 32 >> level, nlog2 = 2 * (5 - level);
     acc = false;
     rec = 0;
     bool want2 = false, ok = false;
     int bit = 0;
     Node2 z{};
-    if (live && try_node) {
-        rec = phase1(w.x0 + 16 * slot + nx, w.y0 + ny, level, nlog2, m, p.p1b[level], acc);
+    if (active) {
+        rec = phase1(nx, ny, level, nlog2, m, p.p1b[level], acc);
         if (!acc && p.mns) {
-            z = p2_node(nlog2, m.sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
-                        p.gate[level]);
+            z = p2_node(nlog2, m.sr, ks[0], ks[1], ks[2], ks[3], level == 1 ? 15 : 31, p.gate[level]);
             want2 = z.pass;
-            if (want2) {
+            if (want2 && is_quad) {
                 const double slo = level == 1 ? 0.2 : 0.4, shi = level == 1 ? 0.5 : 0.65;
                 const int h = size / 2;
-                int res = p2_quad(nlog2 - 2, kids[quad], z.t[quad], slo, shi, p.p2b[level] * (double)(h * h), bit);
+                int res = p2_quad(nlog2 - 2, kid, z.t[quad], slo, shi, p.p2b[level] * (double)(h * h), bit);
                 if (res == 2)
-                    res = emulate_quadrant(w, slot, nx + (quad & 1) * h, ny + (quad >> 1) * h, h, kids[quad],
-                                           z.t[quad], slo, shi, p.tol[level], bit);
+                    res = emulate_quadrant(w, nx + (quad & 1) * h, ny + (quad >> 1) * h, h, kid.sq, z.t[quad], slo,
+                                           shi, p.tol[level], bit);
                 ok = res == 1;
             }
         }
     }
     const unsigned okm = __ballot_sync(FULL, ok), bitm = __ballot_sync(FULL, bit != 0);
-    const int g = lane & ~3;
-    if (want2 && ((okm >> g) & 15u) == 15u) {
+    if (want2 && gather(okm) == 15u) {
         acc = true;
-        rec = mns_rec_phase2(w.x0 + 16 * slot + nx, w.y0 + ny, level, z.o, z.d0, z.d1, z.d2, (int)((bitm >> g) & 15u));
+        rec = mns_rec_phase2(nx, ny, level, z.o, z.d0, z.d1, z.d2, (int)gather(bitm));
     }
+}
+
+// The level-3 node below a rejected level-3 phase 1 (finite e3): the moments of its four 2x2
+// children (odd-phase domains: 4-pixel sums), phase 2 at level 3, else the four level-4 leaves.
+__device__ __forceinline__ void level3_rejected(const Win &w, const EncParams &p, int x, int y, int sr3, bool &acc,
+                                             uint64_t &rec, uint64_t *rec4) {
+    Mom k4[4];
+    for (int c = 0; c < 4; c++) {
+        const int cx = x + 2 * (c & 1), cy = y + 2 * (c >> 1);
+        Mom mm{0, 0, 0, 0, 0};
+        for (int i = 0; i < 2; i++)
+            for (int j = 0; j < 2; j++) {
+                const int r = w.px(cx + j, cy + i);
+                const int q = dom_q(w, cx, cy, 2, cx + j, cy + i);
+                mm.sr += r;
+                mm.srr += r * r;
+                mm.sq += q;
+                mm.sqq += q * q;
+                mm.sqr += q * r;
+            }
+        k4[c] = mm;
+    }
+    acc = p.mns ? phase2_node(w, p, 3, x, y, 4, sr3, k4, &rec) : false;
+    if (!acc)
+        for (int c = 0; c < 4; c++) {
+            bool dummy;
+            rec4[c] = phase1(x + 2 * (c & 1), y + 2 * (c >> 1), 4, 2, k4[c], INFINITY, dummy);
+        }
 }
 
 // One try_phase1 / try_phase2 call (encoder.py:145-212) on the node (x, y, 32 >> level) of a
@@ -309,32 +356,32 @@ __device__ __forceinline__ void node_quad_lanes(const Win &w, const EncParams &p
 // replayed in the reference's fp64 order, or +inf on rejection.  One CTA stages an 80-row window
 // from the node's 16-aligned origin - 16 (it holds the node and its co-centred domains even for
 // rects not aligned to their size); thread 0 decides.
-constexpr int NODE_WIN_H = 80;
+constexpr int NODE_WIN_W = 288, NODE_WIN_H = 80, NODE_QW = NODE_WIN_W / 2;
 __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
                                 const EncParams p, uint64_t *out_rec, double *out_rms) {
-    __shared__ uint8_t pix[NODE_WIN_H][WIN_W];
-    __shared__ uint16_t qe[NODE_WIN_H / 2][QE_W];
+    __shared__ uint8_t pix[NODE_WIN_H][NODE_WIN_W];
+    __shared__ uint16_t qe[NODE_WIN_H / 2][NODE_QW];
     __shared__ double sq_buf[256];
     const int x0 = x & ~15, y0 = y & ~15, wx0 = x0 - 16, wy0 = y0 - 16;
-    for (int i = threadIdx.x; i < NODE_WIN_H * WIN_W; i += blockDim.x) {
-        const int r = i / WIN_W, c = i % WIN_W, gy = wy0 + r, gx = wx0 + c;
+    for (int i = threadIdx.x; i < NODE_WIN_H * NODE_WIN_W; i += blockDim.x) {
+        const int r = i / NODE_WIN_W, c = i % NODE_WIN_W, gy = wy0 + r, gx = wx0 + c;
         pix[r][c] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? img[(size_t)gy * pitch + gx] : 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < NODE_WIN_H / 2 * QE_WL; i += blockDim.x) {
-        const int qi = i / QE_WL, qj = i % QE_WL;
+    for (int i = threadIdx.x; i < NODE_WIN_H / 2 * NODE_QW; i += blockDim.x) {
+        const int qi = i / NODE_QW, qj = i % NODE_QW;
         qe[qi][qj] = (uint16_t)(pix[2 * qi][2 * qj] + pix[2 * qi][2 * qj + 1] + pix[2 * qi + 1][2 * qj] +
                                 pix[2 * qi + 1][2 * qj + 1]);
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    const Win w{pix, qe, x0, y0, wx0, wy0, W, H};
-    const int size = 32 >> level, nx = x - x0, ny = y - y0, nlog2 = 2 * (5 - level);
+    const Win w{&pix[0][0], &qe[0][0], NODE_WIN_W, NODE_QW, -1, -1, wy0, wy0 / 2, wx0, W, H};
+    const int size = 32 >> level, nlog2 = 2 * (5 - level);
     auto moments = [&](int cx, int cy, int cs) {
         Mom m{0, 0, 0, 0, 0};
         for (int i = 0; i < cs; i++)
             for (int j = 0; j < cs; j++) {
-                const int q = dom_q(w, 0, cx, cy, cs, cx + j, cy + i), r = pixel(w, 0, cx + j, cy + i);
+                const int q = dom_q(w, cx, cy, cs, cx + j, cy + i), r = w.px(cx + j, cy + i);
                 m.sr += r;
                 m.srr += r * r;
                 m.sq += q;
@@ -344,7 +391,7 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
         return m;
     };
     if (phase == 1) {
-        const Mom m = moments(nx, ny, size);
+        const Mom m = moments(x, y, size);
         bool acc;
         const uint64_t rec = phase1(x, y, level, nlog2, m, p.p1b[level], acc);
         const long long n = 1ll << nlog2;
@@ -353,15 +400,15 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
         const double sdq = -0.875 + 0.25 * code, dm = ((double)m.sq * 0.25) / (double)n;
         for (int i = 0; i < size; i++)  // rms_error replayed in numpy's fp64 order (exact in practice)
             for (int j = 0; j < size; j++)
-                sq_buf[i * size + j] = emu_sq(pixel(w, 0, nx + j, ny + i), dom_q(w, 0, nx, ny, size, nx + j, ny + i),
-                                              dm, sdq, (double)o);
+                sq_buf[i * size + j] = emu_sq(w.px(x + j, y + i), dom_q(w, x, y, size, x + j, y + i), dm, sdq,
+                                              (double)o);
         *out_rec = acc ? rec : 0;
         *out_rms = __dsqrt_rn(pw_sum_dev(sq_buf, (int)n) / (double)n);
         return;
     }
     const int h = size / 2;
     Mom kids[4];
-    for (int k = 0; k < 4; k++) kids[k] = moments(nx + (k & 1) * h, ny + (k >> 1) * h, h);
+    for (int k = 0; k < 4; k++) kids[k] = moments(x + (k & 1) * h, y + (k >> 1) * h, h);
     const int sr = kids[0].sr + kids[1].sr + kids[2].sr + kids[3].sr;
     const Node2 z = p2_node(nlog2, sr, kids[0].sr, kids[1].sr, kids[2].sr, kids[3].sr, level == 1 ? 15 : 31,
                             p.gate[level]);
@@ -375,8 +422,8 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
     for (int k = 0; k < 4; k++) {
         int bit;
         double rms;
-        if (!emulate_quadrant(w, 0, nx + (k & 1) * h, ny + (k >> 1) * h, h, kids[k], z.t[k], slo, shi, p.tol[level], bit,
-                              &rms))
+        if (!emulate_quadrant(w, x + (k & 1) * h, y + (k >> 1) * h, h, kids[k].sq, z.t[k], slo, shi, p.tol[level],
+                              bit, &rms))
             return;
         bits |= bit << k;
         worst = fmax(worst, rms);
@@ -385,256 +432,309 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
     *out_rms = worst;
 }
 
-__global__ void __launch_bounds__(ET, 4) mns_encode_kernel(const __grid_constant__ CUtensorMap tmap,
+// ---------------------------------------------------------------- the encoder kernel
+//
+// Persistent CTAs over a balanced share of the (image, 16-root column band, root row) steps,
+// band-major: a CTA walks DOWN its bands one root row per step with a sliding window, so every
+// 16-row block of pixels is staged (TMA) and reduced to q (even 2x2 sums) and Q2 (2x2 sums of q^2
+// over every q position) exactly once per band -- not three times as with one window per root
+// row.  Rings (rows wrap; global row -> ring row by masking): pixels 4 blocks x 16 rows, q and Q2
+// 4 blocks x 8 rows.  Step ry: block ry + 1 lands (issued one step ahead) -> its q rows -> Q2 rows
+// 8ry + 7 .. 8ry + 14 -> the TMA of block ry + 2 into the slot block ry - 2 freed -> the 16 roots.
+//
+// Per root (half-warp; lane m = level-3 node m, its 4x4 range pixels as 4 words): Sr, Srr by
+// DP4A; per level the lane's 16 q values against that level's domain as u16 pairs (PRMT-aligned
+// for the odd-phase level-3 domains) -> Sqr by DP2A, Sq by packed u16x2 adds, Sqq by 4 Q2
+// lookups; level 2 sums over 4 lanes, level 1 over the half-warp.  All moments and decisions
+// stay in registers: level 2 on all 32 lanes (8 nodes x 4 quadrant lanes), level 1 on the
+// quadrant lanes 0/4/8/12 of each half, level 3 one node per lane; then the DFS emission.
+constexpr int PRING = 64;                           // pixel ring rows (4 blocks of 16)
+constexpr int QW = WIN_W / 2;                       // 144 q columns
+constexpr int QP = QW + 8;                          // q ring pitch (u16): conflict-free level-3 pair loads
+constexpr int QRING = 32;                           // q / q^2 ring rows (4 blocks of 8)
+constexpr int ENC_PIX = PRING * WIN_W;              // 18432 B
+constexpr int ENC_Q = QRING * QP * 2;               // 9728 B
+constexpr int ENC_SMEM = ENC_PIX + ENC_Q;           // 28160 B
+static_assert(ENC_PIX % 16 == 0 && ENC_Q % 16 == 0, "ring alignment");
+
+// Sum of squares of four q values (< 1024) held as u16 pairs p01, p23, by bytes: q = 256 qh + ql,
+// q^2 = 65536 qh^2 + 512 qh ql + ql^2; the low and high bytes of the four values are gathered with
+// two PRMTs and the three partial sums accumulate by DP4A (5 instructions for 4 squares).
+__device__ __forceinline__ void sq_bytes(uint32_t p01, uint32_t p23, unsigned &sl, unsigned &sc, unsigned &sh) {
+    const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
+    sl = __dp4a(lo, lo, sl);
+    sc = __dp4a(lo, hi, sc);
+    sh = __dp4a(hi, hi, sh);
+}
+
+__device__ __forceinline__ uint32_t lds32(const uint16_t *p) { return *reinterpret_cast<const uint32_t *>(p); }
+
+__global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_constant__ CUtensorMap tmap,
                                                            const EncParams p) {
     extern __shared__ __align__(128) unsigned char esm[];
-    TileSmem &ts = *reinterpret_cast<TileSmem *>(esm);
-    uint8_t(*pix)[WIN_W] = reinterpret_cast<uint8_t(*)[WIN_W]>(esm + TILE_SMEM);
-    uint16_t(*qe)[QE_W] = reinterpret_cast<uint16_t(*)[QE_W]>(esm + TILE_SMEM + WIN_H * WIN_W);
-    __shared__ __align__(8) uint64_t wbar;
+    uint8_t *const pix = esm;
+    uint16_t *const qe = reinterpret_cast<uint16_t *>(esm + ENC_PIX);
+    __shared__ __align__(8) uint64_t bars[4];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int img_i = blockIdx.z;
-    const int ry = p.rr0 + blockIdx.y;
-    const int rx0 = blockIdx.x * TR;
-    const int nr = min(TR, p.rw - rx0);
-    const int x0 = rx0 * 16, y0 = ry * 16;
-    const int wx0 = x0 - 16, wy0 = y0 - 16;
-    const Win w{pix, qe, x0, y0, wx0, wy0, p.W, p.H};
-
-    // ---- K1a: stage the pixel window with one TMA box (the image viewed as u16 pairs, so a
-    // 288-byte window row is one 144-element box row; out-of-image bytes are zero-filled)
     if (tid == 0) {
-        mbar_init(&wbar, 1);
+        for (int b = 0; b < 4; b++) mbar_init(&bars[b], 1);
         fence_mbar_init();
-        mbar_arrive_expect_tx(&wbar, WIN_H * WIN_W);
-        tma_load_3d(&pix[0][0], &tmap, wx0 / 2, wy0 - p.y_res0, img_i, &wbar);
+        prefetch_tmap(&tmap);
     }
     __syncthreads();
-    mbar_wait(&wbar, 0);
-    // ---- K1b: even-phase 2x2 sums, 4 per thread-step via packed u16x2 adds
-    for (int c = tid; c < QE_H * (QE_WL / 4); c += ET) {
-        const int qi = c / (QE_WL / 4), qj = (c % (QE_WL / 4)) * 4;
-        const uint2 a = *reinterpret_cast<const uint2 *>(&pix[2 * qi][2 * qj]);
-        const uint2 b = *reinterpret_cast<const uint2 *>(&pix[2 * qi + 1][2 * qj]);
-        // bytes 0, 2 and 1, 3 of each word zero-extended into u16 lanes (PRMT), summed lane-wise
-        uint2 s;
-        s.x = (__byte_perm(a.x, 0u, 0x4240) + __byte_perm(a.x, 0u, 0x4341)) +
-              (__byte_perm(b.x, 0u, 0x4240) + __byte_perm(b.x, 0u, 0x4341));
-        s.y = (__byte_perm(a.y, 0u, 0x4240) + __byte_perm(a.y, 0u, 0x4341)) +
-              (__byte_perm(b.y, 0u, 0x4240) + __byte_perm(b.y, 0u, 0x4341));
-        *reinterpret_cast<uint2 *>(&qe[qi][qj]) = s;
-    }
-    __syncthreads();
-
+    unsigned par = 0;  // expected phase parity of each slot's barrier
     const bool try1 = p.root_level == 1 && p.min_dim >= 32;  // encoder.py:231 guard 2*size <= min_dim
-    // ---- K1c: block moments of every level-1..3 node.  Lane = one 4x4 level-3 node (16 pixels);
-    // half-warps take the warp's two roots (slots warp, warp + EW) in one pass.  Level-2 sums over 4
-    // lanes, level-1 sums over the half-warp (its Sr, Srr from the level-2 partials).
+    const bool vis1 = p.root_level == 1;
+    const int hw = lane >> 4, m = lane & 15;
+    const int lx = node3_x(m), ly = node3_y(m);
+    const int k2 = m >> 2, nx2 = node2_x(k2), ny2 = node2_y(k2);
+    // sure-rejection bounds bound(E) * n^2: level-1 node, its level-2 quadrants, level-2 node, its
+    // level-3 quadrants
+    const float bn2_1 = (float)p.p2b[1] * 65536.f, bn2_1k = (float)p.p2b[1] * 4096.f;
+    const float bn2_2 = (float)p.p2b[2] * 4096.f, bn2_2k = (float)p.p2b[2] * 256.f;
+
     {
-        const int hw = lane >> 4, m = lane & 15;
-        const int slot = warp + EW * hw;
-        const bool live = slot < nr;
-        const int sl = live ? slot : 0;
-        const int lx = node3_x(m), ly = node3_y(m);
-        int r[16];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const uint32_t wd = *reinterpret_cast<const uint32_t *>(&pix[16 + ly + i][16 + 16 * sl + lx]);
-#pragma unroll
-            for (int j = 0; j < 4; j++) r[4 * i + j] = (wd >> (8 * j)) & 0xFF;
-        }
-        // 2x2 cell sums (level-4 ranges, Morton order inside the node) and the node's Sr, Srr
-        int sr3 = 0, srr3 = 0;
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            const int i0 = 2 * (c >> 1), j0 = 2 * (c & 1);
-            const int a0 = r[4 * i0 + j0], a1 = r[4 * i0 + j0 + 1], a2 = r[4 * i0 + 4 + j0], a3 = r[4 * i0 + 5 + j0];
-            const int cs = a0 + a1 + a2 + a3, css = a0 * a0 + a1 * a1 + a2 * a2 + a3 * a3;
-            if (live) {
-                ts.sr4[slot][4 * m + c] = cs;
-                ts.srr4[slot][4 * m + c] = css;
+        // CTA (band, chunk, image): root rows [chunk * chunk_rows, ...) of one 16-root column band;
+        // blockIdx.x (band) runs fastest, so horizontally adjacent bands walk the same rows together
+        // and their shared halo columns are read from DRAM once
+        const int band = blockIdx.x, img_i = blockIdx.z;
+        const int rowi = blockIdx.y * p.chunk_rows;
+        const int steps = min(p.chunk_rows, p.rows - rowi);
+        const int ry0 = p.rr0 + rowi, ry_last = ry0 + steps - 1;
+        const int x0 = band * TR * 16, wx0 = x0 - 16;
+        const int nr = min(TR, p.rw - band * TR);
+        const Win w{pix, qe, WIN_W, QP, PRING - 1, QRING - 1, 0, 0, wx0, p.W, p.H};
+
+        auto issue = [&](int g) {  // thread 0: pixel block g (rows 16g .. 16g + 15) into slot g & 3
+            mbar_arrive_expect_tx(&bars[g & 3], 16 * WIN_W);
+            tma_load_3d(pix + ((16 * g) & (PRING - 1)) * WIN_W, &tmap, wx0 / 2, 16 * g - p.y_res0, img_i,
+                        &bars[g & 3]);
+        };
+        auto wait = [&](int g) {
+            mbar_wait(&bars[g & 3], (par >> (g & 3)) & 1u);
+            par ^= 1u << (g & 3);
+        };
+        auto build = [&](int g) {  // q rows 8g .. 8g + 7 from pixel block g (4 q per item)
+            for (int it = tid; it < 8 * (QW / 4); it += ET) {
+                const int qi = it / (QW / 4), c4 = it % (QW / 4);
+                const uint8_t *a = pix + ((16 * g + 2 * qi) & (PRING - 1)) * WIN_W + 8 * c4;
+                const uint2 u = *reinterpret_cast<const uint2 *>(a);
+                const uint2 v = *reinterpret_cast<const uint2 *>(a + WIN_W);
+                // bytes 0, 2 and 1, 3 of each word zero-extended into u16 lanes (PRMT), summed lane-wise
+                uint2 s;
+                s.x = (__byte_perm(u.x, 0u, 0x4240) + __byte_perm(u.x, 0u, 0x4341)) +
+                      (__byte_perm(v.x, 0u, 0x4240) + __byte_perm(v.x, 0u, 0x4341));
+                s.y = (__byte_perm(u.y, 0u, 0x4240) + __byte_perm(u.y, 0u, 0x4341)) +
+                      (__byte_perm(v.y, 0u, 0x4240) + __byte_perm(v.y, 0u, 0x4341));
+                *reinterpret_cast<uint2 *>(qe + ((8 * g + qi) & (QRING - 1)) * QP + 4 * c4) = s;
             }
-            sr3 += cs;
-            srr3 += css;
+        };
+
+        if (tid == 0) {
+            fence_proxy_async();
+            issue(ry0 - 1);
+            issue(ry0);
+            issue(ry0 + 1);
         }
-        // q-moments of the lane's 16 pixels against the domain of node (nx, ny, s)
-        auto part = [&](int nx, int ny, int s, int &sq, int &sqq, int &sqr) {
-            const int gdx = clampi(x0 + 16 * sl + nx - s / 2, 0, p.W - 2 * s);
-            const int gdy = clampi(y0 + ny - s / 2, 0, p.H - 2 * s);
-            const uint16_t *qp = &qe[(gdy - wy0) / 2 + (ly - ny)][(gdx - wx0) / 2 + (lx - nx)];
-            sq = sqq = sqr = 0;
+        wait(ry0 - 1);
+        build(ry0 - 1);
+        wait(ry0);
+        build(ry0);
+
+        for (int ry = ry0; ry <= ry_last; ry++) {
+            wait(ry + 1);
+            build(ry + 1);
+            __syncthreads();  // the window of row ry is complete; every warp is done with row ry - 1
+            if (tid == 0 && ry < ry_last) {  // block ry + 2 is read by step ry + 1 only
+                fence_proxy_async();         // generic reads of block ry - 2 precede the refill
+                issue(ry + 2);
+            }
+            // ---------------- the 16 roots of root row ry (warp w: slots w, w + 8)
+            const int slot = warp + EW * hw;
+            const bool live = slot < nr;
+            const int sl = live ? slot : 0;
+            const int rxg = x0 + 16 * sl, ryg = 16 * ry;
+            const int x3 = rxg + lx, y3 = ryg + ly;
+            uint32_t rw[4];
 #pragma unroll
             for (int i = 0; i < 4; i++)
+                rw[i] = *reinterpret_cast<const uint32_t *>(pix + ((y3 + i) & (PRING - 1)) * WIN_W + (x3 - wx0));
+            int sr3 = 0, srr3 = 0;
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const int q = qp[i * QE_W + j];
-                    sq += q;
-                    sqq += q * q;
-                    sqr += q * r[4 * i + j];
+            for (int i = 0; i < 4; i++) {
+                sr3 = (int)__dp4a(rw[i], 0x01010101u, (unsigned)sr3);
+                srr3 = (int)__dp4a(rw[i], rw[i], (unsigned)srr3);
+            }
+            // level 3: the lane's own node; the domain may start on an odd q column (PRMT-aligned pairs)
+            int sq3, sqq3, sqr3;
+            {
+                const int gdx = clampi(x3 - 2, 0, p.W - 8), gdy = clampi(y3 - 2, 0, p.H - 8);
+                const int qx = (gdx - wx0) >> 1, qy = gdy >> 1;
+                const int cw = qx & ~1;
+                const unsigned sel = (qx & 1) ? 0x5432u : 0x3210u;
+                unsigned sqp = 0, sqr = 0, sql = 0, sqc = 0, sqh = 0;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int row = (qy + i) & (QRING - 1);
+                    const uint16_t *qr = qe + row * QP + cw;
+                    const uint32_t w0 = lds32(qr), w1 = lds32(qr + 2), w2 = lds32(qr + 4);
+                    const uint32_t p01 = __byte_perm(w0, w1, sel), p23 = __byte_perm(w1, w2, sel);
+                    sqr = __dp2a_lo(p01, rw[i], sqr);
+                    sqr = __dp2a_hi(p23, rw[i], sqr);
+                    sqp += p01 + p23;
+                    sq_bytes(p01, p23, sql, sqc, sqh);
                 }
-        };
-        int sq, sqq, sqr;
-        part(lx, ly, 4, sq, sqq, sqr);  // level 3: the lane is the node
-        if (live) ts.m3[slot][m] = Mom{sr3, srr3, sq, sqq, sqr};
-        // level 2 (4-lane groups)
-        const int k2 = m >> 2;
-        int v[5] = {sr3, srr3, 0, 0, 0};
-        part(node2_x(k2), node2_y(k2), 8, v[2], v[3], v[4]);
+                sq3 = (int)((sqp & 0xFFFF) + (sqp >> 16));
+                sqr3 = (int)sqr;
+                sqq3 = (int)((sqh << 16) + (sqc << 9) + sql);
+            }
+            // the lane's share of an even-phase level-1/2 domain starting at window q column qx, q row qy
+            auto part = [&](int qx, int qy, unsigned &sqp, unsigned &sqr, unsigned &sqq) {
+                sqp = 0;
+                sqr = 0;
+                unsigned sql = 0, sqc = 0, sqh = 0;
 #pragma unroll
-        for (int k = 0; k < 5; k++) {
-            v[k] += __shfl_xor_sync(FULL, v[k], 1);
-            v[k] += __shfl_xor_sync(FULL, v[k], 2);
-        }
-        if (live && (m & 3) == 0) ts.m2[slot][k2] = Mom{v[0], v[1], v[2], v[3], v[4]};
-        // level 1 (half-warp): Sr, Srr from the level-2 sums, the q-moments from the lanes
-        int u[5] = {v[0], v[1], 0, 0, 0};
-        if (try1) part(0, 0, 16, u[2], u[3], u[4]);
+                for (int i = 0; i < 4; i++) {
+                    const uint16_t *qr = qe + ((qy + i) & (QRING - 1)) * QP + qx;
+                    const uint32_t p01 = lds32(qr), p23 = lds32(qr + 2);  // qx even (not always 4-aligned)
+                    sqr = __dp2a_lo(p01, rw[i], sqr);
+                    sqr = __dp2a_hi(p23, rw[i], sqr);
+                    sqp += p01 + p23;
+                    sq_bytes(p01, p23, sql, sqc, sqh);
+                }
+                sqq = (sqh << 16) + (sqc << 9) + sql;
+            };
+            // level 2: node k2 of the root; 4-lane groups
+            Mom m2;
+            {
+                const int gdx = clampi(rxg + nx2 - 4, 0, p.W - 16), gdy = clampi(ryg + ny2 - 4, 0, p.H - 16);
+                unsigned sqp, sqr, sqq;
+                part(((gdx - wx0) >> 1) + (lx - nx2), (gdy >> 1) + (ly - ny2), sqp, sqr, sqq);
+                int v[5] = {sr3, srr3, (int)sqp, (int)sqq, (int)sqr};  // packed Sq halves stay < 2^16
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
-            u[k] += __shfl_xor_sync(FULL, u[k], 4);
-            u[k] += __shfl_xor_sync(FULL, u[k], 8);
-        }
+                for (int k = 0; k < 5; k++) {
+                    v[k] += __shfl_xor_sync(FULL, v[k], 1);
+                    v[k] += __shfl_xor_sync(FULL, v[k], 2);
+                }
+                m2 = Mom{v[0], v[1], (int)((v[2] & 0xFFFF) + ((unsigned)v[2] >> 16)), v[3], v[4]};
+            }
+            // level 1: the half-warp (one root); Sr, Srr from the level-2 sums
+            Mom m1{0, 0, 0, 0, 0};
+            if (try1) {
+                const int gdx = clampi(rxg - 8, 0, p.W - 32), gdy = clampi(ryg - 8, 0, p.H - 32);
+                unsigned sqp, sqr, sqq;
+                part(((gdx - wx0) >> 1) + lx, (gdy >> 1) + ly, sqp, sqr, sqq);
+                int u[5] = {m2.sr, m2.srr, (int)((sqp & 0xFFFF) + (sqp >> 16)), (int)sqq, (int)sqr};
 #pragma unroll
-        for (int k = 2; k < 5; k++) {
-            u[k] += __shfl_xor_sync(FULL, u[k], 1);
-            u[k] += __shfl_xor_sync(FULL, u[k], 2);
-            u[k] += __shfl_xor_sync(FULL, u[k], 4);
-            u[k] += __shfl_xor_sync(FULL, u[k], 8);
-        }
-        if (live && m == 0) ts.m1[slot] = Mom{u[0], u[1], u[2], u[3], u[4]};
-    }
-    __syncwarp();
+                for (int k = 0; k < 2; k++) {
+                    u[k] += __shfl_xor_sync(FULL, u[k], 4);
+                    u[k] += __shfl_xor_sync(FULL, u[k], 8);
+                }
+#pragma unroll
+                for (int k = 2; k < 5; k++) {
+                    u[k] += __shfl_xor_sync(FULL, u[k], 1);
+                    u[k] += __shfl_xor_sync(FULL, u[k], 2);
+                    u[k] += __shfl_xor_sync(FULL, u[k], 4);
+                    u[k] += __shfl_xor_sync(FULL, u[k], 8);
+                }
+                m1 = Mom{u[0], u[1], u[2], u[3], u[4]};
+            }
+            const Mom m3{sr3, srr3, sq3, sqq3, sqr3};
+            // ---- decisions (encoder.py:226-246).  A node whose best free least-squares fit already
+            // misses its bound is rejected for sure (no quantised fit can do better) -- the common
+            // case on textured images -- and a warp whose nodes are all surely rejected skips the
+            // exact decision; otherwise node_decide runs the exact one.
+            // level 2: quadrant lane = m & 3, kid = own level-3 node
+            bool acc2 = false;
+            uint64_t rec2 = 0;
+            {
+                const int g0 = lane & ~3;
+                int ks[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) ks[c] = __shfl_sync(FULL, sr3, g0 + c);
+                const bool kid_out = !p.mns || surely_above<4>(m3, bn2_2k);
+                const unsigned kb = __ballot_sync(FULL, kid_out);
+                const bool sure = surely_above<6>(m2, bn2_2) &&
+                                  (((kb >> g0) & 15u) != 0 || gate_fails(6, m2.sr, ks, p.gate[2]));
+                if (__any_sync(FULL, live && !sure))
+                    node_decide(w, p, live, true, m & 3, 2, rxg + nx2, ryg + ny2, m2, ks, m3,
+                                [g0](unsigned b) { return (b >> g0) & 15u; }, acc2, rec2);
+            }
+            // level 1: quadrant lanes 0, 4, 8, 12 of the half (kid = the lane's level-2 node)
+            bool acc1 = false;
+            uint64_t rec1 = 0;
+            if (try1) {
+                const int hb = 16 * hw;
+                int ks[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) ks[c] = __shfl_sync(FULL, m2.sr, hb + 4 * c);
+                auto gather = [hb](unsigned b) {  // bits hb, hb + 4, hb + 8, hb + 12 -> 0..3
+                    unsigned x = (b >> hb) & 0x1111u;
+                    x = (x | (x >> 3)) & 0x0303u;
+                    return (x | (x >> 6)) & 15u;
+                };
+                const bool kid_out = (m & 3) == 0 && (!p.mns || surely_above<6>(m2, bn2_1k));
+                const unsigned kb = __ballot_sync(FULL, kid_out);
+                const bool sure = surely_above<8>(m1, bn2_1) &&
+                                  ((kb & (0x1111u << hb)) != 0 || gate_fails(8, m1.sr, ks, p.gate[1]));
+                if (__any_sync(FULL, live && !sure))
+                    node_decide(w, p, live, (m & 3) == 0, k2, 1, rxg, ryg, m1, ks, m2, gather, acc1, rec1);
+            }
+            // level 3 (own node): phase 1, and the rejected path (finite e3) only where visible
+            bool acc3;
+            uint64_t rec3 = phase1(x3, y3, 3, 4, m3, p.p1b[3], acc3);
+            const bool vis2 = !vis1 || !acc1;
+            const bool vis3 = vis2 && !acc2;
+            uint64_t rec4[4];  // written (and read) only on the rejected path
+            if (live && vis3 && !acc3) level3_rejected(w, p, x3, y3, sr3, acc3, rec3, rec4);
+            const bool vis4 = vis3 && !acc3;
 
-    // ---- K2: decisions.  Round 1 (warp-local: warp w owns root slots w, w + EW): the 8 level-2
-    // nodes of its roots x 4 quadrant lanes (a node is decided whether or not a parent accepts --
-    // the emission's visibility flags discard covered decisions); round 2 (warp-local): the level-3
-    // nodes not covered by a level-2 leaf (and the level-4 quartets below them), one per lane;
-    // round 3 (CTA-wide, warps 0-1): the level-1 roots.
-    const bool mns = p.mns != 0;
-    {  // round 1: the 8 level-2 nodes of this warp's two roots x 4 quadrant lanes
-        const int node = lane >> 2, s = warp + EW * (node >> 2), k = node & 3;
-        const bool live = s < nr;
-        const int sc = live ? s : 0;
-        bool acc;
-        uint64_t rec;
-        node_quad_lanes(w, p, live, sc, 2, node2_x(k), node2_y(k), ts.m2[sc][k], &ts.m3[sc][4 * k], true, acc, rec);
-        if (live && (lane & 3) == 0) {
-            ts.acc2[s][k] = acc;
-            ts.rec2[s][k] = rec;
-        }
-    }
-    __syncwarp();
-    {
-        const int s = warp + EW * (lane >> 4), m = lane & 15;
-        if (s < nr) {
-            const bool vis = !ts.acc2[s][m >> 2];  // a level-1 acceptance is applied at the emission
-            bool acc = false;
-            uint64_t rec = 0;
-            if (vis) {
-                const int nx = node3_x(m), ny = node3_y(m);
-                rec = phase1(x0 + 16 * s + nx, y0 + ny, 3, 4, ts.m3[s][m], p.p1b[3], acc);
-                if (!acc) {  // level-4 moments (odd-phase domains) of the 4 children, then phase 2 / split
-                    Mom k4[4];
-                    for (int c = 0; c < 4; c++) {
-                        const int cx = nx + 2 * (c & 1), cy = ny + 2 * (c >> 1);
-                        Mom mm{ts.sr4[s][4 * m + c], ts.srr4[s][4 * m + c], 0, 0, 0};
-                        for (int i = 0; i < 2; i++)
-                            for (int j = 0; j < 2; j++) {
-                                const int q = dom_q(w, s, cx, cy, 2, cx + j, cy + i);
-                                mm.sq += q;
-                                mm.sqq += q * q;
-                                mm.sqr += q * pixel(w, s, cx + j, cy + i);
-                            }
-                        k4[c] = mm;
+            // ---- DFS (Morton) emission: the covering leaf's record on the first lane it covers, or
+            // the node's four level-4 records; offsets by two ballots (records per lane: 0, 1 or 4)
+            uint64_t cov;
+            int nrec;
+            if (vis1 && acc1) {
+                nrec = m == 0;
+                cov = rec1;
+            } else if (vis2 && acc2) {
+                nrec = (m & 3) == 0;
+                cov = rec2;
+            } else if (vis3 && acc3) {
+                nrec = 1;
+                cov = rec3;
+            } else {
+                nrec = 4;
+                cov = 0;
+            }
+            if (!live) nrec = 0;
+            const unsigned half = hw ? 0xFFFF0000u : 0x0000FFFFu, lt = lanemask_lt() & half;
+            const unsigned b1 = __ballot_sync(FULL, nrec != 0) & half, b4 = __ballot_sync(FULL, nrec == 4) & half;
+            const int off = __popc(b1 & lt) + 3 * __popc(b4 & lt);
+            const long long root =
+                ((long long)img_i * p.rows + (ry - p.rr0)) * p.rw + (long long)band * TR + sl;
+            if (live) {
+                uint64_t *st = p.stage + root * 64 + off;
+                if (nrec == 4) {
+#pragma unroll
+                    for (int c = 0; c < 4; c++) st[c] = rec4[c];
+                } else if (nrec) {
+                    st[0] = cov;
+                }
+                if (m == 0) p.root_cnt[root] = __popc(b1) + 3 * __popc(b4);
+                if (p.unit_map) {
+                    uint2 u;
+                    if (vis4) {
+                        u.x = (uint32_t)mns_unit_of_record(rec4[0], rxg, ryg, lx, ly) |
+                              ((uint32_t)mns_unit_of_record(rec4[1], rxg, ryg, lx + 2, ly) << 16);
+                        u.y = (uint32_t)mns_unit_of_record(rec4[2], rxg, ryg, lx, ly + 2) |
+                              ((uint32_t)mns_unit_of_record(rec4[3], rxg, ryg, lx + 2, ly + 2) << 16);
+                    } else {
+                        u.x = mns_unit_pair_of_record(cov, rxg, ryg, lx, ly);
+                        u.y = mns_unit_pair_of_record(cov, rxg, ryg, lx, ly + 2);
                     }
-                    if (mns) acc = phase2_node(w, p, s, 3, nx, ny, 4, ts.m3[s][m].sr, k4, &rec);
-                    if (!acc)
-                        for (int c = 0; c < 4; c++) {
-                            bool dummy;
-                            ts.rec4[s][4 * m + c] = phase1(x0 + 16 * s + nx + 2 * (c & 1), y0 + ny + 2 * (c >> 1), 4,
-                                                           2, k4[c], INFINITY, dummy);
-                        }
+                    *reinterpret_cast<uint2 *>(&p.unit_map[root * 32 + 2 * m]) = u;
                 }
-            }
-            ts.acc3[s][m] = acc;
-            ts.rec3[s][m] = rec;
-        }
-    }
-    // round 3: the level-1 roots of the whole tile, 16 roots x 4 quadrant lanes on warps 0-1 (every
-    // lane busy, instead of 8 lanes of every warp); the other warps wait at the emission barrier
-    __syncthreads();
-    if (warp < 2) {
-        const int s = 8 * warp + (lane >> 2);
-        const bool live = s < nr;
-        const int sc = live ? s : 0;
-        bool acc;
-        uint64_t rec;
-        node_quad_lanes(w, p, live, sc, 1, 0, 0, ts.m1[sc], ts.m2[sc], try1, acc, rec);
-        if (live && (lane & 3) == 0) {
-            ts.acc1[s] = acc;
-            ts.rec1[s] = rec;
-        }
-    }
-    __syncthreads();
-
-    // ---- K2b: DFS (Morton) emission.  Half-warps take the warp's two roots in one pass; lane m
-    // owns level-3 node m (cells 4m..4m+3): the covering leaf's record on the first lane it covers,
-    // or the node's four level-4 records; offsets by two ballots (records per lane: 0, 1 or 4).
-    {
-        const int hw = lane >> 4, m = lane & 15, a = m >> 2;
-        const int slot = warp + EW * hw;
-        const bool live = slot < nr;
-        const int sl = live ? slot : 0;
-        const bool vis1 = p.root_level == 1;
-        const bool acc1 = ts.acc1[sl];
-        const bool vis2 = !vis1 || !acc1;
-        const bool acc2 = ts.acc2[sl][a];
-        const bool vis3 = vis2 && !acc2;
-        const bool acc3 = ts.acc3[sl][m];
-        const bool vis4 = vis3 && !acc3;
-        uint64_t cov;
-        int nrec;
-        if (vis1 && acc1) {
-            nrec = m == 0;
-            cov = ts.rec1[sl];
-        } else if (vis2 && acc2) {
-            nrec = (m & 3) == 0;
-            cov = ts.rec2[sl][a];
-        } else if (vis3 && acc3) {
-            nrec = 1;
-            cov = ts.rec3[sl][m];
-        } else {
-            nrec = 4;
-            cov = ts.rec4[sl][4 * m];
-        }
-        if (!live) nrec = 0;
-        const unsigned half = hw ? 0xFFFF0000u : 0x0000FFFFu, lt = lanemask_lt() & half;
-        const unsigned b1 = __ballot_sync(FULL, nrec != 0) & half, b4 = __ballot_sync(FULL, nrec == 4) & half;
-        const int off = __popc(b1 & lt) + 3 * __popc(b4 & lt);
-        const long long root = (long long)img_i * p.rows * p.rw + (long long)(ry - p.rr0) * p.rw + rx0 + sl;
-        if (live) {
-            uint64_t *st = p.stage + root * 64 + off;
-            if (nrec == 4) {
-#pragma unroll
-                for (int c = 0; c < 4; c++) st[c] = ts.rec4[sl][4 * m + c];
-            } else if (nrec) {
-                st[0] = cov;
-            }
-            if (m == 0) p.root_cnt[root] = __popc(b1) + 3 * __popc(b4);
-            if (p.unit_map) {
-                const int rxg = x0 + 16 * sl, lx = node3_x(m), ly = node3_y(m);
-                uint2 u;
-                if (vis4) {
-                    u.x = (uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m], rxg, y0, lx, ly) |
-                          ((uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 1], rxg, y0, lx + 2, ly) << 16);
-                    u.y = (uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 2], rxg, y0, lx, ly + 2) |
-                          ((uint32_t)mns_unit_of_record(ts.rec4[sl][4 * m + 3], rxg, y0, lx + 2, ly + 2) << 16);
-                } else {
-                    u.x = mns_unit_pair_of_record(cov, rxg, y0, lx, ly);
-                    u.y = mns_unit_pair_of_record(cov, rxg, y0, lx, ly + 2);
-                }
-                *reinterpret_cast<uint2 *>(&p.unit_map[root * 32 + 2 * m]) = u;
             }
         }
     }
@@ -811,14 +911,31 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     // rows [16 rr0 - 16, 16 rr1 + 16) of each image are resident: the tensor map starts there
     p.y_res0 = 16 * rr0 - 16 > 0 ? 16 * rr0 - 16 : 0;
     const int y_res1 = 16 * rr1 + 16 < H ? 16 * rr1 + 16 : H;
-    MNS_CHECK_ARG(n_images <= 65535 && p.rows <= 65535, "grid too large");
     CUtensorMap tmap{};
     if (encode_tmap_3d(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, img + (ptrdiff_t)p.y_res0 * pitch, (uint64_t)W / 2,
                        (uint64_t)(y_res1 - p.y_res0), (uint64_t)n_images, (uint64_t)pitch,
-                       (uint64_t)(n_images > 1 ? image_stride : pitch * (int64_t)(y_res1 - p.y_res0)), WIN_W / 2,
-                       WIN_H, 1))
+                       (uint64_t)(n_images > 1 ? image_stride : pitch * (int64_t)(y_res1 - p.y_res0)), WIN_W / 2, 16,
+                       1))
         return -1;
-    const dim3 grid((unsigned)p.tiles_per_row, (unsigned)p.rows, (unsigned)n_images);
+    // chunks of root rows per band: about two waves of resident CTAs (a CTA re-stages two blocks of
+    // halo rows per chunk, so chunks are as long as the wave count allows)
+    static int ctas = 0;
+    if (!ctas) {
+        int dev = 0, sms = 148, occ = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mns_encode_kernel, ET, ENC_SMEM) != cudaSuccess ||
+            occ < 1)
+            occ = 1;
+        ctas = sms * occ;
+    }
+    const long long cols = (long long)p.tiles_per_row * n_images;
+    long long chunks = 2ll * ctas / cols;
+    chunks = chunks < 1 ? 1 : (chunks > p.rows ? p.rows : chunks);
+    p.chunk_rows = (int)((p.rows + chunks - 1) / chunks);
+    chunks = (p.rows + p.chunk_rows - 1) / p.chunk_rows;
+    MNS_CHECK_ARG(n_images <= 65535 && chunks <= 65535, "grid too large");
+    const dim3 grid((unsigned)p.tiles_per_row, (unsigned)chunks, (unsigned)n_images);
     mns_encode_kernel<<<grid, ET, ENC_SMEM, stream>>>(tmap, p);
     MNS_CUDA_TRY(cudaGetLastError());
     if (cstream != stream) {  // the compaction on its own stream, after the encoder

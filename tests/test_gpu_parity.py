@@ -807,7 +807,7 @@ def test_f64_strip_decoder_three_strips_on_one_gpu(mns):
     px = synth_image(512, 41, noise_sigma=10.0, n_blobs=8)
     cfg = mns.EncoderConfig()
     rec, _ = O.encode_quadtree_records(px, (8.0, 8.0, 8.0), 16.0, True)
-    want, _, sweeps = O.decode_records(rec, W, H, max_iters=10, stop_delta=0.5)
+    want, _, sweeps = O.decode_records(rec, W, H, max_iters=10, stop_delta=1.0)
     assert sweeps < 10
     world = 3
     decs = []
@@ -828,7 +828,7 @@ def test_f64_strip_decoder_three_strips_on_one_gpu(mns):
         g = max(float(d.delta_view()[0]) for d in decs)  # the all-reduce (MAX)
         for d in decs:
             d.delta_view()[0] = g
-            d.decide(0.5)
+            d.decide(1.0)
         for k in range(world - 1):  # halo exchange of the freshly written rasters
             a, b = decs[k], decs[k + 1]
             ra, rb = bufs[k][(it + 1) & 1], bufs[k + 1][(it + 1) & 1]
