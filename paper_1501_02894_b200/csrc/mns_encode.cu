@@ -258,23 +258,48 @@ __device__ bool phase2_node(const Win &w, const EncParams &p, int level, int nx,
 // also rounds n Sqq and n Sqr, whose absolute errors enter the margin (`extra`).  The margin is
 // 16x the worst rounding error, so "true" is never wrong.
 template <int NL>
-__device__ __forceinline__ bool surely_above(const Mom &m, float bn2) {
-    float dr, d, nn, extra = 0.f;
+struct FitGap {  // a = Dr D, b = N^2, d = D and the rounding scales of surely_above
+    float a, b, d, dr, extra_s, extra_n;
+    bool d0;
+};
+
+template <int NL>
+__device__ __forceinline__ FitGap<NL> fit_gap(const Mom &m) {
+    FitGap<NL> g;
+    g.extra_s = 0.f;
+    g.extra_n = 0.f;
     if (NL <= 6) {
-        dr = (float)((m.srr << NL) - m.sr * m.sr);
+        g.dr = (float)((m.srr << NL) - m.sr * m.sr);
         const unsigned du = ((unsigned)m.sqq << NL) - (unsigned)m.sq * (unsigned)m.sq;
-        d = (float)du;
-        nn = fmaf(-(float)m.sq, (float)m.sr, (float)(m.sqr << NL));
-        if (du == 0u) return dr > bn2 * (1.f + 1.f / 1048576.f);
+        g.d = (float)du;
+        g.d0 = du == 0u;
+        const float nn = fmaf(-(float)m.sq, (float)m.sr, (float)(m.sqr << NL));
+        g.b = nn * nn;
     } else {
-        dr = (float)(((unsigned)m.srr << NL) - (unsigned)m.sr * (unsigned)m.sr);
+        g.dr = (float)(((unsigned)m.srr << NL) - (unsigned)m.sr * (unsigned)m.sr);
         const float S = (float)m.sqq * (float)(1 << NL), T = (float)m.sqr * (float)(1 << NL);
-        d = fmaf(-(float)m.sq, (float)m.sq, S);
-        nn = fmaf(-(float)m.sq, (float)m.sr, T);
-        extra = (dr + bn2) * S + fabsf(nn) * T;
+        g.d = fmaf(-(float)m.sq, (float)m.sq, S);
+        g.d0 = false;
+        const float nn = fmaf(-(float)m.sq, (float)m.sr, T);
+        g.b = nn * nn;
+        g.extra_s = S;
+        g.extra_n = fabsf(nn) * T;
     }
-    const float a = dr * d, b = nn * nn, c = bn2 * d;
-    return a - b - c > (a + b + c + extra) * (1.f / 1048576.f);
+    g.a = g.dr * g.d;
+    return g;
+}
+
+template <int NL>
+__device__ __forceinline__ bool surely_above(const FitGap<NL> &g, float bn2) {
+    if (NL <= 6 && g.d0) return g.dr > bn2 * (1.f + 1.f / 1048576.f);
+    const float c = bn2 * g.d;
+    const float extra = NL <= 6 ? 0.f : (g.dr + bn2) * g.extra_s + g.extra_n;
+    return g.a - g.b - c > (g.a + g.b + c + extra) * (1.f / 1048576.f);
+}
+
+template <int NL>
+__device__ __forceinline__ bool surely_above(const Mom &m, float bn2) {
+    return surely_above<NL>(fit_gap<NL>(m), bn2);
 }
 
 // The phase-2 mean gate (encoder.py:186-188) fails: some quadrant mean is farther than mean_tol from
@@ -515,10 +540,18 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
             mbar_wait(&bars[g & 3], (par >> (g & 3)) & 1u);
             par ^= 1u << (g & 3);
         };
-        auto build = [&](int g) {  // q rows 8g .. 8g + 7 from pixel block g (4 q per item)
-            for (int it = tid; it < 8 * (QW / 4); it += ET) {
-                const int qi = it / (QW / 4), c4 = it % (QW / 4);
-                const uint8_t *a = pix + ((16 * g + 2 * qi) & (PRING - 1)) * WIN_W + 8 * c4;
+        // this thread's q-table items (the same every block): 8 q rows x 36 groups of 4 columns
+        constexpr int NIT = 8 * (QW / 4);
+        const int it1 = tid + ET < NIT ? tid + ET : tid;  // a second item for the first NIT - ET threads
+        const int src0 = 2 * (tid / (QW / 4)) * WIN_W + 8 * (tid % (QW / 4)), dst0 = (tid / (QW / 4)) * QP + 4 * (tid % (QW / 4));
+        const int src1 = 2 * (it1 / (QW / 4)) * WIN_W + 8 * (it1 % (QW / 4)), dst1 = (it1 / (QW / 4)) * QP + 4 * (it1 % (QW / 4));
+        auto build = [&](int g) {  // q rows 8g .. 8g + 7 from pixel block g (4 q per item, packed adds)
+            const uint8_t *pb = pix + ((16 * g) & (PRING - 1)) * WIN_W;
+            uint16_t *qb = qe + ((8 * g) & (QRING - 1)) * QP;
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (k == 1 && tid + ET >= NIT) break;
+                const uint8_t *a = pb + (k ? src1 : src0);
                 const uint2 u = *reinterpret_cast<const uint2 *>(a);
                 const uint2 v = *reinterpret_cast<const uint2 *>(a + WIN_W);
                 // bytes 0, 2 and 1, 3 of each word zero-extended into u16 lanes (PRMT), summed lane-wise
@@ -527,7 +560,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                       (__byte_perm(v.x, 0u, 0x4240) + __byte_perm(v.x, 0u, 0x4341));
                 s.y = (__byte_perm(u.y, 0u, 0x4240) + __byte_perm(u.y, 0u, 0x4341)) +
                       (__byte_perm(v.y, 0u, 0x4240) + __byte_perm(v.y, 0u, 0x4341));
-                *reinterpret_cast<uint2 *>(qe + ((8 * g + qi) & (QRING - 1)) * QP + 4 * c4) = s;
+                *reinterpret_cast<uint2 *>(qb + (k ? dst1 : dst0)) = s;
             }
         };
 
@@ -542,6 +575,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
         wait(ry0);
         build(ry0);
 
+        long long row_root = ((long long)img_i * p.rows + rowi) * p.rw + (long long)band * TR;  // root index of slot 0
         for (int ry = ry0; ry <= ry_last; ry++) {
             wait(ry + 1);
             build(ry + 1);
@@ -648,6 +682,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
             // level 2: quadrant lane = m & 3, kid = own level-3 node
             bool acc2 = false;
             uint64_t rec2 = 0;
+            const FitGap<6> g2 = fit_gap<6>(m2);  // shared by the level-2 node test and level 1's quadrant test
             {
                 const int g0 = lane & ~3;
                 int ks[4];
@@ -655,7 +690,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                 for (int c = 0; c < 4; c++) ks[c] = __shfl_sync(FULL, sr3, g0 + c);
                 const bool kid_out = !p.mns || surely_above<4>(m3, bn2_2k);
                 const unsigned kb = __ballot_sync(FULL, kid_out);
-                const bool sure = surely_above<6>(m2, bn2_2) &&
+                const bool sure = surely_above<6>(g2, bn2_2) &&
                                   (((kb >> g0) & 15u) != 0 || gate_fails(6, m2.sr, ks, p.gate[2]));
                 if (__any_sync(FULL, live && !sure))
                     node_decide(w, p, live, true, m & 3, 2, rxg + nx2, ryg + ny2, m2, ks, m3,
@@ -674,7 +709,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                     x = (x | (x >> 3)) & 0x0303u;
                     return (x | (x >> 6)) & 15u;
                 };
-                const bool kid_out = (m & 3) == 0 && (!p.mns || surely_above<6>(m2, bn2_1k));
+                const bool kid_out = (m & 3) == 0 && (!p.mns || surely_above<6>(g2, bn2_1k));
                 const unsigned kb = __ballot_sync(FULL, kid_out);
                 const bool sure = surely_above<8>(m1, bn2_1) &&
                                   ((kb & (0x1111u << hb)) != 0 || gate_fails(8, m1.sr, ks, p.gate[1]));
@@ -711,8 +746,8 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
             const unsigned half = hw ? 0xFFFF0000u : 0x0000FFFFu, lt = lanemask_lt() & half;
             const unsigned b1 = __ballot_sync(FULL, nrec != 0) & half, b4 = __ballot_sync(FULL, nrec == 4) & half;
             const int off = __popc(b1 & lt) + 3 * __popc(b4 & lt);
-            const long long root =
-                ((long long)img_i * p.rows + (ry - p.rr0)) * p.rw + (long long)band * TR + sl;
+            const long long root = row_root + sl;
+            row_root += p.rw;
             if (live) {
                 uint64_t *st = p.stage + root * 64 + off;
                 if (nrec == 4) {
@@ -729,6 +764,11 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                               ((uint32_t)mns_unit_of_record(rec4[1], rxg, ryg, lx + 2, ly) << 16);
                         u.y = (uint32_t)mns_unit_of_record(rec4[2], rxg, ryg, lx, ly + 2) |
                               ((uint32_t)mns_unit_of_record(rec4[3], rxg, ryg, lx + 2, ly + 2) << 16);
+                    } else if (!((cov >> MNS_REC_PHASE2_SHIFT) & 1)) {  // a phase-1 leaf: one descriptor
+                        const uint32_t d = mns_unit_desc((int)((cov >> MNS_REC_PAYLOAD_SHIFT) & 7),
+                                                         (int)((cov >> MNS_REC_O_SHIFT) & 0xFF),
+                                                         4 - (int)((cov >> MNS_REC_LEVEL_SHIFT) & 3));
+                        u.x = u.y = d | (d << 16);
                     } else {
                         u.x = mns_unit_pair_of_record(cov, rxg, ryg, lx, ly);
                         u.y = mns_unit_pair_of_record(cov, rxg, ryg, lx, ly + 2);
