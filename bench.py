@@ -517,22 +517,24 @@ def run_ours(args, img_np, rank, world, local_rank):
                                  "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3),
                                  "effective_tflops": tf, "tensor_peak_tflops": tpk, "tensor_peak_source": tsrc,
                                  "frac_of_tensor_peak": tf / tpk}
-        for radius in (4, 32):  # encoder.py:312-347 local search (+-4; +-32 is the config-c4 extension)
+        for radius, n_iso in ((4, 1), (32, 1), (32, 8)):  # encoder.py:312-347 local search (+-4 identity =
+            # the reference; +-32 x 8 isometries is the config-c4 extension)
             for _ in range(2):
-                mns.local_search_device(c4, radius)
+                mns.local_search_device(c4, radius, n_iso=n_iso)
             torch.cuda.synchronize()
             runs = []
             for _ in range(5):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                mns.local_search_device(c4, radius)
+                mns.local_search_device(c4, radius, n_iso=n_iso)
                 b.record()
                 torch.cuda.synchronize()
                 runs.append(a.elapsed_time(b))
             ms = float(np.median(runs))
-            cands = 4096 * (2 * radius + 1) ** 2
-            fs[f"local{radius}"] = {"config": f"c4 512^2 B=8 local search +-{radius} (identity)",
-                                    "candidate_fits": cands, "ms": ms, "candidate_fits_per_s": cands / (ms / 1e3)}
+            pairs = 4096 * (2 * radius + 1) ** 2 * n_iso
+            fs[f"local{radius}" + ("" if n_iso == 1 else f"_iso{n_iso}")] = {
+                "config": f"c4 512^2 B=8 local search +-{radius}, {n_iso} isometr{'y' if n_iso == 1 else 'ies'}",
+                "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3)}
 
     small = None if args.no_small else small_configs(dev, rank, world)
 

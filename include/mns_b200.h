@@ -225,11 +225,13 @@ int mns_full_search(const uint8_t *img, int32_t width, int32_t height, int32_t B
                     int32_t range_begin, int32_t range_end, int32_t *out_dom, int8_t *out_iso, uint8_t *out_o,
                     uint8_t *out_code, void *workspace, int64_t workspace_bytes, void *stream);
 
-/* Replaces: encoder.encode_local_search (encoder.py:312-347); radius 4 is the
- * reference (81 candidates), other radii (e.g. 32) are the extension.  Outputs
- * the winning domain origin per 8x8 range of the 8-padded raster. */
-int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t *out_dx,
-                     int32_t *out_dy, uint8_t *out_o, uint8_t *out_code, void *stream);
+/* Replaces: encoder.encode_local_search (encoder.py:312-347); radius 4 and n_iso 1 are the
+ * reference (81 candidates), other radii (up to 32) and n_iso = 8 (the isometries of
+ * mns_full_search, ties to the lowest candidate then isometry) are the extension.  Outputs the
+ * winning domain origin (and isometry; out_iso may be NULL) per 8x8 range of the 8-padded raster. */
+int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t n_iso,
+                     int32_t *out_dx, int32_t *out_dy, int8_t *out_iso, uint8_t *out_o, uint8_t *out_code,
+                     void *stream);
 
 /* Packed .mns bitstream (bitstream.py:130-205) of a record array: per-leaf
  * widths, exclusive scan, MSB-first scatter.  out must hold

@@ -525,39 +525,46 @@ EXPORT int orc_full_search(const uint8_t *img, int W, int H, int B, int step, in
 }
 
 /* encoder.py:312-347 encode_local_search restated with a radius parameter (reference: 4 ->
- * 81 candidates; radius 32 is the extension).  Over the 8-padded raster, 8x8 ranges in raster
- * order; candidates = co-centred 16x16 domain translated by (dy, dx) in [-R, R]^2, dy outer,
- * each clamped; strict '<' keeps the first best.  Outputs per range: domain x, y, o, code. */
-EXPORT int orc_local_search(const uint8_t *img, int W, int H, int radius, int32_t *out_dx, int32_t *out_dy,
-                            uint8_t *out_o, uint8_t *out_code, int nthreads) {
+ * 81 candidates; radius 32 is the extension) and an isometry count (reference: 1; 8 is the
+ * extension: candidate t of a domain is d_t(i,j) = d(src_t(i,j)), as in orc_full_search).  Over the
+ * 8-padded raster, 8x8 ranges in raster order; candidates = co-centred 16x16 domain translated by
+ * (dy, dx) in [-R, R]^2, dy outer, each clamped, then the isometries; strict '<' keeps the first
+ * best.  Outputs per range: domain x, y, isometry, o, code. */
+EXPORT int orc_local_search(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx,
+                            int32_t *out_dy, int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, int nthreads) {
     int rpr = W / 8;
     int64_t nr = (int64_t)rpr * (H / 8);
     if (nthreads < 1) nthreads = 1;
 #pragma omp parallel for schedule(dynamic, 4) num_threads(nthreads)
     for (int64_t ri = 0; ri < nr; ri++) {
         int rx = (int)(ri % rpr) * 8, ry = (int)(ri / rpr) * 8;
-        double r[64], d[64], o_fit;
+        double r[64], d[64], dt[64], o_fit;
         block_u8(img, W, rx, ry, 8, r);
         int bx, by;
         co_domain(rx, ry, 8, W, H, &bx, &by);
         int ob = round_to_int(pw_sum(r, 64) / 64);
         double best_rms = INFINITY;
-        int best_x = bx, best_y = by, best_code = 0;
+        int best_x = bx, best_y = by, best_code = 0, best_t = 0;
         for (int dy = -radius; dy <= radius; dy++)
             for (int dx = -radius; dx <= radius; dx++) {
                 int cx = clampi(bx + dx, 0, W - 16), cy = clampi(by + dy, 0, H - 16);
                 downsample_u8(img, W, cx, cy, 8, d);
-                int code = quantize_contrast(fit_affine_s(r, d, 64, &o_fit));
-                double rms = rms_error(r, d, 64, dequantize_contrast(code), (double)ob);
-                if (rms < best_rms) {
-                    best_rms = rms;
-                    best_x = cx;
-                    best_y = cy;
-                    best_code = code;
+                for (int t = 0; t < n_iso; t++) {
+                    for (int k = 0; k < 64; k++) dt[k] = d[iso_src(t, k / 8, k % 8, 8)];
+                    int code = quantize_contrast(fit_affine_s(r, dt, 64, &o_fit));
+                    double rms = rms_error(r, dt, 64, dequantize_contrast(code), (double)ob);
+                    if (rms < best_rms) {
+                        best_rms = rms;
+                        best_x = cx;
+                        best_y = cy;
+                        best_code = code;
+                        best_t = t;
+                    }
                 }
             }
         out_dx[ri] = best_x;
         out_dy[ri] = best_y;
+        out_iso[ri] = (int8_t)best_t;
         out_o[ri] = (uint8_t)ob;
         out_code[ri] = (uint8_t)best_code;
     }

@@ -75,7 +75,8 @@ def lib():
         L.orc_full_search.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
                                       ctypes.c_int64, P, P, P, P, ctypes.c_int]
         L.orc_local_search.restype = ctypes.c_int
-        L.orc_local_search.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, ctypes.c_int]
+        L.orc_local_search.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
+                                       ctypes.c_int]
         _lib = L
     return _lib
 
@@ -187,18 +188,19 @@ def full_search(pixels: np.ndarray, B: int = 8, step: int = 1, n_iso: int = 1, r
             "iso": iso, "o": o, "code": code, "padded_w": w, "padded_h": h}
 
 
-def local_search(pixels: np.ndarray, radius: int = 4, nthreads=None):
-    """encoder.py:312-347 over the 8-padded image (radius 4 = the reference)."""
+def local_search(pixels: np.ndarray, radius: int = 4, nthreads=None, n_iso: int = 1):
+    """encoder.py:312-347 over the 8-padded image (radius 4, n_iso 1 = the reference)."""
     img = pad(np.asarray(pixels, dtype=np.uint8), 8)
     h, w = img.shape
     n = (w // 8) * (h // 8)
     dx = np.empty(n, np.int32)
     dy = np.empty(n, np.int32)
+    iso = np.empty(n, np.int8)
     o = np.empty(n, np.uint8)
     code = np.empty(n, np.uint8)
-    lib().orc_local_search(_ptr(img), w, h, int(radius), _ptr(dx), _ptr(dy), _ptr(o), _ptr(code),
-                           nthreads or default_threads())
-    return {"dom_x": dx, "dom_y": dy, "o": o, "code": code, "padded_w": w, "padded_h": h}
+    lib().orc_local_search(_ptr(img), w, h, int(radius), int(n_iso), _ptr(dx), _ptr(dy), _ptr(iso), _ptr(o),
+                           _ptr(code), nthreads or default_threads())
+    return {"dom_x": dx, "dom_y": dy, "iso": iso, "o": o, "code": code, "padded_w": w, "padded_h": h}
 
 
 # ---------------------------------------------------------------- records

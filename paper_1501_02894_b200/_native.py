@@ -73,7 +73,7 @@ def _declare(L):
         "mns_decode_f64_finalize": [P, P, P, I32, I32, I32, P, P, P],
         "mns_search_workspace_bytes": [I32, I32, I32, I32, I32, P],
         "mns_full_search": [P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, I64, P],
-        "mns_local_search": [P, I32, I32, I32, P, P, P, P, P],
+        "mns_local_search": [P, I32, I32, I32, I32, P, P, P, P, P, P],
         "mns_stream_workspace_bytes": [I64, P],
         "mns_write_stream": [P, I64, I32, I32, I32, I32, I32, I32, P, I64, P, P, I64, P],
         "mns_read_stream_workspace_bytes": [I64, P],

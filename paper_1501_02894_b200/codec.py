@@ -365,16 +365,19 @@ def full_search_device(img, B: int, step: int = 1, n_iso: int = 1, ranges: Optio
     return out
 
 
-def local_search_device(img, radius: int = 4, stream=None):
+def local_search_device(img, radius: int = 4, stream=None, n_iso: int = 1):
+    """Local search (encoder.py:312-347; radius 4 / n_iso 1 = the reference) over an 8-padded uint8 CUDA
+    image; per-range (dx, dy, iso, o, code) tensors."""
     torch = _torch()
     L = N.lib()
     h, w = img.shape
     nr = (w // 8) * (h // 8)
     dev = img.device
     out = {k: torch.empty(nr, dtype=dt, device=dev) for k, dt in
-           (("dx", torch.int32), ("dy", torch.int32), ("o", torch.uint8), ("code", torch.uint8))}
-    N.check(L.mns_local_search(N.ptr(img), w, h, int(radius), N.ptr(out["dx"]), N.ptr(out["dy"]), N.ptr(out["o"]),
-                               N.ptr(out["code"]), N.stream_ptr(stream)))
+           (("dx", torch.int32), ("dy", torch.int32), ("iso", torch.int8), ("o", torch.uint8),
+            ("code", torch.uint8))}
+    N.check(L.mns_local_search(N.ptr(img), w, h, int(radius), int(n_iso), N.ptr(out["dx"]), N.ptr(out["dy"]),
+                               N.ptr(out["iso"]), N.ptr(out["o"]), N.ptr(out["code"]), N.stream_ptr(stream)))
     return out
 
 
@@ -657,16 +660,18 @@ def encode_full_search(image, range_size: int, config: EncoderConfig, *, n_iso: 
     return code, samples
 
 
-def encode_local_search(image, config: EncoderConfig, *, radius: int = 4) -> QuadtreeCode:
-    """encoder.py:312-347 (radius 4 = the reference's 81 candidates; other radii are the extension)."""
+def encode_local_search(image, config: EncoderConfig, *, radius: int = 4, n_iso: int = 1) -> QuadtreeCode:
+    """encoder.py:312-347 (radius 4, n_iso 1 = the reference's 81 candidates; other radii and 8
+    isometries are the extension)."""
     px = _pixels(image)
     if px.shape[1] < 16 or px.shape[0] < 16:
         raise ValueError("local search needs at least a 16x16 image")
     padded = _padded_np(px, 8)
     h, w = padded.shape
-    res = local_search_device(_to_device_u8(padded), radius)
+    res = local_search_device(_to_device_u8(padded), radius, n_iso=n_iso)
     ids = np.arange(res["dx"].numel())
     rpr = w // 8
     cols = {"range_size": 8, "rx": (ids % rpr) * 8, "ry": (ids // rpr) * 8, "dom_x": res["dx"].cpu().numpy(),
-            "dom_y": res["dy"].cpu().numpy(), "o": res["o"].cpu().numpy(), "code": res["code"].cpu().numpy()}
+            "dom_y": res["dy"].cpu().numpy(), "o": res["o"].cpu().numpy(), "code": res["code"].cpu().numpy(),
+            "iso": res["iso"].cpu().numpy()}
     return QuadtreeCode(None, w, h, px.shape[1], px.shape[0], "local_search", False, columns=cols)

@@ -186,15 +186,20 @@ __global__ void fill_u64_kernel(unsigned long long *a, unsigned long long v, lon
         a[i] = v;
 }
 
-// ---- local search: CTA per 8x8 range; stride-1 2x2 sums of the candidate window in smem
-template <int R>
+// ---- local search: CTA per 8x8 range; stride-1 2x2 sums of the candidate window in smem.
+// NI isometries (1 = the reference, 8 = the extension): the range is stored once per isometry,
+// permuted (rt[t][src_t(e)] = r(e)), so candidate (c, t)'s cross term is sum_m q_c(m) rt[t][m]; a
+// thread keeps its candidate's 64 q values in registers across the isometries.  Winner = the
+// lexicographic minimum of (1024 n SSE, c * NI + t): the reference's first strict '<' over the
+// (dy, dx) order, then the lowest isometry.
+template <int R, int NI>
 __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, int W, int H, int radius,
-                                                           int32_t *out_dx, int32_t *out_dy, uint8_t *out_o,
-                                                           uint8_t *out_code) {
+                                                           int32_t *out_dx, int32_t *out_dy, int8_t *out_iso,
+                                                           uint8_t *out_o, uint8_t *out_code) {
     constexpr int WS = 16 + 2 * R;  // window side (pixels) covering every clamped candidate
     __shared__ uint16_t s2[WS][WS];
     __shared__ uint8_t pw[WS + 1][WS + 1];
-    __shared__ int rr[64];
+    __shared__ int rt[NI][64];
     __shared__ unsigned long long wbest[8];
     const int rpr = W / 8;
     const int ri = blockIdx.x;
@@ -208,7 +213,10 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
         const int i = k / ww, j = k % ww;
         pw[i][j] = img[(size_t)(lo_y + i) * W + lo_x + j];
     }
-    if (threadIdx.x < 64) rr[threadIdx.x] = img[(size_t)(ry + threadIdx.x / 8) * W + rx + threadIdx.x % 8];
+    for (int k = threadIdx.x; k < NI * 64; k += blockDim.x) {
+        const int t = k / 64, e = k % 64;
+        rt[t][iso_src(t, e / 8, e % 8, 8)] = img[(size_t)(ry + e / 8) * W + rx + e % 8];
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < (wh - 1) * (ww - 1); k += blockDim.x) {
         const int i = k / (ww - 1), j = k % (ww - 1);
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     __syncthreads();
     int sr = 0, srr = 0;
     for (int e = 0; e < 64; e++) {
-        sr += rr[e];
-        srr += rr[e] * rr[e];
+        sr += rt[0][e];
+        srr += rt[0][e] * rt[0][e];
     }
     const int o = (2 * sr + 64) / 128;
     const long long A = (long long)srr - 2ll * o * sr + 64ll * o * o;
@@ -227,20 +235,32 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     for (int c = threadIdx.x; c < side * side; c += blockDim.x) {
         const int dy = c / side - radius, dx = c % side - radius;
         const int cx = clampi(bx + dx, 0, W - 16) - lo_x, cy = clampi(by + dy, 0, H - 16) - lo_y;
-        int sq = 0, sqq = 0, sqr = 0;
+        constexpr int QN = NI == 1 ? 1 : 64;  // identity: one pass, no q registers
+        int q[QN];
+        int sq = 0, sqq = 0, sqr0 = 0;
         for (int i = 0; i < 8; i++)
 #pragma unroll
             for (int j = 0; j < 8; j++) {
-                const int q = s2[cy + 2 * i][cx + 2 * j];
-                sq += q;
-                sqq += q * q;
-                sqr += q * rr[8 * i + j];
+                const int v = s2[cy + 2 * i][cx + 2 * j];
+                if constexpr (NI == 1) sqr0 += v * rt[0][8 * i + j];
+                else q[8 * i + j] = v;
+                sq += v;
+                sqq += v * v;
             }
-        const long long N = 64ll * sqr - (long long)sq * sr, D = 64ll * sqq - (long long)sq * sq;
-        const long long k2 = 2 * quant_code(N, D) - 7;
-        const long long X = 65536ll * A - 64 * k2 * N + k2 * k2 * D;  // 1024 * n * SSE, n = 64
-        const unsigned long long key = make_key(X, c);
-        best = key < best ? key : best;
+        const long long D = 64ll * sqq - (long long)sq * sq;
+#pragma unroll 1
+        for (int t = 0; t < NI; t++) {
+            int sqr = sqr0;
+            if constexpr (NI > 1) {
+#pragma unroll
+                for (int e = 0; e < 64; e++) sqr += q[e] * rt[t][e];
+            }
+            const long long N = 64ll * sqr - (long long)sq * sr;
+            const long long k2 = 2 * quant_code(N, D) - 7;
+            const long long X = 65536ll * A - 64 * k2 * N + k2 * k2 * D;  // 1024 * n * SSE, n = 64
+            const unsigned long long key = make_key(X, (long long)c * NI + t);
+            best = key < best ? key : best;
+        }
     }
     for (int off = 16; off > 0; off >>= 1) {
         const unsigned long long other = __shfl_xor_sync(FULL, best, off);
@@ -251,7 +271,8 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); w++) best = wbest[w] < best ? wbest[w] : best;
         best = wbest[0] < best ? wbest[0] : best;
-        const int c = (int)(best & ((1ull << 21) - 1));
+        const int cand = (int)(best & ((1ull << 21) - 1));
+        const int c = cand / NI, t = cand % NI;
         const int dy = c / side - radius, dx = c % side - radius;
         const int cx = clampi(bx + dx, 0, W - 16), cy = clampi(by + dy, 0, H - 16);
         int sq = 0, sqq = 0, sqr = 0;
@@ -260,11 +281,12 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
                 const int q = s2[cy - lo_y + 2 * i][cx - lo_x + 2 * j];
                 sq += q;
                 sqq += q * q;
-                sqr += q * rr[8 * i + j];
+                sqr += q * rt[t][8 * i + j];
             }
         const long long N = 64ll * sqr - (long long)sq * sr, D = 64ll * sqq - (long long)sq * sq;
         out_dx[ri] = cx;
         out_dy[ri] = cy;
+        if (out_iso) out_iso[ri] = (int8_t)t;
         out_o[ri] = (uint8_t)o;
         out_code[ri] = (uint8_t)quant_code(N, D);
     }
@@ -364,17 +386,23 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     return 0;
 }
 
-int local_search(const uint8_t *img, int W, int H, int radius, int32_t *out_dx, int32_t *out_dy, uint8_t *out_o,
-                 uint8_t *out_code, cudaStream_t st) {
+int local_search(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx, int32_t *out_dy,
+                 int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, cudaStream_t st) {
     MNS_CHECK_ARG(W >= 16 && H >= 16 && W % 8 == 0 && H % 8 == 0, "local search needs at least a 16x16 image");
     MNS_CHECK_ARG(radius >= 0 && radius <= 32, "radius must be in [0, 32]");
+    MNS_CHECK_ARG(n_iso == 1 || n_iso == 8, "n_iso must be 1 or 8");
     const int nr = (W / 8) * (H / 8);
-    if (radius <= 4)
-        local_search_kernel<4><<<nr, 128, 0, st>>>(img, W, H, radius, out_dx, out_dy, out_o, out_code);
-    else if (radius <= 16)
-        local_search_kernel<16><<<nr, 256, 0, st>>>(img, W, H, radius, out_dx, out_dy, out_o, out_code);
-    else
-        local_search_kernel<32><<<nr, 256, 0, st>>>(img, W, H, radius, out_dx, out_dy, out_o, out_code);
+#define LS_LAUNCH(Rr, NI, T) local_search_kernel<Rr, NI><<<nr, T, 0, st>>>(img, W, H, radius, out_dx, out_dy, out_iso, out_o, out_code)
+    if (n_iso == 1) {
+        if (radius <= 4) LS_LAUNCH(4, 1, 128);
+        else if (radius <= 16) LS_LAUNCH(16, 1, 256);
+        else LS_LAUNCH(32, 1, 256);
+    } else {
+        if (radius <= 4) LS_LAUNCH(4, 8, 128);
+        else if (radius <= 16) LS_LAUNCH(16, 8, 256);
+        else LS_LAUNCH(32, 8, 256);
+    }
+#undef LS_LAUNCH
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -152,12 +152,15 @@ def test_c4_full_search_all_ranges_vs_oracle(mns, n_iso):
         assert bad.size == 0, (n_iso, k, bad[:5])
 
 
-@pytest.mark.parametrize("radius", [4, 32])
-def test_c4_local_search_all_ranges_vs_oracle(mns, radius):
+@pytest.mark.parametrize("radius,n_iso", [(4, 1), (32, 1), (4, 8), (32, 8)])
+def test_c4_local_search_all_ranges_vs_oracle(mns, radius, n_iso):
+    """All 4096 ranges; (32, 8) is config c4's +-32 x 8-isometry variant (1.38e8 pairs)."""
     from paper_1501_02894_b200.synth import config_image
 
     px = config_image("c4")
-    res = {k: v.cpu().numpy() for k, v in mns.local_search_device(torch.from_numpy(px).cuda(), radius).items()}
-    ref = O.local_search(px, radius)
+    res = {k: v.cpu().numpy() for k, v in
+           mns.local_search_device(torch.from_numpy(px).cuda(), radius, n_iso=n_iso).items()}
+    ref = O.local_search(px, radius, n_iso=n_iso)
     assert np.array_equal(res["dx"], ref["dom_x"]) and np.array_equal(res["dy"], ref["dom_y"])
+    assert np.array_equal(res["iso"], ref["iso"])
     assert np.array_equal(res["o"], ref["o"]) and np.array_equal(res["code"], ref["code"])
