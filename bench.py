@@ -465,7 +465,8 @@ def run_ours(args, img_np, rank, world, local_rank):
     if world > 1:
         def step_gather():
             step()
-            sharding.gather_codes(code.records, int(code.count.item()), code.root_offsets, rank, world)
+            code.join()
+            sharding.gather_codes(code.records, code.count, code.root_offsets, rank, world)
 
         for _ in range(2):
             step_gather()
@@ -538,6 +539,35 @@ def run_ours(args, img_np, rank, world, local_rank):
 
     small = None if args.no_small else small_configs(dev, rank, world)
 
+    # config c4 as SURVEY 8(e) shards it: ranges split across ranks (pool replicated, no data-path
+    # collective), then the all-gather of the 8-byte per-range results; max over ranks
+    c4_split = None
+    if not args.no_search:
+        from paper_1501_02894_b200.synth import config_image
+
+        c4 = torch.from_numpy(config_image("c4")).to(dev)
+        c4_split = {}
+        for n_iso in (1, 8):
+            fn = lambda a, b, n_iso=n_iso: mns.full_search_device(c4, 8, 1, n_iso, ranges=(a, b))  # noqa: E731
+            for _ in range(2):
+                sharding.search_sharded(fn, 4096, rank, world)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            reps = 5
+            for _ in range(reps):
+                sharding.search_sharded(fn, 4096, rank, world)
+            b.record()
+            barrier()
+            ms = a.elapsed_time(b) / reps
+            if world > 1:
+                m = torch.tensor([ms], device=dev)
+                dist.all_reduce(m, op=dist.ReduceOp.MAX)
+                ms = float(m.item())
+            pairs = 4096 * 497 * 497 * n_iso
+            c4_split[f"iso{n_iso}"] = {"ms": ms, "pair_evals_per_s": pairs / (ms / 1e3), "ranks": world,
+                                       "note": "ranges split across ranks + all_gather of (domain, isometry, o, code)"}
+
     # the benchmarked output, read back after timing for the parity check (one more untimed step)
     final = None
     if not args.no_parity:  # every rank steps (the decode exchanges halos); rank 0 checks its strip
@@ -581,7 +611,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                        "decode_ms": dec_ms, "decode_mpix_per_s": own_px / (dec_ms / 1e3) / 1e6,
                        "pass_ms": pass_ms, "pass_ms_each": pass_ms_each, "sweeps_per_pass": 2,
                        "sweep_ms_effective": pass_ms / 2,
-                       "leaves_rank0": n_leaves, "full_search": fs, "small_configs": small,
+                       "leaves_rank0": n_leaves, "full_search": fs, "c4_range_split": c4_split,
+                       "small_configs": small,
                        "with_code_gather": gather},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic(kname) if world == 1 else None,

@@ -113,11 +113,11 @@ def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world
     run_ops(unit_map_ops(umap, r0, r1, height, rank, world, group))
 
 
-def gather_codes(records, count: int, root_offsets, rank: int, world: int, dst: int = 0, group=None):
+def gather_codes(records, count, root_offsets, rank: int, world: int, dst: int = 0, group=None):
     """Concatenate per-rank codes on rank ``dst`` (the final code gather).
 
-    ``records[:count]`` (int64, mns_record.h) and ``root_offsets`` (int32, n_local_roots + 1,
-    strip-local) of each rank's contiguous share of roots (strip rows of one image, or images of a
+    ``records[:count]`` (int64, mns_record.h; ``count`` an int or the encoder's device count tensor)
+    and ``root_offsets`` (int32, n_local_roots + 1, strip-local) of each rank's contiguous share of roots (strip rows of one image, or images of a
     batch).  Returns (records, root_offsets) of the whole job on ``dst`` -- records in rank order,
     root offsets rebased -- and None on the other ranks.  Any torch.distributed backend.
     """
@@ -125,13 +125,19 @@ def gather_codes(records, count: int, root_offsets, rank: int, world: int, dst: 
     import torch.distributed as dist
 
     n_roots = root_offsets.numel() - 1
+    if torch.is_tensor(count):  # the encoder's device count: no separate host read
+        sizes = torch.cat([count.reshape(1).to(torch.int64),
+                           torch.full((1,), n_roots, dtype=torch.int64, device=count.device)])
+    else:
+        sizes = torch.tensor([count, n_roots], dtype=torch.int64, device=records.device)
     if world == 1:
-        return records[:count], root_offsets
-    sizes = torch.tensor([count, n_roots], dtype=torch.int64, device=records.device)
-    all_sizes = [torch.empty_like(sizes) for _ in range(world)]
-    dist.all_gather(all_sizes, sizes, group=group)
-    counts = [int(t[0]) for t in all_sizes]
-    roots = [int(t[1]) for t in all_sizes]
+        return records[: int(sizes[0])], root_offsets
+    all_sizes = torch.empty(2 * world, dtype=torch.int64, device=sizes.device)
+    dist.all_gather_into_tensor(all_sizes, sizes, group=group)
+    table = all_sizes.view(world, 2).tolist()  # the one host read: transfer sizes
+    counts = [int(t[0]) for t in table]
+    roots = [int(t[1]) for t in table]
+    count = counts[rank]
     if rank != dst:
         ops = [dist.P2POp(dist.isend, records[:count].contiguous(), dst, group),
                dist.P2POp(dist.isend, root_offsets[:n_roots].contiguous(), dst, group)]
@@ -199,6 +205,8 @@ class StripDecoder:
         own.copy_(code.unit_map.view(r1 - r0, rw32))
         code.unit_map = own.view(-1)
         self._ops = {}
+        self.overlap = True  # world > 1: boundary rows first, halo exchange beside the interior rows
+        self._comm = None
 
     def _vbase(self, t, row0: int, elem: int):
         return ctypes.c_void_p(t.data_ptr() - row0 * self.W * elem)
@@ -263,22 +271,59 @@ class StripDecoder:
             nxt = None if last else (self.ping if cur is not self.ping else self.pong)
             if sweep_events is not None:
                 sweep_events[n][0].record()
-            if self.lattice:
-                N.check(L.mns_decode_pass_lattice(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
-                                                  self._state_base(cur), float(initial_value), self._state_base(nxt),
-                                                  ob if last else ctypes.c_void_p(0), N.ptr(self.error), s))
+            if last or not self._overlap():
+                self._pass(L, cur, nxt, ob, last, initial_value, self.r0, self.r1, s)
+                if not last:
+                    self._exchange(nxt)
             else:
-                N.check(L.mns_decode_sweep2(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
-                                            self._state_base(cur), float(initial_value), self._state_base(nxt),
-                                            ob if last else ctypes.c_void_p(0), s))
+                # the rows the neighbours need first, their halo exchange on the side stream while the
+                # interior rows compute; the next pass waits for both
+                import torch
+
+                main = torch.cuda.current_stream() if stream is None else stream
+                b0, b1 = self._boundary()
+                for a, b in ((self.r0, b0), (b1, self.r1)):
+                    if a < b:
+                        self._pass(L, cur, nxt, ob, False, initial_value, a, b, s)
+                self._comm.wait_stream(main)
+                with torch.cuda.stream(self._comm):
+                    self._exchange(nxt)
+                if b0 < b1:
+                    self._pass(L, cur, nxt, ob, False, initial_value, b0, b1, s)
+                main.wait_stream(self._comm)
             if sweep_events is not None:
                 sweep_events[n][1].record()
             n += 1
             it += 2
             if not last:
-                self._exchange(nxt)
                 cur = nxt
         return out
+
+    def _overlap(self) -> bool:
+        """Split passes into boundary + interior (halo exchange overlapped) for strips of >= 6 root rows."""
+        if self.world == 1 or not self.overlap or self.r1 - self.r0 < 6:
+            return False
+        if self._comm is None:
+            import torch
+
+            self._comm = torch.cuda.Stream(device=self.code.records.device)
+        return True
+
+    def _boundary(self):
+        """Root rows [b0, b1) not sent to a neighbour: the 32 halo rows are the first / last two root rows."""
+        return self.r0 + (2 if self.rank > 0 else 0), self.r1 - (2 if self.rank < self.world - 1 else 0)
+
+    def _pass(self, L, cur, nxt, ob, last, initial_value, a, b, s):
+        from . import _native as N
+
+        if self.lattice:
+            N.check(L.mns_decode_pass_lattice(N.ptr(self.umap), self.u0, self.W, self.H, a, b, self._state_base(cur),
+                                              float(initial_value), self._state_base(nxt),
+                                              ob if last else ctypes.c_void_p(0), N.ptr(self.error), s))
+        else:
+            N.check(L.mns_decode_sweep2(N.ptr(self.umap), self.u0, self.W, self.H, a, b, self._state_base(cur),
+                                        float(initial_value), self._state_base(nxt),
+                                        ob if last else ctypes.c_void_p(0), s))
 
 
 class StripDecoderF64:
@@ -371,3 +416,41 @@ class StripDecoderF64:
             self._exchange(nxt)
             cur, nxt = nxt, cur
         return self.finalize(stream)
+
+
+def pack_search(res: dict):
+    """Per-range search result (dom int32, iso int8, o uint8, code uint8) -> one int64 per range."""
+    import torch
+
+    return (res["dom"].to(torch.int64) | (res["iso"].to(torch.int64) & 0xFF) << 32 |
+            res["o"].to(torch.int64) << 40 | res["code"].to(torch.int64) << 48)
+
+
+def unpack_search(packed) -> dict:
+    import torch
+
+    return {"dom": (packed & 0xFFFFFFFF).to(torch.int32), "iso": ((packed >> 32) & 0xFF).to(torch.int8),
+            "o": ((packed >> 40) & 0xFF).to(torch.uint8), "code": ((packed >> 48) & 0xFF).to(torch.uint8)}
+
+
+def search_sharded(search_fn, n_ranges: int, rank: int, world: int, group=None):
+    """Full / local search with the ranges split across ranks: this rank runs
+    ``search_fn(r0, r1)`` on its contiguous share [r0, r1) (image and domain pool replicated, no
+    data-path collective) and the per-range results (8 B each: domain, isometry, offset, contrast)
+    are all-gathered, so every rank ends with the whole image's result in range order.  Shares are
+    near-equal (split), so the gather pads to the largest share."""
+    import torch
+    import torch.distributed as dist
+
+    r0, r1 = split(n_ranges, world, rank)
+    mine = pack_search(search_fn(r0, r1))
+    if world == 1:
+        return unpack_search(mine)
+    width = -(-n_ranges // world)
+    buf = torch.zeros(width, dtype=torch.int64, device=mine.device)
+    buf[: r1 - r0] = mine
+    allb = torch.empty(world * width, dtype=torch.int64, device=mine.device)
+    dist.all_gather_into_tensor(allb, buf, group=group)
+    parts = [allb[r * width: r * width + (split(n_ranges, world, r)[1] - split(n_ranges, world, r)[0])]
+             for r in range(world)]
+    return unpack_search(torch.cat(parts))

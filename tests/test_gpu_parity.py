@@ -838,3 +838,24 @@ def test_f64_strip_decoder_three_strips_on_one_gpu(mns):
     got = np.concatenate([d.finalize().cpu().numpy() for d in decs])
     assert all(int(d.iters_done.item()) == sweeps for d in decs)
     assert np.array_equal(got, want)
+
+
+def test_strip_decoder_split_passes_equal_whole(mns, monkeypatch):
+    """The overlapped multi-GPU schedule (boundary root rows first, interior rows after, each a
+    sub-range launch of the same pass) composes to the single-launch decode: a whole-image strip run
+    as rank 0 of 2 with the exchange stubbed out (there is no neighbour below the last row)."""
+    from paper_1501_02894_b200 import sharding
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(512, 23, noise_sigma=10.0, n_blobs=8)
+    H = W = 512
+    outs = []
+    for world, lattice in ((1, True), (2, True), (1, False), (2, False)):
+        code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+        dec = sharding.StripDecoder(code, H, W, 0, H // 16, 0, world, lattice=lattice)
+        monkeypatch.setattr(dec, "_exchange", lambda t: None)
+        monkeypatch.setattr(sharding, "unit_map_ops", lambda *a, **k: [])
+        assert dec._overlap() == (world == 2)
+        outs.append(dec.run(10, 128.0).clone())
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[2], outs[3]) and torch.equal(outs[0], outs[2])

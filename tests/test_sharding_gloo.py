@@ -332,3 +332,61 @@ def test_f64_strip_decode_early_stop_matches_whole_image(world, stop, tmp_path):
         done, swept = np.load(tmp_path / f"iters{r}.npy")
         assert done == sweeps and swept == sweeps
     assert stop == 0.0 or sweeps < 12  # the stop actually triggered
+
+
+def _search_worker(rank, world, px, kind, out_dir):
+    """Config c4's range split: every rank searches its share of the ranges (the oracle stands in
+    for the GPU search on CPU) and search_sharded all-gathers the packed per-range results."""
+    from oracle import oracle as O
+
+    B = 8
+    n_ranges = (px.shape[0] // B) * (px.shape[1] // B)
+
+    def search_fn(r0, r1):
+        if kind == "full":
+            res = O.full_search(px, B, 1, n_iso=8, range_ids=np.arange(r0, r1), nthreads=1)
+            return {k: torch.from_numpy(np.ascontiguousarray(res[k])) for k in ("dom", "iso", "o", "code")}
+        res = O.local_search(px, 4, nthreads=1, n_iso=8)
+        ndx = px.shape[1] - 16 + 1
+        dom = (res["dom_y"] * ndx + res["dom_x"]).astype(np.int32)
+        return {"dom": torch.from_numpy(dom[r0:r1]), "iso": torch.from_numpy(res["iso"][r0:r1]),
+                "o": torch.from_numpy(res["o"][r0:r1]), "code": torch.from_numpy(res["code"][r0:r1])}
+
+    got = sharding.search_sharded(search_fn, n_ranges, rank, world)
+    np.save(os.path.join(out_dir, f"search{rank}.npy"),
+            np.stack([got[k].numpy().astype(np.int64) for k in ("dom", "iso", "o", "code")]))
+
+
+@pytest.mark.parametrize("world,kind", [(2, "full"), (3, "full"), (3, "local")])
+def test_search_range_split_gloo(world, kind, tmp_path):
+    from oracle import oracle as O
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = synth_image(64, 17, noise_sigma=8.0, n_blobs=3)
+    _run(world, _search_worker, px, kind, str(tmp_path))
+    if kind == "full":
+        ref = O.full_search(px, 8, 1, n_iso=8)
+        want = np.stack([ref[k].astype(np.int64) for k in ("dom", "iso", "o", "code")])
+    else:
+        ref = O.local_search(px, 4, n_iso=8)
+        want = np.stack([(ref["dom_y"] * 49 + ref["dom_x"]).astype(np.int64), ref["iso"].astype(np.int64),
+                         ref["o"].astype(np.int64), ref["code"].astype(np.int64)])
+    for r in range(world):  # every rank holds the whole result
+        assert np.array_equal(np.load(tmp_path / f"search{r}.npy"), want)
+
+
+def _gather_tensor_count_worker(rank, world, out_dir):  # noqa: ARG001
+    counts = [7, 3, 0][:world]
+    rec = torch.arange(100 * rank, 100 * rank + counts[rank] + 5, dtype=torch.int64)
+    offs = torch.tensor([0, counts[rank]], dtype=torch.int32)
+    got = sharding.gather_codes(rec, torch.tensor([counts[rank]], dtype=torch.int64), offs, rank, world)
+    if rank == 0:
+        out, o = got
+        want = np.concatenate([np.arange(100 * r, 100 * r + counts[r]) for r in range(world)])
+        assert np.array_equal(out.numpy(), want)
+        assert o.numpy().tolist()[-1] == sum(counts)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_codes_device_count_gloo(world, tmp_path):
+    _run(world, _gather_tensor_count_worker, str(tmp_path))
