@@ -114,3 +114,30 @@ def test_mse_psnr_match_float64_mean(cuda):
     assert mns.psnr(a, a) == math.inf
     with pytest.raises(ValueError, match="image dimensions differ"):
         mns.mse(np.zeros((4, 4), np.uint8), np.zeros((4, 5), np.uint8))
+
+
+def test_csv_writers_byte_identical_to_reference():
+    """rd_csv / histogram_csv against the reference's own writers (baseline/_ref, when installed)."""
+    import math
+    import os
+    import sys
+
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "mnscodec")):
+        pytest.skip("reference not installed (tools/install_reference.py)")
+    sys.path.insert(0, ref_dir)
+    try:
+        import mnscodec.bench as RB
+    finally:
+        sys.path.remove(ref_dir)
+    rng = np.random.default_rng(4)
+    pts = [rd.RdPoint(mode=m, thresholds=(float(a), float(b), math.inf if i % 3 == 0 else 2.5), technique2=bool(i % 2),
+                      bits=int(rng.integers(0, 10**7)), bpp=float(rng.random()), psnr=math.inf if i == 4 else 30 + rng.random(),
+                      encode_seconds=float(rng.random()), leaf_counts=tuple(int(v) for v in rng.integers(0, 999, 4)),
+                      phase2_count=int(rng.integers(0, 99)))
+           for i, (m, a, b) in enumerate([("mns", 4, 8), ("no_search", 0.5, 12), ("mns", 1e-3, 7.25)] * 3)]
+    assert rd.rd_csv(pts) == RB.rd_csv(pts)
+    samples = [tuple(int(v) for v in rng.integers(-9, 10, 2)) for _ in range(500)]
+    mine, theirs = rd.offset_histogram(samples), RB.offset_histogram(samples)
+    assert rd.histogram_csv(mine) == RB.histogram_csv(theirs)
+    assert (mine.mode_x(), mine.mode_y()) == (theirs.mode_x(), theirs.mode_y())
