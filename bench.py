@@ -298,6 +298,23 @@ def small_configs(dev, rank, world):
             us = a.elapsed_time(b) * 1e3 / reps
             out[name] = {"config": desc, "latency_us": us, "blocks_per_s": W * H / 64 / (us * 1e-6),
                          "graph_replays": reps}
+    if rank == 0:  # c2 with the 8-isometry extension (BASELINE configs[1]): encode + exact fp64 decode
+        px = config_image("c2")
+        img = torch.from_numpy(px).to(dev)
+        for _ in range(3):
+            c = mns.encode_device(img, cfg, n_iso=8)
+            mns.decode_device(c, iters=10, stop_delta=0.0)
+        torch.cuda.synchronize()
+        reps, a, b = 20, ev(), ev()
+        a.record()
+        for _ in range(reps):
+            c = mns.encode_device(img, cfg, n_iso=8)
+            mns.decode_device(c, iters=10, stop_delta=0.0)
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / reps
+        out["c2_iso8"] = {"config": "512^2, 16->8->4 quadtree, 8 isometries (extension), 10 exact fp64 decode sweeps",
+                          "latency_us": us, "blocks_per_s": 4096 / (us * 1e-6), "note": "not graph-captured"}
     # c3: batched encode, images split across ranks
     i0, i1 = sharding.split(256, world, rank)
     seeds = batch_seeds()[i0:i1]

@@ -41,6 +41,8 @@ typedef struct {
     double mean_tol;  /* phase-2 gate */
     int32_t mns;      /* 1: mode "mns"; 0: mode "no_search" */
     int32_t root_level;
+    int32_t n_iso;    /* 1 (0): the reference; 8: phase 1 also tries the 8 isometries of the co-centred
+                         domain (extension, BASELINE configs[1]; records carry the isometry, MNS_REC_ISO_SHIFT) */
 } mns_enc_cfg;
 
 /* Replaces: encoder.encode_quadtree (encoder.py:215-246) for n_images images of
@@ -168,7 +170,8 @@ int mns_decode_unit_map_lattice(const uint32_t *unit_map, int32_t width, int32_t
                                 void *workspace, int64_t workspace_bytes, void *stream);
 
 /* Generic painted units (decoder.py:32-34 _paint): destination square (x, y, size),
- * domain origin (dx, dy) of the 2*size domain, map (s, o).  Used for search-
+ * domain origin (dx, dy) of the 2*size domain, map (s, o).  usize = side | isometry << 8: the
+ * isometry extension paints d_t(i, j) = d(src_t(i, j)) (0 = identity, the reference).  Used for search-
  * baseline codes whose domains are explicit (BaselinePayload) and for arbitrary
  * leaf orders.  Units are SoA arrays of length n_units. */
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

@@ -25,6 +25,8 @@
 #define MNS_REC_PHASE2_SHIFT 32
 #define MNS_REC_O_SHIFT 33
 #define MNS_REC_PAYLOAD_SHIFT 41
+/* extension: the isometry (0..7, 0 = identity) of a phase-1 leaf's domain (n_iso = 8 encodes) */
+#define MNS_REC_ISO_SHIFT 44
 
 #ifdef __CUDACC__
 #define MNS_REC_INLINE __host__ __device__ static inline

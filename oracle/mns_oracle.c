@@ -141,26 +141,41 @@ typedef struct {
     double mean_tol;  /* encoder.py:59 */
     int mns;          /* mode == "mns" (1) or "no_search" (0) */
     int root_level;   /* 1 = reference driver; 2 = "8->4" extension: roots forced to split once */
+    int n_iso;        /* 0 / 1 = the reference; 8 = extension: phase 1 also tries the 8 isometries */
 } orc_enc_cfg;
 
 static const double CONTRAST_SETS[4][2] = {{0, 0}, {0.2, 0.5}, {0.4, 0.65}, {0.5, 0.9}}; /* encoder.py:36 */
 static const int DELTA_LIMIT[4] = {0, 15, 31, 31};                                   /* encoder.py:39-44 */
 
-/* encoder.py:145-166 try_phase1 */
+static inline int iso_src(int t, int i, int j, int B);
+
+/* encoder.py:145-166 try_phase1.  Isometry extension (cfg->n_iso = 8): the same fit on each
+ * d_t(i, j) = d(src_t(i, j)), the first smallest rms wins (strict '<' over t), t goes in the record. */
 static int try_phase1(const uint8_t *img, int W, int H, int x, int y, int size, int level, const orc_enc_cfg *cfg,
                       uint64_t *rec, double *rms_out) {
-    double d[256], r[256], o;
-    int dx, dy, n = size * size;
+    double d[256], dt[256], r[256], o;
+    int dx, dy, n = size * size, n_iso = cfg->n_iso > 1 ? cfg->n_iso : 1;
     co_domain(x, y, size, W, H, &dx, &dy);
     downsample_u8(img, W, dx, dy, size, d);
     block_u8(img, W, x, y, size, r);
-    double s = fit_affine_s(r, d, n, &o);
-    int code = quantize_contrast(s);
-    int ob = round_to_int(o);
-    double rms = rms_error(r, d, n, dequantize_contrast(code), (double)ob);
-    if (rms_out) *rms_out = rms;
-    if (level == 4 || rms <= cfg->e[level - 1]) {
-        *rec = mns_rec_phase1(x, y, level, ob, code);
+    double best = INFINITY;
+    int bcode = 0, bob = 0, bt = 0;
+    for (int t = 0; t < n_iso; t++) {
+        for (int k = 0; k < n; k++) dt[k] = t ? d[iso_src(t, k / size, k % size, size)] : d[k];
+        double s = fit_affine_s(r, dt, n, &o);
+        int code = quantize_contrast(s);
+        int ob = round_to_int(o);
+        double rms = rms_error(r, dt, n, dequantize_contrast(code), (double)ob);
+        if (rms < best || t == 0) {
+            best = rms;
+            bcode = code;
+            bob = ob;
+            bt = t;
+        }
+    }
+    if (rms_out) *rms_out = best;
+    if (level == 4 || best <= cfg->e[level - 1]) {
+        *rec = mns_rec_phase1(x, y, level, bob, bcode) | ((uint64_t)bt << MNS_REC_ISO_SHIFT);
         return 1;
     }
     return 0;
@@ -327,8 +342,8 @@ EXPORT int64_t orc_records_to_units(const uint64_t *rec, int64_t n, int W, int H
         int size = 32 >> level;
         int ob = (int)((r >> MNS_REC_O_SHIFT) & 0xFF);
         if (!((r >> MNS_REC_PHASE2_SHIFT) & 1)) {
-            int code = (int)((r >> MNS_REC_PAYLOAD_SHIFT) & 7);
-            orc_unit v = {x, y, size, 0, 0, dequantize_contrast(code), (double)ob};
+            int code = (int)((r >> MNS_REC_PAYLOAD_SHIFT) & 7), iso = (int)((r >> MNS_REC_ISO_SHIFT) & 7);
+            orc_unit v = {x, y, size | (iso << 8), 0, 0, dequantize_contrast(code), (double)ob};  /* side | iso << 8 */
             co_domain(x, y, size, W, H, &v.dx, &v.dy);
             u[k++] = v;
         } else {
@@ -353,13 +368,15 @@ EXPORT int64_t orc_records_to_units(const uint64_t *rec, int64_t n, int W, int H
 
 /* decoder.py:32-34 _paint + transform.py:63-66 apply_map */
 static void paint(double *out, const double *cur, int W, const orc_unit *u) {
-    double d[256];
-    int n = u->size * u->size;
-    downsample_f64(cur, W, u->dx, u->dy, u->size, d);
+    double d0[256], d[256];
+    int size = u->size & 255, iso = u->size >> 8, n = size * size; /* size = side | isometry << 8 */
+    downsample_f64(cur, W, u->dx, u->dy, size, d0);
+    /* isometry extension: the transformed domain d_t(i, j) = d(src_t(i, j)), then apply_map on it */
+    for (int k = 0; k < n; k++) d[k] = iso ? d0[iso_src(iso, k / size, k % size, size)] : d0[k];
     double dm = pw_sum(d, n) / n;
-    for (int i = 0; i < u->size; i++)
-        for (int j = 0; j < u->size; j++) {
-            double v = u->s * (d[i * u->size + j] - dm) + u->o;
+    for (int i = 0; i < size; i++)
+        for (int j = 0; j < size; j++) {
+            double v = u->s * (d[i * size + j] - dm) + u->o;
             v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
             out[(size_t)(u->y + i) * W + (u->x + j)] = v;
         }

@@ -33,6 +33,7 @@ class EncCfg(ctypes.Structure):
         ("mean_tol", ctypes.c_double),
         ("mns", ctypes.c_int),
         ("root_level", ctypes.c_int),
+        ("n_iso", ctypes.c_int),
     ]
 
 
@@ -98,8 +99,9 @@ def pad(pixels: np.ndarray, m: int) -> np.ndarray:
     return np.ascontiguousarray(np.pad(pixels, ((0, nh - h), (0, nw - w)), mode="edge"), dtype=np.uint8)
 
 
-def _cfg(e, mean_tol, mns, root_level) -> EncCfg:
+def _cfg(e, mean_tol, mns, root_level, n_iso=1) -> EncCfg:
     c = EncCfg()
+    c.n_iso = int(n_iso)
     for i in range(3):
         c.e[i] = float(e[i])
     c.mean_tol = float(mean_tol)
@@ -109,7 +111,7 @@ def _cfg(e, mean_tol, mns, root_level) -> EncCfg:
 
 
 def encode_quadtree_records(pixels: np.ndarray, e=(8.0, 8.0, 8.0), mean_tol=16.0, mns=True, root_level=1,
-                            nthreads=None):
+                            nthreads=None, n_iso=1):
     """Packed leaf records (include/mns_record.h) of the reference quadtree encode of the
     16-padded image, plus per-root leaf counts."""
     img = pad(np.asarray(pixels, dtype=np.uint8), 16)
@@ -118,7 +120,7 @@ def encode_quadtree_records(pixels: np.ndarray, e=(8.0, 8.0, 8.0), mean_tol=16.0
     cap = nroots * 64
     out = np.empty(cap, dtype=np.uint64)
     counts = np.empty(nroots, dtype=np.int32)
-    cfg = _cfg(e, mean_tol, mns, root_level)
+    cfg = _cfg(e, mean_tol, mns, root_level, n_iso)
     n = lib().orc_encode_quadtree(_ptr(img), w, h, ctypes.byref(cfg), _ptr(out), cap, _ptr(counts),
                                   nthreads or default_threads())
     if n < 0:

@@ -30,7 +30,7 @@ class NativeError(RuntimeError):
 
 class EncCfg(ctypes.Structure):
     _fields_ = [("e", ctypes.c_double * 3), ("mean_tol", ctypes.c_double), ("mns", ctypes.c_int32),
-                ("root_level", ctypes.c_int32)]
+                ("root_level", ctypes.c_int32), ("n_iso", ctypes.c_int32)]
 
 
 def sources() -> list[str]:

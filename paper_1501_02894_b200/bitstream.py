@@ -141,6 +141,14 @@ def _check_header(code) -> None:
         raise ValueError("dimensions exceed the 16-bit header fields")
 
 
+def has_isometries(records) -> bool:
+    """True for records of the n_iso = 8 extension: a phase-1 leaf with a non-identity isometry
+    (bits 44..46, mns_record.h MNS_REC_ISO_SHIFT; phase-2 records use those bits for deltas)."""
+    r = np.asarray(records, dtype=np.uint64)
+    p1 = ((r >> np.uint64(32)) & np.uint64(1)) == 0
+    return bool((((r >> np.uint64(44)) & np.uint64(7)) != 0)[p1].any())
+
+
 def write_stream(code) -> bytes:
     """bitstream.py:203-205 on the GPU packer."""
     from . import codec
@@ -151,6 +159,8 @@ def write_stream(code) -> bytes:
     _check_header(code)
     if code._records is None:  # user-built leaf list: validate like the reference before packing
         _validate_tiling(code.leaves, code.padded_w, code.padded_h, code.mode)
+    elif code.mode in ("no_search", "mns") and has_isometries(code.records):
+        raise ValueError("isometry codes (the n_iso=8 extension) have no .mns representation (SPEC.md:16)")
     import torch
 
     rec = torch.from_numpy(np.ascontiguousarray(code.records).view(np.int64)).to(codec._device())

@@ -111,6 +111,7 @@ class DeviceCode:
     unit_map_valid: bool = False  # unit_map holds this code's map (emitted by the encoder / build_unit_map)
     compact_event: "object" = None  # set by encode_device(compact_stream=...): records/count valid after it
     decode_error: "object" = None   # set by decode_device on the lattice path (device int32 flag)
+    n_iso: int = 1                  # 8: the isometry extension (phase-1 records carry an isometry)
 
     def join(self, stream=None) -> None:
         """Make `stream` (default: current) wait until records / root_offsets / count are complete
@@ -143,8 +144,9 @@ class _Workspace:
 _WS = _Workspace()
 
 
-def enc_cfg(config: EncoderConfig, root_level: int = 1) -> N.EncCfg:
+def enc_cfg(config: EncoderConfig, root_level: int = 1, n_iso: int = 1) -> N.EncCfg:
     c = N.EncCfg()
+    c.n_iso = int(n_iso)
     c.e[0], c.e[1], c.e[2] = float(config.e1), float(config.e2), float(config.e3)
     c.mean_tol = float(config.mean_tol)
     c.mns = 1 if config.mode == "mns" else 0
@@ -154,12 +156,16 @@ def enc_cfg(config: EncoderConfig, root_level: int = 1) -> N.EncCfg:
 
 def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows: Optional[tuple] = None,
                   height: Optional[int] = None, out: Optional[DeviceCode] = None, with_unit_map: bool = True,
-                  stream=None, compact_stream=None) -> DeviceCode:
+                  stream=None, compact_stream=None, n_iso: int = 1) -> DeviceCode:
     """MNS quadtree encode of a padded uint8 CUDA tensor [H, W] or a batch [B, H, W].
 
     root_rows=(r0, r1) restricts the work to root rows [r0, r1) (strip sharding); then ``img``
     may be a halo'd slice and ``height`` gives the full image height (global clamping).
+    n_iso=8 is the isometry extension (BASELINE configs[1]): phase 1 also tries the 8 isometries of
+    the co-centred domain; such codes carry no decoder unit map and decode on the exact unit path.
     """
+    if n_iso not in (1, 8):
+        raise ValueError("n_iso must be 1 or 8")
     torch = _torch()
     L = N.lib()
     if config.mode not in ("no_search", "mns"):
@@ -186,8 +192,9 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     # e3 = inf: every visited level-3 node passes phase 1 (encoder.py:160-165, before phase 2), so no
     # leaf is 2x2 and no level-3 phase-2 leaf has 2x2 quadrants
     out.min_leaf = 4 if math.isinf(config.e3) else 0
-    out.unit_map_valid = out.unit_map is not None
-    cfg = enc_cfg(config, root_level)
+    out.unit_map_valid = out.unit_map is not None and n_iso == 1
+    out.n_iso = n_iso
+    cfg = enc_cfg(config, root_level, n_iso)
     if compact_stream is None:
         N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
                                       ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
@@ -249,8 +256,9 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
                    torch.empty((H, W), dtype=torch.float32, device=dev))
     if out is None and want_u8:
         out = torch.empty((H, W), dtype=torch.uint8, device=dev)
-    if stop_delta > 0.0 and want_u8:
-        # the reference's early stop (decoder.py:70-75) decided exactly: bit-exact fp64 sweeps
+    if (stop_delta > 0.0 or code.n_iso > 1) and want_u8:
+        # the reference's early stop (decoder.py:70-75) decided exactly: bit-exact fp64 sweeps (also the
+        # isometry extension's codes, which the unit-map decoders cannot express)
         code.decode_error = None
         return decode_device_f64(code, iters, stop_delta, initial_value, out=out, stream=stream) + (None,)
     wsb = N.out_i64(L, L.mns_decode_workspace_bytes, W, H)
@@ -435,13 +443,14 @@ def _to_device_u8(px: np.ndarray):
     return torch.from_numpy(px).to(_device(), non_blocking=False)
 
 
-def encode_quadtree(image, config: EncoderConfig, *, root_level: int = 1) -> QuadtreeCode:
-    """encoder.py:215-246.  root_level=2 is the '8->4' extension (every root split once)."""
+def encode_quadtree(image, config: EncoderConfig, *, root_level: int = 1, n_iso: int = 1) -> QuadtreeCode:
+    """encoder.py:215-246.  root_level=2 is the '8->4' extension (every root split once); n_iso=8 the
+    isometry extension (records carry each phase-1 leaf's isometry; see encode_device)."""
     if config.mode not in ("no_search", "mns"):
         raise ValueError(f"encode_quadtree handles no_search/mns, not {config.mode!r}")
     px = _pixels(image)
     padded = _padded_np(px, ROOT_SIZE)
-    code = encode_device(_to_device_u8(padded), config, root_level=root_level)
+    code = encode_device(_to_device_u8(padded), config, root_level=root_level, n_iso=n_iso)
     n = code.n_records()
     rec = code.records[:n].cpu().numpy().view(np.uint64)
     offs = code.root_offsets.cpu().numpy()
@@ -541,7 +550,8 @@ def _quadtree_units(code) -> dict:
     xs, ys, ss, ss_, os_ = [], [], [], [], []
     size = np.array([LEVEL_SIZES[int(v)] for v in range(1, 5)])[f["level"] - 1]
     p1 = ~f["phase2"]
-    xs.append(f["x"][p1]); ys.append(f["y"][p1]); ss.append(size[p1])
+    iso = ((np.asarray(code.records, dtype=np.uint64) >> np.uint64(44)) & np.uint64(7)).astype(np.int64)
+    xs.append(f["x"][p1]); ys.append(f["y"][p1]); ss.append(size[p1] | (iso[p1] << 8))  # side | isometry << 8
     ss_.append(-0.875 + 0.25 * f["s_code"][p1]); os_.append(f["o"][p1].astype(np.float64))
     p2 = f["phase2"]
     if p2.any():
@@ -555,8 +565,9 @@ def _quadtree_units(code) -> dict:
     x = np.concatenate(xs).astype(np.int32)
     y = np.concatenate(ys).astype(np.int32)
     sz = np.concatenate(ss).astype(np.int32)
-    dx = np.clip(x - sz // 2, 0, W - 2 * sz).astype(np.int32)
-    dy = np.clip(y - sz // 2, 0, H - 2 * sz).astype(np.int32)
+    side = sz & 255
+    dx = np.clip(x - side // 2, 0, W - 2 * side).astype(np.int32)
+    dy = np.clip(y - side // 2, 0, H - 2 * side).astype(np.int32)
     return {"x": x, "y": y, "size": sz, "dx": dx, "dy": dy, "s": np.concatenate(ss_), "o": np.concatenate(os_)}
 
 
@@ -578,7 +589,11 @@ def decode(code, config: Optional[DecodeConfig] = None) -> GrayImage:
     W, H = code.padded_w, code.padded_h
     if cfg.max_iters < 1:
         raise ValueError("max_iters must be >= 1")
-    if cfg.stop_delta > 0.0:
+    from .bitstream import has_isometries
+
+    iso = code.mode in ("no_search", "mns") and isinstance(code, QuadtreeCode) and code.has_records and \
+        has_isometries(code.records)
+    if cfg.stop_delta > 0.0 or iso:  # exact fp64 path (the isometry extension always decodes here)
         if code.mode in ("no_search", "mns"):
             u = _quadtree_units(code if isinstance(code, QuadtreeCode) else _wrap_reference(code))
         else:

@@ -909,7 +909,9 @@ __global__ void __launch_bounds__(256) decode_units_kernel(const UnitParams p) {
     float lmax = 0.f;
     const long long warps = (long long)gridDim.x * (blockDim.x / 32);
     for (long long u = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); u < p.n; u += warps) {
-        const int size = p.usize[u], x = p.ux[u], y = p.uy[u], dx = p.udx[u], dy = p.udy[u];
+        // usize = side | isometry << 8 (extension: d_t(i, j) = d(src_t(i, j)); the mean is order-free here)
+        const int size = p.usize[u] & 255, iso = p.usize[u] >> 8, x = p.ux[u], y = p.uy[u], dx = p.udx[u],
+                  dy = p.udy[u];
         const float s = p.us[u], o = p.uo[u];
         const int n = size * size;
         float acc = 0.f;
@@ -922,8 +924,8 @@ __global__ void __launch_bounds__(256) decode_units_kernel(const UnitParams p) {
         for (int o2 = 16; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(FULL, acc, o2);
         const float mean = acc * 0.25f / (float)n;
         for (int k = lane; k < n; k += 32) {
-            const int i = k / size, j = k % size;
-            const float *pp = p.cur + (size_t)(dy + 2 * i) * p.W + dx + 2 * j;
+            const int i = k / size, j = k % size, m = iso ? iso_src(iso, i, j, size) : k;
+            const float *pp = p.cur + (size_t)(dy + 2 * (m / size)) * p.W + dx + 2 * (m % size);
             const float q = ((pp[0] + pp[1]) + pp[p.W]) + pp[p.W + 1];
             const float v = fminf(255.f, fmaxf(0.f, fmaf(s, q * 0.25f - mean, o)));
             const size_t idx = (size_t)(y + i) * p.W + x + j;
@@ -958,11 +960,12 @@ __global__ void decode_step_f64_kernel(const int32_t *ux, const int32_t *uy, con
                                        long long n, int W, const double *cur, double *out) {
     const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (u >= n) return;
-    const int size = usize[u], m = size * size;
+    const int size = usize[u] & 255, iso = usize[u] >> 8, m = size * size;  // side | isometry << 8
     double d[256];
     for (int i = 0; i < size; i++)
-        for (int j = 0; j < size; j++) {
-            const double *pp = cur + (size_t)(udy[u] + 2 * i) * W + udx[u] + 2 * j;
+        for (int j = 0; j < size; j++) {  // d_t(i, j) = d(src_t(i, j)), stored in output order
+            const int k = iso ? iso_src(iso, i, j, size) : i * size + j;
+            const double *pp = cur + (size_t)(udy[u] + 2 * (k / size)) * W + udx[u] + 2 * (k % size);
             d[i * size + j] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), pp[W]), pp[W + 1]), 0.25);
         }
     const double dm = __ddiv_rn(pw_sum_dev(d, m), (double)m);

@@ -30,13 +30,14 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // One unit of decode_step (decoder.py:32-63, transform.py:63-66) in the reference's fp64 order.
 // Returns this unit's max |v - cur| over its pixels.
-__device__ double paint_unit_f64(int x, int y, int size, int dx, int dy, double s, double o, int W,
+__device__ double paint_unit_f64(int x, int y, int size, int iso, int dx, int dy, double s, double o, int W,
                                  const double *cur, double *out) {
     const int m = size * size;
     double d[256];
     for (int i = 0; i < size; i++)
-        for (int j = 0; j < size; j++) {
-            const double *pp = cur + (size_t)(dy + 2 * i) * W + dx + 2 * j;
+        for (int j = 0; j < size; j++) {  // isometry extension: d_t(i, j) = d(src_t(i, j)), in output order
+            const int k = iso ? iso_src(iso, i, j, size) : i * size + j;
+            const double *pp = cur + (size_t)(dy + 2 * (k / size)) * W + dx + 2 * (k % size);
             d[i * size + j] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), pp[W]), pp[W + 1]), 0.25);
         }
     const double dm = __ddiv_rn(pw_sum_dev(d, m), (double)m);
@@ -59,8 +60,9 @@ __global__ void __launch_bounds__(256) sweep_f64_kernel(const int32_t *ux, const
     if (state[0]) return;  // converged in an earlier sweep
     const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     double dmax = 0.0;
-    if (u < n && usize[u] > 0)
-        dmax = paint_unit_f64(ux[u], uy[u], usize[u], udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+    if (u < n && (usize[u] & 255) > 0)  // usize = side | isometry << 8
+        dmax = paint_unit_f64(ux[u], uy[u], usize[u] & 255, usize[u] >> 8, udx[u], udy[u], us[u], uo[u], W, cur,
+                              nxt);
     long long bits = __double_as_longlong(dmax);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
@@ -116,7 +118,7 @@ __global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W,
             usize[t] = 0;
             return;
         }
-        sz = size;
+        sz = size | (int)(((r >> MNS_REC_ISO_SHIFT) & 7) << 8);  // side | isometry << 8
         px = x;
         py = y;
         s = -0.875 + 0.25 * (double)((r >> 41) & 7);
@@ -141,8 +143,9 @@ __global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W,
     ux[t] = px;
     uy[t] = py;
     usize[t] = sz;
-    udx[t] = clampi(px - sz / 2, 0, W - 2 * sz);  // co_domain_rect (image.py:174-187)
-    udy[t] = clampi(py - sz / 2, 0, H - 2 * sz);
+    const int side = sz & 255;
+    udx[t] = clampi(px - side / 2, 0, W - 2 * side);  // co_domain_rect (image.py:174-187)
+    udy[t] = clampi(py - side / 2, 0, H - 2 * side);
     us[t] = s;
     uo[t] = o;
 }

@@ -780,6 +780,140 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
     }
 }
 
+// ---------------------------------------------------------------- isometry extension
+//
+// n_iso = 8 (BASELINE configs[1], not in the reference: SPEC.md:16): phase 1 of every node also tries
+// the 8 isometries d_t(i, j) = d(src_t(i, j)) of its co-centred domain (mns_common.cuh iso_src, as in
+// the full search) and keeps the one with the smallest exact quantised SSE (ties: the lowest t); the
+// record carries t (MNS_REC_ISO_SHIFT).  Phase 2 and the traversal are the reference's.  One warp per
+// root walks the quadtree depth first with an explicit stack; every node's moments (and the
+// isometries' cross terms) are warp reductions over its pixels, the decisions run on every lane
+// (phase 2 through phase2_node, emulation included), records go straight into the root's staged
+// slots (the same compaction follows).
+constexpr int IWIN = 48;  // a root's window: [x0 - 16, x0 + 32) x [y0 - 16, y0 + 32)
+constexpr int IWARPS = 4;
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// Identity moments of node (x, y, size) against its co-centred domain, warp-wide (every lane gets them)
+__device__ Mom warp_moments(const Win &w, int x, int y, int size) {
+    const int lane = threadIdx.x & 31, n = size * size;
+    int v[5] = {0, 0, 0, 0, 0};
+    for (int e = lane; e < n; e += 32) {
+        const int px = x + e % size, py = y + e / size;
+        const int r = w.px(px, py), q = dom_q(w, x, y, size, px, py);
+        v[0] += r;
+        v[1] += r * r;
+        v[2] += q;
+        v[3] += q * q;
+        v[4] += q * r;
+    }
+    return Mom{warp_sum(v[0]), warp_sum(v[1]), warp_sum(v[2]), warp_sum(v[3]), warp_sum(v[4])};
+}
+
+// Phase 1 with the isometry search; returns acceptance (level 4 always) and the record.
+__device__ bool phase1_iso(const Win &w, const EncParams &p, int x, int y, int level, int n_iso, uint64_t &rec) {
+    const int lane = threadIdx.x & 31, size = 32 >> level, n = size * size, nlog2 = 2 * (5 - level);
+    int m5[5] = {0, 0, 0, 0, 0}, sqr_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int e = lane; e < n; e += 32) {
+        const int i = e / size, j = e % size;
+        const int r = w.px(x + j, y + i), q = dom_q(w, x, y, size, x + j, y + i);
+        m5[0] += r;
+        m5[1] += r * r;
+        m5[2] += q;
+        m5[3] += q * q;
+        for (int t = 0; t < n_iso; t++) {  // d_t(i, j) = d(src_t(i, j))
+            const int m = t ? iso_src(t, i, j, size) : e;
+            sqr_t[t] += r * (t ? dom_q(w, x, y, size, x + m % size, y + m / size) : q);
+        }
+    }
+    const int sr = warp_sum(m5[0]), srr = warp_sum(m5[1]), sq = warp_sum(m5[2]), sqq = warp_sum(m5[3]);
+    const int o = (2 * sr + n) >> (nlog2 + 1);  // round_to_int(mean)
+    const long long D = ((long long)sqq << nlog2) - (long long)sq * sq;
+    const long long A = (long long)srr - 2ll * o * sr + ((long long)o * o << nlog2);  // sum (r - o)^2
+    long long best = LLONG_MAX;
+    int bt = 0, bcode = 4;
+    for (int t = 0; t < n_iso; t++) {
+        const int sqr = warp_sum(sqr_t[t]);
+        const long long N = ((long long)sqr << nlog2) - (long long)sq * sr;
+        const int code = quant_code(16.0 * (double)N, (double)D);
+        const long long k2 = 2 * code - 7;
+        const long long X = (A << (nlog2 + 10)) - 64 * k2 * N + k2 * k2 * D;  // 1024 n SSE, exact
+        if (X < best) {
+            best = X;
+            bt = t;
+            bcode = code;
+        }
+    }
+    rec = mns_rec_phase1(x, y, level, o, bcode) | ((uint64_t)bt << MNS_REC_ISO_SHIFT);
+    return level == 4 || (double)best <= p.p1b[level];
+}
+
+__global__ void __launch_bounds__(IWARPS * 32) mns_encode_iso_kernel(const uint8_t *img, int64_t pitch,
+                                                                    int64_t image_stride, int y_res0, int y_res1,
+                                                                    const EncParams p, int n_iso) {
+    __shared__ uint8_t pix[IWARPS][IWIN][IWIN];
+    __shared__ uint16_t qe[IWARPS][IWIN / 2][IWIN / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long root = (long long)blockIdx.x * IWARPS + warp;
+    if (root >= p.n_roots) return;  // whole warps
+    const int rx = (int)(root % p.rw);
+    const long long t = root / p.rw;
+    const int ry = p.rr0 + (int)(t % p.rows), img_i = (int)(t / p.rows);
+    const int x0 = 16 * rx, y0 = 16 * ry;
+    const uint8_t *base = img + (ptrdiff_t)img_i * image_stride;
+    for (int e = lane; e < IWIN * IWIN; e += 32) {  // rows outside the resident strip are never read
+        const int r = e / IWIN, c = e % IWIN, gy = y0 - 16 + r, gx = x0 - 16 + c;
+        pix[warp][r][c] = (gy >= y_res0 && gy < y_res1 && gx >= 0 && gx < p.W) ? base[(ptrdiff_t)gy * pitch + gx] : 0;
+    }
+    __syncwarp();
+    for (int e = lane; e < (IWIN / 2) * (IWIN / 2); e += 32) {
+        const int r = e / (IWIN / 2), c = e % (IWIN / 2);
+        qe[warp][r][c] = (uint16_t)(pix[warp][2 * r][2 * c] + pix[warp][2 * r][2 * c + 1] + pix[warp][2 * r + 1][2 * c] +
+                                    pix[warp][2 * r + 1][2 * c + 1]);
+    }
+    __syncwarp();
+    const Win w{&pix[warp][0][0], &qe[warp][0][0], IWIN, IWIN / 2, -1, -1, y0 - 16, (y0 - 16) / 2, x0 - 16, p.W,
+                p.H};
+    uint64_t *st = p.stage + root * 64;
+    int cnt = 0;
+    // depth-first stack of (x, y, level) packed as x | y << 8 | level << 16 (root-relative x, y)
+    int stack[16], sp = 0;
+    if (p.root_level == 1) {
+        stack[sp++] = 1 << 16;
+    } else {
+        for (int c = 3; c >= 0; c--) stack[sp++] = (8 * (c & 1)) | ((8 * (c >> 1)) << 8) | (2 << 16);
+    }
+    while (sp) {
+        const int e = stack[--sp];
+        const int level = e >> 16, x = x0 + (e & 255), y = y0 + ((e >> 8) & 255), size = 32 >> level;
+        uint64_t rec = 0;
+        bool acc = false;
+        if (2 * size <= p.min_dim) {  // encoder.py:231
+            acc = phase1_iso(w, p, x, y, level, n_iso, rec);
+            if (!acc && p.mns && level <= 3) {
+                const int h = size / 2;
+                Mom kids[4];
+                for (int c = 0; c < 4; c++) kids[c] = warp_moments(w, x + (c & 1) * h, y + (c >> 1) * h, h);
+                const int sr = kids[0].sr + kids[1].sr + kids[2].sr + kids[3].sr;
+                acc = phase2_node(w, p, level, x, y, size, sr, kids, &rec);
+            }
+        }
+        if (acc) {
+            if (lane == 0) st[cnt] = rec;
+            cnt++;
+        } else {
+            const int h = size / 2, lx = e & 255, ly = (e >> 8) & 255;
+            for (int c = 3; c >= 0; c--) stack[sp++] = (lx + (c & 1) * h) | ((ly + (c >> 1) * h) << 8) | ((level + 1) << 16);
+        }
+    }
+    if (lane == 0) p.root_cnt[root] = cnt;
+}
+
 // Compaction (second half of the encode): exclusive scan of the per-root counts into
 // root_offsets (in place) with a decoupled look-back over uniform 2048-root tiles, then a
 // coalesced copy of every root's staged records to its offset.  Keeping the scan out of the
@@ -906,6 +1040,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     MNS_CHECK_ARG(n_images >= 1 && (n_images == 1 || (image_stride % 16 == 0)), "bad image stride");
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
     MNS_CHECK_ARG(cfg && (cfg->root_level == 1 || cfg->root_level == 2), "root_level must be 1 or 2");
+    MNS_CHECK_ARG(cfg->n_iso == 0 || cfg->n_iso == 1 || cfg->n_iso == 8, "n_iso must be 1 or 8");
     const int rw = W / 16;
     const long long n_roots = (long long)n_images * (rr1 - rr0) * rw;
     MNS_CHECK_ARG(capacity >= 64 * n_roots, "record capacity must be >= 64 * roots");
@@ -976,7 +1111,12 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     chunks = (p.rows + p.chunk_rows - 1) / p.chunk_rows;
     MNS_CHECK_ARG(n_images <= 65535 && chunks <= 65535, "grid too large");
     const dim3 grid((unsigned)p.tiles_per_row, (unsigned)chunks, (unsigned)n_images);
-    mns_encode_kernel<<<grid, ET, ENC_SMEM, stream>>>(tmap, p);
+    if (cfg->n_iso > 1) {  // the isometry extension (no unit map: those codes decode on the unit path)
+        mns_encode_iso_kernel<<<(unsigned)((n_roots + IWARPS - 1) / IWARPS), IWARPS * 32, 0, stream>>>(
+            img, pitch, n_images > 1 ? image_stride : 0, p.y_res0, y_res1, p, cfg->n_iso);
+    } else {
+        mns_encode_kernel<<<grid, ET, ENC_SMEM, stream>>>(tmap, p);
+    }
     MNS_CUDA_TRY(cudaGetLastError());
     if (cstream != stream) {  // the compaction on its own stream, after the encoder
         cudaEvent_t ev;

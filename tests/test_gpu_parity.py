@@ -859,3 +859,34 @@ def test_strip_decoder_split_passes_equal_whole(mns, monkeypatch):
         outs.append(dec.run(10, 128.0).clone())
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[2], outs[3]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("name,e,mode,root_level", [("c2", (8.0, 8.0, math.inf), "mns", 1),
+                                                    ("tex", (6.0, 6.0, 6.0), "mns", 1),
+                                                    ("tex", (6.0, 6.0, 5.0), "no_search", 1),
+                                                    ("tex", (6.0, 6.0, math.inf), "mns", 2)])
+def test_isometry_extension_encode_decode_vs_oracle(mns, name, e, mode, root_level):
+    """BASELINE configs[1]'s 8-isometry MNS encode (an extension: the reference has no isometries):
+    records (with each phase-1 leaf's isometry) bit-exact vs the oracle restatement; the decode (exact
+    fp64 unit path) bit-identical to the oracle's with and without the early stop."""
+    from paper_1501_02894_b200.synth import config_image, synth_image
+
+    px = config_image("c2") if name == "c2" else synth_image(256, 33, noise_sigma=12.0, n_blobs=6)
+    cfg = mns.EncoderConfig(e1=e[0], e2=e[1], e3=e[2], mode=mode)
+    code = mns.encode_quadtree(mns.GrayImage(px), cfg, root_level=root_level, n_iso=8)
+    ref, _ = O.encode_quadtree_records(px, e, 16.0, mode == "mns", root_level, n_iso=8)
+    assert np.array_equal(code.records, ref)
+    from paper_1501_02894_b200.bitstream import has_isometries
+
+    assert has_isometries(ref)  # the isometries are actually used
+    units = O.records_to_units(ref, px.shape[1], px.shape[0])
+    for stop in (0.0, 0.5):
+        want, _, _ = O.decode_units(units, px.shape[1], px.shape[0], max_iters=10, stop_delta=stop)
+        got = mns.decode(code, mns.DecodeConfig(max_iters=10, stop_delta=stop)).pixels
+        assert np.array_equal(got, want), stop
+    dcode = mns.encode_device(torch.from_numpy(px).cuda(), cfg, root_level=root_level, n_iso=8)
+    out, _, _ = mns.decode_device(dcode, iters=10, stop_delta=0.0)
+    want, _, _ = O.decode_units(units, px.shape[1], px.shape[0], max_iters=10, stop_delta=0.0)
+    assert np.array_equal(out.cpu().numpy(), want)
+    with pytest.raises(ValueError, match="isometry"):
+        mns.write_stream(code)
