@@ -442,10 +442,15 @@ def run_ours(args, img_np, rank, world, local_rank):
             enc_done[i].record(stream)
             dec.run(ITERS, 128.0, out=out2[b])
             stream.wait_stream(s_cmp)
+            # the transform code as the reference serialises it (.mns, bitstream.py:130-205), packed on
+            # the GPU; its size is fixed for this image (deterministic encode), measured in the warm-up
+            packed, _ = mns.write_stream_device(code.records, n_rec, W, H, W, H, True, True)
+            keep[b] = packed
             comp[i].record(stream)
-            with torch.cuda.stream(s_out):  # D2H of step i
+            with torch.cuda.stream(s_out):  # D2H of step i: the decoded image and the code
                 s_out.wait_event(comp[i])
                 out_host2[b].copy_(out2[b], non_blocking=True)
+                mns_host2[b].copy_(packed[:n_mns], non_blocking=True)
                 d2h[i].record(s_out)
         stream.wait_event(d2h[k - 1])
         t1.record(stream)
@@ -459,6 +464,12 @@ def run_ours(args, img_np, rank, world, local_rank):
 
     for _ in range(args.warmup):
         step()
+    stream.wait_stream(s_cmp)
+    n_rec = code.n_records()
+    _, bits_t = mns.write_stream_device(code.records, n_rec, W, H, W, H, True, True)
+    n_mns = (int(bits_t.item()) + 7) // 8  # .mns bytes of this strip's code
+    mns_host2 = [torch.empty(n_mns, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    keep = [None, None]
     timed_e2e(2)
     barrier()
     with ClockSampler(local_rank) as clk:
@@ -645,7 +656,10 @@ def run_ours(args, img_np, rank, world, local_rank):
                           "sample": f"c5 rows 0..{args.cpu_baseline_rows - 1} encoded + {ITERS}-sweep decoded as its own "
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
         "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": int(host.numel()) * world,
-                "d2h_bytes_per_step": int(out_host.numel()) * world},
+                "d2h_bytes_per_step": (int(out_host.numel()) + n_mns) * world,
+                "note": "per step: image H2D (pinned), encode, the code packed to .mns on the GPU and copied "
+                        "back, decode, decoded image D2H; copies of neighbouring steps overlap on two copy "
+                        "streams (double-buffered)"},
         "parity": parity,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

@@ -151,6 +151,8 @@ int stream_workspace_bytes(int64_t n, int64_t *bytes) {
     return 0;
 }
 
+__global__ void set_bits_kernel(long long *bits, long long v) { *bits = v; }
+
 int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int ph, int mns, int t2, uint8_t *out,
                  int64_t cap, int64_t *d_bits, void *ws, int64_t ws_bytes, cudaStream_t st) {
     MNS_CHECK_ARG(pw % 16 == 0 && ph % 16 == 0, "padded dimensions must be multiples of 16");
@@ -179,10 +181,8 @@ int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int
     if (n > 0) {
         MNS_CUDA_TRY(cudaMemsetAsync(status, 0, tiles * 8, st));
         width_scan_kernel<<<(unsigned)tiles, SCAN_T, 0, st>>>(records, n, mns, t2, offsets, status, (long long *)d_bits);
-    } else {
-        const long long hbits = HEADER_BITS;
-        MNS_CUDA_TRY(cudaMemcpyAsync(d_bits, &hbits, 8, cudaMemcpyHostToDevice, st));
-        MNS_CUDA_TRY(cudaStreamSynchronize(st));
+    } else {  // an empty code: the header alone (stream-ordered, no host round trip)
+        set_bits_kernel<<<1, 1, 0, st>>>((long long *)d_bits, HEADER_BITS);
     }
     scatter_kernel<<<(unsigned)((max_words + 255) / 256), 256, 0, st>>>(records, offsets, n, mns, t2, (const long long *)d_bits, h[0],
                                                                         h[1], h[2], h[3], out, max_words);
