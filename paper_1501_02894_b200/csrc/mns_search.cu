@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     __shared__ uint16_t s2[WS][WS];
     __shared__ uint8_t pw[WS + 1][WS + 1];
     __shared__ int rt[NI][64];
+    __shared__ uint32_t rtp[NI][16];  // rt packed 4 bytes per word (DP2A operands)
     __shared__ unsigned long long wbest[8];
     const int rpr = W / 8;
     const int ri = blockIdx.x;
@@ -222,6 +223,11 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
         const int i = k / (ww - 1), j = k % (ww - 1);
         s2[i][j] = (uint16_t)(pw[i][j] + pw[i][j + 1] + pw[i + 1][j] + pw[i + 1][j + 1]);
     }
+    for (int k = threadIdx.x; k < NI * 16; k += blockDim.x) {
+        const int t = k / 16, w4 = 4 * (k % 16);
+        rtp[t][k % 16] = (uint32_t)rt[t][w4] | ((uint32_t)rt[t][w4 + 1] << 8) | ((uint32_t)rt[t][w4 + 2] << 16) |
+                         ((uint32_t)rt[t][w4 + 3] << 24);
+    }
     __syncthreads();
     int sr = 0, srr = 0;
     for (int e = 0; e < 64; e++) {
@@ -235,26 +241,29 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     for (int c = threadIdx.x; c < side * side; c += blockDim.x) {
         const int dy = c / side - radius, dx = c % side - radius;
         const int cx = clampi(bx + dx, 0, W - 16) - lo_x, cy = clampi(by + dy, 0, H - 16) - lo_y;
-        constexpr int QN = NI == 1 ? 1 : 64;  // identity: one pass, no q registers
-        int q[QN];
-        int sq = 0, sqq = 0, sqr0 = 0;
+        // the candidate's 64 q as 32 u16 pairs (DP2A: two q x r products per instruction)
+        uint32_t qp[32];
+        int sq = 0, sqq = 0;
+#pragma unroll
         for (int i = 0; i < 8; i++)
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const int v = s2[cy + 2 * i][cx + 2 * j];
-                if constexpr (NI == 1) sqr0 += v * rt[0][8 * i + j];
-                else q[8 * i + j] = v;
-                sq += v;
-                sqq += v * v;
+            for (int j = 0; j < 8; j += 2) {
+                const uint32_t a = s2[cy + 2 * i][cx + 2 * j], b = s2[cy + 2 * i][cx + 2 * j + 2];
+                qp[(8 * i + j) / 2] = __byte_perm(a, b, 0x5410);
+                sq += (int)(a + b);
+                sqq += (int)(a * a + b * b);
             }
         const long long D = 64ll * sqq - (long long)sq * sq;
 #pragma unroll 1
         for (int t = 0; t < NI; t++) {
-            int sqr = sqr0;
-            if constexpr (NI > 1) {
+            unsigned acc = 0;
 #pragma unroll
-                for (int e = 0; e < 64; e++) sqr += q[e] * rt[t][e];
+            for (int w4 = 0; w4 < 16; w4++) {
+                const uint32_t rw4 = rtp[t][w4];
+                acc = __dp2a_lo(qp[2 * w4], rw4, acc);
+                acc = __dp2a_hi(qp[2 * w4 + 1], rw4, acc);
             }
+            const int sqr = (int)acc;
             const long long N = 64ll * sqr - (long long)sq * sr;
             const long long k2 = 2 * quant_code(N, D) - 7;
             const long long X = 65536ll * A - 64 * k2 * N + k2 * k2 * D;  // 1024 * n * SSE, n = 64
