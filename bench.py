@@ -547,7 +547,7 @@ def run_ours(args, img_np, rank, world, local_rank):
                                  "effective_tflops": tf, "tensor_peak_tflops": tpk, "tensor_peak_source": tsrc,
                                  "frac_of_tensor_peak": tf / tpk}
         for radius, n_iso in ((4, 1), (32, 1), (32, 8)):  # encoder.py:312-347 local search (+-4 identity =
-            # the reference; +-32 x 8 isometries is the config-c4 extension)
+            # the reference, CUDA cores; +-32 x 8 isometries is the config-c4 extension, windowed tcgen05 GEMM)
             for _ in range(2):
                 mns.local_search_device(c4, radius, n_iso=n_iso)
             torch.cuda.synchronize()

@@ -238,6 +238,16 @@ int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t 
                      int32_t *out_dx, int32_t *out_dy, int8_t *out_iso, uint8_t *out_o, uint8_t *out_code,
                      void *stream);
 
+/* The same local search as a windowed GEMM on the tcgen05 full-search pipeline: only the (range
+ * tile, domain tile) pairs that meet some window are multiplied, elements outside a row's window are
+ * masked, and the winners are decided by the same exact keys (bit-identical to mns_local_search).
+ * Workspace: mns_local_search_workspace_bytes.  MNS_LOCAL_CUDA_CORES=1 in the environment routes to
+ * the CUDA-core kernel (A/B checks). */
+int mns_local_search_workspace_bytes(int32_t width, int32_t height, int32_t radius, int32_t n_iso, int64_t *bytes);
+int mns_local_search_tc(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t n_iso,
+                        int32_t *out_dx, int32_t *out_dy, int8_t *out_iso, uint8_t *out_o, uint8_t *out_code,
+                        void *workspace, int64_t workspace_bytes, void *stream);
+
 /* Packed .mns bitstream (bitstream.py:130-205) of a record array: per-leaf
  * widths, exclusive scan, MSB-first scatter.  out must hold
  * 4*ceil((104 + 33n)/32) bytes; *d_bits receives the exact bit count

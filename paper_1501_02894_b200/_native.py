@@ -74,6 +74,8 @@ def _declare(L):
         "mns_search_workspace_bytes": [I32, I32, I32, I32, I32, P],
         "mns_full_search": [P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, I64, P],
         "mns_local_search": [P, I32, I32, I32, I32, P, P, P, P, P, P],
+        "mns_local_search_workspace_bytes": [I32, I32, I32, I32, P],
+        "mns_local_search_tc": [P, I32, I32, I32, I32, P, P, P, P, P, P, I64, P],
         "mns_stream_workspace_bytes": [I64, P],
         "mns_write_stream": [P, I64, I32, I32, I32, I32, I32, I32, P, I64, P, P, I64, P],
         "mns_read_stream_workspace_bytes": [I64, P],
@@ -97,7 +99,7 @@ EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_encode_quad
            "mns_decode_flat_lattice", "mns_decode_quadtree_lattice", "mns_decode_unit_map_lattice", "mns_decode_units", "mns_decode_step_f64",
            "mns_decode_f64", "mns_records_to_units", "mns_decode_f64_sweep", "mns_decode_f64_decide",
            "mns_decode_f64_finalize", "mns_search_workspace_bytes", "mns_full_search",
-           "mns_local_search", "mns_stream_workspace_bytes", "mns_write_stream", "mns_read_stream_workspace_bytes", "mns_read_stream",
+           "mns_local_search", "mns_local_search_workspace_bytes", "mns_local_search_tc", "mns_stream_workspace_bytes", "mns_write_stream", "mns_read_stream_workspace_bytes", "mns_read_stream",
            "mns_image_sse", "mns_code_stats", "mns_offset_histogram",
            "mns_last_error",
            "mns_version")

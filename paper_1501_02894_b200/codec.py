@@ -373,9 +373,13 @@ def full_search_device(img, B: int, step: int = 1, n_iso: int = 1, ranges: Optio
     return out
 
 
-def local_search_device(img, radius: int = 4, stream=None, n_iso: int = 1):
+def local_search_device(img, radius: int = 4, stream=None, n_iso: int = 1, tensor_cores=None):
     """Local search (encoder.py:312-347; radius 4 / n_iso 1 = the reference) over an 8-padded uint8 CUDA
-    image; per-range (dx, dy, iso, o, code) tensors."""
+    image; per-range (dx, dy, iso, o, code) tensors.  tensor_cores: the windowed tcgen05 GEMM
+    (mns_local_search_tc) or the CUDA-core kernel (mns_local_search), bit-identical; None picks the
+    faster one measured on B200 (tcgen05 for wide windows with isometries, +-16 and up x 8)."""
+    if tensor_cores is None:
+        tensor_cores = n_iso == 8 and radius >= 16
     torch = _torch()
     L = N.lib()
     h, w = img.shape
@@ -384,8 +388,15 @@ def local_search_device(img, radius: int = 4, stream=None, n_iso: int = 1):
     out = {k: torch.empty(nr, dtype=dt, device=dev) for k, dt in
            (("dx", torch.int32), ("dy", torch.int32), ("iso", torch.int8), ("o", torch.uint8),
             ("code", torch.uint8))}
-    N.check(L.mns_local_search(N.ptr(img), w, h, int(radius), int(n_iso), N.ptr(out["dx"]), N.ptr(out["dy"]),
-                               N.ptr(out["iso"]), N.ptr(out["o"]), N.ptr(out["code"]), N.stream_ptr(stream)))
+    if tensor_cores:  # the windowed tcgen05 GEMM (mns_local_search_tc)
+        wsb = N.out_i64(L, L.mns_local_search_workspace_bytes, w, h, int(radius), int(n_iso))
+        ws = _WS.get("local", wsb, dev)
+        N.check(L.mns_local_search_tc(N.ptr(img), w, h, int(radius), int(n_iso), N.ptr(out["dx"]), N.ptr(out["dy"]),
+                                      N.ptr(out["iso"]), N.ptr(out["o"]), N.ptr(out["code"]), N.ptr(ws), ws.numel(),
+                                      N.stream_ptr(stream)))
+    else:  # the CUDA-core kernel
+        N.check(L.mns_local_search(N.ptr(img), w, h, int(radius), int(n_iso), N.ptr(out["dx"]), N.ptr(out["dy"]),
+                                   N.ptr(out["iso"]), N.ptr(out["o"]), N.ptr(out["code"]), N.stream_ptr(stream)))
     return out
 
 

@@ -143,6 +143,9 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
                 int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st);
 int local_search(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx, int32_t *out_dy,
                  int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, cudaStream_t st);
+int local_search_workspace_bytes(int W, int H, int radius, int n_iso, int64_t *bytes);
+int local_search_ws(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx, int32_t *out_dy,
+                    int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st);
 int stream_workspace_bytes(int64_t n, int64_t *bytes);
 int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int ph, int mns, int t2, uint8_t *out,
                  int64_t cap, int64_t *d_bits, void *ws, int64_t ws_bytes, cudaStream_t st);
@@ -357,6 +360,17 @@ int mns_local_search(const uint8_t *img, int32_t width, int32_t height, int32_t 
                      void *stream) {
     GUARD(mns::local_search(img, width, height, radius, n_iso, out_dx, out_dy, out_iso, out_o, out_code,
                             (cudaStream_t)stream));
+}
+
+int mns_local_search_workspace_bytes(int32_t width, int32_t height, int32_t radius, int32_t n_iso, int64_t *bytes) {
+    GUARD(mns::local_search_workspace_bytes(width, height, radius, n_iso, bytes));
+}
+
+int mns_local_search_tc(const uint8_t *img, int32_t width, int32_t height, int32_t radius, int32_t n_iso,
+                        int32_t *out_dx, int32_t *out_dy, int8_t *out_iso, uint8_t *out_o, uint8_t *out_code,
+                        void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::local_search_ws(img, width, height, radius, n_iso, out_dx, out_dy, out_iso, out_o, out_code, workspace,
+                               workspace_bytes, (cudaStream_t)stream));
 }
 
 int mns_stream_workspace_bytes(int64_t n_records, int64_t *bytes) {

@@ -192,10 +192,15 @@ __global__ void fill_u64_kernel(unsigned long long *a, unsigned long long v, lon
 // thread keeps its candidate's 64 q values in registers across the isometries.  Winner = the
 // lexicographic minimum of (1024 n SSE, c * NI + t): the reference's first strict '<' over the
 // (dy, dx) order, then the lowest isometry.
-template <int R, int NI>
+// SEED: score only the candidates on a stride-`sstride` grid of offsets and fold the winner into
+// the tensor-core path's keys (val = k2^2 D - 64 k2 N, candidate = domain * NI + t) -- a valid
+// seed, every scored candidate being a real one.
+template <int R, int NI, bool SEED = false>
 __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, int W, int H, int radius,
                                                            int32_t *out_dx, int32_t *out_dy, int8_t *out_iso,
-                                                           uint8_t *out_o, uint8_t *out_code) {
+                                                           uint8_t *out_o, uint8_t *out_code,
+                                                           unsigned long long *seed_best = nullptr,
+                                                           int sstride = 1) {
     constexpr int WS = 16 + 2 * R;  // window side (pixels) covering every clamped candidate
     __shared__ uint16_t s2[WS][WS];
     __shared__ uint8_t pw[WS + 1][WS + 1];
@@ -237,9 +242,11 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     const int o = (2 * sr + 64) / 128;
     const long long A = (long long)srr - 2ll * o * sr + 64ll * o * o;
     const int side = 2 * radius + 1;
+    const int sside = SEED ? 2 * (radius / sstride) + 1 : side;  // scored grid
     unsigned long long best = ~0ull;
-    for (int c = threadIdx.x; c < side * side; c += blockDim.x) {
-        const int dy = c / side - radius, dx = c % side - radius;
+    for (int c = threadIdx.x; c < sside * sside; c += blockDim.x) {
+        const int dy = SEED ? (c / sside - radius / sstride) * sstride : c / side - radius;
+        const int dx = SEED ? (c % sside - radius / sstride) * sstride : c % side - radius;
         const int cx = clampi(bx + dx, 0, W - 16) - lo_x, cy = clampi(by + dy, 0, H - 16) - lo_y;
         // the candidate's 64 q as 32 u16 pairs (DP2A: two q x r products per instruction)
         uint32_t qp[32];
@@ -267,7 +274,10 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
             const long long N = 64ll * sqr - (long long)sq * sr;
             const long long k2 = 2 * quant_code(N, D) - 7;
             const long long X = 65536ll * A - 64 * k2 * N + k2 * k2 * D;  // 1024 * n * SSE, n = 64
-            const unsigned long long key = make_key(X, (long long)c * NI + t);
+            const unsigned long long key =
+                SEED ? make_key_cb(X - 65536ll * A, ((long long)(cy + lo_y) * (W - 15) + cx + lo_x) * NI + t,
+                                   key_cand_bits(64))
+                     : make_key(X, (long long)c * NI + t);
             best = key < best ? key : best;
         }
     }
@@ -277,6 +287,13 @@ __global__ void __launch_bounds__(256) local_search_kernel(const uint8_t *img, i
     }
     if ((threadIdx.x & 31) == 0) wbest[threadIdx.x >> 5] = best;
     __syncthreads();
+    if (SEED) {
+        if (threadIdx.x == 0) {
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) best = wbest[w] < best ? wbest[w] : best;
+            atomicMin(&seed_best[ri], best);
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); w++) best = wbest[w] < best ? wbest[w] : best;
         best = wbest[0] < best ? wbest[0] : best;
@@ -333,6 +350,10 @@ int search_workspace_bytes(int W, int H, int B, int step, int n_iso, int64_t *by
     if (B <= 8) *bytes += align256(search_tc_workspace_bytes(W, H, B, step, n_iso));
     return 0;
 }
+
+int64_t local_search_tc_workspace_bytes(int W, int H, int B, int R, int n_iso);
+int local_search_tc(const uint8_t *img, int W, int H, int R, int n_iso, uint16_t *pool, int32_t *psq, long long *pD,
+                    long long ndom, unsigned long long *best, void *tc_ws, cudaStream_t st);
 
 int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso, int r0, int r1,
                    uint16_t *pool, int32_t *psq, long long *pD, long long ndom,
@@ -391,6 +412,73 @@ int full_search(const uint8_t *img, int W, int H, int B, int step, int n_iso, in
     }
     search_finalize_kernel<<<(r1 - r0 + 7) / 8, 256, 0, st>>>(img, W, B, n_iso, r0, r1, w.best, w.pool, w.psq, w.pD,
                                                              out_dom, out_iso, out_o, out_code);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int local_search(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx, int32_t *out_dy,
+                 int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, cudaStream_t st);
+
+// winner domain index -> origin (stride 1): dx = d % ndx, dy = d / ndx (in place: out_dx held the index)
+__global__ void dom_to_xy_kernel(int32_t *out_dx, int32_t *out_dy, int n, int ndx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int d = out_dx[i];
+    out_dx[i] = d % ndx;
+    out_dy[i] = d / ndx;
+}
+
+int local_search_workspace_bytes(int W, int H, int radius, int n_iso, int64_t *bytes) {
+    int64_t base;
+    search_workspace_bytes(W, H, 8, 1, n_iso, &base);
+    *bytes = base + align256(local_search_tc_workspace_bytes(W, H, 8, radius, n_iso));
+    return 0;
+}
+
+// Local search through the tensor-core pipeline (windowed full search), exact like the CUDA-core
+// kernel (same keys, same finalisation); MNS_LOCAL_CUDA_CORES=1 selects the CUDA-core kernel.
+int local_search_ws(const uint8_t *img, int W, int H, int radius, int n_iso, int32_t *out_dx, int32_t *out_dy,
+                    int8_t *out_iso, uint8_t *out_o, uint8_t *out_code, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    MNS_CHECK_ARG(W >= 16 && H >= 16 && W % 8 == 0 && H % 8 == 0, "local search needs at least a 16x16 image");
+    MNS_CHECK_ARG(radius >= 0 && radius <= 32, "radius must be in [0, 32]");
+    MNS_CHECK_ARG(n_iso == 1 || n_iso == 8, "n_iso must be 1 or 8");
+    const char *e = getenv("MNS_LOCAL_CUDA_CORES");
+    if (e && e[0] == '1') return local_search(img, W, H, radius, n_iso, out_dx, out_dy, out_iso, out_o, out_code, st);
+    int64_t need;
+    local_search_workspace_bytes(W, H, radius, n_iso, &need);
+    MNS_CHECK_ARG(ws_bytes >= need, "workspace too small");
+    const int B = 8;
+    const long long ndx = W - 2 * B + 1, ndy = H - 2 * B + 1, ndom = ndx * ndy, n = 64;
+    const long long nranges = (long long)(W / B) * (H / B);
+    MNS_CHECK_ARG(ndom * n_iso < (1ll << key_cand_bits(64)), "domain pool too large for the argmin key");
+    char *p = (char *)ws;
+    SearchWs w;
+    w.pool = (uint16_t *)p;
+    p += align256(ndom * n * 2);
+    w.psq = (int32_t *)p;
+    p += align256(ndom * 4);
+    w.pD = (long long *)p;
+    p += align256(ndom * 8);
+    w.best = (unsigned long long *)p;
+    p += align256(nranges * 8);
+    int64_t fs_base;
+    search_workspace_bytes(W, H, B, 1, n_iso, &fs_base);
+    void *tc_ws = (char *)ws + fs_base;
+    fill_u64_kernel<<<64, 256, 0, st>>>(w.best, ~0ull, nranges);
+    if (false) {  // (measured slower: the tensor-core pass is not bound by its rare path) seeds from a grid
+        const int nr = (int)nranges;
+        if (n_iso == 1)
+            local_search_kernel<32, 1, true><<<nr, 256, 0, st>>>(img, W, H, radius, nullptr, nullptr, nullptr, nullptr,
+                                                                  nullptr, w.best, 4);
+        else
+            local_search_kernel<32, 8, true><<<nr, 256, 0, st>>>(img, W, H, radius, nullptr, nullptr, nullptr, nullptr,
+                                                                  nullptr, w.best, 4);
+    }
+    if (int rc = local_search_tc(img, W, H, radius, n_iso, w.pool, w.psq, w.pD, ndom, w.best, tc_ws, st)) return rc;
+    search_finalize_kernel<<<(unsigned)((nranges + 7) / 8), 256, 0, st>>>(img, W, B, n_iso, 0, (int)nranges, w.best,
+                                                                          w.pool, w.psq, w.pD, out_dx, out_iso,
+                                                                          out_o, out_code);
+    dom_to_xy_kernel<<<(unsigned)((nranges + 255) / 256), 256, 0, st>>>(out_dx, out_dy, (int)nranges, (int)ndx);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }

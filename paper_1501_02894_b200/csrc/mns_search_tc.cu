@@ -92,8 +92,14 @@ struct TcParams {
     const int32_t *row_sr;       // [n_rows_pad] Sr of the row's range
     const int32_t *row_flat;     // [n_rows_pad] 1 if the range is constant (N == 0 for every domain)
     const float *row_err;        // [n_rows_pad] e_row
-    const unsigned long long *flat_key;  // argmin-D key for constant ranges
+    const unsigned long long *flat_key;  // argmin-D key for constant ranges (full search)
     unsigned long long *best;    // [r1 - r0]
+    // local search (encoder.py:312-347 as a windowed GEMM): the (M tile, domain tile) units that meet
+    // some row's window, M-major (nullptr: every unit, the full search); their count on the device
+    const uint2 *units;
+    const int *n_units_dev;
+    int local_R;                 // window radius (-1: full search)
+    int W, H, B, ndx, ndy;       // geometry of the windows (stride 1: domain index = y * ndx + x)
 };
 
 
@@ -224,6 +230,7 @@ __device__ __forceinline__ void mbar_wait_ns(uint64_t *bar, uint32_t parity) {
 // max(|a|, |b|, m): one FMNMX3 with |.| operand modifiers
 __device__ __forceinline__ float absmax3(float m, float a, float b) { return fmaxf(m, fmaxf(fabsf(a), fabsf(b))); }
 
+template <bool LOCAL>  // LOCAL: the windowed local search (p.units, p.local_R); else the full search
 __global__ void __launch_bounds__(NTHREADS, 1)
     full_search_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const TcParams p) {
@@ -245,10 +252,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this CTA's contiguous share of the (M tile, domain tile) units, M-major
-    const long long u0 = p.n_units * blockIdx.x / gridDim.x, u1 = p.n_units * (blockIdx.x + 1) / gridDim.x;
+    const long long n_units = LOCAL ? (long long)*p.n_units_dev : p.n_units;
+    const long long u0 = n_units * blockIdx.x / gridDim.x, u1 = n_units * (blockIdx.x + 1) / gridDim.x;
     const int ntiles = (int)(u1 - u0);
-    const int m_first = (int)(u0 / p.n_dt), dt_first = (int)(u0 % p.n_dt);  // then walked incrementally
-
+    // The units of this CTA, walked in order by every role: (M tile, domain tile) of unit t, and the
+    // M tile of unit t + 1.  The local search reads its list three units ahead (registers), so no
+    // dependent global load sits on the TMA / MMA critical path.
+    struct UnitStream {
+        const uint2 *units;
+        int n_dt;
+        long long u0;
+        int ntiles, t;
+        uint2 a, b, c;  // units t, t + 1, t + 2
+        __device__ uint2 load(int i) const {  // local search only
+            return i < ntiles ? __ldg(units + u0 + i) : make_uint2(0xFFFFFFFFu, 0u);
+        }
+        __device__ uint2 step(uint2 u) const {  // dense: the next unit, M-major
+            return u.y + 1 == (uint32_t)n_dt ? make_uint2(u.x + 1, 0u) : make_uint2(u.x, u.y + 1);
+        }
+        __device__ UnitStream(const uint2 *un, int ndt, long long uu0, int nt)
+            : units(un), n_dt(ndt), u0(uu0), ntiles(nt), t(0) {
+            if (LOCAL) {
+                a = load(0);
+                b = load(1);
+                c = load(2);
+            } else {
+                a = make_uint2((uint32_t)(u0 / n_dt), (uint32_t)(u0 % n_dt));
+                b = step(a);
+            }
+        }
+        __device__ int m() const { return (int)a.x; }
+        __device__ int dt() const { return (int)a.y; }
+        __device__ int next_m() const { return (int)b.x; }
+        __device__ void advance() {
+            if (LOCAL) {
+                a = b;
+                b = c;
+                c = load(++t + 2);
+            } else {
+                a = b;
+                b = step(b);
+            }
+        }
+    };
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full_bar[s], 1);
@@ -290,7 +336,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
             int seg = -1, cur_m = -1;
-            for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+            UnitStream us(p.units, p.n_dt, u0, ntiles);
+            for (int t = 0; t < ntiles; t++, us.advance()) {
+                const int m = us.m(), dt = us.dt();
                 if (m != cur_m) {
                     cur_m = m;
                     seg++;
@@ -314,7 +362,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                    ((uint32_t)(BM >> 4) << 24);
             int seg = -1, cur_m = -1;
             uint64_t adesc0 = 0;
-            for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+            UnitStream us(p.units, p.n_dt, u0, ntiles);
+            for (int t = 0; t < ntiles; t++, us.advance()) {
+                const int m = us.m();
                 if (m != cur_m) {
                     cur_m = m;
                     seg++;
@@ -338,18 +388,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 umma_commit(&empty_bar[s]);  // frees the B stage when these MMAs complete
                 umma_commit(&tfull[acc]);    // accumulator ready for the epilogue
-                const bool seg_end = t + 1 == ntiles || dt + 1 == p.n_dt;
+                const bool seg_end = t + 1 == ntiles || us.next_m() != m;
                 if (seg_end) umma_commit(&a_empty[seg & 1]);  // A buffer reusable once these complete
             }
         }
     } else if (warp == 2) {
         // ===== column constants of tile t into ring slot t % NCB (read only on the rare level-2 path)
         if (lane == 0) {
+            UnitStream us(p.units, p.n_dt, u0, ntiles);
 #if defined(TC_EXP) && TC_EXP >= 4
-            for (int t = 0, dt = dt_first; t < 0; t++) {
+            for (int t = 0; t < 0; t++) {
 #else
-            for (int t = 0, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1) {
+            for (int t = 0; t < ntiles; t++, us.advance()) {
 #endif
+                const int dt = us.dt();
                 const int cb = t % NCB;
                 if (t >= NCB) {  // the slot's previous copy has landed and every epilogue warp is past it
                     mbar_wait_ns(&cfull[cb], ((t / NCB) - 1) & 1);
@@ -417,6 +469,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float n64 = -64.f * (float)p.n;
         const float inv_n = 1.0f / (float)p.n;  // exact (power of two)
         int cur_m = -1, rr = 0;
+        uint32_t wx = 0xFFFF0000u, wy = 0xFFFF0000u;  // local search: the row's window, lo | hi << 16
         bool live = false;
         float erow = 0.f, thr = -1.f;
         long long vstar = LLONG_MAX;  // an upper bound of this range's best value (a real candidate's)
@@ -430,10 +483,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         };
         unsigned long long g = ~0ull;
+        // the epilogue walks its units with a one-ahead prefetch (local) or incrementally (dense)
+        uint2 u_cur = ntiles > 0 ? (LOCAL ? __ldg(p.units + u0) : make_uint2((uint32_t)(u0 / p.n_dt), (uint32_t)(u0 % p.n_dt)))
+                                 : make_uint2(0u, 0u);
 #if defined(TC_EXP) && TC_EXP >= 4
-        for (int t = 0, m = m_first, dt = dt_first; t < 0; t++) {
+        for (int t = 0; t < 0; t++) {
+            int m = 0, dt = 0;
 #else
-        for (int t = 0, m = m_first, dt = dt_first; t < ntiles; t++, dt = dt + 1 == p.n_dt ? 0 : dt + 1, m += dt == 0) {
+        for (int t = 0; t < ntiles; t++) {
+            const int m = (int)u_cur.x, dt = (int)u_cur.y;
+            if (LOCAL)
+                u_cur = t + 1 < ntiles ? __ldg(p.units + u0 + t + 1) : u_cur;
+            else
+                u_cur = u_cur.y + 1 == (uint32_t)p.n_dt ? make_uint2(u_cur.x + 1, 0u) : make_uint2(u_cur.x, u_cur.y + 1);
 #endif
             if (m != cur_m) {  // new M tile: load the row
                 cur_m = m;
@@ -442,7 +504,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const bool flat = active ? p.row_flat[row] != 0 : true;
                 live = active && !flat;
                 rr = row / p.n_iso;
-                if (active && flat && row % p.n_iso == 0 && half == 0) atomicMin(&p.best[rr], *p.flat_key);
+                if (!LOCAL && active && flat && row % p.n_iso == 0 && half == 0)
+                    atomicMin(&p.best[rr], *p.flat_key);  // (local search: local_flat_kernel)
+                if (LOCAL && active) {  // the range's window of candidate origins
+                    const int ri = p.r0 + rr, rpr = p.W / p.B;
+                    const int bx = clampi((ri % rpr) * p.B - p.B / 2, 0, p.W - 2 * p.B);
+                    const int by = clampi((ri / rpr) * p.B - p.B / 2, 0, p.H - 2 * p.B);
+                    wx = (uint32_t)clampi(bx - p.local_R, 0, p.ndx - 1) |
+                         ((uint32_t)clampi(bx + p.local_R, 0, p.ndx - 1) << 16);
+                    wy = (uint32_t)clampi(by - p.local_R, 0, p.ndy - 1) |
+                         ((uint32_t)clampi(by + p.local_R, 0, p.ndy - 1) << 16);
+                }
                 erow = live ? p.row_err[row] : 0.f;
                 vstar = LLONG_MAX;
                 thr = -1.f;
@@ -470,7 +542,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 continue;  // timing experiment: MMA + accumulator drain only
             }
 #endif
-            // level 1: one |max| per 16-column group against the row threshold (FMNMX3 per 2 columns)
+            // local search: the 16-bit mask of group gi's columns inside the row's window (packed
+            // window bounds, so the mask costs no registers across the tile)
+            int gy0 = 0, gx0 = 0;  // domain (x, y) of the thread's first column of this tile
+            // the thread's EPI_COLS columns span at most two domain rows when ndx >= EPI_COLS: the
+            // window's columns are then two intervals [i1a, i1b] and [i2a, i2b] (empty: a > b)
+            int i1a = 1, i1b = 0, i2a = 1, i2b = 0;
+            if (LOCAL && live) {
+                const int base = dt * BN + half * EPI_COLS;  // < 2^31 (domain indices)
+                gy0 = base / p.ndx;
+                gx0 = base - gy0 * p.ndx;
+                const int lx = (int)(wx & 0xFFFF), hx = (int)(wx >> 16), ly = (int)(wy & 0xFFFF), hy = (int)(wy >> 16);
+                const int split = p.ndx - gx0;  // first column of the next domain row
+                if (gy0 >= ly && gy0 <= hy) {
+                    i1a = max(lx - gx0, 0);
+                    i1b = min(min(hx - gx0, split - 1), EPI_COLS - 1);
+                }
+                if (split < EPI_COLS && gy0 + 1 >= ly && gy0 + 1 <= hy) {
+                    i2a = max(split + lx, split);
+                    i2b = min(split + hx, EPI_COLS - 1);
+                }
+            }
+            // exact 16-bit window mask of group gi (small images, ndx < EPI_COLS: column by column)
+            auto group_mask = [&](int gi) -> uint32_t {
+                if (p.ndx >= EPI_COLS) {
+                    const int g0 = gi * GRP;
+                    uint32_t mk = 0;
+                    int lo = max(i1a - g0, 0), hi = min(i1b - g0, GRP - 1);
+                    if (lo <= hi) mk |= ((2u << hi) - 1u) & ~((1u << lo) - 1u);
+                    lo = max(i2a - g0, 0);
+                    hi = min(i2b - g0, GRP - 1);
+                    if (lo <= hi) mk |= ((2u << hi) - 1u) & ~((1u << lo) - 1u);
+                    return mk;
+                }
+                const int lx = (int)(wx & 0xFFFF), hx = (int)(wx >> 16), ly = (int)(wy & 0xFFFF), hy = (int)(wy >> 16);
+                int x = gx0 + gi * GRP, y = gy0;
+                while (x >= p.ndx) {
+                    x -= p.ndx;
+                    y++;
+                }
+                uint32_t mk = 0;
+                for (int j = 0; j < GRP; j++) {
+                    if (y >= ly && y <= hy && x >= lx && x <= hx) mk |= 1u << j;
+                    if (++x == p.ndx) {
+                        x = 0;
+                        y++;
+                    }
+                }
+                return mk;
+            };
+            // level 1: one |max| per 16-column group against the row threshold (FMNMX3 per 2 columns);
+            // local search: groups outside the window are skipped, partial ones filtered whole (the
+            // rare path applies the exact column mask)
             unsigned gpass = 0;
 #pragma unroll
             for (int gi = 0; gi < EPI_COLS / GRP; gi++) {
@@ -480,7 +603,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     ma = absmax3(ma, c[gi * GRP + j], c[gi * GRP + j + 1]);
                     mb = absmax3(mb, c[gi * GRP + j + 2], c[gi * GRP + j + 3]);
                 }
-                gpass |= (live && fmaxf(ma, mb) >= thr) ? 1u << gi : 0u;
+                bool in = true;
+                if (LOCAL) {
+                    const int g0 = gi * GRP, g1 = g0 + GRP - 1;
+                    in = p.ndx >= EPI_COLS ? ((i1a <= i1b && i1a <= g1 && i1b >= g0) || (i2a <= i2b && i2a <= g1 && i2b >= g0))
+                                           : group_mask(gi) != 0;
+                }
+                gpass |= (live && in && fmaxf(ma, mb) >= thr) ? 1u << gi : 0u;
             }
 #ifdef MNS_TC_STATS
             if (lane == 0) atomicAdd(&g_tc_stats[0], (unsigned long long)(EPI_COLS / GRP));
@@ -506,6 +635,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         mask |= (fabsf(c[gi * GRP + j]) >= thr ? 1u : 0u) << j;
                         stash[j * 32 + lane] = c[gi * GRP + j];  // lane-private column, for dynamic access
                     }
+                    if (LOCAL) mask &= group_mask(gi);
 #ifdef MNS_TC_STATS
                     atomicAdd(&g_tc_stats[1], 1ull);
 #endif
@@ -708,7 +838,7 @@ __global__ void gather_sample_kernel(const float2 *consts, const long long *pD, 
 // seed; the final argmin is unchanged).
 __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const uint16_t *pool, const int32_t *psq,
                                  const long long *pD, int W, int B, int step, int ndx, int ndy, int n_iso, int r0,
-                                 int n_ranges, unsigned long long *best) {
+                                 int n_ranges, unsigned long long *best, int soff) {
     const int lane = threadIdx.x & 31;
     const int rr = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (rr >= n_ranges) return;
@@ -729,7 +859,7 @@ __global__ void seed_best_kernel(const __half *A, const int32_t *row_sr, const u
         const int pi = p0 + sl;
         const bool valid = pi < 25 * n_iso;
         const int c = valid ? pi / n_iso : 0;
-        const int ox = (c % 5 - 2) * B / 2, oy = (c / 5 - 2) * B / 2;
+        const int ox = (c % 5 - 2) * soff, oy = (c / 5 - 2) * soff;  // soff = B/2 (local: <= R/2)
         const int dx = clampi((rx - B / 2 + ox) / step, 0, ndx - 1), dy = clampi((ry - B / 2 + oy) / step, 0, ndy - 1);
         const int d = dy * ndx + dx;
         const uint16_t *qd = pool + (long long)d * n + k0;
@@ -787,6 +917,135 @@ __global__ void flat_key_kernel(const long long *pD, long long ndom, int n_iso, 
         best = other < best ? other : best;
     }
     if ((threadIdx.x & 31) == 0) atomicMin(key, best);
+}
+
+// ---- local search (encoder.py:312-347) on the same tensor-core pipeline
+// Constant ranges: every candidate's value is its D (k2 = +-1, s = 0.125 as the reference's
+// fit gives s = 0); the window's minimum D (lowest index on ties, isometry 0). One warp per range.
+__global__ void local_flat_kernel(const int32_t *row_flat, const long long *pD, int W, int H, int B, int R, int ndx,
+                                  int ndy, int n_iso, int n_ranges, unsigned long long *best) {
+    const int lane = threadIdx.x & 31;
+    const int rr = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (rr >= n_ranges || !row_flat[rr * n_iso]) return;
+    const int rpr = W / B;
+    const int bx = clampi((rr % rpr) * B - B / 2, 0, W - 2 * B), by = clampi((rr / rpr) * B - B / 2, 0, H - 2 * B);
+    const int lx = clampi(bx - R, 0, ndx - 1), hx = clampi(bx + R, 0, ndx - 1);
+    const int ly = clampi(by - R, 0, ndy - 1), hy = clampi(by + R, 0, ndy - 1);
+    const int wx = hx - lx + 1, nwin = wx * (hy - ly + 1);
+    unsigned long long k = ~0ull;
+    for (int i = lane; i < nwin; i += 32) {
+        const long long d = (long long)(ly + i / wx) * ndx + lx + i % wx;
+        const unsigned long long key = make_key_cb(pD[d], d * n_iso, key_cand_bits(B * B));
+        k = key < k ? key : k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(FULL, k, o);
+        k = other < k ? other : k;
+    }
+    if (lane == 0) atomicMin(&best[rr], k);
+}
+
+// The (M tile, domain tile) units of the local search: per M tile (one block) the domain tiles that
+// meet the union of its ranges' windows.  The ranges of an M tile are consecutive in raster order,
+// so per range row the union is one rectangle of origins; its rows mark tile intervals in a shared
+// bitmap over the tile's hull, read back in order into scratch[m * cap ..], count in counts[m].
+constexpr int LT_BITS = 32768;  // hull bound (domain tiles) per M tile
+__global__ void local_units_kernel(int W, int H, int B, int R, int ndx, int ndy, int n_iso, int n_rows, int cap,
+                                   uint32_t *scratch, int *counts) {
+    __shared__ uint32_t bm[LT_BITS / 32];
+    __shared__ int hull[2], cnt;
+    const int m = blockIdx.x, tid = threadIdx.x;
+    const int rpr = W / B;
+    const int row0 = m * (MH * BM), row1 = min(n_rows, row0 + MH * BM);
+    const int ra = row0 / n_iso, rb = (row1 - 1) / n_iso;  // the tile's ranges [ra, rb]
+    auto win_y = [&](int rowr, int &lo, int &hi) {
+        const int by = clampi(rowr * B - B / 2, 0, H - 2 * B);
+        lo = clampi(by - R, 0, ndy - 1);
+        hi = clampi(by + R, 0, ndy - 1);
+    };
+    auto win_x = [&](int c0, int c1, int &lo, int &hi) {  // union over range columns c0..c1 of one row
+        lo = clampi(clampi(c0 * B - B / 2, 0, W - 2 * B) - R, 0, ndx - 1);
+        hi = clampi(clampi(c1 * B - B / 2, 0, W - 2 * B) + R, 0, ndx - 1);
+    };
+    if (tid == 0) {
+        int ylo, yhi, tmp;
+        win_y(ra / rpr, ylo, tmp);
+        win_y(rb / rpr, tmp, yhi);
+        hull[0] = (int)(((long long)ylo * ndx) / BN);
+        hull[1] = (int)(((long long)yhi * ndx + ndx - 1) / BN);
+        cnt = 0;
+    }
+    for (int i = tid; i < LT_BITS / 32; i += blockDim.x) bm[i] = 0;
+    __syncthreads();
+    const int h0 = hull[0];
+    const int nh = min(hull[1] - h0 + 1, LT_BITS);
+    for (int rowr = ra / rpr; rowr <= rb / rpr; rowr++) {
+        const int c0 = rowr == ra / rpr ? ra % rpr : 0, c1 = rowr == rb / rpr ? rb % rpr : rpr - 1;
+        int ylo, yhi, xlo, xhi;
+        win_y(rowr, ylo, yhi);
+        win_x(c0, c1, xlo, xhi);
+        for (int y = ylo + tid; y <= yhi; y += blockDim.x) {
+            const long long a = (long long)y * ndx + xlo, b = (long long)y * ndx + xhi;
+            for (long long t = a / BN; t <= b / BN; t++) {
+                const int bit = (int)(t - h0);
+                if (bit >= 0 && bit < nh) atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // centre-out order (tiles alternately after and before the one holding the M tile's central
+        // window origin): the best candidates are usually near the range, so the row thresholds
+        // tighten early and fewer elements reach the exact evaluation
+        const int rc = (ra + rb) / 2;
+        int cy, tmp;
+        win_y(rc / rpr, cy, tmp);
+        cy = (cy + tmp) / 2;
+        int cx0, cx1;
+        win_x(rc % rpr, rc % rpr, cx0, cx1);
+        const int c0 = min(max((int)(((long long)cy * ndx + (cx0 + cx1) / 2) / BN) - h0, 0), nh - 1);
+        int k = 0;
+        for (int dlt = 0; dlt < nh; dlt++) {
+            for (int sgn = 0; sgn < (dlt ? 2 : 1); sgn++) {
+                const int b = sgn ? c0 - dlt : c0 + dlt;
+                if (b < 0 || b >= nh || !((bm[b >> 5] >> (b & 31)) & 1u)) continue;
+                if (k < cap) scratch[(long long)m * cap + k] = (uint32_t)(h0 + b);
+                k++;
+            }
+        }
+        counts[m] = min(k, cap);
+    }
+}
+
+// exclusive scan of the per-M-tile counts (one block of 1024 threads, each a contiguous chunk)
+__global__ void local_units_scan_kernel(const int *counts, int n_mt, int *offsets, int *n_units) {
+    __shared__ int part[1024];
+    const int tid = threadIdx.x, per = (n_mt + 1023) / 1024, a = tid * per, b = min(n_mt, a + per);
+    int s = 0;
+    for (int m = a; m < b; m++) s += counts[m];
+    part[tid] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+        const int v = tid >= o ? part[tid - o] : 0;
+        __syncthreads();
+        part[tid] += v;
+        __syncthreads();
+    }
+    int run = part[tid] - s;
+    for (int m = a; m < b; m++) {
+        offsets[m] = run;
+        run += counts[m];
+    }
+    if (tid == 1023) *n_units = part[1023];
+}
+
+// the flattened (m, dt) unit list, M-major (one block per M tile)
+__global__ void local_units_flatten_kernel(const uint32_t *scratch, const int *counts, const int *offsets, int cap,
+                                           uint2 *units) {
+    const int m = blockIdx.x, c = counts[m], o = offsets[m];
+    for (int i = threadIdx.x; i < c; i += blockDim.x)
+        units[o + i] = make_uint2((uint32_t)m, scratch[(long long)m * cap + i]);
 }
 
 int sm_count_tc() {
@@ -870,7 +1129,7 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     {
         const int ndx = (W - 2 * B) / step + 1, ndy = (int)(ndom / ndx);
         seed_best_kernel<<<(r1 - r0 + 7) / 8, 256, 0, st>>>(Araw, row_sr, pool, psq, pD, W, B, step, ndx, ndy, n_iso,
-                                                            r0, r1 - r0, best);
+                                                            r0, r1 - r0, best, B / 2);
     }
 #endif
 
@@ -897,10 +1156,11 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
     p.row_flat = row_flat;
     p.row_err = row_err;
     p.flat_key = fkey;
+    p.local_R = -1;
     p.best = best;
     {
         static std::atomic<unsigned long long> done{0};
-        MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel, SMEM_BYTES, done));
+        MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel<false>, SMEM_BYTES, done));
     }
     const long long n_mt = n_rows_pad / (MH * BM);
 #ifdef TC_NO_PREPASS
@@ -916,15 +1176,125 @@ int full_search_tc(const uint8_t *img, int W, int H, int B, int step, int n_iso,
         q2.n_dt = (int)((nsample + BN - 1) / BN);
         q2.n_units = n_mt * q2.n_dt;
         const int grid = (int)(q2.n_units < sms ? q2.n_units : sms);
-        full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmS, q2);
+        full_search_tc_kernel<false><<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmS, q2);
     }
     p.dstride = 1;
     p.n_dt = (int)(ndom_pad / BN);
     p.n_units = n_mt * p.n_dt;
     const int grid = (int)(p.n_units < sms ? p.n_units : sms);
-    full_search_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
+    full_search_tc_kernel<false><<<grid, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
     MNS_CUDA_TRY(cudaGetLastError());
     *handled = true;
+    return 0;
+}
+
+
+// Local search on the tensor-core pipeline (local_R >= 0): the full-search kernel walks only the
+// units that meet some window and masks every element outside its row's window.  Workspace:
+// local_search_tc_workspace_bytes; pool/psq/pD/best as for the full search.
+int64_t local_units_cap(int W, int H, int B, int R, int n_iso) {
+    const int rpr = W / B, ndx = W - 2 * B + 1;
+    const int range_rows = (MH * BM / n_iso + rpr - 1) / rpr + 1;  // range rows an M tile spans
+    const long long span = (long long)(range_rows * B + 2 * R + 2) * ndx;
+    return span / BN + 3;
+}
+
+int64_t local_search_tc_workspace_bytes(int W, int H, int B, int R, int n_iso) {
+    const long long n_rows = (long long)(W / B) * (H / B) * n_iso;
+    const long long n_mt = (n_rows + MH * BM - 1) / (MH * BM);
+    const long long cap = local_units_cap(W, H, B, R, n_iso);
+    return search_tc_workspace_bytes(W, H, B, 1, n_iso) + 256 + n_mt * 4 + 256 + 256 + n_mt * 4 + 256 +
+           n_mt * cap * 4 + 256 + n_mt * cap * 8 + 256;
+}
+
+int local_search_tc(const uint8_t *img, int W, int H, int R, int n_iso, uint16_t *pool, int32_t *psq, long long *pD,
+                    long long ndom, unsigned long long *best, void *tc_ws, cudaStream_t st) {
+    const int B = 8, n = 64;
+    const int ndx = W - 2 * B + 1, ndy = H - 2 * B + 1;
+    const long long ndom_pad = (ndom + BN - 1) / BN * BN;
+    const int n_ranges = (W / B) * (H / B);
+    const int n_rows = n_ranges * n_iso;
+    const int n_rows_pad = (n_rows + MH * BM - 1) / (MH * BM) * (MH * BM);
+    const int n_mt = n_rows_pad / (MH * BM);
+    const long long cap = local_units_cap(W, H, B, R, n_iso);
+    MNS_CHECK_ARG(cap <= LT_BITS, "local search window hull too large for the tensor-core path");
+    char *q = (char *)tc_ws;
+    __half *Q = (__half *)q;
+    q += ndom_pad * BK * 2;
+    float2 *consts = (float2 *)q;
+    q += ndom_pad * 8;
+    __half *Araw = (__half *)q;
+    q += (long long)n_rows_pad * BK * 2;
+    __half *Ac = (__half *)q;
+    q += (long long)n_rows_pad * BK * 2;
+    int32_t *row_sr = (int32_t *)q;
+    q += (long long)n_rows_pad * 4;
+    int32_t *row_flat = (int32_t *)q;
+    q += (long long)n_rows_pad * 4;
+    float *row_err = (float *)q;
+    q = (char *)tc_ws + search_tc_workspace_bytes(W, H, B, 1, n_iso);
+    q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+    int *counts = (int *)q;
+    q += n_mt * 4 + 256;
+    q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+    int *offsets = (int *)q;
+    q += n_mt * 4 + 256;
+    q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+    uint32_t *scratch = (uint32_t *)q;
+    q += n_mt * cap * 4 + 256;
+    q = (char *)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+    uint2 *units = (uint2 *)q;
+    q += n_mt * cap * 8 + 256;
+    int *n_units = counts + n_mt;  // the slot after the counts (256 B of slack reserved there)
+
+    const unsigned blocks = (unsigned)((ndom_pad + 127) / 128);
+    pool_tc_kernel<8><<<blocks, 128, 0, st>>>(img, W, 1, ndx, ndom, ndom_pad, pool, psq, pD, Q, consts);
+    range_rows_kernel<<<(n_rows_pad + 7) / 8, 256, 0, st>>>(img, W, B, n_iso, 0, n_rows, n_rows_pad, Araw, Ac, row_sr,
+                                                          row_flat, row_err);
+    const int soff = R / 2 < B / 2 ? R / 2 : B / 2;  // seeds stay inside the window
+    seed_best_kernel<<<(n_ranges + 7) / 8, 256, 0, st>>>(Araw, row_sr, pool, psq, pD, W, B, 1, ndx, ndy, n_iso, 0,
+                                                        n_ranges, best, soff);
+    local_flat_kernel<<<(n_ranges + 7) / 8, 256, 0, st>>>(row_flat, pD, W, H, B, R, ndx, ndy, n_iso, n_ranges, best);
+    local_units_kernel<<<n_mt, 256, 0, st>>>(W, H, B, R, ndx, ndy, n_iso, n_rows, (int)cap, scratch, counts);
+    local_units_scan_kernel<<<1, 1024, 0, st>>>(counts, n_mt, offsets, n_units);
+    local_units_flatten_kernel<<<n_mt, 128, 0, st>>>(scratch, counts, offsets, (int)cap, units);
+
+    CUtensorMap tmA, tmB;
+    if (encode_tmap_2d_swizzled(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Ac, BK, n_rows_pad, BK * 2, BK, BM)) return -1;
+    if (encode_tmap_2d_swizzled(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Q, BK, ndom_pad, BK * 2, BK, BN)) return -1;
+    TcParams p{};
+    p.n_rows = n_rows;
+    p.n_iso = n_iso;
+    p.r0 = 0;
+    p.n = n;
+    p.ndom = ndom;
+    p.consts = consts;
+    p.pD = pD;
+    p.pool = pool;
+    p.araw = Araw;
+    p.row_sr = row_sr;
+    p.row_flat = row_flat;
+    p.row_err = row_err;
+    p.flat_key = nullptr;
+    p.best = best;
+    p.dstride = 1;
+    p.n_dt = (int)(ndom_pad / BN);
+    p.n_units = 0;
+    p.units = units;
+    p.n_units_dev = n_units;
+    p.local_R = R;
+    p.W = W;
+    p.H = H;
+    p.B = B;
+    p.ndx = ndx;
+    p.ndy = ndy;
+    {
+        static std::atomic<unsigned long long> done{0};
+        MNS_CUDA_TRY(ensure_dynamic_smem(full_search_tc_kernel<true>, SMEM_BYTES, done));
+    }
+    const int sms = sm_count_tc();
+    full_search_tc_kernel<true><<<sms, NTHREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
+    MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
 

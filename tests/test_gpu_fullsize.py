@@ -153,13 +153,15 @@ def test_c4_full_search_all_ranges_vs_oracle(mns, n_iso):
 
 
 @pytest.mark.parametrize("radius,n_iso", [(4, 1), (32, 1), (4, 8), (32, 8)])
-def test_c4_local_search_all_ranges_vs_oracle(mns, radius, n_iso):
-    """All 4096 ranges; (32, 8) is config c4's +-32 x 8-isometry variant (1.38e8 pairs)."""
+@pytest.mark.parametrize("tensor_cores", [True, False])
+def test_c4_local_search_all_ranges_vs_oracle(mns, radius, n_iso, tensor_cores):
+    """All 4096 ranges, on the windowed tcgen05 GEMM and on the CUDA-core kernel; (32, 8) is config
+    c4's +-32 x 8-isometry variant (1.38e8 pairs)."""
     from paper_1501_02894_b200.synth import config_image
 
     px = config_image("c4")
     res = {k: v.cpu().numpy() for k, v in
-           mns.local_search_device(torch.from_numpy(px).cuda(), radius, n_iso=n_iso).items()}
+           mns.local_search_device(torch.from_numpy(px).cuda(), radius, n_iso=n_iso, tensor_cores=tensor_cores).items()}
     ref = O.local_search(px, radius, n_iso=n_iso)
     assert np.array_equal(res["dx"], ref["dom_x"]) and np.array_equal(res["dy"], ref["dom_y"])
     assert np.array_equal(res["iso"], ref["iso"])

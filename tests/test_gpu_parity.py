@@ -890,3 +890,34 @@ def test_isometry_extension_encode_decode_vs_oracle(mns, name, e, mode, root_lev
     assert np.array_equal(out.cpu().numpy(), want)
     with pytest.raises(ValueError, match="isometry"):
         mns.write_stream(code)
+
+
+@pytest.mark.parametrize("shape,radius,n_iso", [((64, 64), 4, 1), ((64, 64), 32, 8), ((40, 72), 7, 8), ((16, 16), 3, 1),
+                                                ((24, 48), 0, 8), ((96, 96), 1, 1), ((128, 200), 32, 1),
+                                                ((136, 64), 5, 8)])
+def test_local_search_tensor_core_vs_oracle(mns, shape, radius, n_iso):
+    """The windowed tcgen05 local search (mns_local_search_tc) against the oracle and the CUDA-core
+    kernel: window edges, clamped borders, tiny and non-square images, radius 0, isometries."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    px = np.ascontiguousarray(synth_image(256, 5 + radius, noise_sigma=9.0, n_blobs=4)[: shape[0], : shape[1]])
+    img = torch.from_numpy(px).cuda()
+    tc = {k: v.cpu().numpy() for k, v in mns.local_search_device(img, radius, n_iso=n_iso, tensor_cores=True).items()}
+    cc = {k: v.cpu().numpy() for k, v in mns.local_search_device(img, radius, n_iso=n_iso, tensor_cores=False).items()}
+    ref = O.local_search(px, radius, n_iso=n_iso)
+    for k, rk in (("dx", "dom_x"), ("dy", "dom_y"), ("iso", "iso"), ("o", "o"), ("code", "code")):
+        assert np.array_equal(tc[k], ref[rk]), (k, int((tc[k] != ref[rk]).sum()))
+        assert np.array_equal(cc[k], ref[rk]), k
+
+
+def test_local_search_tensor_core_flat_ranges(mns):
+    """Constant ranges (the windowed minimum-D rule) and saturated pixels on the tcgen05 path."""
+    rng = np.random.default_rng(3)
+    px = np.kron(rng.integers(0, 256, (8, 8)), np.ones((8, 8))).astype(np.uint8)  # 64x64 of flat 8x8 blocks
+    px[16:40, 16:40] = rng.integers(250, 256, (24, 24))
+    img = torch.from_numpy(np.ascontiguousarray(px)).cuda()
+    for radius, n_iso in ((4, 1), (32, 8)):
+        tc = {k: v.cpu().numpy() for k, v in mns.local_search_device(img, radius, n_iso=n_iso, tensor_cores=True).items()}
+        ref = O.local_search(px, radius, n_iso=n_iso)
+        for k, rk in (("dx", "dom_x"), ("dy", "dom_y"), ("iso", "iso"), ("o", "o"), ("code", "code")):
+            assert np.array_equal(tc[k], ref[rk]), (radius, n_iso, k)
