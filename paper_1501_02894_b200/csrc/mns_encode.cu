@@ -475,7 +475,7 @@ __global__ void try_node_kernel(const uint8_t *img, int W, int H, int64_t pitch,
 // quadrant lanes 0/4/8/12 of each half, level 3 one node per lane; then the DFS emission.
 constexpr int PRING = 64;                           // pixel ring rows (4 blocks of 16)
 constexpr int QW = WIN_W / 2;                       // 144 q columns
-constexpr int QP = QW + 8;                          // q ring pitch (u16): conflict-free level-3 pair loads
+constexpr int QP = QW + 4;                          // q ring pitch (u16): 148 halves the level-1/2 load conflicts (4- to 2-way, the floor for these patterns)
 constexpr int QRING = 32;                           // q / q^2 ring rows (4 blocks of 8)
 constexpr int ENC_PIX = PRING * WIN_W;              // 18432 B
 constexpr int ENC_Q = QRING * QP * 2;               // 9728 B
