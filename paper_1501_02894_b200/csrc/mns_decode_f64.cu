@@ -53,6 +53,66 @@ __device__ double paint_unit_f64(int x, int y, int size, int iso, int dx, int dy
     return dmax;
 }
 
+// numpy's pairwise float64 sum (loops_utils.h.src) for a compile-time n <= 128, a in registers
+template <int NN>
+__device__ __forceinline__ double pw_sum_fixed(const double (&a)[NN]) {
+    if constexpr (NN < 8) {
+        double res = 0.0;
+#pragma unroll
+        for (int i = 0; i < NN; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+#pragma unroll
+        for (int i = 8; i < NN - (NN % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+        for (int i = NN - (NN % 8); i < NN; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+}
+
+// paint_unit_f64 for a compile-time side (2 or 4: the bulk of quadtree codes), everything in
+// registers; the domain's 2x2 cells are read as double2 (even domain origins for side >= 4)
+template <int S>
+__device__ __forceinline__ double paint_unit_f64_fixed(int x, int y, int iso, int dx, int dy, double s, double o,
+                                                       int W, const double *cur, double *out) {
+    double d[S * S];
+#pragma unroll
+    for (int i = 0; i < S; i++)
+#pragma unroll
+        for (int j = 0; j < S; j++) {
+            const int k = iso ? iso_src(iso, i, j, S) : i * S + j;
+            const double *pp = cur + (size_t)(dy + 2 * (k / S)) * W + dx + 2 * (k % S);
+            double a0, a1, b0, b1;
+            if (S >= 4 && !(dx & 1)) {  // 16-byte aligned pairs (quadtree domains; search domains may be odd)
+                const double2 ra = *reinterpret_cast<const double2 *>(pp), rb = *reinterpret_cast<const double2 *>(pp + W);
+                a0 = ra.x; a1 = ra.y; b0 = rb.x; b1 = rb.y;
+            } else {
+                a0 = pp[0]; a1 = pp[1]; b0 = pp[W]; b1 = pp[W + 1];
+            }
+            d[i * S + j] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(a0, a1), b0), b1), 0.25);
+        }
+    const double dm = __ddiv_rn(pw_sum_fixed<S * S>(d), (double)(S * S));
+    double dmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < S; i++)
+#pragma unroll
+        for (int j = 0; j < S; j++) {
+            double v = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * S + j], dm)), o);
+            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+            const size_t idx = (size_t)(y + i) * W + x + j;
+            dmax = fmax(dmax, fabs(__dsub_rn(v, cur[idx])));
+            out[idx] = v;
+        }
+    return dmax;
+}
+
 __global__ void __launch_bounds__(256) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
                                                         const int32_t *udx, const int32_t *udy, const double *us,
                                                         const double *uo, long long n, int W, const double *cur,
@@ -60,9 +120,15 @@ __global__ void __launch_bounds__(256) sweep_f64_kernel(const int32_t *ux, const
     if (state[0]) return;  // converged in an earlier sweep
     const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     double dmax = 0.0;
-    if (u < n && (usize[u] & 255) > 0)  // usize = side | isometry << 8
-        dmax = paint_unit_f64(ux[u], uy[u], usize[u] & 255, usize[u] >> 8, udx[u], udy[u], us[u], uo[u], W, cur,
-                              nxt);
+    if (u < n && (usize[u] & 255) > 0) {  // usize = side | isometry << 8
+        const int side = usize[u] & 255, iso = usize[u] >> 8;
+        if (side == 4)
+            dmax = paint_unit_f64_fixed<4>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+        else if (side == 2)
+            dmax = paint_unit_f64_fixed<2>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+        else
+            dmax = paint_unit_f64(ux[u], uy[u], side, iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+    }
     long long bits = __double_as_longlong(dmax);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
