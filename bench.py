@@ -246,7 +246,7 @@ def small_configs(dev, rank, world):
         return mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
                               torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
                               torch.zeros(1, dtype=torch.int64, device=dev), W, H, nb,
-                              unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device=dev))
+                              unit_map=torch.empty(8 * n_roots, dtype=torch.int32, device=dev), map_form=1)
 
     def ev():
         return torch.cuda.Event(enable_timing=True)
@@ -362,7 +362,7 @@ def run_ours(args, img_np, rank, world, local_rank):
     code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
                           torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
                           torch.zeros(1, dtype=torch.int64, device=dev), W, H, 1, r0, r1,
-                          unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device=dev))
+                          unit_map=torch.empty(8 * n_roots, dtype=torch.int32, device=dev), map_form=1)
     # e3 = inf: the code has no 2x2 leaves, so the decoder carries the 2x2-sum lattice between passes
     dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world, lattice=True)
     out_host = torch.empty((16 * (r1 - r0), W), dtype=torch.uint8).pin_memory()

@@ -45,6 +45,8 @@ typedef struct {
     int32_t root_level;
     int32_t n_iso;    /* 1 (0): the reference; 8: phase 1 also tries the 8 isometries of the co-centred
                          domain (extension, BASELINE configs[1]; records carry the isometry, MNS_REC_ISO_SHIFT) */
+    int32_t map_form; /* the decoder map mns_encode_quadtree emits into unit_map (mns_record.h):
+                         0 = unit map (32 words per root), 1 = block map (8 words per root; the lattice decoders) */
 } mns_enc_cfg;
 
 /* Replaces: encoder.encode_quadtree (encoder.py:215-246) for n_images images of
@@ -58,8 +60,8 @@ typedef struct {
  * order, then TL,TR,BL,BR pre-order), root_offsets[i] = index of the first
  * record of root i (roots of the processed rows, image-major, raster order;
  * n_roots + 1 entries, the last = total), *d_count = total records (device).
- * capacity must be >= 64 * n_roots.  unit_map (optional, 32 words per root)
- * receives the decoder's unit map.  Workspace: mns_encode_workspace_bytes (64
+ * capacity must be >= 64 * n_roots.  unit_map (optional) receives the decoder's
+ * map in cfg->map_form: the unit map (32 words per root) or the block map (8).  Workspace: mns_encode_workspace_bytes (64
  * staged record slots per root + the compaction scan state; two kernels: the
  * encoder, whose CTAs never wait on one another, then the scan + compaction). */
 int mns_encode_workspace_bytes(int32_t width, int32_t n_images, int32_t root_row_begin, int32_t root_row_end,
@@ -93,9 +95,12 @@ int mns_encode_quadtree_split(const uint8_t *img, int32_t width, int32_t height,
 
 /* Decoder unit map (mns_record.h) of a record array grouped by root: 32 uint32
  * words (64 cells) per root of the root rows [root_row_begin, root_row_end).
- * mns_encode_quadtree emits the same map directly when unit_map != NULL. */
+ * mns_encode_quadtree emits the same map directly when unit_map != NULL.
+ * mns_build_block_map: the block map (16 uint16 per root), as map_form = 1 emits it. */
 int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,
                        int32_t root_row_end, uint32_t *unit_map, void *stream);
+int mns_build_block_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,
+                        int32_t root_row_end, uint16_t *block_map, void *stream);
 
 /* Replaces: decoder.decode / decode_step (decoder.py:37-77) for quadtree codes.
  * One Jacobi sweep per iteration over an fp32 raster (ping/pong, width*height
@@ -149,25 +154,31 @@ int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int3
  * caller) is set to 1 if a 2x2 unit is met (the output is then undefined; use
  * the raster path).
  *
+ * The lattice decoders read the BLOCK map (mns_record.h: one descriptor per 4x4
+ * block, 16 uint16 per root; a quarter of the unit map's bytes), with the same
+ * root-row conventions as the unit map of mns_decode_sweep2.
+ *
  * mns_decode_pass_lattice: two sweeps t -> t+2 (as mns_decode_sweep2; lattice
  * rows [8*root_row_begin - 16, 8*root_row_end + 16) of cur_lattice resident,
  * 16-byte aligned; cur_lattice NULL = flat start; exactly one of nxt_lattice
  * and out).  mns_decode_flat_lattice: the single first sweep from the flat
- * raster, written as lattice (odd sweep counts).  mns_decode_quadtree_lattice:
+ * raster, written as lattice (odd sweep counts; nxt_lattice) or, for a one-sweep
+ * decode, as the rounded uint8 image (out; exactly one of the two).
+ * mns_decode_quadtree_lattice:
  * the whole decode (stop_delta = 0) into the uint8 image, as mns_decode_quadtree
  * with out != NULL; lat_ping / lat_pong hold (height/2)*(width/2) floats each. */
-int mns_decode_pass_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+int mns_decode_pass_lattice(const uint16_t *block_map, int32_t block_map_row_begin, int32_t width, int32_t height,
                             int32_t root_row_begin, int32_t root_row_end, const float *cur_lattice, float initial_value,
                             float *nxt_lattice, uint8_t *out, int32_t *d_error, void *stream);
-int mns_decode_flat_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+int mns_decode_flat_lattice(const uint16_t *block_map, int32_t block_map_row_begin, int32_t width, int32_t height,
                             int32_t root_row_begin, int32_t root_row_end, float initial_value, float *nxt_lattice,
-                            void *stream);
+                            uint8_t *out, void *stream);
 int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
                                 int32_t iters, float initial_value, float *lat_ping, float *lat_pong, uint8_t *out,
                                 int32_t *d_error, void *workspace, int64_t workspace_bytes, void *stream);
-/* mns_decode_unit_map_lattice: mns_decode_quadtree_lattice from the unit map of every root row (as
- * mns_encode_quadtree emits it: 32 words per root), skipping the map build; workspace >= 64 bytes. */
-int mns_decode_unit_map_lattice(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters,
+/* mns_decode_unit_map_lattice: mns_decode_quadtree_lattice from the block map of every root row (as
+ * mns_encode_quadtree emits it with map_form = 1), skipping the map build; workspace >= 64 bytes. */
+int mns_decode_unit_map_lattice(const uint16_t *block_map, int32_t width, int32_t height, int32_t iters,
                                 float initial_value, float *lat_ping, float *lat_pong, uint8_t *out, int32_t *d_error,
                                 void *workspace, int64_t workspace_bytes, void *stream);
 

@@ -57,7 +57,13 @@ MNS_REC_INLINE uint64_t mns_rec_phase2(int x, int y, int level, int o_byte, int 
  *   bits  4..13  luminance target + 32 (phase-2 targets span -31..286)
  *   bits 14..15  log2(unit side) - 1 (side 2, 4, 8, 16)
  * The unit's origin is the cell position rounded down to the side; its domain is
- * the co-centred one (image.py:174-187). */
+ * the co-centred one (image.py:174-187).
+ *
+ * Block map (lattice decoders): one uint16 per 4x4 block, 16 per root in Morton
+ * order, = the unit-map descriptor of the block's first cell.  A unit of side
+ * >= 4 is aligned to its side, so it covers whole blocks and the four cells of a
+ * block share its descriptor; a block holding 2x2 units carries side bits 0
+ * (the lattice decoders flag it). */
 MNS_REC_INLINE uint16_t mns_unit_desc(int s_index, int target, int side_log2) {
     return (uint16_t)((s_index & 15) | ((target + 32) << 4) | ((side_log2 - 1) << 14));
 }

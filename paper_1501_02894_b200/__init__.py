@@ -29,6 +29,7 @@ from .types import (  # noqa: F401
 )
 from .codec import (  # noqa: F401
     DeviceCode,
+    build_unit_map,
     co_domain_rect,
     decode,
     decode_device,

@@ -106,12 +106,13 @@ class DeviceCode:
     root_row_end: int = 0
     mode: str = "mns"
     technique2: bool = True
-    unit_map: "object" = None  # torch.int32 [n_roots * 32]: decoder unit map (mns_record.h), optional
+    unit_map: "object" = None  # torch.int32: decoder map (mns_record.h) in map_form, optional
     min_leaf: int = 0          # smallest painted unit side if known (4: no 2x2 units -> lattice-state decode), 0 unknown
     unit_map_valid: bool = False  # unit_map holds this code's map (emitted by the encoder / build_unit_map)
     compact_event: "object" = None  # set by encode_device(compact_stream=...): records/count valid after it
     decode_error: "object" = None   # set by decode_device on the lattice path (device int32 flag)
     n_iso: int = 1                  # 8: the isometry extension (phase-1 records carry an isometry)
+    map_form: int = 0               # unit_map holds 0: the unit map (32 words per root), 1: the block map (8)
 
     def join(self, stream=None) -> None:
         """Make `stream` (default: current) wait until records / root_offsets / count are complete
@@ -144,9 +145,13 @@ class _Workspace:
 _WS = _Workspace()
 
 
-def enc_cfg(config: EncoderConfig, root_level: int = 1, n_iso: int = 1) -> N.EncCfg:
+MAP_WORDS = (32, 8)  # int32 words per root of the unit map / the block map
+
+
+def enc_cfg(config: EncoderConfig, root_level: int = 1, n_iso: int = 1, map_form: int = 0) -> N.EncCfg:
     c = N.EncCfg()
     c.n_iso = int(n_iso)
+    c.map_form = int(map_form)
     c.e[0], c.e[1], c.e[2] = float(config.e1), float(config.e2), float(config.e3)
     c.mean_tol = float(config.mean_tol)
     c.mns = 1 if config.mode == "mns" else 0
@@ -156,13 +161,16 @@ def enc_cfg(config: EncoderConfig, root_level: int = 1, n_iso: int = 1) -> N.Enc
 
 def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows: Optional[tuple] = None,
                   height: Optional[int] = None, out: Optional[DeviceCode] = None, with_unit_map: bool = True,
-                  stream=None, compact_stream=None, n_iso: int = 1) -> DeviceCode:
+                  stream=None, compact_stream=None, n_iso: int = 1, map_form: Optional[int] = None) -> DeviceCode:
     """MNS quadtree encode of a padded uint8 CUDA tensor [H, W] or a batch [B, H, W].
 
     root_rows=(r0, r1) restricts the work to root rows [r0, r1) (strip sharding); then ``img``
     may be a halo'd slice and ``height`` gives the full image height (global clamping).
     n_iso=8 is the isometry extension (BASELINE configs[1]): phase 1 also tries the 8 isometries of
     the co-centred domain; such codes carry no decoder unit map and decode on the exact unit path.
+    map_form: the decoder map emitted beside the records -- 1, the block map of the lattice decoders
+    (default for e3 = inf, whose codes have no 2x2 units), or 0, the unit map (default otherwise);
+    with ``out`` given, its ``map_form``.
     """
     if n_iso not in (1, 8):
         raise ValueError("n_iso must be 1 or 8")
@@ -177,12 +185,20 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     r0, r1 = root_rows if root_rows is not None else (0, H // 16)
     n_roots = nb * (r1 - r0) * (w // 16)
     dev = img.device
+    if map_form is None:
+        map_form = out.map_form if out is not None else (1 if math.isinf(config.e3) and n_iso == 1 else 0)
+    if map_form not in (0, 1):
+        raise ValueError("map_form must be 0 (unit map) or 1 (block map)")
     if out is None:
         out = DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device=dev),
                          torch.empty(n_roots + 1, dtype=torch.int32, device=dev),
                          torch.zeros(1, dtype=torch.int64, device=dev), w, H, nb, r0, r1, config.mode,
                          config.technique2,
-                         torch.empty(32 * n_roots, dtype=torch.int32, device=dev) if with_unit_map else None)
+                         torch.empty(MAP_WORDS[map_form] * n_roots, dtype=torch.int32, device=dev)
+                         if with_unit_map else None)
+    if out.unit_map is not None and out.unit_map.numel() < MAP_WORDS[map_form] * n_roots:
+        raise ValueError("unit_map is too small for the requested map_form")
+    out.map_form = map_form
     wsb = N.out_i64(L, L.mns_encode_workspace_bytes, w, nb, r0, r1)
     ws = _WS.get("enc", wsb, dev)
     # `img` points at global row 0 even for halo'd strips: offset the base pointer back
@@ -194,7 +210,7 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     out.min_leaf = 4 if math.isinf(config.e3) else 0
     out.unit_map_valid = out.unit_map is not None and n_iso == 1
     out.n_iso = n_iso
-    cfg = enc_cfg(config, root_level, n_iso)
+    cfg = enc_cfg(config, root_level, n_iso, map_form)
     if compact_stream is None:
         N.check(L.mns_encode_quadtree(ctypes.c_void_p(base), w, H, img.stride(1), img.stride(0), nb, r0, r1,
                                       ctypes.byref(cfg), N.ptr(out.records), out.records.numel(),
@@ -213,16 +229,18 @@ def encode_device(img, config: EncoderConfig, *, root_level: int = 1, root_rows:
     return out
 
 
-def build_unit_map(code: DeviceCode, stream=None):
-    """Decoder unit map of a device code whose encoder did not emit one."""
+def build_unit_map(code: DeviceCode, stream=None, map_form: int = 0):
+    """Decoder map of a device code from its records (map_form 0: the unit map, 1: the block map)."""
     torch = _torch()
     L = N.lib()
     r0, r1 = code.root_row_begin, code.root_row_end or code.padded_h // 16
     n_roots = (code.padded_w // 16) * (r1 - r0)
-    code.unit_map = torch.empty(32 * n_roots, dtype=torch.int32, device=code.records.device)
+    code.unit_map = torch.empty(MAP_WORDS[map_form] * n_roots, dtype=torch.int32, device=code.records.device)
+    code.map_form = map_form
     code.join(stream)
-    N.check(L.mns_build_unit_map(N.ptr(code.records), N.ptr(code.root_offsets), code.padded_w, r0, r1,
-                                 N.ptr(code.unit_map), N.stream_ptr(stream)))
+    build = L.mns_build_block_map if map_form == 1 else L.mns_build_unit_map
+    N.check(build(N.ptr(code.records), N.ptr(code.root_offsets), code.padded_w, r0, r1, N.ptr(code.unit_map),
+                  N.stream_ptr(stream)))
     code.unit_map_valid = True
     return code.unit_map
 
@@ -270,8 +288,8 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
         lat = (rasters[0].view(-1)[:n_lat], rasters[1].view(-1)[:n_lat])
         whole = code.n_images == 1 and code.root_row_begin == 0 and code.root_row_end in (0, H // 16)
         code.decode_error = err  # 1 if a 2x2 unit was met (min_leaf wrong): rerun with lattice=False
-        if code.unit_map is not None and code.unit_map_valid and whole:
-            # the encoder's own unit map: no rebuild from the records
+        if code.unit_map is not None and code.unit_map_valid and code.map_form == 1 and whole:
+            # the encoder's own block map: no rebuild from the records
             N.check(L.mns_decode_unit_map_lattice(N.ptr(code.unit_map), W, H, int(iters), float(initial_value),
                                                   N.ptr(lat[0]), N.ptr(lat[1]), N.ptr(out), N.ptr(err), N.ptr(ws),
                                                   ws.numel(), N.stream_ptr(stream)))

@@ -100,18 +100,20 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
                     cudaStream_t stream, cudaStream_t cstream);
 int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1, uint32_t *unit_map,
                    cudaStream_t stream);
+int build_block_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1,
+                    uint16_t *block_map, cudaStream_t stream);
 int try_node(const uint8_t *img, int W, int H, int64_t pitch, int x, int y, int level, int phase,
              const mns_enc_cfg *cfg, uint64_t *d_rec, double *d_rms, cudaStream_t stream);
 int decode_workspace_bytes(int W, int H, int64_t *bytes);
-int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
+int decode_pass_lattice(const uint16_t *block_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
                         float init, float *nxt, uint8_t *out, int *err, cudaStream_t stream);
-int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
-                        cudaStream_t stream);
+int decode_flat_lattice(const uint16_t *block_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
+                        uint8_t *out, cudaStream_t stream);
 int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
                             float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
                             int64_t workspace_bytes, cudaStream_t stream);
-int decode_umap_lattice(const uint32_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
-                        uint8_t *out, int32_t *err, int *state, cudaStream_t stream);
+int decode_umap_lattice(const uint16_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
+                        uint8_t *out, int32_t *err, cudaStream_t stream);
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
@@ -234,6 +236,12 @@ int mns_build_unit_map(const uint64_t *records, const int32_t *root_offsets, int
                               (cudaStream_t)stream));
 }
 
+int mns_build_block_map(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t root_row_begin,
+                        int32_t root_row_end, uint16_t *block_map, void *stream) {
+    GUARD(mns::build_block_map(records, root_offsets, width, root_row_begin, root_row_end, block_map,
+                               (cudaStream_t)stream));
+}
+
 int mns_decode_workspace_bytes(int32_t width, int32_t height, int64_t *bytes) {
     GUARD(mns::decode_workspace_bytes(width, height, bytes));
 }
@@ -260,18 +268,18 @@ int mns_decode_sweep2(const uint32_t *unit_map, int32_t unit_map_row_begin, int3
                              initial_value, nxt, out, (cudaStream_t)stream));
 }
 
-int mns_decode_pass_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+int mns_decode_pass_lattice(const uint16_t *block_map, int32_t block_map_row_begin, int32_t width, int32_t height,
                             int32_t root_row_begin, int32_t root_row_end, const float *cur_lattice, float initial_value,
                             float *nxt_lattice, uint8_t *out, int32_t *d_error, void *stream) {
-    GUARD(mns::decode_pass_lattice(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end,
+    GUARD(mns::decode_pass_lattice(block_map, block_map_row_begin, width, height, root_row_begin, root_row_end,
                                    cur_lattice, initial_value, nxt_lattice, out, d_error, (cudaStream_t)stream));
 }
 
-int mns_decode_flat_lattice(const uint32_t *unit_map, int32_t unit_map_row_begin, int32_t width, int32_t height,
+int mns_decode_flat_lattice(const uint16_t *block_map, int32_t block_map_row_begin, int32_t width, int32_t height,
                             int32_t root_row_begin, int32_t root_row_end, float initial_value, float *nxt_lattice,
-                            void *stream) {
-    GUARD(mns::decode_flat_lattice(unit_map, unit_map_row_begin, width, height, root_row_begin, root_row_end,
-                                   initial_value, nxt_lattice, (cudaStream_t)stream));
+                            uint8_t *out, void *stream) {
+    GUARD(mns::decode_flat_lattice(block_map, block_map_row_begin, width, height, root_row_begin, root_row_end,
+                                   initial_value, nxt_lattice, out, (cudaStream_t)stream));
 }
 
 int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int32_t width, int32_t height,
@@ -281,15 +289,13 @@ int mns_decode_quadtree_lattice(const uint64_t *records, const int32_t *root_off
                                        out, d_error, workspace, workspace_bytes, (cudaStream_t)stream));
 }
 
-int mns_decode_unit_map_lattice(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters,
+int mns_decode_unit_map_lattice(const uint16_t *block_map, int32_t width, int32_t height, int32_t iters,
                                 float initial_value, float *lat_ping, float *lat_pong, uint8_t *out, int32_t *d_error,
                                 void *workspace, int64_t workspace_bytes, void *stream) {
-    if (workspace_bytes < 64) {
-        mns::set_error("invalid argument: %s", "workspace too small");
-        return -2;
-    }
-    GUARD(mns::decode_umap_lattice(unit_map, width, height, iters, initial_value, lat_ping, lat_pong, out, d_error,
-                                   reinterpret_cast<int *>(workspace), (cudaStream_t)stream));
+    (void)workspace;
+    (void)workspace_bytes;
+    GUARD(mns::decode_umap_lattice(block_map, width, height, iters, initial_value, lat_ping, lat_pong, out, d_error,
+                                   (cudaStream_t)stream));
 }
 
 int mns_decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

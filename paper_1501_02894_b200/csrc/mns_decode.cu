@@ -53,6 +53,7 @@ __constant__ float kUnitS[16] = {-0.875f, -0.625f, -0.375f, -0.125f, 0.125f, 0.3
 
 struct SweepParams {
     const uint32_t *unit_map;  // 32 words (64 cells) per root of the rows [rr0, rr1)
+    const uint16_t *block_map; // lattice passes: 16 block descriptors per root (mns_record.h)
     int W, H, rw, rr0, rr1, y_lo;
     const float *cur;    // null on the first sweep: the flat start raster (init) is implied
     float init;
@@ -749,12 +750,14 @@ __global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __
         const bool interior_col = rxi >= 1 && rxi + 1 < p.rw;
         constexpr int lag = A ? 0 : 2;
         const int row_lo = A ? max(r_s - 1, 0) : r_s, row_hi = A ? min(r_e + 1, rh) : r_e;
-        const uint2 *uptr = reinterpret_cast<const uint2 *>(p.unit_map) +
-                            ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 + (lane & 15) +
-                            (ptrdiff_t)(r_s - 1 - lag) * p.rw * 16;
+        // the block map: one descriptor per lane (its 4x4 block), replicated into the four cell
+        // slots paint_block reads
+        const uint16_t *uptr = p.block_map + ((ptrdiff_t)rxi - (ptrdiff_t)p.umap_r0 * p.rw) * 16 + (lane & 15) +
+                               (ptrdiff_t)(r_s - 1 - lag) * p.rw * 16;
         const ptrdiff_t ustride = (ptrdiff_t)p.rw * 16;
-        auto word_of = [&](int row, const uint2 *ptr) {
-            return col_ok && row >= row_lo && row < row_hi ? __ldg(ptr) : make_uint2(0u, 0u);
+        auto word_of = [&](int row, const uint16_t *ptr) {
+            const uint32_t d = col_ok && row >= row_lo && row < row_hi ? (uint32_t)__ldg(ptr) : 0u;
+            return make_uint2(d | (d << 16), d | (d << 16));
         };
         const int rxg = rxi * 16;
         const LaneTab tab = A ? lane_tab<LQS, LHB>(L, rc, 16) : lane_tab<LQBS, LQBH>(L, rc, 8);
@@ -815,40 +818,45 @@ __global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __
         run(std::false_type{});
 }
 
-// The first sweep from the flat raster straight into lattice form (an odd sweep count): every
-// unit paints the constant x = clip(s/4 * 4 init + (o - s init)) (paint_block's flat path), and
-// each 2x2 cell lies inside one unit, so its lattice entry is ((x + x) + x) + x.  One thread per
-// unit-map word (two cells).
-__global__ void flat_lattice_kernel(const uint32_t *unit_map, int umap_r0, int rw, int rr0, int rr1, float init,
-                                    float *nxt) {
-    const long long n = (long long)(rr1 - rr0) * rw * 32;
+// The first sweep from the flat raster (an odd sweep count) straight into lattice form, or, for a
+// one-sweep decode, into the uint8 image: every unit paints the constant x = clip(s/4 * 4 init +
+// (o - s init)) (paint_block's flat path), so a 4x4 block is one value, its four lattice entries
+// ((x + x) + x) + x and its pixels floor(x + 0.5).  One thread per block-map entry.
+__global__ void flat_lattice_kernel(const uint16_t *block_map, int umap_r0, int rw, int rr0, int rr1, float init,
+                                    float *nxt, uint8_t *out, int W) {
+    const long long n = (long long)(rr1 - rr0) * rw * 16;
     const int lw = rw * 8;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const long long root = i >> 5;
-        const int word = (int)(i & 31), ry = rr0 + (int)(root / rw), rx = (int)(root % rw);
-        const uint32_t w = unit_map[((long long)(ry - umap_r0) * rw + rx) * 32 + word];
+        const long long root = i >> 4;
+        const int l = (int)(i & 15), ry = rr0 + (int)(root / rw), rx = (int)(root % rw);
+        const uint32_t d = block_map[((long long)(ry - umap_r0) * rw + rx) * 16 + l];
+        const int bx = (l & 1) | ((l >> 1) & 2), by = ((l >> 1) & 1) | ((l >> 2) & 2);  // Morton -> block (x, y)
+        const float sc = kUnitS[d & 15];
+        const float x = fminf(255.f, fmaxf(0.f, fmaf(0.25f * sc, 4.f * init, fmaf(-sc, init, unit_o(d)))));
+        if (out) {
+            const uint32_t b = (uint32_t)floorf(x + 0.5f) * 0x01010101u;
+            uint8_t *o = out + (ptrdiff_t)(16 * ry + 4 * by) * W + 16 * rx + 4 * bx;
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const uint32_t d = h ? w >> 16 : w & 0xFFFFu;
-            const int m = 2 * word + h;
-            int cx = 0, cy = 0;
+            for (int r = 0; r < 4; r++) *reinterpret_cast<uint32_t *>(o + (ptrdiff_t)r * W) = b;
+        } else {
+            const float v = ((x + x) + x) + x;
+            const int gy = 8 * ry + 2 * by, gc = 4 * rx + bx;  // lattice row; column pair (2gc, 2gc + 1)
 #pragma unroll
-            for (int b = 0; b < 3; b++) {
-                cx |= ((m >> (2 * b)) & 1) << b;
-                cy |= ((m >> (2 * b + 1)) & 1) << b;
+            for (int r = 0; r < 2; r++) {
+                float *row = nxt + (ptrdiff_t)(gy + r) * lw;
+                row[gc] = v;
+                row[lw / 2 + gc] = v;
             }
-            const float sc = kUnitS[d & 15];
-            const float x = fminf(255.f, fmaxf(0.f, fmaf(0.25f * sc, 4.f * init, fmaf(-sc, init, unit_o(d)))));
-            const int gy = 8 * ry + cy, gx = 8 * rx + cx;
-            nxt[(ptrdiff_t)gy * lw + (gx & 1) * (lw / 2) + (gx >> 1)] = ((x + x) + x) + x;
         }
     }
 }
 
 // Unit map from records grouped by root (one warp per root): cells in smem, then one
 // coalesced 32-bit word (two cells) per lane.
+// BLOCKS: the block map instead (the descriptor of each 4x4 block's first cell, 16 per root).
+template <bool BLOCKS>
 __global__ void build_unit_map_kernel(const uint64_t *records, const int32_t *root_offsets, int rw, int rr0,
-                                      long long n_roots, uint32_t *unit_map) {
+                                      long long n_roots, void *map) {
     __shared__ uint16_t cells[8][64];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long root = (long long)blockIdx.x * 8 + warp;
@@ -863,7 +871,12 @@ __global__ void build_unit_map_kernel(const uint64_t *records, const int32_t *ro
                 cells[warp][morton_of(cx >> 1, cy >> 1)] = mns_unit_of_record(r, rxg, ryg, cx, cy);
     }
     __syncwarp();
-    unit_map[root * 32 + lane] = (uint32_t)cells[warp][2 * lane] | ((uint32_t)cells[warp][2 * lane + 1] << 16);
+    if (BLOCKS) {
+        if (lane < 16) static_cast<uint16_t *>(map)[root * 16 + lane] = cells[warp][4 * lane];
+    } else {
+        static_cast<uint32_t *>(map)[root * 32 + lane] =
+            (uint32_t)cells[warp][2 * lane] | ((uint32_t)cells[warp][2 * lane + 1] << 16);
+    }
 }
 
 // Per-sweep iteration counter when stop_delta == 0 (no early stop possible).
@@ -1007,8 +1020,18 @@ int build_unit_map(const uint64_t *records, const int32_t *root_offsets, int W, 
                    cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && W % 16 == 0 && 0 <= rr0 && rr0 < rr1, "bad unit-map geometry");
     const long long n_roots = (long long)(W / 16) * (rr1 - rr0);
-    build_unit_map_kernel<<<(unsigned)((n_roots + 7) / 8), 256, 0, stream>>>(records, root_offsets, W / 16, rr0,
-                                                                             n_roots, unit_map);
+    build_unit_map_kernel<false><<<(unsigned)((n_roots + 7) / 8), 256, 0, stream>>>(records, root_offsets, W / 16,
+                                                                                    rr0, n_roots, unit_map);
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int build_block_map(const uint64_t *records, const int32_t *root_offsets, int W, int rr0, int rr1,
+                    uint16_t *block_map, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && W % 16 == 0 && 0 <= rr0 && rr0 < rr1, "bad block-map geometry");
+    const long long n_roots = (long long)(W / 16) * (rr1 - rr0);
+    build_unit_map_kernel<true><<<(unsigned)((n_roots + 7) / 8), 256, 0, stream>>>(records, root_offsets, W / 16,
+                                                                                   rr0, n_roots, block_map);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -1110,17 +1133,17 @@ static int ensure_lat_attr() {
 // Two sweeps over root rows [rr0, rr1) on lattice state (see decode_pair_lat_kernel).  cur/nxt are
 // virtual-global lattice bases (lattice row 0); lattice rows [8 rr0 - 16, 8 rr1 + 16) of cur are
 // resident.  err (device int) is set to 1 if a 2x2 unit is met.
-int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
+int decode_pass_lattice(const uint16_t *block_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur,
                         float init, float *nxt, uint8_t *out, int *err, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
-    MNS_CHECK_ARG(umap_r0 <= (rr0 > 0 ? rr0 - 1 : 0) && umap_r0 >= 0, "unit map must start at root row rr0 - 1");
+    MNS_CHECK_ARG(umap_r0 <= (rr0 > 0 ? rr0 - 1 : 0) && umap_r0 >= 0, "block map must start at root row rr0 - 1");
     MNS_CHECK_ARG(H <= 65534, "height exceeds the record coordinate range");
     MNS_CHECK_ARG((nxt != nullptr) != (out != nullptr), "exactly one of nxt / out");
     MNS_CHECK_ARG(err != nullptr, "error flag required");
     if (ensure_lat_attr()) return -1;
     SweepParams p{};
-    p.unit_map = unit_map;
+    p.block_map = block_map;
     p.umap_r0 = umap_r0;
     p.W = W;
     p.H = H;
@@ -1155,35 +1178,33 @@ int decode_pass_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int
     return 0;
 }
 
-int decode_flat_lattice(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
-                        cudaStream_t stream) {
+int decode_flat_lattice(const uint16_t *block_map, int umap_r0, int W, int H, int rr0, int rr1, float init, float *nxt,
+                        uint8_t *out, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16 && 0 <= umap_r0 && umap_r0 <= rr0, "bad root row range");
-    const long long n = (long long)(rr1 - rr0) * (W / 16) * 32;
+    MNS_CHECK_ARG((nxt != nullptr) != (out != nullptr), "exactly one of nxt / out");
+    const long long n = (long long)(rr1 - rr0) * (W / 16) * 16;
     const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 8);
-    flat_lattice_kernel<<<blocks, 256, 0, stream>>>(unit_map, umap_r0, W / 16, rr0, rr1, init, nxt);
+    flat_lattice_kernel<<<blocks, 256, 0, stream>>>(block_map, umap_r0, W / 16, rr0, rr1, init, nxt, out, W);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
 
-// The whole lattice-state decode (codes without 2x2 units; stop_delta = 0, uint8 output) from a unit
+// The whole lattice-state decode (codes without 2x2 units; stop_delta = 0, uint8 output) from a block
 // map of all root rows (lat_ping / lat_pong: (H/2) x (W/2) floats each).  *err (device) = 1 if the code
-// had a 2x2 unit.  `state` (64 bytes of workspace) is used by a single-sweep decode only.
-int decode_umap_lattice(const uint32_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
-                        uint8_t *out, int32_t *err, int *state, cudaStream_t stream) {
+// had a 2x2 unit (a one-sweep decode paints blocks whole and does not look).
+int decode_umap_lattice(const uint16_t *umap, int W, int H, int iters, float init, float *lat_ping, float *lat_pong,
+                        uint8_t *out, int32_t *err, cudaStream_t stream) {
     MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
     MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
     MNS_CHECK_ARG(out != nullptr && err != nullptr, "out and err required");
     MNS_CUDA_TRY(cudaMemsetAsync(err, 0, 4, stream));
-    if (iters == 1) {
-        MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
-        return decode_sweep(umap, W, H, 0, H / 16, nullptr, init, nullptr, out, state, 0.0, stream);
-    }
+    if (iters == 1) return decode_flat_lattice(umap, 0, W, H, 0, H / 16, init, nullptr, out, stream);
     const float *cur = nullptr;
     int it = 0;
     int rc = 0;
     if (iters & 1) {
-        rc = decode_flat_lattice(umap, 0, W, H, 0, H / 16, init, lat_pong, stream);
+        rc = decode_flat_lattice(umap, 0, W, H, 0, H / 16, init, lat_pong, nullptr, stream);
         if (rc) return rc;
         cur = lat_pong;
         it = 1;
@@ -1198,7 +1219,7 @@ int decode_umap_lattice(const uint32_t *umap, int W, int H, int iters, float ini
     return 0;
 }
 
-// decode_quadtree for codes without 2x2 units, on lattice state: the unit map is built from the
+// decode_quadtree for codes without 2x2 units, on lattice state: the block map is built from the
 // records into the workspace, then decode_umap_lattice.
 int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters, float init,
                             float *lat_ping, float *lat_pong, uint8_t *out, int32_t *err, void *workspace,
@@ -1207,11 +1228,10 @@ int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets
     int64_t need;
     decode_workspace_bytes(W, H, &need);
     MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
-    int *state = reinterpret_cast<int *>(workspace);
-    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
-    const int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
+    uint16_t *bmap = reinterpret_cast<uint16_t *>(reinterpret_cast<char *>(workspace) + 256);
+    const int rc = build_block_map(records, root_offsets, W, 0, H / 16, bmap, stream);
     if (rc) return rc;
-    return decode_umap_lattice(umap, W, H, iters, init, lat_ping, lat_pong, out, err, state, stream);
+    return decode_umap_lattice(bmap, W, H, iters, init, lat_ping, lat_pong, out, err, stream);
 }
 
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,

@@ -56,7 +56,8 @@ struct EncParams {
     double mean_tol;
     int gate[4];    // phase-2 mean gate per level: |n * (O_k - O_i)| > gate  <=>  |O_k - O_i| > mean_tol
     uint64_t *stage;     // 64 record slots per root (workspace); compacted by compact_records_kernel
-    uint32_t *unit_map;  // optional: decoder unit map (mns_record.h), 32 words per root
+    uint32_t *unit_map;  // optional: decoder map (mns_record.h), 32 words per root (unit map) or 8 (block map)
+    int map_form;        // 0: unit map, 1: block map
     int32_t *root_cnt;   // per-root record counts (root_offsets, scanned in place by the compaction)
     long long n_roots;
 };
@@ -757,7 +758,10 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                     st[0] = cov;
                 }
                 if (m == 0) p.root_cnt[root] = __popc(b1) + 3 * __popc(b4);
-                if (p.unit_map) {
+                if (p.unit_map && p.map_form == 1) {  // block map: the descriptor of the block's first cell
+                    reinterpret_cast<uint16_t *>(p.unit_map)[root * 16 + m] =
+                        mns_unit_of_record(vis4 ? rec4[0] : cov, rxg, ryg, lx, ly);
+                } else if (p.unit_map) {
                     uint2 u;
                     if (vis4) {
                         u.x = (uint32_t)mns_unit_of_record(rec4[0], rxg, ryg, lx, ly) |
@@ -1041,6 +1045,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     MNS_CHECK_ARG(0 <= rr0 && rr0 < rr1 && rr1 <= H / 16, "bad root row range");
     MNS_CHECK_ARG(cfg && (cfg->root_level == 1 || cfg->root_level == 2), "root_level must be 1 or 2");
     MNS_CHECK_ARG(cfg->n_iso == 0 || cfg->n_iso == 1 || cfg->n_iso == 8, "n_iso must be 1 or 8");
+    MNS_CHECK_ARG(cfg->map_form == 0 || cfg->map_form == 1, "map_form must be 0 (unit map) or 1 (block map)");
     const int rw = W / 16;
     const long long n_roots = (long long)n_images * (rr1 - rr0) * rw;
     MNS_CHECK_ARG(capacity >= 64 * n_roots, "record capacity must be >= 64 * roots");
@@ -1076,6 +1081,7 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     unsigned long long *status = reinterpret_cast<unsigned long long *>(workspace);
     p.stage = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(workspace) + status_bytes);
     p.unit_map = unit_map;
+    p.map_form = cfg->map_form;
     p.root_cnt = root_offsets;
     p.n_roots = n_roots;
     MNS_CUDA_TRY(cudaMemsetAsync(status, 0, ctiles * 8, stream));

@@ -108,7 +108,8 @@ def unit_map_ops(umap, r0: int, r1: int, height: int, rank: int, world: int, gro
 def exchange_unit_map_rows(umap, r0: int, r1: int, height: int, rank: int, world: int, group=None) -> None:
     """Swap the boundary root rows of the decoder unit map with the neighbours (once per code).
 
-    ``umap`` is [u1 - u0, W/16 * 32] int32 (unit_map_rows); own rows are [r0 - u0, r1 - u0).
+    ``umap`` is [u1 - u0, W/16 * words] int32 (unit_map_rows; 32 words per root for the unit map, 8 for
+    the block map); own rows are [r0 - u0, r1 - u0).
     """
     run_ops(unit_map_ops(umap, r0, r1, height, rank, world, group))
 
@@ -171,11 +172,12 @@ class StripDecoder:
     """Jacobi decode of one rank's strip: strip-local code + fp32 halo'd ping/pong state.
 
     Sweeps run two per pass on state with DEC_HALO resident raster rows; the boundary rows are
-    exchanged once per pass, and the unit map carries one neighbour root row on each side.
+    exchanged once per pass, and the decoder map carries one neighbour root row on each side.
     ``code.unit_map`` is rebound to a view of that halo'd map, so an encoder writing into ``code``
     fills it in place.  Codes without 2x2 units (``code.min_leaf == 4``, e.g. e3 = inf) run on
     lattice state (mns_decode_pass_lattice: the even 2x2-sum lattice, a quarter of the raster's
-    bytes, identical output); ``lattice`` forces the choice.
+    bytes, identical output) from the block map (``code.map_form == 1``); the raster passes read
+    the unit map.  ``lattice`` forces the choice.
     """
 
     def __init__(self, code, height: int, width: int, r0: int, r1: int, rank: int = 0, world: int = 1,
@@ -194,15 +196,19 @@ class StripDecoder:
         self.out = torch.empty((16 * (r1 - r0), width), dtype=torch.uint8, device=dev)
         self.state = torch.zeros(4, dtype=torch.int32, device=dev)
         self.error = torch.zeros(1, dtype=torch.int32, device=dev)  # lattice mode: 1 if a 2x2 unit was met
-        if code.unit_map is None:
-            from .codec import build_unit_map
+        from .codec import MAP_WORDS, build_unit_map
 
-            build_unit_map(code)
+        form = 1 if self.lattice else 0
+        if code.unit_map is None or (code.map_form != form and code.unit_map_valid):
+            build_unit_map(code, map_form=form)
+        elif code.map_form != form:
+            raise ValueError(f"code.map_form {code.map_form} does not match the {'lattice' if form else 'raster'} "
+                             "decoder (set it before encoding into the code)")
         self.u0, self.u1 = unit_map_rows(r0, r1, height)
-        rw32 = (width // 16) * 32
-        self.umap = torch.zeros((self.u1 - self.u0, rw32), dtype=torch.int32, device=dev)
+        row_words = (width // 16) * MAP_WORDS[form]
+        self.umap = torch.zeros((self.u1 - self.u0, row_words), dtype=torch.int32, device=dev)
         own = self.umap[r0 - self.u0: r1 - self.u0]
-        own.copy_(code.unit_map.view(r1 - r0, rw32))
+        own.copy_(code.unit_map[: (r1 - r0) * row_words].view(r1 - r0, row_words))
         code.unit_map = own.view(-1)
         self._ops = {}
         self.overlap = True  # world > 1: boundary rows first, halo exchange beside the interior rows
@@ -251,9 +257,11 @@ class StripDecoder:
             last = iters == 1
             if sweep_events is not None:
                 sweep_events[n][0].record()
-            if self.lattice and not last:
+            if self.lattice:
                 N.check(L.mns_decode_flat_lattice(N.ptr(self.umap), self.u0, self.W, self.H, self.r0, self.r1,
-                                                  float(initial_value), self._state_base(self.pong), s))
+                                                  float(initial_value),
+                                                  ctypes.c_void_p(0) if last else self._state_base(self.pong),
+                                                  ob if last else ctypes.c_void_p(0), s))
             else:
                 N.check(L.mns_decode_sweep(N.ptr(self.code.unit_map), self.W, self.H, self.r0, self.r1,
                                            ctypes.c_void_p(0), float(initial_value),

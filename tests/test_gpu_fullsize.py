@@ -76,7 +76,7 @@ def test_c5_bench_path_decode_within_1lsb(mns, c5):
     code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device="cuda"),
                           torch.empty(n_roots + 1, dtype=torch.int32, device="cuda"),
                           torch.zeros(1, dtype=torch.int64, device="cuda"), W, H, 1, 0, H // 16,
-                          unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device="cuda"))
+                          unit_map=torch.empty(8 * n_roots, dtype=torch.int32, device="cuda"), map_form=1)
     dec = sharding.StripDecoder(code, H, W, 0, H // 16, 0, 1, lattice=True)
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())

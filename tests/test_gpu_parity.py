@@ -292,7 +292,7 @@ def test_pair_pass_equals_two_sweeps(mns, W, H, e3, rr):
     L = N.lib()
     side = max(W, H)
     px = np.ascontiguousarray(synth_image(side, 11, noise_sigma=12.0, n_blobs=8)[:H, :W])
-    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=e3))
+    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=e3), map_form=0)
     umap = code.unit_map
     rh = H // 16
     r0, r1 = rr if rr is not None else (0, rh)
@@ -450,7 +450,9 @@ def _lattice_of(t):
 def test_lattice_pass_equals_two_sweeps(mns, W, H, rr):
     """mns_decode_pass_lattice on a code without 2x2 units (e3 = inf): from the flat start and from
     a random raster's lattice, its t+2 lattice equals the lattice of two single raster sweeps and
-    its uint8 output their rounding, bit for bit; mns_decode_flat_lattice equals one flat sweep."""
+    its uint8 output their rounding, bit for bit; mns_decode_flat_lattice equals one flat sweep (as
+    lattice and as the uint8 image).  The lattice passes read the encoder's block map, which equals
+    mns_build_block_map's."""
     import ctypes
 
     from paper_1501_02894_b200 import _native as N
@@ -459,13 +461,18 @@ def test_lattice_pass_equals_two_sweeps(mns, W, H, rr):
     L = N.lib()
     side = max(W, H)
     px = np.ascontiguousarray(synth_image(side, 13, noise_sigma=12.0, n_blobs=8)[:H, :W])
-    code = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e3=math.inf))
+    img = torch.from_numpy(px).cuda()
+    code = mns.encode_device(img, mns.EncoderConfig(e3=math.inf), map_form=0)
     assert code.min_leaf == 4
-    umap = code.unit_map
+    umap = code.unit_map  # the raster sweeps' unit map
+    bcode = mns.encode_device(img, mns.EncoderConfig(e3=math.inf))
+    assert bcode.map_form == 1 and bcode.unit_map.numel() == (H // 16) * (W // 16) * 8
+    bmap = bcode.unit_map.clone()
+    assert torch.equal(mns.build_unit_map(bcode, map_form=1), bmap)
     rh = H // 16
     r0, r1 = rr if rr is not None else (0, rh)
     u0 = max(0, r0 - 1)
-    sub = umap[u0 * (W // 16) * 32:]
+    sub = bmap[u0 * (W // 16) * 8:]
     g = torch.Generator(device="cuda").manual_seed(W + H + 1)
     t0 = torch.rand((H, W), device="cuda", generator=g) * 255.0
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -486,9 +493,12 @@ def test_lattice_pass_equals_two_sweeps(mns, W, H, rr):
         assert torch.equal(out[16 * r0:16 * r1], torch.floor(want[16 * r0:16 * r1] + 0.5).to(torch.uint8))
     one = _sweeps_single(N, L, umap, W, H, (0, rh), None, 128.0, 1)
     flat = torch.full((H // 2, W // 2), float("nan"), device="cuda")
-    N.check(L.mns_decode_flat_lattice(N.ptr(sub), u0, W, H, r0, r1, 128.0, N.ptr(flat), None))
+    N.check(L.mns_decode_flat_lattice(N.ptr(sub), u0, W, H, r0, r1, 128.0, N.ptr(flat), None, None))
+    flat_u8 = torch.zeros((H, W), dtype=torch.uint8, device="cuda")
+    N.check(L.mns_decode_flat_lattice(N.ptr(sub), u0, W, H, r0, r1, 128.0, None, N.ptr(flat_u8), None))
     torch.cuda.synchronize()
     assert torch.equal(flat[ly0:ly1], _lattice_of(one)[ly0:ly1])
+    assert torch.equal(flat_u8[16 * r0:16 * r1], torch.floor(one[16 * r0:16 * r1] + 0.5).to(torch.uint8))
     assert int(err.item()) == 0
 
 
@@ -598,7 +608,7 @@ def test_strip_decoder_lattice_matches_whole_decode(mns, iters):
             ob = d._vbase(d.out, 16 * d.r0, 1)
             if n == 0 and iters & 1:
                 N.check(L.mns_decode_flat_lattice(N.ptr(d.umap), d.u0, W, H, d.r0, d.r1, 128.0, d._state_base(nxt),
-                                                  None))
+                                                  None, None))
             else:
                 N.check(L.mns_decode_pass_lattice(N.ptr(d.umap), d.u0, W, H, d.r0, d.r1, d._state_base(curs[i]),
                                                   128.0, d._state_base(nxt), ob if last else ctypes.c_void_p(0),

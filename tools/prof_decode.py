@@ -17,7 +17,7 @@ n_roots = (H // 16) * (W // 16)
 code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device="cuda"),
                       torch.empty(n_roots + 1, dtype=torch.int32, device="cuda"),
                       torch.zeros(1, dtype=torch.int64, device="cuda"), W, H, 1, 0, H // 16,
-                      unit_map=torch.empty(32 * n_roots, dtype=torch.int32, device="cuda"))
+                      unit_map=torch.empty(8 * n_roots, dtype=torch.int32, device="cuda"), map_form=1)
 dec = sharding.StripDecoder(code, H, W, 0, H // 16, 0, 1, lattice=True)
 mns.encode_device(img, mns.EncoderConfig(e3=math.inf), root_rows=(0, H // 16), height=H, out=code)
 for _ in range(3):
