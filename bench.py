@@ -693,12 +693,11 @@ def run_ours(args, img_np, rank, world, local_rank):
                      "traffic": measured_traffic(kname) if world == 1 else None,
                      "algorithmic_bytes": algo, "kernel": f"{kname} (steady-state pass = 2 sweeps)",
                      "peak_source": which,
-                     "limiter": ("instruction issue (ncu: ~79% issue-active at 2 B/px of DRAM traffic; "
-                                 "profiles/r1/ncu_step_lattice.txt)") if dec.lattice else "latency",
-                     # the same pass against SURVEY 8(d)'s raster-state formula (8 B/px per sweep: fp32 raster
-                     # read + written), i.e. what a raster-state decoder at this speed would have to move
-                     "raster_equivalent": {"bytes": 2 * 8 * own_px, "achieved": 2 * 8 * own_px / (pass_ms / 1e3) / 1e9,
-                                           "frac": 2 * 8 * own_px / (pass_ms / 1e3) / 1e9 / hbm}},
+                     "limiter": ("instruction issue (ncu: ~77% issue slots busy, DRAM ~1.02x the algorithmic "
+                                 "bytes; profiles/r2/ncu_dec_r2_blockmap.txt)") if dec.lattice else "latency",
+                     # informational, NOT a roofline fraction: the bytes SURVEY 8(d)'s raster-state formula
+                     # (8 B/px per sweep) would move at this speed; the lattice state moves 2 B/px per pass
+                     "raster_equivalent_gbs": 2 * 8 * own_px / (pass_ms / 1e3) / 1e9},
         "cpu_baseline": ({"value": cpu_v, "unit": "blocks/s", "cores": O.default_threads(), "kind": "port",
                           "sample": f"c5 rows 0..{args.cpu_baseline_rows - 1} encoded + {ITERS}-sweep decoded as its own "
                                     f"image by the fp64 oracle ({cpu_dt:.2f} s)"} if cpu_v else None),
