@@ -229,6 +229,33 @@ def python_reference_timings():
              ("c1_e3_inf", config_image("c1"), M.EncoderConfig(e3=math.inf), 8),
              ("c2", config_image("c2"), M.EncoderConfig(), 10),
              ("c5_window_512", config_image("c5")[:512, :512].copy(), M.EncoderConfig(e3=math.inf), 10))
+    from paper_1501_02894_b200.synth import batch_seeds, synth_image
+
+    # c3: encode only (the reference has no 8->4 root level: its 16->8->4 with e3 = inf), a 4-image
+    # subset, extrapolated per block
+    t_c3 = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for sd in batch_seeds(4):
+            M.encode_quadtree(M.GrayImage(synth_image(512, sd)), M.EncoderConfig(e3=math.inf))
+        t_c3.append(time.perf_counter() - t0)
+    out["c3_subset_4_images"] = {"encode_s": min(t_c3), "blocks_per_s": 4 * 4096 / min(t_c3),
+                                 "extrapolated_256_images_s": 64 * min(t_c3)}
+    # c4 searches on a 128^2 crop of the c4 image (the full 512^2 full search takes about a minute
+    # on one core): full search B = 8 stride 1 (256 ranges x 113^2 domains) and the +-4 local search
+    c4 = M.GrayImage(config_image("c4")[:128, :128].copy())
+    t_fs, t_ls = [], []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        M.encode_full_search(c4, 8, M.EncoderConfig(mode="full_search"))
+        t_fs.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        M.encode_local_search(c4, M.EncoderConfig())
+        t_ls.append(time.perf_counter() - t0)
+    out["c4_full_search_crop_128"] = {"s": min(t_fs), "pair_evals": 256 * 113 * 113,
+                                      "pair_evals_per_s": 256 * 113 * 113 / min(t_fs)}
+    out["c4_local_search_crop_128"] = {"s": min(t_ls), "candidate_fits": 256 * 81,
+                                       "candidate_fits_per_s": 256 * 81 / min(t_ls)}
     for name, px, cfg, iters in cases:
         img = M.GrayImage(px)
         enc, dec = [], []
