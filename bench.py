@@ -303,6 +303,76 @@ def run_reference(args, img):
 
 # ------------------------------------------------------------------------- GPU leg
 
+def _med_ms(fn, reps=5, warm=2):
+    """Median device time (CUDA events on the current stream) of fn() over reps calls."""
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def next_rows_components(dev, code, W, H, r0, r1):
+    """SURVEY 8(f), measured beside the path (rank 0, informational): the GPU .mns packer and the GPU
+    stream reader on rank 0's c5 code (round trip checked bit-exact), the device RD sweep on c2 and
+    the offset histogram on c4 (full search + counting)."""
+    import torch
+
+    import paper_1501_02894_b200 as mns
+    from paper_1501_02894_b200 import rd
+    from paper_1501_02894_b200.synth import config_image
+
+    out = {}
+    n = code.n_records()
+    h = 16 * (r1 - r0)
+    rec = code.records[:n]
+    packed, bits_t = mns.write_stream_device(rec, n, W, h, W, h, True, True)
+    nbytes = (int(bits_t.item()) + 7) // 8
+    w_ms = _med_ms(lambda: mns.write_stream_device(rec, n, W, h, W, h, True, True))
+    buf = packed[:nbytes].clone()
+    from paper_1501_02894_b200.codec import read_stream_device
+
+    back, status = read_stream_device(buf, True, True, W, h)
+    ok = int(status[0].item()) == -1 and back.n_records() == n and bool(torch.equal(back.records[:n], rec))
+    r_ms = _med_ms(lambda: read_stream_device(buf, True, True, W, h))
+    out["mns_stream"] = {"code": f"c5 rank-0 strip ({W}x{h}), {n} leaves, {nbytes} bytes .mns",
+                         "write_ms": w_ms, "write_leaves_per_s": n / (w_ms / 1e3),
+                         "write_gbs": (8 * n + nbytes) / (w_ms / 1e3) / 1e9,
+                         "read_ms": r_ms, "read_leaves_per_s": n / (r_ms / 1e3),
+                         "read_gbs": (nbytes + 8 * n) / (r_ms / 1e3) / 1e9,
+                         "roundtrip": "bit-exact" if ok else "MISMATCH",
+                         "note": "write: records (8 B/leaf) in, .mns out; read: .mns in, records out"}
+    c2 = config_image("c2")
+    grid = (2.0, 4.0, 8.0, 16.0, 32.0)
+    rd.rd_sweep(c2, ["mns"], grid[:1])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pts = rd.rd_sweep(c2, ["mns", "no_search"], grid)
+    dt = time.perf_counter() - t0
+    out["rd_sweep"] = {"config": "c2 512^2, modes mns + no_search x E in {2, 4, 8, 16, 32}, default decode",
+                       "points": len(pts), "s": dt, "ms_per_point": 1e3 * dt / len(pts),
+                       "note": "host wall clock per point (encode, .mns bit count, decode, SSE on the device)"}
+    c4 = config_image("c4")
+    rd.offset_histogram_device(c4)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        rd.offset_histogram_device(c4)
+    torch.cuda.synchronize()
+    out["offset_histogram"] = {"config": "c4 512^2, B = 8 stride 1, identity", "ms": 1e3 * (time.perf_counter() - t0) / 3,
+                               "note": "host wall clock: H2D of the image, full search, histogram, D2H"}
+    return out
+
+
 def small_configs(dev, rank, world):
     """BASELINE configs 1-3: c1/c2 are latency-bound single images -- one encode +
     decode step captured in a CUDA graph and replayed 1000 times back to back (rank 0); c3 is the
@@ -640,6 +710,7 @@ def run_ours(args, img_np, rank, world, local_rank):
                 "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3)}
 
     small = None if args.no_small else small_configs(dev, rank, world)
+    next_rows = None if (args.no_small or rank != 0) else next_rows_components(dev, code, W, H, r0, r1)
 
     # config c4 as SURVEY 8(e) shards it: ranges split across ranks (pool replicated, no data-path
     # collective), then the all-gather of the 8-byte per-range results; max over ranks
@@ -715,7 +786,8 @@ def run_ours(args, img_np, rank, world, local_rank):
                        "sweep_ms_effective": pass_ms / 2,
                        "leaves_rank0": n_leaves, "full_search": fs, "c4_range_split": c4_split,
                        "small_configs": small,
-                       "with_code_gather": gather},
+                       "with_code_gather": gather,
+                       "next_rows": next_rows},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": measured_traffic(kname) if world == 1 else None,
                      "algorithmic_bytes": algo, "kernel": f"{kname} (steady-state pass = 2 sweeps)",
