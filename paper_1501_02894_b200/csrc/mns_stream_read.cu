@@ -9,11 +9,11 @@
 //    only occurs as a split level-3 node's first child, bitstream.py:249-256).  So a token --
 //    one level-1..3 leaf, or a level-4 quartet -- has a width that is a function of the bits
 //    at its start: 2 + [phase bit] + payload, or 46 (Technique 2) / 52 bits for a quartet.
-//  * chunks of CHUNK bits are walked token by token from their own start in parallel,
-//    marking token starts in a bitmap; then, round after round, a chunk whose true entry (the
-//    previous chunk's exit) differs from the start it walked from re-walks from the entry
-//    until it lands on a start its old walk marked (the walks merge; the rest is shared) or
-//    leaves the chunk with a new exit.  Rounds stop when no exit changes.
+//  * chunks of CHUNK bits: the walk through a chunk maps its entry offset (< 52, the widest
+//    token) to the next chunk's; every chunk tabulates that map for all 52 offsets, the maps
+//    compose over groups and supergroups of 64, the true entries resolve top-down from the
+//    stream start, and one walk per chunk marks the token starts in a bitmap (exit_table_kernel
+//    .. mark_kernel).
 //  * the token starts are compacted; exclusive scans of token areas (in 2x2 cells: 64, 16, 4,
 //    4 for a quartet) and leaf counts give every leaf its root, Morton cell and record slot.
 //  * every check the sequential parser makes (level id below the node's level, interrupted
@@ -75,69 +75,126 @@ struct RP {
     long long nbytes, nbits, nchunks;
     int mns, t2;
     unsigned long long *bitmap;  // token starts, bit (p - HDR)
+    uint64_t wtab;               // tok_width by the token's top three bits, 6 bits per entry
 };
 
-__device__ __forceinline__ bool marked(const RP &r, long long p) {
-    const long long i = p - HDR;
-    return (r.bitmap[i >> 6] >> (i & 63)) & 1;
+// the same widths as one table lookup: width = (wtab >> 6 * top3) & 63
+static uint64_t width_table(int mns, int t2) {
+    uint64_t t = 0;
+    for (int i = 0; i < 8; i++) {
+        const uint64_t w = (uint64_t)i << 61;
+        const int lid = (int)(w >> 62), ph = mns ? (int)((w >> 61) & 1) : 0;
+        const int width = lid == 3 ? (t2 ? 46 : 52) : 2 + mns + (ph ? (lid == 0 ? 27 : 30) : 11);
+        t |= (uint64_t)width << (6 * i);
+    }
+    return t;
 }
-__device__ __forceinline__ void set_mark(const RP &r, long long p) {
-    const long long i = p - HDR;
-    r.bitmap[i >> 6] |= 1ull << (i & 63);
-}
+__device__ __forceinline__ int tok_w(uint64_t w, uint64_t wtab) { return (int)((wtab >> (6 * (int)(w >> 61))) & 63); }
 
-__global__ void spec_walk_kernel(const RP r, long long *exits, long long *starts) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= r.nchunks) return;
-    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
-    long long p = c0;
-    while (p < c1) {
-        set_mark(r, p);
-        p += tok_width(peek64(r.data, r.nbytes, p), r.mns, r.t2);
-    }
-    exits[t] = p;
-    starts[t] = c0;
-}
+// Token synchronisation by exit tables.  A token is at most 52 bits wide, so the first token start
+// at or after a chunk's first bit lies within 52 bits of it: the walk through chunk t is a function
+// f_t of its entry offset (0..51) onto the next chunk's entry offset.  Every chunk tabulates f_t
+// (one lane per entry offset, 52 walks in lockstep over the same bytes), the tables compose in a
+// three-level hierarchy (64 chunks per group, 64 groups per supergroup; each level a chain of
+// table lookups per possible entry), the true entries resolve top-down from offset 0 at the
+// stream start, and a last walk per chunk marks the true token starts.  No host round trips, and
+// the work does not depend on how slowly a misaligned walk re-synchronises.
+constexpr int NE = 64;      // table row (entries 0..51 used)
+constexpr int MAXW = 52;    // widest token (bits)
+constexpr int TG = 64;      // chunks per group, groups per supergroup
 
-__global__ void resync_kernel(const RP r, const long long *exit_in, long long *exit_out, long long *starts,
-                              int *changed) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= r.nchunks) return;
-    if (t == 0) {
-        exit_out[0] = exit_in[0];
-        return;
+// Sequential MSB-first reader for one walk: three big-endian stream words in registers (the one
+// holding the cursor, the next, and one prefetched), so a token costs no load until the walk
+// crosses a word, and that load was issued two words earlier.
+struct Cursor {
+    const uint8_t *d;
+    long long nbytes, k;  // k: word index (8-byte units) of w0
+    uint64_t w0, w1, w2;
+    __device__ __forceinline__ uint64_t word(long long i) const {
+        const long long a = 8 * i;
+        if (a + 8 <= nbytes) return bswap64(__ldg(reinterpret_cast<const unsigned long long *>(d + a)));
+        uint64_t v = 0;
+        for (int b = 0; b < 8; b++) v = (v << 8) | (uint64_t)(a + b < nbytes ? __ldg(d + a + b) : 0);
+        return v;
     }
-    const long long e = exit_in[t - 1];
-    if (e == starts[t]) {
-        exit_out[t] = exit_in[t];
-        return;
+    __device__ __forceinline__ Cursor(const uint8_t *data, long long nb, long long p) : d(data), nbytes(nb) {
+        k = p >> 6;
+        w0 = word(k);
+        w1 = word(k + 1);
+        w2 = word(k + 2);
     }
-    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
-    long long p = e;
-    bool merged = false;
-    while (p < c1) {
-        if (marked(r, p)) {
-            merged = true;
-            break;
+    // 64 bits from p (p >= 64 k, moving forward by less than 64 bits per call)
+    __device__ __forceinline__ uint64_t peek(long long p) {
+        if ((p >> 6) != k) {
+            k++;
+            w0 = w1;
+            w1 = w2;
+            w2 = word(k + 2);
         }
-        p += tok_width(peek64(r.data, r.nbytes, p), r.mns, r.t2);
+        const int off = (int)(p & 63);
+        return off ? (w0 << off) | (w1 >> (64 - off)) : w0;
     }
-    // rewrite this chunk's marks before the merge point: clear, then mark the walk from e
-    const long long stop = min(p, c1);
-    for (long long q = c0; q < stop;) {
-        const long long i = q - HDR, wi = i >> 6;
-        const int b = (int)(i & 63), n = (int)min(64ll - b, stop - q);
-        const unsigned long long m = n == 64 ? ~0ull : (((1ull << n) - 1) << b);
-        r.bitmap[wi] &= ~m;
-        q += n;
+};
+
+// f_t: tab[t * NE + j] = (first token start at or after c1) - c1 for the walk from c0 + j
+__global__ void __launch_bounds__(256) exit_table_kernel(const RP r, uint8_t *tab) {
+    const long long t = blockIdx.x * 4ll + (threadIdx.x >> 6);
+    const int j = threadIdx.x & 63;
+    if (t >= r.nchunks || j >= MAXW) return;
+    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
+    long long p = c0 + j;
+    Cursor cur(r.data, r.nbytes, p);
+    while (p < c1) p += tok_w(cur.peek(p), r.wtab);
+    tab[t * NE + j] = (uint8_t)(p - c1);
+}
+
+// one level up: out[g * NE + j] = the composition of in's rows [g * TG, g * TG + TG) from entry j
+__global__ void __launch_bounds__(256) compose_kernel(const uint8_t *in, long long nrows, uint8_t *out,
+                                                      long long ngroups) {
+    const long long g = blockIdx.x * 4ll + (threadIdx.x >> 6);
+    const int j = threadIdx.x & 63;
+    if (g >= ngroups || j >= MAXW) return;
+    int e = j;
+    const long long t1 = min((g + 1) * TG, nrows);
+    for (long long t = g * TG; t < t1; t++) e = in[t * NE + e];
+    out[g * NE + j] = (uint8_t)e;
+}
+
+// entries top-down: ent[g] for every row of a level from the level above (one thread per parent
+// row, a chain of TG lookups); the root level starts from offset 0 (the stream's first leaf)
+__global__ void resolve_kernel(const uint8_t *tab, long long nrows, const int *parent_ent, long long nparents,
+                               int *ent) {
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= nparents) return;
+    int e = parent_ent ? parent_ent[q] : 0;
+    const long long t1 = min((q + 1) * TG, nrows);
+    for (long long t = q * TG; t < t1; t++) {
+        ent[t] = e;
+        e = tab[t * NE + e];
     }
-    for (long long q = e; q < stop;) {
-        set_mark(r, q);
-        q += tok_width(peek64(r.data, r.nbytes, q), r.mns, r.t2);
+}
+
+// the true token starts of chunk t: the walk from its resolved entry, marks accumulated per bitmap
+// word in a register and each word stored once (a chunk's words are its own: chunks are word
+// aligned; words without a start stay zero from the memset)
+__global__ void mark_kernel(const RP r, const int *ent) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= r.nchunks) return;
+    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
+    long long p = c0 + ent[t], cw = (c0 - HDR) >> 6;
+    unsigned long long acc = 0;
+    Cursor cur(r.data, r.nbytes, p);
+    while (p < c1) {
+        const long long i = p - HDR;
+        if ((i >> 6) != cw) {
+            r.bitmap[cw] = acc;
+            cw = i >> 6;
+            acc = 0;
+        }
+        acc |= 1ull << (i & 63);
+        p += tok_w(cur.peek(p), r.wtab);
     }
-    starts[t] = e;
-    exit_out[t] = merged ? exit_in[t] : p;
-    if (!merged && p != exit_in[t]) atomicAdd(changed, 1);
+    if (acc) r.bitmap[cw] = acc;
 }
 
 // exclusive scan of n int64 (decoupled look-back over STILE-element tiles); total -> *total
@@ -318,8 +375,9 @@ unsigned grid_for(long long n, int threads) {
 
 struct ReadWs {
     unsigned long long *bitmap, *status;
-    long long *exit_a, *exit_b, *starts, *wcnt, *wbase, *tokpos, *area, *nleaf, *cell0, *leaf0, *totals;
-    int *changed;
+    long long *wcnt, *wbase, *tokpos, *area, *nleaf, *cell0, *leaf0, *totals;
+    uint8_t *tab, *gtab, *sgtab;  // exit tables: chunks, groups, supergroups (NE bytes per row)
+    int *ent_c, *ent_g, *ent_s;   // resolved entry offsets per level
     long long nwords, nchunks, maxtok, scan_tiles;
 };
 
@@ -337,9 +395,13 @@ long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     ReadWs t{};
     t.bitmap = (unsigned long long *)take(nwords * 8);
     t.status = (unsigned long long *)take(scan_tiles * 8);
-    t.exit_a = (long long *)take(nchunks * 8);
-    t.exit_b = (long long *)take(nchunks * 8);
-    t.starts = (long long *)take(nchunks * 8);
+    const long long ngroups = (nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
+    t.tab = (uint8_t *)take(nchunks * NE);
+    t.gtab = (uint8_t *)take(ngroups * NE);
+    t.sgtab = (uint8_t *)take(nsg * NE);
+    t.ent_c = (int *)take(nchunks * 4);
+    t.ent_g = (int *)take(ngroups * 4);
+    t.ent_s = (int *)take(nsg * 4);
     t.wcnt = (long long *)take(nwords * 8);
     t.wbase = (long long *)take(nwords * 8);
     t.tokpos = (long long *)take(maxtok * 8);
@@ -348,7 +410,6 @@ long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     t.cell0 = (long long *)take(maxtok * 8);
     t.leaf0 = (long long *)take(maxtok * 8);
     t.totals = (long long *)take(4 * 8);
-    t.changed = (int *)take(8);
     t.nwords = nwords;
     t.nchunks = nchunks;
     t.maxtok = maxtok;
@@ -387,7 +448,7 @@ int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, in
     MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
     ReadWs w;
     read_ws_layout(nbytes, &w, reinterpret_cast<char *>(workspace));
-    RP r{data, nbytes, nbytes * 8, 0, mns ? 1 : 0, t2 ? 1 : 0, w.bitmap};
+    RP r{data, nbytes, nbytes * 8, 0, mns ? 1 : 0, t2 ? 1 : 0, w.bitmap, width_table(mns ? 1 : 0, t2 ? 1 : 0)};
     const long long body = r.nbits - HDR;
     r.nchunks = (body + CHUNK - 1) / CHUNK;
     const long long n_roots = (long long)(pw / 16) * (ph / 16);
@@ -398,19 +459,16 @@ int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, in
     MNS_CUDA_TRY(cudaMemsetAsync(w.bitmap, 0, w.nwords * 8, s));
     long long ntok = 0;
     if (r.nchunks > 0) {
-        spec_walk_kernel<<<grid_for(r.nchunks, 128), 128, 0, s>>>(r, w.exit_a, w.starts);
+        const long long ngroups = (r.nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
+        MNS_CHECK_ARG(nsg <= TG, "stream longer than the reader's three table levels (268 MB)");
+        exit_table_kernel<<<(unsigned)((r.nchunks + 3) / 4), 256, 0, s>>>(r, w.tab);
+        compose_kernel<<<(unsigned)((ngroups + 3) / 4), 256, 0, s>>>(w.tab, r.nchunks, w.gtab, ngroups);
+        compose_kernel<<<(unsigned)((nsg + 3) / 4), 256, 0, s>>>(w.gtab, ngroups, w.sgtab, nsg);
+        resolve_kernel<<<1, 32, 0, s>>>(w.sgtab, nsg, nullptr, 1, w.ent_s);  // from offset 0 (needs nsg <= 64)
+        resolve_kernel<<<grid_for(nsg, 64), 64, 0, s>>>(w.gtab, ngroups, w.ent_s, nsg, w.ent_g);
+        resolve_kernel<<<grid_for(ngroups, 64), 64, 0, s>>>(w.tab, r.nchunks, w.ent_g, ngroups, w.ent_c);
+        mark_kernel<<<grid_for(r.nchunks, 64), 64, 0, s>>>(r, w.ent_c);
         MNS_CUDA_TRY(cudaGetLastError());
-        long long *ein = w.exit_a, *eout = w.exit_b;
-        for (int round = 0; round < 100000; round++) {  // bounded: each round fixes at least one chunk
-            MNS_CUDA_TRY(cudaMemsetAsync(w.changed, 0, 4, s));
-            resync_kernel<<<grid_for(r.nchunks, 128), 128, 0, s>>>(r, ein, eout, w.starts, w.changed);
-            MNS_CUDA_TRY(cudaGetLastError());
-            int changed = 0;
-            MNS_CUDA_TRY(cudaMemcpyAsync(&changed, w.changed, 4, cudaMemcpyDeviceToHost, s));
-            MNS_CUDA_TRY(cudaStreamSynchronize(s));
-            std::swap(ein, eout);
-            if (!changed) break;
-        }
         // token list
         const long long nwords = (body + 63) / 64;
         popc_kernel<<<grid_for(nwords, 256), 256, 0, s>>>(w.bitmap, nwords, w.wcnt);
