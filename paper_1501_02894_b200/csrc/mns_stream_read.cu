@@ -10,7 +10,8 @@
 //    one level-1..3 leaf, or a level-4 quartet -- has a width that is a function of the bits
 //    at its start: 2 + [phase bit] + payload, or 46 (Technique 2) / 52 bits for a quartet.
 //  * chunks of CHUNK bits: the walk through a chunk maps its entry offset (< 52, the widest
-//    token) to the next chunk's; every chunk tabulates that map for all 52 offsets, the maps
+//    token) to the next chunk's; every chunk tabulates that map for all 52 offsets (walks that
+//    meet past a probe point share the rest), the maps
 //    compose over groups and supergroups of 64, the true entries resolve top-down from the
 //    stream start, and one walk per chunk marks the token starts in a bitmap (exit_table_kernel
 //    .. mark_kernel).
@@ -28,7 +29,10 @@ namespace mns {
 namespace {
 
 constexpr long long HDR = 13 * 8;
-constexpr int CHUNK = 8192;  // bits per speculative chunk (128 bitmap words)
+#ifndef RD_CHUNK
+#define RD_CHUNK 8192
+#endif
+constexpr int CHUNK = RD_CHUNK;  // bits per chunk (CHUNK / 64 bitmap words)
 constexpr int ST = 256, SIPT = 8, STILE = ST * SIPT;
 
 enum { E_LEVEL = 1, E_SIBLING = 2, E_NEGZERO = 3, E_TRUNC = 4 };
@@ -136,16 +140,65 @@ struct Cursor {
     }
 };
 
-// f_t: tab[t * NE + j] = (first token start at or after c1) - c1 for the walk from c0 + j
-__global__ void __launch_bounds__(256) exit_table_kernel(const RP r, uint8_t *tab) {
-    const long long t = blockIdx.x * 4ll + (threadIdx.x >> 6);
-    const int j = threadIdx.x & 63;
-    if (t >= r.nchunks || j >= MAXW) return;
-    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
+// f_t: tab[t * NE + j] = (first token start at or after c1) - c1 for the walk from c0 + j.  Walks from
+// nearby offsets land on common token starts after a few tokens, so the 52 walks of a chunk run in
+// lockstep only to the probe point c0 + PROBE; walks whose first start past it coincide share the
+// rest, and only one walk per distinct start goes on (exit_finish_kernel, one thread per distinct
+// start), the others copy its exit (exit_copy_kernel).
+#ifndef RD_PROBE
+#define RD_PROBE 256
+#endif
+constexpr int PROBE = RD_PROBE;  // bits walked by all 52 offsets
+
+__global__ void __launch_bounds__(256) exit_probe_kernel(const RP r, uint8_t *tab, uint8_t *lead,
+                                                         unsigned long long *work, unsigned *nwork) {
+    __shared__ long long qs[4][NE];
+    const int c = threadIdx.x >> 6, j = threadIdx.x & 63;
+    const long long t = blockIdx.x * 4ll + c;
+    const bool on = t < r.nchunks && j < MAXW;
+    const long long c0 = HDR + t * CHUNK, c1 = on ? min(c0 + CHUNK, r.nbits) : 0;
     long long p = c0 + j;
+    if (on) {
+        const long long stop = min(c0 + PROBE, c1);
+        Cursor cur(r.data, r.nbytes, p);
+        while (p < stop) p += tok_w(cur.peek(p), r.wtab);
+        qs[c][j] = p;
+    }
+    __syncthreads();
+    if (!on) return;
+    int leader = j;
+    for (int i = 0; i < j; i++)
+        if (qs[c][i] == p) {
+            leader = i;
+            break;
+        }
+    lead[t * NE + j] = (uint8_t)leader;
+    if (leader != j) return;
+    if (p >= c1) {
+        tab[t * NE + j] = (uint8_t)(p - c1);
+    } else {  // (chunk, offset, walk position - c0)
+        const unsigned k = atomicAdd(nwork, 1u);
+        work[k] = ((unsigned long long)t << 20) | ((unsigned long long)j << 14) | (unsigned long long)(p - c0);
+    }
+}
+
+__global__ void exit_finish_kernel(const RP r, uint8_t *tab, const unsigned long long *work, const unsigned *nwork) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= *nwork) return;
+    const unsigned long long it = work[k];
+    const long long t = (long long)(it >> 20), j = (long long)((it >> 14) & 63);
+    const long long c0 = HDR + t * CHUNK, c1 = min(c0 + CHUNK, r.nbits);
+    long long p = c0 + (long long)(it & 16383);
     Cursor cur(r.data, r.nbytes, p);
     while (p < c1) p += tok_w(cur.peek(p), r.wtab);
     tab[t * NE + j] = (uint8_t)(p - c1);
+}
+
+__global__ void exit_copy_kernel(const RP r, uint8_t *tab, const uint8_t *lead) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= r.nchunks * NE || (i & (NE - 1)) >= MAXW) return;
+    const int l = lead[i];
+    if (l != (int)(i & (NE - 1))) tab[i] = tab[(i & ~(long long)(NE - 1)) + l];
 }
 
 // one level up: out[g * NE + j] = the composition of in's rows [g * TG, g * TG + TG) from entry j
@@ -368,6 +421,12 @@ __global__ void emit_kernel(const RP r, const EmitParams e, const long long *tok
     }
 }
 
+// one thread per item, no cap (the token-synchronisation kernels do not grid-stride)
+unsigned blocks_for(long long n, int threads) {
+    const long long b = (n + threads - 1) / threads;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
 unsigned grid_for(long long n, int threads) {
     const long long b = (n + threads - 1) / threads;
     return (unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
@@ -377,6 +436,9 @@ struct ReadWs {
     unsigned long long *bitmap, *status;
     long long *wcnt, *wbase, *tokpos, *area, *nleaf, *cell0, *leaf0, *totals;
     uint8_t *tab, *gtab, *sgtab;  // exit tables: chunks, groups, supergroups (NE bytes per row)
+    uint8_t *lead;                // per chunk entry: the offset whose walk it shares past the probe
+    unsigned long long *work;     // distinct walks past the probe (chunk, offset, position)
+    unsigned *nwork;
     int *ent_c, *ent_g, *ent_s;   // resolved entry offsets per level
     long long nwords, nchunks, maxtok, scan_tiles;
 };
@@ -397,6 +459,9 @@ long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     t.status = (unsigned long long *)take(scan_tiles * 8);
     const long long ngroups = (nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
     t.tab = (uint8_t *)take(nchunks * NE);
+    t.lead = (uint8_t *)take(nchunks * NE);
+    t.work = (unsigned long long *)take(nchunks * MAXW * 8);
+    t.nwork = (unsigned *)take(8);
     t.gtab = (uint8_t *)take(ngroups * NE);
     t.sgtab = (uint8_t *)take(nsg * NE);
     t.ent_c = (int *)take(nchunks * 4);
@@ -461,13 +526,16 @@ int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, in
     if (r.nchunks > 0) {
         const long long ngroups = (r.nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
         MNS_CHECK_ARG(nsg <= TG, "stream longer than the reader's three table levels (268 MB)");
-        exit_table_kernel<<<(unsigned)((r.nchunks + 3) / 4), 256, 0, s>>>(r, w.tab);
+        MNS_CUDA_TRY(cudaMemsetAsync(w.nwork, 0, 4, s));
+        exit_probe_kernel<<<(unsigned)((r.nchunks + 3) / 4), 256, 0, s>>>(r, w.tab, w.lead, w.work, w.nwork);
+        exit_finish_kernel<<<blocks_for(r.nchunks * MAXW, 128), 128, 0, s>>>(r, w.tab, w.work, w.nwork);
+        exit_copy_kernel<<<blocks_for(r.nchunks * NE, 256), 256, 0, s>>>(r, w.tab, w.lead);
         compose_kernel<<<(unsigned)((ngroups + 3) / 4), 256, 0, s>>>(w.tab, r.nchunks, w.gtab, ngroups);
         compose_kernel<<<(unsigned)((nsg + 3) / 4), 256, 0, s>>>(w.gtab, ngroups, w.sgtab, nsg);
         resolve_kernel<<<1, 32, 0, s>>>(w.sgtab, nsg, nullptr, 1, w.ent_s);  // from offset 0 (needs nsg <= 64)
-        resolve_kernel<<<grid_for(nsg, 64), 64, 0, s>>>(w.gtab, ngroups, w.ent_s, nsg, w.ent_g);
-        resolve_kernel<<<grid_for(ngroups, 64), 64, 0, s>>>(w.tab, r.nchunks, w.ent_g, ngroups, w.ent_c);
-        mark_kernel<<<grid_for(r.nchunks, 64), 64, 0, s>>>(r, w.ent_c);
+        resolve_kernel<<<blocks_for(nsg, 64), 64, 0, s>>>(w.gtab, ngroups, w.ent_s, nsg, w.ent_g);
+        resolve_kernel<<<blocks_for(ngroups, 64), 64, 0, s>>>(w.tab, r.nchunks, w.ent_g, ngroups, w.ent_c);
+        mark_kernel<<<blocks_for(r.nchunks, 64), 64, 0, s>>>(r, w.ent_c);
         MNS_CUDA_TRY(cudaGetLastError());
         // token list
         const long long nwords = (body + 63) / 64;
