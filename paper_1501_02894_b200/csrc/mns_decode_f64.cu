@@ -113,21 +113,96 @@ __device__ __forceinline__ double paint_unit_f64_fixed(int x, int y, int iso, in
     return dmax;
 }
 
-__global__ void __launch_bounds__(256) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
-                                                        const int32_t *udx, const int32_t *udy, const double *us,
-                                                        const double *uo, long long n, int W, const double *cur,
-                                                        double *nxt, long long *state) {
+// A unit of side 8 or 16 painted by a half-warp, bit-identical to paint_unit_f64: numpy's pairwise
+// mean keeps 8 accumulators over each block of <= 128 elements (accumulator k sums elements 8s + k
+// in order), so lane (h, k) -- block h of a side-16 unit, accumulator k -- owns exactly the elements
+// one accumulator sums: it forms their downsampled values, sums them in order, and the half-warp
+// combines ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) (then lo + hi for side 16) by xor
+// shuffles (fp64 addition is commutative, so every lane gets the same bits).  The lane then paints
+// its own elements.  All 16 lanes of the half-warp (mask) must call it.
+__device__ double paint_big_f64(int x, int y, int side, int iso, int dx, int dy, double s, double o, int W,
+                                const double *cur, double *out, int hl, unsigned mask) {
+    const bool big = side == 16;
+    const bool on = big || hl < 8;
+    const int k = hl & 7, base = big ? 128 * (hl >> 3) : 0, nst = big ? 16 : 8, lg = big ? 4 : 3;
+    double d[16];
+    double r = 0.0;
+    if (on) {
+#pragma unroll
+        for (int st = 0; st < 16; st++) {
+            if (st < nst) {
+                const int e = base + 8 * st + k, i = e >> lg, j = e & (side - 1);
+                const int kk = iso ? iso_src(iso, i, j, side) : e;
+                const double *pp = cur + (size_t)(dy + 2 * (kk >> lg)) * W + dx + 2 * (kk & (side - 1));
+                d[st] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), pp[W]), pp[W + 1]), 0.25);
+                r = st == 0 ? d[0] : __dadd_rn(r, d[st]);
+            }
+        }
+    }
+    const double t1 = __dadd_rn(r, __shfl_xor_sync(mask, r, 1));
+    const double t2 = __dadd_rn(t1, __shfl_xor_sync(mask, t1, 2));
+    double tot = __dadd_rn(t2, __shfl_xor_sync(mask, t2, 4));
+    const double other = __shfl_xor_sync(mask, tot, 8);
+    if (big) tot = __dadd_rn(tot, other);
+    const double dm = __dmul_rn(tot, big ? 1.0 / 256.0 : 1.0 / 64.0);  // exact: division by a power of two
+    double dmax = 0.0;
+    if (on) {
+#pragma unroll
+        for (int st = 0; st < 16; st++) {
+            if (st < nst) {
+                const int e = base + 8 * st + k, i = e >> lg, j = e & (side - 1);
+                double v = __dadd_rn(__dmul_rn(s, __dsub_rn(d[st], dm)), o);
+                v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+                const size_t idx = (size_t)(y + i) * W + x + j;
+                dmax = fmax(dmax, fabs(__dsub_rn(v, cur[idx])));
+                out[idx] = v;
+            }
+        }
+    }
+    return dmax;
+}
+
+constexpr int F64_T = 256;  // threads (unit slots) per CTA of the sweep
+
+__global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
+                                                          const int32_t *udx, const int32_t *udy, const double *us,
+                                                          const double *uo, long long n, int W, const double *cur,
+                                                          double *nxt, long long *state) {
     if (state[0]) return;  // converged in an earlier sweep
     const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     double dmax = 0.0;
+    bool big = false;
     if (u < n && (usize[u] & 255) > 0) {  // usize = side | isometry << 8
         const int side = usize[u] & 255, iso = usize[u] >> 8;
         if (side == 4)
             dmax = paint_unit_f64_fixed<4>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
         else if (side == 2)
             dmax = paint_unit_f64_fixed<2>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+        else if (side == 8 || side == 16)
+            big = true;  // painted below by a half-warp
         else
             dmax = paint_unit_f64(ux[u], uy[u], side, iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
+    }
+    // this warp's units of side 8 / 16, a half-warp each (no CTA barrier: codes without such units
+    // pay one ballot)
+    unsigned bb = __ballot_sync(FULL, big);
+    if (bb) {
+        const int lane = threadIdx.x & 31, hl = lane & 15, hw = lane >> 4;
+        const unsigned mask = 0xFFFFu << (16 * hw);
+        const long long w0 = u - lane;
+        for (int r = 0; bb; r++) {
+            const int b0 = __ffs(bb) - 1;  // round r: half-warp 0 takes the lowest, half-warp 1 the next
+            bb &= bb - 1;
+            const int b1 = bb ? __ffs(bb) - 1 : -1;
+            if (b1 >= 0) bb &= bb - 1;
+            const int b = hw ? b1 : b0;
+            if (b >= 0) {
+                const long long v = w0 + b;
+                const int side = usize[v] & 255, iso = usize[v] >> 8;
+                dmax = fmax(dmax, paint_big_f64(ux[v], uy[v], side, iso, udx[v], udy[v], us[v], uo[v], W, cur, nxt,
+                                                hl, mask));
+            }
+        }
     }
     long long bits = __double_as_longlong(dmax);
 #pragma unroll
@@ -244,8 +319,8 @@ int decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize,
                      double *nxt, int64_t *state, cudaStream_t st) {
     MNS_CHECK_ARG(n >= 0 && W > 0, "bad unit count or width");
     if (n == 0) return 0;
-    sweep_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt,
-                                                                 reinterpret_cast<long long *>(state));
+    sweep_f64_kernel<<<(unsigned)((n + F64_T - 1) / F64_T), F64_T, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W,
+                                                                           cur, nxt, reinterpret_cast<long long *>(state));
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
