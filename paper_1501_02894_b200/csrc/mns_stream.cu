@@ -63,18 +63,64 @@ __device__ __forceinline__ uint64_t rec_bits(uint64_t r, int mns, int t2, int &w
     return v;
 }
 
-__global__ void __launch_bounds__(SCAN_T) width_scan_kernel(const uint64_t *rec, long long n, int mns, int t2,
-                                                            long long *offsets, unsigned long long *status,
-                                                            long long *total_bits) {
+// MSB-first bit writer of one thread's run of records: words wholly inside the run are stored, the
+// (at most two) words it shares with the neighbouring runs are OR-ed into the zeroed output.
+struct BitOut {
+    uint32_t *out;
+    long long w;      // current word index
+    int fill;         // bits of the current word already placed (by this run or the previous one)
+    bool shared;      // the current word is shared with the previous run
+    uint32_t cur;     // its value so far (big-endian bit order in a native word)
+    __device__ __forceinline__ BitOut(uint32_t *o, long long bit) : out(o), w(bit >> 5), fill((int)(bit & 31)),
+                                                                    shared((bit & 31) != 0), cur(0) {}
+    __device__ __forceinline__ void flush_word() {
+        const uint32_t be = __byte_perm(cur, 0, 0x0123);
+        if (shared)
+            atomicOr(out + w, be);
+        else
+            out[w] = be;
+    }
+    // append the low `n` (<= 64) bits of v, MSB first
+    __device__ __forceinline__ void put(uint64_t v, int n) {
+        while (n > 0) {
+            const int take = min(n, 32 - fill);
+            const uint32_t bits = (uint32_t)((v >> (n - take)) & ((1ull << take) - 1));
+            cur |= bits << (32 - fill - take);
+            fill += take;
+            n -= take;
+            if (fill == 32) {
+                flush_word();
+                w++;
+                fill = 0;
+                cur = 0;
+                shared = false;
+            }
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (fill > 0) {  // the last word is shared with the next run (or is the stream's tail)
+            shared = true;
+            flush_word();
+        }
+    }
+};
+
+// One pass: per-leaf widths, a decoupled look-back exclusive scan (each thread's run of SCAN_IPT
+// records gets its first bit), and each thread writes its run's bits straight into the output.
+__global__ void __launch_bounds__(SCAN_T) pack_kernel(const uint64_t *rec, long long n, int mns, int t2,
+                                                      unsigned long long *status, long long *total_bits,
+                                                      uint32_t *out) {
     __shared__ long long warp_tot[SCAN_T / 32];
     __shared__ long long base_sh;
     const long long tile = blockIdx.x;
     const long long i0 = tile * SCAN_TILE + (long long)threadIdx.x * SCAN_IPT;
+    uint64_t r[SCAN_IPT];
     int w[SCAN_IPT];
     long long sum = 0;
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; k++) {
-        w[k] = (i0 + k < n) ? rec_width(rec[i0 + k], mns, t2) : 0;
+        r[k] = (i0 + k < n) ? rec[i0 + k] : 0ull;
+        w[k] = (i0 + k < n) ? rec_width(r[k], mns, t2) : 0;
         sum += w[k];
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -85,69 +131,48 @@ __global__ void __launch_bounds__(SCAN_T) width_scan_kernel(const uint64_t *rec,
     }
     if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        long long agg = 0;
+    if (warp == 0) {  // the block's prefix: warp-cooperative decoupled look-back
+        long long agg = 0, mine = 0;
+#pragma unroll
         for (int k = 0; k < SCAN_T / 32; k++) {
-            const long long t = warp_tot[k];
-            warp_tot[k] = agg;
-            agg += t;
+            if (k == lane) mine = agg;
+            agg += warp_tot[k];
         }
-        const long long base = lookback_exclusive(status, tile, agg);
-        base_sh = base;
-        if (tile == gridDim.x - 1) *total_bits = HEADER_BITS + base + agg;
+        const long long base = lookback_exclusive_warp(status, tile, agg);
+        __syncwarp();
+        if (lane < SCAN_T / 32) warp_tot[lane] = mine;
+        if (lane == 0) {
+            base_sh = base;
+            if (tile == gridDim.x - 1) *total_bits = HEADER_BITS + base + agg;
+        }
     }
     __syncthreads();
-    long long off = HEADER_BITS + base_sh + warp_tot[warp] + incl - sum;
+    if (sum == 0) return;
+    BitOut bo(out, HEADER_BITS + base_sh + warp_tot[warp] + incl - sum);
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; k++) {
-        if (i0 + k < n) offsets[i0 + k] = off;
-        off += w[k];
+        if (i0 + k < n) {
+            int wb;
+            const uint64_t v = rec_bits(r[k], mns, t2, wb);
+            bo.put(v, wb);
+        }
     }
+    bo.finish();
 }
 
-__global__ void scatter_kernel(const uint64_t *rec, const long long *offsets, long long n, int mns, int t2,
-                               const long long *total_bits, uint32_t hdr0, uint32_t hdr1, uint32_t hdr2,
-                               uint32_t hdr3, uint8_t *out, long long max_words) {
-    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long tb = *total_bits;
-    const long long nwords = (tb + 31) / 32;
-    if (k >= nwords || k >= max_words) return;
-    const long long b0 = 32 * k, b1 = b0 + 32;
-    uint64_t acc = 0;  // big-endian word value in the low 32 bits
-    if (b0 < HEADER_BITS) {
-        const uint32_t h[4] = {hdr0, hdr1, hdr2, hdr3};
-        acc = h[k];
-    }
-    // first record with offset + width > b0: binary search the last record with offset <= b0
-    long long lo = 0, hi = n;
-    while (lo < hi) {
-        const long long mid = (lo + hi) >> 1;
-        if (offsets[mid] <= b0) lo = mid + 1;
-        else hi = mid;
-    }
-    long long i = lo > 0 ? lo - 1 : 0;
-    for (; i < n; i++) {
-        const long long off = offsets[i];
-        if (off >= b1) break;
-        int w;
-        const uint64_t v = rec_bits(rec[i], mns, t2, w);
-        if (off + w <= b0) continue;
-        // place bits [off, off+w) into window [b0, b0+32)
-        const long long shift = (b1 - (off + w));  // distance of the record's last bit from the window end
-        uint64_t part;
-        if (shift >= 0) part = v << shift;
-        else part = v >> (-shift);
-        acc |= part & 0xFFFFFFFFull;
-    }
-    const uint32_t be = (uint32_t)acc;
-    reinterpret_cast<uint32_t *>(out)[k] = __byte_perm(be, 0, 0x0123);
+// the 13-byte header: words 0..2 stored, its last byte OR-ed into word 3 (shared with the first leaf)
+__global__ void header_kernel(uint32_t *out, uint32_t h0, uint32_t h1, uint32_t h2, uint32_t h3) {
+    out[0] = __byte_perm(h0, 0, 0x0123);
+    out[1] = __byte_perm(h1, 0, 0x0123);
+    out[2] = __byte_perm(h2, 0, 0x0123);
+    atomicOr(out + 3, __byte_perm(h3, 0, 0x0123));
 }
 
 }  // namespace
 
 int stream_workspace_bytes(int64_t n, int64_t *bytes) {
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    *bytes = ((n * 8 + 255) & ~255ll) + ((tiles * 8 + 255) & ~255ll) + 256;
+    *bytes = ((tiles * 8 + 255) & ~255ll) + 256;
     return 0;
 }
 
@@ -164,12 +189,8 @@ int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int
     MNS_CHECK_ARG(ws_bytes >= need, "workspace too small");
     const long long max_words = (HEADER_BITS + 33 * (long long)n + 31) / 32;
     MNS_CHECK_ARG(cap >= 4 * max_words, "output capacity too small (need 4*ceil((104+33n)/32) bytes)");
-    char *p = (char *)ws;
-    long long *offsets = (long long *)p;
-    p += (n * 8 + 255) & ~255ll;
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    unsigned long long *status = (unsigned long long *)p;
-    p += (tiles * 8 + 255) & ~255ll;
+    unsigned long long *status = (unsigned long long *)ws;
     // header: "MNS1", flags, orig_w, orig_h, padded_w, padded_h (big endian), then leaf bits
     const uint8_t flags = (mns ? 1 : 0) | (t2 ? 2 : 0);
     const uint8_t hb[16] = {'M', 'N', 'S', '1', flags, (uint8_t)(ow >> 8), (uint8_t)ow, (uint8_t)(oh >> 8),
@@ -178,14 +199,16 @@ int write_stream(const uint64_t *records, int64_t n, int ow, int oh, int pw, int
     for (int k = 0; k < 4; k++)
         h[k] = ((uint32_t)hb[4 * k] << 24) | ((uint32_t)hb[4 * k + 1] << 16) | ((uint32_t)hb[4 * k + 2] << 8) |
                hb[4 * k + 3];
+    // words shared by two runs are OR-ed: the output starts zeroed (every word the stream can reach)
+    MNS_CUDA_TRY(cudaMemsetAsync(out, 0, 4 * max_words, st));
+    header_kernel<<<1, 1, 0, st>>>(reinterpret_cast<uint32_t *>(out), h[0], h[1], h[2], h[3]);
     if (n > 0) {
         MNS_CUDA_TRY(cudaMemsetAsync(status, 0, tiles * 8, st));
-        width_scan_kernel<<<(unsigned)tiles, SCAN_T, 0, st>>>(records, n, mns, t2, offsets, status, (long long *)d_bits);
+        pack_kernel<<<(unsigned)tiles, SCAN_T, 0, st>>>(records, n, mns, t2, status, (long long *)d_bits,
+                                                         reinterpret_cast<uint32_t *>(out));
     } else {  // an empty code: the header alone (stream-ordered, no host round trip)
         set_bits_kernel<<<1, 1, 0, st>>>((long long *)d_bits, HEADER_BITS);
     }
-    scatter_kernel<<<(unsigned)((max_words + 255) / 256), 256, 0, st>>>(records, offsets, n, mns, t2, (const long long *)d_bits, h[0],
-                                                                        h[1], h[2], h[3], out, max_words);
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
 }
