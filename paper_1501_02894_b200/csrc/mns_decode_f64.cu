@@ -164,6 +164,7 @@ __device__ double paint_big_f64(int x, int y, int side, int iso, int dx, int dy,
 
 constexpr int F64_T = 256;  // threads (unit slots) per CTA of the sweep
 
+template <bool BIGSEP>
 __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
                                                           const int32_t *udx, const int32_t *udy, const double *us,
                                                           const double *uo, long long n, int W, const double *cur,
@@ -179,14 +180,14 @@ __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, 
         else if (side == 2)
             dmax = paint_unit_f64_fixed<2>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
         else if (side == 8 || side == 16)
-            big = true;  // painted below by a half-warp
+            big = !BIGSEP;  // painted below by a half-warp (BIGSEP: by sweep_big_f64_kernel)
         else
             dmax = paint_unit_f64(ux[u], uy[u], side, iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
     }
     // this warp's units of side 8 / 16, a half-warp each (no CTA barrier: codes without such units
     // pay one ballot)
     unsigned bb = __ballot_sync(FULL, big);
-    if (bb) {
+    if (!BIGSEP && bb) {
         const int lane = threadIdx.x & 31, hl = lane & 15, hw = lane >> 4;
         const unsigned mask = 0xFFFFu << (16 * hw);
         const long long w0 = u - lane;
@@ -203,6 +204,34 @@ __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, 
                                                 hl, mask));
             }
         }
+    }
+    long long bits = __double_as_longlong(dmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
+    if ((threadIdx.x & 31) == 0 && bits > 0)
+        atomicMax(reinterpret_cast<unsigned long long *>(&state[2]), (unsigned long long)bits);
+}
+
+// Codes made mostly of units of side 8 / 16 (e.g. the 8-isometry encodes, whose roots mostly stay
+// whole): a half-warp per group of four unit slots (one record's units), so every big unit gets its
+// own half-warp instead of waiting its turn in a warp holding eight.
+__global__ void __launch_bounds__(256) sweep_big_f64_kernel(const int32_t *ux, const int32_t *uy,
+                                                            const int32_t *usize, const int32_t *udx,
+                                                            const int32_t *udy, const double *us, const double *uo,
+                                                            long long n, int W, const double *cur, double *nxt,
+                                                            long long *state) {
+    if (state[0]) return;
+    const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
+    const int hl = threadIdx.x & 15;
+    const unsigned mask = 0xFFFFu << (16 * ((threadIdx.x >> 4) & 1));
+    double dmax = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < 4; k++) {
+        const long long v = 4 * g + k;
+        const int sz = v < n ? usize[v] : 0, side = sz & 255;
+        if (side == 8 || side == 16)  // uniform across the half-warp
+            dmax = fmax(dmax, paint_big_f64(ux[v], uy[v], side, sz >> 8, udx[v], udy[v], us[v], uo[v], W, cur, nxt,
+                                            hl, mask));
     }
     long long bits = __double_as_longlong(dmax);
 #pragma unroll
@@ -314,15 +343,30 @@ int records_to_units(const uint64_t *records, int64_t n, int W, int H, int32_t *
     return 0;
 }
 
+static int f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                     const int32_t *udy, const double *us, const double *uo, int64_t n, int W, const double *cur,
+                     double *nxt, int64_t *state, bool bigsep, cudaStream_t st) {
+    if (n == 0) return 0;
+    const unsigned grid = (unsigned)((n + F64_T - 1) / F64_T);
+    long long *stt = reinterpret_cast<long long *>(state);
+    if (bigsep) {
+        sweep_f64_kernel<true><<<grid, F64_T, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, stt);
+        const long long groups = (n + 3) / 4;
+        sweep_big_f64_kernel<<<(unsigned)((groups * 16 + 255) / 256), 256, 0, st>>>(ux, uy, usize, udx, udy, us, uo,
+                                                                                    n, W, cur, nxt, stt);
+    } else {
+        sweep_f64_kernel<false><<<grid, F64_T, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, stt);
+    }
+    MNS_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 int decode_f64_sweep(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
                      const int32_t *udy, const double *us, const double *uo, int64_t n, int W, const double *cur,
                      double *nxt, int64_t *state, cudaStream_t st) {
     MNS_CHECK_ARG(n >= 0 && W > 0, "bad unit count or width");
     if (n == 0) return 0;
-    sweep_f64_kernel<<<(unsigned)((n + F64_T - 1) / F64_T), F64_T, 0, st>>>(ux, uy, usize, udx, udy, us, uo, n, W,
-                                                                           cur, nxt, reinterpret_cast<long long *>(state));
-    MNS_CUDA_TRY(cudaGetLastError());
-    return 0;
+    return f64_sweep(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, state, false, st);
 }
 
 int decode_f64_decide(int64_t *state, double stop_delta, cudaStream_t st) {
@@ -350,10 +394,13 @@ int decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const
     int64_t *state = reinterpret_cast<int64_t *>(workspace);
     MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 32, st));
     fill_f64_kernel<<<sm_count_f64() * 4, 256, 0, st>>>(ping, init, (long long)W * H);
+    // leaves of 64+ pixels on average (n = 4 unit slots per leaf): units of side 8 / 16 dominate, give each
+    // its own half-warp
+    const bool bigsep = (long long)W * H >= 16 * (long long)n;
     for (int it = 0; it < iters; it++) {
         const double *cur = (it & 1) ? pong : ping;
         double *nxt = (it & 1) ? ping : pong;
-        if (int rc = decode_f64_sweep(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, state, st)) return rc;
+        if (int rc = f64_sweep(ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt, state, bigsep, st)) return rc;
         if (int rc = decode_f64_decide(state, stop_delta, st)) return rc;
     }
     return decode_f64_finalize(ping, pong, state, W, 0, H, out, d_iters_done, st);
