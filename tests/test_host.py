@@ -113,3 +113,23 @@ def test_sqrt_bound_semantics():
         while math.sqrt(math.nextafter(x, math.inf)) <= E:
             x = math.nextafter(x, math.inf)
         assert math.sqrt(x) <= E < math.sqrt(math.nextafter(x, math.inf))
+
+
+def test_integration_listing_matches_binding():
+    """INTEGRATION.md's ctypes listing (what a maintainer would paste into mnscodec) declares every
+    exported entry point with the same argument types as paper_1501_02894_b200/_native.py."""
+    import os
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    integ = open(os.path.join(root, "INTEGRATION.md")).read()
+    nat = open(os.path.join(root, "paper_1501_02894_b200", "_native.py")).read()
+    sig = dict(re.findall(r'"(mns_\w+)": (\[.*?\]),', nat, re.S))
+    doc = dict(re.findall(r"L\.(mns_\w+)\.argtypes = (\[.*?\])", integ, re.S))
+
+    def norm(x):
+        return re.sub(r"\s+", "", x)
+
+    assert sig, "no signatures parsed from _native.py"
+    assert not [k for k, v in doc.items() if k not in sig or norm(v) != norm(sig[k])]
+    assert not [k for k in sig if k not in doc and k != "mns_version"]
