@@ -163,3 +163,28 @@ def test_reference_suite_passes_with_dropin(tmp_path):
     unexpected = [n for n in failed if n not in ALLOWED_FAIL]
     assert not unexpected, (unexpected, proc.stdout[-4000:])
     assert summary["total"] >= 170 and len(passed) >= summary["total"] - len(ALLOWED_FAIL) - len(skipped)
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("side", [16, 32, 48, 80, 144, 272])
+@pytest.mark.parametrize("t2", [True, False])
+def test_gpu_packer_and_reader_byte_equal_to_reference(ref, side, t2):
+    """The one-pass GPU .mns packer against the reference's own writer, and the exit-table GPU reader
+    against the reference's own reader, on small codes whose leaf counts hit every run shape of the
+    packer (runs of 8 leaves, a short final run, words shared between runs) and every chunk shape
+    of the reader (a single partial chunk)."""
+    import paper_1501_02894_b200 as mns
+    from paper_1501_02894_b200 import bitstream
+    from paper_1501_02894_b200.synth import synth_image
+
+    for seed, e in ((side, 4.0), (side + 1, 12.0)):
+        px = synth_image(side, seed, noise_sigma=14.0, n_blobs=3)
+        cfg = dict(e1=e, e2=e, e3=e, mode="mns", technique2=t2)
+        ours = mns.encode_quadtree(mns.GrayImage(px), mns.EncoderConfig(**cfg))
+        theirs = ref.encode_quadtree(ref.GrayImage(px), ref.EncoderConfig(**cfg))
+        blob = bitstream.write_stream(ours)
+        assert blob == ref.write_stream(theirs), (side, seed, t2)
+        back = bitstream.read_stream(blob)
+        assert np.array_equal(back.records, ours.records)
+        assert ref.read_stream(blob) == theirs
