@@ -509,6 +509,10 @@ def run_ours(args, img_np, rank, world, local_rank):
     # e3 = inf: the code has no 2x2 leaves, so the decoder carries the 2x2-sum lattice between passes
     dec = sharding.StripDecoder(code, H, W, r0, r1, rank, world, lattice=True)
     out_host = torch.empty((16 * (r1 - r0), W), dtype=torch.uint8).pin_memory()
+    if os.environ.get("MNS_BENCH_PRIORITY", "1") != "0":
+        # the step's kernels on a high-priority stream: the compaction's CTAs (low priority) fill the
+        # decode passes' tails instead of taking SMs from their waves
+        torch.cuda.set_stream(torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1]))
     stream = torch.cuda.current_stream()
     # the record compaction (second encode kernel) runs on its own stream, overlapping the decode,
     # which only needs the unit map; every step joins it before the step ends
