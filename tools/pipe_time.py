@@ -15,8 +15,9 @@ img = torch.from_numpy(config_image("c5")).cuda()
 H, W = img.shape
 n_roots = (H // 16) * (W // 16)
 hp = torch.cuda.Stream.priority_range()[1]
+NS = int(os.environ.get("NSETS", "2"))
 sets = []
-for _ in range(2):
+for _ in range(NS):
     code = mns.DeviceCode(torch.empty(64 * n_roots, dtype=torch.int64, device="cuda"),
                           torch.empty(n_roots + 1, dtype=torch.int32, device="cuda"),
                           torch.zeros(1, dtype=torch.int64, device="cuda"), W, H, 1, 0, H // 16,
@@ -45,7 +46,7 @@ def run(k, pipelined):
     for _, _, s, _ in sets:
         s.wait_event(a)
     for i in range(k):
-        j = i % 2 if pipelined else 0
+        j = i % NS if pipelined else 0
         if not pipelined and i:
             pass
         step(j)
@@ -57,8 +58,8 @@ def run(k, pipelined):
 
 
 for _ in range(3):
-    step(0)
-    step(1)
+    for j in range(NS):
+        step(j)
 torch.cuda.synchronize()
 for rep in range(2):
     print(f"serial {run(20, False):.4f} ms/step  pipelined {run(20, True):.4f} ms/step", flush=True)
