@@ -368,7 +368,7 @@ EXPORT int64_t orc_records_to_units(const uint64_t *rec, int64_t n, int W, int H
 
 /* decoder.py:32-34 _paint + transform.py:63-66 apply_map */
 static void paint(double *out, const double *cur, int W, const orc_unit *u) {
-    double d0[256], d[256];
+    double d0[256], d[256] = {0};
     int size = u->size & 255, iso = u->size >> 8, n = size * size; /* size = side | isometry << 8 */
     downsample_f64(cur, W, u->dx, u->dy, size, d0);
     /* isometry extension: the transformed domain d_t(i, j) = d(src_t(i, j)), then apply_map on it */

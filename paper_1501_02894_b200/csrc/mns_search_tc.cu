@@ -954,7 +954,7 @@ constexpr int LT_BITS = 32768;  // hull bound (domain tiles) per M tile
 __global__ void local_units_kernel(int W, int H, int B, int R, int ndx, int ndy, int n_iso, int n_rows, int cap,
                                    uint32_t *scratch, int *counts) {
     __shared__ uint32_t bm[LT_BITS / 32];
-    __shared__ int hull[2], cnt;
+    __shared__ int hull[2];
     const int m = blockIdx.x, tid = threadIdx.x;
     const int rpr = W / B;
     const int row0 = m * (MH * BM), row1 = min(n_rows, row0 + MH * BM);
@@ -974,7 +974,6 @@ __global__ void local_units_kernel(int W, int H, int B, int R, int ndx, int ndy,
         win_y(rb / rpr, tmp, yhi);
         hull[0] = (int)(((long long)ylo * ndx) / BN);
         hull[1] = (int)(((long long)yhi * ndx + ndx - 1) / BN);
-        cnt = 0;
     }
     for (int i = tid; i < LT_BITS / 32; i += blockDim.x) bm[i] = 0;
     __syncthreads();
