@@ -116,6 +116,12 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
                         int32_t iters, double stop_delta, float initial_value, float *ping, float *pong,
                         uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
                         void *stream);
+/* mns_decode_unit_map: mns_decode_quadtree from the unit map of every root row (as
+ * mns_encode_quadtree emits it with map_form = 0, or mns_build_unit_map builds it), skipping the map
+ * build; workspace >= 64 bytes. */
+int mns_decode_unit_map(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters, double stop_delta,
+                        float initial_value, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                        void *workspace, int64_t workspace_bytes, void *stream);
 
 /* One Jacobi sweep over the root rows [root_row_begin, root_row_end) (strip
  * sharding: the multi-GPU decoder exchanges 16-row halos between sweeps).

@@ -59,6 +59,7 @@ def _declare(L):
         "mns_try_node": [P, I32, I32, I64, I32, I32, I32, I32, ctypes.POINTER(EncCfg), P, P, P],
         "mns_decode_workspace_bytes": [I32, I32, P],
         "mns_decode_quadtree": [P, P, I32, I32, I32, D, F, P, P, P, P, P, I64, P],
+        "mns_decode_unit_map": [P, I32, I32, I32, D, F, P, P, P, P, P, I64, P],
         "mns_decode_sweep": [P, I32, I32, I32, I32, P, F, P, P, P, D, P],
         "mns_decode_sweep2": [P, I32, I32, I32, I32, I32, P, F, P, P, P],
         "mns_decode_pass_lattice": [P, I32, I32, I32, I32, I32, P, F, P, P, P, P],
@@ -95,7 +96,7 @@ def _declare(L):
     return L
 
 
-EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_encode_quadtree_split", "mns_try_node", "mns_build_unit_map", "mns_build_block_map", "mns_decode_workspace_bytes", "mns_decode_quadtree",
+EXPORTS = ("mns_encode_workspace_bytes", "mns_encode_quadtree", "mns_encode_quadtree_split", "mns_try_node", "mns_build_unit_map", "mns_build_block_map", "mns_decode_workspace_bytes", "mns_decode_quadtree", "mns_decode_unit_map",
            "mns_decode_sweep", "mns_decode_sweep2", "mns_decode_pass_lattice",
            "mns_decode_flat_lattice", "mns_decode_quadtree_lattice", "mns_decode_unit_map_lattice", "mns_decode_units", "mns_decode_step_f64",
            "mns_decode_f64", "mns_records_to_units", "mns_decode_f64_sweep", "mns_decode_f64_decide",

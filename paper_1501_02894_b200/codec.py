@@ -301,6 +301,13 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
         return out, it, rasters
     it = torch.zeros(1, dtype=torch.int32, device=dev)
     code.decode_error = None
+    whole = code.n_images == 1 and code.root_row_begin == 0 and code.root_row_end in (0, H // 16)
+    if code.unit_map is not None and code.unit_map_valid and code.map_form == 0 and whole:
+        # the encoder's own unit map: no rebuild from the records
+        N.check(L.mns_decode_unit_map(N.ptr(code.unit_map), W, H, int(iters), float(stop_delta),
+                                      float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out),
+                                      N.ptr(it), N.ptr(ws), ws.numel(), N.stream_ptr(stream)))
+        return out, it, rasters
     code.join(stream)
     N.check(L.mns_decode_quadtree(N.ptr(code.records), N.ptr(code.root_offsets), W, H, int(iters), float(stop_delta),
                                   float(initial_value), N.ptr(rasters[0]), N.ptr(rasters[1]), N.ptr(out), N.ptr(it),

@@ -117,6 +117,9 @@ int decode_umap_lattice(const uint16_t *umap, int W, int H, int iters, float ini
 int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
                     double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
                     void *workspace, int64_t workspace_bytes, cudaStream_t stream);
+int decode_unit_map(const uint32_t *unit_map, int W, int H, int iters, double stop_delta, float init, float *ping,
+                    float *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                    cudaStream_t stream);
 int decode_sweep(const uint32_t *unit_map, int W, int H, int rr0, int rr1, const float *cur, float init,
                  float *nxt, uint8_t *out, int *state, double stop_delta, cudaStream_t stream);
 int decode_sweep2(const uint32_t *unit_map, int umap_r0, int W, int H, int rr0, int rr1, const float *cur, float init,
@@ -252,6 +255,13 @@ int mns_decode_quadtree(const uint64_t *records, const int32_t *root_offsets, in
                         void *stream) {
     GUARD(mns::decode_quadtree(records, root_offsets, width, height, iters, stop_delta, initial_value, ping, pong,
                                out, d_iters_done, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
+int mns_decode_unit_map(const uint32_t *unit_map, int32_t width, int32_t height, int32_t iters, double stop_delta,
+                        float initial_value, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                        void *workspace, int64_t workspace_bytes, void *stream) {
+    GUARD(mns::decode_unit_map(unit_map, width, height, iters, stop_delta, initial_value, ping, pong, out,
+                               d_iters_done, workspace, workspace_bytes, (cudaStream_t)stream));
 }
 
 int mns_decode_sweep(const uint32_t *unit_map, int32_t width, int32_t height, int32_t root_row_begin,

@@ -1234,21 +1234,12 @@ int decode_quadtree_lattice(const uint64_t *records, const int32_t *root_offsets
     return decode_umap_lattice(bmap, W, H, iters, init, lat_ping, lat_pong, out, err, stream);
 }
 
-int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
-                    double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
-                    void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
-    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
-    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
-    int64_t need;
-    decode_workspace_bytes(W, H, &need);
-    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
-    MNS_CHECK_ARG(((uintptr_t)ping & 15) == 0 && ((uintptr_t)pong & 15) == 0, "rasters must be 16-byte aligned");
-    int *state = reinterpret_cast<int *>(workspace);
-    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
+// The raster sweeps of a whole-image decode from a unit map (map_form 0) of every root row.
+static int decode_from_umap(const uint32_t *umap, int W, int H, int iters, double stop_delta, float init, float *ping,
+                            float *pong, uint8_t *out, int32_t *d_iters_done, int *state, cudaStream_t stream) {
     const long long npx = (long long)W * H;
+    int rc = 0;
     MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, stream));
-    int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream);
-    if (rc) return rc;
     const bool track = stop_delta > 0.0;
     if (out && !track && iters >= 2) {
         // no early stop and only the uint8 image wanted: an odd first sweep alone, then two
@@ -1289,6 +1280,34 @@ int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W,
     if (d_iters_done) MNS_CUDA_TRY(cudaMemcpyAsync(d_iters_done, state + 1, 4, cudaMemcpyDeviceToDevice, stream));
     MNS_CUDA_TRY(cudaGetLastError());
     return 0;
+}
+
+int decode_quadtree(const uint64_t *records, const int32_t *root_offsets, int W, int H, int iters,
+                    double stop_delta, float init, float *ping, float *pong, uint8_t *out, int32_t *d_iters_done,
+                    void *workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    int64_t need;
+    decode_workspace_bytes(W, H, &need);
+    MNS_CHECK_ARG(workspace_bytes >= need, "workspace too small");
+    MNS_CHECK_ARG(((uintptr_t)ping & 15) == 0 && ((uintptr_t)pong & 15) == 0, "rasters must be 16-byte aligned");
+    int *state = reinterpret_cast<int *>(workspace);
+    uint32_t *umap = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
+    if (int rc = build_unit_map(records, root_offsets, W, 0, H / 16, umap, stream)) return rc;
+    return decode_from_umap(umap, W, H, iters, stop_delta, init, ping, pong, out, d_iters_done, state, stream);
+}
+
+// mns_decode_quadtree from the unit map of every root row (as mns_encode_quadtree emits it with
+// map_form = 0), skipping the map build; workspace >= 64 bytes.
+int decode_unit_map(const uint32_t *unit_map, int W, int H, int iters, double stop_delta, float init, float *ping,
+                    float *pong, uint8_t *out, int32_t *d_iters_done, void *workspace, int64_t workspace_bytes,
+                    cudaStream_t stream) {
+    MNS_CHECK_ARG(W > 0 && H > 0 && W % 16 == 0 && H % 16 == 0, "width/height must be positive multiples of 16");
+    MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
+    MNS_CHECK_ARG(workspace_bytes >= 64, "workspace too small");
+    MNS_CHECK_ARG(((uintptr_t)ping & 15) == 0 && ((uintptr_t)pong & 15) == 0, "rasters must be 16-byte aligned");
+    return decode_from_umap(unit_map, W, H, iters, stop_delta, init, ping, pong, out, d_iters_done,
+                            reinterpret_cast<int *>(workspace), stream);
 }
 
 int decode_units(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,

@@ -738,6 +738,28 @@ def test_decode_from_encoder_unit_map_equals_records_path(mns, root_level, iters
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("e3,root_level,iters", [(8.0, 1, 10), (8.0, 2, 7), (2.0, 1, 1), (math.inf, 1, 9)])
+def test_decode_from_encoder_raster_unit_map_equals_records_path(mns, e3, root_level, iters):
+    """decode_device on the encoder's map_form-0 unit map (mns_decode_unit_map: fp32 rasters, 2x2 leaves
+    allowed) equals the decode that rebuilds the map from the records (mns_decode_quadtree), bit for bit,
+    for both the uint8 output and the final raster."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    img = torch.from_numpy(synth_image(256, 13)).cuda()
+    code = mns.encode_device(img, mns.EncoderConfig(e3=e3), root_level=root_level, map_form=0)
+    assert code.unit_map_valid and code.map_form == 0
+    a, ia, _ = mns.decode_device(code, iters=iters, stop_delta=0.0, lattice=False)
+    _, _, ra = mns.decode_device(code, iters=iters, stop_delta=0.0, want_u8=False)
+    code.unit_map_valid = False
+    b, ib, _ = mns.decode_device(code, iters=iters, stop_delta=0.0, lattice=False)
+    _, _, rb = mns.decode_device(code, iters=iters, stop_delta=0.0, want_u8=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert int(ia.item()) == int(ib.item()) == iters
+    final = iters % 2  # the final raster: ping after an even sweep count, else pong
+    assert torch.equal(ra[final], rb[final])
+
+
 def test_full_search_wide_key_large_pool(mns):
     """B = 8 identity search over a 1600^2 image: 1585^2 = 2.5M domains, above the old 2^21
     candidate cap (the key now gives B = 8 candidates 25 bits).  A range slice vs the oracle."""
