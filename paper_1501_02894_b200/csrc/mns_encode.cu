@@ -5,8 +5,8 @@
 //   encoder.py:215-246 encode_quadtree / visit, :145-166 try_phase1,
 //   :169-212 try_phase2, image.py:146-187 block helpers, transform.py:23-80.
 //
-// Work decomposition: one CTA = up to TR = 16 consecutive 16x16 roots of one root
-// row (warp w owns roots w and w + 8).  The CTA stages the uint8 window
+// Work decomposition: one CTA = up to TR = 32 consecutive 16x16 roots of one root
+// row (warp w owns roots w, w + 8, w + 16, w + 24: two per half-warp per step).  The CTA stages the uint8 window
 // [x0-16, x0+16*TR+16) x [y0-16, y0+32) (every clamped domain of every node of its roots lies inside,
 // SURVEY 7 "geometry") with 16-byte coalesced loads, and builds the table of
 // even-phase 2x2 pixel sums q (0..1020, u16) with packed SIMD-in-register adds.
@@ -39,12 +39,18 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 #ifndef ENC_MINB
-#define ENC_MINB 4
+#define ENC_MINB 3
+#endif
+#ifndef ENC_RPW
+#define ENC_RPW 2
 #endif
 constexpr int EW = 8;                // warps per CTA
 constexpr int ET = EW * 32;
-constexpr int TR = 2 * EW;           // 16 consecutive roots of one root row per step (2 per warp)
-constexpr int WIN_W = TR * 16 + 32;  // 288 pixel columns: [x0 - 16, x0 + 272)
+constexpr int RPW = ENC_RPW;         // roots per half-warp per step (2: half the per-step barriers per root;
+                                     // c5 encode 0.632 -> 0.605 ms with 3 CTAs/SM, 85 registers)
+constexpr int TR = 2 * EW * RPW;     // consecutive roots of one root row per step
+constexpr int WIN_W = TR * 16 + 32;  // pixel columns: [x0 - 16, x0 + 16 TR + 16)
+constexpr int TMA_E = WIN_W / 2 <= 256 ? 2 : (WIN_W / 4 <= 256 ? 4 : 8);  // TMA element bytes (box <= 256)
 
 struct EncParams {
     int y_res0;  // first resident image row (the tensor map's row 0)
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
 
         auto issue = [&](int g) {  // thread 0: pixel block g (rows 16g .. 16g + 15) into slot g & 3
             mbar_arrive_expect_tx(&bars[g & 3], 16 * WIN_W);
-            tma_load_3d(pix + ((16 * g) & (PRING - 1)) * WIN_W, &tmap, wx0 / 2, 16 * g - p.y_res0, img_i,
+            tma_load_3d(pix + ((16 * g) & (PRING - 1)) * WIN_W, &tmap, wx0 / TMA_E, 16 * g - p.y_res0, img_i,
                         &bars[g & 3]);
         };
         auto wait = [&](int g) {
@@ -542,17 +548,21 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
             par ^= 1u << (g & 3);
         };
         // this thread's q-table items (the same every block): 8 q rows x 36 groups of 4 columns
-        constexpr int NIT = 8 * (QW / 4);
-        const int it1 = tid + ET < NIT ? tid + ET : tid;  // a second item for the first NIT - ET threads
-        const int src0 = 2 * (tid / (QW / 4)) * WIN_W + 8 * (tid % (QW / 4)), dst0 = (tid / (QW / 4)) * QP + 4 * (tid % (QW / 4));
-        const int src1 = 2 * (it1 / (QW / 4)) * WIN_W + 8 * (it1 % (QW / 4)), dst1 = (it1 / (QW / 4)) * QP + 4 * (it1 % (QW / 4));
+        constexpr int NIT = 8 * (QW / 4), NBI = (NIT + ET - 1) / ET;
+        int src[NBI], dst[NBI];
+#pragma unroll
+        for (int k = 0; k < NBI; k++) {
+            const int it = tid + k * ET < NIT ? tid + k * ET : tid;
+            src[k] = 2 * (it / (QW / 4)) * WIN_W + 8 * (it % (QW / 4));
+            dst[k] = (it / (QW / 4)) * QP + 4 * (it % (QW / 4));
+        }
         auto build = [&](int g) {  // q rows 8g .. 8g + 7 from pixel block g (4 q per item, packed adds)
             const uint8_t *pb = pix + ((16 * g) & (PRING - 1)) * WIN_W;
             uint16_t *qb = qe + ((8 * g) & (QRING - 1)) * QP;
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-                if (k == 1 && tid + ET >= NIT) break;
-                const uint8_t *a = pb + (k ? src1 : src0);
+            for (int k = 0; k < NBI; k++) {
+                if (k == NBI - 1 && tid + k * ET >= NIT) break;
+                const uint8_t *a = pb + src[k];
                 const uint2 u = *reinterpret_cast<const uint2 *>(a);
                 const uint2 v = *reinterpret_cast<const uint2 *>(a + WIN_W);
                 // bytes 0, 2 and 1, 3 of each word zero-extended into u16 lanes (PRMT), summed lane-wise
@@ -561,7 +571,7 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                       (__byte_perm(v.x, 0u, 0x4240) + __byte_perm(v.x, 0u, 0x4341));
                 s.y = (__byte_perm(u.y, 0u, 0x4240) + __byte_perm(u.y, 0u, 0x4341)) +
                       (__byte_perm(v.y, 0u, 0x4240) + __byte_perm(v.y, 0u, 0x4341));
-                *reinterpret_cast<uint2 *>(qb + (k ? dst1 : dst0)) = s;
+                *reinterpret_cast<uint2 *>(qb + dst[k]) = s;
             }
         };
 
@@ -585,8 +595,10 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                 fence_proxy_async();         // generic reads of block ry - 2 precede the refill
                 issue(ry + 2);
             }
-            // ---------------- the 16 roots of root row ry (warp w: slots w, w + 8)
-            const int slot = warp + EW * hw;
+            // ---------------- the TR roots of root row ry (warp w: slots w + 8 (2j + hw))
+#pragma unroll 1
+            for (int j = 0; j < RPW; j++) {
+            const int slot = warp + EW * (2 * j + hw);
             const bool live = slot < nr;
             const int sl = live ? slot : 0;
             const int rxg = x0 + 16 * sl, ryg = 16 * ry;
@@ -748,7 +760,6 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
             const unsigned b1 = __ballot_sync(FULL, nrec != 0) & half, b4 = __ballot_sync(FULL, nrec == 4) & half;
             const int off = __popc(b1 & lt) + 3 * __popc(b4 & lt);
             const long long root = row_root + sl;
-            row_root += p.rw;
             if (live) {
                 uint64_t *st = p.stage + root * 64 + off;
                 if (nrec == 4) {
@@ -780,6 +791,8 @@ __global__ void __launch_bounds__(ET, ENC_MINB) mns_encode_kernel(const __grid_c
                     *reinterpret_cast<uint2 *>(&p.unit_map[root * 32 + 2 * m]) = u;
                 }
             }
+            }
+            row_root += p.rw;
         }
     }
 }
@@ -1093,9 +1106,11 @@ int encode_quadtree(const uint8_t *img, int W, int H, int64_t pitch, int64_t ima
     p.y_res0 = 16 * rr0 - 16 > 0 ? 16 * rr0 - 16 : 0;
     const int y_res1 = 16 * rr1 + 16 < H ? 16 * rr1 + 16 : H;
     CUtensorMap tmap{};
-    if (encode_tmap_3d(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, img + (ptrdiff_t)p.y_res0 * pitch, (uint64_t)W / 2,
+    if (encode_tmap_3d(&tmap, TMA_E == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                   : (TMA_E == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64),
+                       img + (ptrdiff_t)p.y_res0 * pitch, (uint64_t)W / TMA_E,
                        (uint64_t)(y_res1 - p.y_res0), (uint64_t)n_images, (uint64_t)pitch,
-                       (uint64_t)(n_images > 1 ? image_stride : pitch * (int64_t)(y_res1 - p.y_res0)), WIN_W / 2, 16,
+                       (uint64_t)(n_images > 1 ? image_stride : pitch * (int64_t)(y_res1 - p.y_res0)), WIN_W / TMA_E, 16,
                        1))
         return -1;
     // chunks of root rows per band: about two waves of resident CTAs (a CTA re-stages two blocks of
