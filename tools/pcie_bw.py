@@ -20,3 +20,12 @@ def both():
 bb = t(both)
 print(f"H2D {n/h2d/1e9:.1f} GB/s ({h2d*1e3:.2f} ms)  D2H {n/d2h/1e9:.1f} GB/s ({d2h*1e3:.2f} ms)  both {bb*1e3:.2f} ms")
 # chunked H2D (4 MB chunks) to check
+# chunked H2D + D2H on two streams each (8 chunks of 32 MB per direction)
+sa, sb = [torch.cuda.Stream() for _ in range(2)], [torch.cuda.Stream() for _ in range(2)]
+def chunked():
+    c = n // 8
+    for j in range(8):
+        with torch.cuda.stream(sa[j & 1]): d[j * c:(j + 1) * c].copy_(h[j * c:(j + 1) * c], non_blocking=True)
+        with torch.cuda.stream(sb[j & 1]): h2[j * c:(j + 1) * c].copy_(d2[j * c:(j + 1) * c], non_blocking=True)
+ch = t(chunked)
+print(f"both chunked {ch*1e3:.2f} ms")
