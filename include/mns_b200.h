@@ -12,9 +12,8 @@
  * Conventions
  *   - All buffers are caller-owned DEVICE pointers (e.g. torch tensors'
  *     data_ptr()); `stream` is a cudaStream_t cast to void* (NULL = legacy
- *     default stream).  Calls are asynchronous and stream-ordered (one exception:
- *     mns_read_stream synchronises the stream once, to size its token list); the
- *     library keeps no pointers after returning and holds no mutable global state.
+ *     default stream).  Calls are asynchronous and stream-ordered; the library
+ *     keeps no pointers after returning and holds no mutable global state.
  *   - Images are uint8, row-major, already padded (pad_to_multiple,
  *     image.py:123-132, is host work): width/height multiples of 16 for the
  *     quadtree, of B for the search baselines.
@@ -280,8 +279,8 @@ int mns_write_stream(const uint64_t *records, int64_t n_records, int32_t orig_w,
  * as a key (bit position << 16 | code << 8 | a << 4 | b; -1 = none; codes: 1 level-a leaf
  * inside a level-b node, 2 quartet interrupted by a level-a id, 3 negative-zero delta,
  * 4 truncated), d_status[1] = bit position after the final leaf (-1 if the stream ended
- * before every root was tiled).  Trailing / padding checks are the caller's.  Not fully
- * asynchronous: the host reads the token count once (one stream synchronisation). */
+ * before every root was tiled).  Trailing / padding checks are the caller's.  Asynchronous
+ * (no host round trip). */
 int mns_read_stream_workspace_bytes(int64_t n_bytes, int64_t *bytes);
 int mns_read_stream(const uint8_t *data, int64_t n_bytes, int32_t mns, int32_t technique2, int32_t padded_w,
                     int32_t padded_h, uint64_t *records, int64_t capacity, int32_t *root_offsets, int64_t *d_count,

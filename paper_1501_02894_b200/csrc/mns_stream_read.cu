@@ -15,8 +15,10 @@
 //    compose over groups and supergroups of 64, the true entries resolve top-down from the
 //    stream start, and one walk per chunk marks the token starts in a bitmap (exit_table_kernel
 //    .. mark_kernel).
-//  * the token starts are compacted; exclusive scans of token areas (in 2x2 cells: 64, 16, 4,
-//    4 for a quartet) and leaf counts give every leaf its root, Morton cell and record slot.
+//  * one pass over the token-start bitmap (tokens_kernel) sums each tile's token areas (in 2x2
+//    cells: 64, 16, 4, 4 for a quartet) and leaf counts, scans them across tiles (decoupled
+//    look-back), and walks the tokens again to emit every leaf at its root, Morton cell and record
+//    slot -- no token list, no host round trip.
 //  * every check the sequential parser makes (level id below the node's level, interrupted
 //    quartet, negative-zero delta, truncation) is recorded as a key ordered by bit position;
 //    the minimum is the parser's first error (the host maps it to StreamFormatError).
@@ -33,7 +35,6 @@ constexpr long long HDR = 13 * 8;
 #define RD_CHUNK 8192
 #endif
 constexpr int CHUNK = RD_CHUNK;  // bits per chunk (CHUNK / 64 bitmap words)
-constexpr int ST = 256, SIPT = 8, STILE = ST * SIPT;
 
 enum { E_LEVEL = 1, E_SIBLING = 2, E_NEGZERO = 3, E_TRUNC = 4 };
 
@@ -251,73 +252,6 @@ __global__ void mark_kernel(const RP r, const int *ent) {
 }
 
 // exclusive scan of n int64 (decoupled look-back over STILE-element tiles); total -> *total
-__global__ void __launch_bounds__(ST) scan_kernel(const long long *in, long long *out, long long n,
-                                                  unsigned long long *status, long long *total) {
-    __shared__ long long warp_tot[ST / 32];
-    __shared__ long long base_sh;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long tile = blockIdx.x, i0 = tile * STILE + (long long)tid * SIPT;
-    long long v[SIPT], run = 0;
-#pragma unroll
-    for (int k = 0; k < SIPT; k++) {
-        v[k] = i0 + k < n ? in[i0 + k] : 0;
-        run += v[k];
-    }
-    long long incl = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    long long wbase = 0, tt = 0;
-#pragma unroll
-    for (int k = 0; k < ST / 32; k++) {
-        wbase += k < warp ? warp_tot[k] : 0;
-        tt += warp_tot[k];
-    }
-    if (warp == 0) {
-        const long long b = lookback_exclusive_warp(status, tile, tt);
-        if (lane == 0) base_sh = b;
-    }
-    __syncthreads();
-    long long e = base_sh + wbase + incl - run;
-#pragma unroll
-    for (int k = 0; k < SIPT; k++) {
-        if (i0 + k < n) out[i0 + k] = e;
-        e += v[k];
-    }
-    if (tile == gridDim.x - 1 && tid == ST - 1) *total = e;
-}
-
-__global__ void popc_kernel(const unsigned long long *bitmap, long long nwords, long long *cnt) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x)
-        cnt[i] = __popcll(bitmap[i]);
-}
-
-__global__ void token_list_kernel(const unsigned long long *bitmap, long long nwords, const long long *wbase,
-                                  long long *tokpos) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x) {
-        unsigned long long m = bitmap[i];
-        long long k = wbase[i];
-        while (m) {
-            const int b = __ffsll((long long)m) - 1;
-            tokpos[k++] = HDR + i * 64 + b;
-            m &= m - 1;
-        }
-    }
-}
-
-__global__ void token_info_kernel(const RP r, const long long *tokpos, long long ntok, long long *area,
-                                  long long *nleaf) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ntok; i += (long long)gridDim.x * blockDim.x) {
-        const int lid = (int)(peek64(r.data, r.nbytes, tokpos[i]) >> 62);
-        area[i] = lid == 3 ? 4 : (64 >> (2 * lid));
-        nleaf[i] = lid == 3 ? 4 : 1;
-    }
-}
-
 struct EmitParams {
     long long total_cells;
     int rw;
@@ -341,21 +275,19 @@ __device__ __forceinline__ void cell_xy(long long c, int rw, int &x, int &y) {
     y = (int)(root / rw) * 16 + 2 * cy;
 }
 
-__global__ void emit_kernel(const RP r, const EmitParams e, const long long *tokpos, const long long *cell0,
-                            const long long *leaf0, long long ntok) {
+// The token at bit p, whose first 2x2 cell (in the DFS / Morton order of the roots) is c and whose
+// first leaf is record L0: its records, and the checks the sequential parser makes at this token.
+__device__ __forceinline__ void emit_token(const RP &r, const EmitParams &e, long long p, uint64_t w, long long c,
+                                           long long L0) {
     unsigned long long *ekey = reinterpret_cast<unsigned long long *>(&e.status[0]);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ntok; i += (long long)gridDim.x * blockDim.x) {
-        const long long c = cell0[i];
+    do {
         if (c >= e.total_cells) continue;
-        const long long p = tokpos[i];
-        const uint64_t w = peek64(r.data, r.nbytes, p);
         const int lid = (int)(w >> 62);
         const int width = tok_width(w, r.mns, r.t2);
         if (p + 2 > r.nbits) {
             atomicMin(ekey, err_key(r.nbits, E_TRUNC, 0, 0));
             continue;
         }
-        const long long L0 = leaf0[i];
         if (c % 64 == 0) e.root_offsets[c >> 6] = (int32_t)L0;
         if (lid == 3) {  // level-4 quartet: TL leaf with its id, then TR, BL, BR
             for (int k = 0; k < 4; k++) {
@@ -418,6 +350,78 @@ __global__ void emit_kernel(const RP r, const EmitParams e, const long long *tok
             *e.count = L0 + (lid == 3 ? 4 : 1);
             e.root_offsets[e.total_cells >> 6] = (int32_t)(L0 + (lid == 3 ? 4 : 1));
         }
+    } while (false);
+}
+
+// Token pass (one kernel from the token-start bitmap to the records): a tile of TT threads x TW
+// bitmap words; each thread walks the token starts of its words twice -- first summing their
+// (cells, leaves) packed as cells << 28 | leaves (< 2^34 and 2^28 for any stream the exit tables
+// accept: <= 2^31 bits, tokens >= 13 bits, >= 11.5 bits per leaf), then, after a block scan and a
+// decoupled look-back over the tiles, emitting each token at its running (cell, leaf) origin.
+constexpr int TT = 256, TW = 4, TTILE = TT * TW;
+constexpr int PK_SHIFT = 28;
+constexpr unsigned long long PK_LEAF = (1ull << PK_SHIFT) - 1;
+
+__device__ __forceinline__ unsigned long long tok_pack(uint64_t w) {
+    const int lid = (int)(w >> 62);
+    return lid == 3 ? (4ull << PK_SHIFT) | 4ull : ((64ull >> (2 * lid)) << PK_SHIFT) | 1ull;
+}
+
+__global__ void __launch_bounds__(TT) tokens_kernel(const RP r, const EmitParams e, long long nwords,
+                                                    unsigned long long *status) {
+    __shared__ unsigned long long warp_tot[TT / 32];
+    __shared__ unsigned long long base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long tile = blockIdx.x, w0 = tile * TTILE + (long long)tid * TW;
+    unsigned long long m[TW];
+    {
+        const ulonglong2 *b2 = reinterpret_cast<const ulonglong2 *>(r.bitmap + w0);
+#pragma unroll
+        for (int k = 0; k < TW; k += 2) {
+            if (w0 + k + 1 < nwords) {
+                const ulonglong2 v = b2[k / 2];
+                m[k] = v.x;
+                m[k + 1] = v.y;
+            } else {
+                m[k] = w0 + k < nwords ? r.bitmap[w0 + k] : 0ull;
+                m[k + 1] = 0ull;
+            }
+        }
+    }
+    unsigned long long run = 0;
+#pragma unroll
+    for (int k = 0; k < TW; k++) {
+        for (unsigned long long b = m[k]; b; b &= b - 1)
+            run += tok_pack(peek64(r.data, r.nbytes, HDR + (w0 + k) * 64 + (__ffsll((long long)b) - 1)));
+    }
+    unsigned long long incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    unsigned long long wbase = 0, tt = 0;
+#pragma unroll
+    for (int k = 0; k < TT / 32; k++) {
+        wbase += k < warp ? warp_tot[k] : 0ull;
+        tt += warp_tot[k];
+    }
+    if (warp == 0) {
+        const long long b = lookback_exclusive_warp(status, tile, (long long)tt);
+        if (lane == 0) base_sh = (unsigned long long)b;
+    }
+    __syncthreads();
+    unsigned long long ex = base_sh + wbase + incl - run;
+#pragma unroll
+    for (int k = 0; k < TW; k++) {
+        for (unsigned long long b = m[k]; b; b &= b - 1) {
+            const long long p = HDR + (w0 + k) * 64 + (__ffsll((long long)b) - 1);
+            const uint64_t w = peek64(r.data, r.nbytes, p);
+            emit_token(r, e, p, w, (long long)(ex >> PK_SHIFT), (long long)(ex & PK_LEAF));
+            ex += tok_pack(w);
+        }
     }
 }
 
@@ -427,27 +431,21 @@ unsigned blocks_for(long long n, int threads) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
-unsigned grid_for(long long n, int threads) {
-    const long long b = (n + threads - 1) / threads;
-    return (unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
-}
 
 struct ReadWs {
     unsigned long long *bitmap, *status;
-    long long *wcnt, *wbase, *tokpos, *area, *nleaf, *cell0, *leaf0, *totals;
     uint8_t *tab, *gtab, *sgtab;  // exit tables: chunks, groups, supergroups (NE bytes per row)
     uint8_t *lead;                // per chunk entry: the offset whose walk it shares past the probe
     unsigned long long *work;     // distinct walks past the probe (chunk, offset, position)
     unsigned *nwork;
     int *ent_c, *ent_g, *ent_s;   // resolved entry offsets per level
-    long long nwords, nchunks, maxtok, scan_tiles;
+    long long nwords, nchunks, tok_tiles;
 };
 
 long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     const long long nbits = nbytes * 8, body = nbits > HDR ? nbits - HDR : 0;
     const long long nwords = (body + 63) / 64 + 1, nchunks = (body + CHUNK - 1) / CHUNK + 1;
-    const long long maxtok = body / 13 + 2;
-    const long long scan_tiles = (std::max(nwords, maxtok) + STILE - 1) / STILE + 1;
+    const long long tok_tiles = (nwords + TTILE - 1) / TTILE + 1;
     long long off = 0;
     auto take = [&](long long bytes) {
         const long long o = off;
@@ -456,7 +454,7 @@ long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     };
     ReadWs t{};
     t.bitmap = (unsigned long long *)take(nwords * 8);
-    t.status = (unsigned long long *)take(scan_tiles * 8);
+    t.status = (unsigned long long *)take(tok_tiles * 8);
     const long long ngroups = (nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
     t.tab = (uint8_t *)take(nchunks * NE);
     t.lead = (uint8_t *)take(nchunks * NE);
@@ -467,32 +465,11 @@ long long read_ws_layout(long long nbytes, ReadWs *w, char *base) {
     t.ent_c = (int *)take(nchunks * 4);
     t.ent_g = (int *)take(ngroups * 4);
     t.ent_s = (int *)take(nsg * 4);
-    t.wcnt = (long long *)take(nwords * 8);
-    t.wbase = (long long *)take(nwords * 8);
-    t.tokpos = (long long *)take(maxtok * 8);
-    t.area = (long long *)take(maxtok * 8);
-    t.nleaf = (long long *)take(maxtok * 8);
-    t.cell0 = (long long *)take(maxtok * 8);
-    t.leaf0 = (long long *)take(maxtok * 8);
-    t.totals = (long long *)take(4 * 8);
     t.nwords = nwords;
     t.nchunks = nchunks;
-    t.maxtok = maxtok;
-    t.scan_tiles = scan_tiles;
+    t.tok_tiles = tok_tiles;
     if (w) *w = t;
     return off;
-}
-
-int scan(const long long *in, long long *out, long long n, ReadWs &w, long long *total, cudaStream_t s) {
-    const long long tiles = (n + STILE - 1) / STILE;
-    MNS_CUDA_TRY(cudaMemsetAsync(w.status, 0, (tiles > 0 ? tiles : 1) * 8, s));
-    if (n == 0) {
-        MNS_CUDA_TRY(cudaMemsetAsync(total, 0, 8, s));
-        return 0;
-    }
-    scan_kernel<<<(unsigned)tiles, ST, 0, s>>>(in, out, n, w.status, total);
-    MNS_CUDA_TRY(cudaGetLastError());
-    return 0;
 }
 
 }  // namespace
@@ -522,7 +499,6 @@ int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, in
     MNS_CUDA_TRY(cudaMemcpyAsync(d_status, init, 16, cudaMemcpyHostToDevice, s));
     MNS_CUDA_TRY(cudaMemsetAsync(d_count, 0, 8, s));
     MNS_CUDA_TRY(cudaMemsetAsync(w.bitmap, 0, w.nwords * 8, s));
-    long long ntok = 0;
     if (r.nchunks > 0) {
         const long long ngroups = (r.nchunks + TG - 1) / TG, nsg = (ngroups + TG - 1) / TG;
         MNS_CHECK_ARG(nsg <= TG, "stream longer than the reader's three table levels (268 MB)");
@@ -537,25 +513,13 @@ int read_stream(const uint8_t *data, int64_t nbytes, int mns, int t2, int pw, in
         resolve_kernel<<<blocks_for(ngroups, 64), 64, 0, s>>>(w.tab, r.nchunks, w.ent_g, ngroups, w.ent_c);
         mark_kernel<<<blocks_for(r.nchunks, 64), 64, 0, s>>>(r, w.ent_c);
         MNS_CUDA_TRY(cudaGetLastError());
-        // token list
+        // token pass: cells and leaves of every token, their scan, the records
         const long long nwords = (body + 63) / 64;
-        popc_kernel<<<grid_for(nwords, 256), 256, 0, s>>>(w.bitmap, nwords, w.wcnt);
-        MNS_CUDA_TRY(cudaGetLastError());
-        if (scan(w.wcnt, w.wbase, nwords, w, &w.totals[0], s)) return -1;
-        MNS_CUDA_TRY(cudaMemcpyAsync(&ntok, &w.totals[0], 8, cudaMemcpyDeviceToHost, s));
-        MNS_CUDA_TRY(cudaStreamSynchronize(s));
-        MNS_CHECK_ARG(ntok <= w.maxtok, "token count overflow");
-        token_list_kernel<<<grid_for(nwords, 256), 256, 0, s>>>(w.bitmap, nwords, w.wbase, w.tokpos);
-        MNS_CUDA_TRY(cudaGetLastError());
-    }
-    if (ntok > 0) {
-        token_info_kernel<<<grid_for(ntok, 256), 256, 0, s>>>(r, w.tokpos, ntok, w.area, w.nleaf);
-        MNS_CUDA_TRY(cudaGetLastError());
-        if (scan(w.area, w.cell0, ntok, w, &w.totals[1], s)) return -1;
-        if (scan(w.nleaf, w.leaf0, ntok, w, &w.totals[2], s)) return -1;
+        const long long tiles = (nwords + TTILE - 1) / TTILE;
+        MNS_CUDA_TRY(cudaMemsetAsync(w.status, 0, tiles * 8, s));
         EmitParams e{n_roots * 64, pw / 16, records, capacity, root_offsets, d_count,
                      reinterpret_cast<long long *>(d_status)};
-        emit_kernel<<<grid_for(ntok, 256), 256, 0, s>>>(r, e, w.tokpos, w.cell0, w.leaf0, ntok);
+        tokens_kernel<<<(unsigned)tiles, TT, 0, s>>>(r, e, nwords, w.status);
         MNS_CUDA_TRY(cudaGetLastError());
     }
     return 0;
