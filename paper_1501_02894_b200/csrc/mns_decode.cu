@@ -317,6 +317,15 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
         // raster is in [0, 255]; fl(a q + b) is monotone in q): test the two ends, then the
         // block's actual FMNMX3 range, and clip only the lanes that need it.
         const float e0 = b, e1 = fmaf(a, 1020.f, b);
+#ifndef DEC_RANGE_CLIP
+        // clip(v) = max(min(bits, bits(255)), 0) on the fp32 bit patterns (one VIMNMX.RELU per pixel:
+        // non-negative floats order as their bits, negative ones are negative ints); identical to
+        // fminf(255, fmaxf(0, v)) up to the sign of a zero
+        if (fminf(e0, e1) < 0.f || fmaxf(e0, e1) > 255.f) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) v[e] = __int_as_float(__vimin_s32_relu(__float_as_int(v[e]), 0x437F0000));
+        }
+#else
         if (fminf(e0, e1) < 0.f || fmaxf(e0, e1) > 255.f) {
             float lo = fmin3(v[0], v[1], v[2]), hi = fmax3(v[0], v[1], v[2]);
 #pragma unroll
@@ -331,6 +340,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                 for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
             }
         }
+#endif
     }
 }
 
@@ -718,13 +728,9 @@ __global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __
         }
     };
     const uint32_t bar0 = smem_u32(&bars[0]);
-    uint32_t phase = 0;  // per-slot parity of the next wait (stage-A threads wait on every block in order)
+    // block k is its slot's (k / LNS)-th fill: blocks are issued in order, one slot per block
     auto wait_block = [&](int k) {
-        if (k < nblocks) {
-            const int slot = (r_s - 2 + k) & (LNS - 1);
-            mbar_wait_addr(bar0 + 8 * slot, (phase >> slot) & 1);
-            phase ^= 1u << slot;
-        }
+        if (k < nblocks) mbar_wait_addr(bar0 + 8 * ((r_s - 2 + k) & (LNS - 1)), (k / LNS) & 1);
     };
     const Lane L = lane_of(lane);
     const bool stage_a = warp < LNWA;
