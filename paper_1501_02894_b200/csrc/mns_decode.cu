@@ -152,19 +152,6 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return d;
 }
 
-// three-input min / max (sm_100 FMNMX3)
-__device__ __forceinline__ float fmin3(float a, float b, float c) {
-    float d;
-    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
-
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-    float d;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
-
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
@@ -226,14 +213,19 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
         return;
     }
     const uint32_t d0 = word.x & 0xFFFFu;
-    const int k = (int)(d0 >> 14);  // log2(side) - 1 of the unit holding cell 0
+    // Lattice passes (FAST): every lane paints -- dead lanes and the flagged 2x2 units through the
+    // in-ring table addresses, results discarded (liveness is per root, so no dead sum reaches a
+    // live unit) -- which keeps the paint free of divergent branches.
+    const int k = FAST ? max(1, (int)(d0 >> 14)) : (int)(d0 >> 14);  // log2(side) - 1 of cell 0's unit
+    const bool go = FAST || (live && k > 0);
+    const bool use_tab = FAST && (interior || !live);
     float own = 0.f, sa = 0.f, sb = 0.f;
-    if (live && k > 0) {  // one unit of side >= 4 covers the 4x4 block
+    if (go) {  // one unit of side >= 4 covers the 4x4 block
         sa = st[d0 & 15];
         sb = unit_o(d0);
         {
             const float *p0, *p1;  // columns qc, qc + 2 and qc + 1, qc + 3 of the domain's first lattice row
-            if (FAST && interior) {
+            if (use_tab) {
                 const uint32_t t = k == 1 ? tab->t[0] : (k == 2 ? tab->t[1] : tab->t[2]);
                 const float *row = lat + ((ryg >> 1) + (int)(t >> 16) - 8 & (RING - 1)) * QSTR;
                 p0 = row + (t & 255);
@@ -294,7 +286,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
     // sums, so the group's sum is bit-identical on all its lanes)
     // (skipped when no lane of the warp holds a unit larger than its own 4x4 block)
     float s8 = own, s16 = own;
-    if (__any_sync(FULL, live && k > 1)) {
+    if (__any_sync(FULL, go && k > 1)) {
         const float t1 = __shfl_xor_sync(FULL, own, 1), t2 = __shfl_xor_sync(FULL, own, 2),
                     t3 = __shfl_xor_sync(FULL, own, 3);
         s8 = (own + t1) + (t2 + t3);
@@ -302,7 +294,7 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
                     u3 = __shfl_xor_sync(FULL, s8, 12);
         s16 = (s8 + u1) + (u2 + u3);
     }
-    if (live && k > 0) {
+    if (go) {
         const float sum = k == 1 ? own : (k == 2 ? s8 : s16);
         const float mean = sum * __int_as_float((127 - 4 - 2 * k) << 23);  // sum * 0.25 / side^2
         const float b = fmaf(-sa, mean, sb), a = 0.25f * sa;
@@ -313,34 +305,12 @@ __device__ __forceinline__ void paint_block(uint2 word, bool live, const Lane &L
             v[2 * m] = r.x;
             v[2 * m + 1] = r.y;
         }
-        // The clip binds only if the unit's map leaves [0, 255] over q in [0, 1020] (the input
-        // raster is in [0, 255]; fl(a q + b) is monotone in q): test the two ends, then the
-        // block's actual FMNMX3 range, and clip only the lanes that need it.
-        const float e0 = b, e1 = fmaf(a, 1020.f, b);
-#ifndef DEC_RANGE_CLIP
-        // clip(v) = max(min(bits, bits(255)), 0) on the fp32 bit patterns (one VIMNMX.RELU per pixel:
-        // non-negative floats order as their bits, negative ones are negative ints); identical to
-        // fminf(255, fmaxf(0, v)) up to the sign of a zero
-        if (fminf(e0, e1) < 0.f || fmaxf(e0, e1) > 255.f) {
+        // clip(v) = max(min(bits, bits(255)), 0) on the fp32 bit patterns: one VIMNMX.RELU per pixel
+        // (non-negative floats order as their bits, negative ones are negative ints), identical to
+        // fminf(255, fmaxf(0, v)) up to the sign of a zero.  Unconditional: cheaper than testing
+        // whether the unit's map can leave [0, 255] and branching on it.
 #pragma unroll
-            for (int e = 0; e < 16; e++) v[e] = __int_as_float(__vimin_s32_relu(__float_as_int(v[e]), 0x437F0000));
-        }
-#else
-        if (fminf(e0, e1) < 0.f || fmaxf(e0, e1) > 255.f) {
-            float lo = fmin3(v[0], v[1], v[2]), hi = fmax3(v[0], v[1], v[2]);
-#pragma unroll
-            for (int e = 3; e < 15; e += 2) {
-                lo = fmin3(lo, v[e], v[e + 1]);
-                hi = fmax3(hi, v[e], v[e + 1]);
-            }
-            lo = fminf(lo, v[15]);
-            hi = fmaxf(hi, v[15]);
-            if (lo < 0.f || hi > 255.f) {
-#pragma unroll
-                for (int e = 0; e < 16; e++) v[e] = fminf(255.f, fmaxf(0.f, v[e]));
-            }
-        }
-#endif
+        for (int e = 0; e < 16; e++) v[e] = __int_as_float(__vimin_s32_relu(__float_as_int(v[e]), 0x437F0000));
     }
 }
 
@@ -787,7 +757,7 @@ __global__ void __launch_bounds__(LDT, LAT_MINB) decode_pair_lat_kernel(const __
                 const bool live = col_ok && row >= 0 && row < rh && row <= r_e;
                 paint_block<LQS, LHB, LQR, false, true>(word, live, L, st, &qa[0][0], no_raw, FLAT, p.init, rxg, ryg,
                                                         xa0, interior, p.W, p.H, v, &tab);
-                if (live) {
+                {  // dead lanes too (no branch): into ring rows / columns no live lane reads
                     const int wc = 16 * (rc + 1) + L.lx;  // window column in t+1 (origin xb0)
                     const int g = (ryg + L.ly) >> 1;
 #pragma unroll
