@@ -219,8 +219,11 @@ int mns_decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, c
  * all-reduced between mns_decode_f64_sweep and mns_decode_f64_decide).  state: int64[4] zeroed by
  * the caller ([0] converged, [1] sweeps done, [2] the sweep's max|delta| as fp64 bits).  cur/nxt
  * may be "virtual global" base pointers (row 0 of the image) of resident strips.
- * mns_records_to_units expands n packed records into 4n unit slots (decoder.py:48-59; unused
- * slots get size 0 and are skipped). */
+ * mns_records_to_units expands n packed records into 4n unit slots (decoder.py:48-59): slot i is
+ * record i's first unit (the leaf itself, or quadrant 0 of a phase-2 record), slots n + 3i .. + 2
+ * its quadrants 1..3; unused slots get size 0 and are skipped.  The order of a unit list does not
+ * matter to the sweeps (units are disjoint); this one keeps the live units of a mostly phase-1
+ * code dense. */
 int mns_records_to_units(const uint64_t *records, int64_t n_records, int32_t width, int32_t height, int32_t *ux,
                          int32_t *uy, int32_t *usize, int32_t *udx, int32_t *udy, double *us, double *uo,
                          void *stream);

@@ -316,7 +316,8 @@ def decode_device(code: DeviceCode, iters: int = 10, stop_delta: float = 0.0, in
 
 
 def records_to_units_device(records, n: int, W: int, H: int, stream=None) -> dict:
-    """Packed records -> 4n painted-unit slots (decoder.py:48-59) on the device (mns_records_to_units)."""
+    """Packed records -> 4n painted-unit slots (decoder.py:48-59) on the device (mns_records_to_units):
+    slot i = record i's first unit, slots n + 3i .. n + 3i + 2 = quadrants 1..3 of a phase-2 record."""
     torch = _torch()
     L = N.lib()
     dev = records.device

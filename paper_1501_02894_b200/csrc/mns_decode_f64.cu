@@ -90,7 +90,7 @@ __device__ __forceinline__ double paint_unit_f64_fixed(int x, int y, int iso, in
             const int k = iso ? iso_src(iso, i, j, S) : i * S + j;
             const double *pp = cur + (size_t)(dy + 2 * (k / S)) * W + dx + 2 * (k % S);
             double a0, a1, b0, b1;
-            if (S >= 4 && !(dx & 1)) {  // 16-byte aligned pairs (quadtree domains; search domains may be odd)
+            if (S >= 4 && !((dx | W) & 1)) {  // 16-byte aligned pairs (quadtree domains; search domains may be odd)
                 const double2 ra = *reinterpret_cast<const double2 *>(pp), rb = *reinterpret_cast<const double2 *>(pp + W);
                 a0 = ra.x; a1 = ra.y; b0 = rb.x; b1 = rb.y;
             } else {
@@ -100,15 +100,31 @@ __device__ __forceinline__ double paint_unit_f64_fixed(int x, int y, int iso, in
         }
     const double dm = __ddiv_rn(pw_sum_fixed<S * S>(d), (double)(S * S));
     double dmax = 0.0;
+    if ((x | W) & 1) {  // odd origin or pitch (unit lists of arbitrary images): scalar accesses
+#pragma unroll
+        for (int i = 0; i < S; i++)
+#pragma unroll
+            for (int j = 0; j < S; j++) {
+                double v = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * S + j], dm)), o);
+                v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+                const size_t idx = (size_t)(y + i) * W + x + j;
+                dmax = fmax(dmax, fabs(__dsub_rn(v, cur[idx])));
+                out[idx] = v;
+            }
+        return dmax;
+    }
 #pragma unroll
     for (int i = 0; i < S; i++)
 #pragma unroll
-        for (int j = 0; j < S; j++) {
-            double v = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * S + j], dm)), o);
-            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+        for (int j = 0; j < S; j += 2) {  // 16-byte pairs
             const size_t idx = (size_t)(y + i) * W + x + j;
-            dmax = fmax(dmax, fabs(__dsub_rn(v, cur[idx])));
-            out[idx] = v;
+            const double2 c = *reinterpret_cast<const double2 *>(cur + idx);
+            double v0 = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * S + j], dm)), o);
+            double v1 = __dadd_rn(__dmul_rn(s, __dsub_rn(d[i * S + j + 1], dm)), o);
+            v0 = v0 < 0.0 ? 0.0 : (v0 > 255.0 ? 255.0 : v0);
+            v1 = v1 < 0.0 ? 0.0 : (v1 > 255.0 ? 255.0 : v1);
+            dmax = fmax(dmax, fmax(fabs(__dsub_rn(v0, c.x)), fabs(__dsub_rn(v1, c.y))));
+            *reinterpret_cast<double2 *>(out + idx) = make_double2(v0, v1);
         }
     return dmax;
 }
@@ -213,8 +229,10 @@ __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, 
 }
 
 // Codes made mostly of units of side 8 / 16 (e.g. the 8-isometry encodes, whose roots mostly stay
-// whole): a half-warp per group of four unit slots (one record's units), so every big unit gets its
-// own half-warp instead of waiting its turn in a warp holding eight.
+// whole): a half-warp per group of four unit slots -- one record's units in records_to_units'
+// layout (slot g, then n/4 + 3g .. + 2) when n is a multiple of 4, else slots 4g .. 4g + 3; either
+// way every slot is visited once -- so every big unit gets its own half-warp instead of waiting
+// its turn in a warp holding eight.
 __global__ void __launch_bounds__(256) sweep_big_f64_kernel(const int32_t *ux, const int32_t *uy,
                                                             const int32_t *usize, const int32_t *udx,
                                                             const int32_t *udy, const double *us, const double *uo,
@@ -225,9 +243,10 @@ __global__ void __launch_bounds__(256) sweep_big_f64_kernel(const int32_t *ux, c
     const int hl = threadIdx.x & 15;
     const unsigned mask = 0xFFFFu << (16 * ((threadIdx.x >> 4) & 1));
     double dmax = 0.0;
+    const long long nrec = (n & 3) ? 0 : n >> 2;
 #pragma unroll 1
     for (int k = 0; k < 4; k++) {
-        const long long v = 4 * g + k;
+        const long long v = nrec ? (g < nrec ? (k == 0 ? g : nrec + 3 * g + (k - 1)) : n) : 4 * g + k;
         const int sz = v < n ? usize[v] : 0, side = sz & 255;
         if (side == 8 || side == 16)  // uniform across the half-warp
             dmax = fmax(dmax, paint_big_f64(ux[v], uy[v], side, sz >> 8, udx[v], udy[v], us[v], uo[v], W, cur, nxt,
@@ -266,9 +285,11 @@ __global__ void fill_f64_kernel(double *a, double v, long long n) {
         a[i] = v;
 }
 
-// Records (include/mns_record.h) -> painted units (decoder.py:48-59): slot 4i + k holds quadrant k
-// of a phase-2 record (k = 0..3) or, for a phase-1 record, the leaf itself in slot 4i (size 0 in
-// the other three: skipped by the sweep).
+// Records (include/mns_record.h) -> painted units (decoder.py:48-59), 4 slots per record: slot i
+// holds record i's first unit (a phase-1 leaf itself, or quadrant 0 of a phase-2 record), slots
+// n + 3i + (k - 1) its quadrants k = 1..3 (size 0 for a phase-1 record: skipped by the sweep).  The
+// first n slots are therefore dense -- a sweep warp over them paints 32 units, and the parameter
+// arrays of a mostly phase-1 code are read once, not through three empty slots in four.
 __global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W, int H, int32_t *ux, int32_t *uy,
                                         int32_t *usize, int32_t *udx, int32_t *udy, double *us, double *uo) {
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -283,9 +304,10 @@ __global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W,
     const int ob = (int)((r >> 33) & 0xFF);
     int sz, px, py;
     double s, o;
+    const long long slot = k == 0 ? i : n + 3 * i + (k - 1);
     if (!p2) {
         if (k) {
-            usize[t] = 0;
+            usize[slot] = 0;
             return;
         }
         sz = size | (int)(((r >> MNS_REC_ISO_SHIFT) & 7) << 8);  // side | isometry << 8
@@ -310,14 +332,14 @@ __global__ void records_to_units_kernel(const uint64_t *rec, long long n, int W,
         s = bit ? hi[level - 1] : lo[level - 1];
         o = (double)target;
     }
-    ux[t] = px;
-    uy[t] = py;
-    usize[t] = sz;
+    ux[slot] = px;
+    uy[slot] = py;
+    usize[slot] = sz;
     const int side = sz & 255;
-    udx[t] = clampi(px - side / 2, 0, W - 2 * side);  // co_domain_rect (image.py:174-187)
-    udy[t] = clampi(py - side / 2, 0, H - 2 * side);
-    us[t] = s;
-    uo[t] = o;
+    udx[slot] = clampi(px - side / 2, 0, W - 2 * side);  // co_domain_rect (image.py:174-187)
+    udy[slot] = clampi(py - side / 2, 0, H - 2 * side);
+    us[slot] = s;
+    uo[slot] = o;
 }
 
 int sm_count_f64() {
