@@ -323,7 +323,7 @@ def _med_ms(fn, reps=5, warm=2):
     return float(np.median(ts))
 
 
-def next_rows_components(dev, code, W, H, r0, r1):
+def next_rows_components(dev, code, W, H, r0, r1, whole=False):
     """SURVEY 8(f), measured beside the path (rank 0, informational): the GPU .mns packer and the GPU
     stream reader on rank 0's c5 code (round trip checked bit-exact), the device RD sweep on c2 and
     the offset histogram on c4 (full search + counting)."""
@@ -353,6 +353,17 @@ def next_rows_components(dev, code, W, H, r0, r1):
                          "read_gbs": (nbytes + 8 * n) / (r_ms / 1e3) / 1e9,
                          "roundtrip": "bit-exact" if ok else "MISMATCH",
                          "note": "write: records (8 B/leaf) in, .mns out; read: .mns in, records out"}
+    if whole:  # the reference's default DecodeConfig (max_iters 10, stop_delta 0.5): the exact fp64 path
+        _, it, _ = mns.decode_device(code, iters=10, stop_delta=0.5)
+        torch.cuda.synchronize()
+        x_ms = _med_ms(lambda: mns.decode_device(code, iters=10, stop_delta=0.5))
+        sweeps = int(it.item())
+        out["exact_decode"] = {"config": f"c5 code ({n} leaves), DecodeConfig() defaults: max_iters 10, stop_delta 0.5",
+                               "ms": x_ms, "sweeps": sweeps, "mpix_per_s": W * h / (x_ms / 1e3) / 1e6,
+                               "gbs": sweeps * 16.0 * W * h / (x_ms / 1e3) / 1e9,
+                               "note": "bit-exact fp64 decode_step sweeps with the reference's early stop decided on the "
+                                       "device (records -> units, fill, sweeps + decisions, uint8 finalize); gbs = 16 B "
+                                       "per pixel per executed sweep over the whole call"}
     c2 = config_image("c2")
     grid = (2.0, 4.0, 8.0, 16.0, 32.0)
     rd.rd_sweep(c2, ["mns"], grid[:1])
@@ -755,7 +766,9 @@ def run_ours(args, img_np, rank, world, local_rank):
                 "pair_evals": pairs, "ms": ms, "pair_evals_per_s": pairs / (ms / 1e3)}
 
     small = None if args.no_small else small_configs(dev, rank, world)
-    next_rows = None if (args.no_small or rank != 0) else next_rows_components(dev, code, W, H, r0, r1)
+    next_rows = None
+    if not args.no_small and rank == 0:
+        next_rows = next_rows_components(dev, code, W, H, r0, r1, whole=world == 1)
 
     # config c4 as SURVEY 8(e) shards it: ranges split across ranks (pool replicated, no data-path
     # collective), then the all-gather of the 8-byte per-range results; max over ranks
