@@ -208,7 +208,9 @@ int mns_decode_step_f64(const int32_t *ux, const int32_t *uy, const int32_t *usi
  * stop test `delta < stop_delta` runs on the device (later sweeps are no-ops), so the sweep count
  * and the uint8 image (clip(floor(x + 0.5))) equal the reference's bit for bit.  Used for
  * stop_delta > 0 (the default DecodeConfig); the fp32 decoders serve stop_delta = 0.  ping/pong:
- * fp64 [height][width]; *d_iters_done = sweeps run; workspace >= 32 bytes. */
+ * fp64 [height][width]; *d_iters_done = sweeps run; workspace >= 64 bytes (with 32..63 bytes the
+ * one-launch path for small images is not taken).  Images of up to 2^21 pixels decode in ONE
+ * cooperative launch (fill, sweeps, stop decisions, uint8 image), larger ones in a launch chain. */
 int mns_decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx,
                    const int32_t *udy, const double *us, const double *uo, int64_t n_units, int32_t width,
                    int32_t height, int32_t max_iters, double stop_delta, double initial_value, double *ping,

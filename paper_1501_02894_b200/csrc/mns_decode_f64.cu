@@ -18,6 +18,7 @@
 // State (int64[4]): [0] converged flag, [1] sweeps done, [2] this sweep's max|delta| (fp64 bits,
 // non-negative, so the integer max is the fp64 max), [3] spare.
 
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "mns_common.cuh"
@@ -179,14 +180,15 @@ __device__ double paint_big_f64(int x, int y, int side, int iso, int dx, int dy,
 }
 
 constexpr int F64_T = 256;  // threads (unit slots) per CTA of the sweep
+constexpr long long F64_COOP_MAX_PX = 1ll << 21;  // decode_f64: images up to this many pixels decode in one launch
 
+// Slot u of a sweep (thread per unit slot; every thread of the warp must call it): paints a unit of
+// side 2 / 4 (or an odd side) itself, then the warp's units of side 8 / 16 a half-warp each (BIGSEP:
+// those are left to sweep_big_slots).  Returns the thread's max |delta|.
 template <bool BIGSEP>
-__global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
-                                                          const int32_t *udx, const int32_t *udy, const double *us,
-                                                          const double *uo, long long n, int W, const double *cur,
-                                                          double *nxt, long long *state) {
-    if (state[0]) return;  // converged in an earlier sweep
-    const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__device__ __forceinline__ double sweep_slot(long long u, const int32_t *ux, const int32_t *uy, const int32_t *usize,
+                                             const int32_t *udx, const int32_t *udy, const double *us,
+                                             const double *uo, long long n, int W, const double *cur, double *nxt) {
     double dmax = 0.0;
     bool big = false;
     if (u < n && (usize[u] & 255) > 0) {  // usize = side | isometry << 8
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, 
         else if (side == 2)
             dmax = paint_unit_f64_fixed<2>(ux[u], uy[u], iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
         else if (side == 8 || side == 16)
-            big = !BIGSEP;  // painted below by a half-warp (BIGSEP: by sweep_big_f64_kernel)
+            big = !BIGSEP;  // painted below by a half-warp (BIGSEP: by sweep_big_slots)
         else
             dmax = paint_unit_f64(ux[u], uy[u], side, iso, udx[u], udy[u], us[u], uo[u], W, cur, nxt);
     }
@@ -221,11 +223,46 @@ __global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, 
             }
         }
     }
+    return dmax;
+}
+
+// The units of side 8 / 16 of slot group g, by one half-warp (lanes hl of `mask`): one record's
+// units in records_to_units' layout (slot g, then n/4 + 3g .. + 2) when n is a multiple of 4, else
+// slots 4g .. 4g + 3; either way every slot is visited once.
+__device__ __forceinline__ double sweep_big_slots(long long g, int hl, unsigned mask, const int32_t *ux,
+                                                  const int32_t *uy, const int32_t *usize, const int32_t *udx,
+                                                  const int32_t *udy, const double *us, const double *uo, long long n,
+                                                  int W, const double *cur, double *nxt) {
+    const long long nrec = (n & 3) ? 0 : n >> 2;
+    double dmax = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < 4; k++) {
+        const long long v = nrec ? (g < nrec ? (k == 0 ? g : nrec + 3 * g + (k - 1)) : n) : 4 * g + k;
+        const int sz = v < n ? usize[v] : 0, side = sz & 255;
+        if (side == 8 || side == 16)  // uniform across the half-warp
+            dmax = fmax(dmax, paint_big_f64(ux[v], uy[v], side, sz >> 8, udx[v], udy[v], us[v], uo[v], W, cur, nxt,
+                                            hl, mask));
+    }
+    return dmax;
+}
+
+// max over the warp of a non-negative fp64 (its bits order as integers), folded into *slot
+__device__ __forceinline__ void fold_delta(double dmax, long long *slot) {
     long long bits = __double_as_longlong(dmax);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
     if ((threadIdx.x & 31) == 0 && bits > 0)
-        atomicMax(reinterpret_cast<unsigned long long *>(&state[2]), (unsigned long long)bits);
+        atomicMax(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)bits);
+}
+
+template <bool BIGSEP>
+__global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
+                                                          const int32_t *udx, const int32_t *udy, const double *us,
+                                                          const double *uo, long long n, int W, const double *cur,
+                                                          double *nxt, long long *state) {
+    if (state[0]) return;  // converged in an earlier sweep
+    const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    fold_delta(sweep_slot<BIGSEP>(u, ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt), &state[2]);
 }
 
 // Codes made mostly of units of side 8 / 16 (e.g. the 8-isometry encodes, whose roots mostly stay
@@ -240,23 +277,8 @@ __global__ void __launch_bounds__(256) sweep_big_f64_kernel(const int32_t *ux, c
                                                             long long *state) {
     if (state[0]) return;
     const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
-    const int hl = threadIdx.x & 15;
     const unsigned mask = 0xFFFFu << (16 * ((threadIdx.x >> 4) & 1));
-    double dmax = 0.0;
-    const long long nrec = (n & 3) ? 0 : n >> 2;
-#pragma unroll 1
-    for (int k = 0; k < 4; k++) {
-        const long long v = nrec ? (g < nrec ? (k == 0 ? g : nrec + 3 * g + (k - 1)) : n) : 4 * g + k;
-        const int sz = v < n ? usize[v] : 0, side = sz & 255;
-        if (side == 8 || side == 16)  // uniform across the half-warp
-            dmax = fmax(dmax, paint_big_f64(ux[v], uy[v], side, sz >> 8, udx[v], udy[v], us[v], uo[v], W, cur, nxt,
-                                            hl, mask));
-    }
-    long long bits = __double_as_longlong(dmax);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(FULL, bits, o));
-    if ((threadIdx.x & 31) == 0 && bits > 0)
-        atomicMax(reinterpret_cast<unsigned long long *>(&state[2]), (unsigned long long)bits);
+    fold_delta(sweep_big_slots(g, threadIdx.x & 15, mask, ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt), &state[2]);
 }
 
 // decoder.py:71-75: current = nxt; stop if delta < stop_delta
@@ -283,6 +305,55 @@ __global__ void finalize_f64_kernel(const double *ping, const double *pong, cons
 __global__ void fill_f64_kernel(double *a, double v, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         a[i] = v;
+}
+
+// Small images (c1 / c2): the whole decode -- fill, every sweep with its stop decision, the uint8
+// image -- in ONE cooperative launch, a grid barrier per sweep instead of two or three launches
+// (a 512^2 sweep is a few microseconds of work; ten sweeps were launch-bound).  Same slot helpers,
+// so the same bits.  Sweep `it` folds its max |delta| into state[2 + it % 3]; thread 0 clears the
+// next sweep's word before the barrier (its last readers passed the previous barrier), and every
+// thread applies decoder.py:71-75 to the word after it, so the whole grid leaves the loop together.
+template <bool BIGSEP>
+__global__ void __launch_bounds__(F64_T, 2) decode_f64_coop_kernel(
+    const int32_t *ux, const int32_t *uy, const int32_t *usize, const int32_t *udx, const int32_t *udy,
+    const double *us, const double *uo, long long n, int W, int H, int iters, double stop_delta, double init,
+    double *ping, double *pong, long long *state, uint8_t *out, int32_t *iters_done) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const long long gsz = (long long)gridDim.x * blockDim.x, gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long npx = (long long)W * H;
+    for (long long i = gt; i < npx; i += gsz) ping[i] = init;
+    grid.sync();
+    int done = 0;
+    for (int it = 0; it < iters; it++) {
+        const double *cur = (it & 1) ? pong : ping;
+        double *nxt = (it & 1) ? ping : pong;
+        double dmax = 0.0;
+        for (long long base = blockIdx.x * (long long)blockDim.x; base < n; base += gsz)  // CTA-uniform trip count
+            dmax = fmax(dmax, sweep_slot<BIGSEP>(base + threadIdx.x, ux, uy, usize, udx, udy, us, uo, n, W, cur, nxt));
+        if (BIGSEP) {
+            const unsigned mask = 0xFFFFu << (16 * ((threadIdx.x >> 4) & 1));
+            const long long groups = (n + 3) / 4;
+            for (long long g = gt >> 4; g < groups; g += gsz >> 4)
+                dmax = fmax(dmax, sweep_big_slots(g, threadIdx.x & 15, mask, ux, uy, usize, udx, udy, us, uo, n, W,
+                                                  cur, nxt));
+        }
+        fold_delta(dmax, &state[2 + it % 3]);
+        if (gt == 0) state[2 + (it + 1) % 3] = 0;
+        grid.sync();
+        done = it + 1;
+        const long long bits = *reinterpret_cast<volatile long long *>(&state[2 + it % 3]);
+        if (__longlong_as_double(bits) < stop_delta) break;
+    }
+    const double *src = (done & 1) ? pong : ping;  // sweep i writes buffer (i + 1) % 2
+    for (long long i = gt; i < npx; i += gsz) {
+        const double v = floor(src[i] + 0.5);
+        out[i] = (uint8_t)(v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v));
+    }
+    if (gt == 0) {
+        state[0] = 1;
+        state[1] = done;
+        if (iters_done) *iters_done = done;
+    }
 }
 
 // Records (include/mns_record.h) -> painted units (decoder.py:48-59), 4 slots per record: slot i
@@ -414,11 +485,35 @@ int decode_f64(const int32_t *ux, const int32_t *uy, const int32_t *usize, const
     MNS_CHECK_ARG(iters >= 1, "max_iters must be >= 1");
     MNS_CHECK_ARG(workspace_bytes >= 32, "workspace too small");
     int64_t *state = reinterpret_cast<int64_t *>(workspace);
-    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 32, st));
-    fill_f64_kernel<<<sm_count_f64() * 4, 256, 0, st>>>(ping, init, (long long)W * H);
     // leaves of 64+ pixels on average (n = 4 unit slots per leaf): units of side 8 / 16 dominate, give each
     // its own half-warp
     const bool bigsep = (long long)W * H >= 16 * (long long)n;
+    if (n > 0 && (long long)W * H <= F64_COOP_MAX_PX && workspace_bytes >= 64) {  // one cooperative launch
+        static int per_sm[2] = {0, 0}, coop = -1;
+        if (coop < 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], decode_f64_coop_kernel<false>, F64_T, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], decode_f64_coop_kernel<true>, F64_T, 0);
+        }
+        if (coop > 0 && per_sm[bigsep] > 0) {
+            const long long slots = (n + F64_T - 1) / F64_T, groups = bigsep ? ((n + 3) / 4 * 16 + F64_T - 1) / F64_T : 0;
+            long long grid = slots > groups ? slots : groups;
+            const long long cap = (long long)per_sm[bigsep] * sm_count_f64();
+            if (grid > cap) grid = cap;
+            MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 64, st));
+            long long nn = n;
+            long long *stt = reinterpret_cast<long long *>(state);
+            void *args[] = {&ux, &uy, &usize, &udx, &udy, &us, &uo, &nn, &W, &H, &iters, &stop_delta, &init,
+                            &ping, &pong, &stt, &out, &d_iters_done};
+            const void *fn = bigsep ? (const void *)decode_f64_coop_kernel<true> : (const void *)decode_f64_coop_kernel<false>;
+            MNS_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(F64_T), args, 0, st));
+            return 0;
+        }
+    }
+    MNS_CUDA_TRY(cudaMemsetAsync(state, 0, 32, st));
+    fill_f64_kernel<<<sm_count_f64() * 4, 256, 0, st>>>(ping, init, (long long)W * H);
     for (int it = 0; it < iters; it++) {
         const double *cur = (it & 1) ? pong : ping;
         double *nxt = (it & 1) ? ping : pong;
