@@ -810,6 +810,25 @@ def test_early_stop_exact_at_threshold(mns, seed, side):
             assert np.array_equal(dout.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("shape,e", [((1024, 2048), (6.0, 6.0, 6.0)), ((1040, 2048), (6.0, 6.0, 6.0)),
+                                     ((1040, 2048), (8.0, 8.0, math.inf))])
+def test_exact_decode_one_launch_and_launch_chain_vs_oracle(mns, shape, e):
+    """mns_decode_f64 on both sides of its one-launch limit (2^21 pixels: 1024x2048 decodes in the
+    cooperative kernel, 1040x2048 in the launch chain), default DecodeConfig, codes with phase-2
+    quadrants and 2x2 leaves (finite e3) and without: sweep count and image equal the fp64 oracle's."""
+    from paper_1501_02894_b200.synth import synth_image
+
+    H, W = shape
+    px = np.ascontiguousarray(synth_image(2048, 77, noise_sigma=9.0, n_blobs=9)[:H, :W])
+    rec, _ = O.encode_quadtree_records(px, e, 16.0, True)
+    want, _, sweeps = O.decode_records(rec, W, H, max_iters=10, stop_delta=0.5)
+    dcode = mns.encode_device(torch.from_numpy(px).cuda(), mns.EncoderConfig(e1=e[0], e2=e[1], e3=e[2]))
+    assert np.array_equal(dcode.records[: dcode.n_records()].cpu().numpy().view(np.uint64), rec.view(np.uint64))
+    out, it, _ = mns.decode_device(dcode, iters=10, stop_delta=0.5)
+    assert int(it.item()) == sweeps
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
 def test_decode_search_codes_default_config_bit_exact(mns, golden):
     """Baseline (full-search) codes decoded with the default DecodeConfig (early stop 0.5): the
     GPU's exact fp64 decoder equals the fp64 oracle decode of the same units bit for bit."""
