@@ -179,6 +179,9 @@ __device__ double paint_big_f64(int x, int y, int side, int iso, int dx, int dy,
     return dmax;
 }
 
+#ifndef F64_MINB
+#define F64_MINB 4  // resident CTAs per SM the sweep is compiled for (5 and 6 spill or gain nothing: profiles/r2/README.md)
+#endif
 constexpr int F64_T = 256;  // threads (unit slots) per CTA of the sweep
 constexpr long long F64_COOP_MAX_PX = 1ll << 21;  // decode_f64: images up to this many pixels decode in one launch
 
@@ -256,7 +259,7 @@ __device__ __forceinline__ void fold_delta(double dmax, long long *slot) {
 }
 
 template <bool BIGSEP>
-__global__ void __launch_bounds__(F64_T, 4) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
+__global__ void __launch_bounds__(F64_T, F64_MINB) sweep_f64_kernel(const int32_t *ux, const int32_t *uy, const int32_t *usize,
                                                           const int32_t *udx, const int32_t *udy, const double *us,
                                                           const double *uo, long long n, int W, const double *cur,
                                                           double *nxt, long long *state) {
